@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Throughput benchmark of the batched assemble -> PCG -> combine pipeline.
+
+Metric (BASELINE.json): components solved/s & DoF/s (assemble+CG+combine),
+% of FP64/HBM roofline.  One "step" = the whole hot path on one plan:
+assemble every component, solve every component (Jacobi-PCG to 1e-13),
+combine at the configuration's evaluation points.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+    python bench.py --impl reference ...     # reference CPU path (oracle port)
+
+Workload: BASELINE configs[1] (cfg2: 3-D unit cube, p=3 C^2, w=7, 31
+components, 32768 random points, seed 1) unless --config says otherwise.
+Inputs are synthetic and fully defined by the config (no dataset).
+
+`value` = components/s with every input resident in HBM (device timing,
+CUDA events on the library's stream, L2 flushed before each step).
+`e2e`   = the same metric through the public API with host buffers
+(PlanSession.run: H2D of the problem inputs + points, pipeline, D2H of
+the combined values), wall clock.
+N > 1 (torchrun): one independent plan per rank (weak scaling; the
+combination technique has no exchange unless components are split).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as ct
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "components solved/s & DoF/s (assemble+CG+combine), % of FP64/HBM roofline"
+UNIT = "components/s"
+
+
+def canonical_work(plan, p, q, d, levels_to_dims):
+    """Per-component canonical counts: rows, reference nnz,
+    elements, assembly FLOPs F_el (sum-factorised stiffness + load)."""
+    P = p + 1
+    F_el = 2 * d * d * sum(P ** (d + k + 1) for k in range(1, d + 1)) + 2 * d * P ** (d + 1)
+    out = []
+    for beta, _ in plan.terms:
+        n = levels_to_dims(beta)
+        m = [x - 2 for x in n]
+        nnz = 1
+        for mm in m:
+            nnz *= sum(min(mm - 1, i + p) - max(0, i - p) + 1 for i in range(mm))
+        nel = int(np.prod([2**b for b in beta]))
+        out.append(dict(rows=int(np.prod(m)), nnz=int(nnz), dofs=int(np.prod(n)), nel=nel, flops=nel * F_el))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 4 + i and "Active" in r[4 + i]
+                          and "Not" not in r[4 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def fp64_peak_tflops():
+    lib = ct.CDLL(str(ROOT / "paper_1707_09598_b200" / "libsgiga_peaks.so"))
+    lib.sgiga_fp64_peak.argtypes = [ct.c_double, ct.POINTER(ct.c_double), ct.POINTER(ct.c_double)]
+    tf, ms = ct.c_double(), ct.c_double()
+    if lib.sgiga_fp64_peak(0.5, ct.byref(tf), ct.byref(ms)) != 0:
+        return None
+    return float(tf.value)
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU algorithm (oracle port) on host cores
+# ---------------------------------------------------------------------------
+def reference_step(cfg, threads, n_comp_sample=None):
+    from oracle import oracle as O
+    from paper_1707_09598_b200.combination import CombinationPlan
+    from paper_1707_09598_b200.scheduler import make_spec
+
+    terms = tuple(cfg.plan.terms)
+    if n_comp_sample is not None and n_comp_sample < len(terms):
+        # bounded sample: every k-th component (plan order kept)
+        idx = np.linspace(0, len(terms) - 1, n_comp_sample).round().astype(int)
+        terms = tuple(terms[i] for i in sorted(set(idx)))
+    spec = make_spec(terms, cfg.problem, cfg.quad_points)
+    orc = O.Oracle(spec, threads=threads)
+    pts = cfg.points()
+    t0 = time.perf_counter()
+    orc.run_plan(O.SOLVER_DIRECT, threads=threads)
+    orc.combine_points(pts, threads=threads)
+    dt = time.perf_counter() - t0
+    dofs = int(orc.dof_offsets[-1])
+    return len(terms), dofs, dt
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    sample = args.ref_sample
+    for _ in range(args.warmup):
+        reference_step(cfg, threads, sample)
+    times, ncomp, dofs = [], 0, 0
+    for _ in range(args.steps):
+        ncomp, dofs, dt = reference_step(cfg, threads, sample)
+        times.append(dt)
+    t = float(np.mean(times))
+    value = ncomp / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "components": ncomp, "points": cfg.n_points, "dofs": dofs},
+        "dof_per_s": dofs / t,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{ncomp} of {len(cfg.plan)} components (assemble+direct solve, OpenMP over "
+                                   f"components) + {cfg.n_points}-point per-point combine, per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_sgiga(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_09598_b200.pipeline import Batch
+    from paper_1707_09598_b200.scheduler import PlanSession, make_spec
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    batch = Batch(spec)
+    stream = torch.cuda.ExternalStream(batch.stream_ptr)
+    pts_h = cfg.points()
+    npts = pts_h.shape[0]
+    pts_d = torch.from_numpy(pts_h).to(f"cuda:{local}")
+    out_d = torch.empty(npts, dtype=torch.float64, device=f"cuda:{local}")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")   # 256 MB > L2
+
+    def step():
+        batch.assemble()
+        batch.solve(rtol=args.rtol)
+        batch.combine_points_device(pts_d.data_ptr(), npts, out_d.data_ptr())
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    kt_acc = np.zeros(7)
+    launches = 0
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()          # L2 flush, outside the timed events
+            starts[k].record(stream)
+        step()
+        with torch.cuda.stream(stream):
+            ends[k].record(stream)
+        kt = np.zeros(7, dtype=np.float32)
+        batch.lib.sgiga_kernel_times(batch.h, kt.ctypes.data_as(ct.POINTER(ct.c_float)))
+        kt_acc += kt
+        _, ln = batch.phase_stats()
+        launches += int(ln.sum())
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    step_ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
+    total_ms = float(step_ms.sum())
+    if ws > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    n_comp = len(cfg.plan)
+    iters = batch.iters.copy()
+    vals = out_d.cpu().numpy()
+
+    # ---- canonical work and rooflines ---------------------------------------
+    dims = [tuple(int(x) for x in row) for row in batch.dims]
+    lookup = {tuple(b): dims[i] for i, (b, _) in enumerate(cfg.plan.terms)}
+    work = canonical_work(cfg.plan, spec.degree, spec.quad_points, spec.d, lambda b: lookup[tuple(b)])
+    dofs = sum(w["dofs"] for w in work)
+    kt = kt_acc / args.steps   # ms per launch group per step
+    cg_bytes = sum(int(it) * (8 * w["nnz"] + 104 * w["rows"]) for it, w in zip(iters, work))
+    asm_flops = sum(w["flops"] for w in work)
+    d = spec.d
+    comb_flops_pt = 0
+    P = spec.degree + 1
+    levels_per_axis = [len({b[k] for b, _ in cfg.plan.terms}) for k in range(d)]
+    comb_flops_pt = sum(L * (2 * spec.degree + 5 * spec.degree * (spec.degree + 1) // 2) for L in levels_per_axis) \
+        + n_comp * (2 * sum(P**j for j in range(1, d + 1)) + 2)
+    comb_flops = comb_flops_pt * npts
+    comb_bytes = npts * (8 * d + 8) + 8 * dofs
+    peaks, peak_kind = measured_peaks()
+    hbm_peak = float(peaks["hbm_gbs"])
+    fp64 = fp64_peak_tflops() if rank == 0 else None
+    cg_ms = kt[3] + kt[4]
+    groups = {
+        "pcg": dict(ms=cg_ms, bound="hbm", achieved=cg_bytes / (cg_ms * 1e-3) / 1e9 if cg_ms > 0 else 0.0,
+                    peak=hbm_peak, unit="GB/s", traffic_algorithmic_bytes=cg_bytes,
+                    peak_source=f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"),
+        "assembly": dict(ms=kt[2], bound="fp64", achieved=asm_flops / (kt[2] * 1e-3) / 1e12 if kt[2] > 0 else 0.0,
+                         peak=fp64, unit="TFLOP/s", canonical_flops=asm_flops,
+                         peak_source="DFMA micro-benchmark on this GPU (tools/fp64_peak.cu)"),
+        "combine": dict(ms=kt[6], bound="fp64", achieved=comb_flops / (kt[6] * 1e-3) / 1e12 if kt[6] > 0 else 0.0,
+                        peak=fp64, unit="TFLOP/s", canonical_flops=comb_flops,
+                        hbm_gbs=comb_bytes / (kt[6] * 1e-3) / 1e9 if kt[6] > 0 else 0.0,
+                        peak_source="DFMA micro-benchmark on this GPU (tools/fp64_peak.cu)"),
+        "metric": dict(ms=kt[1], note="geometry/metric/load per quadrature point"),
+        "tables": dict(ms=kt[0]),
+        "post": dict(ms=kt[5], note="residual check + expand"),
+    }
+    for g in groups.values():
+        if g.get("peak"):
+            g["frac"] = g["achieved"] / g["peak"]
+    dom = max(("pcg", "assembly", "combine"), key=lambda k: groups[k]["ms"])
+    G = groups[dom]
+    if G["bound"] == "hbm":
+        roofline = {"bound": "hbm", "achieved": G["achieved"], "peak": G["peak"], "unit": "GB/s",
+                    "frac": G["frac"], "traffic": None, "kernel": "k_pcg_small/k_cg_* (batched Jacobi-PCG)",
+                    "algorithmic_bytes_per_launch": cg_bytes, "peak_source": G["peak_source"]}
+    else:
+        roofline = {"bound": "tensor", "achieved": G["achieved"], "peak": G["peak"], "unit": "TFLOP/s",
+                    "frac": G.get("frac"), "traffic": None, "kernel": dom,
+                    "note": "FP64 CUDA-core bound; 'tensor' slot holds the measured DFMA peak",
+                    "peak_source": G["peak_source"]}
+
+    # ---- end to end through the public API, host buffers ---------------------
+    sess = PlanSession(cfg.plan, cfg.problem, cfg.quad_points, rtol=args.rtol)
+    pin = torch.empty(pts_h.shape, dtype=torch.float64, pin_memory=True)
+    pin.copy_(torch.from_numpy(pts_h))
+    pts_pinned = pin.numpy()
+    for _ in range(max(args.warmup, 3)):
+        sess.run(pts_pinned)
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v_e2e = sess.run(pts_pinned)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if ws > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = sess.h2d_input_bytes + pts_h.nbytes
+    d2h = npts * 8 + n_comp * (4 + 8) + 64
+    consistent = bool(np.array_equal(v_e2e, vals))
+    sess.close()
+
+    # ---- CPU baseline (rank 0, N = 1) ---------------------------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        nc, cdofs, dt = reference_step(cfg, threads, args.ref_sample)
+        cpu = {"value": nc / dt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{nc} of {n_comp} components (assemble+direct solve) + {npts}-point combine, 1 step, "
+                         f"oracle/sgiga_oracle.c (C restatement of the reference), OpenMP {threads} threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ws * n_comp / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE config recipe; seeded points)",
+            "config": {"workload": cfg.name, "d": d, "degree": spec.degree, "level_w": cfg.plan.level,
+                       "components": n_comp, "points": npts, "dofs": dofs, "quad_points": spec.quad_points,
+                       "rtol": args.rtol, "l2_flush": "256 MB write before every timed step",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+            "dof_per_s": ws * dofs / (ms_per_step * 1e-3),
+            "e2e": {"value": ws * n_comp / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s,
+                    "matches_device_run_bitwise": consistent},
+            "roofline": roofline,
+            "rooflines": {k: {kk: (float(vv) if isinstance(vv, (np.floating, float)) else vv) for kk, vv in g.items()}
+                          for k, g in groups.items()},
+            "pcg_iterations": {"sum": int(iters.sum()), "max": int(iters.max())},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "fp64_peak_tflops_measured": fp64,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    batch.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="sgiga", choices=["sgiga", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--rtol", type=float, default=1e-13)
+    ap.add_argument("--ref-sample", type=int, default=None,
+                    help="reference arm: components per step (default: all for cfg1-3, 12 for cfg5)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_1707_09598_b200.configs import get_config
+
+    cfg = get_config(args.config)
+    if args.ref_sample is None and cfg.name.startswith("cfg5"):
+        args.ref_sample = 12
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_sgiga(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

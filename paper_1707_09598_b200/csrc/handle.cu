@@ -1,0 +1,739 @@
+// handle.cu -- C ABI of libsgiga: descriptor validation, the batch-wide
+// component table, device allocation, phase orchestration and exports.
+//
+// Reference boundary: scheduler.run_plan (scheduler.py:74-96) ->
+// combination.solve_component (combination.py:183-200) per component;
+// here a whole plan is one handle and every phase is one batched launch.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "handle.cuh"
+
+namespace sgiga {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+size_t assembly_smem_bytes(const Handle* h);
+size_t small_smem_bytes(const Handle* h);
+
+// cumulative tables stored behind d_gauss: [2q] gauss, then
+// tab_qp_cum [ntab+1], comp_qp_cum [ncomp+1], comp_dof_cum [ncomp+1]
+static int64_t* cum_base(Handle* h) {
+    return reinterpret_cast<int64_t*>(h->d_gauss + 2 * h->q);
+}
+int64_t* tab_qp_cum_ptr(Handle* h) { return cum_base(h); }
+int64_t* comp_qp_cum_ptr(Handle* h) { return cum_base(h) + h->tabs.size() + 1; }
+int64_t* comp_dof_cum_ptr(Handle* h) { return comp_qp_cum_ptr(h) + h->ncomp + 1; }
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t n) {
+    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T));
+}
+
+static void free_all(Handle* h) {
+    void* ptrs[] = {h->d_comps, h->d_tabs, h->d_geo, h->d_pencils, h->d_chunks, h->d_small,
+                    h->d_large, h->d_bp, h->d_knots, h->d_gauss, h->d_tabvals, h->d_qx,
+                    h->d_qw, h->d_geob, h->d_geofirst, h->d_geo_knots, h->d_geo_hw, h->d_G,
+                    h->d_hostf, h->d_xphys, h->d_stencil, h->d_rhs, h->d_dinv, h->d_x,
+                    h->d_r, h->d_z, h->d_p, h->d_q, h->d_coef, h->d_cg, h->d_part, h->d_err,
+                    h->d_active_count, h->d_relres};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h->h_pinned_flag) cudaFreeHost(h->h_pinned_flag);
+    for (auto& e : h->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : h->kev)
+        if (e) cudaEventDestroy(e);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+}
+
+// ---------------------------------------------------------------------------
+// descriptor -> component table (host)
+// ---------------------------------------------------------------------------
+static int build_tables(Handle* h, const sgiga_problem_desc* D) {
+    const int d = D->d, p = D->degree;
+    if (d < 1 || d > 3) { set_error("dimension must be 1, 2 or 3"); return SGIGA_ERR_VALUE; }
+    if (p < 1 || p + 1 > PMAX) { set_error("device path supports degree 1..4"); return SGIGA_ERR_VALUE; }
+    if (D->regularity < 0 || D->regularity > p - 1) {
+        set_error("device path supports regularity in [0, degree-1]");
+        return SGIGA_ERR_VALUE;
+    }
+    if (D->quad_points < 1 || D->quad_points > QMAX) {
+        set_error("quadrature points per direction must be in [1, 10]");
+        return SGIGA_ERR_VALUE;
+    }
+    if (D->n_comp < 1) { set_error("a combination plan needs at least one term"); return SGIGA_ERR_VALUE; }
+    if (D->max_level < 0 || D->max_level > 30) { set_error("max_level out of range"); return SGIGA_ERR_VALUE; }
+    h->d = d; h->p = p; h->r = D->regularity; h->q = D->quad_points; h->mu = p - D->regularity;
+    h->ncomp = D->n_comp; h->max_level = D->max_level; h->forcing_id = D->forcing_id;
+    if (h->forcing_id < SGIGA_FORCING_HOST || h->forcing_id > SGIGA_FORCING_LSHAPE) {
+        set_error("unknown forcing id");
+        return SGIGA_ERR_VALUE;
+    }
+    h->levels.assign(D->levels, D->levels + (size_t)d * D->n_comp);
+    h->coefs.assign(D->coefs, D->coefs + D->n_comp);
+    h->gauss_n.assign(D->gauss_nodes, D->gauss_nodes + h->q);
+    h->gauss_w.assign(D->gauss_weights, D->gauss_weights + h->q);
+    // geometry
+    h->geo = GeoInfo{};
+    h->geo.d = d;
+    int64_t koff = 0, ncp = 1;
+    for (int k = 0; k < d; ++k) {
+        int gdeg = D->geo_degree[k], gnk = D->geo_nknots[k];
+        if (gdeg < 1 || gdeg >= GEO_PMAX || gnk < 2 * (gdeg + 1)) {
+            set_error("geometry knot vector invalid or degree > 7");
+            return SGIGA_ERR_VALUE;
+        }
+        h->geo.deg[k] = gdeg; h->geo.nk[k] = gnk; h->geo.n[k] = gnk - gdeg - 1;
+        h->geo.knot_off[k] = koff;
+        koff += gnk;
+        ncp *= h->geo.n[k];
+    }
+    h->geo_knots.assign(D->geo_knots, D->geo_knots + koff);
+    h->geo_hw.assign(D->geo_hw, D->geo_hw + ncp * (d + 1));
+    // knot tables per (axis, level) actually used
+    const int L = D->max_level + 1;
+    h->tab_of.assign((size_t)d * L, -1);
+    h->tabs.clear();
+    h->bp_host.clear();
+    int64_t knots_tot = 0, vals_tot = 0, qp_tot = 0;
+    for (int c = 0; c < D->n_comp; ++c)
+        for (int k = 0; k < d; ++k) {
+            int lv = D->levels[c * d + k];
+            if (lv < 0 || lv > D->max_level) { set_error("level outside [0, max_level]"); return SGIGA_ERR_VALUE; }
+            int key = k * L + lv;
+            if (h->tab_of[key] >= 0) continue;
+            if (D->bp_offset[key] < 0 || D->bp_count[key] < 2) {
+                set_error("missing breakpoint table for an (axis, level) pair");
+                return SGIGA_ERR_VALUE;
+            }
+            const double* bp = D->breakpoints + D->bp_offset[key];
+            int nbp = D->bp_count[key];
+            if (bp[0] != 0.0 || bp[nbp - 1] != 1.0) { set_error("breakpoints must start at 0 and end at 1"); return SGIGA_ERR_VALUE; }
+            for (int i = 1; i < nbp; ++i)
+                if (!(bp[i] > bp[i - 1])) { set_error("breakpoints must be strictly increasing"); return SGIGA_ERR_VALUE; }
+            TabInfo T{};
+            T.axis = k; T.level = lv; T.nel = nbp - 1;
+            T.nk = 2 * (p + 1) + (T.nel - 1) * h->mu;
+            T.n = T.nk - p - 1;
+            T.bp_off = (int64_t)h->bp_host.size();
+            h->bp_host.insert(h->bp_host.end(), bp, bp + nbp);
+            T.knot_off = knots_tot;
+            knots_tot += T.nk;
+            T.val_off = vals_tot;
+            vals_tot += 2LL * T.nel * h->q * (p + 1);
+            T.qp_off = qp_tot;
+            T.geo_off = qp_tot;
+            qp_tot += (int64_t)T.nel * h->q;
+            h->tab_of[key] = (int)h->tabs.size();
+            h->tabs.push_back(T);
+        }
+    h->total_knots = knots_tot;
+    h->total_tabvals = vals_tot;
+    h->total_tabqp = qp_tot;
+
+    // components
+    h->comps.assign(D->n_comp, CompInfo{});
+    h->pencils.clear(); h->chunks.clear(); h->small_comps.clear(); h->large_comps.clear();
+    int64_t vec = 0, mat = 0, qpo = 0, dof = 0, rows_tot = 0, nqp_tot = 0;
+    const int W = 2 * p + 1, nG = d * (d + 1) / 2 + 1;
+    h->max_slots_comp = 0;
+    for (int c = 0; c < D->n_comp; ++c) {
+        CompInfo& C = h->comps[c];
+        C.coef = D->coefs[c];
+        int mmax = -1, s = d - 1;
+        for (int k = 0; k < d; ++k) {
+            const TabInfo& T = h->tabs[h->tab_of[k * L + D->levels[c * d + k]]];
+            C.lv[k] = T.level; C.tab[k] = h->tab_of[k * L + T.level];
+            C.n[k] = T.n; C.m[k] = std::max(0, T.n - 2); C.nel[k] = T.nel;
+            C.S[k] = C.m[k] <= W ? std::max(1, C.m[k]) : W;
+            C.absm[k] = C.m[k] <= W;
+        }
+        for (int k = d - 1; k >= 0; --k)
+            if (C.m[k] > mmax) { mmax = C.m[k]; s = k; }
+        int j = 0;
+        for (int k = 0; k < d; ++k) if (k != s) C.ax[j++] = k;
+        C.ax[d - 1] = s;
+        C.rows = 1; C.nslots = 1; C.ndofs = 1; C.nqp = 1;
+        for (int k = 0; k < d; ++k) {
+            C.rows *= C.m[k]; C.nslots *= C.S[k]; C.ndofs *= C.n[k];
+            C.nqp *= (int64_t)C.nel[k] * h->q;
+        }
+        int64_t pr = 1, ps = 1;
+        for (int jj = d - 1; jj >= 0; --jj) {
+            int k = C.ax[jj];
+            C.rs[k] = pr; pr *= C.m[k];
+            C.ss[k] = ps; ps *= C.S[k];
+        }
+        // qp storage order: s outermost, then ax[d-2], ..., ax[0] innermost
+        int64_t pq = 1;
+        for (int jj = 0; jj < d; ++jj) {
+            int k = C.ax[jj];
+            C.qs[k] = pq;
+            pq *= (int64_t)C.nel[k] * h->q;
+        }
+        C.halo = 0;
+        for (int k = 0; k < d; ++k) if (!C.absm[k]) C.halo += (int64_t)p * C.rs[k];
+        C.vec_off = vec + C.halo;
+        vec += C.rows + 2 * C.halo;
+        C.mat_off = mat;
+        mat += C.rows * C.nslots;
+        C.qp_off = qpo;
+        qpo += (int64_t)nG * C.nqp;
+        C.dof_off = dof;
+        dof += C.ndofs;
+        rows_tot += C.rows;
+        nqp_tot += C.nqp;
+        h->max_slots_comp = std::max<int>(h->max_slots_comp, (int)C.nslots);
+        if (C.rows == 0) { C.small = 0; C.nchunks = 0; C.chunk_off = (int64_t)h->chunks.size(); continue; }
+        C.small = (C.rows <= 2048 && (6 * C.rows + 2 * C.halo + 64) * 8 <= 200 * 1024) ? 1 : 0;
+        (C.small ? h->small_comps : h->large_comps).push_back(c);
+        C.chunk_off = (int64_t)h->chunks.size();
+        C.nchunks = (int)((C.rows + 255) / 256);
+        for (int i = 0; i < C.nchunks; ++i) {
+            Chunk ch;
+            ch.comp = c; ch.row0 = i * 256; ch.idx = i;
+            ch.nrow = (int)std::min<int64_t>(256, C.rows - (int64_t)i * 256);
+            h->chunks.push_back(ch);
+        }
+        // assembly pencils: tile rows along ax[d-2], ax[d-3]; segments along s
+        int na = d >= 2 ? C.m[C.ax[d - 2]] : 1, nb = d >= 3 ? C.m[C.ax[d - 3]] : 1;
+        int ms = C.m[s];
+        const int SEG = 128;
+        int nseg = (ms + SEG - 1) / SEG;
+        for (int ib = 0; ib < nb; ++ib)
+            for (int ia = 0; ia < na; ++ia)
+                for (int sg = 0; sg < nseg; ++sg) {
+                    Pencil pc;
+                    pc.comp = c;
+                    pc.ia = d >= 2 ? ia + 1 : 0;
+                    pc.ib = d >= 3 ? ib + 1 : 0;
+                    pc.r0 = 1 + sg * SEG;
+                    pc.r1 = std::min(1 + ms, 1 + (sg + 1) * SEG);
+                    h->pencils.push_back(pc);
+                }
+    }
+    h->total_vec = vec; h->total_slots = mat; h->total_qp = nqp_tot; h->total_rows = rows_tot;
+    h->total_dofs = dof;
+    if (assembly_smem_bytes(h) > 227 * 1024) {
+        set_error("quadrature/degree combination exceeds the assembly kernel's shared memory");
+        return SGIGA_ERR_VALUE;
+    }
+    return SGIGA_OK;
+}
+
+static int upload_all(Handle* h) {
+    cudaStream_t s = h->stream;
+    SG_CUDA(cudaMemcpyAsync(h->d_comps, h->comps.data(), sizeof(CompInfo) * h->comps.size(), cudaMemcpyHostToDevice, s));
+    SG_CUDA(cudaMemcpyAsync(h->d_tabs, h->tabs.data(), sizeof(TabInfo) * h->tabs.size(), cudaMemcpyHostToDevice, s));
+    SG_CUDA(cudaMemcpyAsync(h->d_geo, &h->geo, sizeof(GeoInfo), cudaMemcpyHostToDevice, s));
+    if (!h->pencils.empty())
+        SG_CUDA(cudaMemcpyAsync(h->d_pencils, h->pencils.data(), sizeof(Pencil) * h->pencils.size(), cudaMemcpyHostToDevice, s));
+    if (!h->chunks.empty())
+        SG_CUDA(cudaMemcpyAsync(h->d_chunks, h->chunks.data(), sizeof(Chunk) * h->chunks.size(), cudaMemcpyHostToDevice, s));
+    if (!h->small_comps.empty())
+        SG_CUDA(cudaMemcpyAsync(h->d_small, h->small_comps.data(), sizeof(int) * h->small_comps.size(), cudaMemcpyHostToDevice, s));
+    SG_CUDA(cudaMemcpyAsync(h->d_bp, h->bp_host.data(), sizeof(double) * h->bp_host.size(), cudaMemcpyHostToDevice, s));
+    SG_CUDA(cudaMemcpyAsync(h->d_geo_knots, h->geo_knots.data(), sizeof(double) * h->geo_knots.size(), cudaMemcpyHostToDevice, s));
+    SG_CUDA(cudaMemcpyAsync(h->d_geo_hw, h->geo_hw.data(), sizeof(double) * h->geo_hw.size(), cudaMemcpyHostToDevice, s));
+    // gauss + cumulative index tables
+    std::vector<char> blob;
+    std::vector<double> g(2 * h->q);
+    for (int i = 0; i < h->q; ++i) { g[i] = h->gauss_n[i]; g[h->q + i] = h->gauss_w[i]; }
+    std::vector<int64_t> cum;
+    int64_t acc = 0;
+    cum.push_back(0);
+    for (auto& T : h->tabs) { acc += (int64_t)T.nel * h->q; cum.push_back(acc); }
+    acc = 0;
+    cum.push_back(0);
+    for (auto& C : h->comps) { acc += C.nqp; cum.push_back(acc); }
+    acc = 0;
+    cum.push_back(0);
+    for (auto& C : h->comps) { acc += C.ndofs; cum.push_back(acc); }
+    blob.resize(g.size() * 8 + cum.size() * 8);
+    memcpy(blob.data(), g.data(), g.size() * 8);
+    memcpy(blob.data() + g.size() * 8, cum.data(), cum.size() * 8);
+    SG_CUDA(cudaMemcpyAsync(h->d_gauss, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+    SG_CUDA(cudaStreamSynchronize(s));  // blob is a host temporary
+    h->tables_ready = false;
+    h->assembled = false;
+    h->solved = false;
+    return SGIGA_OK;
+}
+
+static int check_err(Handle* h) {
+    int e = 0;
+    SG_CUDA(cudaMemcpyAsync(&e, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    if (e & ERRF_GEOMETRY) {
+        set_error("geometry map is degenerate: det J <= 0 at a quadrature point");
+        SG_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
+        return SGIGA_ERR_GEOMETRY;
+    }
+    if (e & ERRF_SPAN) {
+        set_error("quadrature node escaped its element");
+        SG_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
+        return SGIGA_ERR_VALUE;
+    }
+    return SGIGA_OK;
+}
+
+static int ensure_tables(Handle* h) {
+    if (h->tables_ready) return SGIGA_OK;
+    h->kstart(0);
+    SG_CUDA(launch_build_knots(h));
+    SG_CUDA(launch_basis_tables(h));
+    h->kstop(0);
+    h->tables_ready = true;
+    return SGIGA_OK;
+}
+
+}  // namespace sgiga
+
+using namespace sgiga;
+
+extern "C" {
+
+const char* sgiga_last_error(void) { return g_last_error.c_str(); }
+
+int sgiga_device_count(int32_t* n) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) { *n = 0; set_error(cudaGetErrorString(e)); return SGIGA_ERR_CUDA; }
+    *n = c;
+    return SGIGA_OK;
+}
+
+int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** out) {
+    if (!desc || !out) { set_error("null argument"); return SGIGA_ERR_VALUE; }
+    *out = nullptr;
+    Handle* h = new Handle();
+    int st = build_tables(h, desc);
+    if (st) { delete h; return st; }
+    cudaError_t e = cudaGetDevice(&h->dev);
+    if (e != cudaSuccess) { set_error(std::string("no CUDA device: ") + cudaGetErrorString(e)); delete h; return SGIGA_ERR_CUDA; }
+    if (stream) {
+        h->stream = (cudaStream_t)stream;
+    } else {
+        e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); delete h; return SGIGA_ERR_CUDA; }
+        h->own_stream = true;
+    }
+    const int nG = h->nG();
+    cudaError_t ea = cudaSuccess;
+#define A_(ptr, n) if (ea == cudaSuccess) ea = dalloc(&h->ptr, (size_t)(n))
+    A_(d_comps, h->comps.size());
+    A_(d_tabs, h->tabs.size());
+    A_(d_geo, 1);
+    A_(d_pencils, h->pencils.size());
+    A_(d_chunks, h->chunks.size());
+    A_(d_small, h->small_comps.size());
+    A_(d_large, h->large_comps.size());
+    A_(d_bp, h->bp_host.size());
+    A_(d_knots, h->total_knots);
+    A_(d_gauss, 2 * h->q + (h->tabs.size() + 1) + 2 * (h->ncomp + 1));
+    A_(d_tabvals, h->total_tabvals);
+    A_(d_qx, h->total_tabqp);
+    A_(d_qw, h->total_tabqp);
+    A_(d_geob, h->total_tabqp * 2 * GEO_PMAX);
+    A_(d_geofirst, h->total_tabqp);
+    A_(d_geo_knots, h->geo_knots.size());
+    A_(d_geo_hw, h->geo_hw.size());
+    A_(d_G, nG * h->total_qp);
+    A_(d_stencil, h->total_slots);
+    A_(d_rhs, h->total_vec);
+    A_(d_dinv, h->total_vec);
+    A_(d_x, h->total_vec);
+    A_(d_r, h->total_vec);
+    A_(d_z, h->total_vec);
+    A_(d_p, h->total_vec);
+    A_(d_q, h->total_vec);
+    A_(d_coef, h->total_dofs);
+    A_(d_cg, h->ncomp);
+    A_(d_part, 3 * h->chunks.size());
+    A_(d_err, 1);
+    A_(d_active_count, 1);
+    A_(d_relres, h->ncomp);
+#undef A_
+    if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned_flag), sizeof(int) * 4);
+    for (auto& ev : h->ev)
+        if (ea == cudaSuccess) ea = cudaEventCreate(&ev);
+    for (auto& ev : h->kev)
+        if (ea == cudaSuccess) ea = cudaEventCreate(&ev);
+    if (ea != cudaSuccess) {
+        set_error(std::string("device allocation failed: ") + cudaGetErrorString(ea));
+        free_all(h);
+        delete h;
+        return SGIGA_ERR_CUDA;
+    }
+    // zero everything that is gathered through halos or reduced
+    cudaStream_t s = h->stream;
+    double* vecs[] = {h->d_rhs, h->d_dinv, h->d_x, h->d_r, h->d_z, h->d_p, h->d_q};
+    for (double* v : vecs) cudaMemsetAsync(v, 0, sizeof(double) * std::max<int64_t>(1, h->total_vec), s);
+    cudaMemsetAsync(h->d_cg, 0, sizeof(CgState) * h->ncomp, s);
+    cudaMemsetAsync(h->d_err, 0, sizeof(int), s);
+    cudaMemsetAsync(h->d_coef, 0, sizeof(double) * std::max<int64_t>(1, h->total_dofs), s);
+    st = upload_all(h);
+    if (st) { free_all(h); delete h; return st; }
+    h->iters.assign(h->ncomp, 0);
+    *out = reinterpret_cast<sgiga_handle*>(h);
+    return SGIGA_OK;
+}
+
+int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !desc) { set_error("null argument"); return SGIGA_ERR_VALUE; }
+    // same-shape re-upload: rebuild the tables on a scratch handle and compare sizes
+    Handle tmp;
+    int st = build_tables(&tmp, desc);
+    if (st) return st;
+    if (tmp.total_slots != h->total_slots || tmp.total_qp != h->total_qp ||
+        tmp.ncomp != h->ncomp || tmp.tabs.size() != h->tabs.size() || tmp.d != h->d ||
+        tmp.p != h->p || tmp.q != h->q) {
+        set_error("sgiga_upload: descriptor shape differs from the handle's");
+        return SGIGA_ERR_VALUE;
+    }
+    h->levels.swap(tmp.levels); h->coefs.swap(tmp.coefs);
+    h->gauss_n.swap(tmp.gauss_n); h->gauss_w.swap(tmp.gauss_w);
+    h->geo = tmp.geo; h->geo_knots.swap(tmp.geo_knots); h->geo_hw.swap(tmp.geo_hw);
+    h->bp_host.swap(tmp.bp_host); h->comps.swap(tmp.comps); h->tabs.swap(tmp.tabs);
+    h->forcing_id = tmp.forcing_id;
+    return upload_all(h);
+}
+
+int sgiga_batch_sizes(sgiga_handle* hh, int64_t* total_qp, int64_t* total_rows,
+                      int64_t* total_dofs, int64_t* total_slots) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h) return SGIGA_ERR_VALUE;
+    if (total_qp) *total_qp = h->total_qp;
+    if (total_rows) *total_rows = h->total_rows;
+    if (total_dofs) *total_dofs = h->total_dofs;
+    if (total_slots) *total_slots = h->total_slots;
+    return SGIGA_OK;
+}
+
+int sgiga_component_info(sgiga_handle* hh, int32_t* dims, int64_t* dof_offsets) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h) return SGIGA_ERR_VALUE;
+    for (int c = 0; c < h->ncomp; ++c) {
+        if (dims) for (int k = 0; k < h->d; ++k) dims[c * h->d + k] = h->comps[c].n[k];
+        if (dof_offsets) dof_offsets[c] = h->comps[c].dof_off;
+    }
+    if (dof_offsets) dof_offsets[h->ncomp] = h->total_dofs;
+    return SGIGA_OK;
+}
+
+int sgiga_quad_points_physical(sgiga_handle* hh, double* x_out) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !x_out) return SGIGA_ERR_VALUE;
+    if (h->forcing_id != SGIGA_FORCING_HOST) { set_error("only for SGIGA_FORCING_HOST"); return SGIGA_ERR_STATE; }
+    if (!h->d_xphys) SG_CUDA(dalloc(&h->d_xphys, h->total_qp * h->d));
+    if (!h->d_hostf) {
+        SG_CUDA(dalloc(&h->d_hostf, h->total_qp));
+        SG_CUDA(cudaMemsetAsync(h->d_hostf, 0, sizeof(double) * std::max<int64_t>(1, h->total_qp), h->stream));
+    }
+    int st = ensure_tables(h);
+    if (st) return st;
+    SG_CUDA(launch_metric(h));
+    st = check_err(h);
+    if (st) return st;
+    SG_CUDA(cudaMemcpy(x_out, h->d_xphys, sizeof(double) * h->total_qp * h->d, cudaMemcpyDeviceToHost));
+    return SGIGA_OK;
+}
+
+int sgiga_set_forcing_density(sgiga_handle* hh, const double* f) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !f) return SGIGA_ERR_VALUE;
+    if (!h->d_hostf) SG_CUDA(dalloc(&h->d_hostf, h->total_qp));
+    SG_CUDA(cudaMemcpyAsync(h->d_hostf, f, sizeof(double) * h->total_qp, cudaMemcpyHostToDevice, h->stream));
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    h->density_ready = true;
+    return SGIGA_OK;
+}
+
+int sgiga_assemble(sgiga_handle* hh) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h) return SGIGA_ERR_VALUE;
+    if (h->forcing_id == SGIGA_FORCING_HOST && !h->density_ready) {
+        set_error("host forcing: call sgiga_set_forcing_density first");
+        return SGIGA_ERR_STATE;
+    }
+    h->launches[0] = 0;
+    SG_CUDA(cudaEventRecord(h->ev[0], h->stream));
+    int st = ensure_tables(h);
+    if (st) return st;
+    h->kstart(1);
+    SG_CUDA(launch_metric(h));
+    h->kstop(1);
+    h->kstart(2);
+    SG_CUDA(launch_assembly(h));
+    h->kstop(2);
+    SG_CUDA(cudaEventRecord(h->ev[1], h->stream));
+    st = check_err(h);
+    if (st) return st;
+    SG_CUDA(cudaEventElapsedTime(&h->ms[0], h->ev[0], h->ev[1]));
+    h->assembled = true;
+    h->solved = false;
+    return SGIGA_OK;
+}
+
+int sgiga_solve(sgiga_handle* hh, double rtol, int32_t maxit, int32_t* iters_out,
+                double* relres_out) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h) return SGIGA_ERR_VALUE;
+    if (!h->assembled) { set_error("sgiga_solve before sgiga_assemble"); return SGIGA_ERR_STATE; }
+    if (!(rtol > 0.0)) { set_error("rtol must be positive"); return SGIGA_ERR_VALUE; }
+    if (maxit < 1) maxit = 1000000;
+    h->launches[1] = 0;
+    SG_CUDA(cudaEventRecord(h->ev[2], h->stream));
+    SG_CUDA(cudaMemsetAsync(h->d_cg, 0, sizeof(CgState) * h->ncomp, h->stream));
+    int st = run_pcg(h, rtol, maxit);
+    if (st) return st;
+    h->kstart(5);
+    SG_CUDA(launch_residual_check(h));
+    SG_CUDA(launch_expand(h));
+    h->kstop(5);
+    SG_CUDA(cudaEventRecord(h->ev[3], h->stream));
+    std::vector<CgState> cg(h->ncomp);
+    std::vector<double> rel(h->ncomp);
+    SG_CUDA(cudaMemcpyAsync(cg.data(), h->d_cg, sizeof(CgState) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaMemcpyAsync(rel.data(), h->d_relres, sizeof(double) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    SG_CUDA(cudaEventElapsedTime(&h->ms[1], h->ev[2], h->ev[3]));
+    h->have_coefs = true;
+    h->solved = true;
+    int status = SGIGA_OK;
+    char buf[256];
+    for (int c = 0; c < h->ncomp; ++c) {
+        const CompInfo& C = h->comps[c];
+        h->iters[c] = C.rows ? cg[c].it : 0;
+        if (iters_out) iters_out[c] = h->iters[c];
+        if (relres_out) relres_out[c] = C.rows ? rel[c] : 0.0;
+        if (!C.rows || cg[c].bb == 0.0) continue;
+        if (!std::isfinite(rel[c])) {
+            snprintf(buf, sizeof buf, "component %d: solve produced non-finite values", c);
+            set_error(buf);
+            status = SGIGA_ERR_SOLVE;
+        } else if (!cg[c].conv) {
+            snprintf(buf, sizeof buf, "component %d: PCG did not converge in %d iterations", c, cg[c].it);
+            set_error(buf);
+            status = SGIGA_ERR_SOLVE;
+        } else if (rel[c] > 1e-10) {   // linsolve.py:49-53
+            snprintf(buf, sizeof buf, "component %d: relative residual %.3e exceeds tol 1.0e-10", c, rel[c]);
+            set_error(buf);
+            status = SGIGA_ERR_SOLVE;
+        }
+    }
+    return status;
+}
+
+int sgiga_iterations(sgiga_handle* hh, int32_t* iters) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !iters) return SGIGA_ERR_VALUE;
+    for (int c = 0; c < h->ncomp; ++c) iters[c] = h->iters[c];
+    return SGIGA_OK;
+}
+
+int sgiga_coefficients(sgiga_handle* hh, double* out) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !out) return SGIGA_ERR_VALUE;
+    if (!h->have_coefs) { set_error("no coefficients: solve or set them first"); return SGIGA_ERR_STATE; }
+    SG_CUDA(cudaMemcpyAsync(out, h->d_coef, sizeof(double) * h->total_dofs, cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    return SGIGA_OK;
+}
+
+int sgiga_set_coefficients(sgiga_handle* hh, const double* full) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !full) return SGIGA_ERR_VALUE;
+    SG_CUDA(cudaMemcpyAsync(h->d_coef, full, sizeof(double) * h->total_dofs, cudaMemcpyHostToDevice, h->stream));
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    int st = ensure_tables(h);
+    if (st) return st;
+    h->have_coefs = true;
+    return SGIGA_OK;
+}
+
+static int ensure_scratch(double** buf, size_t* cap, size_t n) {
+    if (*cap >= n && *buf) return SGIGA_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    SG_CUDA(cudaMalloc(reinterpret_cast<void**>(buf), std::max<size_t>(n, 1) * sizeof(double)));
+    *cap = n;
+    return SGIGA_OK;
+}
+
+static thread_local double* s_pts = nullptr;
+static thread_local size_t s_pts_cap = 0;
+static thread_local double* s_out = nullptr;
+static thread_local size_t s_out_cap = 0;
+
+int sgiga_combine_points(sgiga_handle* hh, const double* pts, int64_t npts, double* out,
+                         int32_t device) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || npts < 0) return SGIGA_ERR_VALUE;
+    if (!h->have_coefs) { set_error("combine before solve"); return SGIGA_ERR_STATE; }
+    if (npts == 0) return SGIGA_OK;
+    h->launches[2] = 0;
+    SG_CUDA(cudaEventRecord(h->ev[4], h->stream));
+    const double* dp = pts;
+    double* dout = out;
+    int st;
+    int per_comp = device < 0;       // device = -1 / -2: per-component values (host / device)
+    int dev_ptrs = (device == 1 || device == -2);
+    size_t nout = per_comp ? (size_t)npts * h->ncomp : (size_t)npts;
+    if (!dev_ptrs) {
+        if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
+        if ((st = ensure_scratch(&s_out, &s_out_cap, nout))) return st;
+        SG_CUDA(cudaMemcpyAsync(s_pts, pts, sizeof(double) * npts * h->d, cudaMemcpyHostToDevice, h->stream));
+        dp = s_pts;
+        dout = s_out;
+    }
+    h->kstart(6);
+    SG_CUDA(launch_combine_points(h, dp, npts, dout, per_comp));
+    h->kstop(6);
+    if (!dev_ptrs)
+        SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaEventRecord(h->ev[5], h->stream));
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    SG_CUDA(cudaEventElapsedTime(&h->ms[2], h->ev[4], h->ev[5]));
+    return SGIGA_OK;
+}
+
+int sgiga_combine_grid(sgiga_handle* hh, const double* pts_per_dir, const int64_t* npd,
+                       int32_t comp, double* vals, double* grads) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !pts_per_dir || !npd || !vals) return SGIGA_ERR_VALUE;
+    if (!h->have_coefs) { set_error("combine before solve"); return SGIGA_ERR_STATE; }
+    if (comp >= h->ncomp) { set_error("component index out of range"); return SGIGA_ERR_KEY; }
+    int64_t N = 1, P = 0;
+    for (int k = 0; k < h->d; ++k) { N *= npd[k]; P += npd[k]; }
+    double *dp = nullptr, *dv = nullptr, *dg = nullptr;
+    SG_CUDA(cudaMalloc(&dp, sizeof(double) * std::max<int64_t>(P, 1)));
+    SG_CUDA(cudaMalloc(&dv, sizeof(double) * std::max<int64_t>(N, 1)));
+    if (grads) SG_CUDA(cudaMalloc(&dg, sizeof(double) * std::max<int64_t>(N * h->d, 1)));
+    SG_CUDA(cudaMemcpyAsync(dp, pts_per_dir, sizeof(double) * P, cudaMemcpyHostToDevice, h->stream));
+    SG_CUDA(launch_combine_grid(h, dp, npd, comp, dv, dg));
+    SG_CUDA(cudaMemcpyAsync(vals, dv, sizeof(double) * N, cudaMemcpyDeviceToHost, h->stream));
+    if (grads) SG_CUDA(cudaMemcpyAsync(grads, dg, sizeof(double) * N * h->d, cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    cudaFree(dp); cudaFree(dv);
+    if (dg) cudaFree(dg);
+    return SGIGA_OK;
+}
+
+int sgiga_error_norms(sgiga_handle* hh, const double* pts, const double* wts,
+                      const int64_t* npd, int32_t solution_id, double* out) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !pts || !wts || !npd || !out) return SGIGA_ERR_VALUE;
+    if (!h->have_coefs) { set_error("error norms before solve"); return SGIGA_ERR_STATE; }
+    int64_t N = 1, P = 0;
+    for (int k = 0; k < h->d; ++k) { N *= npd[k]; P += npd[k]; }
+    int64_t nb = (N + 255) / 256;
+    double *dp = nullptr, *dw = nullptr, *dpart = nullptr;
+    SG_CUDA(cudaMalloc(&dp, sizeof(double) * std::max<int64_t>(P, 1)));
+    SG_CUDA(cudaMalloc(&dw, sizeof(double) * std::max<int64_t>(P, 1)));
+    SG_CUDA(cudaMalloc(&dpart, sizeof(double) * (2 * nb + 2)));
+    SG_CUDA(cudaMemcpyAsync(dp, pts, sizeof(double) * P, cudaMemcpyHostToDevice, h->stream));
+    SG_CUDA(cudaMemcpyAsync(dw, wts, sizeof(double) * P, cudaMemcpyHostToDevice, h->stream));
+    int64_t nbl = 0;
+    SG_CUDA(launch_error_norms(h, dp, dw, npd, solution_id, dpart, &nbl));
+    SG_CUDA(cudaMemcpyAsync(out, dpart + 2 * nbl, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    cudaFree(dp); cudaFree(dw); cudaFree(dpart);
+    return check_err(h);
+}
+
+int sgiga_export_csr(sgiga_handle* hh, int32_t comp, int64_t* nnz_out, int64_t* indptr,
+                     int32_t* indices, double* data, double* rhs) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !nnz_out) return SGIGA_ERR_VALUE;
+    if (comp < 0 || comp >= h->ncomp) { set_error("component index out of range"); return SGIGA_ERR_KEY; }
+    if (!h->assembled) { set_error("export before assemble"); return SGIGA_ERR_STATE; }
+    const CompInfo& C = h->comps[comp];
+    const int d = h->d, p = h->p;
+    std::vector<double> st((size_t)C.rows * C.nslots), b((size_t)C.rows);
+    if (C.rows) {
+        SG_CUDA(cudaMemcpy(st.data(), h->d_stencil + C.mat_off, sizeof(double) * st.size(), cudaMemcpyDeviceToHost));
+        SG_CUDA(cudaMemcpy(b.data(), h->d_rhs + C.vec_off, sizeof(double) * b.size(), cudaMemcpyDeviceToHost));
+    }
+    int64_t M[3] = {1, 1, 1};
+    for (int k = d - 2; k >= 0; --k) M[k] = M[k + 1] * C.m[k + 1];
+    int64_t nnz = 0;
+    if (indptr) indptr[0] = 0;
+    for (int64_t ref = 0; ref < C.rows; ++ref) {
+        int r[3] = {0, 0, 0};
+        int64_t rem = ref, irow = 0;
+        for (int k = d - 1; k >= 0; --k) { r[k] = (int)(rem % C.m[k]); rem /= C.m[k]; }
+        for (int k = 0; k < d; ++k) irow += (int64_t)r[k] * C.rs[k];
+        if (rhs) rhs[ref] = b[irow];
+        int S0 = C.S[0], S1 = d > 1 ? C.S[1] : 1, S2 = d > 2 ? C.S[2] : 1;
+        for (int s0 = 0; s0 < S0; ++s0)
+            for (int s1 = 0; s1 < S1; ++s1)
+                for (int s2 = 0; s2 < S2; ++s2) {
+                    int sl[3] = {s0, s1, s2};
+                    int64_t col = 0, slot = 0;
+                    bool ok = true;
+                    for (int k = 0; k < d; ++k) {
+                        int c = C.absm[k] ? sl[k] : r[k] + sl[k] - p;
+                        if (c < 0 || c >= C.m[k] || std::abs(c - r[k]) > p) { ok = false; break; }
+                        col += (int64_t)c * M[k];
+                        slot += (int64_t)sl[k] * C.ss[k];
+                    }
+                    if (!ok) continue;
+                    double v = st[(size_t)slot * C.rows + irow];
+                    if (v == 0.0) continue;   // scipy csr addition drops exact zeros
+                    if (indices) indices[nnz] = (int32_t)col;
+                    if (data) data[nnz] = v;
+                    ++nnz;
+                }
+        if (indptr) indptr[ref + 1] = nnz;
+    }
+    *nnz_out = nnz;
+    return SGIGA_OK;
+}
+
+int sgiga_phase_stats(sgiga_handle* hh, float* ms3, int64_t* launches3) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h) return SGIGA_ERR_VALUE;
+    for (int i = 0; i < 3; ++i) {
+        if (ms3) ms3[i] = h->ms[i];
+        if (launches3) launches3[i] = h->launches[i];
+    }
+    return SGIGA_OK;
+}
+
+int sgiga_kernel_times(sgiga_handle* hh, float* ms7) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !ms7) return SGIGA_ERR_VALUE;
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    for (int g = 0; g < 7; ++g) {
+        float ms = 0.0f;
+        if (h->kran[g] && cudaEventElapsedTime(&ms, h->kev[2 * g], h->kev[2 * g + 1]) != cudaSuccess) ms = -1.0f;
+        ms7[g] = h->kran[g] ? ms : 0.0f;
+    }
+    cudaGetLastError();
+    return SGIGA_OK;
+}
+
+void* sgiga_stream(sgiga_handle* hh) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    return h ? (void*)h->stream : nullptr;
+}
+
+int sgiga_destroy(sgiga_handle* hh) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h) return SGIGA_OK;
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    free_all(h);
+    delete h;
+    return SGIGA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// handle.cuh -- host-side state of one batched plan (C++ only).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "sgiga_internal.cuh"
+
+namespace sgiga {
+
+void set_error(const std::string& msg);
+
+#define SG_CUDA(call)                                                             \
+    do {                                                                          \
+        cudaError_t _e = (call);                                                  \
+        if (_e != cudaSuccess) {                                                  \
+            ::sgiga::set_error(std::string(#call) + ": " + cudaGetErrorString(_e)); \
+            return SGIGA_ERR_CUDA;                                                \
+        }                                                                         \
+    } while (0)
+
+struct Handle {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+
+    // problem
+    int d = 0, p = 0, r = 0, q = 0, mu = 1, ncomp = 0, max_level = 0, forcing_id = 0;
+    std::vector<int> levels, coefs;
+    std::vector<double> gauss_n, gauss_w;
+    GeoInfo geo{};
+    std::vector<double> geo_knots, geo_hw;
+
+    // component / table / work lists (host mirrors)
+    std::vector<CompInfo> comps;
+    std::vector<TabInfo> tabs;
+    std::vector<int> tab_of;           // [d*(max_level+1)] -> tab index
+    std::vector<double> bp_host;       // concatenated breakpoints
+    std::vector<Pencil> pencils;
+    std::vector<Chunk> chunks;
+    std::vector<int> small_comps, large_comps;
+    int64_t total_qp = 0, total_rows = 0, total_vec = 0, total_slots = 0, total_dofs = 0;
+    int64_t total_knots = 0, total_tabvals = 0, total_tabqp = 0;
+    int max_slots_comp = 0;
+
+    // device buffers
+    CompInfo* d_comps = nullptr;
+    TabInfo* d_tabs = nullptr;
+    GeoInfo* d_geo = nullptr;
+    Pencil* d_pencils = nullptr;
+    Chunk* d_chunks = nullptr;
+    int* d_small = nullptr;
+    int* d_large = nullptr;
+    double* d_bp = nullptr;
+    double* d_knots = nullptr;
+    double* d_gauss = nullptr;   // nodes [q], weights [q]
+    double* d_tabvals = nullptr;
+    double* d_qx = nullptr;      // xi at table quad points
+    double* d_qw = nullptr;      // h * w_g
+    double* d_geob = nullptr;    // geometry basis at table quad points
+    int* d_geofirst = nullptr;   // first active geometry function
+    double* d_geo_knots = nullptr;
+    double* d_geo_hw = nullptr;
+    double* d_G = nullptr;       // metric (ncg comps) + load per qp
+    double* d_hostf = nullptr;   // host forcing densities (SGIGA_FORCING_HOST)
+    double* d_xphys = nullptr;   // physical qp coordinates (host forcing only)
+    double* d_stencil = nullptr;
+    double* d_rhs = nullptr;
+    double* d_dinv = nullptr;
+    double* d_x = nullptr;
+    double* d_r = nullptr;
+    double* d_z = nullptr;
+    double* d_p = nullptr;
+    double* d_q = nullptr;
+    double* d_coef = nullptr;    // full coefficients, reference C order
+    CgState* d_cg = nullptr;
+    double* d_part = nullptr;    // per-chunk partial sums [3*nchunks]
+    int* d_err = nullptr;
+    int* d_active_count = nullptr;
+    double* d_relres = nullptr;
+    int* h_pinned_flag = nullptr;  // pinned host mirror of the active count
+
+    // state
+    bool tables_ready = false, density_ready = false, assembled = false, solved = false,
+         have_coefs = false;
+    cudaEvent_t ev[8] = {};
+    cudaEvent_t kev[14] = {};     // kernel-group start/stop pairs (sgiga_kernel_times)
+    float kms[7] = {0, 0, 0, 0, 0, 0, 0};
+    bool kran[7] = {false, false, false, false, false, false, false};
+    float ms[3] = {0, 0, 0};
+    long long launches[3] = {0, 0, 0};
+    std::vector<int> iters;
+
+    void kstart(int g) { cudaEventRecord(kev[2 * g], stream); kran[g] = true; }
+    void kstop(int g) { cudaEventRecord(kev[2 * g + 1], stream); }
+    int ncg() const { return d * (d + 1) / 2; }   // symmetric metric entries
+    int nG() const { return ncg() + 1; }           // + load
+};
+
+// symmetric index of (m, n) in the packed metric (row-major upper triangle)
+__host__ __device__ inline int sym_index(int d, int m, int n) {
+    if (m > n) { int t = m; m = n; n = t; }
+    // rows: m=0: n=0..d-1 ; m=1: n=1..d-1 ; ...
+    return m * d - (m * (m - 1)) / 2 + (n - m);
+}
+
+}  // namespace sgiga

@@ -1,0 +1,399 @@
+// k_combine.cu -- kernel 4: the combination step sum_beta c_beta u_beta at
+// scattered points or on tensor grids (with parametric gradients), and the
+// L2 / H1-seminorm error quadrature against a device closed form.
+//
+// Reference: combination.evaluate_combined (combination.py:209-236) with
+// DiscreteSpace.eval_grid / _tensor_apply (assembly.py:101-138), the
+// per-point idiom of tests/test_acceptance.py:224-230, and
+// analysis.error_norms / _push_gradient (analysis.py:235-270).
+//
+// One thread per point.  Components are visited in plan (lexicographic)
+// order; the 1-D Cox-de Boor values of an axis are recomputed only when the
+// level changes between consecutive components (lexicographic order keeps
+// the leading axes constant for long runs).  The tensor contraction is
+// sum-factorised (P^D + ... + P FMAs per component).
+#include "forcing.cuh"
+#include "handle.cuh"
+
+namespace sgiga {
+
+template <int D, bool GRAD>
+__device__ __forceinline__ void eval_component(const CompInfo& C, const double* __restrict__ coef,
+                                               const int* first, const double (*Bv)[PMAX],
+                                               const double (*Bd)[PMAX], int P, double& v,
+                                               double* g) {
+    const double* cf = coef + C.dof_off;
+    if (D == 1) {
+        double sv = 0.0, sd = 0.0;
+        for (int a = 0; a < P; ++a) {
+            double c = cf[first[0] + a];
+            sv += Bv[0][a] * c;
+            if (GRAD) sd += Bd[0][a] * c;
+        }
+        v = sv;
+        if (GRAD) g[0] = sd;
+    } else if (D == 2) {
+        const int n1 = C.n[1];
+        double v0 = 0.0, g0 = 0.0, g1 = 0.0;
+        for (int a = 0; a < P; ++a) {
+            const double* row = cf + (int64_t)(first[0] + a) * n1 + first[1];
+            double tv = 0.0, td = 0.0;
+            for (int b = 0; b < P; ++b) {
+                double c = row[b];
+                tv += Bv[1][b] * c;
+                if (GRAD) td += Bd[1][b] * c;
+            }
+            v0 += Bv[0][a] * tv;
+            if (GRAD) { g0 += Bd[0][a] * tv; g1 += Bv[0][a] * td; }
+        }
+        v = v0;
+        if (GRAD) { g[0] = g0; g[1] = g1; }
+    } else {
+        const int n1 = C.n[1], n2 = C.n[2];
+        double v0 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
+        for (int a = 0; a < P; ++a) {
+            double uv = 0.0, u1 = 0.0, u2 = 0.0;
+            for (int b = 0; b < P; ++b) {
+                const double* row = cf + ((int64_t)(first[0] + a) * n1 + (first[1] + b)) * n2 + first[2];
+                double tv = 0.0, td = 0.0;
+#pragma unroll 5
+                for (int l = 0; l < P; ++l) {
+                    double c = row[l];
+                    tv += Bv[2][l] * c;
+                    if (GRAD) td += Bd[2][l] * c;
+                }
+                uv += Bv[1][b] * tv;
+                if (GRAD) { u1 += Bd[1][b] * tv; u2 += Bv[1][b] * td; }
+            }
+            v0 += Bv[0][a] * uv;
+            if (GRAD) { g0 += Bd[0][a] * uv; g1 += Bv[0][a] * u1; g2 += Bv[0][a] * u2; }
+        }
+        v = v0;
+        if (GRAD) { g[0] = g0; g[1] = g1; g[2] = g2; }
+    }
+}
+
+template <int D, bool GRAD>
+__device__ __forceinline__ void axis_basis(const TabInfo& T, const double* __restrict__ knots,
+                                           int p, double xi, int& first, double* bv, double* bd) {
+    const double* k = knots + T.knot_off;
+    int span = find_span(k, T.nk, p, xi, xi == 1.0);   // splines.py:255-257
+    double tab[2 * (PMAX + 2)];
+    ders_basis_funs(span, xi, p, GRAD ? 1 : 0, k, tab);
+    first = span - p;
+    for (int j = 0; j <= p; ++j) {
+        bv[j] = tab[j];
+        if (GRAD) bd[j] = tab[p + 1 + j];
+    }
+}
+
+// sum over components (plan order) at one parametric point
+template <int D, bool GRAD>
+__device__ __forceinline__ void combine_at(const CompInfo* __restrict__ comps, int c_lo, int c_hi,
+                                           bool weighted, const TabInfo* __restrict__ tabs,
+                                           const double* __restrict__ knots,
+                                           const double* __restrict__ coef, int p,
+                                           const double* xi, double& acc, double* gacc,
+                                           double* per_comp, int64_t per_stride) {
+    int cur[D], first[D];
+    double Bv[D][PMAX], Bd[D][PMAX];
+#pragma unroll
+    for (int k = 0; k < D; ++k) cur[k] = -1;
+    bool started = false;
+    acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) gacc[k] = 0.0;
+    for (int c = c_lo; c < c_hi; ++c) {
+        const CompInfo& C = comps[c];
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+            if (C.tab[k] != cur[k]) {
+                cur[k] = C.tab[k];
+                axis_basis<D, GRAD>(tabs[cur[k]], knots, p, xi[k], first[k], Bv[k], Bd[k]);
+            }
+        double v, g[D];
+        eval_component<D, GRAD>(C, coef, first, Bv, Bd, p + 1, v, g);
+        if (per_comp) { per_comp[(int64_t)c * per_stride] = v; continue; }
+        double cf = weighted ? (double)C.coef : 1.0;
+        // plan-order accumulation: vals = c*v, then vals += c*v (combination.py:227-233)
+        if (!started) {
+            acc = cf * v;
+#pragma unroll
+            for (int k = 0; k < D; ++k) gacc[k] = cf * g[k];
+            started = true;
+        } else {
+            acc = __dadd_rn(acc, cf * v);
+#pragma unroll
+            for (int k = 0; k < D; ++k) gacc[k] = __dadd_rn(gacc[k], cf * g[k]);
+        }
+    }
+}
+
+template <int D>
+__global__ void k_combine_points(const CompInfo* __restrict__ comps, int ncomp,
+                                 const TabInfo* __restrict__ tabs, const double* __restrict__ knots,
+                                 const double* __restrict__ coef, int p,
+                                 const double* __restrict__ pts, int64_t npts,
+                                 double* __restrict__ out, int per_component) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= npts) return;
+    double xi[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) xi[k] = pts[t * D + k];
+    double acc, g[D];
+    combine_at<D, false>(comps, 0, ncomp, true, tabs, knots, coef, p, xi, acc, g,
+                         per_component ? out + t : nullptr, npts);
+    if (!per_component) out[t] = acc;
+}
+
+template <int D>
+__global__ void k_combine_grid(const CompInfo* __restrict__ comps, int ncomp,
+                               const TabInfo* __restrict__ tabs, const double* __restrict__ knots,
+                               const double* __restrict__ coef, int p,
+                               const double* __restrict__ pts, int64_t n0, int64_t n1, int64_t n2,
+                               int comp, double* __restrict__ vals, double* __restrict__ grads) {
+    int64_t N = n0 * (D > 1 ? n1 : 1) * (D > 2 ? n2 : 1);
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int64_t npd[3] = {n0, n1, n2}, off[3] = {0, n0, n0 + n1};
+    double xi[D];
+    int64_t rem = t;
+#pragma unroll
+    for (int k = D - 1; k >= 0; --k) { xi[k] = pts[off[k] + rem % npd[k]]; rem /= npd[k]; }
+    double acc, g[D];
+    int lo = comp >= 0 ? comp : 0, hi = comp >= 0 ? comp + 1 : ncomp;
+    if (grads) {
+        combine_at<D, true>(comps, lo, hi, comp < 0, tabs, knots, coef, p, xi, acc, g, nullptr, 0);
+#pragma unroll
+        for (int k = 0; k < D; ++k) grads[t * D + k] = g[k];
+    } else {
+        combine_at<D, false>(comps, lo, hi, comp < 0, tabs, knots, coef, p, xi, acc, g, nullptr, 0);
+    }
+    vals[t] = acc;
+}
+
+// geometry map at one parametric point (geometry.py:87-132)
+template <int D>
+__device__ __forceinline__ double geo_point(const GeoInfo& G, const double* __restrict__ gknots,
+                                            const double* __restrict__ hw, const double* xi,
+                                            double* x, double (*Ji)[D]) {
+    int first[D];
+    double bv[D][GEO_PMAX + 1], bd[D][GEO_PMAX + 1];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const double* kk = gknots + G.knot_off[k];
+        int span = find_span(kk, G.nk[k], G.deg[k], xi[k], xi[k] == 1.0);
+        double tab[2 * (GEO_PMAX + 1)];
+        ders_basis_funs(span, xi[k], G.deg[k], 1, kk, tab);
+        first[k] = span - G.deg[k];
+        for (int j = 0; j <= G.deg[k]; ++j) { bv[k][j] = tab[j]; bd[k][j] = tab[G.deg[k] + 1 + j]; }
+    }
+    double hom[D + 1], dh[D][D + 1];
+#pragma unroll
+    for (int c = 0; c <= D; ++c) {
+        hom[c] = 0.0;
+#pragma unroll
+        for (int m = 0; m < D; ++m) dh[m][c] = 0.0;
+    }
+    int c0 = G.deg[0] + 1, c1 = D > 1 ? G.deg[D > 1 ? 1 : 0] + 1 : 1, c2 = D > 2 ? G.deg[D - 1] + 1 : 1;
+    for (int i = 0; i < c0; ++i)
+        for (int j = 0; j < c1; ++j)
+            for (int l = 0; l < c2; ++l) {
+                int idx[3] = {i, j, l};
+                int64_t L = 0;
+                double prod = 1.0, pm[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) L = L * G.n[k] + (first[k] + idx[k]);
+#pragma unroll
+                for (int k = 0; k < D; ++k) prod *= bv[k][idx[k]];
+#pragma unroll
+                for (int m = 0; m < D; ++m) {
+                    double t = 1.0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) t *= (k == m) ? bd[k][idx[k]] : bv[k][idx[k]];
+                    pm[m] = t;
+                }
+#pragma unroll
+                for (int c = 0; c <= D; ++c) {
+                    double hv = hw[L * (D + 1) + c];
+                    hom[c] += prod * hv;
+#pragma unroll
+                    for (int m = 0; m < D; ++m) dh[m][c] += pm[m] * hv;
+                }
+            }
+    double J[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[i] = hom[i] / hom[D];
+#pragma unroll
+    for (int m = 0; m < D; ++m)
+#pragma unroll
+        for (int i = 0; i < D; ++i) J[i][m] = (dh[m][i] - x[i] * dh[m][D]) / hom[D];
+    double det;
+    if constexpr (D == 1) {
+        det = J[0][0];
+        Ji[0][0] = 1.0 / det;
+    } else if constexpr (D == 2) {
+        det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        Ji[0][0] = J[1][1] / det; Ji[0][1] = -J[0][1] / det;
+        Ji[1][0] = -J[1][0] / det; Ji[1][1] = J[0][0] / det;
+    } else {
+        double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+        double c01 = J[1][0] * J[2][2] - J[1][2] * J[2][0];
+        double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+        det = J[0][0] * c00 - J[0][1] * c01 + J[0][2] * c02;
+        Ji[0][0] = c00 / det;
+        Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+        Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+        Ji[1][0] = -c01 / det;
+        Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+        Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+        Ji[2][0] = c02 / det;
+        Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+        Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+    }
+    return det;
+}
+
+constexpr int ERR_THREADS = 256;
+
+template <int D>
+__global__ void __launch_bounds__(ERR_THREADS)
+k_error_norms(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
+              const double* __restrict__ knots, const double* __restrict__ coef, int p,
+              const GeoInfo* __restrict__ geo, const double* __restrict__ gknots,
+              const double* __restrict__ hw, const double* __restrict__ pts,
+              const double* __restrict__ wts, int64_t n0, int64_t n1, int64_t n2, int sol_id,
+              double* __restrict__ partials, int* __restrict__ err) {
+    __shared__ double red[2][ERR_THREADS / 32];
+    int64_t N = n0 * (D > 1 ? n1 : 1) * (D > 2 ? n2 : 1);
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double e2 = 0.0, h2 = 0.0;
+    if (t < N) {
+        int64_t npd[3] = {n0, n1, n2}, off[3] = {0, n0, n0 + n1};
+        double xi[D], w = 1.0;
+        int64_t rem = t;
+        int64_t jj[D];
+#pragma unroll
+        for (int k = D - 1; k >= 0; --k) { jj[k] = rem % npd[k]; xi[k] = pts[off[k] + jj[k]]; rem /= npd[k]; }
+#pragma unroll
+        for (int k = 0; k < D; ++k) w = (k == 0) ? wts[off[0] + jj[0]] : w * wts[off[k] + jj[k]];
+        double x[D], Ji[D][D];
+        const GeoInfo G = *geo;
+        double det = geo_point<D>(G, gknots, hw, xi, x, Ji);
+        if (!(det > 0.0)) atomicOr(err, ERRF_GEOMETRY);
+        double acc, g[D];
+        combine_at<D, true>(comps, 0, ncomp, true, tabs, knots, coef, p, xi, acc, g, nullptr, 0);
+        double ue, ge[D];
+        solution_value<D>(sol_id, x, ue, ge);
+        double dv = acc - ue, dg2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {   // J^-T grad (analysis.py:235-237)
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s += Ji[k][i] * g[k];
+            double e = s - ge[i];
+            dg2 += e * e;
+        }
+        double wd = w * det;   // QuadGrid.weights = wgrid * det (assembly.py:178)
+        e2 = wd * (dv * dv);
+        h2 = wd * dg2;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+    }
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { red[0][wid] = e2; red[1][wid] = h2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int i = 0; i < ERR_THREADS / 32; ++i) { a += red[0][i]; b += red[1][i]; }
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+    }
+}
+
+// ordered final sum of the block partials (one CTA)
+__global__ void k_sum_partials(const double* __restrict__ partials, int64_t nblocks,
+                               double* __restrict__ out) {
+    __shared__ double red[2][32];
+    double a = 0.0, b = 0.0;
+    for (int64_t i = threadIdx.x; i < nblocks; i += blockDim.x) {
+        a += partials[2 * i];
+        b += partials[2 * i + 1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { red[0][wid] = a; red[1][wid] = b; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { s0 += red[0][i]; s1 += red[1][i]; }
+        out[0] = sqrt(s0);
+        out[1] = sqrt(s1);
+    }
+}
+
+cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, double* d_out,
+                                  int per_component) {
+    if (npts == 0) return cudaSuccess;
+    unsigned blocks = (unsigned)((npts + 127) / 128);
+#define LAUNCH_CP(DD)                                                                       \
+    k_combine_points<DD><<<blocks, 128, 0, h->stream>>>(h->d_comps, h->ncomp, h->d_tabs,     \
+                                                         h->d_knots, h->d_coef, h->p, d_pts, \
+                                                         npts, d_out, per_component)
+    if (h->d == 1) LAUNCH_CP(1);
+    else if (h->d == 2) LAUNCH_CP(2);
+    else LAUNCH_CP(3);
+#undef LAUNCH_CP
+    h->launches[2]++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_combine_grid(Handle* h, const double* d_pts, const int64_t* npd, int comp,
+                                double* d_vals, double* d_grads) {
+    int64_t N = 1;
+    for (int k = 0; k < h->d; ++k) N *= npd[k];
+    if (N == 0) return cudaSuccess;
+    unsigned blocks = (unsigned)((N + 127) / 128);
+    int64_t n1 = h->d > 1 ? npd[1] : 1, n2 = h->d > 2 ? npd[2] : 1;
+#define LAUNCH_CG(DD)                                                                          \
+    k_combine_grid<DD><<<blocks, 128, 0, h->stream>>>(h->d_comps, h->ncomp, h->d_tabs,          \
+                                                       h->d_knots, h->d_coef, h->p, d_pts,      \
+                                                       npd[0], n1, n2, comp, d_vals, d_grads)
+    if (h->d == 1) LAUNCH_CG(1);
+    else if (h->d == 2) LAUNCH_CG(2);
+    else LAUNCH_CG(3);
+#undef LAUNCH_CG
+    h->launches[2]++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_error_norms(Handle* h, const double* d_pts, const double* d_wts,
+                               const int64_t* npd, int solution_id, double* d_partials,
+                               int64_t* nblocks) {
+    int64_t N = 1;
+    for (int k = 0; k < h->d; ++k) N *= npd[k];
+    int64_t nb = (N + ERR_THREADS - 1) / ERR_THREADS;
+    *nblocks = nb;
+    int64_t n1 = h->d > 1 ? npd[1] : 1, n2 = h->d > 2 ? npd[2] : 1;
+#define LAUNCH_EN(DD)                                                                          \
+    k_error_norms<DD><<<(unsigned)nb, ERR_THREADS, 0, h->stream>>>(                            \
+        h->d_comps, h->ncomp, h->d_tabs, h->d_knots, h->d_coef, h->p, h->d_geo,                \
+        h->d_geo_knots, h->d_geo_hw, d_pts, d_wts, npd[0], n1, n2, solution_id, d_partials,    \
+        h->d_err)
+    if (h->d == 1) LAUNCH_EN(1);
+    else if (h->d == 2) LAUNCH_EN(2);
+    else LAUNCH_EN(3);
+#undef LAUNCH_EN
+    k_sum_partials<<<1, 1024, 0, h->stream>>>(d_partials, nb, d_partials + 2 * nb);
+    h->launches[2] += 2;
+    return cudaGetLastError();
+}
+
+}  // namespace sgiga

@@ -1,0 +1,257 @@
+// k_tables.cu -- kernel 1 (knots + Cox-de Boor basis tables at Gauss
+// points, staged per (axis, level)) and the fused per-quadrature-point
+// geometry / metric / load kernel.
+//
+// Reference: splines.make_open_knot_vector (splines.py:83-110),
+// assembly._direction_tables (assembly.py:209-234), NurbsPatch.eval_grid
+// (geometry.py:87-132), metric + load (assembly.py:286-294).
+#include "forcing.cuh"
+#include "handle.cuh"
+
+namespace sgiga {
+
+// ---- open knot vectors from breakpoints ---------------------------------
+__global__ void k_build_knots(const TabInfo* __restrict__ tabs, int ntab, int p, int mu,
+                              const double* __restrict__ bp, double* __restrict__ knots) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntab) return;
+    TabInfo T = tabs[t];
+    double* k = knots + T.knot_off;
+    const double* b = bp + T.bp_off;
+    int pos = 0;
+    for (int i = 0; i <= p; ++i) k[pos++] = 0.0;
+    for (int e = 1; e < T.nel; ++e)
+        for (int j = 0; j < mu; ++j) k[pos++] = b[e];
+    for (int i = 0; i <= p; ++i) k[pos++] = 1.0;
+}
+
+// ---- basis + geometry-basis tables at every (table, element, node) -------
+__global__ void k_basis_tables(const TabInfo* __restrict__ tabs, int ntab,
+                               const int64_t* __restrict__ tab_qp_cum, int p, int mu, int q,
+                               const double* __restrict__ gauss, const double* __restrict__ bp,
+                               const double* __restrict__ knots, const GeoInfo* __restrict__ geo,
+                               const double* __restrict__ gknots, double* __restrict__ vals,
+                               double* __restrict__ qx, double* __restrict__ qw,
+                               double* __restrict__ geob, int* __restrict__ geofirst,
+                               int* __restrict__ err) {
+    int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= tab_qp_cum[ntab]) return;
+    int lo = 0, hi = ntab;  // table of this thread
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (tab_qp_cum[mid] <= gid) lo = mid; else hi = mid;
+    }
+    const TabInfo T = tabs[lo];
+    int local = (int)(gid - tab_qp_cum[lo]);
+    int e = local / q, g = local % q;
+    const double* b = bp + T.bp_off;
+    double a0 = b[e], h = __dsub_rn(b[e + 1], a0);
+    double xi = __dadd_rn(a0, __dmul_rn(h, gauss[g]));   // assembly.py:224
+    double w = __dmul_rn(h, gauss[q + g]);                // assembly.py:233
+    int P = p + 1;
+    double tab[2 * (PMAX + 2)];
+    ders_basis_funs(p + e * mu, xi, p, 1, knots + T.knot_off, tab);
+    double* vv = vals + T.val_off;
+    int64_t nq = (int64_t)T.nel * q;
+    for (int j = 0; j < P; ++j) {
+        vv[(int64_t)local * P + j] = tab[j];
+        vv[nq * P + (int64_t)local * P + j] = tab[P + j];
+    }
+    qx[T.qp_off + local] = xi;
+    qw[T.qp_off + local] = w;
+    // geometry basis of this axis at xi (collocation_matrix, splines.py:262-274)
+    const GeoInfo G = *geo;
+    int ax = T.axis, pg = G.deg[ax];
+    const double* gk = gknots + G.knot_off[ax];
+    int span = find_span(gk, G.nk[ax], pg, xi, xi == 1.0);
+    double gt[2 * (GEO_PMAX + 1)];
+    ders_basis_funs(span, xi, pg, 1, gk, gt);
+    double* gb = geob + (T.geo_off + local) * (2 * GEO_PMAX);
+    for (int j = 0; j <= pg; ++j) {
+        gb[j] = gt[j];
+        gb[GEO_PMAX + j] = gt[pg + 1 + j];
+    }
+    geofirst[T.geo_off + local] = span - pg;
+    if (!(xi > 0.0 && xi < 1.0)) atomicOr(err, ERRF_SPAN);
+}
+
+// ---- fused geometry -> metric + load --------------------------------------
+// One thread per (component, quadrature point), storage order (s, a, b).
+template <int D>
+__global__ void k_metric(const CompInfo* __restrict__ comps, int ncomp,
+                         const int64_t* __restrict__ qp_cum, const TabInfo* __restrict__ tabs,
+                         const double* __restrict__ qx, const double* __restrict__ qw,
+                         const double* __restrict__ geob, const int* __restrict__ geofirst,
+                         const GeoInfo* __restrict__ geo, const double* __restrict__ hw,
+                         int q, int forcing_id, const double* __restrict__ hostf,
+                         double* __restrict__ xphys, double* __restrict__ Gout,
+                         int* __restrict__ err) {
+    int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= qp_cum[ncomp]) return;
+    int lo = 0, hi = ncomp;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (qp_cum[mid] <= gid) lo = mid; else hi = mid;
+    }
+    const CompInfo& C = comps[lo];
+    int64_t lin = gid - qp_cum[lo];
+    const GeoInfo Gi = *geo;
+    double xi[D], w = 1.0;
+    const double* bv[D];
+    int first[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        int64_t Nq = (int64_t)C.nel[k] * q;
+        int64_t Qk = (lin / C.qs[k]) % Nq;
+        const TabInfo& T = tabs[C.tab[k]];
+        xi[k] = qx[T.qp_off + Qk];
+        double wk = qw[T.qp_off + Qk];
+        w = (k == 0) ? wk : __dmul_rn(w, wk);   // _outer_product, assembly.py:186-190
+        bv[k] = geob + (T.geo_off + Qk) * (2 * GEO_PMAX);
+        first[k] = geofirst[T.geo_off + Qk];
+    }
+    // homogeneous contraction (geometry.py:114, 124) over active functions
+    double hom[D + 1], dh[D][D + 1];
+#pragma unroll
+    for (int c = 0; c <= D; ++c) {
+        hom[c] = 0.0;
+#pragma unroll
+        for (int m = 0; m < D; ++m) dh[m][c] = 0.0;
+    }
+    int c0 = Gi.deg[0] + 1, c1 = D > 1 ? Gi.deg[1] + 1 : 1, c2 = D > 2 ? Gi.deg[2] + 1 : 1;
+    for (int i = 0; i < c0; ++i)
+        for (int j = 0; j < c1; ++j)
+            for (int l = 0; l < c2; ++l) {
+                int idx[3] = {i, j, l};
+                int64_t L = 0;
+                double v[D], dv[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    L = L * Gi.n[k] + (first[k] + idx[k]);
+                    v[k] = bv[k][idx[k]];
+                    dv[k] = bv[k][GEO_PMAX + idx[k]];
+                }
+                double prod = v[0];
+#pragma unroll
+                for (int k = 1; k < D; ++k) prod = __dmul_rn(prod, v[k]);
+                double pm[D];
+#pragma unroll
+                for (int m = 0; m < D; ++m) {
+                    double t = (m == 0) ? dv[0] : v[0];
+#pragma unroll
+                    for (int k = 1; k < D; ++k) t = __dmul_rn(t, (k == m) ? dv[k] : v[k]);
+                    pm[m] = t;
+                }
+#pragma unroll
+                for (int c = 0; c <= D; ++c) {
+                    double hv = hw[L * (D + 1) + c];
+                    hom[c] = __dadd_rn(hom[c], __dmul_rn(prod, hv));
+#pragma unroll
+                    for (int m = 0; m < D; ++m) dh[m][c] = __dadd_rn(dh[m][c], __dmul_rn(pm[m], hv));
+                }
+            }
+    double x[D], J[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[i] = __ddiv_rn(hom[i], hom[D]);
+#pragma unroll
+    for (int m = 0; m < D; ++m)
+#pragma unroll
+        for (int i = 0; i < D; ++i)   // quotient rule, geometry.py:126
+            J[i][m] = __ddiv_rn(__dsub_rn(dh[m][i], __dmul_rn(x[i], dh[m][D])), hom[D]);
+    double det, Ji[D][D];
+    if constexpr (D == 1) {
+        det = J[0][0];
+        Ji[0][0] = __ddiv_rn(1.0, J[0][0]);
+    } else if constexpr (D == 2) {
+        det = __dsub_rn(__dmul_rn(J[0][0], J[1][1]), __dmul_rn(J[0][1], J[1][0]));
+        Ji[0][0] = __ddiv_rn(J[1][1], det);
+        Ji[0][1] = __ddiv_rn(-J[0][1], det);
+        Ji[1][0] = __ddiv_rn(-J[1][0], det);
+        Ji[1][1] = __ddiv_rn(J[0][0], det);
+    } else {
+        // cofactors in the oracle's order (oracle/sgiga_oracle.c det_small / inv_small)
+        auto mm = [&](int i, int j) { return J[i][j]; };
+        auto cof = [&](int a, int b, int c, int e) {
+            return __dsub_rn(__dmul_rn(mm(a / 3, a % 3), mm(b / 3, b % 3)), __dmul_rn(mm(c / 3, c % 3), mm(e / 3, e % 3)));
+        };
+        double c00 = cof(4, 8, 5, 7), c01 = cof(3, 8, 5, 6), c02 = cof(3, 7, 4, 6);
+        det = __dadd_rn(__dsub_rn(__dmul_rn(J[0][0], c00), __dmul_rn(J[0][1], c01)), __dmul_rn(J[0][2], c02));
+        Ji[0][0] = __ddiv_rn(c00, det);
+        Ji[0][1] = __ddiv_rn(cof(2, 7, 1, 8), det);
+        Ji[0][2] = __ddiv_rn(cof(1, 5, 2, 4), det);
+        Ji[1][0] = __ddiv_rn(cof(5, 6, 3, 8), det);
+        Ji[1][1] = __ddiv_rn(cof(0, 8, 2, 6), det);
+        Ji[1][2] = __ddiv_rn(cof(2, 3, 0, 5), det);
+        Ji[2][0] = __ddiv_rn(cof(3, 7, 4, 6), det);
+        Ji[2][1] = __ddiv_rn(cof(1, 6, 0, 7), det);
+        Ji[2][2] = __ddiv_rn(cof(0, 4, 1, 3), det);
+    }
+    if (!(det > 0.0)) atomicOr(err, ERRF_GEOMETRY);   // geometry.py:128-131
+    int64_t nqp = C.nqp;
+    double* Gc = Gout + C.qp_off;
+    double dw = __dmul_rn(det, w);
+#pragma unroll
+    for (int m = 0; m < D; ++m)
+#pragma unroll
+        for (int n = m; n < D; ++n) {    // (Jinv Jinv^T) * (det * w), assembly.py:288-289
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) s = __dadd_rn(s, __dmul_rn(Ji[m][i], Ji[n][i]));
+            Gc[(int64_t)sym_index(D, m, n) * nqp + lin] = __dmul_rn(s, dw);
+        }
+    double f;
+    if (forcing_id == SGIGA_FORCING_HOST) {
+        f = hostf ? hostf[gid] : 0.0;
+        if (xphys)
+#pragma unroll
+            for (int i = 0; i < D; ++i) xphys[gid * D + i] = x[i];
+    } else {
+        f = forcing_value<D>(forcing_id, x);
+    }
+    // load = f * det * w (assembly.py:292)
+    Gc[(int64_t)(D * (D + 1) / 2) * nqp + lin] = __dmul_rn(__dmul_rn(f, det), w);
+}
+
+cudaError_t launch_build_knots(Handle* h) {
+    int nt = (int)h->tabs.size();
+    k_build_knots<<<(nt + 127) / 128, 128, 0, h->stream>>>(h->d_tabs, nt, h->p, h->mu, h->d_bp,
+                                                           h->d_knots);
+    h->launches[0]++;
+    return cudaGetLastError();
+}
+
+// tab_qp_cum / qp_cum live right after d_gauss (see handle.cu)
+extern int64_t* tab_qp_cum_ptr(Handle* h);
+extern int64_t* comp_qp_cum_ptr(Handle* h);
+
+cudaError_t launch_basis_tables(Handle* h) {
+    int nt = (int)h->tabs.size();
+    int64_t n = h->total_tabqp;
+    int blocks = (int)((n + 127) / 128);
+    k_basis_tables<<<blocks, 128, 0, h->stream>>>(
+        h->d_tabs, nt, tab_qp_cum_ptr(h), h->p, h->mu, h->q, h->d_gauss, h->d_bp, h->d_knots,
+        h->d_geo, h->d_geo_knots, h->d_tabvals, h->d_qx, h->d_qw, h->d_geob, h->d_geofirst,
+        h->d_err);
+    h->launches[0]++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_metric(Handle* h) {
+    int64_t n = h->total_qp;
+    if (n == 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    const double* hostf = (h->forcing_id == SGIGA_FORCING_HOST) ? h->d_hostf : nullptr;
+#define LAUNCH_METRIC(DD)                                                                    \
+    k_metric<DD><<<(unsigned)blocks, 256, 0, h->stream>>>(                                   \
+        h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->d_geob,    \
+        h->d_geofirst, h->d_geo, h->d_geo_hw, h->q, h->forcing_id, hostf, h->d_xphys, h->d_G, \
+        h->d_err)
+    if (h->d == 1) LAUNCH_METRIC(1);
+    else if (h->d == 2) LAUNCH_METRIC(2);
+    else LAUNCH_METRIC(3);
+#undef LAUNCH_METRIC
+    h->launches[0]++;
+    return cudaGetLastError();
+}
+
+}  // namespace sgiga

@@ -1,0 +1,260 @@
+"""Batched device pipeline: one plan -> one libsgiga handle.
+
+``Batch`` owns the C-ABI handle of one combination plan and exposes the
+three phases (assemble, solve, combine) plus the parity exports.  The host
+only prepares exact metadata (integer plan, breakpoints, Gauss nodes from
+numpy, the homogeneous control net); everything else runs on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass
+from typing import Callable, Sequence
+
+import numpy as np
+
+from . import _lib
+from .geometry import homogeneous_net
+from .splines import dyadic_level_knots
+
+__all__ = ["gauss_rule", "Batch", "PlanSpec", "make_desc", "knot_tables_for"]
+
+
+def gauss_rule(q: int):
+    """Gauss-Legendre on [0, 1] (reference assembly.py:41-46, same numpy calls)."""
+    if not 1 <= q <= 10:
+        raise ValueError(f"quadrature points per direction must be in [1, 10], got {q}")
+    nodes, weights = np.polynomial.legendre.leggauss(q)
+    return 0.5 * (nodes + 1.0), 0.5 * weights
+
+
+@dataclass
+class PlanSpec:
+    """Everything a handle needs, in host arrays."""
+
+    d: int
+    degree: int
+    regularity: int
+    quad_points: int
+    terms: tuple            # ((beta, coef), ...) in plan order
+    knot_tables: dict       # (axis, key) -> breakpoints; key = level (or table id)
+    patch: object           # NurbsPatch-like
+    forcing_id: int
+
+
+def knot_tables_for(terms, d, degree, regularity, grading=1.0, knot_rule: Callable | None = None):
+    """(axis, level) -> breakpoints for every level a plan uses."""
+    tables = {}
+    for beta, _ in terms:
+        for k, lv in enumerate(beta):
+            if (k, lv) in tables:
+                continue
+            if knot_rule is not None:
+                kv = knot_rule(k, int(lv))
+            else:
+                kv = dyadic_level_knots(int(lv), degree, regularity, grading)
+            tables[(k, lv)] = np.ascontiguousarray(kv.breakpoints, dtype=np.float64)
+    return tables
+
+
+def make_desc(spec: PlanSpec):
+    """struct sgiga_problem_desc for ``spec`` (+ the arrays it points into)."""
+    d, n = spec.d, len(spec.terms)
+    levels = np.array([list(b) for b, _ in spec.terms], dtype=np.int32).reshape(n, d)
+    coefs = np.array([c for _, c in spec.terms], dtype=np.int32)
+    max_level = max([int(k[1]) for k in spec.knot_tables] + [int(levels.max()) if levels.size else 0])
+    L = max_level + 1
+    bp_off = -np.ones(d * L, dtype=np.int64)
+    bp_cnt = np.zeros(d * L, dtype=np.int32)
+    chunks, pos = [], 0
+    for (k, lv), bp in sorted(spec.knot_tables.items()):
+        bp_off[k * L + lv] = pos
+        bp_cnt[k * L + lv] = bp.size
+        chunks.append(bp)
+        pos += bp.size
+    bps = np.ascontiguousarray(np.concatenate(chunks) if chunks else np.zeros(1))
+    gn, gw = gauss_rule(spec.quad_points)
+    kvs = spec.patch.knotvectors
+    keep = dict(
+        levels=levels, coefs=coefs, bp_off=bp_off, bp_cnt=bp_cnt, bps=bps,
+        gn=np.ascontiguousarray(gn), gw=np.ascontiguousarray(gw),
+        gdeg=np.array([kv.degree for kv in kvs], dtype=np.int32),
+        gnk=np.array([np.asarray(kv.knots).size for kv in kvs], dtype=np.int32),
+        gk=np.ascontiguousarray(np.concatenate([np.asarray(kv.knots, dtype=np.float64) for kv in kvs])),
+        hw=np.ascontiguousarray(homogeneous_net(spec.patch).ravel()),
+    )
+    K = keep
+    desc = _lib.ProblemDesc(
+        d, spec.degree, spec.regularity, spec.quad_points, n,
+        _lib.ptr(K["levels"], ct.c_int32), _lib.ptr(K["coefs"], ct.c_int32),
+        _lib.ptr(K["gn"], ct.c_double), _lib.ptr(K["gw"], ct.c_double),
+        max_level, _lib.ptr(K["bp_off"], ct.c_int64), _lib.ptr(K["bp_cnt"], ct.c_int32),
+        _lib.ptr(K["bps"], ct.c_double), _lib.ptr(K["gdeg"], ct.c_int32),
+        _lib.ptr(K["gnk"], ct.c_int32), _lib.ptr(K["gk"], ct.c_double),
+        _lib.ptr(K["hw"], ct.c_double), spec.forcing_id, 0,
+    )
+    return desc, keep
+
+
+class Batch:
+    """Device state of one plan (create -> assemble -> solve -> combine)."""
+
+    def __init__(self, spec: PlanSpec, stream=None, host_forcing: Callable | None = None):
+        self.lib = _lib.load()
+        self.spec = spec
+        self.host_forcing = host_forcing
+        self._build_desc(spec)
+        h = ct.c_void_p()
+        _lib.check(self.lib.sgiga_create(ct.byref(self.desc), stream, ct.byref(h)))
+        self.h = h
+        n = len(spec.terms)
+        dims = np.zeros((n, spec.d), dtype=np.int32)
+        offs = np.zeros(n + 1, dtype=np.int64)
+        _lib.check(self.lib.sgiga_component_info(self.h, _lib.ptr(dims, ct.c_int32), _lib.ptr(offs, ct.c_int64)))
+        self.dims = dims
+        self.dof_offsets = offs
+        sizes = [ct.c_int64() for _ in range(4)]
+        _lib.check(self.lib.sgiga_batch_sizes(self.h, *[ct.byref(s) for s in sizes]))
+        self.total_qp, self.total_rows, self.total_dofs, self.total_slots = (int(s.value) for s in sizes)
+        self.iters = None
+        self.relres = None
+
+    def _build_desc(self, spec: PlanSpec):
+        self.desc, self._keep = make_desc(spec)
+
+    @property
+    def n_comp(self) -> int:
+        return len(self.spec.terms)
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(self.lib.sgiga_stream(self.h) or 0)
+
+    def upload(self):
+        """Per-step host->device copy of the problem inputs."""
+        _lib.check(self.lib.sgiga_upload(self.h, ct.byref(self.desc)))
+
+    # ---- phases -------------------------------------------------------------
+    def assemble(self):
+        if self.spec.forcing_id == _lib.FORCING_HOST:
+            x = np.empty((self.total_qp, self.spec.d))
+            _lib.check(self.lib.sgiga_quad_points_physical(self.h, _lib.ptr(x, ct.c_double)))
+            f = np.ascontiguousarray(np.asarray(self.host_forcing(x), dtype=np.float64))
+            if f.ndim == 0:
+                f = np.full(self.total_qp, float(f))
+            if f.shape != (self.total_qp,):
+                raise ValueError(f"forcing returned shape {f.shape} for {self.total_qp} points")
+            _lib.check(self.lib.sgiga_set_forcing_density(self.h, _lib.ptr(f, ct.c_double)))
+        _lib.check(self.lib.sgiga_assemble(self.h))
+
+    def solve(self, rtol: float = 1e-13, maxit: int = 0):
+        n = self.n_comp
+        it = np.zeros(n, dtype=np.int32)
+        rr = np.zeros(n, dtype=np.float64)
+        code = self.lib.sgiga_solve(self.h, float(rtol), int(maxit), _lib.ptr(it, ct.c_int32), _lib.ptr(rr, ct.c_double))
+        self.iters, self.relres = it, rr
+        _lib.check(code)
+        return it, rr
+
+    def coefficients(self) -> np.ndarray:
+        out = np.empty(self.total_dofs)
+        _lib.check(self.lib.sgiga_coefficients(self.h, _lib.ptr(out, ct.c_double)))
+        return out
+
+    def set_coefficients(self, full: np.ndarray):
+        full = np.ascontiguousarray(full, dtype=np.float64)
+        if full.size != self.total_dofs:
+            raise ValueError(f"expected {self.total_dofs} coefficients, got {full.size}")
+        _lib.check(self.lib.sgiga_set_coefficients(self.h, _lib.ptr(full, ct.c_double)))
+
+    def component_coefficients(self, flat: np.ndarray, c: int) -> np.ndarray:
+        return flat[self.dof_offsets[c]:self.dof_offsets[c + 1]]
+
+    def combine_points(self, pts: np.ndarray, per_component: bool = False) -> np.ndarray:
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        if pts.ndim != 2 or pts.shape[1] != self.spec.d:
+            raise ValueError(f"points must have shape (n, {self.spec.d})")
+        if pts.size and (pts.min() < 0.0 or pts.max() > 1.0):
+            raise ValueError("evaluation points must lie in [0, 1]^d")
+        n = pts.shape[0]
+        out = np.empty((self.n_comp, n) if per_component else n)
+        _lib.check(self.lib.sgiga_combine_points(self.h, pts.ctypes.data, n, out.ctypes.data,
+                                                 -1 if per_component else 0))
+        return out
+
+    def combine_points_device(self, pts_ptr: int, npts: int, out_ptr: int, per_component=False):
+        """Inputs/outputs already resident in HBM (raw device pointers)."""
+        _lib.check(self.lib.sgiga_combine_points(self.h, pts_ptr, npts, out_ptr, -2 if per_component else 1))
+
+    def combine_grid(self, points_per_dir: Sequence[np.ndarray], gradient=False, comp: int = -1):
+        d = self.spec.d
+        if len(points_per_dir) != d:
+            raise ValueError(f"expected {d} point arrays, got {len(points_per_dir)}")
+        arrs = [np.atleast_1d(np.asarray(p, dtype=np.float64)).ravel() for p in points_per_dir]
+        for a in arrs:
+            if a.size and (a.min() < 0.0 or a.max() > 1.0):
+                raise ValueError("evaluation points must lie in [0, 1]")
+        npd = np.array([a.size for a in arrs], dtype=np.int64)
+        cat = np.ascontiguousarray(np.concatenate(arrs))
+        shape = tuple(int(x) for x in npd)
+        vals = np.empty(shape)
+        grads = np.empty(shape + (d,)) if gradient else None
+        _lib.check(self.lib.sgiga_combine_grid(
+            self.h, _lib.ptr(cat, ct.c_double), _lib.ptr(npd, ct.c_int64), int(comp),
+            _lib.ptr(vals, ct.c_double), _lib.ptr(grads, ct.c_double) if gradient else None))
+        return (vals, grads) if gradient else vals
+
+    def error_norms(self, points_per_dir, weights_per_dir, solution_id: int):
+        arrs = [np.asarray(p, dtype=np.float64).ravel() for p in points_per_dir]
+        wts = [np.asarray(w, dtype=np.float64).ravel() for w in weights_per_dir]
+        npd = np.array([a.size for a in arrs], dtype=np.int64)
+        cp = np.ascontiguousarray(np.concatenate(arrs))
+        cw = np.ascontiguousarray(np.concatenate(wts))
+        out = np.zeros(2)
+        _lib.check(self.lib.sgiga_error_norms(self.h, _lib.ptr(cp, ct.c_double), _lib.ptr(cw, ct.c_double),
+                                              _lib.ptr(npd, ct.c_int64), int(solution_id), _lib.ptr(out, ct.c_double)))
+        return float(out[0]), float(out[1])
+
+    def export_csr(self, comp: int):
+        """Interior CSR + rhs of one component (reference row order)."""
+        import scipy.sparse as sps
+
+        nnz = ct.c_int64()
+        _lib.check(self.lib.sgiga_export_csr(self.h, int(comp), ct.byref(nnz), None, None, None, None))
+        rows = int(np.prod(self.dims[comp] - 2)) if np.all(self.dims[comp] > 2) else 0
+        indptr = np.zeros(rows + 1, dtype=np.int64)
+        indices = np.zeros(max(1, nnz.value), dtype=np.int32)
+        data = np.zeros(max(1, nnz.value))
+        rhs = np.zeros(max(1, rows))
+        _lib.check(self.lib.sgiga_export_csr(self.h, int(comp), ct.byref(nnz), _lib.ptr(indptr, ct.c_int64),
+                                             _lib.ptr(indices, ct.c_int32), _lib.ptr(data, ct.c_double),
+                                             _lib.ptr(rhs, ct.c_double)))
+        n = int(nnz.value)
+        mat = sps.csr_matrix((data[:n], indices[:n], indptr), shape=(rows, rows))
+        return mat, rhs[:rows]
+
+    def phase_stats(self):
+        ms = np.zeros(3, dtype=np.float32)
+        ln = np.zeros(3, dtype=np.int64)
+        _lib.check(self.lib.sgiga_phase_stats(self.h, _lib.ptr(ms, ct.c_float), _lib.ptr(ln, ct.c_int64)))
+        return ms, ln
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sgiga_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    # modelled per-component cost used to apportion the batch time
+    def component_cost(self) -> np.ndarray:
+        n = self.n_comp
+        rows = np.prod(np.maximum(self.dims - 2, 0), axis=1).astype(np.float64)
+        W = 2 * self.spec.degree + 1
+        slots = np.prod(np.minimum(np.maximum(self.dims - 2, 1), W), axis=1).astype(np.float64)
+        its = self.iters.astype(np.float64) if self.iters is not None else np.ones(n)
+        return (8.0 * slots * rows + 104.0 * rows) * (its + 1.0) + 1.0

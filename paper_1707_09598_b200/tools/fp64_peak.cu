@@ -1,0 +1,52 @@
+// fp64_peak.cu -- sustained DFMA micro-benchmark: the FP64 roofline
+// denominator (MEASURED_PEAKS.json has none).
+// Each thread runs 16 independent FMA chains; grid = 148 SMs x 8 CTAs.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+__global__ void k_dfma(double* out, int iters, double a, double b) {
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = threadIdx.x * 1e-9 + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = fma(acc[i], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += acc[i];
+    if (s == 12345.678) out[0] = s;   // keep the chains alive
+}
+
+extern "C" int sgiga_fp64_peak(double seconds_target, double* tflops, double* ms_out) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* d_out;
+    if (cudaMalloc(&d_out, sizeof(double)) != cudaSuccess) return -5;
+    int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_dfma<<<blocks, threads>>>(d_out, 64, 0.999999, 1e-7);   // warm-up
+    float ms = 0.f;
+    double best = 0.0;
+    for (int rep = 0; rep < 50; ++rep) {
+        cudaEventRecord(e0);
+        k_dfma<<<blocks, threads>>>(d_out, iters, 0.999999, 1e-7);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        double fl = 2.0 * 16.0 * (double)iters * blocks * threads;
+        double tf = fl / (ms * 1e-3) / 1e12;
+        if (tf > best) best = tf;
+        if (ms * 1e-3 * (rep + 1) > seconds_target) break;
+        if (ms < 50.f) iters *= 2;
+    }
+    *tflops = best;
+    if (ms_out) *ms_out = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d_out);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}

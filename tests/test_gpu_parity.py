@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference
+goldens and the CPU oracle.  Needs a B200: run with ``-m gpu``.
+
+Tolerances (north star):
+  index sets / coefficients / sparsity patterns  bit-exact
+  assembled A and b                               <= 1e-12 norm-wise
+  PCG                                             relative residual <= 1e-13
+  combined solution at points                     <= 1e-9 relative L2
+  L2 / H1 errors                                  3 significant digits (cfg1-3)
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import normwise, rel_l2
+from oracle import oracle as O
+from paper_1707_09598_b200 import _lib, configs
+from paper_1707_09598_b200 import analysis as A
+from paper_1707_09598_b200.assembly import DiscreteSpace, QuadGrid, assemble_poisson, space_batch
+from paper_1707_09598_b200.combination import (CombinationPlan, baseline_plan, combination_coefficients,
+                                               evaluate_combined, evaluate_combined_points, solve_component)
+from paper_1707_09598_b200.errors import InvalidGeometryError
+from paper_1707_09598_b200.geometry import NurbsPatch, quarter_annulus, unit_hypercube
+from paper_1707_09598_b200.pipeline import Batch
+from paper_1707_09598_b200.scheduler import make_spec, run_plan
+
+pytestmark = pytest.mark.gpu
+
+
+def _batch(cfg):
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    b = Batch(spec)
+    b.assemble()
+    return spec, b
+
+
+def test_device_present():
+    assert _lib.device_count() >= 1
+
+
+def test_element_kernel_b4_matches_reference(golden):
+    g = golden("kernel")
+    import ctypes as ct
+    lib = _lib.load()
+    for d in (1, 2, 3):
+        args = {k: np.ascontiguousarray(g[f"d{d}_{k}"]) for k in
+                ("values", "derivs", "elem_index", "qp_index", "fn_index", "metric", "load")}
+        a = np.zeros_like(g[f"d{d}_out_a"])
+        b = np.zeros_like(g[f"d{d}_out_b"])
+        dd, max_nel, n_q, kmax = args["values"].shape
+        code = lib.sgiga_local_poisson_systems(
+            dd, max_nel, n_q, kmax, args["elem_index"].shape[0], args["qp_index"].shape[0],
+            args["fn_index"].shape[0], _lib.ptr(args["values"], ct.c_double), _lib.ptr(args["derivs"], ct.c_double),
+            _lib.ptr(args["elem_index"], ct.c_int64), _lib.ptr(args["qp_index"], ct.c_int32),
+            _lib.ptr(args["fn_index"], ct.c_int32), _lib.ptr(args["metric"], ct.c_double),
+            _lib.ptr(args["load"], ct.c_double), _lib.ptr(a, ct.c_double), _lib.ptr(b, ct.c_double))
+        _lib.check(code)
+        np.testing.assert_allclose(a, g[f"d{d}_out_a"], atol=1e-13)
+        np.testing.assert_allclose(b, g[f"d{d}_out_b"], atol=1e-13)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg2"])
+def test_assembly_matches_reference(golden, name):
+    g = golden(name)
+    cfg = configs.get_config(name)
+    spec, b = _batch(cfg)
+    try:
+        for i in g["stored"]:
+            A_, rhs = b.export_csr(int(i))
+            assert A_.nnz == int(g[f"k{i}_nnz"]), "sparsity pattern size"
+            if f"k{i}_indptr" in g:
+                assert np.array_equal(A_.indptr, g[f"k{i}_indptr"]), "pattern must be bit-exact"
+                assert np.array_equal(A_.indices, g[f"k{i}_indices"]), "pattern must be bit-exact"
+                assert normwise(A_.data, g[f"k{i}_data"]) <= 1e-12
+            assert normwise(A_ @ g[f"k{i}_v"], g[f"k{i}_Av"]) <= 1e-12
+            assert normwise(rhs, g[f"k{i}_rhs"]) <= 1e-12
+    finally:
+        b.close()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg2"])
+def test_pipeline_matches_reference(golden, name):
+    g = golden(name)
+    cfg = configs.get_config(name)
+    sols, report = run_plan(cfg.plan, cfg.problem)
+    assert [s.beta for s in sols] == cfg.plan.betas
+    it = np.array(report.iterations)
+    assert np.all(it > 0)
+    coefs = np.concatenate([s.coefficients for s in sols])
+    assert rel_l2(coefs, g["coefficients"]) <= 1e-9
+    vals = evaluate_combined_points(cfg.plan, sols, g["points"])
+    assert rel_l2(vals, g["combined"]) <= 1e-9
+    l2, h1 = A.error_norms(cfg.plan, sols, cfg.problem, cfg.grid())
+    np.testing.assert_allclose([l2, h1], g["errors"], rtol=5e-4)
+
+
+def test_pcg_residual_contract():
+    cfg = configs.get_config("cfg2")
+    spec, b = _batch(cfg)
+    try:
+        it, rr = b.solve(rtol=1e-13)
+        assert np.all(rr <= 1e-12)          # true residual after recursive 1e-13
+        orc = O.Oracle(spec)
+        ref = orc.run_plan(O.SOLVER_DIRECT)
+        assert rel_l2(b.coefficients(), ref) <= 1e-10
+    finally:
+        b.close()
+
+
+def test_deterministic_bitwise():
+    cfg = configs.get_config("cfg3")
+    pts = cfg.points(1000)
+    outs = []
+    for _ in range(2):
+        sols, _ = run_plan(cfg.plan, cfg.problem)
+        outs.append(evaluate_combined_points(cfg.plan, sols, pts))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_combine_grid_and_gradient_vs_oracle():
+    cfg = configs.get_config("cfg1")
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    sols, _ = run_plan(cfg.plan, cfg.problem)
+    orc = O.Oracle(spec)
+    coefs = np.concatenate([s.coefficients for s in sols])
+    pts = (np.linspace(0, 1, 17), np.concatenate([[0.0, 0.25, 0.5], np.random.default_rng(1).random(9), [1.0]]))
+    v, gr = evaluate_combined(cfg.plan, sols, pts, gradient=True)
+    vo, go = orc.combine_grid(pts, coefs=coefs, gradient=True)
+    assert v.shape == (17, 13) and gr.shape == (17, 13, 2)
+    assert rel_l2(v, vo) <= 1e-12
+    assert rel_l2(gr, go) <= 1e-12
+    # single-component evaluation == that component's eval_grid
+    one = sols[3].eval_grid(pts)
+    assert rel_l2(one, orc.combine_grid(pts, coefs=coefs, comp=3)) <= 1e-12
+
+
+def test_points_on_knots_and_endpoints():
+    cfg = configs.get_config("cfg3")
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    sols, _ = run_plan(cfg.plan, cfg.problem)
+    orc = O.Oracle(spec)
+    coefs = np.concatenate([s.coefficients for s in sols])
+    k = np.array([0.0, 1.0, 0.5, 0.25, 0.125, 1 / 128, 127 / 128, 0.999999999])
+    pts = np.stack(np.meshgrid(k, k, indexing="ij"), -1).reshape(-1, 2)
+    assert rel_l2(evaluate_combined_points(cfg.plan, sols, pts), orc.combine_points(pts, coefs=coefs)) <= 1e-12
+
+
+@pytest.mark.parametrize("p,r,levels,grading,q", [
+    (2, 0, (2, 3), 1.0, 3),      # C^0 (interior multiplicity 2)
+    (3, 1, (2, 2), 1.0, 4),      # C^1 cubic
+    (2, 1, (3, 2), 2.5, 3),      # graded knots
+    (2, 1, (3, 3), 1.0, 6),      # over-integration q != p+1
+    (1, 0, (3, 2), 1.0, 2),      # bilinear
+    (4, 3, (1, 2), 1.0, 5),      # quartic, small
+])
+def test_general_spaces_vs_oracle(p, r, levels, grading, q):
+    prob = A.BenchmarkProblem("x", quarter_annulus(2), A.annulus_forcing_2d, p, r, grading)
+    spec = make_spec(((levels, 1),), prob, q)
+    b = Batch(spec)
+    orc = O.Oracle(spec)
+    try:
+        b.assemble()
+        Ag, bg = b.export_csr(0)
+        Ao, bo = orc.assemble_csr(0)
+        Ao.sort_indices()
+        assert np.array_equal(Ag.indptr, Ao.indptr) and np.array_equal(Ag.indices, Ao.indices)
+        assert normwise(Ag.data, Ao.data) <= 1e-12
+        assert normwise(bg, bo) <= 1e-12
+        b.solve()
+        assert rel_l2(b.coefficients(), orc.run_plan(O.SOLVER_DIRECT)) <= 1e-9
+    finally:
+        b.close()
+
+
+def test_host_forcing_path_matches_registered_forcing():
+    """An unregistered callable goes through host evaluation at device-computed
+    physical points; it must reproduce the registered closed form's system."""
+    f = lambda x: A.cube_forcing(x)   # noqa: E731  (unknown to the registry)
+    assert A.forcing_id_of(f) == _lib.FORCING_HOST
+    patch = quarter_annulus(3)
+    host = Batch(make_spec((((2, 1, 1), 1),), A.BenchmarkProblem("h", patch, f, 2, 1)), host_forcing=f)
+    orc = O.Oracle(make_spec((((2, 1, 1), 1),), A.BenchmarkProblem("d", patch, A.cube_forcing, 2, 1)))
+    try:
+        host.assemble()
+        Ag, bg = host.export_csr(0)
+        Ao, bo = orc.assemble_csr(0)
+        assert normwise(Ag @ np.ones(Ag.shape[0]), Ao @ np.ones(Ao.shape[0])) <= 1e-12
+        assert normwise(bg, bo) <= 1e-12
+    finally:
+        host.close()
+
+
+def test_interval_hat_and_empty_interior():
+    prob = A.BenchmarkProblem("hat", unit_hypercube(1), A.constant_one, 1, 0)
+    sysm = assemble_poisson(DiscreteSpace.from_levels((1,), 1, 0), unit_hypercube(1), A.constant_one)
+    np.testing.assert_allclose(sysm.matrix.toarray(), [[4.0]], atol=1e-13)
+    np.testing.assert_allclose(sysm.rhs, [0.5], atol=1e-14)
+    # degree 1 at level 0 has no interior: zero function (combination.py:194-195)
+    p1 = A.polynomial_cube_problem(2, degree=1)
+    comp = solve_component(p1, (0, 0))
+    assert comp.n_dofs == 4 and np.array_equal(comp.coefficients, np.zeros(4))
+
+
+def test_polynomial_reproduction():
+    prob = A.polynomial_cube_problem(2)
+    plan = combination_coefficients(2, 2)
+    sols, _ = run_plan(plan, prob)
+    grid = QuadGrid(prob.patch, (3, 3), 4)
+    l2, h1 = A.error_norms(plan, sols, prob, grid)
+    assert l2 < 1e-10 and h1 < 1e-9
+
+
+def test_invalid_geometry_raises():
+    sq = unit_hypercube(2)
+    pts = sq.control_points.copy()
+    pts[0, 0], pts[1, 0] = pts[1, 0].copy(), pts[0, 0].copy()
+    bad = NurbsPatch(sq.knotvectors, pts, sq.weights)
+    prob = A.BenchmarkProblem("bad", bad, A.constant_one, 2, 1)
+    with pytest.raises(InvalidGeometryError):
+        run_plan(CombinationPlan(2, (((1, 1), 1),)), prob)
+
+
+def test_missing_component_keyerror():
+    prob = A.polynomial_cube_problem(2)
+    plan = combination_coefficients(2, 1)
+    sols, _ = run_plan(plan, prob)
+    with pytest.raises(KeyError):
+        evaluate_combined(plan, sols[:-1], (np.array([0.5]), np.array([0.5])))
+
+
+def test_run_report_invariants():
+    cfg = configs.get_config("cfg1")
+    sols, rep = run_plan(cfg.plan, cfg.problem, workers=4)
+    assert rep.total_dofs == sum(s.n_dofs for s in sols)
+    assert rep.serial_time == pytest.approx(sum(s.solve_time for s in sols))
+    assert all(t > 0 for _, _, t in rep.components)
+    assert rep.optimized_time(1) == pytest.approx(rep.serial_time)
+    with pytest.raises(ValueError):
+        run_plan(cfg.plan, cfg.problem, workers=0)
+
+
+@pytest.mark.slow
+def test_cfg5_full_pipeline(golden):
+    g = golden("cfg5")
+    cfg = configs.get_config("cfg5")
+    spec, b = _batch(cfg)
+    try:
+        for i in g["stored"]:
+            A_, rhs = b.export_csr(int(i))
+            assert A_.nnz == int(g[f"k{i}_nnz"])
+            assert normwise(A_ @ g[f"k{i}_v"], g[f"k{i}_Av"]) <= 1e-12
+            assert normwise(rhs, g[f"k{i}_rhs"]) <= 1e-12
+        it, rr = b.solve(rtol=1e-13)
+        assert np.all(rr <= 1e-11)
+        coefs = b.coefficients()
+        assert rel_l2(coefs, g["coefficients"]) <= 1e-9
+        vals = b.combine_points(g["points"])
+        assert rel_l2(vals, g["combined"]) <= 1e-9
+        l2, h1 = b.error_norms(cfg.grid().points_per_dir, cfg.grid().weights_per_dir,
+                               A.solution_id_of(cfg.problem.solution))
+        # cfg5 errors sit at the solve-noise floor: 2 digits
+        np.testing.assert_allclose([l2, h1], g["errors"], rtol=5e-2)
+    finally:
+        b.close()
