@@ -19,7 +19,6 @@ static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 size_t assembly_smem_bytes(const Handle* h);
-size_t small_smem_bytes(const Handle* h);
 
 // cumulative tables stored behind d_gauss: [2q] gauss, then
 // tab_qp_cum [ntab+1], comp_qp_cum [ncomp+1], comp_dof_cum [ncomp+1]
@@ -40,8 +39,8 @@ static void free_all(Handle* h) {
                     h->d_large, h->d_bp, h->d_knots, h->d_gauss, h->d_tabvals, h->d_qx,
                     h->d_qw, h->d_geob, h->d_geofirst, h->d_geo_knots, h->d_geo_hw, h->d_G,
                     h->d_hostf, h->d_xphys, h->d_stencil, h->d_rhs, h->d_dinv, h->d_x,
-                    h->d_r, h->d_z, h->d_p, h->d_q, h->d_coef, h->d_cg, h->d_part, h->d_err,
-                    h->d_active_count, h->d_relres};
+                    h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
+                    h->d_active_count, h->d_relres, h->d_slotoff};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->h_pinned_flag) cudaFreeHost(h->h_pinned_flag);
@@ -121,6 +120,9 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
             T.axis = k; T.level = lv; T.nel = nbp - 1;
             T.nk = 2 * (p + 1) + (T.nel - 1) * h->mu;
             T.n = T.nk - p - 1;
+            T.uniform = (T.nel & (T.nel - 1)) == 0;
+            for (int i = 0; i < nbp && T.uniform; ++i)
+                if (bp[i] != (double)i / (double)T.nel) T.uniform = 0;
             T.bp_off = (int64_t)h->bp_host.size();
             h->bp_host.insert(h->bp_host.end(), bp, bp + nbp);
             T.knot_off = knots_tot;
@@ -139,7 +141,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
 
     // components
     h->comps.assign(D->n_comp, CompInfo{});
-    h->pencils.clear(); h->chunks.clear(); h->small_comps.clear(); h->large_comps.clear();
+    h->pencils.clear(); h->chunks.clear(); h->small_comps.clear(); h->large_comps.clear(); h->slotoff.clear();
     int64_t vec = 0, mat = 0, qpo = 0, dof = 0, rows_tot = 0, nqp_tot = 0;
     const int W = 2 * p + 1, nG = d * (d + 1) / 2 + 1;
     h->max_slots_comp = 0;
@@ -179,6 +181,16 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
         }
         C.halo = 0;
         for (int k = 0; k < d; ++k) if (!C.absm[k]) C.halo += (int64_t)p * C.rs[k];
+        // slot offsets in the stencil's linear slot order
+        C.so_off = (int64_t)h->slotoff.size();
+        for (int64_t t = 0; t < C.nslots; ++t) {
+            int64_t off = 0;
+            for (int k = 0; k < d; ++k) {
+                int sk = (int)((t / C.ss[k]) % C.S[k]);
+                off += (int64_t)(C.absm[k] ? sk : sk - p) * C.rs[k];
+            }
+            h->slotoff.push_back((int)off);
+        }
         C.vec_off = vec + C.halo;
         vec += C.rows + 2 * C.halo;
         C.mat_off = mat;
@@ -201,10 +213,20 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
             ch.nrow = (int)std::min<int64_t>(256, C.rows - (int64_t)i * 256);
             h->chunks.push_back(ch);
         }
-        // assembly pencils: tile rows along ax[d-2], ax[d-3]; segments along s
+    }
+    // assembly pencils: tile rows along ax[d-2], ax[d-3]; segments along the
+    // stream axis.  Short segments when the batch has few pencils (latency),
+    // long ones otherwise (the p-element halo of a segment is recomputed).
+    int64_t cross = 0;
+    for (const CompInfo& C : h->comps)
+        if (C.rows) cross += (d >= 2 ? C.m[C.ax[d - 2]] : 1) * (int64_t)(d >= 3 ? C.m[C.ax[d - 3]] : 1);
+    const int SEG = cross >= 8 * 148 ? 128 : (cross >= 2 * 148 ? 32 : 16);
+    for (int c = 0; c < D->n_comp; ++c) {
+        const CompInfo& C = h->comps[c];
+        if (!C.rows) continue;
+        int s = C.ax[d - 1];
         int na = d >= 2 ? C.m[C.ax[d - 2]] : 1, nb = d >= 3 ? C.m[C.ax[d - 3]] : 1;
         int ms = C.m[s];
-        const int SEG = 128;
         int nseg = (ms + SEG - 1) / SEG;
         for (int ib = 0; ib < nb; ++ib)
             for (int ia = 0; ia < na; ++ia)
@@ -238,6 +260,8 @@ static int upload_all(Handle* h) {
         SG_CUDA(cudaMemcpyAsync(h->d_chunks, h->chunks.data(), sizeof(Chunk) * h->chunks.size(), cudaMemcpyHostToDevice, s));
     if (!h->small_comps.empty())
         SG_CUDA(cudaMemcpyAsync(h->d_small, h->small_comps.data(), sizeof(int) * h->small_comps.size(), cudaMemcpyHostToDevice, s));
+    if (!h->slotoff.empty())
+        SG_CUDA(cudaMemcpyAsync(h->d_slotoff, h->slotoff.data(), sizeof(int) * h->slotoff.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_bp, h->bp_host.data(), sizeof(double) * h->bp_host.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_geo_knots, h->geo_knots.data(), sizeof(double) * h->geo_knots.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_geo_hw, h->geo_hw.data(), sizeof(double) * h->geo_hw.size(), cudaMemcpyHostToDevice, s));
@@ -353,12 +377,14 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_z, h->total_vec);
     A_(d_p, h->total_vec);
     A_(d_q, h->total_vec);
+    A_(d_q2, h->total_vec);
     A_(d_coef, h->total_dofs);
     A_(d_cg, h->ncomp);
     A_(d_part, 3 * h->chunks.size());
     A_(d_err, 1);
     A_(d_active_count, 1);
     A_(d_relres, h->ncomp);
+    A_(d_slotoff, h->slotoff.size());
 #undef A_
     if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned_flag), sizeof(int) * 4);
     for (auto& ev : h->ev)
@@ -373,7 +399,7 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     }
     // zero everything that is gathered through halos or reduced
     cudaStream_t s = h->stream;
-    double* vecs[] = {h->d_rhs, h->d_dinv, h->d_x, h->d_r, h->d_z, h->d_p, h->d_q};
+    double* vecs[] = {h->d_rhs, h->d_dinv, h->d_x, h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2};
     for (double* v : vecs) cudaMemsetAsync(v, 0, sizeof(double) * std::max<int64_t>(1, h->total_vec), s);
     cudaMemsetAsync(h->d_cg, 0, sizeof(CgState) * h->ncomp, s);
     cudaMemsetAsync(h->d_err, 0, sizeof(int), s);
@@ -402,6 +428,7 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
     h->gauss_n.swap(tmp.gauss_n); h->gauss_w.swap(tmp.gauss_w);
     h->geo = tmp.geo; h->geo_knots.swap(tmp.geo_knots); h->geo_hw.swap(tmp.geo_hw);
     h->bp_host.swap(tmp.bp_host); h->comps.swap(tmp.comps); h->tabs.swap(tmp.tabs);
+    h->slotoff.swap(tmp.slotoff);
     h->forcing_id = tmp.forcing_id;
     return upload_all(h);
 }
@@ -465,6 +492,7 @@ int sgiga_assemble(sgiga_handle* hh) {
     }
     h->launches[0] = 0;
     SG_CUDA(cudaEventRecord(h->ev[0], h->stream));
+    h->tables_ready = false;   // kernel 1 is part of every assembly pass
     int st = ensure_tables(h);
     if (st) return st;
     h->kstart(1);

@@ -39,6 +39,8 @@ struct Handle {
     std::vector<Pencil> pencils;
     std::vector<Chunk> chunks;
     std::vector<int> small_comps, large_comps;
+    std::vector<int> slotoff;          // per-component slot column offsets
+    int* d_slotoff = nullptr;
     int64_t total_qp = 0, total_rows = 0, total_vec = 0, total_slots = 0, total_dofs = 0;
     int64_t total_knots = 0, total_tabvals = 0, total_tabqp = 0;
     int max_slots_comp = 0;
@@ -72,6 +74,7 @@ struct Handle {
     double* d_z = nullptr;
     double* d_p = nullptr;
     double* d_q = nullptr;
+    double* d_q2 = nullptr;      // second direction buffer (PCG parity)
     double* d_coef = nullptr;    // full coefficients, reference C order
     CgState* d_cg = nullptr;
     double* d_part = nullptr;    // per-chunk partial sums [3*nchunks]

@@ -7,24 +7,43 @@
 // per-point idiom of tests/test_acceptance.py:224-230, and
 // analysis.error_norms / _push_gradient (analysis.py:235-270).
 //
-// One thread per point.  Components are visited in plan (lexicographic)
-// order; the 1-D Cox-de Boor values of an axis are recomputed only when the
-// level changes between consecutive components (lexicographic order keeps
-// the leading axes constant for long runs).  The tensor contraction is
-// sum-factorised (P^D + ... + P FMAs per component).
+// One thread per point, templated on (D, p) so the Cox-de Boor tables and
+// the coefficient window stay in registers.  Components are visited in plan
+// (lexicographic) order -- the accumulation order the reference guarantees
+// -- and an axis' 1-D basis is recomputed only when its level changes
+// between consecutive components.  The span of a uniform dyadic knot vector
+// is closed-form (floor(xi*2^l), exact), graded ones use a binary search
+// with the reference's side rule (splines.py:149-169, 255-257).
 #include "forcing.cuh"
 #include "handle.cuh"
 
 namespace sgiga {
 
-template <int D, bool GRAD>
+template <int P, bool GRAD>
+__device__ __forceinline__ int axis_basis(const TabInfo& T, const double* __restrict__ knots,
+                                          int mu, double xi, double* bv, double* bd) {
+    constexpr int p = P - 1;
+    const double* k = knots + T.knot_off;
+    int span;
+    if (T.uniform) {
+        int e = (int)(xi * (double)T.nel);   // exact: nel is a power of two
+        if (e > T.nel - 1) e = T.nel - 1;
+        span = p + e * mu;
+    } else {
+        span = find_span(k, T.nk, p, xi, xi == 1.0);
+    }
+    ders_basis_funs_t<p>(span, xi, k, bv, GRAD ? bd : nullptr);
+    return span - p;
+}
+
+template <int D, int P, bool GRAD>
 __device__ __forceinline__ void eval_component(const CompInfo& C, const double* __restrict__ coef,
-                                               const int* first, const double (*Bv)[PMAX],
-                                               const double (*Bd)[PMAX], int P, double& v,
-                                               double* g) {
+                                               const int* first, const double (*Bv)[P],
+                                               const double (*Bd)[P], double& v, double* g) {
     const double* cf = coef + C.dof_off;
-    if (D == 1) {
+    if constexpr (D == 1) {
         double sv = 0.0, sd = 0.0;
+#pragma unroll
         for (int a = 0; a < P; ++a) {
             double c = cf[first[0] + a];
             sv += Bv[0][a] * c;
@@ -32,14 +51,16 @@ __device__ __forceinline__ void eval_component(const CompInfo& C, const double* 
         }
         v = sv;
         if (GRAD) g[0] = sd;
-    } else if (D == 2) {
+    } else if constexpr (D == 2) {
         const int n1 = C.n[1];
         double v0 = 0.0, g0 = 0.0, g1 = 0.0;
+#pragma unroll
         for (int a = 0; a < P; ++a) {
             const double* row = cf + (int64_t)(first[0] + a) * n1 + first[1];
             double tv = 0.0, td = 0.0;
+#pragma unroll
             for (int b = 0; b < P; ++b) {
-                double c = row[b];
+                double c = __ldg(row + b);
                 tv += Bv[1][b] * c;
                 if (GRAD) td += Bd[1][b] * c;
             }
@@ -51,14 +72,16 @@ __device__ __forceinline__ void eval_component(const CompInfo& C, const double* 
     } else {
         const int n1 = C.n[1], n2 = C.n[2];
         double v0 = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
+#pragma unroll
         for (int a = 0; a < P; ++a) {
             double uv = 0.0, u1 = 0.0, u2 = 0.0;
+#pragma unroll
             for (int b = 0; b < P; ++b) {
                 const double* row = cf + ((int64_t)(first[0] + a) * n1 + (first[1] + b)) * n2 + first[2];
                 double tv = 0.0, td = 0.0;
-#pragma unroll 5
+#pragma unroll
                 for (int l = 0; l < P; ++l) {
-                    double c = row[l];
+                    double c = __ldg(row + l);
                     tv += Bv[2][l] * c;
                     if (GRAD) td += Bd[2][l] * c;
                 }
@@ -73,30 +96,16 @@ __device__ __forceinline__ void eval_component(const CompInfo& C, const double* 
     }
 }
 
-template <int D, bool GRAD>
-__device__ __forceinline__ void axis_basis(const TabInfo& T, const double* __restrict__ knots,
-                                           int p, double xi, int& first, double* bv, double* bd) {
-    const double* k = knots + T.knot_off;
-    int span = find_span(k, T.nk, p, xi, xi == 1.0);   // splines.py:255-257
-    double tab[2 * (PMAX + 2)];
-    ders_basis_funs(span, xi, p, GRAD ? 1 : 0, k, tab);
-    first = span - p;
-    for (int j = 0; j <= p; ++j) {
-        bv[j] = tab[j];
-        if (GRAD) bd[j] = tab[p + 1 + j];
-    }
-}
-
-// sum over components (plan order) at one parametric point
-template <int D, bool GRAD>
+// sum over components [c_lo, c_hi) in plan order at one parametric point
+template <int D, int P, bool GRAD>
 __device__ __forceinline__ void combine_at(const CompInfo* __restrict__ comps, int c_lo, int c_hi,
                                            bool weighted, const TabInfo* __restrict__ tabs,
-                                           const double* __restrict__ knots,
-                                           const double* __restrict__ coef, int p,
-                                           const double* xi, double& acc, double* gacc,
-                                           double* per_comp, int64_t per_stride) {
+                                           const double* __restrict__ knots, int mu,
+                                           const double* __restrict__ coef, const double* xi,
+                                           double& acc, double* gacc, double* per_comp,
+                                           int64_t per_stride) {
     int cur[D], first[D];
-    double Bv[D][PMAX], Bd[D][PMAX];
+    double Bv[D][P], Bd[D][P];
 #pragma unroll
     for (int k = 0; k < D; ++k) cur[k] = -1;
     bool started = false;
@@ -106,16 +115,18 @@ __device__ __forceinline__ void combine_at(const CompInfo* __restrict__ comps, i
     for (int c = c_lo; c < c_hi; ++c) {
         const CompInfo& C = comps[c];
 #pragma unroll
-        for (int k = 0; k < D; ++k)
-            if (C.tab[k] != cur[k]) {
-                cur[k] = C.tab[k];
-                axis_basis<D, GRAD>(tabs[cur[k]], knots, p, xi[k], first[k], Bv[k], Bd[k]);
+        for (int k = 0; k < D; ++k) {
+            int t = C.tab[k];
+            if (t != cur[k]) {
+                cur[k] = t;
+                first[k] = axis_basis<P, GRAD>(tabs[t], knots, mu, xi[k], Bv[k], Bd[k]);
             }
+        }
         double v, g[D];
-        eval_component<D, GRAD>(C, coef, first, Bv, Bd, p + 1, v, g);
+        eval_component<D, P, GRAD>(C, coef, first, Bv, Bd, v, g);
         if (per_comp) { per_comp[(int64_t)c * per_stride] = v; continue; }
         double cf = weighted ? (double)C.coef : 1.0;
-        // plan-order accumulation: vals = c*v, then vals += c*v (combination.py:227-233)
+        // vals = c*v, then vals += c*v in plan order (combination.py:227-233)
         if (!started) {
             acc = cf * v;
 #pragma unroll
@@ -129,29 +140,29 @@ __device__ __forceinline__ void combine_at(const CompInfo* __restrict__ comps, i
     }
 }
 
-template <int D>
-__global__ void k_combine_points(const CompInfo* __restrict__ comps, int ncomp,
-                                 const TabInfo* __restrict__ tabs, const double* __restrict__ knots,
-                                 const double* __restrict__ coef, int p,
-                                 const double* __restrict__ pts, int64_t npts,
-                                 double* __restrict__ out, int per_component) {
+template <int D, int P>
+__global__ void __launch_bounds__(128)
+k_combine_points(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
+                 const double* __restrict__ knots, int mu, const double* __restrict__ coef,
+                 const double* __restrict__ pts, int64_t npts, double* __restrict__ out,
+                 int per_component) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= npts) return;
     double xi[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) xi[k] = pts[t * D + k];
     double acc, g[D];
-    combine_at<D, false>(comps, 0, ncomp, true, tabs, knots, coef, p, xi, acc, g,
-                         per_component ? out + t : nullptr, npts);
+    combine_at<D, P, false>(comps, 0, ncomp, true, tabs, knots, mu, coef, xi, acc, g,
+                            per_component ? out + t : nullptr, npts);
     if (!per_component) out[t] = acc;
 }
 
-template <int D>
-__global__ void k_combine_grid(const CompInfo* __restrict__ comps, int ncomp,
-                               const TabInfo* __restrict__ tabs, const double* __restrict__ knots,
-                               const double* __restrict__ coef, int p,
-                               const double* __restrict__ pts, int64_t n0, int64_t n1, int64_t n2,
-                               int comp, double* __restrict__ vals, double* __restrict__ grads) {
+template <int D, int P>
+__global__ void __launch_bounds__(128)
+k_combine_grid(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
+               const double* __restrict__ knots, int mu, const double* __restrict__ coef,
+               const double* __restrict__ pts, int64_t n0, int64_t n1, int64_t n2, int comp,
+               double* __restrict__ vals, double* __restrict__ grads) {
     int64_t N = n0 * (D > 1 ? n1 : 1) * (D > 2 ? n2 : 1);
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= N) return;
@@ -163,11 +174,11 @@ __global__ void k_combine_grid(const CompInfo* __restrict__ comps, int ncomp,
     double acc, g[D];
     int lo = comp >= 0 ? comp : 0, hi = comp >= 0 ? comp + 1 : ncomp;
     if (grads) {
-        combine_at<D, true>(comps, lo, hi, comp < 0, tabs, knots, coef, p, xi, acc, g, nullptr, 0);
+        combine_at<D, P, true>(comps, lo, hi, comp < 0, tabs, knots, mu, coef, xi, acc, g, nullptr, 0);
 #pragma unroll
         for (int k = 0; k < D; ++k) grads[t * D + k] = g[k];
     } else {
-        combine_at<D, false>(comps, lo, hi, comp < 0, tabs, knots, coef, p, xi, acc, g, nullptr, 0);
+        combine_at<D, P, false>(comps, lo, hi, comp < 0, tabs, knots, mu, coef, xi, acc, g, nullptr, 0);
     }
     vals[t] = acc;
 }
@@ -256,10 +267,10 @@ __device__ __forceinline__ double geo_point(const GeoInfo& G, const double* __re
 
 constexpr int ERR_THREADS = 256;
 
-template <int D>
+template <int D, int P>
 __global__ void __launch_bounds__(ERR_THREADS)
 k_error_norms(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
-              const double* __restrict__ knots, const double* __restrict__ coef, int p,
+              const double* __restrict__ knots, int mu, const double* __restrict__ coef,
               const GeoInfo* __restrict__ geo, const double* __restrict__ gknots,
               const double* __restrict__ hw, const double* __restrict__ pts,
               const double* __restrict__ wts, int64_t n0, int64_t n1, int64_t n2, int sol_id,
@@ -271,8 +282,7 @@ k_error_norms(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __re
     if (t < N) {
         int64_t npd[3] = {n0, n1, n2}, off[3] = {0, n0, n0 + n1};
         double xi[D], w = 1.0;
-        int64_t rem = t;
-        int64_t jj[D];
+        int64_t rem = t, jj[D];
 #pragma unroll
         for (int k = D - 1; k >= 0; --k) { jj[k] = rem % npd[k]; xi[k] = pts[off[k] + jj[k]]; rem /= npd[k]; }
 #pragma unroll
@@ -282,7 +292,7 @@ k_error_norms(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __re
         double det = geo_point<D>(G, gknots, hw, xi, x, Ji);
         if (!(det > 0.0)) atomicOr(err, ERRF_GEOMETRY);
         double acc, g[D];
-        combine_at<D, true>(comps, 0, ncomp, true, tabs, knots, coef, p, xi, acc, g, nullptr, 0);
+        combine_at<D, P, true>(comps, 0, ncomp, true, tabs, knots, mu, coef, xi, acc, g, nullptr, 0);
         double ue, ge[D];
         solution_value<D>(sol_id, x, ue, ge);
         double dv = acc - ue, dg2 = 0.0;
@@ -339,17 +349,27 @@ __global__ void k_sum_partials(const double* __restrict__ partials, int64_t nblo
     }
 }
 
+// (d, p) dispatch: D in 1..3, P = p + 1 in 2..5
+#define SGIGA_DISPATCH_DP(d, P, MACRO)                                   \
+    switch ((d) * 10 + (P)) {                                            \
+    case 12: MACRO(1, 2); break; case 13: MACRO(1, 3); break;            \
+    case 14: MACRO(1, 4); break; case 15: MACRO(1, 5); break;            \
+    case 22: MACRO(2, 2); break; case 23: MACRO(2, 3); break;            \
+    case 24: MACRO(2, 4); break; case 25: MACRO(2, 5); break;            \
+    case 32: MACRO(3, 2); break; case 33: MACRO(3, 3); break;            \
+    case 34: MACRO(3, 4); break; case 35: MACRO(3, 5); break;            \
+    default: return cudaErrorInvalidValue;                               \
+    }
+
 cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, double* d_out,
                                   int per_component) {
     if (npts == 0) return cudaSuccess;
     unsigned blocks = (unsigned)((npts + 127) / 128);
-#define LAUNCH_CP(DD)                                                                       \
-    k_combine_points<DD><<<blocks, 128, 0, h->stream>>>(h->d_comps, h->ncomp, h->d_tabs,     \
-                                                         h->d_knots, h->d_coef, h->p, d_pts, \
-                                                         npts, d_out, per_component)
-    if (h->d == 1) LAUNCH_CP(1);
-    else if (h->d == 2) LAUNCH_CP(2);
-    else LAUNCH_CP(3);
+#define LAUNCH_CP(DD, PP)                                                                     \
+    k_combine_points<DD, PP><<<blocks, 128, 0, h->stream>>>(h->d_comps, h->ncomp, h->d_tabs,   \
+                                                            h->d_knots, h->mu, h->d_coef,     \
+                                                            d_pts, npts, d_out, per_component)
+    SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CP)
 #undef LAUNCH_CP
     h->launches[2]++;
     return cudaGetLastError();
@@ -362,13 +382,11 @@ cudaError_t launch_combine_grid(Handle* h, const double* d_pts, const int64_t* n
     if (N == 0) return cudaSuccess;
     unsigned blocks = (unsigned)((N + 127) / 128);
     int64_t n1 = h->d > 1 ? npd[1] : 1, n2 = h->d > 2 ? npd[2] : 1;
-#define LAUNCH_CG(DD)                                                                          \
-    k_combine_grid<DD><<<blocks, 128, 0, h->stream>>>(h->d_comps, h->ncomp, h->d_tabs,          \
-                                                       h->d_knots, h->d_coef, h->p, d_pts,      \
-                                                       npd[0], n1, n2, comp, d_vals, d_grads)
-    if (h->d == 1) LAUNCH_CG(1);
-    else if (h->d == 2) LAUNCH_CG(2);
-    else LAUNCH_CG(3);
+#define LAUNCH_CG(DD, PP)                                                                      \
+    k_combine_grid<DD, PP><<<blocks, 128, 0, h->stream>>>(h->d_comps, h->ncomp, h->d_tabs,      \
+                                                          h->d_knots, h->mu, h->d_coef, d_pts,  \
+                                                          npd[0], n1, n2, comp, d_vals, d_grads)
+    SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CG)
 #undef LAUNCH_CG
     h->launches[2]++;
     return cudaGetLastError();
@@ -382,14 +400,12 @@ cudaError_t launch_error_norms(Handle* h, const double* d_pts, const double* d_w
     int64_t nb = (N + ERR_THREADS - 1) / ERR_THREADS;
     *nblocks = nb;
     int64_t n1 = h->d > 1 ? npd[1] : 1, n2 = h->d > 2 ? npd[2] : 1;
-#define LAUNCH_EN(DD)                                                                          \
-    k_error_norms<DD><<<(unsigned)nb, ERR_THREADS, 0, h->stream>>>(                            \
-        h->d_comps, h->ncomp, h->d_tabs, h->d_knots, h->d_coef, h->p, h->d_geo,                \
+#define LAUNCH_EN(DD, PP)                                                                      \
+    k_error_norms<DD, PP><<<(unsigned)nb, ERR_THREADS, 0, h->stream>>>(                        \
+        h->d_comps, h->ncomp, h->d_tabs, h->d_knots, h->mu, h->d_coef, h->d_geo,               \
         h->d_geo_knots, h->d_geo_hw, d_pts, d_wts, npd[0], n1, n2, solution_id, d_partials,    \
         h->d_err)
-    if (h->d == 1) LAUNCH_EN(1);
-    else if (h->d == 2) LAUNCH_EN(2);
-    else LAUNCH_EN(3);
+    SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_EN)
 #undef LAUNCH_EN
     k_sum_partials<<<1, 1024, 0, h->stream>>>(d_partials, nb, d_partials + 2 * nb);
     h->launches[2] += 2;

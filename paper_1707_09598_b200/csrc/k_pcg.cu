@@ -7,77 +7,62 @@
 // ||Ax-b|| <= 1e-10 ||b|| (linsolve.py:49-53), zero-rhs shortcut (43-45),
 // expand with zero boundary (assembly.py:202-206).
 //
+// Stencil SpMV: column of (row, slot) = rowbase(row) + off[slot], with
+// rowbase = row - sum_{absolute axes} r_k rs_k and off[] a per-component
+// table (handle.cu), so the inner loop is two loads and one FMA.
+//
 // Two regimes:
-//  * small components (rows <= SMALL_ROWS): one CTA per component runs the
-//    whole CG loop with all vectors in shared memory (no grid syncs);
-//  * large components: row chunks of 256, three fused kernels per
-//    iteration, per-component scalars reduced by the last chunk to finish
-//    (fixed chunk order -> deterministic), iterations replayed as CUDA
-//    graphs with the convergence test on the device.
+//  * small components (rows <= 2048): one CTA per component runs the whole
+//    CG loop; vectors (and the matrix, when it fits) live in shared memory;
+//    3 barriers per iteration, double-buffered deterministic reductions.
+//  * large components: 256-row chunks, two fused kernels per iteration
+//    (SpMV with the direction update folded in, then the x/r/z update),
+//    per-component scalars reduced by the last chunk to finish in fixed
+//    chunk order (deterministic), iterations replayed as a CUDA graph with
+//    the convergence test on the device.
 #include "handle.cuh"
 
 namespace sgiga {
 
-constexpr int SMALL_ROWS = 2048;
 constexpr int SMALL_THREADS = 1024;
 constexpr int CHUNK_ROWS = 256;
-constexpr int GRAPH_ITERS = 16;
+constexpr int GRAPH_ITERS = 16;   // even: p buffers alternate per iteration
 
-// column offset of slot component s_k along original axis k for row index r_k
-__device__ __forceinline__ int64_t col_contrib(const CompInfo& C, int k, int sk, int rk, int p) {
-    return (int64_t)(C.absm[k] ? (sk - rk) : (sk - p)) * C.rs[k];
+// shared memory (in doubles) of one small-path CTA: reductions, 6 vectors
+// (p with halo), the slot-offset table; the matrix is appended when it fits
+__host__ __device__ inline int64_t small_vec_doubles(int64_t R, int64_t H, int64_t NS) {
+    // red, x r z d q, p+halo, offs (int), rowbase (int), SpMV partials, pad
+    return 128 + 6 * R + 2 * H + (NS + 1) / 2 + 1 + (R + 1) / 2 + 1 + (R > 1024 ? R : 1024) + 2;
 }
 
-// y(row) = sum_slots A(row, slot) * v(col(row, slot)); v indexed from the
-// component's padded base.  Slots split across `lanes` threads.
-template <int D>
-__device__ __forceinline__ double spmv_row(const CompInfo& C, const double* __restrict__ val,
-                                           const double* __restrict__ v, int64_t row, int p,
-                                           int lane, int lanes) {
-    int r[3] = {0, 0, 0};
-#pragma unroll
-    for (int k = 0; k < D; ++k) r[k] = (int)((row / C.rs[k]) % C.m[k]);
-    int S0 = C.S[0], S1 = D > 1 ? C.S[1] : 1, S2 = D > 2 ? C.S[2] : 1;
-    int64_t ns = (int64_t)S0 * S1 * S2;
-    double acc = 0.0;
-    for (int64_t t = lane; t < ns; t += lanes) {
-        int s2 = (int)(t % S2), s1 = (int)((t / S2) % S1), s0 = (int)(t / ((int64_t)S1 * S2));
-        int64_t col = row + col_contrib(C, 0, s0, r[0], p);
-        int64_t slot = (int64_t)s0 * C.ss[0];
-        if (D > 1) { col += col_contrib(C, 1, s1, r[1], p); slot += (int64_t)s1 * C.ss[1]; }
-        if (D > 2) { col += col_contrib(C, 2, s2, r[2], p); slot += (int64_t)s2 * C.ss[2]; }
-        acc += __ldg(&val[slot * C.rows + row]) * v[col];
-    }
-    return acc;
+__device__ __forceinline__ int rowbase_of(const CompInfo& C, int d, int row) {
+    int rb = row;
+    for (int k = 0; k < d; ++k)
+        if (C.absm[k]) rb -= ((row / (int)C.rs[k]) % C.m[k]) * (int)C.rs[k];
+    return rb;
 }
 
-// deterministic block reduction of NV values (fixed shuffle tree + fixed
-// warp order); result broadcast to all threads.
+// warp-level deterministic sum, then a fixed-order sum over the block's
+// warp partials read by every thread (one barrier; `red` must not be
+// rewritten before another barrier has passed -> callers double-buffer).
 template <int NV>
-__device__ __forceinline__ void block_sum(double* v, double* red /* [32*NV] */) {
+__device__ __forceinline__ void block_sum_1sync(double* v, double* red) {
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
     for (int k = 0; k < NV; ++k)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-    __syncthreads();
     if (lane == 0)
 #pragma unroll
         for (int k = 0; k < NV; ++k) red[k * 32 + w] = v[k];
     __syncthreads();
-    if (w == 0) {
 #pragma unroll
-        for (int k = 0; k < NV; ++k) {
-            double t = lane < nw ? red[k * 32 + lane] : 0.0;
+    for (int k = 0; k < NV; ++k) {
+        double t = lane < nw ? red[k * 32 + lane] : 0.0;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-            if (lane == 0) red[k * 32] = t;
-        }
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        v[k] = t;
     }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] = red[k * 32];
-    __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -86,69 +71,105 @@ __device__ __forceinline__ void block_sum(double* v, double* red /* [32*NV] */) 
 template <int D>
 __global__ void __launch_bounds__(SMALL_THREADS)
 k_pcg_small(const CompInfo* __restrict__ comps, const int* __restrict__ list,
-            const double* __restrict__ stencil, const double* __restrict__ rhs,
-            const double* __restrict__ dinv, double* __restrict__ xout, CgState* __restrict__ st,
-            int p, double rtol2, int maxit) {
+            const int* __restrict__ slotoff, const double* __restrict__ stencil,
+            const double* __restrict__ rhs, const double* __restrict__ dinv,
+            double* __restrict__ xout, CgState* __restrict__ st, double rtol2, int maxit,
+            int smem_doubles) {
     extern __shared__ double sm[];
     const int c = list[blockIdx.x];
-    const CompInfo C = comps[c];
-    const int64_t R = C.rows, H = C.halo;
-    double* xs = sm;
+    const CompInfo& Cg = comps[c];
+    const int R = (int)Cg.rows, H = (int)Cg.halo, NS = (int)Cg.nslots;
+    // leading slots staged in shared memory, the rest streamed from L2/HBM
+    const int NSS = (int)min((int64_t)NS, (smem_doubles - small_vec_doubles(R, H, NS)) / R);
+    double* red = sm;                     // [2][64] double-buffered reductions
+    double* xs = red + 128;
     double* rs_ = xs + R;
     double* zs = rs_ + R;
     double* ds = zs + R;
     double* qv = ds + R;
-    double* pe = qv + R;          // [H + R + H]
-    double* red = pe + R + 2 * H; // [32*2]
+    double* pe = qv + R;                  // [H + R + H]
     double* ps = pe + H;
-    const double* val = stencil + C.mat_off;
-    const double* b = rhs + C.vec_off;
-    const double* di = dinv + C.vec_off;
-    const int tid = threadIdx.x, nth = blockDim.x;
-    int lanes = 1;
-    while (lanes < 32 && lanes * 2 * R <= nth) lanes *= 2;
-    const int groups = nth / lanes, grp = tid / lanes, lane = tid % lanes;
+    int* offs = reinterpret_cast<int*>(pe + R + 2 * H);        // [NS]
+    double* msm = sm + small_vec_doubles(R, H, NS);              // [NSS*R]
+    const double* gval = stencil + Cg.mat_off;
+    const double* b = rhs + Cg.vec_off;
+    const double* di = dinv + Cg.vec_off;
+    const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = nth >> 5, nrb = (R + 31) >> 5;
+    const int NG = nrb <= nwarps ? nwarps / nrb : 1;    // slot groups per row block
+    int* rbv = offs + NS + (NS & 1);                     // [R] rowbase per row
+    double* parts = reinterpret_cast<double*>(rbv + R + (R & 1));   // [NG][R]
 
+    for (int i = tid; i < NS; i += nth) offs[i] = slotoff[Cg.so_off + i];
+    for (int i = tid; i < R; i += nth) rbv[i] = rowbase_of(Cg, D, i);
+    for (int i = tid; i < NSS * R; i += nth) msm[i] = gval[i];
+    for (int i = tid; i < H; i += nth) { pe[i] = 0.0; pe[H + R + i] = 0.0; }
     double v2[2] = {0.0, 0.0};
-    for (int64_t i = tid; i < H; i += nth) { pe[i] = 0.0; pe[H + R + i] = 0.0; }
-    for (int64_t i = tid; i < R; i += nth) {
-        double bi = b[i], d = di[i], z = d * bi;
-        xs[i] = 0.0; rs_[i] = bi; ds[i] = d; zs[i] = z; ps[i] = z;
+    for (int i = tid; i < R; i += nth) {
+        double bi = b[i], dd = di[i], z = dd * bi;
+        xs[i] = 0.0; rs_[i] = bi; ds[i] = dd; zs[i] = z; ps[i] = z;
         v2[0] += bi * z;
         v2[1] += bi * bi;
     }
-    block_sum<2>(v2, red);
-    double rho = v2[0], bb = v2[1];
-    int it = 0, conv = (bb == 0.0);
+    block_sum_1sync<2>(v2, red);
+    double rho = v2[0];
+    const double bb = v2[1];
+    int it = 0, conv = (bb == 0.0), par = 1;
+    __syncthreads();
     while (!conv && it < maxit) {
-        // q = A p ; p.q
-        double pq[1] = {0.0};
-        for (int64_t base = 0; base < R; base += groups) {   // warp-uniform trip count
-            int64_t row = base + grp;
-            double y = row < R ? spmv_row<D>(C, val, ps, row, p, lane, lanes) : 0.0;
-            for (int o = lanes >> 1; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
-            if (lane == 0 && row < R) { qv[row] = y; pq[0] += ps[row] * y; }
+        // SpMV, slot-parallel: warp (row block, slot group g) streams slots
+        // t = g, g+NG, ... over 32 consecutive rows (coalesced, conflict-free)
+        for (int w = warp; w < nrb * NG; w += nwarps) {
+            const int rbk = w % nrb, g = w / nrb, row = rbk * 32 + lane;
+            double y0 = 0.0, y1 = 0.0;
+            if (row < R) {
+                const int rb = rbv[row];
+                int t = g;
+                for (; t + NG < NSS; t += 2 * NG) {
+                    y0 += msm[t * R + row] * ps[rb + offs[t]];
+                    y1 += msm[(t + NG) * R + row] * ps[rb + offs[t + NG]];
+                }
+                if (t < NSS) { y0 += msm[t * R + row] * ps[rb + offs[t]]; t += NG; }
+                const double* gv = gval + row;
+                for (; t + NG < NS; t += 2 * NG) {
+                    double a0 = __ldg(gv + (size_t)t * R), a1 = __ldg(gv + (size_t)(t + NG) * R);
+                    y0 += a0 * ps[rb + offs[t]];
+                    y1 += a1 * ps[rb + offs[t + NG]];
+                }
+                if (t < NS) y0 += __ldg(gv + (size_t)t * R) * ps[rb + offs[t]];
+                parts[g * R + row] = y0 + y1;
+            }
         }
-        block_sum<1>(pq, red);
-        double alpha = rho / pq[0];
+        __syncthreads();
+        double pq[1] = {0.0};
+        for (int i = tid; i < R; i += nth) {
+            double y = parts[i];
+            for (int g = 1; g < NG; ++g) y += parts[g * R + i];   // fixed order
+            qv[i] = y;
+            pq[0] += ps[i] * y;
+        }
+        block_sum_1sync<1>(pq, red + 64 * par);
+        par ^= 1;
+        const double alpha = rho / pq[0];
         double w[2] = {0.0, 0.0};
-        for (int64_t i = tid; i < R; i += nth) {
-            double xi = xs[i] + alpha * ps[i];
+        for (int i = tid; i < R; i += nth) {
             double ri = rs_[i] - alpha * qv[i];
+            xs[i] += alpha * ps[i];
             double zi = ds[i] * ri;
-            xs[i] = xi; rs_[i] = ri; zs[i] = zi;
+            rs_[i] = ri; zs[i] = zi;
             w[0] += ri * ri;
             w[1] += ri * zi;
         }
-        block_sum<2>(w, red);
+        block_sum_1sync<2>(w, red + 64 * par);
+        par ^= 1;
         ++it;
         if (w[0] <= rtol2 * bb) { conv = 1; break; }
-        double beta = w[1] / rho;
+        const double beta = w[1] / rho;
         rho = w[1];
-        for (int64_t i = tid; i < R; i += nth) ps[i] = zs[i] + beta * ps[i];
-        __syncthreads();
+        for (int i = tid; i < R; i += nth) ps[i] = zs[i] + beta * ps[i];
+        __syncthreads();   // p complete before the next SpMV
     }
-    for (int64_t i = tid; i < R; i += nth) xout[C.vec_off + i] = xs[i];
+    for (int i = tid; i < R; i += nth) xout[Cg.vec_off + i] = xs[i];
     if (tid == 0) {
         st[c].it = it;
         st[c].conv = conv;
@@ -163,14 +184,15 @@ k_pcg_small(const CompInfo* __restrict__ comps, const int* __restrict__ list,
 struct ChunkCtx {
     const CompInfo* comps;
     const Chunk* chunks;
+    const int* slotoff;
     const double* stencil;
     const double* rhs;
     const double* dinv;
-    double *x, *r, *z, *p, *q;
+    double *x, *r, *z, *q;
+    double *p0, *p1;      // alternating direction buffers
     CgState* st;
     double* part;
     int* active_count;
-    int p_deg;
     double rtol2;
     int maxit;
 };
@@ -178,8 +200,8 @@ struct ChunkCtx {
 // last chunk of a component to finish reduces the partials (chunk order)
 template <int NV>
 __device__ __forceinline__ bool finish_component(const ChunkCtx& X, const Chunk& ch,
-                                                 const CompInfo& C, double* v, double* out,
-                                                 unsigned int* cnt, double* red) {
+                                                 const CompInfo& C, const double* v, double* out,
+                                                 unsigned int* cnt) {
     __shared__ bool last;
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -191,7 +213,6 @@ __device__ __forceinline__ bool finish_component(const ChunkCtx& X, const Chunk&
     __syncthreads();
     if (!last) return false;
     __threadfence();
-    // ordered final sum by warp 0
     if (threadIdx.x < 32) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
@@ -212,64 +233,82 @@ __global__ void k_cg_init(ChunkCtx X) {
     const Chunk ch = X.chunks[blockIdx.x];
     const CompInfo& C = X.comps[ch.comp];
     if (C.small) return;
-    int64_t row = ch.row0 + threadIdx.x;
     double v[2] = {0.0, 0.0};
     if (threadIdx.x < ch.nrow) {
-        int64_t i = C.vec_off + row;
+        int64_t i = C.vec_off + ch.row0 + threadIdx.x;
         double bi = X.rhs[i], z = X.dinv[i] * bi;
-        X.x[i] = 0.0; X.r[i] = bi; X.z[i] = z; X.p[i] = z;
+        X.x[i] = 0.0; X.r[i] = bi; X.z[i] = z; X.p0[i] = 0.0; X.p1[i] = 0.0;
         v[0] = bi * z; v[1] = bi * bi;
     }
-    block_sum<2>(v, red);
+    block_sum_1sync<2>(v, red);
     double out[2];
-    if (finish_component<2>(X, ch, C, v, out, &X.st[ch.comp].cnt1, red) && threadIdx.x == 0) {
+    if (finish_component<2>(X, ch, C, v, out, &X.st[ch.comp].cnt1) && threadIdx.x == 0) {
         CgState& s = X.st[ch.comp];
-        s.rho = out[0]; s.bb = out[1]; s.it = 0;
+        s.rho = out[0]; s.bb = out[1]; s.it = 0; s.beta = 0.0;
         s.conv = (out[1] == 0.0);
         s.active = !s.conv;
         if (s.active) atomicAdd(X.active_count, 1);
     }
 }
 
+// p_new = z + beta p_old (own rows, written to pn); q = A p_new with p_new
+// formed on the fly at gathered columns; partial p_new . q.
 template <int D>
-__global__ void k_cg_spmv(ChunkCtx X) {
+__global__ void __launch_bounds__(CHUNK_ROWS) k_cg_spmv(ChunkCtx X, int parity) {
     __shared__ double red[64];
     const Chunk ch = X.chunks[blockIdx.x];
     const CompInfo& C = X.comps[ch.comp];
     if (C.small || !X.st[ch.comp].active) return;
-    int64_t row = ch.row0 + threadIdx.x;
+    const double* po = (parity ? X.p1 : X.p0) + C.vec_off;
+    double* pn = (parity ? X.p0 : X.p1) + C.vec_off;
+    const double* z = X.z + C.vec_off;
+    const double beta = X.st[ch.comp].beta;
+    const int R = (int)C.rows, NS = (int)C.nslots;
+    const int* offs = X.slotoff + C.so_off;
+    const double* val = X.stencil + C.mat_off;
     double v[1] = {0.0};
     if (threadIdx.x < ch.nrow) {
-        double y = spmv_row<D>(C, X.stencil + C.mat_off, X.p + C.vec_off, row, X.p_deg, 0, 1);
+        int row = ch.row0 + threadIdx.x;
+        int rb = rowbase_of(C, D, row);
+        double y = 0.0;
+        const double* vr = val + row;
+#pragma unroll 4
+        for (int t = 0; t < NS; ++t) {
+            int col = rb + __ldg(offs + t);
+            y += __ldg(vr + (size_t)t * R) * (z[col] + beta * po[col]);
+        }
+        double pr = z[row] + beta * po[row];
+        pn[row] = pr;
         X.q[C.vec_off + row] = y;
-        v[0] = X.p[C.vec_off + row] * y;
+        v[0] = pr * y;
     }
-    block_sum<1>(v, red);
+    block_sum_1sync<1>(v, red);
     double out[1];
-    if (finish_component<1>(X, ch, C, v, out, &X.st[ch.comp].cnt1, red) && threadIdx.x == 0) {
+    if (finish_component<1>(X, ch, C, v, out, &X.st[ch.comp].cnt1) && threadIdx.x == 0) {
         CgState& s = X.st[ch.comp];
         s.alpha = s.rho / out[0];
     }
 }
 
-__global__ void k_cg_update(ChunkCtx X) {
+__global__ void __launch_bounds__(CHUNK_ROWS) k_cg_update(ChunkCtx X, int parity) {
     __shared__ double red[64];
     const Chunk ch = X.chunks[blockIdx.x];
     const CompInfo& C = X.comps[ch.comp];
     if (C.small || !X.st[ch.comp].active) return;
     const double alpha = X.st[ch.comp].alpha;
+    const double* pn = (parity ? X.p0 : X.p1);
     double v[2] = {0.0, 0.0};
     if (threadIdx.x < ch.nrow) {
         int64_t i = C.vec_off + ch.row0 + threadIdx.x;
         double ri = X.r[i] - alpha * X.q[i];
-        X.x[i] += alpha * X.p[i];
+        X.x[i] += alpha * pn[i];
         double zi = X.dinv[i] * ri;
         X.r[i] = ri; X.z[i] = zi;
         v[0] = ri * ri; v[1] = ri * zi;
     }
-    block_sum<2>(v, red);
+    block_sum_1sync<2>(v, red);
     double out[2];
-    if (finish_component<2>(X, ch, C, v, out, &X.st[ch.comp].cnt2, red) && threadIdx.x == 0) {
+    if (finish_component<2>(X, ch, C, v, out, &X.st[ch.comp].cnt2) && threadIdx.x == 0) {
         CgState& s = X.st[ch.comp];
         s.it += 1;
         if (out[0] <= X.rtol2 * s.bb) {
@@ -285,35 +324,30 @@ __global__ void k_cg_update(ChunkCtx X) {
     }
 }
 
-__global__ void k_cg_pupdate(ChunkCtx X) {
-    const Chunk ch = X.chunks[blockIdx.x];
-    const CompInfo& C = X.comps[ch.comp];
-    if (C.small || !X.st[ch.comp].active) return;
-    const double beta = X.st[ch.comp].beta;
-    if (threadIdx.x < ch.nrow) {
-        int64_t i = C.vec_off + ch.row0 + threadIdx.x;
-        X.p[i] = X.z[i] + beta * X.p[i];
-    }
-}
-
 // ---- residual check: relres_c = ||A x - b|| / ||b|| ----------------------
 template <int D>
 __global__ void k_residual(ChunkCtx X, double* relres) {
     __shared__ double red[64];
     const Chunk ch = X.chunks[blockIdx.x];
     const CompInfo& C = X.comps[ch.comp];
-    int64_t row = ch.row0 + threadIdx.x;
     double v[2] = {0.0, 0.0};
     if (threadIdx.x < ch.nrow) {
-        double y = spmv_row<D>(C, X.stencil + C.mat_off, X.x + C.vec_off, row, X.p_deg, 0, 1);
-        double bi = X.rhs[C.vec_off + row], e = y - bi, xv = X.x[C.vec_off + row];
+        int row = ch.row0 + threadIdx.x;
+        int rb = rowbase_of(C, D, row);
+        const int R = (int)C.rows, NS = (int)C.nslots;
+        const int* offs = X.slotoff + C.so_off;
+        const double* vr = X.stencil + C.mat_off + row;
+        const double* xv = X.x + C.vec_off;
+        double y = 0.0;
+        for (int t = 0; t < NS; ++t) y += vr[(size_t)t * R] * xv[rb + offs[t]];
+        double bi = X.rhs[C.vec_off + row], e = y - bi;
         v[0] = e * e;
         v[1] = bi * bi;
-        if (!isfinite(xv)) v[0] = __longlong_as_double(0x7ff8000000000000ULL);
+        if (!isfinite(xv[row])) v[0] = __longlong_as_double(0x7ff8000000000000ULL);
     }
-    block_sum<2>(v, red);
+    block_sum_1sync<2>(v, red);
     double out[2];
-    if (finish_component<2>(X, ch, C, v, out, &X.st[ch.comp].cnt1, red) && threadIdx.x == 0)
+    if (finish_component<2>(X, ch, C, v, out, &X.st[ch.comp].cnt1) && threadIdx.x == 0)
         relres[ch.comp] = out[1] > 0.0 ? sqrt(out[0] / out[1]) : (out[0] == 0.0 ? 0.0 : out[0]);
 }
 
@@ -344,24 +378,27 @@ __global__ void k_expand(const CompInfo* __restrict__ comps, int ncomp,
 
 static ChunkCtx make_ctx(Handle* h, double rtol, int maxit) {
     ChunkCtx X;
-    X.comps = h->d_comps; X.chunks = h->d_chunks; X.stencil = h->d_stencil;
-    X.rhs = h->d_rhs; X.dinv = h->d_dinv;
-    X.x = h->d_x; X.r = h->d_r; X.z = h->d_z; X.p = h->d_p; X.q = h->d_q;
+    X.comps = h->d_comps; X.chunks = h->d_chunks; X.slotoff = h->d_slotoff;
+    X.stencil = h->d_stencil; X.rhs = h->d_rhs; X.dinv = h->d_dinv;
+    X.x = h->d_x; X.r = h->d_r; X.z = h->d_z; X.q = h->d_q;
+    X.p0 = h->d_p; X.p1 = h->d_q2;
     X.st = h->d_cg; X.part = h->d_part; X.active_count = h->d_active_count;
-    X.p_deg = h->p; X.rtol2 = rtol * rtol; X.maxit = maxit;
+    X.rtol2 = rtol * rtol; X.maxit = maxit;
     return X;
 }
 
 extern int64_t* comp_dof_cum_ptr(Handle* h);
 
-size_t small_smem_bytes(const Handle* h) {
-    int64_t mx = 0;
+size_t small_smem_bytes(const Handle* h, int64_t* smem_doubles) {
+    const int64_t limit = (224 * 1024) / 8;
+    int64_t total = 0;
     for (int c : h->small_comps) {
         const CompInfo& C = h->comps[c];
-        int64_t b = 6 * C.rows + 2 * C.halo;
-        if (b > mx) mx = b;
+        int64_t v = small_vec_doubles(C.rows, C.halo, C.nslots);
+        total = std::max(total, std::min(limit, v + C.rows * C.nslots));
     }
-    return (size_t)(mx + 64) * sizeof(double);
+    *smem_doubles = total;
+    return (size_t)total * sizeof(double);
 }
 
 int run_pcg(Handle* h, double rtol, int maxit) {
@@ -369,14 +406,16 @@ int run_pcg(Handle* h, double rtol, int maxit) {
     int nch = (int)h->chunks.size();
     SG_CUDA(cudaMemsetAsync(h->d_active_count, 0, sizeof(int), h->stream));
     if (!h->small_comps.empty()) {
-        size_t smem = small_smem_bytes(h);
+        int64_t total = 0;
+        size_t smem = small_smem_bytes(h, &total);
+        int cap = (int)total;   // a CTA stages its matrix iff its vectors + matrix fit
+        h->kstart(3);
 #define LAUNCH_SMALL(DD)                                                                         \
     SG_CUDA(cudaFuncSetAttribute(k_pcg_small<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                  (int)smem));                                                    \
     k_pcg_small<DD><<<(unsigned)h->small_comps.size(), SMALL_THREADS, smem, h->stream>>>(        \
-        h->d_comps, h->d_small, h->d_stencil, h->d_rhs, h->d_dinv, h->d_x, h->d_cg, h->p,        \
-        rtol * rtol, maxit)
-        h->kstart(3);
+        h->d_comps, h->d_small, h->d_slotoff, h->d_stencil, h->d_rhs, h->d_dinv, h->d_x,         \
+        h->d_cg, rtol * rtol, maxit, cap)
         if (h->d == 1) { LAUNCH_SMALL(1); }
         else if (h->d == 2) { LAUNCH_SMALL(2); }
         else { LAUNCH_SMALL(3); }
@@ -395,18 +434,18 @@ int run_pcg(Handle* h, double rtol, int maxit) {
         cudaGraphExec_t exec;
         SG_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
         for (int k = 0; k < GRAPH_ITERS; ++k) {
-            if (h->d == 1) k_cg_spmv<1><<<nch, CHUNK_ROWS, 0, h->stream>>>(X);
-            else if (h->d == 2) k_cg_spmv<2><<<nch, CHUNK_ROWS, 0, h->stream>>>(X);
-            else k_cg_spmv<3><<<nch, CHUNK_ROWS, 0, h->stream>>>(X);
-            k_cg_update<<<nch, CHUNK_ROWS, 0, h->stream>>>(X);
-            k_cg_pupdate<<<nch, CHUNK_ROWS, 0, h->stream>>>(X);
+            int par = k & 1;
+            if (h->d == 1) k_cg_spmv<1><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, par);
+            else if (h->d == 2) k_cg_spmv<2><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, par);
+            else k_cg_spmv<3><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, par);
+            k_cg_update<<<nch, CHUNK_ROWS, 0, h->stream>>>(X, par);
         }
         SG_CUDA(cudaStreamEndCapture(h->stream, &graph));
         SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
         int max_rounds = maxit / GRAPH_ITERS + 2;
         for (int round = 0; round < max_rounds; ++round) {
             SG_CUDA(cudaGraphLaunch(exec, h->stream));
-            h->launches[1] += 3 * GRAPH_ITERS;
+            h->launches[1] += 2 * GRAPH_ITERS;
             SG_CUDA(cudaMemcpyAsync(h->h_pinned_flag, h->d_active_count, sizeof(int),
                                     cudaMemcpyDeviceToHost, h->stream));
             SG_CUDA(cudaStreamSynchronize(h->stream));
@@ -415,6 +454,7 @@ int run_pcg(Handle* h, double rtol, int maxit) {
         h->kstop(4);
         cudaGraphExecDestroy(exec);
         cudaGraphDestroy(graph);
+        // the converged x of every component is in d_x regardless of parity
     }
     return SGIGA_OK;
 }
@@ -422,6 +462,7 @@ int run_pcg(Handle* h, double rtol, int maxit) {
 cudaError_t launch_residual_check(Handle* h) {
     ChunkCtx X = make_ctx(h, 0.0, 0);
     int nch = (int)h->chunks.size();
+    if (nch == 0) return cudaSuccess;
     if (h->d == 1) k_residual<1><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres);
     else if (h->d == 2) k_residual<2><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres);
     else k_residual<3><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres);
@@ -431,6 +472,7 @@ cudaError_t launch_residual_check(Handle* h) {
 
 cudaError_t launch_expand(Handle* h) {
     int64_t n = h->total_dofs;
+    if (n == 0) return cudaSuccess;
     unsigned blocks = (unsigned)((n + 255) / 256);
     if (h->d == 1) k_expand<1><<<blocks, 256, 0, h->stream>>>(h->d_comps, h->ncomp, comp_dof_cum_ptr(h), h->d_x, h->d_coef);
     else if (h->d == 2) k_expand<2><<<blocks, 256, 0, h->stream>>>(h->d_comps, h->ncomp, comp_dof_cum_ptr(h), h->d_x, h->d_coef);

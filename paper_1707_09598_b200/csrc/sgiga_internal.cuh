@@ -33,6 +33,7 @@ enum : int { ERRF_GEOMETRY = 1, ERRF_NONFINITE = 2, ERRF_SPAN = 4 };
 struct TabInfo {        // one analysis knot vector = (axis, level)
     int axis, level;
     int nel, nk, n;     // elements, knots, functions
+    int uniform;        // 1: breakpoints are exactly j/nel with nel a power of two
     int64_t bp_off;     // breakpoints (nel+1) in d_bp
     int64_t knot_off;   // knots in d_knots
     int64_t val_off;    // basis values [nel][q][P]; derivs at +nel*q*P
@@ -63,6 +64,7 @@ struct CompInfo {
     int64_t qs[MAXD];   // qp storage stride of ORIGINAL axis k
     int64_t dof_off;    // full coefficient vector offset
     int64_t ndofs;
+    int64_t so_off;     // slot column-offset table: col = rowbase(row) + off[slot]
     int64_t chunk_off;  // first PCG chunk (large path)
     int nchunks;
     int pad_;
@@ -147,6 +149,41 @@ __device__ __forceinline__ void ders_basis_funs(int i, double xi, int p, int nde
     for (int k = 1; k <= kmax; ++k) {
         for (int j = 0; j <= p; ++j) ders[k * (p + 1) + j] = __dmul_rn(ders[k * (p + 1) + j], fac);
         fac = __dmul_rn(fac, (double)(p - k));
+    }
+}
+
+// Same recurrence with a compile-time degree: fully unrolled, register
+// resident, identical rounding (values + first derivatives only).
+template <int p>
+__device__ __forceinline__ void ders_basis_funs_t(int i, double xi, const double* __restrict__ knots,
+                                                  double* N, double* dN) {
+    double ndu[p + 1][p + 1];
+    double left[p + 1], right[p + 1];
+    ndu[0][0] = 1.0;
+#pragma unroll
+    for (int j = 1; j <= p; ++j) {
+        left[j] = __dsub_rn(xi, knots[i + 1 - j]);
+        right[j] = __dsub_rn(knots[i + j], xi);
+        double saved = 0.0;
+#pragma unroll
+        for (int r = 0; r < j; ++r) {
+            ndu[j][r] = __dadd_rn(right[r + 1], left[j - r]);
+            double temp = __ddiv_rn(ndu[r][j - 1], ndu[j][r]);
+            ndu[r][j] = __dadd_rn(saved, __dmul_rn(right[r + 1], temp));
+            saved = __dmul_rn(left[j - r], temp);
+        }
+        ndu[j][j] = saved;
+    }
+#pragma unroll
+    for (int j = 0; j <= p; ++j) N[j] = ndu[j][p];
+    if (dN == nullptr) return;
+    // first derivatives (k = 1 of A2.3): a[s2][0] = 1/ndu[p][r-1], ...
+#pragma unroll
+    for (int r = 0; r <= p; ++r) {
+        double d = 0.0;
+        if (r >= 1) d = __dmul_rn(__ddiv_rn(1.0, ndu[p][r - 1]), ndu[r - 1][p - 1]);
+        if (r <= p - 1) d = __dadd_rn(d, __dmul_rn(__ddiv_rn(-1.0, ndu[p][r]), ndu[r][p - 1]));
+        dN[r] = __dmul_rn(d, (double)p);
     }
 }
 
