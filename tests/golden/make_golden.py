@@ -222,6 +222,17 @@ def gen_config(name, comps_to_store=None, n_points=512, workers=1):
                                   analysis.analytic_evaluator(u, g), grid)
     out["errors"] = np.array([l2, h1])
     out["errors_wall"] = np.array(time.perf_counter() - t0)
+    if name == "cfg5":
+        # 1.4 M coefficients are too big for a fixture: keep the stored
+        # components in full and a per-component checksum (norm, seeded dot)
+        coef = out.pop("coefficients")
+        off = np.concatenate([[0], np.cumsum(np.prod(out["dims"], axis=1))])
+        vs = [coef[off[c]:off[c + 1]] for c in range(len(off) - 1)]
+        out["coef_norms"] = np.array([np.linalg.norm(v) for v in vs])
+        out["coef_dots"] = np.array([np.random.default_rng(1000 + c).standard_normal(v.size) @ v
+                                     for c, v in enumerate(vs)])
+        for i in out["stored"]:
+            out[f"k{i}_coef"] = vs[i]
     np.savez_compressed(HERE / f"{name}.npz", **out)
     print(name, "components", len(plan), "L2/H1", l2, h1, flush=True)
 

@@ -254,7 +254,14 @@ def test_cfg5_full_pipeline(golden):
         it, rr = b.solve(rtol=1e-13)
         assert np.all(rr <= 1e-11)
         coefs = b.coefficients()
-        assert rel_l2(coefs, g["coefficients"]) <= 1e-9
+        # checksum of checksums: per-component norm and seeded dot product
+        for c in range(len(cfg.plan)):
+            v = b.component_coefficients(coefs, c)
+            assert abs(np.linalg.norm(v) - g["coef_norms"][c]) <= 1e-9 * g["coef_norms"][c]
+            w = np.random.default_rng(1000 + c).standard_normal(v.size)
+            assert abs(w @ v - g["coef_dots"][c]) <= 1e-8 * g["coef_norms"][c] * np.sqrt(v.size)
+        for i in g["stored"]:
+            assert rel_l2(b.component_coefficients(coefs, int(i)), g[f"k{i}_coef"]) <= 1e-9
         vals = b.combine_points(g["points"])
         assert rel_l2(vals, g["combined"]) <= 1e-9
         l2, h1 = b.error_norms(cfg.grid().points_per_dir, cfg.grid().weights_per_dir,
