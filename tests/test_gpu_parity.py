@@ -240,6 +240,33 @@ def test_run_report_invariants():
         run_plan(cfg.plan, cfg.problem, workers=0)
 
 
+def test_distributed_path_single_rank_bitwise():
+    """run_plan_distributed (NCCL, world 1; ranks>1 are covered by the gloo
+    tests) is bitwise equal to the single-GPU plan-order combine."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_09598_b200.distributed import run_plan_distributed
+
+    cfg = configs.get_config("cfg3")
+    pts = cfg.points(2000)
+    sols, _ = run_plan(cfg.plan, cfg.problem)
+    ref = evaluate_combined_points(cfg.plan, sols, pts)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        vals = run_plan_distributed(cfg.plan, cfg.problem, pts)
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(vals, ref)
+
+
 @pytest.mark.slow
 def test_cfg5_full_pipeline(golden):
     g = golden("cfg5")
@@ -252,7 +279,10 @@ def test_cfg5_full_pipeline(golden):
             assert normwise(A_ @ g[f"k{i}_v"], g[f"k{i}_Av"]) <= 1e-12
             assert normwise(rhs, g[f"k{i}_rhs"]) <= 1e-12
         it, rr = b.solve(rtol=1e-13)
-        assert np.all(rr <= 1e-11)
+        # recursive residual <= 1e-13; the true residual drifts to ~5e-11 on the
+        # kappa~1e6 (1,1,10) components and must meet linsolve.py:49-53 (1e-10)
+        assert np.all(rr <= 1e-10)
+        assert int(it.sum()) == pytest.approx(408300, rel=0.01)   # SURVEY 8(d) CPU-CG count
         coefs = b.coefficients()
         # checksum of checksums: per-component norm and seeded dot product
         for c in range(len(cfg.plan)):
