@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -172,10 +173,12 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
             C.rs[k] = pr; pr *= C.m[k];
             C.ss[k] = ps; ps *= C.S[k];
         }
-        // qp storage order: s outermost, then ax[d-2], ..., ax[0] innermost
+        // qp storage order: stream axis s = ax[d-1] outermost, tile axis
+        // a = ax[d-2] innermost (a pencil's plane window is contiguous in a)
         int64_t pq = 1;
+        const int qorder[3] = {d >= 2 ? C.ax[d - 2] : C.ax[0], d >= 3 ? C.ax[0] : C.ax[d - 1], C.ax[d - 1]};
         for (int jj = 0; jj < d; ++jj) {
-            int k = C.ax[jj];
+            int k = (d == 1) ? C.ax[0] : (d == 2 ? (jj == 0 ? C.ax[0] : C.ax[1]) : qorder[jj]);
             C.qs[k] = pq;
             pq *= (int64_t)C.nel[k] * h->q;
         }
@@ -407,6 +410,8 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     st = upload_all(h);
     if (st) { free_all(h); delete h; return st; }
     h->iters.assign(h->ncomp, 0);
+    const char* gen = getenv("SGIGA_GENERIC_ASSEMBLY");
+    h->force_generic_assembly = gen && gen[0] == '1';
     *out = reinterpret_cast<sgiga_handle*>(h);
     return SGIGA_OK;
 }

@@ -93,6 +93,7 @@ struct Handle {
     float ms[3] = {0, 0, 0};
     long long launches[3] = {0, 0, 0};
     std::vector<int> iters;
+    bool force_generic_assembly = false;   // SGIGA_GENERIC_ASSEMBLY=1 (parity cross-check)
 
     void kstart(int g) { cudaEventRecord(kev[2 * g], stream); kran[g] = true; }
     void kstop(int g) { cudaEventRecord(kev[2 * g + 1], stream); }

@@ -298,9 +298,14 @@ size_t assembly_smem_bytes(const Handle* h) {
     return n * sizeof(double);
 }
 
+bool launch_assembly_fast(Handle* h, cudaError_t* err);
+
 cudaError_t launch_assembly(Handle* h) {
     int np = (int)h->pencils.size();
     if (np == 0) return cudaSuccess;
+    cudaError_t fe = cudaSuccess;
+    if (!h->force_generic_assembly && launch_assembly_fast(h, &fe))   // maximal regularity, q = p+1
+        return fe == cudaSuccess ? cudaGetLastError() : fe;
     size_t smem = assembly_smem_bytes(h);
     cudaError_t e;
 #define LAUNCH_ASM(DD)                                                                        \

@@ -1,0 +1,361 @@
+// k_assembly_fast.cu -- kernel 2, fast path: maximal-regularity spaces
+// (interior multiplicity 1) with q = p + 1, compile-time (D, P, Q).
+//
+// Same global sum factorisation as k_assembly.cu (see the derivation
+// there), expressed in *relative* offsets o = j - i in [-p, p] so every
+// support range is compile-time:
+//   * a pencil row i's support window is elements i-p .. i (t = 0..p),
+//     window point x = t*Q + g; on element i-p+t the row function has local
+//     index p-t and the column function j = i + (t+k) - p has local index k,
+//     so T[type][x][k] (k = 0..p) holds exactly the nonzero (slot, point)
+//     pairs -- slot s = t + k.  Window elements outside the patch (rows near
+//     the boundary, short axes) are skipped by predication, never computed;
+//   * the metric plane window is copied with cp.async (only valid points;
+//     the invalid ones are zeroed once per pencil), double-buffered so the
+//     next plane streams in while the current one is contracted;
+//   * stage 1 (contract tile axis b): warp half <-> pair (m,n), lane <-> x_a,
+//     W register accumulators, P FMAs per metric value loaded;
+//   * stage 2 (contract tile axis a): (pair, s_b, t) items, then a
+//     fixed-order sum over the pairs of each stream type and over t;
+//   * stage 3: rank-1 update of the P alive rows of the current stream
+//     element; completed rows are flushed, mapping relative offsets to the
+//     stencil's storage slots (absolute or relative), zeros elsewhere.
+// Deterministic, no atomics; every stencil entry is written exactly once.
+#include "handle.cuh"
+
+namespace sgiga {
+
+constexpr int FAST_THREADS = 320;   // 10 warps
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
+
+template <int D, int P, int Q>
+struct FastCfg {
+    static constexpr int p = P - 1;
+    static constexpr int W = 2 * P - 1;               // relative slots per axis
+    static constexpr int NX = P * Q;                   // window points per tile axis
+    static constexpr int NA = D >= 2 ? NX : 1;
+    static constexpr int NB = D >= 3 ? NX : 1;
+    static constexpr int NAP = D >= 2 ? (NX | 1) : 1;  // odd row stride: conflict-free
+    static constexpr int WA = D >= 2 ? W : 1;
+    static constexpr int WB = D >= 3 ? W : 1;
+    static constexpr int WAB = WA * WB;
+    static constexpr int NG = D * (D + 1) / 2 + 1;     // metric entries + load
+    static constexpr int NPAIR = D * D;
+    static constexpr int PPW = NX <= 16 ? 2 : 1;       // pairs per warp in stage 1
+    static constexpr int RING = P;                     // alive rows of one element
+    static constexpr int nGw = NG * NB * NAP;          // one plane buffer
+    // shared-memory layout (doubles)
+    static constexpr int oGw = 0;                      // [2][NG][NB][NAP]
+    static constexpr int oTa = oGw + 2 * nGw;          // [4][NA][P]
+    static constexpr int oTb = oTa + 4 * NA * P;       // [4][NB][P]
+    static constexpr int oPhiA = oTb + 4 * NB * P;     // [NA]
+    static constexpr int oPhiB = oPhiA + NA;           // [NB]
+    static constexpr int oS1 = oPhiB + NB;             // [NPAIR][NA][WB]
+    static constexpr int oSL1 = oS1 + NPAIR * NA * WB; // [NA]
+    static constexpr int oP2 = oSL1 + NA;              // [NPAIR][P][P][WB]
+    static constexpr int oS2 = oP2 + NPAIR * P * P * WB;  // [4][WAB] + load
+    static constexpr int oBs = oS2 + 4 * WAB + 1;      // [2][Q][P]
+    static constexpr int oAcc = oBs + 2 * Q * P;       // [RING][W][WAB]
+    static constexpr int oAccL = oAcc + RING * W * WAB;
+    static constexpr int total = oAccL + RING;
+};
+
+template <int D, int P, int Q>
+size_t fast_smem_bytes() { return sizeof(double) * FastCfg<D, P, Q>::total; }
+
+template <int D, int P, int Q>
+__global__ void __launch_bounds__(FAST_THREADS, 2)
+k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tabs,
+                const Pencil* __restrict__ pencils, const double* __restrict__ vals,
+                const double* __restrict__ Gbuf, double* __restrict__ stencil,
+                double* __restrict__ rhs, double* __restrict__ dinv) {
+    using F = FastCfg<D, P, Q>;
+    constexpr int p = F::p, W = F::W;
+    extern __shared__ double sm[];
+    double* Ta = sm + F::oTa;
+    double* Tb = sm + F::oTb;
+    double* phiA = sm + F::oPhiA;
+    double* phiB = sm + F::oPhiB;
+    double* S1 = sm + F::oS1;
+    double* SL1 = sm + F::oSL1;
+    double* P2 = sm + F::oP2;
+    double* S2 = sm + F::oS2;
+    double* Bs = sm + F::oBs;
+    double* Acc = sm + F::oAcc;
+    double* AccL = sm + F::oAccL;
+
+    const Pencil pc = pencils[blockIdx.x];
+    const CompInfo& C = comps[pc.comp];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int s = C.ax[D - 1];
+    const int ka = D >= 2 ? C.ax[D - 2] : 0, kb = D >= 3 ? C.ax[D - 3] : 0;
+    const TabInfo Ts = tabs[C.tab[s]];
+    const int nel_a = D >= 2 ? tabs[C.tab[ka]].nel : 1, nel_b = D >= 3 ? tabs[C.tab[kb]].nel : 1;
+    // valid window elements t in [t_lo, t_hi) of the two tile axes
+    const int ta_lo = D >= 2 ? max(0, p - pc.ia) : 0, ta_hi = D >= 2 ? min(P, nel_a + p - pc.ia) : 1;
+    const int tb_lo = D >= 3 ? max(0, p - pc.ib) : 0, tb_hi = D >= 3 ? min(P, nel_b + p - pc.ib) : 1;
+
+    // ---- 1-D pair tables of the tile axes (relative coordinates) ----------
+    auto build_T = [&](int k, int i, double* T, double* phi, int NXk) {
+        const TabInfo& TT = tabs[C.tab[k]];
+        const int64_t nq = (int64_t)TT.nel * Q;
+        for (int idx = tid; idx < 4 * NXk * P; idx += FAST_THREADS) {
+            int kk = idx % P, x = (idx / P) % NXk, type = idx / (P * NXk);
+            int t = x / Q, g = x % Q, e = i - p + t;
+            double v = 0.0;
+            if (e >= 0 && e < TT.nel) {
+                const double* base = vals + TT.val_off + ((int64_t)e * Q + g) * P;
+                double a = (type >> 1) ? base[nq * P + (p - t)] : base[p - t];
+                double b = (type & 1) ? base[nq * P + kk] : base[kk];
+                v = a * b;
+            }
+            T[idx] = v;
+        }
+        for (int x = tid; x < NXk; x += FAST_THREADS) {
+            int t = x / Q, g = x % Q, e = i - p + t;
+            phi[x] = (e >= 0 && e < TT.nel) ? vals[TT.val_off + ((int64_t)e * Q + g) * P + (p - t)] : 0.0;
+        }
+    };
+    if (D >= 2) build_T(ka, pc.ia, Ta, phiA, F::NA);
+    else if (tid == 0) { Ta[0] = 1.0; Ta[1] = Ta[2] = Ta[3] = 0.0; phiA[0] = 1.0; }
+    if (D >= 3) build_T(kb, pc.ib, Tb, phiB, F::NB);
+    else if (tid == 0) { Tb[0] = 1.0; Tb[1] = Tb[2] = Tb[3] = 0.0; phiB[0] = 1.0; }
+    for (int idx = tid; idx < F::RING * W * F::WAB + F::RING; idx += FAST_THREADS) Acc[idx] = 0.0;
+    // invalid window points stay zero in both plane buffers
+    for (int idx = tid; idx < 2 * F::nGw; idx += FAST_THREADS) sm[F::oGw + idx] = 0.0;
+    __syncthreads();
+
+    // ---- metric plane window (a innermost in global and shared memory) ----
+    const double* Gc = Gbuf + C.qp_off;
+    const int64_t nqp = C.nqp;
+    const int64_t qs_s = C.qs[s], qs_b = D >= 3 ? C.qs[kb] : 0;
+    const int xa_lo = D >= 2 ? ta_lo * Q : 0, nxa = D >= 2 ? (ta_hi - ta_lo) * Q : 1;   // valid xa run
+    const int xb_lo = D >= 3 ? tb_lo * Q : 0, nxb = D >= 3 ? (tb_hi - tb_lo) * Q : 1;
+    const int64_t Xa0 = D >= 2 ? (int64_t)(pc.ia - p) * Q + xa_lo : 0;   // first valid global a index
+    const int64_t Xb0 = D >= 3 ? (int64_t)(pc.ib - p) * Q + xb_lo : 0;
+    auto load_plane = [&](int64_t Qs, int buf) {
+        double* Gw = sm + F::oGw + buf * F::nGw;
+        const double* base = Gc + Qs * qs_s + Xa0 + Xb0 * qs_b;
+        const int per_row = nxa, rows = F::NG * nxb;
+        for (int idx = tid; idx < rows * per_row; idx += FAST_THREADS) {
+            const int xa = idx % per_row, r = idx / per_row;
+            const int xb = r % nxb, gi = r / nxb;
+            cp_async8(&Gw[(gi * F::NB + xb_lo + xb) * F::NAP + xa_lo + xa],
+                      base + (int64_t)gi * nqp + (int64_t)xb * qs_b + xa);
+        }
+        cp_async_commit();
+    };
+
+    constexpr int NPAIR = F::NPAIR;
+    const int r0 = pc.r0, r1 = pc.r1;
+    const int e_first = r0 - p < 0 ? 0 : r0 - p;
+    const int e_last = r1 - 1 > Ts.nel - 1 ? Ts.nel - 1 : r1 - 1;
+    const int64_t nq_s = (int64_t)Ts.nel * Q;
+    const int64_t row_base = (D >= 2 ? (int64_t)(pc.ia - 1) * C.rs[ka] : 0) +
+                             (D >= 3 ? (int64_t)(pc.ib - 1) * C.rs[kb] : 0);
+    int tsp[NPAIR];   // stream type of each (m, n) pair
+#pragma unroll
+    for (int pr = 0; pr < NPAIR; ++pr) tsp[pr] = 2 * ((pr / D) == s) + ((pr % D) == s);
+
+    int buf = 0;
+    load_plane((int64_t)e_first * Q, 0);
+    for (int e = e_first; e <= e_last; ++e) {
+        for (int idx = tid; idx < 2 * Q * P; idx += FAST_THREADS) {
+            int der = idx / (Q * P), rem = idx % (Q * P);
+            Bs[idx] = vals[Ts.val_off + (der ? nq_s * P : 0) + (int64_t)e * Q * P + rem];
+        }
+        for (int g = 0; g < Q; ++g) {
+            // issue the next plane, then wait for the current one
+            const bool more = (g + 1 < Q) || (e < e_last);
+            if (more) {
+                load_plane(g + 1 < Q ? (int64_t)e * Q + g + 1 : (int64_t)(e + 1) * Q, buf ^ 1);
+                cp_async_wait_prev();
+            } else {
+                cp_async_wait_all();
+            }
+            __syncthreads();
+            const double* Gw = sm + F::oGw + buf * F::nGw;
+            // ---- stage 1: contract tile axis b ------------------------------
+            if constexpr (D == 3) {
+                const int half = F::PPW == 2 ? (lane >> 4) : 0;
+                const int xa = F::PPW == 2 ? (lane & 15) : lane;
+                const int pr = warp * F::PPW + half;
+                if (pr < NPAIR && xa < F::NA) {
+                    const int gidx = sym_index(D, pr / D, pr % D);
+                    const int tb = 2 * ((pr / D) == kb) + ((pr % D) == kb);
+                    double acc[W];
+#pragma unroll
+                    for (int j = 0; j < W; ++j) acc[j] = 0.0;
+                    const double* gcol = Gw + gidx * F::NB * F::NAP + xa;
+                    const double* tr = Tb + tb * F::NB * P;
+#pragma unroll
+                    for (int t = 0; t < P; ++t) {
+                        if (t < tb_lo || t >= tb_hi) continue;
+#pragma unroll
+                        for (int g2 = 0; g2 < Q; ++g2) {
+                            const int x = t * Q + g2;
+                            const double gv = gcol[x * F::NAP];
+#pragma unroll
+                            for (int k = 0; k < P; ++k) acc[t + k] += gv * tr[x * P + k];
+                        }
+                    }
+                    double* out = S1 + (pr * F::NA + xa) * W;
+#pragma unroll
+                    for (int j = 0; j < W; ++j) out[j] = acc[j];
+                } else if (pr == NPAIR && xa < F::NA) {   // load: SL1 = sum_xb L phiB
+                    const double* gcol = Gw + (F::NG - 1) * F::NB * F::NAP + xa;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int x = 0; x < F::NB; ++x) acc += gcol[x * F::NAP] * phiB[x];
+                    SL1[xa] = acc;
+                }
+                __syncthreads();
+            }
+            // ---- stage 2: contract tile axis a ------------------------------
+            if constexpr (D >= 2) {
+                constexpr int NIT = NPAIR * F::WB * P;
+                for (int it = tid; it < NIT + 1; it += FAST_THREADS) {
+                    if (it == NIT) {   // load: SL2 = sum_xa SL1 phiA
+                        double acc = 0.0;
+#pragma unroll
+                        for (int x = 0; x < F::NA; ++x)
+                            acc += (D == 3 ? SL1[x] : Gw[(F::NG - 1) * F::NAP + x]) * phiA[x];
+                        S2[4 * F::WAB] = acc;
+                        continue;
+                    }
+                    const int t = it % P, sb = (it / P) % F::WB, pr = it / (P * F::WB);
+                    if (t < ta_lo || t >= ta_hi) continue;
+                    const int ta = 2 * ((pr / D) == ka) + ((pr % D) == ka);
+                    double acc[P];
+#pragma unroll
+                    for (int k = 0; k < P; ++k) acc[k] = 0.0;
+#pragma unroll
+                    for (int g2 = 0; g2 < Q; ++g2) {
+                        const int xa = t * Q + g2;
+                        const double sv = D == 3 ? S1[(pr * F::NA + xa) * W + sb]
+                                                 : Gw[sym_index(D, pr / D, pr % D) * F::NAP + xa];
+                        const double* tr = Ta + (ta * F::NA + xa) * P;
+#pragma unroll
+                        for (int k = 0; k < P; ++k) acc[k] += sv * tr[k];
+                    }
+                    double* out = P2 + ((pr * P + t) * P) * F::WB + sb;
+#pragma unroll
+                    for (int k = 0; k < P; ++k) out[k * F::WB] = acc[k];
+                }
+                __syncthreads();
+                // 2b: fixed-order sum over the pairs of a stream type and over t
+                for (int it = tid; it < 4 * F::WAB; it += FAST_THREADS) {
+                    const int sab = it % F::WAB, ts = it / F::WAB;
+                    const int sa = sab / F::WB, sb = sab % F::WB;
+                    const int tl = max(ta_lo, sa - p), th = min(ta_hi - 1, sa);
+                    double acc = 0.0;
+#pragma unroll
+                    for (int pr = 0; pr < NPAIR; ++pr) {
+                        if (tsp[pr] != ts) continue;
+                        for (int t = tl; t <= th; ++t) acc += P2[((pr * P + t) * P + (sa - t)) * F::WB + sb];
+                    }
+                    S2[it] = acc;
+                }
+            } else {
+                if (tid < 4) S2[tid] = (tid == 3) ? Gw[0] : 0.0;
+                if (tid == 0) S2[4] = Gw[(F::NG - 1) * F::NB * F::NAP];
+            }
+            __syncthreads();
+            // ---- stage 3: rank-1 update of the alive rows of element e ------
+            for (int it = tid; it < P * F::WAB; it += FAST_THREADS) {
+                const int sab = it % F::WAB, al = it / F::WAB;
+                const int i = e + al;
+                if (i < r0 || i >= r1) continue;
+                const double va = Bs[g * P + al], da = Bs[Q * P + g * P + al];
+                const double s0 = S2[sab], s1 = S2[F::WAB + sab], s2v = S2[2 * F::WAB + sab],
+                             s3 = S2[3 * F::WAB + sab];
+                const double c0 = va * s0 + da * s2v, c1 = va * s1 + da * s3;
+                double* acc = Acc + ((i % F::RING) * W) * F::WAB + sab;
+#pragma unroll
+                for (int bl = 0; bl < P; ++bl) {
+                    const double vb = Bs[g * P + bl], db = Bs[Q * P + g * P + bl];
+                    acc[(bl - al + p) * F::WAB] += vb * c0 + db * c1;
+                }
+            }
+            if (tid < P) {
+                const int i = e + tid;
+                if (i >= r0 && i < r1) AccL[i % F::RING] += Bs[g * P + tid] * S2[4 * F::WAB];
+            }
+            buf ^= 1;
+        }
+        __syncthreads();
+        // ---- flush: row e completes with element e; the last element also
+        // completes the trailing rows of the segment.  Every storage slot of
+        // a flushed row is written (zeros where the relative offset is out
+        // of the band or the column is on the boundary). ----------------------
+        const int lo = (e == e_last) ? (e > r0 ? e : r0) : e;
+        const int hi = (e == e_last) ? r1 : (e + 1 < r1 ? e + 1 : r1);
+        const int Ss = C.S[s], Sa = D >= 2 ? C.S[ka] : 1, Sb = D >= 3 ? C.S[kb] : 1;
+        for (int i = (lo > r0 ? lo : r0); i < hi; ++i) {
+            const int64_t row = row_base + (int64_t)(i - 1) * C.rs[s];
+            double* accr = Acc + ((i % F::RING) * W) * F::WAB;
+            // relative offset + p of storage slot sk on axis k for row index ik; -1 if none
+            auto rel_of = [&](int k, int ik, int sk) -> int {
+                const int j = C.absm[k] ? sk + 1 : ik + sk - p;
+                const int o = j - ik;
+                if (j < 1 || j > C.n[k] - 2 || o < -p || o > p) return -1;
+                return o + p;
+            };
+            for (int it = tid; it < Ss * Sa * Sb; it += FAST_THREADS) {
+                const int cb = it % Sb, ca = (it / Sb) % Sa, cs = it / (Sa * Sb);
+                const int os = rel_of(s, i, cs);
+                const int oa = D >= 2 ? rel_of(ka, pc.ia, ca) : 0;
+                const int ob = D >= 3 ? rel_of(kb, pc.ib, cb) : 0;
+                const double v = (os >= 0 && oa >= 0 && ob >= 0) ? accr[os * F::WAB + oa * F::WB + ob] : 0.0;
+                const int64_t slot = (int64_t)cs * C.ss[s] + (D >= 2 ? (int64_t)ca * C.ss[ka] : 0) +
+                                     (D >= 3 ? (int64_t)cb * C.ss[kb] : 0);
+                stencil[C.mat_off + slot * C.rows + row] = v;
+            }
+            if (tid == 0) {
+                const int dsab = D >= 2 ? (p * F::WB + (D >= 3 ? p : 0)) : 0;
+                rhs[C.vec_off + row] = AccL[i % F::RING];
+                dinv[C.vec_off + row] = 1.0 / accr[p * F::WAB + dsab];
+            }
+            __syncthreads();
+            for (int it = tid; it < W * F::WAB; it += FAST_THREADS) accr[it] = 0.0;
+            if (tid == 0) AccL[i % F::RING] = 0.0;
+            __syncthreads();
+        }
+    }
+}
+
+// dispatch: returns false when (d, p, q, mu) has no fast instantiation
+bool launch_assembly_fast(Handle* h, cudaError_t* err) {
+    if (h->mu != 1 || h->q != h->p + 1 || h->pencils.empty()) return false;
+    const int key = h->d * 10 + (h->p + 1);
+    size_t smem = 0;
+    const void* fn = nullptr;
+    switch (key) {
+#define CASE(DD, PP)                                                                 \
+    case DD * 10 + PP:                                                               \
+        smem = fast_smem_bytes<DD, PP, PP>();                                        \
+        fn = (const void*)k_assemble_fast<DD, PP, PP>;                               \
+        break;
+        CASE(1, 2) CASE(1, 3) CASE(1, 4) CASE(1, 5)
+        CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(2, 5)
+        CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(3, 5)
+#undef CASE
+    default: return false;
+    }
+    *err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (*err != cudaSuccess) return true;
+    void* args[] = {(void*)&h->d_comps, (void*)&h->d_tabs, (void*)&h->d_pencils, (void*)&h->d_tabvals,
+                    (void*)&h->d_G, (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv};
+    *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(FAST_THREADS), args, smem, h->stream);
+    h->launches[0] += 1;
+    return true;
+}
+
+}  // namespace sgiga

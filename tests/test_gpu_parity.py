@@ -95,6 +95,31 @@ def test_pipeline_matches_reference(golden, name):
     np.testing.assert_allclose([l2, h1], g["errors"], rtol=5e-4)
 
 
+@pytest.mark.parametrize("name,terms", [
+    ("cfg1", None), ("cfg3", None), ("cfg2", None),
+    ("cfg5", (((1, 1, 4), 1), ((2, 3, 2), 1), ((3, 1, 1), 1), ((1, 2, 1), 1))),
+])
+def test_fast_assembly_matches_generic(name, terms, monkeypatch):
+    """The templated fast kernel (q = p+1, maximal regularity) and the
+    generic runtime-sized kernel assemble the same stencil."""
+    cfg = configs.get_config(name)
+    terms = tuple(cfg.plan.terms) if terms is None else terms
+    spec = make_spec(terms, cfg.problem, cfg.quad_points)
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("SGIGA_GENERIC_ASSEMBLY", flag)
+        b = Batch(spec)
+        try:
+            b.assemble()
+            out.append([b.export_csr(c) for c in range(len(terms))])
+        finally:
+            b.close()
+    for (Af, bf), (Ag, bg) in zip(*out):
+        assert np.array_equal(Af.indptr, Ag.indptr) and np.array_equal(Af.indices, Ag.indices)
+        assert normwise(Af.data, Ag.data) <= 1e-13
+        assert normwise(bf, bg) <= 1e-13
+
+
 def test_pcg_residual_contract():
     cfg = configs.get_config("cfg2")
     spec, b = _batch(cfg)
@@ -294,9 +319,18 @@ def test_cfg5_full_pipeline(golden):
             assert rel_l2(b.component_coefficients(coefs, int(i)), g[f"k{i}_coef"]) <= 1e-9
         vals = b.combine_points(g["points"])
         assert rel_l2(vals, g["combined"]) <= 1e-9
-        l2, h1 = b.error_norms(cfg.grid().points_per_dir, cfg.grid().weights_per_dir,
-                               A.solution_id_of(cfg.problem.solution))
-        # cfg5 errors sit at the solve-noise floor: 2 digits
-        np.testing.assert_allclose([l2, h1], g["errors"], rtol=5e-2)
+        sid = A.solution_id_of(cfg.problem.solution)
+        l2, h1 = b.error_norms(cfg.grid().points_per_dir, cfg.grid().weights_per_dir, sid)
+        # cfg5's errors sit at the FP64 solve-noise floor (the
+        # reference's own CPU-CG moved them by 1.6%); the GPU solution must be
+        # at least as accurate as the reference's direct solve ...
+        assert l2 <= 1.05 * g["errors"][0] and h1 <= 1.05 * g["errors"][1]
+        # ... and the device error quadrature must agree with the oracle's on
+        # the same coefficients (coarser grid to keep the CPU side short)
+        spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+        grid = QuadGrid(cfg.problem.patch, (3, 3, 3), 5)
+        gl2, gh1 = b.error_norms(grid.points_per_dir, grid.weights_per_dir, sid)
+        ol2, oh1 = O.Oracle(spec).error_norms(grid.points_per_dir, grid.weights_per_dir, sid, coefs=coefs)
+        np.testing.assert_allclose([gl2, gh1], [ol2, oh1], rtol=1e-3)
     finally:
         b.close()
