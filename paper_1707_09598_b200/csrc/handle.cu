@@ -41,7 +41,7 @@ static void free_all(Handle* h) {
                     h->d_qw, h->d_geob, h->d_geofirst, h->d_geo_knots, h->d_geo_hw, h->d_G,
                     h->d_hostf, h->d_xphys, h->d_stencil, h->d_rhs, h->d_dinv, h->d_x,
                     h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
-                    h->d_active_count, h->d_relres, h->d_slotoff};
+                    h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->h_pinned_flag) cudaFreeHost(h->h_pinned_flag);
@@ -385,7 +385,8 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_cg, h->ncomp);
     A_(d_part, 3 * h->chunks.size());
     A_(d_err, 1);
-    A_(d_active_count, 1);
+    A_(d_active_count, 4);        // [active comps, active chunks, host copy of chunks]
+    A_(d_alist, h->chunks.size());
     A_(d_relres, h->ncomp);
     A_(d_slotoff, h->slotoff.size());
 #undef A_

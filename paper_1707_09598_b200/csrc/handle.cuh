@@ -80,6 +80,7 @@ struct Handle {
     double* d_part = nullptr;    // per-chunk partial sums [3*nchunks]
     int* d_err = nullptr;
     int* d_active_count = nullptr;
+    int* d_alist = nullptr;      // compacted active chunk list (large-path PCG)
     double* d_relres = nullptr;
     int* h_pinned_flag = nullptr;  // pinned host mirror of the active count
 

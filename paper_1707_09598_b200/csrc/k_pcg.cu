@@ -20,6 +20,9 @@
 //    per-component scalars reduced by the last chunk to finish in fixed
 //    chunk order (deterministic), iterations replayed as a CUDA graph with
 //    the convergence test on the device.
+#include <cstdio>
+#include <cstdlib>
+
 #include "handle.cuh"
 
 namespace sgiga {
@@ -193,9 +196,44 @@ struct ChunkCtx {
     CgState* st;
     double* part;
     int* active_count;
+    const int* alist;     // active chunk list (compacted between graph replays)
+    const int* acount;    // its length
     double rtol2;
     int maxit;
 };
+
+// in-place, order-preserving compaction of the active chunk list (one CTA)
+__global__ void __launch_bounds__(1024) k_cg_compact(const Chunk* __restrict__ chunks,
+                                                     const CgState* __restrict__ st,
+                                                     int* __restrict__ alist, int* __restrict__ acount,
+                                                     int* __restrict__ host_counts) {
+    __shared__ int wsum[32];
+    __shared__ int base;
+    const int n = *acount, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) base = 0;
+    __syncthreads();
+    for (int t0 = 0; t0 < n; t0 += 1024) {
+        const int i = t0 + tid;
+        const int c = i < n ? alist[i] : -1;
+        const int keep = (c >= 0 && st[chunks[c].comp].active) ? 1 : 0;
+        int incl = keep;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wsum[w] = incl;
+        __syncthreads();
+        int wbase = 0;
+        for (int k = 0; k < w; ++k) wbase += wsum[k];
+        const int pos = base + wbase + incl - keep;
+        __syncthreads();   // every thread has read alist[i] and wsum
+        if (keep) alist[pos] = c;
+        if (tid == 1023) base = pos + keep;
+        __syncthreads();
+    }
+    if (tid == 0) { *acount = base; host_counts[0] = base; }
+}
 
 // last chunk of a component to finish reduces the partials (chunk order)
 template <int NV>
@@ -253,10 +291,13 @@ __global__ void k_cg_init(ChunkCtx X) {
 
 // p_new = z + beta p_old (own rows, written to pn); q = A p_new with p_new
 // formed on the fly at gathered columns; partial p_new . q.
-template <int D>
-__global__ void __launch_bounds__(CHUNK_ROWS) k_cg_spmv(ChunkCtx X, int parity) {
+// L lanes per row: L = 1 in the bulk (enough rows in flight), L = 2 / 4
+// when the active set is small (latency-bound tail: more loads in flight).
+template <int D, int L>
+__global__ void __launch_bounds__(CHUNK_ROWS * L) k_cg_spmv(ChunkCtx X, int parity) {
     __shared__ double red[64];
-    const Chunk ch = X.chunks[blockIdx.x];
+    if ((int)blockIdx.x >= *X.acount) return;
+    const Chunk ch = X.chunks[X.alist[blockIdx.x]];
     const CompInfo& C = X.comps[ch.comp];
     if (C.small || !X.st[ch.comp].active) return;
     const double* po = (parity ? X.p1 : X.p0) + C.vec_off;
@@ -266,17 +307,22 @@ __global__ void __launch_bounds__(CHUNK_ROWS) k_cg_spmv(ChunkCtx X, int parity) 
     const int R = (int)C.rows, NS = (int)C.nslots;
     const int* offs = X.slotoff + C.so_off;
     const double* val = X.stencil + C.mat_off;
+    const int lr = threadIdx.x / L, ln = threadIdx.x % L;
     double v[1] = {0.0};
-    if (threadIdx.x < ch.nrow) {
-        int row = ch.row0 + threadIdx.x;
-        int rb = rowbase_of(C, D, row);
-        double y = 0.0;
+    double y = 0.0;
+    const int row = ch.row0 + lr;
+    if (lr < ch.nrow) {
+        const int rb = rowbase_of(C, D, row);
         const double* vr = val + row;
 #pragma unroll 4
-        for (int t = 0; t < NS; ++t) {
+        for (int t = ln; t < NS; t += L) {
             int col = rb + __ldg(offs + t);
             y += __ldg(vr + (size_t)t * R) * (z[col] + beta * po[col]);
         }
+    }
+#pragma unroll
+    for (int o = L >> 1; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+    if (lr < ch.nrow && ln == 0) {
         double pr = z[row] + beta * po[row];
         pn[row] = pr;
         X.q[C.vec_off + row] = y;
@@ -292,7 +338,8 @@ __global__ void __launch_bounds__(CHUNK_ROWS) k_cg_spmv(ChunkCtx X, int parity) 
 
 __global__ void __launch_bounds__(CHUNK_ROWS) k_cg_update(ChunkCtx X, int parity) {
     __shared__ double red[64];
-    const Chunk ch = X.chunks[blockIdx.x];
+    if ((int)blockIdx.x >= *X.acount) return;
+    const Chunk ch = X.chunks[X.alist[blockIdx.x]];
     const CompInfo& C = X.comps[ch.comp];
     if (C.small || !X.st[ch.comp].active) return;
     const double alpha = X.st[ch.comp].alpha;
@@ -379,6 +426,7 @@ __global__ void k_expand(const CompInfo* __restrict__ comps, int ncomp,
 static ChunkCtx make_ctx(Handle* h, double rtol, int maxit) {
     ChunkCtx X;
     X.comps = h->d_comps; X.chunks = h->d_chunks; X.slotoff = h->d_slotoff;
+    X.alist = nullptr; X.acount = nullptr;
     X.stencil = h->d_stencil; X.rhs = h->d_rhs; X.dinv = h->d_dinv;
     X.x = h->d_x; X.r = h->d_r; X.z = h->d_z; X.q = h->d_q;
     X.p0 = h->d_p; X.p1 = h->d_q2;
@@ -429,31 +477,74 @@ int run_pcg(Handle* h, double rtol, int maxit) {
         k_cg_init<<<nch, CHUNK_ROWS, 0, h->stream>>>(X);
         SG_CUDA(cudaGetLastError());
         h->launches[1]++;
-        // capture GRAPH_ITERS iterations once, replay until all converged
-        cudaGraph_t graph;
-        cudaGraphExec_t exec;
-        SG_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-        for (int k = 0; k < GRAPH_ITERS; ++k) {
-            int par = k & 1;
-            if (h->d == 1) k_cg_spmv<1><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, par);
-            else if (h->d == 2) k_cg_spmv<2><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, par);
-            else k_cg_spmv<3><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, par);
-            k_cg_update<<<nch, CHUNK_ROWS, 0, h->stream>>>(X, par);
-        }
-        SG_CUDA(cudaStreamEndCapture(h->stream, &graph));
-        SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        // active chunk list: every chunk of a large component, plan order
+        std::vector<int> al;
+        for (int c : h->large_comps)
+            for (int i = 0; i < h->comps[c].nchunks; ++i) al.push_back((int)h->comps[c].chunk_off + i);
+        int ncur = (int)al.size();
+        SG_CUDA(cudaMemcpyAsync(h->d_alist, al.data(), sizeof(int) * al.size(), cudaMemcpyHostToDevice, h->stream));
+        SG_CUDA(cudaMemcpyAsync(h->d_active_count + 1, &ncur, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+        X.alist = h->d_alist;
+        X.acount = h->d_active_count + 1;
+        // capture GRAPH_ITERS iterations over `grid` chunks; replay until all
+        // converged; re-capture with a smaller grid whenever the active set
+        // (compacted on the device after every replay) halves
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        auto capture = [&](int grid) -> int {
+            if (exec) { cudaGraphExecDestroy(exec); exec = nullptr; }
+            if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
+            SG_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+            for (int k = 0; k < GRAPH_ITERS; ++k) {
+                int par = k & 1;
+                const int lanes = grid <= 2 * 148 ? 4 : (grid <= 6 * 148 ? 2 : 1);
+#define SPMV(DD, LL) k_cg_spmv<DD, LL><<<grid, CHUNK_ROWS * LL, 0, h->stream>>>(X, par)
+#define SPMV_L(DD) { if (lanes == 4) SPMV(DD, 4); else if (lanes == 2) SPMV(DD, 2); else SPMV(DD, 1); }
+                if (h->d == 1) SPMV_L(1)
+                else if (h->d == 2) SPMV_L(2)
+                else SPMV_L(3)
+#undef SPMV_L
+#undef SPMV
+                k_cg_update<<<grid, CHUNK_ROWS, 0, h->stream>>>(X, par);
+            }
+            k_cg_compact<<<1, 1024, 0, h->stream>>>(h->d_chunks, h->d_cg, h->d_alist, h->d_active_count + 1,
+                                                     h->d_active_count + 2);
+            SG_CUDA(cudaStreamEndCapture(h->stream, &graph));
+            SG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+            return SGIGA_OK;
+        };
+        int grid = ncur;
+        int st = capture(grid);
+        if (st) return st;
         int max_rounds = maxit / GRAPH_ITERS + 2;
+        const char* tr = getenv("SGIGA_PCG_TRACE");
+        const bool trace = tr && tr[0] == '1';
+        cudaEvent_t tev0 = nullptr, tev1 = nullptr;
+        if (trace) { cudaEventCreate(&tev0); cudaEventCreate(&tev1); cudaEventRecord(tev0, h->stream); }
         for (int round = 0; round < max_rounds; ++round) {
+            if (trace && (round & 63) == 0) {
+                cudaEventRecord(tev1, h->stream);
+                cudaEventSynchronize(tev1);
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, tev0, tev1);
+                fprintf(stderr, "pcg-trace it=%d ms=%.3f active_comps=%d grid=%d\n", round * GRAPH_ITERS, ms,
+                        round ? h->h_pinned_flag[0] : (int)h->large_comps.size(), grid);
+            }
             SG_CUDA(cudaGraphLaunch(exec, h->stream));
-            h->launches[1] += 2 * GRAPH_ITERS;
-            SG_CUDA(cudaMemcpyAsync(h->h_pinned_flag, h->d_active_count, sizeof(int),
+            h->launches[1] += 2 * GRAPH_ITERS + 1;
+            SG_CUDA(cudaMemcpyAsync(h->h_pinned_flag, h->d_active_count, 3 * sizeof(int),
                                     cudaMemcpyDeviceToHost, h->stream));
             SG_CUDA(cudaStreamSynchronize(h->stream));
-            if (*h->h_pinned_flag <= 0) break;
+            const int active_comps = h->h_pinned_flag[0], active_chunks = h->h_pinned_flag[2];
+            if (active_comps <= 0 || active_chunks <= 0) break;
+            if (2 * active_chunks <= grid) {
+                grid = active_chunks;
+                if ((st = capture(grid))) return st;
+            }
         }
         h->kstop(4);
-        cudaGraphExecDestroy(exec);
-        cudaGraphDestroy(graph);
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
         // the converged x of every component is in d_x regardless of parity
     }
     return SGIGA_OK;
