@@ -302,6 +302,11 @@ static int check_err(Handle* h) {
         SG_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
         return SGIGA_ERR_GEOMETRY;
     }
+    if (e & 8) {
+        set_error("small-path PCG: thread-block cluster launched with an unexpected shape");
+        SG_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
+        return SGIGA_ERR_CUDA;
+    }
     if (e & ERRF_SPAN) {
         set_error("quadrature node escaped its element");
         SG_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
@@ -539,6 +544,10 @@ int sgiga_solve(sgiga_handle* hh, double rtol, int32_t maxit, int32_t* iters_out
     SG_CUDA(cudaMemcpyAsync(rel.data(), h->d_relres, sizeof(double) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
     SG_CUDA(cudaStreamSynchronize(h->stream));
     SG_CUDA(cudaEventElapsedTime(&h->ms[1], h->ev[2], h->ev[3]));
+    {
+        int est = check_err(h);
+        if (est) return est;
+    }
     h->have_coefs = true;
     h->solved = true;
     int status = SGIGA_OK;

@@ -211,6 +211,7 @@ cudaError_t launch_basis_tables(Handle* h);
 cudaError_t launch_metric(Handle* h);
 cudaError_t launch_assembly(Handle* h);
 int run_pcg(Handle* h, double rtol, int maxit);
+int launch_pcg_cluster(Handle* h, double rtol, int maxit);
 cudaError_t launch_residual_check(Handle* h);
 cudaError_t launch_expand(Handle* h);
 cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, double* d_out,
