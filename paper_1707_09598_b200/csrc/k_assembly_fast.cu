@@ -21,11 +21,14 @@
 //     element; completed rows are flushed, mapping relative offsets to the
 //     stencil's storage slots (absolute or relative), zeros elsewhere.
 // Deterministic, no atomics; every stencil entry is written exactly once.
+#include <cstdio>
+#include <cstdlib>
+
 #include "handle.cuh"
 
 namespace sgiga {
 
-constexpr int FAST_THREADS = 320;   // 10 warps
+constexpr int FAST_THREADS = 352;   // 11 warps: 4*W^2+1 stage-2 items for p = 4 in one round
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     unsigned s = (unsigned)__cvta_generic_to_shared(dst);
@@ -75,7 +78,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
 k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tabs,
                 const Pencil* __restrict__ pencils, const double* __restrict__ vals,
                 const double* __restrict__ Gbuf, double* __restrict__ stencil,
-                double* __restrict__ rhs, double* __restrict__ dinv) {
+                double* __restrict__ rhs, double* __restrict__ dinv, long long* __restrict__ prof) {
     using F = FastCfg<D, P, Q>;
     constexpr int p = F::p, W = F::W;
     extern __shared__ double sm[];
@@ -160,11 +163,30 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const int64_t nq_s = (int64_t)Ts.nel * Q;
     const int64_t row_base = (D >= 2 ? (int64_t)(pc.ia - 1) * C.rs[ka] : 0) +
                              (D >= 3 ? (int64_t)(pc.ib - 1) * C.rs[kb] : 0);
+    // flush maps of the tile axes: storage slot (ca, cb) -> relative accumulator
+    // index oa*WB + ob (-1 if the column is outside the band / on the boundary)
+    // and its storage-slot stride part
+    __shared__ int flt_rel[WMAX * WMAX], flt_slot[WMAX * WMAX];
+    const int Ss = C.S[s], Sa = D >= 2 ? C.S[ka] : 1, Sb = D >= 3 ? C.S[kb] : 1, SAB = Sa * Sb;
+    const int absm_s = C.absm[s], n_s = C.n[s];
+    const int64_t ss_s = C.ss[s], rs_s = C.rs[s], rows_c = C.rows;
+    for (int cab = tid; cab < SAB; cab += FAST_THREADS) {
+        const int ca = cab / Sb, cb = cab % Sb;
+        auto rel = [&](int k, int ik, int sk) -> int {
+            const int j = C.absm[k] ? sk + 1 : ik + sk - p, o = j - ik;
+            return (j < 1 || j > C.n[k] - 2 || o < -p || o > p) ? -1 : o + p;
+        };
+        const int oa = D >= 2 ? rel(ka, pc.ia, ca) : 0, ob = D >= 3 ? rel(kb, pc.ib, cb) : 0;
+        flt_rel[cab] = (oa < 0 || ob < 0) ? -1 : oa * F::WB + ob;
+        flt_slot[cab] = (int)((D >= 2 ? (int64_t)ca * C.ss[ka] : 0) + (D >= 3 ? (int64_t)cb * C.ss[kb] : 0));
+    }
     int tsp[NPAIR];   // stream type of each (m, n) pair
 #pragma unroll
     for (int pr = 0; pr < NPAIR; ++pr) tsp[pr] = 2 * ((pr / D) == s) + ((pr % D) == s);
 
     int buf = 0;
+    const bool pr = prof != nullptr && blockIdx.x == 0 && tid == 0;   // phase profile
+    long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc = 0;
     load_plane((int64_t)e_first * Q, 0);
     for (int e = e_first; e <= e_last; ++e) {
         for (int idx = tid; idx < 2 * Q * P; idx += FAST_THREADS) {
@@ -172,6 +194,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             Bs[idx] = vals[Ts.val_off + (der ? nq_s * P : 0) + (int64_t)e * Q * P + rem];
         }
         for (int g = 0; g < Q; ++g) {
+            if (pr) tc = clock64();
             // issue the next plane, then wait for the current one
             const bool more = (g + 1 < Q) || (e < e_last);
             if (more) {
@@ -181,6 +204,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 cp_async_wait_all();
             }
             __syncthreads();
+            if (pr) { long long t = clock64(); tp[0] += t - tc; tc = t; }
             const double* Gw = sm + F::oGw + buf * F::nGw;
             // ---- stage 1: contract tile axis b ------------------------------
             if constexpr (D == 3) {
@@ -218,11 +242,13 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 }
                 __syncthreads();
             }
+            if (pr) { long long t = clock64(); tp[1] += t - tc; tc = t; }
             // ---- stage 2: contract tile axis a ------------------------------
             if constexpr (D >= 2) {
-                constexpr int NIT = NPAIR * F::WB * P;
-                for (int it = tid; it < NIT + 1; it += FAST_THREADS) {
-                    if (it == NIT) {   // load: SL2 = sum_xa SL1 phiA
+                // one pass: S2[ts][sa][sb] = sum over the pairs of stream type ts,
+                // window elements t with k = sa - t in [0, p], and their Q points
+                for (int it = tid; it < 4 * F::WAB + 1; it += FAST_THREADS) {
+                    if (it == 4 * F::WAB) {   // load: SL2 = sum_xa SL1 phiA
                         double acc = 0.0;
 #pragma unroll
                         for (int x = 0; x < F::NA; ++x)
@@ -230,44 +256,35 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                         S2[4 * F::WAB] = acc;
                         continue;
                     }
-                    const int t = it % P, sb = (it / P) % F::WB, pr = it / (P * F::WB);
-                    if (t < ta_lo || t >= ta_hi) continue;
-                    const int ta = 2 * ((pr / D) == ka) + ((pr % D) == ka);
-                    double acc[P];
-#pragma unroll
-                    for (int k = 0; k < P; ++k) acc[k] = 0.0;
-#pragma unroll
-                    for (int g2 = 0; g2 < Q; ++g2) {
-                        const int xa = t * Q + g2;
-                        const double sv = D == 3 ? S1[(pr * F::NA + xa) * W + sb]
-                                                 : Gw[sym_index(D, pr / D, pr % D) * F::NAP + xa];
-                        const double* tr = Ta + (ta * F::NA + xa) * P;
-#pragma unroll
-                        for (int k = 0; k < P; ++k) acc[k] += sv * tr[k];
-                    }
-                    double* out = P2 + ((pr * P + t) * P) * F::WB + sb;
-#pragma unroll
-                    for (int k = 0; k < P; ++k) out[k * F::WB] = acc[k];
-                }
-                __syncthreads();
-                // 2b: fixed-order sum over the pairs of a stream type and over t
-                for (int it = tid; it < 4 * F::WAB; it += FAST_THREADS) {
                     const int sab = it % F::WAB, ts = it / F::WAB;
                     const int sa = sab / F::WB, sb = sab % F::WB;
                     const int tl = max(ta_lo, sa - p), th = min(ta_hi - 1, sa);
-                    double acc = 0.0;
+                    double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
                     for (int pr = 0; pr < NPAIR; ++pr) {
                         if (tsp[pr] != ts) continue;
-                        for (int t = tl; t <= th; ++t) acc += P2[((pr * P + t) * P + (sa - t)) * F::WB + sb];
+                        const int ta = 2 * ((pr / D) == ka) + ((pr % D) == ka);
+                        for (int t = tl; t <= th; ++t) {
+                            const double* tr = Ta + (ta * F::NA + t * Q) * P + (sa - t);
+#pragma unroll
+                            for (int g2 = 0; g2 < Q; ++g2) {
+                                const int xa = t * Q + g2;
+                                const double sv = D == 3 ? S1[(pr * F::NA + xa) * W + sb]
+                                                         : Gw[sym_index(D, pr / D, pr % D) * F::NAP + xa];
+                                if (g2 & 1) acc1 += sv * tr[g2 * P];
+                                else acc0 += sv * tr[g2 * P];
+                            }
+                        }
                     }
-                    S2[it] = acc;
+                    S2[it] = acc0 + acc1;
                 }
+                if (pr) { long long t = clock64(); tp[2] += t - tc; tc = t; }
             } else {
                 if (tid < 4) S2[tid] = (tid == 3) ? Gw[0] : 0.0;
                 if (tid == 0) S2[4] = Gw[(F::NG - 1) * F::NB * F::NAP];
             }
             __syncthreads();
+            if (pr) { long long t = clock64(); tp[3] += t - tc; tc = t; }
             // ---- stage 3: rank-1 update of the alive rows of element e ------
             for (int it = tid; it < P * F::WAB; it += FAST_THREADS) {
                 const int sab = it % F::WAB, al = it / F::WAB;
@@ -289,34 +306,27 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 if (i >= r0 && i < r1) AccL[i % F::RING] += Bs[g * P + tid] * S2[4 * F::WAB];
             }
             buf ^= 1;
+            if (pr) { long long t = clock64(); tp[4] += t - tc; tc = t; tp[6] += 1; }
         }
         __syncthreads();
+        if (pr) tc = clock64();
         // ---- flush: row e completes with element e; the last element also
         // completes the trailing rows of the segment.  Every storage slot of
         // a flushed row is written (zeros where the relative offset is out
         // of the band or the column is on the boundary). ----------------------
         const int lo = (e == e_last) ? (e > r0 ? e : r0) : e;
         const int hi = (e == e_last) ? r1 : (e + 1 < r1 ? e + 1 : r1);
-        const int Ss = C.S[s], Sa = D >= 2 ? C.S[ka] : 1, Sb = D >= 3 ? C.S[kb] : 1;
         for (int i = (lo > r0 ? lo : r0); i < hi; ++i) {
-            const int64_t row = row_base + (int64_t)(i - 1) * C.rs[s];
+            const int64_t row = row_base + (int64_t)(i - 1) * rs_s;
             double* accr = Acc + ((i % F::RING) * W) * F::WAB;
-            // relative offset + p of storage slot sk on axis k for row index ik; -1 if none
-            auto rel_of = [&](int k, int ik, int sk) -> int {
-                const int j = C.absm[k] ? sk + 1 : ik + sk - p;
-                const int o = j - ik;
-                if (j < 1 || j > C.n[k] - 2 || o < -p || o > p) return -1;
-                return o + p;
-            };
-            for (int it = tid; it < Ss * Sa * Sb; it += FAST_THREADS) {
-                const int cb = it % Sb, ca = (it / Sb) % Sa, cs = it / (Sa * Sb);
-                const int os = rel_of(s, i, cs);
-                const int oa = D >= 2 ? rel_of(ka, pc.ia, ca) : 0;
-                const int ob = D >= 3 ? rel_of(kb, pc.ib, cb) : 0;
-                const double v = (os >= 0 && oa >= 0 && ob >= 0) ? accr[os * F::WAB + oa * F::WB + ob] : 0.0;
-                const int64_t slot = (int64_t)cs * C.ss[s] + (D >= 2 ? (int64_t)ca * C.ss[ka] : 0) +
-                                     (D >= 3 ? (int64_t)cb * C.ss[kb] : 0);
-                stencil[C.mat_off + slot * C.rows + row] = v;
+            double* dst = stencil + C.mat_off + row;
+            for (int it = tid; it < Ss * SAB; it += FAST_THREADS) {
+                const int cab = it % SAB, cs = it / SAB;
+                const int j = absm_s ? cs + 1 : i + cs - p, o = j - i;   // stream-axis column
+                const int oab = flt_rel[cab];
+                const bool ok = oab >= 0 && j >= 1 && j <= n_s - 2 && o >= -p && o <= p;
+                const double v = ok ? accr[(o + p) * F::WAB + oab] : 0.0;
+                dst[((int64_t)cs * ss_s + flt_slot[cab]) * rows_c] = v;
             }
             if (tid == 0) {
                 const int dsab = D >= 2 ? (p * F::WB + (D >= 3 ? p : 0)) : 0;
@@ -328,7 +338,10 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             if (tid == 0) AccL[i % F::RING] = 0.0;
             __syncthreads();
         }
+        if (pr) { tp[5] += clock64() - tc; tp[7] += 1; }
     }
+    if (pr)
+        for (int k = 0; k < 8; ++k) prof[k] = tp[k];
 }
 
 // dispatch: returns false when (d, p, q, mu) has no fast instantiation
@@ -351,9 +364,25 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     }
     *err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (*err != cudaSuccess) return true;
+    long long* prof = nullptr;
+    const char* pe = getenv("SGIGA_ASM_PROFILE");
+    if (pe && pe[0] == '1') {
+        cudaMalloc(&prof, 8 * sizeof(long long));
+        cudaMemsetAsync(prof, 0, 8 * sizeof(long long), h->stream);
+    }
     void* args[] = {(void*)&h->d_comps, (void*)&h->d_tabs, (void*)&h->d_pencils, (void*)&h->d_tabvals,
-                    (void*)&h->d_G, (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv};
+                    (void*)&h->d_G, (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv,
+                    (void*)&prof};
     *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(FAST_THREADS), args, smem, h->stream);
+    if (prof) {
+        long long t[8];
+        cudaMemcpy(t, prof, sizeof t, cudaMemcpyDeviceToHost);
+        const double n = t[6] > 0 ? (double)t[6] : 1.0;
+        fprintf(stderr, "asm-profile block0 planes=%lld elements=%lld cycles/plane: load-wait=%.0f stage1=%.0f "
+                "stage2a=%.0f stage2b=%.0f stage3=%.0f ; flush/element=%.0f\n", t[6], t[7], t[0] / n, t[1] / n,
+                t[2] / n, t[3] / n, t[4] / n, t[5] / (t[7] > 0 ? (double)t[7] : 1.0));
+        cudaFree(prof);
+    }
     h->launches[0] += 1;
     return true;
 }
