@@ -217,13 +217,40 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
             h->chunks.push_back(ch);
         }
     }
-    // assembly pencils: tile rows along ax[d-2], ax[d-3]; segments along the
-    // stream axis.  Short segments when the batch has few pencils (latency),
-    // long ones otherwise (the p-element halo of a segment is recomputed).
-    int64_t cross = 0;
-    for (const CompInfo& C : h->comps)
-        if (C.rows) cross += (d >= 2 ? C.m[C.ax[d - 2]] : 1) * (int64_t)(d >= 3 ? C.m[C.ax[d - 3]] : 1);
-    const int SEG = cross >= 8 * 148 ? 128 : (cross >= 2 * 148 ? 32 : 16);
+    // assembly pencils: tile rows along ax[d-2], ax[d-3]; segments of SEG
+    // rows along the stream axis.  A pencil walks its elements one quadrature
+    // plane at a time, so its cost is ~ planes (+ a fixed setup); a segment
+    // recomputes a p-element halo.  SEG minimises the estimated makespan
+    // max(longest pencil, total / resident CTAs); pencils are issued longest
+    // first (LPT), so the long ones start in the first wave.
+    auto seg_elems = [&](const CompInfo& C, int r0, int r1) {
+        const int nel_s = C.nel[C.ax[d - 1]];
+        const int ef = std::max(0, r0 - p), el = std::min(r1 - 1, nel_s - 1);
+        return std::max(0, el - ef + 1);
+    };
+    int nsm = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const double slots = 2.0 * nsm, setup = 2.0;   // 2 resident CTAs/SM; setup in elements
+    int SEG = 1 << 20;
+    if (const char* e = getenv("SGIGA_ASM_SEG")) SEG = std::max(1, atoi(e));
+    else {
+        double best = 1e300;
+        for (int cand : {1 << 20, 128, 64, 48, 32, 24, 16, 12, 8, 6, 4}) {
+            double tot = 0, mx = 0;
+            for (const CompInfo& C : h->comps) {
+                if (!C.rows) continue;
+                const double cross = (double)(d >= 2 ? C.m[C.ax[d - 2]] : 1) * (d >= 3 ? C.m[C.ax[d - 3]] : 1);
+                const int ms = C.m[C.ax[d - 1]];
+                for (int r0 = 1; r0 < 1 + ms; r0 += cand) {
+                    const double cost = seg_elems(C, r0, std::min(1 + ms, r0 + cand)) + setup;
+                    tot += cost * cross;
+                    mx = std::max(mx, cost);
+                }
+            }
+            const double span = std::max(mx, tot / slots);
+            if (span < best * 0.97) { best = span; SEG = cand; }
+        }
+    }
     for (int c = 0; c < D->n_comp; ++c) {
         const CompInfo& C = h->comps[c];
         if (!C.rows) continue;
@@ -239,10 +266,14 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
                     pc.ia = d >= 2 ? ia + 1 : 0;
                     pc.ib = d >= 3 ? ib + 1 : 0;
                     pc.r0 = 1 + sg * SEG;
-                    pc.r1 = std::min(1 + ms, 1 + (sg + 1) * SEG);
+                    pc.r1 = (int)std::min<int64_t>(1 + ms, 1 + (int64_t)(sg + 1) * SEG);
                     h->pencils.push_back(pc);
                 }
     }
+    std::stable_sort(h->pencils.begin(), h->pencils.end(), [&](const Pencil& x, const Pencil& y) {
+        return seg_elems(h->comps[x.comp], x.r0, x.r1) > seg_elems(h->comps[y.comp], y.r0, y.r1);
+    });
+    h->asm_seg = SEG;
     h->total_vec = vec; h->total_slots = mat; h->total_qp = nqp_tot; h->total_rows = rows_tot;
     h->total_dofs = dof;
     if (assembly_smem_bytes(h) > 227 * 1024) {

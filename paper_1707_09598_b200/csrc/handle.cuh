@@ -95,6 +95,7 @@ struct Handle {
     long long launches[3] = {0, 0, 0};
     std::vector<int> iters;
     bool force_generic_assembly = false;   // SGIGA_GENERIC_ASSEMBLY=1 (parity cross-check)
+    int asm_seg = 0;                       // stream-axis segment length of the pencils
 
     void kstart(int g) { cudaEventRecord(kev[2 * g], stream); kran[g] = true; }
     void kstop(int g) { cudaEventRecord(kev[2 * g + 1], stream); }
