@@ -192,10 +192,8 @@ def run_sgiga(args, cfg):
     out_d = torch.empty(npts, dtype=torch.float64, device=f"cuda:{local}")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")   # 256 MB > L2
 
-    def step():
-        batch.assemble()
-        batch.solve(rtol=args.rtol)
-        batch.combine_points_device(pts_d.data_ptr(), npts, out_d.data_ptr())
+    def step():   # assemble + solve + combine, one library call, one sync
+        batch.run_device(pts_d.data_ptr(), npts, out_d.data_ptr(), rtol=args.rtol)
 
     for _ in range(max(args.warmup, 3)):
         step()

@@ -155,6 +155,16 @@ int sgiga_set_coefficients(sgiga_handle* h, const double* full_coefs);
 int sgiga_combine_points(sgiga_handle* h, const double* pts, int64_t npts,
                          double* out, int32_t device);
 
+/* The whole plan in one call: assemble, solve, combine at npts points
+ * (device = 0 host / 1 device pointers, as sgiga_combine_points), all
+ * enqueued on the handle's stream with ONE synchronisation at the end.
+ * Replaces run_plan + evaluate_combined (scheduler.py:74-96,
+ * combination.py:209-236).  Errors are reported as by the three phase
+ * calls (the first failing phase wins); npts = 0 skips the combine.     */
+int sgiga_run(sgiga_handle* h, double rtol, int32_t maxit, const double* pts,
+              int64_t npts, double* out, int32_t device, int32_t* iters_out,
+              double* relres_out);
+
 /* Tensor grid variant: per-axis parameter arrays concatenated; vals has
  * prod(npts) entries (C order), grads (optional, may be NULL) prod*d.
  * comp = -1 combines the plan; comp >= 0 evaluates that component alone

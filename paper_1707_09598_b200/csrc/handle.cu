@@ -44,7 +44,9 @@ static void free_all(Handle* h) {
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    if (h->h_pinned_flag) cudaFreeHost(h->h_pinned_flag);
+    void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};
+    for (void* p : hptrs)
+        if (p) cudaFreeHost(p);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : h->kev)
@@ -324,10 +326,17 @@ static int upload_all(Handle* h) {
     return SGIGA_OK;
 }
 
+// device error flags: the copy is enqueued on the stream, decoded after the
+// caller's (single) synchronisation
+static int decode_err(Handle* h);
 static int check_err(Handle* h) {
-    int e = 0;
-    SG_CUDA(cudaMemcpyAsync(&e, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     SG_CUDA(cudaStreamSynchronize(h->stream));
+    return decode_err(h);
+}
+static int decode_err(Handle* h) {
+    const int e = *h->h_err;
+    *h->h_err = 0;
     if (e & ERRF_GEOMETRY) {
         set_error("geometry map is degenerate: det J <= 0 at a quadrature point");
         SG_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
@@ -427,6 +436,9 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_slotoff, h->slotoff.size());
 #undef A_
     if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned_flag), sizeof(int) * 4);
+    if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_err), sizeof(int));
+    if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_cg), sizeof(CgState) * std::max(1, h->ncomp));
+    if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_rel), sizeof(double) * std::max(1, h->ncomp));
     for (auto& ev : h->ev)
         if (ea == cudaSuccess) ea = cudaEventCreate(&ev);
     for (auto& ev : h->kev)
@@ -525,9 +537,9 @@ int sgiga_set_forcing_density(sgiga_handle* hh, const double* f) {
     return SGIGA_OK;
 }
 
-int sgiga_assemble(sgiga_handle* hh) {
-    Handle* h = reinterpret_cast<Handle*>(hh);
-    if (!h) return SGIGA_ERR_VALUE;
+// ---- the three phases, split into an enqueue part (async, on the
+// handle's stream) and a finish part (after one synchronisation) -----------
+static int assemble_enqueue(Handle* h) {
     if (h->forcing_id == SGIGA_FORCING_HOST && !h->density_ready) {
         set_error("host forcing: call sgiga_set_forcing_density first");
         return SGIGA_ERR_STATE;
@@ -544,6 +556,104 @@ int sgiga_assemble(sgiga_handle* hh) {
     SG_CUDA(launch_assembly(h));
     h->kstop(2);
     SG_CUDA(cudaEventRecord(h->ev[1], h->stream));
+    return SGIGA_OK;
+}
+
+static int solve_enqueue(Handle* h, double rtol, int32_t maxit) {
+    if (!(rtol > 0.0)) { set_error("rtol must be positive"); return SGIGA_ERR_VALUE; }
+    if (maxit < 1) maxit = 1000000;
+    h->launches[1] = 0;
+    SG_CUDA(cudaEventRecord(h->ev[2], h->stream));
+    SG_CUDA(cudaMemsetAsync(h->d_cg, 0, sizeof(CgState) * h->ncomp, h->stream));
+    int st = run_pcg(h, rtol, maxit);
+    if (st) return st;
+    h->kstart(5);
+    SG_CUDA(launch_residual_check(h));
+    SG_CUDA(launch_expand(h));
+    h->kstop(5);
+    SG_CUDA(cudaEventRecord(h->ev[3], h->stream));
+    SG_CUDA(cudaMemcpyAsync(h->h_cg, h->d_cg, sizeof(CgState) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaMemcpyAsync(h->h_rel, h->d_relres, sizeof(double) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
+    return SGIGA_OK;
+}
+
+// per-component convergence verdict (linsolve.py:49-53 acceptance)
+static int solve_finish(Handle* h, int32_t* iters_out, double* relres_out) {
+    SG_CUDA(cudaEventElapsedTime(&h->ms[1], h->ev[2], h->ev[3]));
+    h->have_coefs = true;
+    h->solved = true;
+    int status = SGIGA_OK;
+    char buf[256];
+    for (int c = 0; c < h->ncomp; ++c) {
+        const CompInfo& C = h->comps[c];
+        const CgState& cg = h->h_cg[c];
+        const double rel = h->h_rel[c];
+        h->iters[c] = C.rows ? cg.it : 0;
+        if (iters_out) iters_out[c] = h->iters[c];
+        if (relres_out) relres_out[c] = C.rows ? rel : 0.0;
+        if (!C.rows || cg.bb == 0.0) continue;
+        if (!std::isfinite(rel)) {
+            snprintf(buf, sizeof buf, "component %d: solve produced non-finite values", c);
+            set_error(buf);
+            status = SGIGA_ERR_SOLVE;
+        } else if (!cg.conv) {
+            snprintf(buf, sizeof buf, "component %d: PCG did not converge in %d iterations", c, cg.it);
+            set_error(buf);
+            status = SGIGA_ERR_SOLVE;
+        } else if (rel > 1e-10) {   // linsolve.py:49-53
+            snprintf(buf, sizeof buf, "component %d: relative residual %.3e exceeds tol 1.0e-10", c, rel);
+            set_error(buf);
+            status = SGIGA_ERR_SOLVE;
+        }
+    }
+    return status;
+}
+
+static int ensure_scratch(double** buf, size_t* cap, size_t n) {
+    if (*cap >= n && *buf) return SGIGA_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    SG_CUDA(cudaMalloc(reinterpret_cast<void**>(buf), std::max<size_t>(n, 1) * sizeof(double)));
+    *cap = n;
+    return SGIGA_OK;
+}
+
+static thread_local double* s_pts = nullptr;
+static thread_local size_t s_pts_cap = 0;
+static thread_local double* s_out = nullptr;
+static thread_local size_t s_out_cap = 0;
+
+static int combine_enqueue(Handle* h, const double* pts, int64_t npts, double* out, int32_t device) {
+    h->launches[2] = 0;
+    SG_CUDA(cudaEventRecord(h->ev[4], h->stream));
+    const double* dp = pts;
+    double* dout = out;
+    int st;
+    int per_comp = device < 0;       // device = -1 / -2: per-component values (host / device)
+    int dev_ptrs = (device == 1 || device == -2);
+    size_t nout = per_comp ? (size_t)npts * h->ncomp : (size_t)npts;
+    if (!dev_ptrs) {
+        if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
+        if ((st = ensure_scratch(&s_out, &s_out_cap, nout))) return st;
+        SG_CUDA(cudaMemcpyAsync(s_pts, pts, sizeof(double) * npts * h->d, cudaMemcpyHostToDevice, h->stream));
+        dp = s_pts;
+        dout = s_out;
+    }
+    h->kstart(6);
+    SG_CUDA(launch_combine_points(h, dp, npts, dout, per_comp));
+    h->kstop(6);
+    if (!dev_ptrs)
+        SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaEventRecord(h->ev[5], h->stream));
+    return SGIGA_OK;
+}
+
+int sgiga_assemble(sgiga_handle* hh) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h) return SGIGA_ERR_VALUE;
+    int st = assemble_enqueue(h);
+    if (st) return st;
     st = check_err(h);
     if (st) return st;
     SG_CUDA(cudaEventElapsedTime(&h->ms[0], h->ev[0], h->ev[1]));
@@ -557,53 +667,32 @@ int sgiga_solve(sgiga_handle* hh, double rtol, int32_t maxit, int32_t* iters_out
     Handle* h = reinterpret_cast<Handle*>(hh);
     if (!h) return SGIGA_ERR_VALUE;
     if (!h->assembled) { set_error("sgiga_solve before sgiga_assemble"); return SGIGA_ERR_STATE; }
-    if (!(rtol > 0.0)) { set_error("rtol must be positive"); return SGIGA_ERR_VALUE; }
-    if (maxit < 1) maxit = 1000000;
-    h->launches[1] = 0;
-    SG_CUDA(cudaEventRecord(h->ev[2], h->stream));
-    SG_CUDA(cudaMemsetAsync(h->d_cg, 0, sizeof(CgState) * h->ncomp, h->stream));
-    int st = run_pcg(h, rtol, maxit);
+    int st = solve_enqueue(h, rtol, maxit);
     if (st) return st;
-    h->kstart(5);
-    SG_CUDA(launch_residual_check(h));
-    SG_CUDA(launch_expand(h));
-    h->kstop(5);
-    SG_CUDA(cudaEventRecord(h->ev[3], h->stream));
-    std::vector<CgState> cg(h->ncomp);
-    std::vector<double> rel(h->ncomp);
-    SG_CUDA(cudaMemcpyAsync(cg.data(), h->d_cg, sizeof(CgState) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
-    SG_CUDA(cudaMemcpyAsync(rel.data(), h->d_relres, sizeof(double) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
-    SG_CUDA(cudaStreamSynchronize(h->stream));
-    SG_CUDA(cudaEventElapsedTime(&h->ms[1], h->ev[2], h->ev[3]));
-    {
-        int est = check_err(h);
-        if (est) return est;
-    }
-    h->have_coefs = true;
-    h->solved = true;
-    int status = SGIGA_OK;
-    char buf[256];
-    for (int c = 0; c < h->ncomp; ++c) {
-        const CompInfo& C = h->comps[c];
-        h->iters[c] = C.rows ? cg[c].it : 0;
-        if (iters_out) iters_out[c] = h->iters[c];
-        if (relres_out) relres_out[c] = C.rows ? rel[c] : 0.0;
-        if (!C.rows || cg[c].bb == 0.0) continue;
-        if (!std::isfinite(rel[c])) {
-            snprintf(buf, sizeof buf, "component %d: solve produced non-finite values", c);
-            set_error(buf);
-            status = SGIGA_ERR_SOLVE;
-        } else if (!cg[c].conv) {
-            snprintf(buf, sizeof buf, "component %d: PCG did not converge in %d iterations", c, cg[c].it);
-            set_error(buf);
-            status = SGIGA_ERR_SOLVE;
-        } else if (rel[c] > 1e-10) {   // linsolve.py:49-53
-            snprintf(buf, sizeof buf, "component %d: relative residual %.3e exceeds tol 1.0e-10", c, rel[c]);
-            set_error(buf);
-            status = SGIGA_ERR_SOLVE;
-        }
-    }
-    return status;
+    st = check_err(h);   // synchronises: h_cg / h_rel are valid after it
+    if (st) return st;
+    return solve_finish(h, iters_out, relres_out);
+}
+
+int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, int64_t npts,
+              double* out, int32_t device, int32_t* iters_out, double* relres_out) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || npts < 0 || (npts > 0 && (!pts || !out))) { set_error("null argument"); return SGIGA_ERR_VALUE; }
+    if (device < 0) { set_error("sgiga_run: per-component output is not supported"); return SGIGA_ERR_VALUE; }
+    int st = assemble_enqueue(h);
+    if (st) return st;
+    st = solve_enqueue(h, rtol, maxit);
+    if (st) return st;
+    if (npts > 0 && (st = combine_enqueue(h, pts, npts, out, device))) return st;
+    SG_CUDA(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    SG_CUDA(cudaStreamSynchronize(h->stream));   // the one synchronisation of the call
+    st = decode_err(h);
+    if (st) return st;
+    SG_CUDA(cudaEventElapsedTime(&h->ms[0], h->ev[0], h->ev[1]));
+    h->assembled = true;
+    st = solve_finish(h, iters_out, relres_out);
+    if (npts > 0) SG_CUDA(cudaEventElapsedTime(&h->ms[2], h->ev[4], h->ev[5]));
+    return st;
 }
 
 int sgiga_iterations(sgiga_handle* hh, int32_t* iters) {
@@ -633,48 +722,14 @@ int sgiga_set_coefficients(sgiga_handle* hh, const double* full) {
     return SGIGA_OK;
 }
 
-static int ensure_scratch(double** buf, size_t* cap, size_t n) {
-    if (*cap >= n && *buf) return SGIGA_OK;
-    if (*buf) cudaFree(*buf);
-    *buf = nullptr;
-    *cap = 0;
-    SG_CUDA(cudaMalloc(reinterpret_cast<void**>(buf), std::max<size_t>(n, 1) * sizeof(double)));
-    *cap = n;
-    return SGIGA_OK;
-}
-
-static thread_local double* s_pts = nullptr;
-static thread_local size_t s_pts_cap = 0;
-static thread_local double* s_out = nullptr;
-static thread_local size_t s_out_cap = 0;
-
 int sgiga_combine_points(sgiga_handle* hh, const double* pts, int64_t npts, double* out,
                          int32_t device) {
     Handle* h = reinterpret_cast<Handle*>(hh);
     if (!h || npts < 0) return SGIGA_ERR_VALUE;
     if (!h->have_coefs) { set_error("combine before solve"); return SGIGA_ERR_STATE; }
     if (npts == 0) return SGIGA_OK;
-    h->launches[2] = 0;
-    SG_CUDA(cudaEventRecord(h->ev[4], h->stream));
-    const double* dp = pts;
-    double* dout = out;
-    int st;
-    int per_comp = device < 0;       // device = -1 / -2: per-component values (host / device)
-    int dev_ptrs = (device == 1 || device == -2);
-    size_t nout = per_comp ? (size_t)npts * h->ncomp : (size_t)npts;
-    if (!dev_ptrs) {
-        if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
-        if ((st = ensure_scratch(&s_out, &s_out_cap, nout))) return st;
-        SG_CUDA(cudaMemcpyAsync(s_pts, pts, sizeof(double) * npts * h->d, cudaMemcpyHostToDevice, h->stream));
-        dp = s_pts;
-        dout = s_out;
-    }
-    h->kstart(6);
-    SG_CUDA(launch_combine_points(h, dp, npts, dout, per_comp));
-    h->kstop(6);
-    if (!dev_ptrs)
-        SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream));
-    SG_CUDA(cudaEventRecord(h->ev[5], h->stream));
+    int st = combine_enqueue(h, pts, npts, out, device);
+    if (st) return st;
     SG_CUDA(cudaStreamSynchronize(h->stream));
     SG_CUDA(cudaEventElapsedTime(&h->ms[2], h->ev[4], h->ev[5]));
     return SGIGA_OK;

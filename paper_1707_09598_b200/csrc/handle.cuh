@@ -83,6 +83,9 @@ struct Handle {
     int* d_alist = nullptr;      // compacted active chunk list (large-path PCG)
     double* d_relres = nullptr;
     int* h_pinned_flag = nullptr;  // pinned host mirror of the active count
+    int* h_err = nullptr;          // pinned mirrors read after the one sync of a call
+    CgState* h_cg = nullptr;
+    double* h_rel = nullptr;
 
     // state
     bool tables_ready = false, density_ready = false, assembled = false, solved = false,

@@ -135,7 +135,7 @@ class Batch:
         _lib.check(self.lib.sgiga_upload(self.h, ct.byref(self.desc)))
 
     # ---- phases -------------------------------------------------------------
-    def assemble(self):
+    def _host_forcing_density(self):
         if self.spec.forcing_id == _lib.FORCING_HOST:
             x = np.empty((self.total_qp, self.spec.d))
             _lib.check(self.lib.sgiga_quad_points_physical(self.h, _lib.ptr(x, ct.c_double)))
@@ -145,6 +145,9 @@ class Batch:
             if f.shape != (self.total_qp,):
                 raise ValueError(f"forcing returned shape {f.shape} for {self.total_qp} points")
             _lib.check(self.lib.sgiga_set_forcing_density(self.h, _lib.ptr(f, ct.c_double)))
+
+    def assemble(self):
+        self._host_forcing_density()
         _lib.check(self.lib.sgiga_assemble(self.h))
 
     def solve(self, rtol: float = 1e-13, maxit: int = 0):
@@ -155,6 +158,40 @@ class Batch:
         self.iters, self.relres = it, rr
         _lib.check(code)
         return it, rr
+
+    def run(self, pts: np.ndarray | None = None, rtol: float = 1e-13, maxit: int = 0):
+        """assemble + solve + combine at ``pts`` in ONE library call (one
+        stream synchronisation): run_plan + evaluate_combined
+        (scheduler.py:74-96, combination.py:209-236).  Returns the combined
+        values (empty when ``pts`` is None)."""
+        self._host_forcing_density()
+        n = self.n_comp
+        it = np.zeros(n, dtype=np.int32)
+        rr = np.zeros(n, dtype=np.float64)
+        if pts is None:
+            pts = np.zeros((0, self.spec.d))
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        if pts.ndim != 2 or pts.shape[1] != self.spec.d:
+            raise ValueError(f"points must have shape (n, {self.spec.d})")
+        if pts.size and (pts.min() < 0.0 or pts.max() > 1.0):
+            raise ValueError("evaluation points must lie in [0, 1]^d")
+        out = np.empty(pts.shape[0])
+        code = self.lib.sgiga_run(self.h, float(rtol), int(maxit), pts.ctypes.data, pts.shape[0],
+                                  out.ctypes.data, 0, _lib.ptr(it, ct.c_int32), _lib.ptr(rr, ct.c_double))
+        self.iters, self.relres = it, rr
+        _lib.check(code)
+        return out
+
+    def run_device(self, pts_ptr: int, npts: int, out_ptr: int, rtol: float = 1e-13, maxit: int = 0):
+        """As run(), with the points and the output resident in HBM."""
+        self._host_forcing_density()
+        n = self.n_comp
+        it = np.zeros(n, dtype=np.int32)
+        rr = np.zeros(n, dtype=np.float64)
+        code = self.lib.sgiga_run(self.h, float(rtol), int(maxit), pts_ptr, int(npts), out_ptr, 1,
+                                  _lib.ptr(it, ct.c_int32), _lib.ptr(rr, ct.c_double))
+        self.iters, self.relres = it, rr
+        _lib.check(code)
 
     def coefficients(self) -> np.ndarray:
         out = np.empty(self.total_dofs)

@@ -158,9 +158,7 @@ class PlanSession:
     def run(self, points) -> np.ndarray:
         b = self.batch
         b.upload()
-        b.assemble()
-        b.solve(self.rtol)
-        return b.combine_points(points)
+        return b.run(points, self.rtol)
 
     def close(self):
         self.batch.close()

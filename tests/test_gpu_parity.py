@@ -246,6 +246,42 @@ def test_invalid_geometry_raises():
         run_plan(CombinationPlan(2, (((1, 1), 1),)), prob)
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_single_call_run_matches_phase_calls(name):
+    """sgiga_run (one sync) == assemble + solve + combine_points, bitwise."""
+    cfg = configs.get_config(name)
+    pts = cfg.points(2000)
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    b = Batch(spec)
+    try:
+        b.assemble()
+        it0, rr0 = b.solve(rtol=1e-13)
+        v0 = b.combine_points(pts)
+        c0 = b.coefficients()
+        for _ in range(2):
+            v1 = b.run(pts, rtol=1e-13)
+            assert np.array_equal(v0, v1)
+            assert np.array_equal(it0, b.iters) and np.array_equal(rr0, b.relres)
+            assert np.array_equal(c0, b.coefficients())
+        assert b.run(None).shape == (0,)
+    finally:
+        b.close()
+
+
+def test_single_call_run_reports_geometry_error():
+    sq = unit_hypercube(2)
+    pts = sq.control_points.copy()
+    pts[0, 0], pts[1, 0] = pts[1, 0].copy(), pts[0, 0].copy()
+    bad = NurbsPatch(sq.knotvectors, pts, sq.weights)
+    prob = A.BenchmarkProblem("bad", bad, A.constant_one, 2, 1)
+    b = Batch(make_spec((((1, 1), 1),), prob, 3))
+    try:
+        with pytest.raises(InvalidGeometryError):
+            b.run(np.full((4, 2), 0.5))
+    finally:
+        b.close()
+
+
 def test_missing_component_keyerror():
     prob = A.polynomial_cube_problem(2)
     plan = combination_coefficients(2, 1)
