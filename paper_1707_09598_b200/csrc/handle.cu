@@ -41,7 +41,7 @@ static void free_all(Handle* h) {
                     h->d_qw, h->d_geob, h->d_geofirst, h->d_geo_knots, h->d_geo_hw, h->d_G,
                     h->d_hostf, h->d_xphys, h->d_stencil, h->d_rhs, h->d_dinv, h->d_x,
                     h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
-                    h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist};
+                    h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};

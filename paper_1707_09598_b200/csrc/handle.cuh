@@ -82,6 +82,9 @@ struct Handle {
     int* d_active_count = nullptr;
     int* d_alist = nullptr;      // compacted active chunk list (large-path PCG)
     double* d_relres = nullptr;
+    int* d_cperm = nullptr;        // combine: cell-order permutation of the points
+    size_t cperm_cap = 0;
+    int* d_chist = nullptr;        // combine: cell histogram / cursors
     int* h_pinned_flag = nullptr;  // pinned host mirror of the active count
     int* h_err = nullptr;          // pinned mirrors read after the one sync of a call
     CgState* h_cg = nullptr;

@@ -14,6 +14,8 @@
 // between consecutive components.  The span of a uniform dyadic knot vector
 // is closed-form (floor(xi*2^l), exact), graded ones use a binary search
 // with the reference's side rule (splines.py:149-169, 255-257).
+#include <cstdlib>
+
 #include "forcing.cuh"
 #include "handle.cuh"
 
@@ -155,6 +157,139 @@ k_combine_points(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* _
     combine_at<D, P, false>(comps, 0, ncomp, true, tabs, knots, mu, coef, xi, acc, g,
                             per_component ? out + t : nullptr, npts);
     if (!per_component) out[t] = acc;
+}
+
+// Scattered-point combine, tiled: a CTA owns NPT points and splits the work
+// three ways so every thread has independent work (one thread per point
+// leaves an SM with a handful of warps, latency-bound):
+//   A. one item per (basis table = (axis, level), point): span + Cox-de Boor
+//      values into shared memory (pt innermost: conflict-free) -- each
+//      table is evaluated once per point, not once per component;
+//   B. one item per (component, point): the P^D tensor contraction with the
+//      component's coefficient window -> V[c][pt];
+//   C. one thread per point: the plan-order sum acc = c0 v0, acc += c v
+//      (combination.py:227-233) -- the same operations, in the same order,
+//      as combine_at, so the result is bitwise the per-thread kernel's.
+constexpr int CP_THREADS = 256;
+
+template <int D, int P>
+__global__ void __launch_bounds__(CP_THREADS)
+k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
+                       int ntab, const double* __restrict__ knots, int mu, const double* __restrict__ coef,
+                       const double* __restrict__ pts, int64_t npts, const int* __restrict__ perm,
+                       double* __restrict__ out, int per_component, int npt) {
+    extern __shared__ double csm[];
+    double* Bt = csm;                                   // [ntab][P][npt]
+    double* V = Bt + (size_t)ntab * P * npt;            // [ncomp][npt]
+    int* first = reinterpret_cast<int*>(V + (per_component ? 0 : (size_t)ncomp * npt));   // [ntab][npt]
+    int* gidx = first + (size_t)ntab * npt;             // [npt] point index (cell order -> input order)
+    const int tid = threadIdx.x;
+    const int64_t p0 = (int64_t)blockIdx.x * npt;
+    const int nloc = npts - p0 < npt ? (int)(npts - p0) : npt;
+    for (int pt = tid; pt < nloc; pt += CP_THREADS) gidx[pt] = perm ? perm[p0 + pt] : (int)(p0 + pt);
+    __syncthreads();
+    for (int it = tid; it < ntab * npt; it += CP_THREADS) {
+        const int pt = it % npt, t = it / npt;
+        if (pt >= nloc) continue;
+        const TabInfo T = tabs[t];
+        const double xi = pts[(int64_t)gidx[pt] * D + T.axis];
+        double bv[P];
+        first[t * npt + pt] = axis_basis<P, false>(T, knots, mu, xi, bv, nullptr);
+#pragma unroll
+        for (int j = 0; j < P; ++j) Bt[(t * P + j) * npt + pt] = bv[j];
+    }
+    __syncthreads();
+    for (int it = tid; it < ncomp * npt; it += CP_THREADS) {
+        const int pt = it % npt, c = it / npt;
+        if (pt >= nloc) continue;
+        const CompInfo& C = comps[c];
+        double Bv[D][P];
+        int fs[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const int t = C.tab[k];
+            fs[k] = first[t * npt + pt];
+#pragma unroll
+            for (int j = 0; j < P; ++j) Bv[k][j] = Bt[(t * P + j) * npt + pt];
+        }
+        double v, g[D];
+        eval_component<D, P, false>(C, coef, fs, Bv, Bv, v, g);
+        if (per_component) out[(int64_t)c * npts + gidx[pt]] = v;
+        else V[c * npt + pt] = v;
+    }
+    if (per_component) return;
+    __syncthreads();
+    for (int pt = tid; pt < nloc; pt += CP_THREADS) {
+        double acc = 0.0;
+        for (int c = 0; c < ncomp; ++c) {
+            const double cv = (double)comps[c].coef * V[c * npt + pt];
+            acc = (c == 0) ? cv : __dadd_rn(acc, cv);
+        }
+        out[gidx[pt]] = acc;
+    }
+}
+
+// ---- cell sort of the points (locality of the coefficient windows) --------
+// key = row-major cell index on a 2^bits-per-axis grid; a counting sort
+// gives a permutation of the points in cell order.  The order inside a cell
+// depends on atomic timing, but every point's value is computed by the same
+// operations wherever it lands, so the output stays bitwise deterministic.
+constexpr int SORT_BITS = 12;   // 4096 cells
+template <int D>
+__device__ __forceinline__ int cell_key(const double* x) {
+    constexpr int b = SORT_BITS / D, n = 1 << b;
+    int key = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        int c = (int)(x[k] * (double)n);
+        c = c < 0 ? 0 : (c > n - 1 ? n - 1 : c);
+        key = key * n + c;
+    }
+    return key;
+}
+
+template <int D>
+__global__ void k_cell_hist(const double* __restrict__ pts, int64_t npts, int* __restrict__ hist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < npts) atomicAdd(&hist[cell_key<D>(pts + i * D)], 1);
+}
+
+// exclusive scan of the 4096 bin counts, one CTA of 1024 threads
+__global__ void __launch_bounds__(1024) k_cell_scan(int* __restrict__ hist) {
+    __shared__ int ws[32];
+    constexpr int PER = (1 << SORT_BITS) / 1024;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int v[PER], s = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) { v[j] = hist[tid * PER + j]; s += v[j]; }
+    int inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int w = ws[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        ws[lane] = w;
+    }
+    __syncthreads();
+    int run = inc - s + (wid ? ws[wid - 1] : 0);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) { hist[tid * PER + j] = run; run += v[j]; }
+}
+
+template <int D>
+__global__ void k_cell_scatter(const double* __restrict__ pts, int64_t npts, int* __restrict__ cursor,
+                               int* __restrict__ perm) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < npts) perm[atomicAdd(&cursor[cell_key<D>(pts + i * D)], 1)] = (int)i;
 }
 
 template <int D, int P>
@@ -364,13 +499,64 @@ __global__ void k_sum_partials(const double* __restrict__ partials, int64_t nblo
 cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, double* d_out,
                                   int per_component) {
     if (npts == 0) return cudaSuccess;
-    unsigned blocks = (unsigned)((npts + 127) / 128);
+    const int ntab = (int)h->tabs.size(), P = h->p + 1;
+    // points per CTA: as many as fit ~100 KB of shared memory (2 CTAs/SM), <= 64
+    auto smem_of = [&](int n) {
+        return (size_t)n * (ntab * P * sizeof(double) + ntab * sizeof(int) +
+                            (per_component ? 0 : (size_t)h->ncomp * sizeof(double)));
+    };
+    int npt = 64;
+    while (npt > 1 && smem_of(npt) > 100 * 1024) npt >>= 1;
+    const char* ev = getenv("SGIGA_COMBINE_PERTHREAD");
+    if (smem_of(npt) > 200 * 1024 || (ev && ev[0] == '1')) {   // huge plans: one thread per point
+        unsigned blocks = (unsigned)((npts + 127) / 128);
 #define LAUNCH_CP(DD, PP)                                                                     \
     k_combine_points<DD, PP><<<blocks, 128, 0, h->stream>>>(h->d_comps, h->ncomp, h->d_tabs,   \
                                                             h->d_knots, h->mu, h->d_coef,     \
                                                             d_pts, npts, d_out, per_component)
-    SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CP)
+        SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CP)
 #undef LAUNCH_CP
+        h->launches[2]++;
+        return cudaGetLastError();
+    }
+    const size_t smem = smem_of(npt) + sizeof(int) * npt;
+    const unsigned blocks = (unsigned)((npts + npt - 1) / npt);
+    // cell sort (enough points per cell to matter, int32 indices)
+    const char* ns = getenv("SGIGA_COMBINE_NOSORT");
+    const int* perm = nullptr;
+    if (npts >= 2048 && npts < (int64_t)1 << 31 && !(ns && ns[0] == '1')) {
+        cudaError_t e;
+        if ((size_t)npts > h->cperm_cap) {
+            if (h->d_cperm) cudaFree(h->d_cperm);
+            h->d_cperm = nullptr;
+            h->cperm_cap = 0;
+            if ((e = cudaMalloc(&h->d_cperm, sizeof(int) * npts)) != cudaSuccess) return e;
+            h->cperm_cap = (size_t)npts;
+        }
+        if (!h->d_chist && (e = cudaMalloc(&h->d_chist, sizeof(int) << SORT_BITS)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(h->d_chist, 0, sizeof(int) << SORT_BITS, h->stream)) != cudaSuccess) return e;
+        const unsigned sb = (unsigned)((npts + 255) / 256);
+        if (h->d == 1) k_cell_hist<1><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist);
+        else if (h->d == 2) k_cell_hist<2><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist);
+        else k_cell_hist<3><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist);
+        k_cell_scan<<<1, 1024, 0, h->stream>>>(h->d_chist);
+        if (h->d == 1) k_cell_scatter<1><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist, h->d_cperm);
+        else if (h->d == 2) k_cell_scatter<2><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist, h->d_cperm);
+        else k_cell_scatter<3><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist, h->d_cperm);
+        h->launches[2] += 3;
+        perm = h->d_cperm;
+    }
+#define LAUNCH_CPT(DD, PP)                                                                          \
+    {                                                                                               \
+        cudaError_t e_ = cudaFuncSetAttribute(k_combine_points_tiled<DD, PP>,                       \
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e_ != cudaSuccess) return e_;                                                           \
+        k_combine_points_tiled<DD, PP><<<blocks, CP_THREADS, smem, h->stream>>>(                    \
+            h->d_comps, h->ncomp, h->d_tabs, ntab, h->d_knots, h->mu, h->d_coef, d_pts, npts, perm,  \
+            d_out, per_component, npt);                                                             \
+    }
+    SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CPT)
+#undef LAUNCH_CPT
     h->launches[2]++;
     return cudaGetLastError();
 }

@@ -268,6 +268,28 @@ def test_single_call_run_matches_phase_calls(name):
         b.close()
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_tiled_combine_matches_per_thread_kernel(name, monkeypatch):
+    """k_combine_points_tiled == the one-thread-per-point kernel, bitwise,
+    for the plan sum and the per-component values (ragged last tile)."""
+    cfg = configs.get_config(name)
+    pts = cfg.points(3001)
+    spec, b = _batch(cfg)
+    try:
+        b.solve(rtol=1e-13)
+        tiled = b.combine_points(pts), b.combine_points(pts, per_component=True)
+        monkeypatch.setenv("SGIGA_COMBINE_NOSORT", "1")        # tiled, input order
+        unsorted = b.combine_points(pts), b.combine_points(pts, per_component=True)
+        assert np.array_equal(tiled[0], unsorted[0])
+        assert np.array_equal(tiled[1], unsorted[1])
+        monkeypatch.setenv("SGIGA_COMBINE_PERTHREAD", "1")
+        ref = b.combine_points(pts), b.combine_points(pts, per_component=True)
+        assert np.array_equal(tiled[0], ref[0])
+        assert np.array_equal(tiled[1], ref[1])
+    finally:
+        b.close()
+
+
 def test_single_call_run_reports_geometry_error():
     sq = unit_hypercube(2)
     pts = sq.control_points.copy()
