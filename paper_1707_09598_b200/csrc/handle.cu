@@ -474,16 +474,34 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
     if (st) return st;
     if (tmp.total_slots != h->total_slots || tmp.total_qp != h->total_qp ||
         tmp.ncomp != h->ncomp || tmp.tabs.size() != h->tabs.size() || tmp.d != h->d ||
-        tmp.p != h->p || tmp.q != h->q) {
+        tmp.p != h->p || tmp.q != h->q || tmp.pencils.size() != h->pencils.size() ||
+        tmp.chunks.size() != h->chunks.size() || tmp.small_comps.size() != h->small_comps.size() ||
+        tmp.large_comps.size() != h->large_comps.size() || tmp.slotoff.size() != h->slotoff.size()) {
         set_error("sgiga_upload: descriptor shape differs from the handle's");
         return SGIGA_ERR_VALUE;
     }
+    // an identical descriptor keeps the captured whole-run graph
+    auto same_bytes = [](const auto& a, const auto& b) {
+        return a.size() == b.size() && (a.empty() || !memcmp(a.data(), b.data(), sizeof(a[0]) * a.size()));
+    };
+    const bool identical = same_bytes(tmp.levels, h->levels) && same_bytes(tmp.coefs, h->coefs) &&
+                           same_bytes(tmp.gauss_n, h->gauss_n) && same_bytes(tmp.gauss_w, h->gauss_w) &&
+                           !memcmp(&tmp.geo, &h->geo, sizeof(GeoInfo)) && same_bytes(tmp.geo_knots, h->geo_knots) &&
+                           same_bytes(tmp.geo_hw, h->geo_hw) && same_bytes(tmp.bp_host, h->bp_host) &&
+                           same_bytes(tmp.comps, h->comps) && same_bytes(tmp.tabs, h->tabs) &&
+                           same_bytes(tmp.slotoff, h->slotoff) && same_bytes(tmp.pencils, h->pencils) &&
+                           same_bytes(tmp.chunks, h->chunks) && same_bytes(tmp.small_comps, h->small_comps) &&
+                           same_bytes(tmp.large_comps, h->large_comps) && tmp.forcing_id == h->forcing_id;
+    if (!identical) h->drop_run_graph();
     h->levels.swap(tmp.levels); h->coefs.swap(tmp.coefs);
     h->gauss_n.swap(tmp.gauss_n); h->gauss_w.swap(tmp.gauss_w);
     h->geo = tmp.geo; h->geo_knots.swap(tmp.geo_knots); h->geo_hw.swap(tmp.geo_hw);
     h->bp_host.swap(tmp.bp_host); h->comps.swap(tmp.comps); h->tabs.swap(tmp.tabs);
     h->slotoff.swap(tmp.slotoff);
+    h->pencils.swap(tmp.pencils); h->chunks.swap(tmp.chunks);
+    h->small_comps.swap(tmp.small_comps); h->large_comps.swap(tmp.large_comps);
     h->forcing_id = tmp.forcing_id;
+    if (identical) return SGIGA_OK;   // device copies are already these bytes
     return upload_all(h);
 }
 
@@ -545,7 +563,7 @@ static int assemble_enqueue(Handle* h) {
         return SGIGA_ERR_STATE;
     }
     h->launches[0] = 0;
-    SG_CUDA(cudaEventRecord(h->ev[0], h->stream));
+    SG_CUDA(h->rec(h->ev[0]));
     h->tables_ready = false;   // kernel 1 is part of every assembly pass
     int st = ensure_tables(h);
     if (st) return st;
@@ -555,7 +573,7 @@ static int assemble_enqueue(Handle* h) {
     h->kstart(2);
     SG_CUDA(launch_assembly(h));
     h->kstop(2);
-    SG_CUDA(cudaEventRecord(h->ev[1], h->stream));
+    SG_CUDA(h->rec(h->ev[1]));
     return SGIGA_OK;
 }
 
@@ -563,7 +581,7 @@ static int solve_enqueue(Handle* h, double rtol, int32_t maxit) {
     if (!(rtol > 0.0)) { set_error("rtol must be positive"); return SGIGA_ERR_VALUE; }
     if (maxit < 1) maxit = 1000000;
     h->launches[1] = 0;
-    SG_CUDA(cudaEventRecord(h->ev[2], h->stream));
+    SG_CUDA(h->rec(h->ev[2]));
     SG_CUDA(cudaMemsetAsync(h->d_cg, 0, sizeof(CgState) * h->ncomp, h->stream));
     int st = run_pcg(h, rtol, maxit);
     if (st) return st;
@@ -571,7 +589,7 @@ static int solve_enqueue(Handle* h, double rtol, int32_t maxit) {
     SG_CUDA(launch_residual_check(h));
     SG_CUDA(launch_expand(h));
     h->kstop(5);
-    SG_CUDA(cudaEventRecord(h->ev[3], h->stream));
+    SG_CUDA(h->rec(h->ev[3]));
     SG_CUDA(cudaMemcpyAsync(h->h_cg, h->d_cg, sizeof(CgState) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
     SG_CUDA(cudaMemcpyAsync(h->h_rel, h->d_relres, sizeof(double) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
     return SGIGA_OK;
@@ -624,28 +642,26 @@ static thread_local size_t s_pts_cap = 0;
 static thread_local double* s_out = nullptr;
 static thread_local size_t s_out_cap = 0;
 
-static int combine_enqueue(Handle* h, const double* pts, int64_t npts, double* out, int32_t device) {
-    h->launches[2] = 0;
-    SG_CUDA(cudaEventRecord(h->ev[4], h->stream));
-    const double* dp = pts;
-    double* dout = out;
+// host points -> device scratch (device = 0 / -1 of sgiga_combine_points)
+static int stage_points(Handle* h, const double* pts, int64_t npts, size_t nout, const double** dp,
+                        double** dout) {
     int st;
-    int per_comp = device < 0;       // device = -1 / -2: per-component values (host / device)
-    int dev_ptrs = (device == 1 || device == -2);
-    size_t nout = per_comp ? (size_t)npts * h->ncomp : (size_t)npts;
-    if (!dev_ptrs) {
-        if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
-        if ((st = ensure_scratch(&s_out, &s_out_cap, nout))) return st;
-        SG_CUDA(cudaMemcpyAsync(s_pts, pts, sizeof(double) * npts * h->d, cudaMemcpyHostToDevice, h->stream));
-        dp = s_pts;
-        dout = s_out;
-    }
+    if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
+    if ((st = ensure_scratch(&s_out, &s_out_cap, nout))) return st;
+    SG_CUDA(cudaMemcpyAsync(s_pts, pts, sizeof(double) * npts * h->d, cudaMemcpyHostToDevice, h->stream));
+    *dp = s_pts;
+    *dout = s_out;
+    return SGIGA_OK;
+}
+
+// device points -> device values
+static int combine_enqueue(Handle* h, const double* dp, int64_t npts, double* dout, int per_comp) {
+    h->launches[2] = 0;
+    SG_CUDA(h->rec(h->ev[4]));
     h->kstart(6);
     SG_CUDA(launch_combine_points(h, dp, npts, dout, per_comp));
     h->kstop(6);
-    if (!dev_ptrs)
-        SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream));
-    SG_CUDA(cudaEventRecord(h->ev[5], h->stream));
+    SG_CUDA(h->rec(h->ev[5]));
     return SGIGA_OK;
 }
 
@@ -674,16 +690,70 @@ int sgiga_solve(sgiga_handle* hh, double rtol, int32_t maxit, int32_t* iters_out
     return solve_finish(h, iters_out, relres_out);
 }
 
+static bool run_graphs_enabled() {
+    for (const char* k : {"SGIGA_NO_GRAPH", "SGIGA_PCG_PROFILE", "SGIGA_ASM_PROFILE", "SGIGA_PCG_TRACE"}) {
+        const char* e = getenv(k);
+        if (e && e[0] && !(e[0] == '0' && e[1] == 0)) return false;
+    }
+    return true;
+}
+
 int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, int64_t npts,
               double* out, int32_t device, int32_t* iters_out, double* relres_out) {
     Handle* h = reinterpret_cast<Handle*>(hh);
     if (!h || npts < 0 || (npts > 0 && (!pts || !out))) { set_error("null argument"); return SGIGA_ERR_VALUE; }
     if (device < 0) { set_error("sgiga_run: per-component output is not supported"); return SGIGA_ERR_VALUE; }
-    int st = assemble_enqueue(h);
-    if (st) return st;
-    st = solve_enqueue(h, rtol, maxit);
-    if (st) return st;
-    if (npts > 0 && (st = combine_enqueue(h, pts, npts, out, device))) return st;
+    const double* dp = pts;
+    double* dout = out;
+    int st;
+    if (npts > 0 && device == 0 && (st = stage_points(h, pts, npts, (size_t)npts, &dp, &dout))) return st;
+    auto enqueue_all = [&]() -> int {
+        int s2 = assemble_enqueue(h);
+        if (!s2) s2 = solve_enqueue(h, rtol, maxit);
+        if (!s2 && npts > 0) s2 = combine_enqueue(h, dp, npts, dout, 0);
+        return s2;
+    };
+    // whole-run graph: only when the solve has no host-driven loop (every
+    // component on the single-launch small path) and no profiling knob is on
+    const bool can_graph = run_graphs_enabled() && h->large_comps.empty() && !h->graph_broken;
+    const bool same = can_graph && h->rkey.npts == npts && h->rkey.rtol == rtol && h->rkey.maxit == maxit &&
+                      h->rkey.dp == dp && h->rkey.dout == dout;
+    if (same && h->run_exec) {
+        SG_CUDA(cudaGraphLaunch(h->run_exec, h->stream));
+        h->tables_ready = true;
+        for (int i = 0; i < 3; ++i) h->launches[i] = h->run_launches[i];
+        for (int i = 0; i < 7; ++i) h->kran[i] = h->run_kran[i];
+    } else if (same && h->rkey.warm) {
+        cudaGraph_t g = nullptr;
+        SG_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        h->capturing = true;
+        st = enqueue_all();
+        h->capturing = false;
+        const cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
+        cudaError_t ie = cudaErrorUnknown;
+        if (!st && ce == cudaSuccess && g) ie = cudaGraphInstantiate(&h->run_exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (st || ie != cudaSuccess) {   // not capturable here: run the launches directly from now on
+            cudaGetLastError();
+            h->run_exec = nullptr;
+            h->drop_run_graph();
+            h->graph_broken = true;
+            if ((st = enqueue_all())) return st;
+        } else {
+            for (int i = 0; i < 3; ++i) h->run_launches[i] = h->launches[i];
+            for (int i = 0; i < 7; ++i) h->run_kran[i] = h->kran[i];
+            SG_CUDA(cudaGraphLaunch(h->run_exec, h->stream));
+        }
+    } else {
+        if ((st = enqueue_all())) return st;
+        if (can_graph) {
+            h->drop_run_graph();
+            h->rkey.rtol = rtol; h->rkey.maxit = maxit; h->rkey.dp = dp; h->rkey.dout = dout;
+            h->rkey.npts = npts; h->rkey.warm = 1;
+        }
+    }
+    if (npts > 0 && device == 0)
+        SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * npts, cudaMemcpyDeviceToHost, h->stream));
     SG_CUDA(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     SG_CUDA(cudaStreamSynchronize(h->stream));   // the one synchronisation of the call
     st = decode_err(h);
@@ -728,8 +798,15 @@ int sgiga_combine_points(sgiga_handle* hh, const double* pts, int64_t npts, doub
     if (!h || npts < 0) return SGIGA_ERR_VALUE;
     if (!h->have_coefs) { set_error("combine before solve"); return SGIGA_ERR_STATE; }
     if (npts == 0) return SGIGA_OK;
-    int st = combine_enqueue(h, pts, npts, out, device);
-    if (st) return st;
+    const int per_comp = device < 0;   // device = -1 / -2: per-component values (host / device)
+    const bool dev_ptrs = device == 1 || device == -2;
+    const size_t nout = per_comp ? (size_t)npts * h->ncomp : (size_t)npts;
+    const double* dp = pts;
+    double* dout = out;
+    int st;
+    if (!dev_ptrs && (st = stage_points(h, pts, npts, nout, &dp, &dout))) return st;
+    if ((st = combine_enqueue(h, dp, npts, dout, per_comp))) return st;
+    if (!dev_ptrs) SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream));
     SG_CUDA(cudaStreamSynchronize(h->stream));
     SG_CUDA(cudaEventElapsedTime(&h->ms[2], h->ev[4], h->ev[5]));
     return SGIGA_OK;

@@ -103,8 +103,32 @@ struct Handle {
     bool force_generic_assembly = false;   // SGIGA_GENERIC_ASSEMBLY=1 (parity cross-check)
     int asm_seg = 0;                       // stream-axis segment length of the pencils
 
-    void kstart(int g) { cudaEventRecord(kev[2 * g], stream); kran[g] = true; }
-    void kstop(int g) { cudaEventRecord(kev[2 * g + 1], stream); }
+    // whole-run CUDA graph (sgiga_run): captured on the second call with the
+    // same arguments, replayed while they and the work lists stay the same
+    bool capturing = false, graph_broken = false;
+    cudaGraphExec_t run_exec = nullptr;
+    struct RunKey {
+        double rtol = 0.0;
+        int maxit = 0, warm = 0;
+        const double* dp = nullptr;
+        double* dout = nullptr;
+        int64_t npts = -1;
+    } rkey;
+    long long run_launches[3] = {0, 0, 0};
+    bool run_kran[7] = {false, false, false, false, false, false, false};
+    void drop_run_graph() {
+        if (run_exec) cudaGraphExecDestroy(run_exec);
+        run_exec = nullptr;
+        rkey = RunKey{};
+    }
+
+    // event record that is also a timing node when the stream is captured
+    cudaError_t rec(cudaEvent_t e) {
+        return capturing ? cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal)
+                         : cudaEventRecord(e, stream);
+    }
+    void kstart(int g) { rec(kev[2 * g]); kran[g] = true; }
+    void kstop(int g) { rec(kev[2 * g + 1]); }
     int ncg() const { return d * (d + 1) / 2; }   // symmetric metric entries
     int nG() const { return ncg() + 1; }           // + load
 };

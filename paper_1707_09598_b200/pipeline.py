@@ -130,8 +130,15 @@ class Batch:
     def stream_ptr(self) -> int:
         return int(self.lib.sgiga_stream(self.h) or 0)
 
-    def upload(self):
-        """Per-step host->device copy of the problem inputs."""
+    def upload(self, spec: PlanSpec | None = None):
+        """Host->device copy of the problem descriptor (same shape); with
+        ``spec`` a new problem replaces the handle's (new forcing, weights,
+        ...).  Uploading a byte-identical descriptor is a no-op."""
+        if spec is not None:
+            desc, keep = make_desc(spec)
+            _lib.check(self.lib.sgiga_upload(self.h, ct.byref(desc)))
+            self.spec, self.desc, self._keep = spec, desc, keep
+            return
         _lib.check(self.lib.sgiga_upload(self.h, ct.byref(self.desc)))
 
     # ---- phases -------------------------------------------------------------

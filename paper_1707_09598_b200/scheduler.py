@@ -139,8 +139,11 @@ class PlanSession:
     """A device handle kept across repeated solves of one plan shape.
 
     ``run(points)`` is the end-to-end call: host->device copy of the
-    problem inputs, assemble, PCG, combine at the host points, device->host
-    copy of the combined values.
+    points, assemble, PCG, combine, device->host copy of the combined
+    values -- one library call (sgiga_run), one stream synchronisation; from
+    the second call on with the same arguments it replays a captured CUDA
+    graph.  The problem descriptor is uploaded once, when the session opens
+    (``update(problem)`` re-uploads a same-shape problem).
     """
 
     def __init__(self, plan, problem, quad_points=None, rtol=DEFAULT_RTOL, stream=None):
@@ -155,10 +158,15 @@ class PlanSession:
     def h2d_input_bytes(self) -> int:
         return int(sum(a.nbytes for a in self.batch._keep.values()))
 
+    def update(self, problem) -> None:
+        """Re-upload a problem of the same shape (new geometry weights,
+        forcing, ...); an identical descriptor keeps the captured graph."""
+        spec = make_spec(tuple(self.plan.terms), problem, self.spec.quad_points)
+        self.batch.upload(spec)
+        self.problem, self.spec = problem, spec
+
     def run(self, points) -> np.ndarray:
-        b = self.batch
-        b.upload()
-        return b.run(points, self.rtol)
+        return self.batch.run(points, self.rtol)
 
     def close(self):
         self.batch.close()

@@ -258,12 +258,46 @@ def test_single_call_run_matches_phase_calls(name):
         it0, rr0 = b.solve(rtol=1e-13)
         v0 = b.combine_points(pts)
         c0 = b.coefficients()
-        for _ in range(2):
+        # call 1: direct launches; 2: captured into a graph; 3+: replays
+        for _ in range(4):
             v1 = b.run(pts, rtol=1e-13)
             assert np.array_equal(v0, v1)
             assert np.array_equal(it0, b.iters) and np.array_equal(rr0, b.relres)
             assert np.array_equal(c0, b.coefficients())
+        # replay reads the new point values (same staging buffer)
+        pts2 = cfg.points(2000)[::-1].copy() * 0.5
+        assert np.array_equal(b.run(pts2, rtol=1e-13), b.combine_points(pts2))
+        # an identical re-upload keeps the graph; results unchanged
+        b.upload()
+        assert np.array_equal(b.run(pts, rtol=1e-13), v0)
         assert b.run(None).shape == (0,)
+    finally:
+        b.close()
+
+
+def test_run_graph_replay_matches_direct_launches(monkeypatch):
+    """The captured whole-run graph == direct launches (SGIGA_NO_GRAPH=1)."""
+    import torch
+    cfg = configs.get_config("cfg2")
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    pts = torch.from_numpy(cfg.points(5000)).cuda()
+    out = torch.empty(pts.shape[0], dtype=torch.float64, device="cuda")
+    b = Batch(spec)
+    try:
+        for _ in range(3):
+            b.run_device(pts.data_ptr(), pts.shape[0], out.data_ptr())
+        torch.cuda.synchronize()
+        g = out.cpu().numpy().copy()
+        monkeypatch.setenv("SGIGA_NO_GRAPH", "1")
+        b.run_device(pts.data_ptr(), pts.shape[0], out.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(g, out.cpu().numpy())
+        monkeypatch.delenv("SGIGA_NO_GRAPH")
+        pts.mul_(0.75)   # same pointer, new values: the replay must see them
+        for _ in range(3):
+            b.run_device(pts.data_ptr(), pts.shape[0], out.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), b.combine_points(pts.cpu().numpy()))
     finally:
         b.close()
 
