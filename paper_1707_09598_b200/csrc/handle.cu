@@ -47,9 +47,7 @@ static void free_all(Handle* h) {
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};
     for (void* p : hptrs)
         if (p) cudaFreeHost(p);
-    for (auto& e : h->ev)
-        if (e) cudaEventDestroy(e);
-    for (auto& e : h->kev)
+    for (auto& e : h->evp)
         if (e) cudaEventDestroy(e);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
 }
@@ -434,14 +432,20 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_alist, h->chunks.size());
     A_(d_relres, h->ncomp);
     A_(d_slotoff, h->slotoff.size());
+    A_(d_chist, COMBINE_SORT_BINS);
 #undef A_
     if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned_flag), sizeof(int) * 4);
-    if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_err), sizeof(int));
-    if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_cg), sizeof(CgState) * std::max(1, h->ncomp));
-    if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_rel), sizeof(double) * std::max(1, h->ncomp));
-    for (auto& ev : h->ev)
-        if (ea == cudaSuccess) ea = cudaEventCreate(&ev);
-    for (auto& ev : h->kev)
+    // mapped pinned mirrors: the status kernel writes them directly (no copy nodes)
+    if (ea == cudaSuccess) ea = cudaHostAlloc(reinterpret_cast<void**>(&h->h_err), sizeof(int), cudaHostAllocMapped);
+    if (ea == cudaSuccess)
+        ea = cudaHostAlloc(reinterpret_cast<void**>(&h->h_cg), sizeof(CgState) * std::max(1, h->ncomp), cudaHostAllocMapped);
+    if (ea == cudaSuccess)
+        ea = cudaHostAlloc(reinterpret_cast<void**>(&h->h_rel), sizeof(double) * std::max(1, h->ncomp), cudaHostAllocMapped);
+    if (ea == cudaSuccess) ea = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_err), h->h_err, 0);
+    if (ea == cudaSuccess) ea = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_cg), h->h_cg, 0);
+    if (ea == cudaSuccess) ea = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_rel), h->h_rel, 0);
+    if (ea == cudaSuccess) ea = cudaMemsetAsync(h->d_chist, 0, sizeof(int) * COMBINE_SORT_BINS, h->stream);
+    for (auto& ev : h->evp)
         if (ea == cudaSuccess) ea = cudaEventCreate(&ev);
     if (ea != cudaSuccess) {
         set_error(std::string("device allocation failed: ") + cudaGetErrorString(ea));
@@ -461,6 +465,8 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     h->iters.assign(h->ncomp, 0);
     const char* gen = getenv("SGIGA_GENERIC_ASSEMBLY");
     h->force_generic_assembly = gen && gen[0] == '1';
+    const char* nk = getenv("SGIGA_NO_KTIMES");
+    h->ktimes = !(nk && nk[0] == '1');
     *out = reinterpret_cast<sgiga_handle*>(h);
     return SGIGA_OK;
 }
@@ -536,6 +542,7 @@ int sgiga_quad_points_physical(sgiga_handle* hh, double* x_out) {
         SG_CUDA(dalloc(&h->d_hostf, h->total_qp));
         SG_CUDA(cudaMemsetAsync(h->d_hostf, 0, sizeof(double) * std::max<int64_t>(1, h->total_qp), h->stream));
     }
+    h->begin_call();
     int st = ensure_tables(h);
     if (st) return st;
     SG_CUDA(launch_metric(h));
@@ -563,7 +570,8 @@ static int assemble_enqueue(Handle* h) {
         return SGIGA_ERR_STATE;
     }
     h->launches[0] = 0;
-    SG_CUDA(h->rec(h->ev[0]));
+    h->begin_call();           // assembly always opens a call's launch sequence
+    h->pmark(0);
     h->tables_ready = false;   // kernel 1 is part of every assembly pass
     int st = ensure_tables(h);
     if (st) return st;
@@ -573,7 +581,7 @@ static int assemble_enqueue(Handle* h) {
     h->kstart(2);
     SG_CUDA(launch_assembly(h));
     h->kstop(2);
-    SG_CUDA(h->rec(h->ev[1]));
+    h->pmark(1);
     return SGIGA_OK;
 }
 
@@ -581,23 +589,21 @@ static int solve_enqueue(Handle* h, double rtol, int32_t maxit) {
     if (!(rtol > 0.0)) { set_error("rtol must be positive"); return SGIGA_ERR_VALUE; }
     if (maxit < 1) maxit = 1000000;
     h->launches[1] = 0;
-    SG_CUDA(h->rec(h->ev[2]));
-    SG_CUDA(cudaMemsetAsync(h->d_cg, 0, sizeof(CgState) * h->ncomp, h->stream));
+    h->pmark(2);
+    SG_CUDA(launch_solve_prologue(h));   // zero the solver state and the active counts
     int st = run_pcg(h, rtol, maxit);
     if (st) return st;
     h->kstart(5);
     SG_CUDA(launch_residual_check(h));
     SG_CUDA(launch_expand(h));
     h->kstop(5);
-    SG_CUDA(h->rec(h->ev[3]));
-    SG_CUDA(cudaMemcpyAsync(h->h_cg, h->d_cg, sizeof(CgState) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
-    SG_CUDA(cudaMemcpyAsync(h->h_rel, h->d_relres, sizeof(double) * h->ncomp, cudaMemcpyDeviceToHost, h->stream));
+    h->pmark(3);
     return SGIGA_OK;
 }
 
 // per-component convergence verdict (linsolve.py:49-53 acceptance)
 static int solve_finish(Handle* h, int32_t* iters_out, double* relres_out) {
-    SG_CUDA(cudaEventElapsedTime(&h->ms[1], h->ev[2], h->ev[3]));
+    SG_CUDA(h->elapsed(&h->ms[1], Handle::PHASE_EV + 2, Handle::PHASE_EV + 3));
     h->have_coefs = true;
     h->solved = true;
     int status = SGIGA_OK;
@@ -657,11 +663,11 @@ static int stage_points(Handle* h, const double* pts, int64_t npts, size_t nout,
 // device points -> device values
 static int combine_enqueue(Handle* h, const double* dp, int64_t npts, double* dout, int per_comp) {
     h->launches[2] = 0;
-    SG_CUDA(h->rec(h->ev[4]));
+    h->pmark(4);
     h->kstart(6);
     SG_CUDA(launch_combine_points(h, dp, npts, dout, per_comp));
     h->kstop(6);
-    SG_CUDA(h->rec(h->ev[5]));
+    h->pmark(5);
     return SGIGA_OK;
 }
 
@@ -672,7 +678,7 @@ int sgiga_assemble(sgiga_handle* hh) {
     if (st) return st;
     st = check_err(h);
     if (st) return st;
-    SG_CUDA(cudaEventElapsedTime(&h->ms[0], h->ev[0], h->ev[1]));
+    SG_CUDA(h->elapsed(&h->ms[0], Handle::PHASE_EV + 0, Handle::PHASE_EV + 1));
     h->assembled = true;
     h->solved = false;
     return SGIGA_OK;
@@ -683,10 +689,12 @@ int sgiga_solve(sgiga_handle* hh, double rtol, int32_t maxit, int32_t* iters_out
     Handle* h = reinterpret_cast<Handle*>(hh);
     if (!h) return SGIGA_ERR_VALUE;
     if (!h->assembled) { set_error("sgiga_solve before sgiga_assemble"); return SGIGA_ERR_STATE; }
+    h->begin_call();
     int st = solve_enqueue(h, rtol, maxit);
     if (st) return st;
-    st = check_err(h);   // synchronises: h_cg / h_rel are valid after it
-    if (st) return st;
+    SG_CUDA(launch_status(h));
+    SG_CUDA(cudaStreamSynchronize(h->stream));   // h_cg / h_rel / h_err are valid after it
+    if ((st = decode_err(h))) return st;
     return solve_finish(h, iters_out, relres_out);
 }
 
@@ -711,6 +719,7 @@ int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, i
         int s2 = assemble_enqueue(h);
         if (!s2) s2 = solve_enqueue(h, rtol, maxit);
         if (!s2 && npts > 0) s2 = combine_enqueue(h, dp, npts, dout, 0);
+        if (!s2 && launch_status(h) != cudaSuccess) s2 = SGIGA_ERR_CUDA;
         return s2;
     };
     // whole-run graph: only when the solve has no host-driven loop (every
@@ -723,6 +732,8 @@ int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, i
         h->tables_ready = true;
         for (int i = 0; i < 3; ++i) h->launches[i] = h->run_launches[i];
         for (int i = 0; i < 7; ++i) h->kran[i] = h->run_kran[i];
+        for (int i = 0; i < Handle::NEV; ++i) h->alias[i] = h->run_alias[i];
+        h->last_mark = -1;
     } else if (same && h->rkey.warm) {
         cudaGraph_t g = nullptr;
         SG_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
@@ -742,6 +753,8 @@ int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, i
         } else {
             for (int i = 0; i < 3; ++i) h->run_launches[i] = h->launches[i];
             for (int i = 0; i < 7; ++i) h->run_kran[i] = h->kran[i];
+            for (int i = 0; i < Handle::NEV; ++i) h->run_alias[i] = h->alias[i];
+            h->last_mark = -1;
             SG_CUDA(cudaGraphLaunch(h->run_exec, h->stream));
         }
     } else {
@@ -754,14 +767,13 @@ int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, i
     }
     if (npts > 0 && device == 0)
         SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * npts, cudaMemcpyDeviceToHost, h->stream));
-    SG_CUDA(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     SG_CUDA(cudaStreamSynchronize(h->stream));   // the one synchronisation of the call
     st = decode_err(h);
     if (st) return st;
-    SG_CUDA(cudaEventElapsedTime(&h->ms[0], h->ev[0], h->ev[1]));
+    SG_CUDA(h->elapsed(&h->ms[0], Handle::PHASE_EV + 0, Handle::PHASE_EV + 1));
     h->assembled = true;
     st = solve_finish(h, iters_out, relres_out);
-    if (npts > 0) SG_CUDA(cudaEventElapsedTime(&h->ms[2], h->ev[4], h->ev[5]));
+    if (npts > 0) SG_CUDA(h->elapsed(&h->ms[2], Handle::PHASE_EV + 4, Handle::PHASE_EV + 5));
     return st;
 }
 
@@ -786,6 +798,7 @@ int sgiga_set_coefficients(sgiga_handle* hh, const double* full) {
     if (!h || !full) return SGIGA_ERR_VALUE;
     SG_CUDA(cudaMemcpyAsync(h->d_coef, full, sizeof(double) * h->total_dofs, cudaMemcpyHostToDevice, h->stream));
     SG_CUDA(cudaStreamSynchronize(h->stream));
+    h->begin_call();
     int st = ensure_tables(h);
     if (st) return st;
     h->have_coefs = true;
@@ -805,10 +818,11 @@ int sgiga_combine_points(sgiga_handle* hh, const double* pts, int64_t npts, doub
     double* dout = out;
     int st;
     if (!dev_ptrs && (st = stage_points(h, pts, npts, nout, &dp, &dout))) return st;
+    h->begin_call();
     if ((st = combine_enqueue(h, dp, npts, dout, per_comp))) return st;
     if (!dev_ptrs) SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream));
     SG_CUDA(cudaStreamSynchronize(h->stream));
-    SG_CUDA(cudaEventElapsedTime(&h->ms[2], h->ev[4], h->ev[5]));
+    SG_CUDA(h->elapsed(&h->ms[2], Handle::PHASE_EV + 4, Handle::PHASE_EV + 5));
     return SGIGA_OK;
 }
 
@@ -921,7 +935,7 @@ int sgiga_kernel_times(sgiga_handle* hh, float* ms7) {
     SG_CUDA(cudaStreamSynchronize(h->stream));
     for (int g = 0; g < 7; ++g) {
         float ms = 0.0f;
-        if (h->kran[g] && cudaEventElapsedTime(&ms, h->kev[2 * g], h->kev[2 * g + 1]) != cudaSuccess) ms = -1.0f;
+        if (h->kran[g] && h->elapsed(&ms, 2 * g, 2 * g + 1) != cudaSuccess) ms = -1.0f;
         ms7[g] = h->kran[g] ? ms : 0.0f;
     }
     cudaGetLastError();

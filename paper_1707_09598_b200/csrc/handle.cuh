@@ -19,6 +19,17 @@ void set_error(const std::string& msg);
         }                                                                         \
     } while (0)
 
+// launch counter that also advances the handle's launch sequence number
+struct LaunchCount {
+    long long n = 0;
+    long long* seq = nullptr;
+    LaunchCount& operator++() { ++n; ++*seq; return *this; }
+    long long operator++(int) { const long long o = n; ++*this; return o; }
+    LaunchCount& operator+=(long long k) { n += k; ++*seq; return *this; }
+    LaunchCount& operator=(long long v) { n = v; return *this; }
+    operator long long() const { return n; }
+};
+
 struct Handle {
     int dev = 0;
     cudaStream_t stream = nullptr;
@@ -86,22 +97,33 @@ struct Handle {
     size_t cperm_cap = 0;
     int* d_chist = nullptr;        // combine: cell histogram / cursors
     int* h_pinned_flag = nullptr;  // pinned host mirror of the active count
-    int* h_err = nullptr;          // pinned mirrors read after the one sync of a call
+    int* h_err = nullptr;          // mapped pinned mirrors read after the one sync of a call
     CgState* h_cg = nullptr;
     double* h_rel = nullptr;
+    int* dh_err = nullptr;         // ... and their device-side addresses
+    CgState* dh_cg = nullptr;
+    double* dh_rel = nullptr;
 
     // state
     bool tables_ready = false, density_ready = false, assembled = false, solved = false,
          have_coefs = false;
-    cudaEvent_t ev[8] = {};
-    cudaEvent_t kev[14] = {};     // kernel-group start/stop pairs (sgiga_kernel_times)
-    float kms[7] = {0, 0, 0, 0, 0, 0, 0};
+    // timing marks: slots 0..13 = kernel-group start/stop pairs
+    // (sgiga_kernel_times), 14..19 = phase boundaries (sgiga_phase_stats).
+    // A mark with no launch since the previous mark reuses that event, so a
+    // chain of adjacent boundaries costs one event record, not several.
+    static constexpr int NEV = 20, PHASE_EV = 14;
+    cudaEvent_t evp[NEV] = {};
+    int alias[NEV] = {};
+    int last_mark = -1;
+    long long last_seq = -1;
+    long long seq = 0;            // bumped by every counted launch
     bool kran[7] = {false, false, false, false, false, false, false};
     float ms[3] = {0, 0, 0};
-    long long launches[3] = {0, 0, 0};
+    LaunchCount launches[3] = {{0, &seq}, {0, &seq}, {0, &seq}};
     std::vector<int> iters;
     bool force_generic_assembly = false;   // SGIGA_GENERIC_ASSEMBLY=1 (parity cross-check)
     int asm_seg = 0;                       // stream-axis segment length of the pencils
+    bool small_checked = false;            // small comps' true residual came from the cluster PCG
 
     // whole-run CUDA graph (sgiga_run): captured on the second call with the
     // same arguments, replayed while they and the work lists stay the same
@@ -116,6 +138,7 @@ struct Handle {
     } rkey;
     long long run_launches[3] = {0, 0, 0};
     bool run_kran[7] = {false, false, false, false, false, false, false};
+    int run_alias[NEV] = {};
     void drop_run_graph() {
         if (run_exec) cudaGraphExecDestroy(run_exec);
         run_exec = nullptr;
@@ -127,8 +150,21 @@ struct Handle {
         return capturing ? cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal)
                          : cudaEventRecord(e, stream);
     }
-    void kstart(int g) { rec(kev[2 * g]); kran[g] = true; }
-    void kstop(int g) { rec(kev[2 * g + 1]); }
+    void mark(int slot) {
+        if (last_mark >= 0 && last_seq == seq) { alias[slot] = last_mark; return; }
+        rec(evp[slot]);
+        alias[slot] = slot;
+        last_mark = slot;
+        last_seq = seq;
+    }
+    void begin_call() { last_mark = -1; }   // never alias an event of an earlier call
+    cudaError_t elapsed(float* out, int a, int b) const {
+        return cudaEventElapsedTime(out, evp[alias[a]], evp[alias[b]]);
+    }
+    bool ktimes = true;   // kernel-group events (SGIGA_NO_KTIMES=1 turns them off)
+    void kstart(int g) { if (ktimes) { mark(2 * g); kran[g] = true; } }
+    void kstop(int g) { if (ktimes) mark(2 * g + 1); }
+    void pmark(int i) { mark(PHASE_EV + i); }
     int ncg() const { return d * (d + 1) / 2; }   // symmetric metric entries
     int nG() const { return ncg() + 1; }           // + load
 };

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(CP_THREADS)
 k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
                        int ntab, const double* __restrict__ knots, int mu, const double* __restrict__ coef,
                        const double* __restrict__ pts, int64_t npts, const int* __restrict__ perm,
-                       double* __restrict__ out, int per_component, int npt) {
+                       double* __restrict__ out, int per_component, int npt, int* __restrict__ hist) {
     extern __shared__ double csm[];
     double* Bt = csm;                                   // [ntab][P][npt]
     double* V = Bt + (size_t)ntab * P * npt;            // [ncomp][npt]
@@ -187,6 +187,8 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
     const int64_t p0 = (int64_t)blockIdx.x * npt;
     const int nloc = npts - p0 < npt ? (int)(npts - p0) : npt;
     for (int pt = tid; pt < nloc; pt += CP_THREADS) gidx[pt] = perm ? perm[p0 + pt] : (int)(p0 + pt);
+    if (hist && blockIdx.x == 0)   // the sort is done: leave its cursors zero for the next call
+        for (int i = tid; i < COMBINE_SORT_BINS; i += CP_THREADS) hist[i] = 0;
     __syncthreads();
     for (int it = tid; it < ntab * npt; it += CP_THREADS) {
         const int pt = it % npt, t = it / npt;
@@ -234,7 +236,7 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
 // gives a permutation of the points in cell order.  The order inside a cell
 // depends on atomic timing, but every point's value is computed by the same
 // operations wherever it lands, so the output stays bitwise deterministic.
-constexpr int SORT_BITS = 12;   // 4096 cells
+constexpr int SORT_BITS = COMBINE_SORT_BITS;   // 4096 cells
 template <int D>
 __device__ __forceinline__ int cell_key(const double* x) {
     constexpr int b = SORT_BITS / D, n = 1 << b;
@@ -533,8 +535,8 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
             if ((e = cudaMalloc(&h->d_cperm, sizeof(int) * npts)) != cudaSuccess) return e;
             h->cperm_cap = (size_t)npts;
         }
-        if (!h->d_chist && (e = cudaMalloc(&h->d_chist, sizeof(int) << SORT_BITS)) != cudaSuccess) return e;
-        if ((e = cudaMemsetAsync(h->d_chist, 0, sizeof(int) << SORT_BITS, h->stream)) != cudaSuccess) return e;
+        // d_chist is zero here: zeroed at create, re-zeroed by the combine
+        // kernel after every sorted launch
         const unsigned sb = (unsigned)((npts + 255) / 256);
         if (h->d == 1) k_cell_hist<1><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist);
         else if (h->d == 2) k_cell_hist<2><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist);
@@ -553,7 +555,7 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
         if (e_ != cudaSuccess) return e_;                                                           \
         k_combine_points_tiled<DD, PP><<<blocks, CP_THREADS, smem, h->stream>>>(                    \
             h->d_comps, h->ncomp, h->d_tabs, ntab, h->d_knots, h->mu, h->d_coef, d_pts, npts, perm,  \
-            d_out, per_component, npt);                                                             \
+            d_out, per_component, npt, perm ? h->d_chist : nullptr);                                \
     }
     SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CPT)
 #undef LAUNCH_CPT

@@ -538,10 +538,11 @@ __global__ void __launch_bounds__(CHUNK_ROWS) k_cg_update(ChunkCtx X, int parity
 
 // ---- residual check: relres_c = ||A x - b|| / ||b|| ----------------------
 template <int D>
-__global__ void k_residual(ChunkCtx X, double* relres) {
+__global__ void k_residual(ChunkCtx X, double* relres, int skip_small) {
     __shared__ double red[64];
     const Chunk ch = X.chunks[blockIdx.x];
     const CompInfo& C = X.comps[ch.comp];
+    if (skip_small && C.small) return;   // the cluster PCG kernel checked these
     double v[2] = {0.0, 0.0};
     if (threadIdx.x < ch.nrow) {
         int row = ch.row0 + threadIdx.x;
@@ -617,9 +618,10 @@ size_t small_smem_bytes(const Handle* h, int64_t* smem_doubles) {
 int run_pcg(Handle* h, double rtol, int maxit) {
     ChunkCtx X = make_ctx(h, rtol, maxit);
     int nch = (int)h->chunks.size();
-    SG_CUDA(cudaMemsetAsync(h->d_active_count, 0, sizeof(int), h->stream));
     const char* nc = getenv("SGIGA_NO_CLUSTER");
+    h->small_checked = false;
     if (!h->small_comps.empty() && !(nc && nc[0] == '1')) {
+        h->small_checked = true;   // the cluster kernel also computes the true residual
         h->kstart(3);
         int st = launch_pcg_cluster(h, rtol, maxit);   // k_pcg_cluster.cu
         h->kstop(3);
@@ -721,13 +723,46 @@ int run_pcg(Handle* h, double rtol, int maxit) {
     return SGIGA_OK;
 }
 
+// ---- per-solve prologue / per-call status (single small launches that
+// replace memset and copy nodes) --------------------------------------------
+__global__ void k_solve_prologue(CgState* __restrict__ st, int ncomp, int* __restrict__ active_count) {
+    int* w = reinterpret_cast<int*>(st);
+    const int n = ncomp * (int)(sizeof(CgState) / sizeof(int));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = 0;
+    if (threadIdx.x < 4) active_count[threadIdx.x] = 0;
+}
+
+// solver state, true residuals and the error flags -> mapped host memory
+__global__ void k_status(const CgState* __restrict__ st, const double* __restrict__ relres,
+                         const int* __restrict__ err, int ncomp, CgState* hst, double* hrel, int* herr) {
+    for (int c = threadIdx.x; c < ncomp; c += blockDim.x) {
+        hst[c] = st[c];
+        hrel[c] = relres[c];
+    }
+    if (threadIdx.x == 0) *herr = *err;
+    __threadfence_system();
+}
+
+cudaError_t launch_solve_prologue(Handle* h) {
+    k_solve_prologue<<<1, 256, 0, h->stream>>>(h->d_cg, h->ncomp, h->d_active_count);
+    h->launches[1]++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_status(Handle* h) {
+    k_status<<<1, 256, 0, h->stream>>>(h->d_cg, h->d_relres, h->d_err, h->ncomp, h->dh_cg, h->dh_rel, h->dh_err);
+    h->launches[1]++;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_residual_check(Handle* h) {
     ChunkCtx X = make_ctx(h, 0.0, 0);
     int nch = (int)h->chunks.size();
-    if (nch == 0) return cudaSuccess;
-    if (h->d == 1) k_residual<1><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres);
-    else if (h->d == 2) k_residual<2><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres);
-    else k_residual<3><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres);
+    if (nch == 0 || (h->small_checked && h->large_comps.empty())) return cudaSuccess;
+    const int sk = h->small_checked ? 1 : 0;
+    if (h->d == 1) k_residual<1><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres, sk);
+    else if (h->d == 2) k_residual<2><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres, sk);
+    else k_residual<3><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres, sk);
     h->launches[1]++;
     return cudaGetLastError();
 }

@@ -48,7 +48,8 @@ k_pcg_cg1(const CompInfo* __restrict__ comps, const int* __restrict__ list,
           const int* __restrict__ slotoff, const double* __restrict__ stencil,
           const double* __restrict__ rhs, const double* __restrict__ dinv,
           double* __restrict__ xout, CgState* __restrict__ st, double rtol2, int maxit,
-          int smem_doubles, int nlist, int* errflag, long long* prof, int prof_slot) {
+          int smem_doubles, int nlist, int* errflag, long long* prof, int prof_slot,
+          double* __restrict__ relres) {
     namespace cgs = cooperative_groups;
     cgs::cluster_group cluster = cgs::this_cluster();
     const int K = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
@@ -247,12 +248,27 @@ k_pcg_cg1(const CompInfo* __restrict__ comps, const int* __restrict__ list,
     }
     if (pr)
         for (int k = 0; k < 6; ++k) prof[k] = tp[k];
-    for (int il = tid; il < RL; il += CL_THREADS) xout[Cg.vec_off + lo + il] = xs[il];
+    // acceptance check of the reference (linsolve.py:49-53): the TRUE
+    // residual ||A x - b|| / ||b||, with the register-resident matrix: x is
+    // broadcast like u (every rank finished reading uf and cred above)
+    for (int il = tid; il < RL; il += CL_THREADS) {
+        xout[Cg.vec_off + lo + il] = xs[il];
+        for (int r = 0; r < K; ++r) cluster.map_shared_rank(uf, r)[lo + il] = xs[il];
+    }
+    cluster.sync();
+    spmv_dots(dots);   // ws = A x
+    double ev[3] = {0.0, 0.0, 0.0};
+    for (int il = tid; il < RL; il += CL_THREADS) {
+        const double e = ws[il] - b[lo + il];
+        ev[0] += isfinite(xs[il]) ? e * e : __longlong_as_double(0x7ff8000000000000ULL);
+    }
+    cluster_sum3(ev);
     if (tid == 0 && rank == 0) {
         st[c].it = it;
         st[c].conv = conv;
         st[c].active = 0;
         st[c].bb = bb;
+        relres[c] = bb > 0.0 ? sqrt(ev[0] / bb) : (ev[0] == 0.0 ? 0.0 : ev[0]);
     }
     cluster.sync();   // no CTA exits while others may still write into its smem
 }
@@ -302,7 +318,7 @@ int launch_pcg_cluster(Handle* h, double rtol, int maxit) {
                                (const int*)h->d_small, (const int*)h->d_slotoff,              \
                                (const double*)h->d_stencil, (const double*)h->d_rhs,          \
                                (const double*)h->d_dinv, h->d_x, h->d_cg, rt2, maxit, sd, ns, \
-                               h->d_err, dprof, pslot))
+                               h->d_err, dprof, pslot, h->d_relres))
     if (h->d == 1) { LAUNCH_CG1(1); }
     else if (h->d == 2) { LAUNCH_CG1(2); }
     else { LAUNCH_CG1(3); }

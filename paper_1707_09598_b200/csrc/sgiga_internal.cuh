@@ -26,6 +26,8 @@ constexpr int PMAX = 5;   // p + 1 <= 5 (degree <= 4) on the device path
 constexpr int QMAX = 10;  // gauss_rule accepts q <= 10 (assembly.py:43)
 constexpr int WMAX = 2 * PMAX - 1;  // stencil slots per axis (2p+1)
 constexpr int GEO_PMAX = 8;         // geometry degree <= 7
+constexpr int COMBINE_SORT_BITS = 12;                      // cell sort of the combine points
+constexpr int COMBINE_SORT_BINS = 1 << COMBINE_SORT_BITS;
 
 // device error flags (bit mask in Handle::d_err)
 enum : int { ERRF_GEOMETRY = 1, ERRF_NONFINITE = 2, ERRF_SPAN = 4 };
@@ -213,6 +215,8 @@ cudaError_t launch_assembly(Handle* h);
 int run_pcg(Handle* h, double rtol, int maxit);
 int launch_pcg_cluster(Handle* h, double rtol, int maxit);
 cudaError_t launch_residual_check(Handle* h);
+cudaError_t launch_solve_prologue(Handle* h);
+cudaError_t launch_status(Handle* h);
 cudaError_t launch_expand(Handle* h);
 cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, double* d_out,
                                   int per_component);
