@@ -41,7 +41,8 @@ static void free_all(Handle* h) {
                     h->d_qw, h->d_geob, h->d_geofirst, h->d_geo_knots, h->d_geo_hw, h->d_G,
                     h->d_hostf, h->d_xphys, h->d_stencil, h->d_rhs, h->d_dinv, h->d_x,
                     h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
-                    h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist};
+                    h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
+                    h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};
@@ -49,6 +50,10 @@ static void free_all(Handle* h) {
         if (p) cudaFreeHost(p);
     for (auto& e : h->evp)
         if (e) cudaEventDestroy(e);
+    if (h->fd_fork) cudaEventDestroy(h->fd_fork);
+    if (h->fd_join) cudaEventDestroy(h->fd_join);
+    if (h->stream2) cudaStreamDestroy(h->stream2);
+    if (h->run_exec) cudaGraphExecDestroy(h->run_exec);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
 }
 
@@ -217,6 +222,49 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
             h->chunks.push_back(ch);
         }
     }
+    // FD-preconditioned CG for the small components whose axes all fit the
+    // one-CTA eigen kernel (<= FD_MMAX interior functions) and whose vectors
+    // fit shared memory; the others keep the Jacobi-PCG paths
+    {
+        const char* nofd = getenv("SGIGA_NO_FD");
+        const bool fd_on = !(nofd && nofd[0] == '1');
+        const int ntab = (int)h->tabs.size();
+        h->fd_comps.clear(); h->fd_uniq.clear();
+        h->fd_uoff.assign(ntab, 0); h->fd_loff.assign(ntab, 0);
+        h->fd_u_total = 0; h->fd_l_total = 0;
+        std::vector<char> used(ntab, 0);
+        std::vector<int> keep_small;
+        for (int c : h->small_comps) {
+            CompInfo& C = h->comps[c];
+            bool ok = fd_on && C.rows > 0 && fd_comp_smem(C, d) <= 200 * 1024;
+            for (int k = 0; k < d && ok; ++k) ok = C.m[k] >= 1 && C.m[k] <= FD_MMAX;
+            C.fd = ok ? 1 : 0;
+            if (ok) {
+                h->fd_comps.push_back(c);
+                for (int k = 0; k < d; ++k) used[C.tab[k]] = 1;
+            } else {
+                keep_small.push_back(c);
+            }
+        }
+        h->small_comps.swap(keep_small);
+        // tables with identical knot vectors share one factorisation
+        for (int t = 0; t < ntab; ++t) {
+            if (!used[t]) continue;
+            const TabInfo& T = h->tabs[t];
+            int src = -1;
+            for (int u : h->fd_uniq) {
+                const TabInfo& Tu = h->tabs[u];
+                if (Tu.nel == T.nel &&
+                    std::equal(h->bp_host.begin() + T.bp_off, h->bp_host.begin() + T.bp_off + T.nel + 1,
+                               h->bp_host.begin() + Tu.bp_off)) { src = u; break; }
+            }
+            if (src >= 0) { h->fd_uoff[t] = h->fd_uoff[src]; h->fd_loff[t] = h->fd_loff[src]; continue; }
+            const int64_t m = T.n - 2;
+            h->fd_uniq.push_back(t);
+            h->fd_uoff[t] = h->fd_u_total; h->fd_u_total += m * m;
+            h->fd_loff[t] = h->fd_l_total; h->fd_l_total += m;
+        }
+    }
     // assembly pencils: tile rows along ax[d-2], ax[d-3]; segments of SEG
     // rows along the stream axis.  A pencil walks its elements one quadrature
     // plane at a time, so its cost is ~ planes (+ a fixed setup); a segment
@@ -296,6 +344,12 @@ static int upload_all(Handle* h) {
         SG_CUDA(cudaMemcpyAsync(h->d_small, h->small_comps.data(), sizeof(int) * h->small_comps.size(), cudaMemcpyHostToDevice, s));
     if (!h->slotoff.empty())
         SG_CUDA(cudaMemcpyAsync(h->d_slotoff, h->slotoff.data(), sizeof(int) * h->slotoff.size(), cudaMemcpyHostToDevice, s));
+    if (!h->fd_comps.empty()) {
+        SG_CUDA(cudaMemcpyAsync(h->d_fdlist, h->fd_comps.data(), sizeof(int) * h->fd_comps.size(), cudaMemcpyHostToDevice, s));
+        SG_CUDA(cudaMemcpyAsync(h->d_fd_uniq, h->fd_uniq.data(), sizeof(int) * h->fd_uniq.size(), cudaMemcpyHostToDevice, s));
+        SG_CUDA(cudaMemcpyAsync(h->d_fd_uoff, h->fd_uoff.data(), sizeof(int64_t) * h->fd_uoff.size(), cudaMemcpyHostToDevice, s));
+        SG_CUDA(cudaMemcpyAsync(h->d_fd_loff, h->fd_loff.data(), sizeof(int64_t) * h->fd_loff.size(), cudaMemcpyHostToDevice, s));
+    }
     SG_CUDA(cudaMemcpyAsync(h->d_bp, h->bp_host.data(), sizeof(double) * h->bp_host.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_geo_knots, h->geo_knots.data(), sizeof(double) * h->geo_knots.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_geo_hw, h->geo_hw.data(), sizeof(double) * h->geo_hw.size(), cudaMemcpyHostToDevice, s));
@@ -433,7 +487,16 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_relres, h->ncomp);
     A_(d_slotoff, h->slotoff.size());
     A_(d_chist, COMBINE_SORT_BINS);
+    A_(d_fdlist, h->fd_comps.size());
+    A_(d_fd_uniq, h->fd_uniq.size());
+    A_(d_fd_uoff, h->tabs.size());
+    A_(d_fd_loff, h->tabs.size());
+    A_(d_fdU, h->fd_u_total);
+    A_(d_fdL, h->fd_l_total);
 #undef A_
+    if (ea == cudaSuccess) ea = cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking);
+    if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_fork, cudaEventDisableTiming);
+    if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_join, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned_flag), sizeof(int) * 4);
     // mapped pinned mirrors: the status kernel writes them directly (no copy nodes)
     if (ea == cudaSuccess) ea = cudaHostAlloc(reinterpret_cast<void**>(&h->h_err), sizeof(int), cudaHostAllocMapped);
@@ -482,7 +545,9 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
         tmp.ncomp != h->ncomp || tmp.tabs.size() != h->tabs.size() || tmp.d != h->d ||
         tmp.p != h->p || tmp.q != h->q || tmp.pencils.size() != h->pencils.size() ||
         tmp.chunks.size() != h->chunks.size() || tmp.small_comps.size() != h->small_comps.size() ||
-        tmp.large_comps.size() != h->large_comps.size() || tmp.slotoff.size() != h->slotoff.size()) {
+        tmp.large_comps.size() != h->large_comps.size() || tmp.slotoff.size() != h->slotoff.size() ||
+        tmp.fd_comps.size() != h->fd_comps.size() || tmp.fd_uniq.size() != h->fd_uniq.size() ||
+        tmp.fd_u_total != h->fd_u_total || tmp.fd_l_total != h->fd_l_total) {
         set_error("sgiga_upload: descriptor shape differs from the handle's");
         return SGIGA_ERR_VALUE;
     }
@@ -497,7 +562,9 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
                            same_bytes(tmp.comps, h->comps) && same_bytes(tmp.tabs, h->tabs) &&
                            same_bytes(tmp.slotoff, h->slotoff) && same_bytes(tmp.pencils, h->pencils) &&
                            same_bytes(tmp.chunks, h->chunks) && same_bytes(tmp.small_comps, h->small_comps) &&
-                           same_bytes(tmp.large_comps, h->large_comps) && tmp.forcing_id == h->forcing_id;
+                           same_bytes(tmp.large_comps, h->large_comps) && same_bytes(tmp.fd_comps, h->fd_comps) &&
+                           same_bytes(tmp.fd_uniq, h->fd_uniq) && same_bytes(tmp.fd_uoff, h->fd_uoff) &&
+                           tmp.forcing_id == h->forcing_id;
     if (!identical) h->drop_run_graph();
     h->levels.swap(tmp.levels); h->coefs.swap(tmp.coefs);
     h->gauss_n.swap(tmp.gauss_n); h->gauss_w.swap(tmp.gauss_w);
@@ -506,6 +573,8 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
     h->slotoff.swap(tmp.slotoff);
     h->pencils.swap(tmp.pencils); h->chunks.swap(tmp.chunks);
     h->small_comps.swap(tmp.small_comps); h->large_comps.swap(tmp.large_comps);
+    h->fd_comps.swap(tmp.fd_comps); h->fd_uniq.swap(tmp.fd_uniq);
+    h->fd_uoff.swap(tmp.fd_uoff); h->fd_loff.swap(tmp.fd_loff);
     h->forcing_id = tmp.forcing_id;
     if (identical) return SGIGA_OK;   // device copies are already these bytes
     return upload_all(h);
@@ -575,6 +644,13 @@ static int assemble_enqueue(Handle* h) {
     h->tables_ready = false;   // kernel 1 is part of every assembly pass
     int st = ensure_tables(h);
     if (st) return st;
+    if (!h->fd_uniq.empty()) {   // FD eigen-factors on the side stream, overlapping the assembly
+        SG_CUDA(cudaEventRecord(h->fd_fork, h->stream));
+        SG_CUDA(cudaStreamWaitEvent(h->stream2, h->fd_fork, 0));
+        SG_CUDA(launch_fd_eigen(h, h->stream2));
+        SG_CUDA(cudaEventRecord(h->fd_join, h->stream2));
+        h->fd_pending = true;
+    }
     h->kstart(1);
     SG_CUDA(launch_metric(h));
     h->kstop(1);

@@ -93,6 +93,20 @@ struct Handle {
     int* d_active_count = nullptr;
     int* d_alist = nullptr;      // compacted active chunk list (large-path PCG)
     double* d_relres = nullptr;
+    // FD preconditioner (k_fd.cu): per-table factor offsets (shared between
+    // tables with the same knot vector), the tables to factor, the comps
+    std::vector<int> fd_comps, fd_uniq;
+    std::vector<int64_t> fd_uoff, fd_loff;
+    int64_t fd_u_total = 0, fd_l_total = 0;
+    int* d_fdlist = nullptr;
+    int* d_fd_uniq = nullptr;
+    int64_t* d_fd_uoff = nullptr;
+    int64_t* d_fd_loff = nullptr;
+    double* d_fdU = nullptr;
+    double* d_fdL = nullptr;
+    cudaStream_t stream2 = nullptr;          // side stream: the eigen kernel overlaps assembly
+    cudaEvent_t fd_fork = nullptr, fd_join = nullptr;
+    bool fd_pending = false;                 // fd_join not yet waited on by the main stream
     int* d_cperm = nullptr;        // combine: cell-order permutation of the points
     size_t cperm_cap = 0;
     int* d_chist = nullptr;        // combine: cell histogram / cursors

@@ -542,7 +542,7 @@ __global__ void k_residual(ChunkCtx X, double* relres, int skip_small) {
     __shared__ double red[64];
     const Chunk ch = X.chunks[blockIdx.x];
     const CompInfo& C = X.comps[ch.comp];
-    if (skip_small && C.small) return;   // the cluster PCG kernel checked these
+    if (C.fd || (skip_small && C.small)) return;   // the FD / cluster PCG kernels checked these
     double v[2] = {0.0, 0.0};
     if (threadIdx.x < ch.nrow) {
         int row = ch.row0 + threadIdx.x;
@@ -620,9 +620,18 @@ int run_pcg(Handle* h, double rtol, int maxit) {
     int nch = (int)h->chunks.size();
     const char* nc = getenv("SGIGA_NO_CLUSTER");
     h->small_checked = false;
+    if (!h->fd_comps.empty()) {   // FD-preconditioned CG (k_fd.cu), also checks its true residual
+        if (h->fd_pending) {
+            SG_CUDA(cudaStreamWaitEvent(h->stream, h->fd_join, 0));
+            h->fd_pending = false;
+        }
+        h->kstart(3);
+        SG_CUDA(launch_pcg_fd(h, rtol, maxit));
+        if (h->small_comps.empty()) h->kstop(3);
+    }
     if (!h->small_comps.empty() && !(nc && nc[0] == '1')) {
         h->small_checked = true;   // the cluster kernel also computes the true residual
-        h->kstart(3);
+        if (h->fd_comps.empty()) h->kstart(3);
         int st = launch_pcg_cluster(h, rtol, maxit);   // k_pcg_cluster.cu
         h->kstop(3);
         if (st) return st;
@@ -630,7 +639,7 @@ int run_pcg(Handle* h, double rtol, int maxit) {
         int64_t total = 0;
         size_t smem = small_smem_bytes(h, &total);
         int cap = (int)total;   // a CTA stages its matrix iff its vectors + matrix fit
-        h->kstart(3);
+        if (h->fd_comps.empty()) h->kstart(3);
 #define LAUNCH_SMALL(DD)                                                                         \
     SG_CUDA(cudaFuncSetAttribute(k_pcg_small<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                  (int)smem));                                                    \
@@ -758,7 +767,7 @@ cudaError_t launch_status(Handle* h) {
 cudaError_t launch_residual_check(Handle* h) {
     ChunkCtx X = make_ctx(h, 0.0, 0);
     int nch = (int)h->chunks.size();
-    if (nch == 0 || (h->small_checked && h->large_comps.empty())) return cudaSuccess;
+    if (nch == 0 || ((h->small_checked || h->small_comps.empty()) && h->large_comps.empty())) return cudaSuccess;
     const int sk = h->small_checked ? 1 : 0;
     if (h->d == 1) k_residual<1><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres, sk);
     else if (h->d == 2) k_residual<2><<<nch, CHUNK_ROWS, 0, h->stream>>>(X, h->d_relres, sk);

@@ -158,6 +158,33 @@ def test_reported_true_residual_matches_host_residual(name, monkeypatch):
         b.close()
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_fd_preconditioned_cg_matches_jacobi_pcg(name, monkeypatch):
+    """FD-preconditioned CG (k_fd.cu) vs the Jacobi-PCG paths: same
+    coefficients to solver tolerance, residual contract met; on the unit
+    cube the FD preconditioner is the exact inverse (<= 3 iterations)."""
+    cfg = configs.get_config(name)
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    res = {}
+    for mode in ("fd", "jacobi"):
+        if mode == "jacobi":
+            monkeypatch.setenv("SGIGA_NO_FD", "1")
+        b = Batch(spec)
+        try:
+            b.assemble()
+            it, rr = b.solve(rtol=1e-13)
+            res[mode] = (b.coefficients(), it.copy(), rr.copy())
+        finally:
+            b.close()
+    cf, itf, rrf = res["fd"]
+    cj, itj, _ = res["jacobi"]
+    assert np.all(rrf <= 1e-12)
+    assert rel_l2(cf, cj) <= 1e-11
+    assert itf.sum() < itj.sum()
+    if name == "cfg2":
+        assert itf.max() <= 3, itf
+
+
 def test_deterministic_bitwise():
     cfg = configs.get_config("cfg3")
     pts = cfg.points(1000)
@@ -424,7 +451,9 @@ def test_cfg5_full_pipeline(golden):
         # recursive residual <= 1e-13; the true residual drifts to ~5e-11 on the
         # kappa~1e6 (1,1,10) components and must meet linsolve.py:49-53 (1e-10)
         assert np.all(rr <= 1e-10)
-        assert int(it.sum()) == pytest.approx(408300, rel=0.01)   # SURVEY 8(d) CPU-CG count
+        # the reference-side Jacobi-CG needed 408300 iterations in
+        # total; the FD-preconditioned small components take fewer, never more
+        assert 0 < int(it.sum()) <= 1.01 * 408300
         coefs = b.coefficients()
         # checksum of checksums: per-component norm and seeded dot product
         for c in range(len(cfg.plan)):
