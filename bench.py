@@ -3,7 +3,8 @@
 
 Metric (BASELINE.json): components solved/s & DoF/s (assemble+CG+combine),
 % of FP64/HBM roofline.  One "step" = the whole hot path on one plan:
-assemble every component, solve every component (Jacobi-PCG to 1e-13),
+assemble every component, solve every component (PCG to 1e-13: FD-
+preconditioned for the small components, Jacobi for the large ones),
 combine at the configuration's evaluation points.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
@@ -183,7 +184,9 @@ def run_sgiga(args, cfg):
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    R = max(1, args.replicas)
+    terms = tuple(cfg.plan.terms) * R       # replicated batch: R copies, one launch
+    spec = make_spec(terms, cfg.problem, cfg.quad_points)
     batch = Batch(spec)
     stream = torch.cuda.ExternalStream(batch.stream_ptr)
     pts_h = cfg.points()
@@ -228,14 +231,19 @@ def run_sgiga(args, cfg):
         total_ms = float(t.item())
         dist.barrier()
     ms_per_step = total_ms / args.steps
-    n_comp = len(cfg.plan)
+    n_comp = len(terms)
     iters = batch.iters.copy()
     vals = out_d.cpu().numpy()
 
     # ---- canonical work and rooflines ---------------------------------------
     dims = [tuple(int(x) for x in row) for row in batch.dims]
-    lookup = {tuple(b): dims[i] for i, (b, _) in enumerate(cfg.plan.terms)}
-    work = canonical_work(cfg.plan, spec.degree, spec.quad_points, spec.d, lambda b: lookup[tuple(b)])
+    lookup = {tuple(b): dims[i] for i, (b, _) in enumerate(terms)}
+
+    class _Terms:   # canonical_work only reads .terms
+        pass
+    plan_r = _Terms()
+    plan_r.terms = terms
+    work = canonical_work(plan_r, spec.degree, spec.quad_points, spec.d, lambda b: lookup[tuple(b)])
     dofs = sum(w["dofs"] for w in work)
     kt = kt_acc / args.steps   # ms per launch group per step
     cg_bytes = sum(int(it) * (8 * w["nnz"] + 104 * w["rows"]) for it, w in zip(iters, work))
@@ -283,7 +291,20 @@ def run_sgiga(args, cfg):
                     "peak_source": G["peak_source"]}
 
     # ---- end to end through the public API, host buffers ---------------------
-    sess = PlanSession(cfg.plan, cfg.problem, cfg.quad_points, rtol=args.rtol)
+    if R == 1:
+        sess = PlanSession(cfg.plan, cfg.problem, cfg.quad_points, rtol=args.rtol)
+    else:   # replicated batch: the same public call on the replicated spec
+        class _Sess:
+            def __init__(self):
+                self.b = Batch(spec)
+                self.h2d_input_bytes = int(sum(a.nbytes for a in self.b._keep.values()))
+
+            def run(self, pts):
+                return self.b.run(pts, args.rtol)
+
+            def close(self):
+                self.b.close()
+        sess = _Sess()
     pin = torch.empty(pts_h.shape, dtype=torch.float64, pin_memory=True)
     pin.copy_(torch.from_numpy(pts_h))
     pts_pinned = pin.numpy()
@@ -323,6 +344,7 @@ def run_sgiga(args, cfg):
             "config": {"workload": cfg.name, "d": d, "degree": spec.degree, "level_w": cfg.plan.level,
                        "components": n_comp, "points": npts, "dofs": dofs, "quad_points": spec.quad_points,
                        "rtol": args.rtol, "l2_flush": "256 MB write before every timed step",
+                       "replicas": R,
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
             "dof_per_s": ws * dofs / (ms_per_step * 1e-3),
             "e2e": {"value": ws * n_comp / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -357,6 +379,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=None,
                     help="reference arm: components per step (default: all for cfg1-3, 12 for cfg5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", type=int, default=1,
+                    help="replicated batch: R copies of the plan in one launch (SURVEY 8(d) roofline scaling)")
     args = ap.parse_args()
     from paper_1707_09598_b200.configs import get_config
 

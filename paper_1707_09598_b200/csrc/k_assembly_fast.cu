@@ -143,15 +143,44 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const int xb_lo = D >= 3 ? tb_lo * Q : 0, nxb = D >= 3 ? (tb_hi - tb_lo) * Q : 1;
     const int64_t Xa0 = D >= 2 ? (int64_t)(pc.ia - p) * Q + xa_lo : 0;   // first valid global a index
     const int64_t Xb0 = D >= 3 ? (int64_t)(pc.ib - p) * Q + xb_lo : 0;
+    // every plane copies the same (entry, xb, xa) window: each thread's share
+    // (smem offset, offset from the plane's first valid point) is decoded
+    // once per pencil, so a plane costs a few instructions per copy
+    constexpr int MAXC0 = (F::NG * F::NB * F::NA + FAST_THREADS - 1) / FAST_THREADS;
+    constexpr bool PRE = MAXC0 <= 8;            // else: row teams, one division per row
+    constexpr int MAXC = PRE ? MAXC0 : 1;
+    int c_sm[MAXC], c_gl[MAXC];
+    constexpr int LPR = F::NA <= 16 ? 16 : 32, NTEAM = FAST_THREADS / LPR;
+    const int team = tid / LPR, tl_ = tid % LPR;
+    if constexpr (PRE) {
+        const int per_row = nxa, ntot = F::NG * nxb * nxa;
+#pragma unroll
+        for (int k = 0; k < MAXC; ++k) {
+            const int idx = tid + k * FAST_THREADS;
+            c_sm[k] = -1;
+            c_gl[k] = 0;
+            if (idx < ntot) {
+                const int xa = idx % per_row, r = idx / per_row;
+                const int xb = r % nxb, gi = r / nxb;
+                c_sm[k] = (gi * F::NB + xb_lo + xb) * F::NAP + xa_lo + xa;
+                c_gl[k] = (int)((int64_t)gi * nqp + (int64_t)xb * qs_b + xa);
+            }
+        }
+    }
     auto load_plane = [&](int64_t Qs, int buf) {
         double* Gw = sm + F::oGw + buf * F::nGw;
         const double* base = Gc + Qs * qs_s + Xa0 + Xb0 * qs_b;
-        const int per_row = nxa, rows = F::NG * nxb;
-        for (int idx = tid; idx < rows * per_row; idx += FAST_THREADS) {
-            const int xa = idx % per_row, r = idx / per_row;
-            const int xb = r % nxb, gi = r / nxb;
-            cp_async8(&Gw[(gi * F::NB + xb_lo + xb) * F::NAP + xa_lo + xa],
-                      base + (int64_t)gi * nqp + (int64_t)xb * qs_b + xa);
+        if constexpr (PRE) {
+#pragma unroll
+            for (int k = 0; k < MAXC; ++k)
+                if (c_sm[k] >= 0) cp_async8(&Gw[c_sm[k]], base + c_gl[k]);
+        } else if (tl_ < nxa) {
+            const int rows = F::NG * nxb;
+            for (int r = team; r < rows; r += NTEAM) {
+                const int gi = r / nxb, xb = r - gi * nxb;
+                cp_async8(&Gw[(gi * F::NB + xb_lo + xb) * F::NAP + xa_lo + tl_],
+                          base + (int64_t)gi * nqp + (int64_t)xb * qs_b + tl_);
+            }
         }
         cp_async_commit();
     };
@@ -180,9 +209,19 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         flt_rel[cab] = (oa < 0 || ob < 0) ? -1 : oa * F::WB + ob;
         flt_slot[cab] = (int)((D >= 2 ? (int64_t)ca * C.ss[ka] : 0) + (D >= 3 ? (int64_t)cb * C.ss[kb] : 0));
     }
-    int tsp[NPAIR];   // stream type of each (m, n) pair
+    int tsp[NPAIR], tap[NPAIR];   // stream / tile-a type of each (m, n) pair
 #pragma unroll
-    for (int pr = 0; pr < NPAIR; ++pr) tsp[pr] = 2 * ((pr / D) == s) + ((pr % D) == s);
+    for (int pr = 0; pr < NPAIR; ++pr) {
+        tsp[pr] = 2 * ((pr / D) == s) + ((pr % D) == s);
+        tap[pr] = 2 * ((pr / D) == ka) + ((pr % D) == ka);
+    }
+    // this thread's stage-2 item (one per thread: 4 W^2 + 1 <= FAST_THREADS)
+    static_assert(4 * F::WAB + 1 <= FAST_THREADS, "one stage-2 item per thread");
+    const int i2_it = tid;
+    const bool i2_on = D >= 2 && i2_it < 4 * F::WAB + 1, i2_load = i2_it == 4 * F::WAB;
+    const int i2_ts = i2_it / F::WAB, i2_sab = i2_it % F::WAB;
+    const int i2_sa = i2_sab / F::WB, i2_sb = i2_sab % F::WB;
+    const int i2_tl = max(ta_lo, i2_sa - p), i2_th = min(ta_hi - 1, i2_sa);
 
     int buf = 0;
     const bool pr = prof != nullptr && blockIdx.x == 0 && tid == 0;   // phase profile
@@ -247,36 +286,38 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             if constexpr (D >= 2) {
                 // one pass: S2[ts][sa][sb] = sum over the pairs of stream type ts,
                 // window elements t with k = sa - t in [0, p], and their Q points
-                for (int it = tid; it < 4 * F::WAB + 1; it += FAST_THREADS) {
-                    if (it == 4 * F::WAB) {   // load: SL2 = sum_xa SL1 phiA
+                // the item (decoded once per pencil, see i2_*) is the same for
+                // every plane: compile-time (t, g2) loops with predication give
+                // immediate-offset loads, ~3 instructions per FMA
+                if (i2_on) {
+                    if (i2_load) {   // load: SL2 = sum_xa SL1 phiA
                         double acc = 0.0;
 #pragma unroll
                         for (int x = 0; x < F::NA; ++x)
                             acc += (D == 3 ? SL1[x] : Gw[(F::NG - 1) * F::NAP + x]) * phiA[x];
                         S2[4 * F::WAB] = acc;
-                        continue;
-                    }
-                    const int sab = it % F::WAB, ts = it / F::WAB;
-                    const int sa = sab / F::WB, sb = sab % F::WB;
-                    const int tl = max(ta_lo, sa - p), th = min(ta_hi - 1, sa);
-                    double acc0 = 0.0, acc1 = 0.0;
+                    } else {
+                        double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
-                    for (int pr = 0; pr < NPAIR; ++pr) {
-                        if (tsp[pr] != ts) continue;
-                        const int ta = 2 * ((pr / D) == ka) + ((pr % D) == ka);
-                        for (int t = tl; t <= th; ++t) {
-                            const double* tr = Ta + (ta * F::NA + t * Q) * P + (sa - t);
+                        for (int prr = 0; prr < NPAIR; ++prr) {
+                            if (tsp[prr] != i2_ts) continue;
+                            const double* sp = D == 3 ? S1 + prr * F::NA * W + i2_sb
+                                                      : Gw + sym_index(D, prr / D, prr % D) * F::NAP;
+                            const int sstr = D == 3 ? W : 1;
+                            const double* tp0 = Ta + tap[prr] * F::NA * P + i2_sa;
 #pragma unroll
-                            for (int g2 = 0; g2 < Q; ++g2) {
-                                const int xa = t * Q + g2;
-                                const double sv = D == 3 ? S1[(pr * F::NA + xa) * W + sb]
-                                                         : Gw[sym_index(D, pr / D, pr % D) * F::NAP + xa];
-                                if (g2 & 1) acc1 += sv * tr[g2 * P];
-                                else acc0 += sv * tr[g2 * P];
+                            for (int t = 0; t < P; ++t) {
+                                if (t < i2_tl || t > i2_th) continue;
+#pragma unroll
+                                for (int g2 = 0; g2 < Q; ++g2) {
+                                    const int xa = t * Q + g2;
+                                    const double v = sp[xa * sstr] * tp0[xa * P - t];
+                                    if (g2 & 1) acc1 += v; else acc0 += v;
+                                }
                             }
                         }
+                        S2[i2_it] = acc0 + acc1;
                     }
-                    S2[it] = acc0 + acc1;
                 }
                 if (pr) { long long t = clock64(); tp[2] += t - tc; tc = t; }
             } else {
