@@ -63,8 +63,12 @@ struct FastCfg {
     static constexpr int oS1 = oPhiB + NB;             // [NPAIR][NA][WB]
     static constexpr int oSL1 = oS1 + NPAIR * NA * WB; // [NA]
     static constexpr int oP2 = oSL1 + NA;              // [NPAIR][P][P][WB]
-    static constexpr int oS2 = oP2 + NPAIR * P * P * WB;  // [4][WAB] + load
-    static constexpr int oBs = oS2 + 4 * WAB + 1;      // [2][Q][P]
+    // stage-2 output slots: the 4 stream types, type 0 (4 pairs in 3-D) split
+    // in two halves when the threads allow, + the load term
+    static constexpr bool SPLIT = D == 3 && 5 * WAB + 1 <= 352;
+    static constexpr int NT2 = SPLIT ? 5 : 4;
+    static constexpr int oS2 = oP2 + NPAIR * P * P * WB;  // [NT2][WAB] + load
+    static constexpr int oBs = oS2 + NT2 * WAB + 1;    // [2][Q][P]
     static constexpr int oAcc = oBs + 2 * Q * P;       // [RING][W][WAB]
     static constexpr int oAccL = oAcc + RING * W * WAB;
     static constexpr int total = oAccL + RING;
@@ -216,10 +220,23 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         tap[pr] = 2 * ((pr / D) == ka) + ((pr % D) == ka);
     }
     // this thread's stage-2 item (one per thread: 4 W^2 + 1 <= FAST_THREADS)
-    static_assert(4 * F::WAB + 1 <= FAST_THREADS, "one stage-2 item per thread");
+    constexpr int NT2 = F::NT2, LOAD2 = NT2 * F::WAB;
+    static_assert(LOAD2 + 1 <= FAST_THREADS, "one stage-2 item per thread");
     const int i2_it = tid;
-    const bool i2_on = D >= 2 && i2_it < 4 * F::WAB + 1, i2_load = i2_it == 4 * F::WAB;
-    const int i2_ts = i2_it / F::WAB, i2_sab = i2_it % F::WAB;
+    const bool i2_on = D >= 2 && i2_it < LOAD2 + 1, i2_load = i2_it == LOAD2;
+    const int i2_slot = i2_it / F::WAB, i2_sab = i2_it % F::WAB;
+    const int i2_ts = i2_slot == 4 ? 0 : i2_slot;
+    int i2_mask = 0;   // pairs this item sums (slots 0 / 4 take the first / last half of type 0)
+    {
+        int c0 = 0;
+#pragma unroll
+        for (int pr = 0; pr < NPAIR; ++pr) {
+            if (tsp[pr] != i2_ts) continue;
+            const bool take = !F::SPLIT || i2_ts != 0 || ((i2_slot == 4) == (c0 >= 2));
+            if (i2_ts == 0) ++c0;
+            if (take) i2_mask |= 1 << pr;
+        }
+    }
     const int i2_sa = i2_sab / F::WB, i2_sb = i2_sab % F::WB;
     const int i2_tl = max(ta_lo, i2_sa - p), i2_th = min(ta_hi - 1, i2_sa);
 
@@ -295,12 +312,12 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 #pragma unroll
                         for (int x = 0; x < F::NA; ++x)
                             acc += (D == 3 ? SL1[x] : Gw[(F::NG - 1) * F::NAP + x]) * phiA[x];
-                        S2[4 * F::WAB] = acc;
+                        S2[LOAD2] = acc;
                     } else {
                         double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
                         for (int prr = 0; prr < NPAIR; ++prr) {
-                            if (tsp[prr] != i2_ts) continue;
+                            if (!((i2_mask >> prr) & 1)) continue;
                             const double* sp = D == 3 ? S1 + prr * F::NA * W + i2_sb
                                                       : Gw + sym_index(D, prr / D, prr % D) * F::NAP;
                             const int sstr = D == 3 ? W : 1;
@@ -332,8 +349,8 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 const int i = e + al;
                 if (i < r0 || i >= r1) continue;
                 const double va = Bs[g * P + al], da = Bs[Q * P + g * P + al];
-                const double s0 = S2[sab], s1 = S2[F::WAB + sab], s2v = S2[2 * F::WAB + sab],
-                             s3 = S2[3 * F::WAB + sab];
+                const double s0 = F::SPLIT ? S2[sab] + S2[4 * F::WAB + sab] : S2[sab];
+                const double s1 = S2[F::WAB + sab], s2v = S2[2 * F::WAB + sab], s3 = S2[3 * F::WAB + sab];
                 const double c0 = va * s0 + da * s2v, c1 = va * s1 + da * s3;
                 double* acc = Acc + ((i % F::RING) * W) * F::WAB + sab;
 #pragma unroll
@@ -344,7 +361,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             }
             if (tid < P) {
                 const int i = e + tid;
-                if (i >= r0 && i < r1) AccL[i % F::RING] += Bs[g * P + tid] * S2[4 * F::WAB];
+                if (i >= r0 && i < r1) AccL[i % F::RING] += Bs[g * P + tid] * S2[LOAD2];
             }
             buf ^= 1;
             if (pr) { long long t = clock64(); tp[4] += t - tc; tc = t; tp[6] += 1; }

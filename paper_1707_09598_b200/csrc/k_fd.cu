@@ -28,7 +28,7 @@
 namespace sgiga {
 
 constexpr int FD_THREADS = 256;
-constexpr int EIG_THREADS = 1024;
+constexpr int EIG_THREADS = 512;
 constexpr int EIG_ITEMS = ((FD_MMAX / 2) * (FD_MMAX / 2) + (FD_MMAX / 2) * FD_MMAX + EIG_THREADS - 1) / EIG_THREADS;
 constexpr int FD_LD = FD_MMAX + 1;   // padded row stride of the eigen work arrays
 
@@ -48,10 +48,29 @@ __device__ __forceinline__ double fd_block_sum(double v, double* red) {
 }
 
 // ---- 3a: generalized eigen-decomposition of the 1-D interior pencils ------
-// Jacobi step = (rotation of every pair of the round-robin pairing) then ONE
-// pass of fused two-sided 2x2 block updates J_k^T C_kl J_l (every entry of C
-// belongs to exactly one (pair k, pair l) block, so the pass is race-free)
+// Persymmetric pencils (symmetric knot vectors, e.g. uniform): M and K
+// commute with the exchange J, so the pencil splits exactly into its even
+// (dimension ceil(m/2)) and odd (floor(m/2)) halves, solved side by side --
+// half the Jacobi steps, a quarter of the work per step.  Both halves sit
+// block-diagonally in one m x m array, so the banded Cholesky and the
+// substitutions run unchanged (each half is banded with bandwidth p).
+// Jacobi step = rotations of every pair of the round-robin pairings (one per
+// half) then ONE pass of fused two-sided 2x2 block updates J_k^T C_kl J_l
+// (every entry of C belongs to exactly one (pair k, pair l) block: race-free)
 // plus the column rotations of V: two barriers per step.
+__device__ __forceinline__ double fd_block_max(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < EIG_THREADS / 32; ++w) s = fmax(s, red[w]);
+    return s;
+}
+
 __global__ void __launch_bounds__(EIG_THREADS)
 k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
            const int64_t* __restrict__ uoff, const int64_t* __restrict__ loff,
@@ -60,8 +79,9 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
     extern __shared__ double fsm[];
     long long t0 = clock64();
     auto stamp = [&](int k) { if (prof && threadIdx.x == 0) prof[blockIdx.x * 8 + k] = clock64() - t0; };
-    __shared__ double rc[FD_MMAX / 2 + 1], rs[FD_MMAX / 2 + 1], red[EIG_THREADS / 32];
-    __shared__ int rp[FD_MMAX / 2 + 1], rq[FD_MMAX / 2 + 1];
+    constexpr int NPMAX = FD_MMAX / 2 + 1;
+    __shared__ double rc[NPMAX + 1], rs[NPMAX + 1], red[EIG_THREADS / 32];
+    __shared__ int rp[NPMAX + 1], rq[NPMAX + 1];
     const int t = uniq[blockIdx.x];
     const TabInfo T = tabs[t];
     const int m = T.n - 2, tid = threadIdx.x, P = p + 1;
@@ -74,6 +94,7 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
     const double* w = qw + T.qp_off;
 
     // interior mass / stiffness (global functions 1..n-2), band |i-j| <= p
+    double dmx = 0.0, amx = 0.0;
     for (int idx = tid; idx < m * m; idx += EIG_THREADS) {
         const int i = idx / m, j = idx % m, gi = i + 1, gj = j + 1;
         double mv = 0.0, kv = 0.0;
@@ -93,8 +114,49 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
         }
         L[i * FD_LD + j] = mv;
         Cm[i * FD_LD + j] = kv;
-        V[i * FD_LD + j] = (i == j) ? 1.0 : 0.0;
     }
+    __syncthreads();
+    // persymmetry test (relative to the largest entry; K dominates the scale)
+    for (int idx = tid; idx < m * m; idx += EIG_THREADS) {
+        const int i = idx / m, j = idx % m, ii = m - 1 - i, jj = m - 1 - j;
+        dmx = fmax(dmx, fmax(fabs(L[i * FD_LD + j] - L[ii * FD_LD + jj]),
+                             fabs(Cm[i * FD_LD + j] - Cm[ii * FD_LD + jj]) * 1e-6));
+        amx = fmax(amx, fmax(fabs(L[i * FD_LD + j]), fabs(Cm[i * FD_LD + j]) * 1e-6));
+    }
+    dmx = fd_block_max(dmx, red);
+    amx = fd_block_max(amx, red);
+    const bool sym = m >= 2 && dmx <= 1e-13 * amx;
+    const int h = m / 2, ms = sym ? m - h : m, ma = sym ? h : 0;
+    const double r2 = 0.70710678118654752440;
+    // column c of the even / odd basis S: entries (index, weight)
+    auto sbasis = [&](int c, int* ix, double* wt) -> int {   // c < ms
+        if (c < h) { ix[0] = c; wt[0] = r2; ix[1] = m - 1 - c; wt[1] = r2; return 2; }
+        ix[0] = h; wt[0] = 1.0; return 1;                      // the middle function (m odd)
+    };
+    if (sym) {   // L, Cm <- S^T M S (+) A^T M A, block-diagonal (V as scratch)
+        for (int pass = 0; pass < 2; ++pass) {
+            double* X = pass ? Cm : L;
+            for (int idx = tid; idx < m * m; idx += EIG_THREADS) {
+                const int i = idx / m, j = idx % m;
+                double v = 0.0;
+                if (i < ms && j < ms) {
+                    int ia[2], ja[2];
+                    double wa[2], wb[2];
+                    const int na = sbasis(i, ia, wa), nb = sbasis(j, ja, wb);
+                    for (int x = 0; x < na; ++x)
+                        for (int y = 0; y < nb; ++y) v += wa[x] * wb[y] * X[ia[x] * FD_LD + ja[y]];
+                } else if (i >= ms && j >= ms) {
+                    const int a = i - ms, b = j - ms, a2 = m - 1 - a, b2 = m - 1 - b;
+                    v = 0.5 * ((X[a * FD_LD + b] - X[a * FD_LD + b2]) - (X[a2 * FD_LD + b] - X[a2 * FD_LD + b2]));
+                }
+                V[i * FD_LD + j] = v;
+            }
+            __syncthreads();
+            for (int idx = tid; idx < m * m; idx += EIG_THREADS) X[(idx / m) * FD_LD + idx % m] = V[(idx / m) * FD_LD + idx % m];
+            __syncthreads();
+        }
+    }
+    for (int idx = tid; idx < m * m; idx += EIG_THREADS) V[(idx / m) * FD_LD + idx % m] = (idx / m == idx % m) ? 1.0 : 0.0;
     __syncthreads();
     stamp(0);
     // banded Cholesky M = L L^T (lower triangle of L)
@@ -141,17 +203,25 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
     }
     __syncthreads();
     stamp(2);
-    // cyclic parallel Jacobi, round-robin pairing (n even; index m is a dummy)
-    const int n = (m & 1) ? m + 1 : m, np = n / 2;
+    // cyclic parallel Jacobi: one round-robin pairing per half (block b at
+    // offset ob, size sb, padded to nb even; local index sb is a dummy)
+    const int o1 = ms, s0 = ms, s1 = ma;
+    const int n0 = s0 + (s0 & 1), n1 = s1 + (s1 & 1), np0 = n0 / 2, np1 = n1 / 2, npt = np0 + np1;
+    const int nsteps = max(n0, n1) - 1;
+    const int nc0 = np0 * np0, nc1 = np1 * np1, ncs = nc0 + nc1;
+    const int nitems = ncs + np0 * s0 + np1 * s1;
     int nsweep = 0;
-    // this thread's update items, decoded once: (pair k, pair l) blocks of C,
-    // then (pair k, row i) rotations of V
+    // this thread's update items, decoded once: (pair k, pair l) blocks of C
+    // (same half), then (pair k, row i of its half) rotations of V
     int dk_[EIG_ITEMS], dl_[EIG_ITEMS];
 #pragma unroll
     for (int u = 0; u < EIG_ITEMS; ++u) {
         const int idx = tid + u * EIG_THREADS;
-        if (idx < np * np) { dk_[u] = idx / np; dl_[u] = idx % np; }
-        else { const int r = idx - np * np; dk_[u] = r / max(m, 1); dl_[u] = r % max(m, 1); }
+        dk_[u] = 0; dl_[u] = 0;
+        if (idx < nc0) { dk_[u] = idx / np0; dl_[u] = idx % np0; }
+        else if (idx < ncs) { const int r = idx - nc0; dk_[u] = np0 + r / np1; dl_[u] = np0 + r % np1; }
+        else if (idx < ncs + np0 * s0) { const int r = idx - ncs; dk_[u] = r / s0; dl_[u] = r % s0; }
+        else if (idx < nitems) { const int r = idx - ncs - np0 * s0; dk_[u] = np0 + r / s1; dl_[u] = o1 + r % s1; }
     }
     // stop at ||offdiag|| <= 1e-13 ||diag||: below that the off-diagonal is
     // rounding noise of the rotations (~eps * lambda_max per entry); the
@@ -167,17 +237,24 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
         dia = fd_block_sum<EIG_THREADS>(dia, red);
         if (off <= 1e-26 * dia) break;
         ++nsweep;
-        for (int s = 0; s < n - 1; ++s) {
-            if (tid < np) {   // rotation of pair tid (round-robin pairing, step s)
-                int a, b;
-                if (tid == 0) { a = n - 1; b = s; }
-                else {   // (s + tid) mod (n-1), (s - tid) mod (n-1) without integer division
-                    a = s + tid; if (a >= n - 1) a -= n - 1;
-                    b = s - tid; if (b < 0) b += n - 1;
-                }
-                const int pi = min(a, b), qi = max(a, b);
+        for (int st = 0; st < nsteps; ++st) {
+            if (tid < npt) {   // rotation of pair tid (its half's round-robin pairing, step st)
+                const int b = tid < np0 ? 0 : 1, k = b ? tid - np0 : tid;
+                const int nb = b ? n1 : n0, sb = b ? s1 : s0, ob = b ? o1 : 0;
+                int pi = -1, qi = -1;
                 double c = 1.0, sn = 0.0;
-                if (qi < m) {
+                if (st < nb - 1) {
+                    int a, bb;
+                    if (k == 0) { a = nb - 1; bb = st; }
+                    else {   // (st + k) mod (nb-1), (st - k) mod (nb-1) without integer division
+                        a = st + k; if (a >= nb - 1) a -= nb - 1;
+                        bb = st - k; if (bb < 0) bb += nb - 1;
+                    }
+                    const int lo = min(a, bb), hi = max(a, bb);
+                    if (hi < sb) { pi = ob + lo; qi = ob + hi; }
+                    else if (lo < sb) { pi = ob + lo; }   // paired with the dummy
+                }
+                if (qi >= 0) {
                     const double apq = Cm[pi * FD_LD + qi];
                     const double app = Cm[pi * FD_LD + pi], aqq = Cm[qi * FD_LD + qi];
                     if (apq != 0.0 && apq * apq > 1e-36 * fabs(app * aqq)) {
@@ -193,14 +270,14 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
 #pragma unroll
             for (int u = 0; u < EIG_ITEMS; ++u) {
                 const int idx = tid + u * EIG_THREADS;
-                if (idx >= np * np + np * m) break;
-                if (idx < np * np) {   // block (pair k rows) x (pair l columns)
+                if (idx >= nitems) break;
+                if (idx < ncs) {   // block (pair k rows) x (pair l columns)
                     const int k = dk_[u], l = dl_[u];
                     const double sk = rs[k], sl = rs[l];
                     if (sk == 0.0 && sl == 0.0) continue;
                     const int pk = rp[k], qk = rq[k], pl = rp[l], ql = rq[l];
                     const double ck = rc[k], cl = rc[l];
-                    const bool hq = qk < m, hl = ql < m;
+                    const bool hq = qk >= 0, hl = ql >= 0;   // (pk, pl exist: a rotating pair has both)
                     double a = Cm[pk * FD_LD + pl];
                     double b = hl ? Cm[pk * FD_LD + ql] : 0.0;
                     double c = hq ? Cm[qk * FD_LD + pl] : 0.0;
@@ -218,9 +295,8 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
                 } else {               // V J_k, row i
                     const int k = dk_[u], i = dl_[u];
                     const double sk = rs[k];
-                    const int qk = rq[k];
-                    if (qk >= m || sk == 0.0) continue;
-                    const int pk = rp[k];
+                    if (sk == 0.0) continue;
+                    const int pk = rp[k], qk = rq[k];
                     const double ck = rc[k];
                     const double va = V[i * FD_LD + pk], vb = V[i * FD_LD + qk];
                     V[i * FD_LD + pk] = ck * va - sk * vb;
@@ -231,8 +307,8 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
         }
     }
     stamp(3);
-    if (prof && tid == 0) { prof[blockIdx.x * 8 + 5] = nsweep; prof[blockIdx.x * 8 + 6] = m; }
-    // U = L^-T Q (column j per thread, back substitution with the band of L)
+    if (prof && tid == 0) { prof[blockIdx.x * 8 + 5] = nsweep; prof[blockIdx.x * 8 + 6] = m + (sym ? 1000 : 0); }
+    // U' = L^-T Q (column j per thread, back substitution with the band of L)
     if (tid < m) {
         const int j = tid;
         for (int i = m - 1; i >= 0; --i) {
@@ -242,10 +318,15 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
         }
     }
     __syncthreads();
+    // back to the original basis: u = S u' (even half) or A u' (odd half)
     double* U = dU + uoff[t];
     for (int idx = tid; idx < m * m; idx += EIG_THREADS) {
         const int a = idx / m, j = idx % m;   // eigenvector a, entry j
-        U[idx] = V[j * FD_LD + a];
+        double v;
+        if (!sym) v = V[j * FD_LD + a];
+        else if (a < ms) v = (j < h) ? r2 * V[j * FD_LD + a] : (j >= m - h ? r2 * V[(m - 1 - j) * FD_LD + a] : V[h * FD_LD + a]);
+        else v = (j < h) ? r2 * V[(ms + j) * FD_LD + a] : (j >= m - h ? -r2 * V[(ms + m - 1 - j) * FD_LD + a] : 0.0);
+        U[idx] = v;
     }
     for (int a = tid; a < m; a += EIG_THREADS) dL[loff[t] + a] = Cm[a * FD_LD + a];
     stamp(4);
