@@ -52,7 +52,13 @@ struct FastCfg {
     static constexpr int NG = D * (D + 1) / 2 + 1;     // metric entries + load
     static constexpr int NPAIR = D * D;
     static constexpr int PPW = NX <= 16 ? 2 : 1;       // pairs per warp in stage 1
-    static constexpr int RING = P;                     // alive rows of one element
+    // software-pipelined 3-D variant: stage 1 of plane j and stage 3 of plane
+    // j-1 share one barrier interval (disjoint thread groups); needs the
+    // stage-1 units in <= 192 threads, a ring of P+1 rows (a flushed row's
+    // slot is zeroed one interval later) and two stream-basis buffers
+    static constexpr int S1T = 32 * ((NPAIR + 1 + PPW - 1) / PPW);
+    static constexpr bool PIPE = D == 3 && S1T <= 192;
+    static constexpr int RING = PIPE ? P + 1 : P;      // alive rows (+1 draining)
     static constexpr int nGw = NG * NB * NAP;          // one plane buffer
     // shared-memory layout (doubles)
     static constexpr int oGw = 0;                      // [2][NG][NB][NAP]
@@ -69,7 +75,7 @@ struct FastCfg {
     static constexpr int NT2 = SPLIT ? 5 : 4;
     static constexpr int oS2 = oP2 + NPAIR * P * P * WB;  // [NT2][WAB] + load
     static constexpr int oBs = oS2 + NT2 * WAB + 1;    // [2][Q][P]
-    static constexpr int oAcc = oBs + 2 * Q * P;       // [RING][W][WAB]
+    static constexpr int oAcc = oBs + (PIPE ? 4 : 2) * Q * P;   // Bs: [PIPE ? 2 : 1][2][Q][P]; Acc: [RING][W][WAB]
     static constexpr int oAccL = oAcc + RING * W * WAB;
     static constexpr int total = oAccL + RING;
 };
@@ -241,6 +247,163 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const int i2_tl = max(ta_lo, i2_sa - p), i2_th = min(ta_hi - 1, i2_sa);
 
     int buf = 0;
+    // flush of one completed row: every storage slot is written (zeros where
+    // the relative offset is out of the band or the column is on the boundary)
+    auto flush_row = [&](int i) {
+        const int64_t row = row_base + (int64_t)(i - 1) * rs_s;
+        const double* accr = Acc + ((i % F::RING) * W) * F::WAB;
+        double* dst = stencil + C.mat_off + row;
+        for (int it = tid; it < Ss * SAB; it += FAST_THREADS) {
+            const int cab = it % SAB, cs = it / SAB;
+            const int j = absm_s ? cs + 1 : i + cs - p, o = j - i;   // stream-axis column
+            const int oab = flt_rel[cab];
+            const bool ok = oab >= 0 && j >= 1 && j <= n_s - 2 && o >= -p && o <= p;
+            const double v = ok ? accr[(o + p) * F::WAB + oab] : 0.0;
+            dst[((int64_t)cs * ss_s + flt_slot[cab]) * rows_c] = v;
+        }
+        if (tid == 0) {
+            const int dsab = D >= 2 ? (p * F::WB + (D >= 3 ? p : 0)) : 0;
+            rhs[C.vec_off + row] = AccL[i % F::RING];
+            dinv[C.vec_off + row] = 1.0 / accr[p * F::WAB + dsab];
+        }
+    };
+    if constexpr (F::PIPE) {
+        // interval j: [issue plane j+1, wait plane j] B1 [threads < S1T: stage 1
+        // of plane j (+ zero the ring slot flushed last interval) | the rest:
+        // stage 3 of plane j-1] B2 [stage 2 of plane j; flush the row element
+        // e(j-1) completed]; j = nplanes drains the last stage 3 and flushes
+        constexpr int S1T = F::S1T, S3T = FAST_THREADS - F::S1T;
+        const int nplanes = (e_last - e_first + 1) * Q;
+        auto load_bs = [&](int e) {
+            double* Bd = Bs + (e & 1) * 2 * Q * P;
+            for (int idx = tid; idx < 2 * Q * P; idx += FAST_THREADS) {
+                const int der = idx / (Q * P), rem = idx % (Q * P);
+                Bd[idx] = vals[Ts.val_off + (der ? nq_s * P : 0) + (int64_t)e * Q * P + rem];
+            }
+        };
+        if (nplanes > 0) {
+            load_bs(e_first);
+            load_plane((int64_t)e_first * Q, 0);
+        }
+        int zrow = -1;
+        for (int j = 0; j <= nplanes; ++j) {
+            const bool has = j < nplanes;
+            const int e = e_first + j / Q, g = j % Q;
+            if (has) {
+                if (j + 1 < nplanes) {
+                    load_plane((int64_t)e_first * Q + j + 1, buf ^ 1);
+                    cp_async_wait_prev();
+                } else {
+                    cp_async_wait_all();
+                }
+                if (g == 0 && j > 0) load_bs(e);
+            }
+            __syncthreads();   // B1
+            const double* Gw = sm + F::oGw + buf * F::nGw;
+            if (tid < S1T) {
+                if (has) {   // ---- stage 1 (plane j): contract tile axis b ----
+                    const int half = F::PPW == 2 ? (lane >> 4) : 0;
+                    const int xa = F::PPW == 2 ? (lane & 15) : lane;
+                    const int prr = warp * F::PPW + half;
+                    if (prr < NPAIR && xa < F::NA) {
+                        const int gidx = sym_index(D, prr / D, prr % D);
+                        const int tb = 2 * ((prr / D) == kb) + ((prr % D) == kb);
+                        double acc[W];
+#pragma unroll
+                        for (int q2 = 0; q2 < W; ++q2) acc[q2] = 0.0;
+                        const double* gcol = Gw + gidx * F::NB * F::NAP + xa;
+                        const double* tr = Tb + tb * F::NB * P;
+#pragma unroll
+                        for (int t = 0; t < P; ++t) {
+                            if (t < tb_lo || t >= tb_hi) continue;
+#pragma unroll
+                            for (int g2 = 0; g2 < Q; ++g2) {
+                                const int x = t * Q + g2;
+                                const double gv = gcol[x * F::NAP];
+#pragma unroll
+                                for (int k = 0; k < P; ++k) acc[t + k] += gv * tr[x * P + k];
+                            }
+                        }
+                        double* out = S1 + (prr * F::NA + xa) * W;
+#pragma unroll
+                        for (int q2 = 0; q2 < W; ++q2) out[q2] = acc[q2];
+                    } else if (prr == NPAIR && xa < F::NA) {   // load: SL1 = sum_xb L phiB
+                        const double* gcol = Gw + (F::NG - 1) * F::NB * F::NAP + xa;
+                        double acc = 0.0;
+#pragma unroll
+                        for (int x = 0; x < F::NB; ++x) acc += gcol[x * F::NAP] * phiB[x];
+                        SL1[xa] = acc;
+                    }
+                }
+                if (zrow >= 0) {   // the row flushed last interval: its slot is not in use now
+                    double* accz = Acc + ((zrow % F::RING) * W) * F::WAB;
+                    for (int it = tid; it < W * F::WAB; it += S1T) accz[it] = 0.0;
+                    if (tid == 0) AccL[zrow % F::RING] = 0.0;
+                }
+            } else if (j > 0) {   // ---- stage 3 (plane j-1): rank-1 updates ----
+                const int jp = j - 1, ep = e_first + jp / Q, gp = jp % Q;
+                const double* Bp = Bs + (ep & 1) * 2 * Q * P;
+                const int t3 = tid - S1T;
+                for (int it = t3; it < P * F::WAB; it += S3T) {
+                    const int sab = it % F::WAB, al = it / F::WAB;
+                    const int i = ep + al;
+                    if (i < r0 || i >= r1) continue;
+                    const double va = Bp[gp * P + al], da = Bp[Q * P + gp * P + al];
+                    const double s0 = F::SPLIT ? S2[sab] + S2[4 * F::WAB + sab] : S2[sab];
+                    const double s1 = S2[F::WAB + sab], s2v = S2[2 * F::WAB + sab], s3 = S2[3 * F::WAB + sab];
+                    const double c0 = va * s0 + da * s2v, c1 = va * s1 + da * s3;
+                    double* acc = Acc + ((i % F::RING) * W) * F::WAB + sab;
+#pragma unroll
+                    for (int bl = 0; bl < P; ++bl) {
+                        const double vb = Bp[gp * P + bl], db = Bp[Q * P + gp * P + bl];
+                        acc[(bl - al + p) * F::WAB] += vb * c0 + db * c1;
+                    }
+                }
+                if (t3 < P) {
+                    const int i = ep + t3;
+                    if (i >= r0 && i < r1) AccL[i % F::RING] += Bp[gp * P + t3] * S2[LOAD2];
+                }
+            }
+            __syncthreads();   // B2
+            zrow = -1;
+            if (has && i2_on) {   // ---- stage 2 (plane j): contract tile axis a ----
+                if (i2_load) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int x = 0; x < F::NA; ++x) acc += SL1[x] * phiA[x];
+                    S2[LOAD2] = acc;
+                } else {
+                    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+                    for (int prr = 0; prr < NPAIR; ++prr) {
+                        if (!((i2_mask >> prr) & 1)) continue;
+                        const double* sp = S1 + prr * F::NA * W + i2_sb;
+                        const double* tp0 = Ta + tap[prr] * F::NA * P + i2_sa;
+#pragma unroll
+                        for (int t = 0; t < P; ++t) {
+                            if (t < i2_tl || t > i2_th) continue;
+#pragma unroll
+                            for (int g2 = 0; g2 < Q; ++g2) {
+                                const int xa = t * Q + g2;
+                                const double v = sp[xa * W] * tp0[xa * P - t];
+                                if (g2 & 1) acc1 += v; else acc0 += v;
+                            }
+                        }
+                    }
+                    S2[i2_it] = acc0 + acc1;
+                }
+            }
+            if (j > 0 && (j - 1) % Q == Q - 1) {   // element e(j-1) complete
+                const int ep = e_first + (j - 1) / Q;
+                if (ep < e_last) {
+                    if (ep >= r0 && ep < r1) { flush_row(ep); zrow = ep; }
+                } else {
+                    for (int i = (ep > r0 ? ep : r0); i < r1; ++i) flush_row(i);
+                }
+            }
+            buf ^= 1;
+        }
+    } else {
     const bool pr = prof != nullptr && blockIdx.x == 0 && tid == 0;   // phase profile
     long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc = 0;
     load_plane((int64_t)e_first * Q, 0);
@@ -400,6 +563,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     }
     if (pr)
         for (int k = 0; k < 8; ++k) prof[k] = tp[k];
+    }
 }
 
 // dispatch: returns false when (d, p, q, mu) has no fast instantiation
