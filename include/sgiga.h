@@ -176,6 +176,18 @@ int sgiga_combine_grid(sgiga_handle* h, const double* pts_per_dir,
 /* L2 and H1-seminorm error of the combined solution against the device
  * closed-form solution on a tensor Gauss grid (per-axis points/weights as
  * QuadGrid builds them).  out[0] = L2, out[1] = H1 seminorm.            */
+/* Same quadrature for an explicit signed term list: the field
+ * sum_t weights[t] * u_{comps[t]} (accumulated in the given order, as the
+ * reference's surplus, combination.py:269-272) against the closed-form
+ * solution_id, or against zero when solution_id < 0 (then out = the L2 norm
+ * and H1 seminorm of the field itself).  Serves surplus_norm / profit_table
+ * (combination.py:247-302) and the study drivers' per-level errors
+ * (analysis.py:325-386), several plans sharing one solved batch.         */
+int sgiga_subset_error_norms(sgiga_handle* h, const double* pts_per_dir,
+                             const double* wts_per_dir, const int64_t* npts_per_dir,
+                             int32_t n_terms, const int32_t* comps, const double* weights,
+                             int32_t solution_id, double* out);
+
 int sgiga_error_norms(sgiga_handle* h, const double* pts_per_dir,
                       const double* wts_per_dir, const int64_t* npts_per_dir,
                       int32_t solution_id, double* out);

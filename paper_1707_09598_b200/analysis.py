@@ -171,6 +171,25 @@ def annulus_gradient_2d(x):
     return np.stack([gx, gy], axis=-1)
 
 
+@_tag(_lib.FORCING_ANNULUS_3D)
+def annulus_solution_3d(x):
+    """The 2-D annulus solution times sin(pi z) (prism over the annulus)."""
+    return annulus_solution_2d(x) * np.sin(np.pi * x[..., 2])
+
+
+@_tag(_lib.FORCING_ANNULUS_3D)
+def annulus_gradient_3d(x):
+    sz, cz = np.sin(np.pi * x[..., 2]), np.cos(np.pi * x[..., 2])
+    g = annulus_gradient_2d(x)
+    return np.stack([g[..., 0] * sz, g[..., 1] * sz, np.pi * cz * annulus_solution_2d(x)], axis=-1)
+
+
+@_tag(_lib.FORCING_ANNULUS_3D)
+def annulus_forcing_3d(x):
+    # -Lap(u2 sin(pi z)) = (f2 + pi^2 u2) sin(pi z)
+    return (annulus_forcing_2d(x) + np.pi**2 * annulus_solution_2d(x)) * np.sin(np.pi * x[..., 2])
+
+
 @_tag(_lib.FORCING_CONSTANT_ONE)
 def constant_one(x):
     return np.ones(x.shape[0])
@@ -234,12 +253,27 @@ def regular_annulus_problem(d=2, degree=2, regularity=None, grading=1.0) -> Benc
     """Reference analysis.py:155-176 (2-D variant)."""
     from .geometry import quarter_annulus
 
-    if d != 2:
-        raise ValueError("only the 2-D annulus closed form is registered")
+    if d == 2:
+        sol, grad, forc = annulus_solution_2d, annulus_gradient_2d, annulus_forcing_2d
+    elif d == 3:
+        sol, grad, forc = annulus_solution_3d, annulus_gradient_3d, annulus_forcing_3d
+    else:
+        raise ValueError(f"regular annulus problem needs d in (2, 3), got {d}")
     return BenchmarkProblem(
-        f"regular_annulus_{d}d", quarter_annulus(d), annulus_forcing_2d, degree,
-        degree - 1 if regularity is None else regularity, grading,
-        annulus_solution_2d, annulus_gradient_2d)
+        f"regular_annulus_{d}d", quarter_annulus(d), forc, degree,
+        degree - 1 if regularity is None else regularity, grading, sol, grad)
+
+
+def constant_forcing_problem(d, grading=1.0, degree=3, regularity=None) -> BenchmarkProblem:
+    """Quarter annulus with unit forcing, no closed form (reference
+    analysis.py:192-205): errors need the overkill reference."""
+    from .geometry import quarter_annulus
+
+    if d not in (2, 3):
+        raise ValueError(f"constant forcing problem needs d in (2, 3), got {d}")
+    return BenchmarkProblem(
+        f"constant_forcing_{d}d", quarter_annulus(d), constant_one, degree,
+        degree - 1 if regularity is None else regularity, grading)
 
 
 def polynomial_cube_problem(d, degree=2, regularity=None) -> BenchmarkProblem:
@@ -251,11 +285,96 @@ def polynomial_cube_problem(d, degree=2, regularity=None) -> BenchmarkProblem:
         degree - 1 if regularity is None else regularity, 1.0, cube_solution, cube_gradient)
 
 
-def error_norms(plan, components, problem, grid):
-    """(L2 error, H1-seminorm error) of the combined solution against the
-    problem's closed-form solution on ``grid`` -- one device pass replacing
-    error_norms(combined_evaluator(plan, comps), analytic_evaluator(u, grad u),
-    QuadGrid) (reference analysis.py:226-270)."""
+class Evaluator:
+    """A field the device error quadrature understands (reference
+    analysis.py:226-259 returns closures; here they are descriptors):
+    kind "analytic" (registered closed form), "spline" (one space +
+    coefficients) or "combined" (plan + component solutions)."""
+
+    def __init__(self, kind, **payload):
+        self.kind = kind
+        self.payload = payload
+
+    def __call__(self, grid):
+        raise TypeError("device evaluators are consumed by analysis.error_norms")
+
+    def fields(self):
+        """[(space, coefficients, weight), ...] in accumulation order."""
+        if self.kind == "spline":
+            return [(self.payload["space"], self.payload["coeffs"], 1.0)]
+        if self.kind == "combined":
+            from .combination import _lookup
+
+            lookup = _lookup(self.payload["components"])
+            out = []
+            for beta, c in self.payload["plan"].terms:
+                if beta not in lookup:
+                    raise KeyError(f"no component solution supplied for index {beta}")
+                s = lookup[beta]
+                out.append((s.space, s.coefficients, float(c)))
+            return out
+        return []
+
+
+def analytic_evaluator(solution, gradient):
+    """Closed-form solution (must carry a device registry id)."""
+    return Evaluator("analytic", solution=solution, gradient=gradient)
+
+
+def spline_evaluator(space, coeffs):
+    return Evaluator("spline", space=space, coeffs=coeffs)
+
+
+def combined_evaluator(plan, components):
+    return Evaluator("combined", plan=plan, components=components)
+
+
+def _evaluator_error_norms(solution_eval, reference_eval, grid):
+    """||a - b|| (L2, H1 seminorm) for two evaluators on a QuadGrid, one
+    device pass: the spline / combined fields of both sides go into one
+    handle as a signed term list, a closed-form side becomes the kernel's
+    solution (reference analysis.py:262-270)."""
+    from .assembly import space_batch
+
+    sid = None
+    terms = []   # (space, coeffs, weight)
+    for ev, sign in ((solution_eval, 1.0), (reference_eval, -1.0)):
+        if not isinstance(ev, Evaluator):
+            raise TypeError("error_norms expects evaluators from analytic/spline/combined_evaluator")
+        if ev.kind == "analytic":
+            if sid is not None:
+                raise ValueError("at most one closed-form side")
+            sid = solution_id_of(ev.payload["solution"])
+            if sid is None:
+                raise ValueError("closed-form solution not registered on the device")
+            sign_analytic = sign
+            continue
+        terms += [(s, c, sign * w) for s, c, w in ev.fields()]
+    if not terms:
+        raise ValueError("nothing to integrate")
+    if sid is not None and sign_analytic > 0:   # ||u - f|| = ||f - u||
+        terms = [(s, c, -w) for s, c, w in terms]
+    batch = space_batch([(s, 1) for s, _, _ in terms], patch=grid.patch)
+    try:
+        batch.set_coefficients(np.concatenate([np.asarray(c, dtype=np.float64).ravel() for _, c, _ in terms]))
+        return batch.subset_error_norms(grid.points_per_dir, grid.weights_per_dir,
+                                        [(i, w) for i, (_, _, w) in enumerate(terms)], sid)
+    finally:
+        batch.close()
+
+
+def error_norms(*args):
+    """(L2 error, H1-seminorm error).  Two forms:
+
+    * ``error_norms(solution_eval, reference_eval, grid)`` -- the reference
+      signature (analysis.py:262-270) with the evaluators above;
+    * ``error_norms(plan, components, problem, grid)`` -- the combined
+      solution against the problem's closed form, one device pass reusing
+      the components' own handle when possible.
+    """
+    if len(args) == 3:
+        return _evaluator_error_norms(*args)
+    plan, components, problem, grid = args
     from .combination import _combine_batch
 
     sid = solution_id_of(problem.solution)
@@ -267,3 +386,15 @@ def error_norms(plan, components, problem, grid):
     finally:
         if owned:
             batch.close()
+
+
+# study drivers (reference analysis.py:273-528), batched on the device
+from .studies import (ConvergenceRecord, GammaSweepRow, convergence_study, fit_rate,  # noqa: E402
+                      gamma_sweep, read_convergence_csv, write_convergence_csv, write_gamma_csv)
+
+__all__ += [
+    "annulus_solution_3d", "annulus_forcing_3d", "annulus_gradient_3d", "constant_forcing_problem",
+    "Evaluator", "analytic_evaluator", "spline_evaluator", "combined_evaluator", "error_norms",
+    "fit_rate", "ConvergenceRecord", "convergence_study", "write_convergence_csv", "read_convergence_csv",
+    "GammaSweepRow", "gamma_sweep", "write_gamma_csv",
+]

@@ -192,3 +192,7 @@ def evaluate_combined_points(plan, components, points) -> np.ndarray:
     finally:
         if owned:
             batch.close()
+
+
+# surplus / profit (reference combination.py:239-302), batched on the device
+from .studies import ProfitRow, profit_table, surplus_norm  # noqa: E402,F401

@@ -924,26 +924,55 @@ int sgiga_combine_grid(sgiga_handle* hh, const double* pts_per_dir, const int64_
     return SGIGA_OK;
 }
 
-int sgiga_error_norms(sgiga_handle* hh, const double* pts, const double* wts,
-                      const int64_t* npd, int32_t solution_id, double* out) {
-    Handle* h = reinterpret_cast<Handle*>(hh);
-    if (!h || !pts || !wts || !npd || !out) return SGIGA_ERR_VALUE;
+static int error_norms_impl(Handle* h, const double* pts, const double* wts, const int64_t* npd,
+                            int32_t nterm, const int32_t* tcomp, const double* tw, int32_t solution_id,
+                            double* out) {
     if (!h->have_coefs) { set_error("error norms before solve"); return SGIGA_ERR_STATE; }
+    for (int t = 0; t < nterm; ++t)
+        if (tcomp[t] < 0 || tcomp[t] >= h->ncomp) { set_error("term component index out of range"); return SGIGA_ERR_KEY; }
     int64_t N = 1, P = 0;
     for (int k = 0; k < h->d; ++k) { N *= npd[k]; P += npd[k]; }
     int64_t nb = (N + 255) / 256;
-    double *dp = nullptr, *dw = nullptr, *dpart = nullptr;
+    double *dp = nullptr, *dw = nullptr, *dpart = nullptr, *dtw = nullptr;
+    int* dtc = nullptr;
     SG_CUDA(cudaMalloc(&dp, sizeof(double) * std::max<int64_t>(P, 1)));
     SG_CUDA(cudaMalloc(&dw, sizeof(double) * std::max<int64_t>(P, 1)));
     SG_CUDA(cudaMalloc(&dpart, sizeof(double) * (2 * nb + 2)));
     SG_CUDA(cudaMemcpyAsync(dp, pts, sizeof(double) * P, cudaMemcpyHostToDevice, h->stream));
     SG_CUDA(cudaMemcpyAsync(dw, wts, sizeof(double) * P, cudaMemcpyHostToDevice, h->stream));
+    if (nterm > 0) {
+        SG_CUDA(cudaMalloc(&dtc, sizeof(int) * nterm));
+        SG_CUDA(cudaMalloc(&dtw, sizeof(double) * nterm));
+        SG_CUDA(cudaMemcpyAsync(dtc, tcomp, sizeof(int) * nterm, cudaMemcpyHostToDevice, h->stream));
+        SG_CUDA(cudaMemcpyAsync(dtw, tw, sizeof(double) * nterm, cudaMemcpyHostToDevice, h->stream));
+    }
     int64_t nbl = 0;
-    SG_CUDA(launch_error_norms(h, dp, dw, npd, solution_id, dpart, &nbl));
+    SG_CUDA(launch_error_norms(h, dp, dw, npd, solution_id, dpart, &nbl, dtc, dtw, nterm));
     SG_CUDA(cudaMemcpyAsync(out, dpart + 2 * nbl, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     SG_CUDA(cudaStreamSynchronize(h->stream));
     cudaFree(dp); cudaFree(dw); cudaFree(dpart);
+    if (dtc) cudaFree(dtc);
+    if (dtw) cudaFree(dtw);
     return check_err(h);
+}
+
+int sgiga_error_norms(sgiga_handle* hh, const double* pts, const double* wts,
+                      const int64_t* npd, int32_t solution_id, double* out) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !pts || !wts || !npd || !out) return SGIGA_ERR_VALUE;
+    if (solution_id < 0) { set_error("unknown solution id"); return SGIGA_ERR_VALUE; }
+    return error_norms_impl(h, pts, wts, npd, 0, nullptr, nullptr, solution_id, out);
+}
+
+int sgiga_subset_error_norms(sgiga_handle* hh, const double* pts, const double* wts,
+                             const int64_t* npd, int32_t n_terms, const int32_t* comps,
+                             const double* weights, int32_t solution_id, double* out) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !pts || !wts || !npd || !out || n_terms < 1 || !comps || !weights) {
+        set_error("null argument or empty term list");
+        return SGIGA_ERR_VALUE;
+    }
+    return error_norms_impl(h, pts, wts, npd, n_terms, comps, weights, solution_id < 0 ? -1 : solution_id, out);
 }
 
 int sgiga_export_csr(sgiga_handle* hh, int32_t comp, int64_t* nnz_out, int64_t* indptr,

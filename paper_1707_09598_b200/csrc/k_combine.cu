@@ -142,6 +142,48 @@ __device__ __forceinline__ void combine_at(const CompInfo* __restrict__ comps, i
     }
 }
 
+// explicit signed term list (component index, weight) in the given order:
+// acc = w0 v0, acc += w_t v_t -- the reference's surplus accumulation
+// (combination.py:269-272) and, with the plan's terms, evaluate_combined
+template <int D, int P, bool GRAD>
+__device__ __forceinline__ void combine_terms(const CompInfo* __restrict__ comps,
+                                              const int* __restrict__ tcomp, const double* __restrict__ tw,
+                                              int nterm, const TabInfo* __restrict__ tabs,
+                                              const double* __restrict__ knots, int mu,
+                                              const double* __restrict__ coef, const double* xi,
+                                              double& acc, double* gacc) {
+    int cur[D], first[D];
+    double Bv[D][P], Bd[D][P];
+#pragma unroll
+    for (int k = 0; k < D; ++k) cur[k] = -1;
+    acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) gacc[k] = 0.0;
+    for (int t = 0; t < nterm; ++t) {
+        const CompInfo& C = comps[tcomp[t]];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            int tb = C.tab[k];
+            if (tb != cur[k]) {
+                cur[k] = tb;
+                first[k] = axis_basis<P, GRAD>(tabs[tb], knots, mu, xi[k], Bv[k], Bd[k]);
+            }
+        }
+        double v, g[D];
+        eval_component<D, P, GRAD>(C, coef, first, Bv, Bd, v, g);
+        const double cf = tw[t];
+        if (t == 0) {
+            acc = cf * v;
+#pragma unroll
+            for (int k = 0; k < D; ++k) gacc[k] = cf * g[k];
+        } else {
+            acc = __dadd_rn(acc, cf * v);
+#pragma unroll
+            for (int k = 0; k < D; ++k) gacc[k] = __dadd_rn(gacc[k], cf * g[k]);
+        }
+    }
+}
+
 template <int D, int P>
 __global__ void __launch_bounds__(128)
 k_combine_points(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
@@ -411,7 +453,8 @@ k_error_norms(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __re
               const GeoInfo* __restrict__ geo, const double* __restrict__ gknots,
               const double* __restrict__ hw, const double* __restrict__ pts,
               const double* __restrict__ wts, int64_t n0, int64_t n1, int64_t n2, int sol_id,
-              double* __restrict__ partials, int* __restrict__ err) {
+              double* __restrict__ partials, int* __restrict__ err, const int* __restrict__ tcomp,
+              const double* __restrict__ tw, int nterm) {
     __shared__ double red[2][ERR_THREADS / 32];
     int64_t N = n0 * (D > 1 ? n1 : 1) * (D > 2 ? n2 : 1);
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -429,9 +472,12 @@ k_error_norms(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __re
         double det = geo_point<D>(G, gknots, hw, xi, x, Ji);
         if (!(det > 0.0)) atomicOr(err, ERRF_GEOMETRY);
         double acc, g[D];
-        combine_at<D, P, true>(comps, 0, ncomp, true, tabs, knots, mu, coef, xi, acc, g, nullptr, 0);
-        double ue, ge[D];
-        solution_value<D>(sol_id, x, ue, ge);
+        if (tcomp) combine_terms<D, P, true>(comps, tcomp, tw, nterm, tabs, knots, mu, coef, xi, acc, g);
+        else combine_at<D, P, true>(comps, 0, ncomp, true, tabs, knots, mu, coef, xi, acc, g, nullptr, 0);
+        double ue = 0.0, ge[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) ge[i] = 0.0;
+        if (sol_id >= 0) solution_value<D>(sol_id, x, ue, ge);   // < 0: norms of the combination itself
         double dv = acc - ue, dg2 = 0.0;
 #pragma unroll
         for (int i = 0; i < D; ++i) {   // J^-T grad (analysis.py:235-237)
@@ -582,7 +628,7 @@ cudaError_t launch_combine_grid(Handle* h, const double* d_pts, const int64_t* n
 
 cudaError_t launch_error_norms(Handle* h, const double* d_pts, const double* d_wts,
                                const int64_t* npd, int solution_id, double* d_partials,
-                               int64_t* nblocks) {
+                               int64_t* nblocks, const int* d_tcomp, const double* d_tw, int nterm) {
     int64_t N = 1;
     for (int k = 0; k < h->d; ++k) N *= npd[k];
     int64_t nb = (N + ERR_THREADS - 1) / ERR_THREADS;
@@ -592,7 +638,7 @@ cudaError_t launch_error_norms(Handle* h, const double* d_pts, const double* d_w
     k_error_norms<DD, PP><<<(unsigned)nb, ERR_THREADS, 0, h->stream>>>(                        \
         h->d_comps, h->ncomp, h->d_tabs, h->d_knots, h->mu, h->d_coef, h->d_geo,               \
         h->d_geo_knots, h->d_geo_hw, d_pts, d_wts, npd[0], n1, n2, solution_id, d_partials,    \
-        h->d_err)
+        h->d_err, d_tcomp, d_tw, nterm)
     SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_EN)
 #undef LAUNCH_EN
     k_sum_partials<<<1, 1024, 0, h->stream>>>(d_partials, nb, d_partials + 2 * nb);

@@ -228,6 +228,7 @@ cudaError_t launch_combine_grid(Handle* h, const double* d_pts, const int64_t* n
                                 double* d_vals, double* d_grads);
 cudaError_t launch_error_norms(Handle* h, const double* d_pts, const double* d_wts,
                                const int64_t* npd, int solution_id, double* d_partials,
-                               int64_t* nblocks);
+                               int64_t* nblocks, const int* d_tcomp = nullptr, const double* d_tw = nullptr,
+                               int nterm = 0);
 
 }  // namespace sgiga

@@ -259,6 +259,24 @@ class Batch:
                                               _lib.ptr(npd, ct.c_int64), int(solution_id), _lib.ptr(out, ct.c_double)))
         return float(out[0]), float(out[1])
 
+    def subset_error_norms(self, points_per_dir, weights_per_dir, terms, solution_id=None):
+        """L2 / H1-seminorm of sum_t w_t u_{c_t} (minus the closed form
+        ``solution_id``; None = against zero) on a tensor quadrature grid;
+        ``terms`` = [(component index, weight), ...] in accumulation order."""
+        arrs = [np.asarray(p, dtype=np.float64).ravel() for p in points_per_dir]
+        wts = [np.asarray(w, dtype=np.float64).ravel() for w in weights_per_dir]
+        npd = np.array([a.size for a in arrs], dtype=np.int64)
+        cp = np.ascontiguousarray(np.concatenate(arrs))
+        cw = np.ascontiguousarray(np.concatenate(wts))
+        tc = np.ascontiguousarray([int(c) for c, _ in terms], dtype=np.int32)
+        tw = np.ascontiguousarray([float(w) for _, w in terms], dtype=np.float64)
+        out = np.zeros(2)
+        _lib.check(self.lib.sgiga_subset_error_norms(
+            self.h, _lib.ptr(cp, ct.c_double), _lib.ptr(cw, ct.c_double), _lib.ptr(npd, ct.c_int64),
+            len(tc), _lib.ptr(tc, ct.c_int32), _lib.ptr(tw, ct.c_double),
+            -1 if solution_id is None else int(solution_id), _lib.ptr(out, ct.c_double)))
+        return float(out[0]), float(out[1])
+
     def export_csr(self, comp: int):
         """Interior CSR + rhs of one component (reference row order)."""
         import scipy.sparse as sps

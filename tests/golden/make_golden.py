@@ -237,6 +237,38 @@ def gen_config(name, comps_to_store=None, n_points=512, workers=1):
     print(name, "components", len(plan), "L2/H1", l2, h1, flush=True)
 
 
+def gen_studies():
+    """Surplus / profit tables and convergence studies
+    computed by the reference's own drivers."""
+    from sparseiga import analysis, combination
+
+    out = {}
+    cases = {
+        "annulus2_p2": (analysis.regular_annulus_problem(2, degree=2), 2),
+        "cube3_p2": (analysis.polynomial_cube_problem(3, degree=2), (1, 1, 2)),
+        "const2_p2_g2": (analysis.constant_forcing_problem(2, grading=2.0, degree=2), 2),
+    }
+    for key, (prob, bmax) in cases.items():
+        rows = combination.profit_table(prob, bmax)
+        out[f"profit_{key}_beta"] = np.array([r.beta for r in rows], dtype=np.int32)
+        out[f"profit_{key}_l2"] = np.array([r.surplus_l2 for r in rows])
+        out[f"profit_{key}_dofs"] = np.array([r.dofs for r in rows], dtype=np.int64)
+    studies = {
+        "annulus2_sparse": (analysis.regular_annulus_problem(2, degree=2), "sparse", [1, 2, 3, 4]),
+        "annulus2_tensor": (analysis.regular_annulus_problem(2, degree=2), "tensor", [1, 2, 3]),
+        "const2_sparse": (analysis.constant_forcing_problem(2, grading=1.0, degree=2), "sparse", [1, 2, 3]),
+    }
+    for key, (prob, method, levels) in studies.items():
+        recs = analysis.convergence_study(prob, method, levels)
+        out[f"conv_{key}_levels"] = np.array(levels, dtype=np.int32)
+        out[f"conv_{key}_l2"] = np.array([r.l2_error for r in recs])
+        out[f"conv_{key}_h1"] = np.array([r.h1_semi_error for r in recs])
+        out[f"conv_{key}_dofs"] = np.array([r.dofs_total for r in recs], dtype=np.int64)
+        out[f"conv_{key}_ncomp"] = np.array([r.n_components for r in recs], dtype=np.int32)
+    np.savez_compressed(HERE / "studies.npz", **out)
+    print("studies", sorted(k for k in out if k.endswith("_l2")), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg5", action="store_true", help="also run cfg5 (minutes, 8 workers)")
@@ -258,6 +290,8 @@ def main():
         plan = shifted_plan(combination, 3, 7)
         pick = [plan.betas.index(b) for b in ((3, 2, 2), (5, 1, 1), (1, 1, 5), (2, 3, 2))]
         gen_config("cfg2", comps_to_store=pick)
+    if args.only in (None, "studies"):
+        gen_studies()
     if args.cfg5 or args.only == "cfg5":
         from sparseiga import combination
         plan = shifted_plan(combination, 3, 12)
