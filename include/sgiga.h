@@ -212,6 +212,42 @@ int sgiga_kernel_times(sgiga_handle* h, float* ms7);
 /* Per-component PCG iteration counts of the last solve.                 */
 int sgiga_iterations(sgiga_handle* h, int32_t* iters);
 
+/* ---- multipatch pieces (BASELINE cfg4; no reference
+ * code path exists -- SPEC.md:150,208 -- so these extend the single-patch
+ * discretisation of assembly.py:357-390 the GeoPDEs way).  All pointers
+ * named d_* are DEVICE pointers; launches go to the handle's / the given
+ * stream; the caller orchestrates (paper_1707_09598_b200/multipatch.py).
+ *
+ * Full-patch stiffness of component comp of an assembled patch handle:
+ * every function (boundary rows included), rows in reference C order over
+ * n_1 x ... x n_d, (2p+1)^d relative-offset slots (last axis fastest, zero
+ * outside the patch): d_vals[slot*rows + row]; load vector d_rhs[rows].   */
+int sgiga_full_patch_system(sgiga_handle* h, int32_t comp, double* d_vals, double* d_rhs);
+
+/* Dirichlet data moments on one edge of a 2-D patch: the edge runs along
+ * parametric axis `axis` with the other coordinate = side (0/1).  Banded
+ * 1-D mass d_band[i*(2p+1) + j-i+p] = int B_i B_j |dx/dxi| and
+ * d_rhs[i] = int g B_i |dx/dxi|, g = device closed form solution_id.     */
+int sgiga_edge_projection_system(sgiga_handle* h, int32_t comp, int32_t axis, int32_t side,
+                                 int32_t solution_id, double* d_band, double* d_rhs);
+
+/* d_dst[k] = sum_{t=d_start[k]}^{d_start[k+1]-1} d_src[d_idx[t]] (fixed order). */
+int sgiga_gather_sum(void* stream, int64_t n, const int64_t* d_start, const int64_t* d_idx,
+                     const double* d_src, double* d_dst);
+/* d_dst[k] = d_idx[k] >= 0 ? d_src[d_idx[k]] : 0.                         */
+int sgiga_gather(void* stream, int64_t n, const int64_t* d_idx, const double* d_src, double* d_dst);
+/* d_y[r] -= sum_k val[k] x[col[k]] over CSR row r.                         */
+int sgiga_csr_spmv_sub(void* stream, int64_t nrows, const int64_t* d_rowptr, const int32_t* d_col,
+                       const double* d_val, const double* d_x, double* d_y);
+/* Batched Jacobi-PCG: system s = rows [d_off[s], d_off[s+1]) of one CSR
+ * over the concatenated vector; ||r|| <= rtol ||b||; iters_out < 0 flags
+ * non-convergence; relres_out = true residual (host arrays, synchronises). */
+int sgiga_csr_pcg(void* stream, int32_t nsys, const int64_t* d_off, int64_t nrows_total,
+                  const int64_t* d_rowptr, const int32_t* d_col, const double* d_val, const double* d_b,
+                  double* d_x, double rtol, int32_t maxit, int32_t* iters_out, double* relres_out);
+/* Device-to-device sgiga_set_coefficients (full C-order vectors).        */
+int sgiga_set_coefficients_device(sgiga_handle* h, const double* d_full);
+
 /* The CUDA stream (cudaStream_t) every launch of this handle goes to. */
 void* sgiga_stream(sgiga_handle* h);
 

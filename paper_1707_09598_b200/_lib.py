@@ -43,6 +43,8 @@ EXPORTED = (
     "sgiga_combine_grid", "sgiga_error_norms", "sgiga_subset_error_norms", "sgiga_export_csr", "sgiga_phase_stats",
     "sgiga_iterations", "sgiga_kernel_times", "sgiga_stream", "sgiga_destroy", "sgiga_last_error",
     "sgiga_device_count", "sgiga_local_poisson_systems",
+    "sgiga_full_patch_system", "sgiga_edge_projection_system", "sgiga_gather_sum", "sgiga_gather",
+    "sgiga_csr_spmv_sub", "sgiga_csr_pcg", "sgiga_set_coefficients_device",
 )
 
 
@@ -99,6 +101,14 @@ def _declare(lib):
         "sgiga_combine_grid": ([VP, P_F64, P_I64, ct.c_int32, P_F64, P_F64], ct.c_int),
         "sgiga_error_norms": ([VP, P_F64, P_F64, P_I64, ct.c_int32, P_F64], ct.c_int),
         "sgiga_subset_error_norms": ([VP, P_F64, P_F64, P_I64, ct.c_int32, P_I32, P_F64, ct.c_int32, P_F64], ct.c_int),
+        "sgiga_full_patch_system": ([VP, ct.c_int32, VP, VP], ct.c_int),
+        "sgiga_edge_projection_system": ([VP, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, VP, VP], ct.c_int),
+        "sgiga_gather_sum": ([VP, ct.c_int64, VP, VP, VP, VP], ct.c_int),
+        "sgiga_gather": ([VP, ct.c_int64, VP, VP, VP], ct.c_int),
+        "sgiga_csr_spmv_sub": ([VP, ct.c_int64, VP, VP, VP, VP, VP], ct.c_int),
+        "sgiga_csr_pcg": ([VP, ct.c_int32, VP, ct.c_int64, VP, VP, VP, VP, VP, ct.c_double, ct.c_int32,
+                           P_I32, P_F64], ct.c_int),
+        "sgiga_set_coefficients_device": ([VP, VP], ct.c_int),
         "sgiga_export_csr": ([VP, ct.c_int32, P_I64, P_I64, P_I32, P_F64, P_F64], ct.c_int),
         "sgiga_phase_stats": ([VP, P_F32, P_I64], ct.c_int),
         "sgiga_iterations": ([VP, P_I32], ct.c_int),

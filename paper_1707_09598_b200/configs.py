@@ -58,3 +58,30 @@ def get_config(name: str) -> Config:
         plan = baseline_plan(3, 12) if name == "cfg5" else CombinationPlan(3, (((6, 6, 6), 1),), level=6)
         return Config(name, prob, plan, 32768, 4, (6, 6, 6), 5)
     raise KeyError(f"unknown config {name!r}; expected one of {CONFIG_NAMES}")
+
+
+@dataclass
+class MultipatchConfig:
+    """BASELINE cfg4: the L-shape, p=2 C1, combination
+    technique w=9 (15 components), uniform or one-sided graded knots,
+    4096 random parametric points per patch (seed 3), per-patch (8,8) error
+    grid with q=3 on the same knots."""
+
+    name: str
+    problem: object
+    plan: CombinationPlan
+    n_points: int = 4096
+    seed: int = 3
+    grid_levels: tuple = (8, 8)
+    quad_points: int = 3
+
+    def points(self, n=None) -> np.ndarray:
+        return np.random.default_rng(self.seed).random((self.n_points if n is None else n, 2))
+
+
+def get_multipatch_config(name: str = "cfg4") -> MultipatchConfig:
+    from .multipatch import lshape_problem
+
+    if name not in ("cfg4", "cfg4_graded"):
+        raise KeyError(f"unknown multipatch config {name!r}")
+    return MultipatchConfig(name, lshape_problem(graded=name == "cfg4_graded"), baseline_plan(2, 9))   # w = 9 (BASELINE configs[3])
