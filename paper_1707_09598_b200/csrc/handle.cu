@@ -42,7 +42,7 @@ static void free_all(Handle* h) {
                     h->d_hostf, h->d_xphys, h->d_stencil, h->d_rhs, h->d_dinv, h->d_x,
                     h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
-                    h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL};
+                    h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};
@@ -333,6 +333,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
 
 static int upload_all(Handle* h) {
     cudaStream_t s = h->stream;
+    h->tmaps_state = 0;   // tensor maps follow the component table
     SG_CUDA(cudaMemcpyAsync(h->d_comps, h->comps.data(), sizeof(CompInfo) * h->comps.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_tabs, h->tabs.data(), sizeof(TabInfo) * h->tabs.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_geo, &h->geo, sizeof(GeoInfo), cudaMemcpyHostToDevice, s));

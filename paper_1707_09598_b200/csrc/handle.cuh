@@ -137,6 +137,8 @@ struct Handle {
     std::vector<int> iters;
     bool force_generic_assembly = false;   // SGIGA_GENERIC_ASSEMBLY=1 (parity cross-check)
     int asm_seg = 0;                       // stream-axis segment length of the pencils
+    void* d_tmaps = nullptr;               // per-component CUtensorMap of d_G (TMA plane copies)
+    int tmaps_state = 0;                   // 0 = not built, 1 = ready, -1 = unavailable
     bool small_checked = false;            // small comps' true residual came from the cluster PCG
 
     // whole-run CUDA graph (sgiga_run): captured on the second call with the

@@ -21,8 +21,11 @@
 //     element; completed rows are flushed, mapping relative offsets to the
 //     stencil's storage slots (absolute or relative), zeros elsewhere.
 // Deterministic, no atomics; every stencil entry is written exactly once.
+#include <cuda.h>
+
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "handle.cuh"
 
@@ -34,18 +37,31 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     unsigned s = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
 }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
 
-template <int D, int P, int Q>
+template <int D, int P, int Q, bool TM = false>
 struct FastCfg {
     static constexpr int p = P - 1;
     static constexpr int W = 2 * P - 1;               // relative slots per axis
     static constexpr int NX = P * Q;                   // window points per tile axis
     static constexpr int NA = D >= 2 ? NX : 1;
     static constexpr int NB = D >= 3 ? NX : 1;
-    static constexpr int NAP = D >= 2 ? (NX | 1) : 1;  // odd row stride: conflict-free
     static constexpr int WA = D >= 2 ? W : 1;
     static constexpr int WB = D >= 3 ? W : 1;
     static constexpr int WAB = WA * WB;
@@ -58,6 +74,11 @@ struct FastCfg {
     // slot is zeroed one interval later) and two stream-basis buffers
     static constexpr int S1T = 32 * ((NPAIR + 1 + PPW - 1) / PPW);
     static constexpr bool PIPE = D == 3 && S1T <= 192;
+    // plane windows by one TMA tensor copy per plane (TM: the component's
+    // 4-D tensor map exists -- Q even makes every global stride a multiple of
+    // 16 bytes); the smem window is then dense (row stride NX)
+    static constexpr bool TMA = TM && PIPE && Q % 2 == 0;
+    static constexpr int NAP = D >= 2 ? (TMA ? NX : (NX | 1)) : 1;   // smem row stride of a plane
     static constexpr int RING = PIPE ? P + 1 : P;      // alive rows (+1 draining)
     static constexpr int nGw = NG * NB * NAP;          // one plane buffer
     // shared-memory layout (doubles)
@@ -80,18 +101,19 @@ struct FastCfg {
     static constexpr int total = oAccL + RING;
 };
 
-template <int D, int P, int Q>
-size_t fast_smem_bytes() { return sizeof(double) * FastCfg<D, P, Q>::total; }
+template <int D, int P, int Q, bool TM>
+size_t fast_smem_bytes() { return sizeof(double) * FastCfg<D, P, Q, TM>::total; }
 
-template <int D, int P, int Q>
+template <int D, int P, int Q, bool TM>
 __global__ void __launch_bounds__(FAST_THREADS, 2)
 k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tabs,
                 const Pencil* __restrict__ pencils, const double* __restrict__ vals,
                 const double* __restrict__ Gbuf, double* __restrict__ stencil,
-                double* __restrict__ rhs, double* __restrict__ dinv, long long* __restrict__ prof) {
-    using F = FastCfg<D, P, Q>;
+                double* __restrict__ rhs, double* __restrict__ dinv, long long* __restrict__ prof,
+                const CUtensorMap* __restrict__ tmaps) {
+    using F = FastCfg<D, P, Q, TM>;
     constexpr int p = F::p, W = F::W;
-    extern __shared__ double sm[];
+    extern __shared__ __align__(128) double sm[];
     double* Ta = sm + F::oTa;
     double* Tb = sm + F::oTb;
     double* phiA = sm + F::oPhiA;
@@ -143,6 +165,12 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     for (int idx = tid; idx < F::RING * W * F::WAB + F::RING; idx += FAST_THREADS) Acc[idx] = 0.0;
     // invalid window points stay zero in both plane buffers
     for (int idx = tid; idx < 2 * F::nGw; idx += FAST_THREADS) sm[F::oGw + idx] = 0.0;
+    __shared__ __align__(8) uint64_t fast_mbar[2];   // TMA variant: one barrier per plane buffer
+    if (F::TMA && tid == 0) {
+        mbar_init(&fast_mbar[0], 1);
+        mbar_init(&fast_mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     __syncthreads();
 
     // ---- metric plane window (a innermost in global and shared memory) ----
@@ -157,7 +185,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     // (smem offset, offset from the plane's first valid point) is decoded
     // once per pencil, so a plane costs a few instructions per copy
     constexpr int MAXC0 = (F::NG * F::NB * F::NA + FAST_THREADS - 1) / FAST_THREADS;
-    constexpr bool PRE = MAXC0 <= 8;            // else: row teams, one division per row
+    constexpr bool PRE = !F::TMA && MAXC0 <= 8;   // else: row teams, one division per row
     constexpr int MAXC = PRE ? MAXC0 : 1;
     int c_sm[MAXC], c_gl[MAXC];
     constexpr int LPR = F::NA <= 16 ? 16 : 32, NTEAM = FAST_THREADS / LPR;
@@ -177,6 +205,30 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             }
         }
     }
+    // TMA variant: ONE 4-D tensor copy per plane -- box (x_a, x_b, 1, entry)
+    // of the component's metric tensor map, out-of-patch window points
+    // zero-filled by the TMA unit -- armed and issued by one thread, completion
+    // counted on the buffer's mbarrier (phase bit per buffer in mb_phase)
+    uint32_t mb_phase = 0;
+    const CUtensorMap* tmap = F::TMA ? tmaps + pc.comp : nullptr;
+    const int tx0 = D >= 2 ? (pc.ia - p) * Q : 0, tx1 = D >= 3 ? (pc.ib - p) * Q : 0;
+    auto load_plane_tma = [&](int64_t Qs, int buf) {
+        if (tid != 0) return;
+        double* Gw = sm + F::oGw + buf * F::nGw;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(&fast_mbar[buf], (uint32_t)(F::nGw * 8));
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+            ::"r"(smem_u32(Gw)), "l"(tmap), "r"(tx0), "r"(tx1), "r"((int)Qs), "r"(0), "r"(smem_u32(&fast_mbar[buf]))
+            : "memory");
+    };
+    auto wait_plane_tma = [&](int buf) {
+        const uint32_t par = (mb_phase >> buf) & 1u;
+        while (!mbar_try_wait(&fast_mbar[buf], par)) {
+        }
+        mb_phase ^= 1u << buf;
+    };
     auto load_plane = [&](int64_t Qs, int buf) {
         double* Gw = sm + F::oGw + buf * F::nGw;
         const double* base = Gc + Qs * qs_s + Xa0 + Xb0 * qs_b;
@@ -283,14 +335,18 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         };
         if (nplanes > 0) {
             load_bs(e_first);
-            load_plane((int64_t)e_first * Q, 0);
+            if constexpr (F::TMA) load_plane_tma((int64_t)e_first * Q, 0);
+            else load_plane((int64_t)e_first * Q, 0);
         }
         int zrow = -1;
         for (int j = 0; j <= nplanes; ++j) {
             const bool has = j < nplanes;
             const int e = e_first + j / Q, g = j % Q;
             if (has) {
-                if (j + 1 < nplanes) {
+                if constexpr (F::TMA) {
+                    if (j + 1 < nplanes) load_plane_tma((int64_t)e_first * Q + j + 1, buf ^ 1);
+                    wait_plane_tma(buf);
+                } else if (j + 1 < nplanes) {
                     load_plane((int64_t)e_first * Q + j + 1, buf ^ 1);
                     cp_async_wait_prev();
                 } else {
@@ -567,16 +623,74 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 }
 
 // dispatch: returns false when (d, p, q, mu) has no fast instantiation
+// Per-component 4-D tensor maps of the metric buffer for the TMA plane
+// copies: dims (x_a, x_b, x_s, entry) with element strides (1, N_a, N_a N_b,
+// nqp) -- the qp storage order of build_tables (a innermost) -- and box
+// (NX, NX, 1, NG).  Built once per handle (host encode, one H2D copy);
+// false when the driver entry point or an encode is unavailable.
+static bool build_tmaps(Handle* h, int NX) {
+    if (h->tmaps_state != 0) return h->tmaps_state > 0;
+    h->tmaps_state = -1;
+    if (h->d != 3) return false;
+    void* fnp = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &qres) != cudaSuccess ||
+        qres != cudaDriverEntryPointSuccess || !fnp) {
+        cudaGetLastError();
+        return false;
+    }
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    EncodeFn encode = reinterpret_cast<EncodeFn>(fnp);
+    std::vector<CUtensorMap> maps(h->ncomp);
+    const int q = h->q, NG = h->nG();
+    for (int c = 0; c < h->ncomp; ++c) {
+        const CompInfo& C = h->comps[c];
+        const int s = C.ax[2], a = C.ax[1], b = C.ax[0];
+        const cuuint64_t Na = (cuuint64_t)C.nel[a] * q, Nb = (cuuint64_t)C.nel[b] * q, Ns = (cuuint64_t)C.nel[s] * q;
+        if (C.qs[a] != 1 || C.qs[b] != (int64_t)Na || C.qs[s] != (int64_t)(Na * Nb)) return false;
+        const cuuint64_t dims[4] = {Na, Nb, Ns, (cuuint64_t)NG};
+        const cuuint64_t strides[3] = {Na * 8, Na * Nb * 8, (cuuint64_t)C.nqp * 8};
+        const cuuint32_t box[4] = {(cuuint32_t)NX, (cuuint32_t)NX, 1, (cuuint32_t)NG};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (encode(&maps[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)(h->d_G + C.qp_off), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    if (!h->d_tmaps && cudaMalloc(&h->d_tmaps, sizeof(CUtensorMap) * h->ncomp) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (cudaMemcpyAsync(h->d_tmaps, maps.data(), sizeof(CUtensorMap) * h->ncomp, cudaMemcpyHostToDevice,
+                        h->stream) != cudaSuccess ||
+        cudaStreamSynchronize(h->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    h->tmaps_state = 1;
+    return true;
+}
+
 bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     if (h->mu != 1 || h->q != h->p + 1 || h->pencils.empty()) return false;
     const int key = h->d * 10 + (h->p + 1);
+    const char* nt = getenv("SGIGA_NO_TMA");
+    const bool tma = h->d == 3 && (h->q % 2 == 0) && !(nt && nt[0] == '1') &&
+                     build_tmaps(h, (h->p + 1) * h->q);
     size_t smem = 0;
     const void* fn = nullptr;
     switch (key) {
 #define CASE(DD, PP)                                                                 \
     case DD * 10 + PP:                                                               \
-        smem = fast_smem_bytes<DD, PP, PP>();                                        \
-        fn = (const void*)k_assemble_fast<DD, PP, PP>;                               \
+        if (tma && FastCfg<DD, PP, PP, true>::TMA) {                                 \
+            smem = fast_smem_bytes<DD, PP, PP, true>();                              \
+            fn = (const void*)k_assemble_fast<DD, PP, PP, true>;                     \
+        } else {                                                                     \
+            smem = fast_smem_bytes<DD, PP, PP, false>();                             \
+            fn = (const void*)k_assemble_fast<DD, PP, PP, false>;                    \
+        }                                                                            \
         break;
         CASE(1, 2) CASE(1, 3) CASE(1, 4) CASE(1, 5)
         CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(2, 5)
@@ -594,7 +708,7 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     }
     void* args[] = {(void*)&h->d_comps, (void*)&h->d_tabs, (void*)&h->d_pencils, (void*)&h->d_tabvals,
                     (void*)&h->d_G, (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv,
-                    (void*)&prof};
+                    (void*)&prof, (void*)&h->d_tmaps};
     *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(FAST_THREADS), args, smem, h->stream);
     if (prof) {
         long long t[8];

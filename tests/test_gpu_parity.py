@@ -120,6 +120,25 @@ def test_fast_assembly_matches_generic(name, terms, monkeypatch):
         assert normwise(bf, bg) <= 1e-13
 
 
+def test_tma_plane_copies_match_cp_async(monkeypatch):
+    """The TMA tensor-copy plane loads (zero-filled out-of-patch windows)
+    assemble bitwise the same stencil as the cp.async path."""
+    cfg = configs.get_config("cfg2")
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    mats = {}
+    for mode in ("tma", "cpasync"):
+        if mode == "cpasync":
+            monkeypatch.setenv("SGIGA_NO_TMA", "1")
+        b = Batch(spec)
+        try:
+            b.assemble()
+            mats[mode] = [b.export_csr(c) for c in (0, 5, 17, 30)]
+        finally:
+            b.close()
+    for (A1, b1), (A2, b2) in zip(mats["tma"], mats["cpasync"]):
+        assert np.array_equal(A1.data, A2.data) and np.array_equal(b1, b2)
+
+
 def test_pcg_residual_contract():
     cfg = configs.get_config("cfg2")
     spec, b = _batch(cfg)
