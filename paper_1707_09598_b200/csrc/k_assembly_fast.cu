@@ -10,9 +10,13 @@
 //     so T[type][x][k] (k = 0..p) holds exactly the nonzero (slot, point)
 //     pairs -- slot s = t + k.  Window elements outside the patch (rows near
 //     the boundary, short axes) are skipped by predication, never computed;
-//   * the metric plane window is copied with cp.async (only valid points;
-//     the invalid ones are zeroed once per pencil), double-buffered so the
-//     next plane streams in while the current one is contracted;
+//   * the metric plane window is double-buffered so the next plane streams
+//     in while the current one is contracted: in 3-D with Q even by ONE TMA
+//     tensor copy per plane (per-component 4-D tensor map, out-of-patch
+//     points zero-filled, mbarrier completion), otherwise by cp.async of the
+//     valid points from per-thread copy lists (the invalid ones stay zero);
+//   * 3-D planes are software-pipelined: stage 1 of plane j and stage 3 of
+//     plane j-1 run on disjoint thread groups in one barrier interval;
 //   * stage 1 (contract tile axis b): warp half <-> pair (m,n), lane <-> x_a,
 //     W register accumulators, P FMAs per metric value loaded;
 //   * stage 2 (contract tile axis a): (pair, s_b, t) items, then a
