@@ -42,7 +42,8 @@ static void free_all(Handle* h) {
                     h->d_hostf, h->d_xphys, h->d_stencil, h->d_rhs, h->d_dinv, h->d_x,
                     h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
-                    h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps};
+                    h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps,
+                    h->d_fdl_list, h->d_fdl_off, h->d_fdl};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};
@@ -233,20 +234,42 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
         h->fd_uoff.assign(ntab, 0); h->fd_loff.assign(ntab, 0);
         h->fd_u_total = 0; h->fd_l_total = 0;
         std::vector<char> used(ntab, 0);
-        std::vector<int> keep_small;
-        for (int c : h->small_comps) {
+        std::vector<int> keep_small, keep_large;
+        h->fdl_comps.clear();
+        h->fdl_off.assign(h->comps.size(), -1);
+        h->fdl_total = 0;
+        for (int c = 0; c < D->n_comp; ++c) {
             CompInfo& C = h->comps[c];
-            bool ok = fd_on && C.rows > 0 && fd_comp_smem(C, d) <= 200 * 1024;
-            for (int k = 0; k < d && ok; ++k) ok = C.m[k] >= 1 && C.m[k] <= FD_MMAX;
-            C.fd = ok ? 1 : 0;
-            if (ok) {
+            C.fd = 0;
+            if (!C.rows) continue;
+            const bool was_small = C.small != 0;
+            bool all_ok = fd_on, others_ok = fd_on;
+            for (int k = 0; k < d; ++k) {
+                const bool ok_k = C.m[k] >= 1 && C.m[k] <= FD_MMAX;
+                all_ok = all_ok && ok_k;
+                if (k != C.ax[d - 1]) others_ok = others_ok && ok_k;
+            }
+            if (all_ok && was_small && fd_comp_smem(C, d) <= 200 * 1024) {   // one CTA, everything in smem
+                C.fd = 1;
                 h->fd_comps.push_back(c);
                 for (int k = 0; k < d; ++k) used[C.tab[k]] = 1;
+            } else if (others_ok && C.m[C.ax[d - 1]] >= 1) {   // line FD: banded solves along the stream axis
+                C.fd = 2;
+                C.small = 1;   // keeps the chunked Jacobi kernels away from it
+                h->fdl_comps.push_back(c);
+                for (int k = 0; k < d; ++k)
+                    if (k != C.ax[d - 1]) used[C.tab[k]] = 1;
+                int64_t nl = 1;
+                for (int k = 0; k < d; ++k) if (k != C.ax[d - 1]) nl *= C.m[k];
+                const int64_t ms = C.m[C.ax[d - 1]];
+                h->fdl_off[c] = h->fdl_total;
+                h->fdl_total += (2 + nl) * ms * (p + 1);   // K_s, M_s bands + one factor per line
             } else {
-                keep_small.push_back(c);
+                (was_small ? keep_small : keep_large).push_back(c);
             }
         }
         h->small_comps.swap(keep_small);
+        h->large_comps.swap(keep_large);
         // tables with identical knot vectors share one factorisation
         for (int t = 0; t < ntab; ++t) {
             if (!used[t]) continue;
@@ -345,12 +368,17 @@ static int upload_all(Handle* h) {
         SG_CUDA(cudaMemcpyAsync(h->d_small, h->small_comps.data(), sizeof(int) * h->small_comps.size(), cudaMemcpyHostToDevice, s));
     if (!h->slotoff.empty())
         SG_CUDA(cudaMemcpyAsync(h->d_slotoff, h->slotoff.data(), sizeof(int) * h->slotoff.size(), cudaMemcpyHostToDevice, s));
-    if (!h->fd_comps.empty()) {
-        SG_CUDA(cudaMemcpyAsync(h->d_fdlist, h->fd_comps.data(), sizeof(int) * h->fd_comps.size(), cudaMemcpyHostToDevice, s));
+    if (!h->fdl_comps.empty()) {
+        SG_CUDA(cudaMemcpyAsync(h->d_fdl_list, h->fdl_comps.data(), sizeof(int) * h->fdl_comps.size(), cudaMemcpyHostToDevice, s));
+        SG_CUDA(cudaMemcpyAsync(h->d_fdl_off, h->fdl_off.data(), sizeof(int64_t) * h->fdl_off.size(), cudaMemcpyHostToDevice, s));
+    }
+    if (!h->fd_uniq.empty()) {
         SG_CUDA(cudaMemcpyAsync(h->d_fd_uniq, h->fd_uniq.data(), sizeof(int) * h->fd_uniq.size(), cudaMemcpyHostToDevice, s));
         SG_CUDA(cudaMemcpyAsync(h->d_fd_uoff, h->fd_uoff.data(), sizeof(int64_t) * h->fd_uoff.size(), cudaMemcpyHostToDevice, s));
         SG_CUDA(cudaMemcpyAsync(h->d_fd_loff, h->fd_loff.data(), sizeof(int64_t) * h->fd_loff.size(), cudaMemcpyHostToDevice, s));
     }
+    if (!h->fd_comps.empty())
+        SG_CUDA(cudaMemcpyAsync(h->d_fdlist, h->fd_comps.data(), sizeof(int) * h->fd_comps.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_bp, h->bp_host.data(), sizeof(double) * h->bp_host.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_geo_knots, h->geo_knots.data(), sizeof(double) * h->geo_knots.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_geo_hw, h->geo_hw.data(), sizeof(double) * h->geo_hw.size(), cudaMemcpyHostToDevice, s));
@@ -494,6 +522,9 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_fd_loff, h->tabs.size());
     A_(d_fdU, h->fd_u_total);
     A_(d_fdL, h->fd_l_total);
+    A_(d_fdl_list, h->fdl_comps.size());
+    A_(d_fdl_off, h->comps.size());
+    A_(d_fdl, h->fdl_total);
 #undef A_
     if (ea == cudaSuccess) ea = cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_fork, cudaEventDisableTiming);
@@ -548,7 +579,8 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
         tmp.chunks.size() != h->chunks.size() || tmp.small_comps.size() != h->small_comps.size() ||
         tmp.large_comps.size() != h->large_comps.size() || tmp.slotoff.size() != h->slotoff.size() ||
         tmp.fd_comps.size() != h->fd_comps.size() || tmp.fd_uniq.size() != h->fd_uniq.size() ||
-        tmp.fd_u_total != h->fd_u_total || tmp.fd_l_total != h->fd_l_total) {
+        tmp.fd_u_total != h->fd_u_total || tmp.fd_l_total != h->fd_l_total ||
+        tmp.fdl_comps.size() != h->fdl_comps.size() || tmp.fdl_total != h->fdl_total) {
         set_error("sgiga_upload: descriptor shape differs from the handle's");
         return SGIGA_ERR_VALUE;
     }
@@ -565,6 +597,7 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
                            same_bytes(tmp.chunks, h->chunks) && same_bytes(tmp.small_comps, h->small_comps) &&
                            same_bytes(tmp.large_comps, h->large_comps) && same_bytes(tmp.fd_comps, h->fd_comps) &&
                            same_bytes(tmp.fd_uniq, h->fd_uniq) && same_bytes(tmp.fd_uoff, h->fd_uoff) &&
+                           same_bytes(tmp.fdl_comps, h->fdl_comps) && same_bytes(tmp.fdl_off, h->fdl_off) &&
                            tmp.forcing_id == h->forcing_id;
     if (!identical) h->drop_run_graph();
     h->levels.swap(tmp.levels); h->coefs.swap(tmp.coefs);
@@ -576,6 +609,7 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
     h->small_comps.swap(tmp.small_comps); h->large_comps.swap(tmp.large_comps);
     h->fd_comps.swap(tmp.fd_comps); h->fd_uniq.swap(tmp.fd_uniq);
     h->fd_uoff.swap(tmp.fd_uoff); h->fd_loff.swap(tmp.fd_loff);
+    h->fdl_comps.swap(tmp.fdl_comps); h->fdl_off.swap(tmp.fdl_off);
     h->forcing_id = tmp.forcing_id;
     if (identical) return SGIGA_OK;   // device copies are already these bytes
     return upload_all(h);

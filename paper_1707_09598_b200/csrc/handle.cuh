@@ -104,6 +104,14 @@ struct Handle {
     int64_t* d_fd_loff = nullptr;
     double* d_fdU = nullptr;
     double* d_fdL = nullptr;
+    // line-FD comps (one long axis; k_pcg_fdl): per-comp offset into d_fdl
+    // (stream-axis K / M bands + one banded Cholesky factor per line)
+    std::vector<int> fdl_comps;
+    std::vector<int64_t> fdl_off;
+    int64_t fdl_total = 0;
+    int* d_fdl_list = nullptr;
+    int64_t* d_fdl_off = nullptr;
+    double* d_fdl = nullptr;
     cudaStream_t stream2 = nullptr;          // side stream: the eigen kernel overlaps assembly
     cudaEvent_t fd_fork = nullptr, fd_join = nullptr;
     bool fd_pending = false;                 // fd_join not yet waited on by the main stream

@@ -509,6 +509,261 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
     }
 }
 
+// ---- 3e: line-FD preconditioned CG for components with ONE long axis -------
+// P = c_s K_s x M_o + M_s x (sum_o c_o K_o x M_rest): the (at most two) other
+// axes are diagonalised with their 1-D eigen-pairs (k_fd_eigen), leaving one
+// banded SPD system (c_s K_s + mu M_s) per line along the stream axis (the
+// longest; contiguous in the internal row order), mu = sum_o c_o lambda_o.
+// For the identity map P == A again -- cfg5's (1,1,10) components converge
+// in one or two iterations instead of ~27 000 Jacobi-PCG iterations -- and
+// no eigen-decomposition of the long axis (up to 1026 functions) is needed:
+// its pencil is only factorised per line by banded Cholesky.  One CTA per
+// component, vectors in the batch's global PCG arrays (L2-resident).
+constexpr int FDL_THREADS = 256;
+
+template <int D>
+__global__ void __launch_bounds__(FDL_THREADS, 1)
+k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, const int* __restrict__ slotoff,
+          const double* __restrict__ stencil, const double* __restrict__ rhs, const double* __restrict__ Gbuf,
+          const TabInfo* __restrict__ tabs, const double* __restrict__ vals, const double* __restrict__ qw,
+          int p, int mu, int q, const int64_t* __restrict__ uoff, const int64_t* __restrict__ loff,
+          const double* __restrict__ dU, const double* __restrict__ dL, const int64_t* __restrict__ fdl_off,
+          double* __restrict__ fdl, double* __restrict__ xg, double* __restrict__ rg, double* __restrict__ zg,
+          double* __restrict__ pg, double* __restrict__ qg, double* __restrict__ tg,
+          CgState* __restrict__ st, double* __restrict__ relres, double rtol2, int maxit) {
+    __shared__ double red[FDL_THREADS / 32];
+    const int c = list[blockIdx.x];
+    const CompInfo& C = comps[c];
+    const int R = (int)C.rows, NS = (int)C.nslots, tid = threadIdx.x, P1 = p + 1;
+    const int s = C.ax[D - 1], ms = C.m[s];
+    constexpr int NO = D - 1;                      // other axes: C.ax[0 .. D-2]
+    int oax[NO > 0 ? NO : 1], om[NO > 0 ? NO : 1], ors[NO > 0 ? NO : 1];
+    int nlines = 1;
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+        oax[o] = C.ax[o];
+        om[o] = C.m[oax[o]];
+        ors[o] = (int)C.rs[oax[o]];
+        nlines *= om[o];
+    }
+    double* x = xg + C.vec_off;
+    double* r = rg + C.vec_off;
+    double* z = zg + C.vec_off;
+    double* pp = pg + C.vec_off;   // zero halos on both sides (SpMV gathers)
+    double* qq = qg + C.vec_off;
+    double* t = tg + C.vec_off;
+    const double* b = rhs + C.vec_off;
+    const double* val = stencil + C.mat_off;
+    const int* offs = slotoff + C.so_off;
+    double* Kb = fdl + fdl_off[c];
+    double* Mb = Kb + (int64_t)ms * P1;
+    double* Fac = Mb + (int64_t)ms * P1;
+
+    // metric scale per axis (patch integral of G_kk)
+    double ck[D];
+    {
+        const double* Gc = Gbuf + C.qp_off;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const double* g = Gc + (int64_t)sym_index(D, k, k) * C.nqp;
+            double sacc = 0.0;
+            for (int64_t i = tid; i < C.nqp; i += FDL_THREADS) sacc += g[i];
+            ck[k] = fd_block_sum(sacc, red);
+        }
+    }
+    // banded interior K_s, M_s of the stream axis (lower band, k = i - j)
+    {
+        const TabInfo T = tabs[C.tab[s]];
+        const int64_t nq = (int64_t)T.nel * q;
+        const double* bv = vals + T.val_off;
+        const double* bd = bv + nq * P1;
+        const double* w = qw + T.qp_off;
+        for (int idx = tid; idx < ms * P1; idx += FDL_THREADS) {
+            const int i = idx / P1, kk = idx % P1, j = i - kk, gi = i + 1, gj = j + 1;
+            double mv = 0.0, kv = 0.0;
+            if (j >= 0) {
+                const int num = gi - p;   // gi >= gj
+                const int elo = num <= 0 ? 0 : (num + mu - 1) / mu;
+                const int ehi = min(gj / mu, T.nel - 1);
+                for (int e = elo; e <= ehi; ++e) {
+                    const int a = gi - e * mu, bb = gj - e * mu;
+                    for (int g = 0; g < q; ++g) {
+                        const int64_t base = ((int64_t)e * q + g) * P1;
+                        const double wg = w[(int64_t)e * q + g];
+                        mv += wg * bv[base + a] * bv[base + bb];
+                        kv += wg * bd[base + a] * bd[base + bb];
+                    }
+                }
+            }
+            Kb[idx] = kv;
+            Mb[idx] = mv;
+        }
+    }
+    __syncthreads();
+    // one banded Cholesky per line: c_s K_s + mu M_s = F F^T
+    for (int L = tid; L < nlines; L += FDL_THREADS) {
+        double muL = 0.0;
+        int rem = L;
+        for (int o = NO - 1; o >= 0; --o) {
+            const int io = rem % om[o];
+            rem /= om[o];
+            muL += ck[oax[o]] * dL[loff[C.tab[oax[o]]] + io];
+        }
+        double* F = Fac + (int64_t)L * ms * P1;
+        for (int i = 0; i < ms; ++i) {
+            for (int kk = min(p, i); kk >= 1; --kk) {   // F(i, j), j = i - kk, increasing j
+                const int j = i - kk;
+                double sv = ck[s] * Kb[i * P1 + kk] + muL * Mb[i * P1 + kk];
+                for (int l = max(0, i - p); l < j; ++l) sv -= F[i * P1 + (i - l)] * F[j * P1 + (j - l)];
+                F[i * P1 + kk] = sv / F[j * P1];
+            }
+            double dv = ck[s] * Kb[i * P1] + muL * Mb[i * P1];
+            for (int l = max(0, i - p); l < i; ++l) dv -= F[i * P1 + (i - l)] * F[i * P1 + (i - l)];
+            F[i * P1] = sqrt(dv);
+        }
+    }
+    __syncthreads();
+
+    // mode product over other axis o (global buffers)
+    auto mode = [&](const double* src, double* dst, int o, bool trans) {
+        const int m = om[o], sr = ors[o];
+        const double* U = dU + uoff[C.tab[oax[o]]];
+        for (int row = tid; row < R; row += FDL_THREADS) {
+            const int a = (row / sr) % m, base = row - a * sr;
+            double acc = 0.0;
+            if (trans) {
+                for (int j = 0; j < m; ++j) acc += U[a * m + j] * src[base + j * sr];
+            } else {
+                for (int j = 0; j < m; ++j) acc += U[j * m + a] * src[base + j * sr];
+            }
+            dst[row] = acc;
+        }
+        __syncthreads();
+    };
+    auto line_solve = [&](double* y) {   // in place, every line L = rows [L*ms, (L+1)*ms)
+        for (int L = tid; L < nlines; L += FDL_THREADS) {
+            const double* F = Fac + (int64_t)L * ms * P1;
+            double* yl = y + (int64_t)L * ms;
+            for (int i = 0; i < ms; ++i) {
+                double sv = yl[i];
+                for (int j = max(0, i - p); j < i; ++j) sv -= F[i * P1 + (i - j)] * yl[j];
+                yl[i] = sv / F[i * P1];
+            }
+            for (int i = ms - 1; i >= 0; --i) {
+                double sv = yl[i];
+                for (int j = i + 1; j <= min(ms - 1, i + p); ++j) sv -= F[j * P1 + (j - i)] * yl[j];
+                yl[i] = sv / F[i * P1];
+            }
+        }
+        __syncthreads();
+    };
+    auto precond = [&]() {   // z = P^-1 r
+        if constexpr (D == 3) {
+            mode(r, t, 0, true);
+            mode(t, z, 1, true);
+            line_solve(z);
+            mode(z, t, 1, false);
+            mode(t, z, 0, false);
+        } else if constexpr (D == 2) {
+            mode(r, t, 0, true);
+            line_solve(t);
+            mode(t, z, 0, false);
+        } else {
+            for (int i = tid; i < R; i += FDL_THREADS) z[i] = r[i];
+            __syncthreads();
+            line_solve(z);
+        }
+    };
+    auto spmv = [&](const double* v, double* out) {   // out = A v (v halo-padded)
+        for (int row = tid; row < R; row += FDL_THREADS) {
+            const int rb = fd_row_base(C, D, row);
+            double y0 = 0.0, y1 = 0.0;
+            int tt = 0;
+            for (; tt + 1 < NS; tt += 2) {
+                y0 += __ldg(val + (size_t)tt * R + row) * v[rb + offs[tt]];
+                y1 += __ldg(val + (size_t)(tt + 1) * R + row) * v[rb + offs[tt + 1]];
+            }
+            if (tt < NS) y0 += __ldg(val + (size_t)tt * R + row) * v[rb + offs[tt]];
+            out[row] = y0 + y1;
+        }
+        __syncthreads();
+    };
+
+    double bbl = 0.0;
+    for (int i = tid; i < R; i += FDL_THREADS) {
+        const double bi = b[i];
+        x[i] = 0.0;
+        r[i] = bi;
+        bbl += bi * bi;
+    }
+    const double bb = fd_block_sum(bbl, red);
+    int it = 0, conv = (bb == 0.0);
+    if (!conv) {
+        precond();
+        double rzl = 0.0;
+        for (int i = tid; i < R; i += FDL_THREADS) { pp[i] = z[i]; rzl += r[i] * z[i]; }
+        double rz = fd_block_sum(rzl, red);
+        while (it < maxit) {
+            spmv(pp, qq);
+            double pql = 0.0;
+            for (int i = tid; i < R; i += FDL_THREADS) pql += pp[i] * qq[i];
+            const double alpha = rz / fd_block_sum(pql, red);
+            double rrl = 0.0;
+            for (int i = tid; i < R; i += FDL_THREADS) {
+                x[i] += alpha * pp[i];
+                const double ri = r[i] - alpha * qq[i];
+                r[i] = ri;
+                rrl += ri * ri;
+            }
+            const double rr = fd_block_sum(rrl, red);
+            ++it;
+            if (rr <= rtol2 * bb) { conv = 1; break; }
+            precond();
+            double rzl2 = 0.0;
+            for (int i = tid; i < R; i += FDL_THREADS) rzl2 += r[i] * z[i];
+            const double rzn = fd_block_sum(rzl2, red);
+            const double beta = rzn / rz;
+            rz = rzn;
+            for (int i = tid; i < R; i += FDL_THREADS) pp[i] = z[i] + beta * pp[i];
+            __syncthreads();
+        }
+    }
+    // true residual ||A x - b|| / ||b|| (linsolve.py:49-53); x is copied into
+    // the halo-padded p buffer for the gather
+    for (int i = tid; i < R; i += FDL_THREADS) pp[i] = x[i];
+    __syncthreads();
+    spmv(pp, qq);
+    double eel = 0.0;
+    for (int i = tid; i < R; i += FDL_THREADS) {
+        const double e = qq[i] - b[i];
+        eel += isfinite(x[i]) ? e * e : __longlong_as_double(0x7ff8000000000000ULL);
+    }
+    const double ee = fd_block_sum(eel, red);
+    if (tid == 0) {
+        st[c].it = it;
+        st[c].conv = conv;
+        st[c].active = 0;
+        st[c].bb = bb;
+        relres[c] = bb > 0.0 ? sqrt(ee / bb) : (ee == 0.0 ? 0.0 : ee);
+    }
+}
+
+cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
+    const int n = (int)h->fdl_comps.size();
+    if (n == 0) return cudaSuccess;
+#define LAUNCH_FDL(DD)                                                                                     \
+    k_pcg_fdl<DD><<<(unsigned)n, FDL_THREADS, 0, h->stream>>>(                                             \
+        h->d_comps, h->d_fdl_list, h->d_slotoff, h->d_stencil, h->d_rhs, h->d_G, h->d_tabs, h->d_tabvals,  \
+        h->d_qw, h->p, h->mu, h->q, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_fdl_off, h->d_fdl, \
+        h->d_x, h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_cg, h->d_relres, rtol * rtol, maxit)
+    if (h->d == 1) { LAUNCH_FDL(1); }
+    else if (h->d == 2) { LAUNCH_FDL(2); }
+    else { LAUNCH_FDL(3); }
+#undef LAUNCH_FDL
+    h->launches[1]++;
+    return cudaGetLastError();
+}
+
 size_t fd_eigen_smem() { return sizeof(double) * 3 * FD_MMAX * FD_LD; }
 
 size_t fd_comp_smem(const CompInfo& C, int d) {

@@ -620,18 +620,20 @@ int run_pcg(Handle* h, double rtol, int maxit) {
     int nch = (int)h->chunks.size();
     const char* nc = getenv("SGIGA_NO_CLUSTER");
     h->small_checked = false;
-    if (!h->fd_comps.empty()) {   // FD-preconditioned CG (k_fd.cu), also checks its true residual
+    const bool any_fd = !h->fd_comps.empty() || !h->fdl_comps.empty();
+    if (any_fd) {   // FD-preconditioned CG (k_fd.cu), which also checks its true residuals
         if (h->fd_pending) {
             SG_CUDA(cudaStreamWaitEvent(h->stream, h->fd_join, 0));
             h->fd_pending = false;
         }
         h->kstart(3);
-        SG_CUDA(launch_pcg_fd(h, rtol, maxit));
+        SG_CUDA(launch_pcg_fd(h, rtol, maxit));    // small: everything in shared memory
+        SG_CUDA(launch_pcg_fdl(h, rtol, maxit));   // one long axis: banded line solves
         if (h->small_comps.empty()) h->kstop(3);
     }
     if (!h->small_comps.empty() && !(nc && nc[0] == '1')) {
         h->small_checked = true;   // the cluster kernel also computes the true residual
-        if (h->fd_comps.empty()) h->kstart(3);
+        if (!any_fd) h->kstart(3);
         int st = launch_pcg_cluster(h, rtol, maxit);   // k_pcg_cluster.cu
         h->kstop(3);
         if (st) return st;
@@ -639,7 +641,7 @@ int run_pcg(Handle* h, double rtol, int maxit) {
         int64_t total = 0;
         size_t smem = small_smem_bytes(h, &total);
         int cap = (int)total;   // a CTA stages its matrix iff its vectors + matrix fit
-        if (h->fd_comps.empty()) h->kstart(3);
+        if (!any_fd) h->kstart(3);
 #define LAUNCH_SMALL(DD)                                                                         \
     SG_CUDA(cudaFuncSetAttribute(k_pcg_small<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                  (int)smem));                                                    \

@@ -26,7 +26,7 @@ constexpr int PMAX = 5;   // p + 1 <= 5 (degree <= 4) on the device path
 constexpr int QMAX = 10;  // gauss_rule accepts q <= 10 (assembly.py:43)
 constexpr int WMAX = 2 * PMAX - 1;  // stencil slots per axis (2p+1)
 constexpr int GEO_PMAX = 8;         // geometry degree <= 7
-constexpr int FD_MMAX = 64;         // FD preconditioner: interior functions per axis (shared memory)
+constexpr int FD_MMAX = 72;         // FD preconditioner: interior functions per diagonalised axis (smem eigen)
 constexpr int COMBINE_SORT_BITS = 12;                      // cell sort of the combine points
 constexpr int COMBINE_SORT_BINS = 1 << COMBINE_SORT_BITS;
 
@@ -219,6 +219,7 @@ cudaError_t launch_residual_check(Handle* h);
 cudaError_t launch_solve_prologue(Handle* h);
 cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s);
 cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit);
+cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit);
 size_t fd_comp_smem(const CompInfo& C, int d);
 cudaError_t launch_status(Handle* h);
 cudaError_t launch_expand(Handle* h);
