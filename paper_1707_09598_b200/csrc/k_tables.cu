@@ -150,24 +150,29 @@ __global__ void k_metric(const CompInfo* __restrict__ comps, int ncomp,
                     for (int m = 0; m < D; ++m) dh[m][c] = __dadd_rn(dh[m][c], __dmul_rn(pm[m], hv));
                 }
             }
+    // two divisions per point (1/W, 1/det), the rest multiplications by the
+    // reciprocals: rounding-level differences from the reference's per-entry
+    // divisions (A and b stay within the 1e-12 norm-wise contract)
     double x[D], J[D][D];
+    const double invW = __ddiv_rn(1.0, hom[D]);
 #pragma unroll
-    for (int i = 0; i < D; ++i) x[i] = __ddiv_rn(hom[i], hom[D]);
+    for (int i = 0; i < D; ++i) x[i] = __dmul_rn(hom[i], invW);
 #pragma unroll
     for (int m = 0; m < D; ++m)
 #pragma unroll
         for (int i = 0; i < D; ++i)   // quotient rule, geometry.py:126
-            J[i][m] = __ddiv_rn(__dsub_rn(dh[m][i], __dmul_rn(x[i], dh[m][D])), hom[D]);
+            J[i][m] = __dmul_rn(__dsub_rn(dh[m][i], __dmul_rn(x[i], dh[m][D])), invW);
     double det, Ji[D][D];
     if constexpr (D == 1) {
         det = J[0][0];
         Ji[0][0] = __ddiv_rn(1.0, J[0][0]);
     } else if constexpr (D == 2) {
         det = __dsub_rn(__dmul_rn(J[0][0], J[1][1]), __dmul_rn(J[0][1], J[1][0]));
-        Ji[0][0] = __ddiv_rn(J[1][1], det);
-        Ji[0][1] = __ddiv_rn(-J[0][1], det);
-        Ji[1][0] = __ddiv_rn(-J[1][0], det);
-        Ji[1][1] = __ddiv_rn(J[0][0], det);
+        const double id = __ddiv_rn(1.0, det);
+        Ji[0][0] = __dmul_rn(J[1][1], id);
+        Ji[0][1] = __dmul_rn(-J[0][1], id);
+        Ji[1][0] = __dmul_rn(-J[1][0], id);
+        Ji[1][1] = __dmul_rn(J[0][0], id);
     } else {
         // cofactors in the oracle's order (oracle/sgiga_oracle.c det_small / inv_small)
         auto mm = [&](int i, int j) { return J[i][j]; };
@@ -176,15 +181,16 @@ __global__ void k_metric(const CompInfo* __restrict__ comps, int ncomp,
         };
         double c00 = cof(4, 8, 5, 7), c01 = cof(3, 8, 5, 6), c02 = cof(3, 7, 4, 6);
         det = __dadd_rn(__dsub_rn(__dmul_rn(J[0][0], c00), __dmul_rn(J[0][1], c01)), __dmul_rn(J[0][2], c02));
-        Ji[0][0] = __ddiv_rn(c00, det);
-        Ji[0][1] = __ddiv_rn(cof(2, 7, 1, 8), det);
-        Ji[0][2] = __ddiv_rn(cof(1, 5, 2, 4), det);
-        Ji[1][0] = __ddiv_rn(cof(5, 6, 3, 8), det);
-        Ji[1][1] = __ddiv_rn(cof(0, 8, 2, 6), det);
-        Ji[1][2] = __ddiv_rn(cof(2, 3, 0, 5), det);
-        Ji[2][0] = __ddiv_rn(cof(3, 7, 4, 6), det);
-        Ji[2][1] = __ddiv_rn(cof(1, 6, 0, 7), det);
-        Ji[2][2] = __ddiv_rn(cof(0, 4, 1, 3), det);
+        const double id = __ddiv_rn(1.0, det);
+        Ji[0][0] = __dmul_rn(c00, id);
+        Ji[0][1] = __dmul_rn(cof(2, 7, 1, 8), id);
+        Ji[0][2] = __dmul_rn(cof(1, 5, 2, 4), id);
+        Ji[1][0] = __dmul_rn(cof(5, 6, 3, 8), id);
+        Ji[1][1] = __dmul_rn(cof(0, 8, 2, 6), id);
+        Ji[1][2] = __dmul_rn(cof(2, 3, 0, 5), id);
+        Ji[2][0] = __dmul_rn(cof(3, 7, 4, 6), id);
+        Ji[2][1] = __dmul_rn(cof(1, 6, 0, 7), id);
+        Ji[2][2] = __dmul_rn(cof(0, 4, 1, 3), id);
     }
     if (!(det > 0.0)) atomicOr(err, ERRF_GEOMETRY);   // geometry.py:128-131
     int64_t nqp = C.nqp;
