@@ -183,168 +183,6 @@ k_pcg_small(const CompInfo* __restrict__ comps, const int* __restrict__ list,
     }
 }
 
-// ---------------------------------------------------------------------------
-// small path on a thread-block cluster: K CTAs (SMs) per component, rows
-// split contiguously, every CTA keeps a full copy of p; reductions and the
-// new p slice are broadcast through distributed shared memory (DSMEM) and
-// ordered by cluster barriers.  All CTAs sum the K partials in rank order,
-// so the scalars (and the iterates) are identical on every CTA and
-// deterministic run to run.
-// ---------------------------------------------------------------------------
-__host__ __device__ inline int64_t cluster_vec_doubles(int64_t R, int64_t RL, int64_t H, int64_t NS) {
-    // cluster partials [2][8], red [64], x r z d q (own rows), p (+halo, full),
-    // offs (int), rowbase (int, own rows), SpMV partials, pad
-    return 16 + 64 + 5 * RL + R + 2 * H + (NS + 1) / 2 + 1 + (RL + 1) / 2 + 1 + (RL > 1024 ? RL : 1024) + 2;
-}
-
-template <int D>
-__global__ void __launch_bounds__(SMALL_THREADS)
-k_pcg_cluster(const CompInfo* __restrict__ comps, const int* __restrict__ list,
-              const int* __restrict__ slotoff, const double* __restrict__ stencil,
-              const double* __restrict__ rhs, const double* __restrict__ dinv,
-              double* __restrict__ xout, CgState* __restrict__ st, double rtol2, int maxit,
-              int smem_doubles) {
-    namespace cgs = cooperative_groups;
-    cgs::cluster_group cluster = cgs::this_cluster();
-    const int K = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
-    extern __shared__ double sm[];
-    const int c = list[blockIdx.x / K];
-    const CompInfo& Cg = comps[c];
-    const int R = (int)Cg.rows, H = (int)Cg.halo, NS = (int)Cg.nslots;
-    const int RLmax = (R + K - 1) / K;
-    const int lo = min(R, rank * RLmax), hi = min(R, lo + RLmax), RL = hi - lo;
-    const int64_t vec = cluster_vec_doubles(R, RLmax, H, NS);
-    const int NSS = RL > 0 ? (int)min((int64_t)NS, (smem_doubles - vec) / max(RL, 1)) : 0;
-    double* cred = sm;                    // [2][8] partials of every rank (written remotely)
-    double* red = cred + 16;              // [64]
-    double* xs = red + 64;                // own rows
-    double* rs_ = xs + RLmax;
-    double* zs = rs_ + RLmax;
-    double* ds = zs + RLmax;
-    double* qv = ds + RLmax;
-    double* pe = qv + RLmax;              // [H + R + H], full copy
-    double* ps = pe + H;
-    int* offs = reinterpret_cast<int*>(pe + R + 2 * H);
-    int* rbv = offs + NS + (NS & 1);
-    double* parts = reinterpret_cast<double*>(rbv + RLmax + (RLmax & 1));
-    double* msm = sm + vec;               // [NSS][RL] own rows, slot-major
-    const double* gval = stencil + Cg.mat_off;
-    const double* b = rhs + Cg.vec_off;
-    const double* di = dinv + Cg.vec_off;
-    const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = nth >> 5, nrb = (RL + 31) >> 5;
-    const int NG = nrb == 0 ? 1 : (nrb <= nwarps ? nwarps / nrb : 1);
-
-    for (int i = tid; i < NS; i += nth) offs[i] = slotoff[Cg.so_off + i];
-    for (int i = tid; i < RL; i += nth) rbv[i] = rowbase_of(Cg, D, lo + i);
-    for (int i = tid; i < NSS * RL; i += nth) {
-        const int t = i / RL, il = i % RL;
-        msm[i] = gval[(size_t)t * R + lo + il];
-    }
-    for (int i = tid; i < H; i += nth) { pe[i] = 0.0; pe[H + R + i] = 0.0; }
-    for (int i = tid; i < R; i += nth) ps[i] = di[i] * b[i];   // p0 = z0 = D^-1 b, full copy
-    double v2[2] = {0.0, 0.0};
-    for (int il = tid; il < RL; il += nth) {
-        const int i = lo + il;
-        double bi = b[i], dd = di[i], z = dd * bi;
-        xs[il] = 0.0; rs_[il] = bi; ds[il] = dd; zs[il] = z;
-        v2[0] += bi * z;
-        v2[1] += bi * bi;
-    }
-    // cluster-wide sum of NV values: block reduce, broadcast to every rank's
-    // cred[slot][rank], cluster barrier, fixed rank-order sum
-    auto cluster_sum = [&](double* v, int NV, int slot) {
-        for (int k = 0; k < NV; ++k)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-        if (lane == 0)
-            for (int k = 0; k < NV; ++k) red[k * 32 + warp] = v[k];
-        __syncthreads();
-        if (warp == 0) {
-            for (int k = 0; k < NV; ++k) {
-                double t = lane < nwarps ? red[k * 32 + lane] : 0.0;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                if (lane < K) {   // lane r writes this CTA's partial into rank r's smem
-                    double* dst = cluster.map_shared_rank(cred, lane);
-                    dst[(slot + k) * 8 + rank] = t;
-                }
-            }
-        }
-        cluster.sync();
-        for (int k = 0; k < NV; ++k) {
-            double s = 0.0;
-            for (int r = 0; r < K; ++r) s += cred[(slot + k) * 8 + r];
-            v[k] = s;
-        }
-    };
-    cluster_sum(v2, 2, 0);
-    double rho = v2[0];
-    const double bb = v2[1];
-    int it = 0, conv = (bb == 0.0);
-    cluster.sync();   // every rank has read cred before it is rewritten
-    while (!conv && it < maxit) {
-        for (int w = warp; w < nrb * NG; w += nwarps) {
-            const int rbk = w % nrb, g = w / nrb, il = rbk * 32 + lane;
-            double y0 = 0.0, y1 = 0.0;
-            if (il < RL) {
-                const int rb = rbv[il];
-                int t = g;
-                for (; t + NG < NSS; t += 2 * NG) {
-                    y0 += msm[t * RL + il] * ps[rb + offs[t]];
-                    y1 += msm[(t + NG) * RL + il] * ps[rb + offs[t + NG]];
-                }
-                if (t < NSS) { y0 += msm[t * RL + il] * ps[rb + offs[t]]; t += NG; }
-                const double* gv = gval + lo + il;
-                for (; t + NG < NS; t += 2 * NG) {
-                    double a0 = __ldg(gv + (size_t)t * R), a1 = __ldg(gv + (size_t)(t + NG) * R);
-                    y0 += a0 * ps[rb + offs[t]];
-                    y1 += a1 * ps[rb + offs[t + NG]];
-                }
-                if (t < NS) y0 += __ldg(gv + (size_t)t * R) * ps[rb + offs[t]];
-                parts[g * RL + il] = y0 + y1;
-            }
-        }
-        __syncthreads();
-        double pq[1] = {0.0};
-        for (int il = tid; il < RL; il += nth) {
-            double y = parts[il];
-            for (int g = 1; g < NG; ++g) y += parts[g * RL + il];
-            qv[il] = y;
-            pq[0] += ps[lo + il] * y;
-        }
-        cluster_sum(pq, 1, 2);
-        const double alpha = rho / pq[0];
-        double w[2] = {0.0, 0.0};
-        for (int il = tid; il < RL; il += nth) {
-            double ri = rs_[il] - alpha * qv[il];
-            xs[il] += alpha * ps[lo + il];
-            double zi = ds[il] * ri;
-            rs_[il] = ri; zs[il] = zi;
-            w[0] += ri * ri;
-            w[1] += ri * zi;
-        }
-        cluster_sum(w, 2, 0);
-        ++it;
-        if (w[0] <= rtol2 * bb) { conv = 1; break; }
-        const double beta = w[1] / rho;
-        rho = w[1];
-        // new p for own rows, written into every rank's full copy
-        for (int il = tid; il < RL; il += nth) {
-            const double pn = zs[il] + beta * ps[lo + il];
-            for (int r = 0; r < K; ++r) cluster.map_shared_rank(ps, r)[lo + il] = pn;
-        }
-        cluster.sync();   // all p slices visible; cred slots free again
-    }
-    for (int il = tid; il < RL; il += nth) xout[Cg.vec_off + lo + il] = xs[il];
-    if (tid == 0 && rank == 0) {
-        st[c].it = it;
-        st[c].conv = conv;
-        st[c].active = 0;
-        st[c].bb = bb;
-    }
-    cluster.sync();   // no CTA exits while others may still write into its smem
-}
 
 // ---------------------------------------------------------------------------
 // large path: chunked kernels
