@@ -35,7 +35,6 @@
 
 namespace sgiga {
 
-constexpr int FAST_THREADS = 352;   // 11 warps: 4*W^2+1 stage-2 items for p = 4 in one round
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     unsigned s = (unsigned)__cvta_generic_to_shared(dst);
@@ -77,28 +76,33 @@ struct FastCfg {
     // stage-1 units in <= 192 threads, a ring of P+1 rows (a flushed row's
     // slot is zeroed one interval later) and two stream-basis buffers
     static constexpr int S1T = 32 * ((NPAIR + 1 + PPW - 1) / PPW);
-    static constexpr bool PIPE = D == 3 && S1T <= 192;
+    // threads: 352 (11 warps); a 3-D stage 1 wider than 6 warps (P = 5: ten
+    // warps, one pair each) gets a 9-warp stage-3 group on top (608 threads,
+    // one CTA per SM)
+    static constexpr int NT = (D == 3 && S1T > 192) ? S1T + 288 : 352;
+    static constexpr int MINB = NT > 352 ? 1 : 2;      // resident CTAs per SM (launch bounds)
+    static constexpr bool PIPE = D == 3;
     // plane windows by one TMA tensor copy per plane (TM: the component's
-    // 4-D tensor map exists -- Q even makes every global stride a multiple of
-    // 16 bytes); the smem window is then dense (row stride NX)
-    static constexpr bool TMA = TM && PIPE && Q % 2 == 0;
-    static constexpr int NAP = D >= 2 ? (TMA ? NX : (NX | 1)) : 1;   // smem row stride of a plane
+    // 4-D tensor map exists -- every global stride a multiple of 16 bytes);
+    // the smem rows are then NX padded to an even count (box inner extent)
+    static constexpr bool TMA = TM && PIPE;
+    static constexpr int NAP = D >= 2 ? (TMA ? ((NX + 1) & ~1) : (NX | 1)) : 1;   // smem row stride of a plane
     static constexpr int RING = PIPE ? P + 1 : P;      // alive rows (+1 draining)
     static constexpr int nGw = NG * NB * NAP;          // one plane buffer
+    static constexpr int sGw = (nGw + 15) & ~15;       // buffer stride (128-byte aligned TMA destination)
     // shared-memory layout (doubles)
     static constexpr int oGw = 0;                      // [2][NG][NB][NAP]
-    static constexpr int oTa = oGw + 2 * nGw;          // [4][NA][P]
+    static constexpr int oTa = oGw + 2 * sGw;          // [4][NA][P]
     static constexpr int oTb = oTa + 4 * NA * P;       // [4][NB][P]
     static constexpr int oPhiA = oTb + 4 * NB * P;     // [NA]
     static constexpr int oPhiB = oPhiA + NA;           // [NB]
     static constexpr int oS1 = oPhiB + NB;             // [NPAIR][NA][WB]
     static constexpr int oSL1 = oS1 + NPAIR * NA * WB; // [NA]
-    static constexpr int oP2 = oSL1 + NA;              // [NPAIR][P][P][WB]
     // stage-2 output slots: the 4 stream types, type 0 (4 pairs in 3-D) split
     // in two halves when the threads allow, + the load term
-    static constexpr bool SPLIT = D == 3 && 5 * WAB + 1 <= 352;
+    static constexpr bool SPLIT = D == 3 && 5 * WAB + 1 <= NT;
     static constexpr int NT2 = SPLIT ? 5 : 4;
-    static constexpr int oS2 = oP2 + NPAIR * P * P * WB;  // [NT2][WAB] + load
+    static constexpr int oS2 = oSL1 + NA;              // [NT2][WAB] + load
     static constexpr int oBs = oS2 + NT2 * WAB + 1;    // [2][Q][P]
     static constexpr int oAcc = oBs + (PIPE ? 4 : 2) * Q * P;   // Bs: [PIPE ? 2 : 1][2][Q][P]; Acc: [RING][W][WAB]
     static constexpr int oAccL = oAcc + RING * W * WAB;
@@ -109,13 +113,14 @@ template <int D, int P, int Q, bool TM>
 size_t fast_smem_bytes() { return sizeof(double) * FastCfg<D, P, Q, TM>::total; }
 
 template <int D, int P, int Q, bool TM>
-__global__ void __launch_bounds__(FAST_THREADS, 2)
+__global__ void __launch_bounds__(FastCfg<D, P, Q, TM>::NT, FastCfg<D, P, Q, TM>::MINB)
 k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tabs,
                 const Pencil* __restrict__ pencils, const double* __restrict__ vals,
                 const double* __restrict__ Gbuf, double* __restrict__ stencil,
                 double* __restrict__ rhs, double* __restrict__ dinv, long long* __restrict__ prof,
                 const CUtensorMap* __restrict__ tmaps) {
     using F = FastCfg<D, P, Q, TM>;
+    constexpr int NT = F::NT;
     constexpr int p = F::p, W = F::W;
     extern __shared__ __align__(128) double sm[];
     double* Ta = sm + F::oTa;
@@ -124,7 +129,6 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     double* phiB = sm + F::oPhiB;
     double* S1 = sm + F::oS1;
     double* SL1 = sm + F::oSL1;
-    double* P2 = sm + F::oP2;
     double* S2 = sm + F::oS2;
     double* Bs = sm + F::oBs;
     double* Acc = sm + F::oAcc;
@@ -145,7 +149,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     auto build_T = [&](int k, int i, double* T, double* phi, int NXk) {
         const TabInfo& TT = tabs[C.tab[k]];
         const int64_t nq = (int64_t)TT.nel * Q;
-        for (int idx = tid; idx < 4 * NXk * P; idx += FAST_THREADS) {
+        for (int idx = tid; idx < 4 * NXk * P; idx += NT) {
             int kk = idx % P, x = (idx / P) % NXk, type = idx / (P * NXk);
             int t = x / Q, g = x % Q, e = i - p + t;
             double v = 0.0;
@@ -157,7 +161,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             }
             T[idx] = v;
         }
-        for (int x = tid; x < NXk; x += FAST_THREADS) {
+        for (int x = tid; x < NXk; x += NT) {
             int t = x / Q, g = x % Q, e = i - p + t;
             phi[x] = (e >= 0 && e < TT.nel) ? vals[TT.val_off + ((int64_t)e * Q + g) * P + (p - t)] : 0.0;
         }
@@ -166,9 +170,9 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     else if (tid == 0) { Ta[0] = 1.0; Ta[1] = Ta[2] = Ta[3] = 0.0; phiA[0] = 1.0; }
     if (D >= 3) build_T(kb, pc.ib, Tb, phiB, F::NB);
     else if (tid == 0) { Tb[0] = 1.0; Tb[1] = Tb[2] = Tb[3] = 0.0; phiB[0] = 1.0; }
-    for (int idx = tid; idx < F::RING * W * F::WAB + F::RING; idx += FAST_THREADS) Acc[idx] = 0.0;
+    for (int idx = tid; idx < F::RING * W * F::WAB + F::RING; idx += NT) Acc[idx] = 0.0;
     // invalid window points stay zero in both plane buffers
-    for (int idx = tid; idx < 2 * F::nGw; idx += FAST_THREADS) sm[F::oGw + idx] = 0.0;
+    for (int idx = tid; idx < 2 * F::sGw; idx += NT) sm[F::oGw + idx] = 0.0;
     __shared__ __align__(8) uint64_t fast_mbar[2];   // TMA variant: one barrier per plane buffer
     if (F::TMA && tid == 0) {
         mbar_init(&fast_mbar[0], 1);
@@ -188,17 +192,17 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     // every plane copies the same (entry, xb, xa) window: each thread's share
     // (smem offset, offset from the plane's first valid point) is decoded
     // once per pencil, so a plane costs a few instructions per copy
-    constexpr int MAXC0 = (F::NG * F::NB * F::NA + FAST_THREADS - 1) / FAST_THREADS;
+    constexpr int MAXC0 = (F::NG * F::NB * F::NA + NT - 1) / NT;
     constexpr bool PRE = !F::TMA && MAXC0 <= 8;   // else: row teams, one division per row
     constexpr int MAXC = PRE ? MAXC0 : 1;
     int c_sm[MAXC], c_gl[MAXC];
-    constexpr int LPR = F::NA <= 16 ? 16 : 32, NTEAM = FAST_THREADS / LPR;
+    constexpr int LPR = F::NA <= 16 ? 16 : 32, NTEAM = NT / LPR;
     const int team = tid / LPR, tl_ = tid % LPR;
     if constexpr (PRE) {
         const int per_row = nxa, ntot = F::NG * nxb * nxa;
 #pragma unroll
         for (int k = 0; k < MAXC; ++k) {
-            const int idx = tid + k * FAST_THREADS;
+            const int idx = tid + k * NT;
             c_sm[k] = -1;
             c_gl[k] = 0;
             if (idx < ntot) {
@@ -215,10 +219,13 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     // counted on the buffer's mbarrier (phase bit per buffer in mb_phase)
     uint32_t mb_phase = 0;
     const CUtensorMap* tmap = F::TMA ? tmaps + pc.comp : nullptr;
-    const int tx0 = D >= 2 ? (pc.ia - p) * Q : 0, tx1 = D >= 3 ? (pc.ib - p) * Q : 0;
+    // the innermost box start must be 16-byte aligned: an odd window start
+    // (Q odd) is rounded down one point and the plane is read shifted by tsh
+    const int tx0u = D >= 2 ? (pc.ia - p) * Q : 0, tx1 = D >= 3 ? (pc.ib - p) * Q : 0;
+    const int tsh = F::TMA ? (tx0u & 1) : 0, tx0 = tx0u - tsh;
     auto load_plane_tma = [&](int64_t Qs, int buf) {
         if (tid != 0) return;
-        double* Gw = sm + F::oGw + buf * F::nGw;
+        double* Gw = sm + F::oGw + buf * F::sGw;
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_expect_tx(&fast_mbar[buf], (uint32_t)(F::nGw * 8));
         asm volatile(
@@ -234,7 +241,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         mb_phase ^= 1u << buf;
     };
     auto load_plane = [&](int64_t Qs, int buf) {
-        double* Gw = sm + F::oGw + buf * F::nGw;
+        double* Gw = sm + F::oGw + buf * F::sGw;
         const double* base = Gc + Qs * qs_s + Xa0 + Xb0 * qs_b;
         if constexpr (PRE) {
 #pragma unroll
@@ -265,7 +272,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const int Ss = C.S[s], Sa = D >= 2 ? C.S[ka] : 1, Sb = D >= 3 ? C.S[kb] : 1, SAB = Sa * Sb;
     const int absm_s = C.absm[s], n_s = C.n[s];
     const int64_t ss_s = C.ss[s], rs_s = C.rs[s], rows_c = C.rows;
-    for (int cab = tid; cab < SAB; cab += FAST_THREADS) {
+    for (int cab = tid; cab < SAB; cab += NT) {
         const int ca = cab / Sb, cb = cab % Sb;
         auto rel = [&](int k, int ik, int sk) -> int {
             const int j = C.absm[k] ? sk + 1 : ik + sk - p, o = j - ik;
@@ -281,9 +288,9 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         tsp[pr] = 2 * ((pr / D) == s) + ((pr % D) == s);
         tap[pr] = 2 * ((pr / D) == ka) + ((pr % D) == ka);
     }
-    // this thread's stage-2 item (one per thread: 4 W^2 + 1 <= FAST_THREADS)
+    // this thread's stage-2 item (one per thread: 4 W^2 + 1 <= NT)
     constexpr int NT2 = F::NT2, LOAD2 = NT2 * F::WAB;
-    static_assert(LOAD2 + 1 <= FAST_THREADS, "one stage-2 item per thread");
+    static_assert(LOAD2 + 1 <= NT, "one stage-2 item per thread");
     const int i2_it = tid;
     const bool i2_on = D >= 2 && i2_it < LOAD2 + 1, i2_load = i2_it == LOAD2;
     const int i2_slot = i2_it / F::WAB, i2_sab = i2_it % F::WAB;
@@ -309,7 +316,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         const int64_t row = row_base + (int64_t)(i - 1) * rs_s;
         const double* accr = Acc + ((i % F::RING) * W) * F::WAB;
         double* dst = stencil + C.mat_off + row;
-        for (int it = tid; it < Ss * SAB; it += FAST_THREADS) {
+        for (int it = tid; it < Ss * SAB; it += NT) {
             const int cab = it % SAB, cs = it / SAB;
             const int j = absm_s ? cs + 1 : i + cs - p, o = j - i;   // stream-axis column
             const int oab = flt_rel[cab];
@@ -328,11 +335,11 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         // of plane j (+ zero the ring slot flushed last interval) | the rest:
         // stage 3 of plane j-1] B2 [stage 2 of plane j; flush the row element
         // e(j-1) completed]; j = nplanes drains the last stage 3 and flushes
-        constexpr int S1T = F::S1T, S3T = FAST_THREADS - F::S1T;
+        constexpr int S1T = F::S1T, S3T = NT - F::S1T;
         const int nplanes = (e_last - e_first + 1) * Q;
         auto load_bs = [&](int e) {
             double* Bd = Bs + (e & 1) * 2 * Q * P;
-            for (int idx = tid; idx < 2 * Q * P; idx += FAST_THREADS) {
+            for (int idx = tid; idx < 2 * Q * P; idx += NT) {
                 const int der = idx / (Q * P), rem = idx % (Q * P);
                 Bd[idx] = vals[Ts.val_off + (der ? nq_s * P : 0) + (int64_t)e * Q * P + rem];
             }
@@ -359,7 +366,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 if (g == 0 && j > 0) load_bs(e);
             }
             __syncthreads();   // B1
-            const double* Gw = sm + F::oGw + buf * F::nGw;
+            const double* Gw = sm + F::oGw + buf * F::sGw + tsh;
             if (tid < S1T) {
                 if (has) {   // ---- stage 1 (plane j): contract tile axis b ----
                     const int half = F::PPW == 2 ? (lane >> 4) : 0;
@@ -468,7 +475,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc = 0;
     load_plane((int64_t)e_first * Q, 0);
     for (int e = e_first; e <= e_last; ++e) {
-        for (int idx = tid; idx < 2 * Q * P; idx += FAST_THREADS) {
+        for (int idx = tid; idx < 2 * Q * P; idx += NT) {
             int der = idx / (Q * P), rem = idx % (Q * P);
             Bs[idx] = vals[Ts.val_off + (der ? nq_s * P : 0) + (int64_t)e * Q * P + rem];
         }
@@ -484,7 +491,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             }
             __syncthreads();
             if (pr) { long long t = clock64(); tp[0] += t - tc; tc = t; }
-            const double* Gw = sm + F::oGw + buf * F::nGw;
+            const double* Gw = sm + F::oGw + buf * F::sGw;
             // ---- stage 1: contract tile axis b ------------------------------
             if constexpr (D == 3) {
                 const int half = F::PPW == 2 ? (lane >> 4) : 0;
@@ -567,7 +574,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             __syncthreads();
             if (pr) { long long t = clock64(); tp[3] += t - tc; tc = t; }
             // ---- stage 3: rank-1 update of the alive rows of element e ------
-            for (int it = tid; it < P * F::WAB; it += FAST_THREADS) {
+            for (int it = tid; it < P * F::WAB; it += NT) {
                 const int sab = it % F::WAB, al = it / F::WAB;
                 const int i = e + al;
                 if (i < r0 || i >= r1) continue;
@@ -601,7 +608,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             const int64_t row = row_base + (int64_t)(i - 1) * rs_s;
             double* accr = Acc + ((i % F::RING) * W) * F::WAB;
             double* dst = stencil + C.mat_off + row;
-            for (int it = tid; it < Ss * SAB; it += FAST_THREADS) {
+            for (int it = tid; it < Ss * SAB; it += NT) {
                 const int cab = it % SAB, cs = it / SAB;
                 const int j = absm_s ? cs + 1 : i + cs - p, o = j - i;   // stream-axis column
                 const int oab = flt_rel[cab];
@@ -615,7 +622,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 dinv[C.vec_off + row] = 1.0 / accr[p * F::WAB + dsab];
             }
             __syncthreads();
-            for (int it = tid; it < W * F::WAB; it += FAST_THREADS) accr[it] = 0.0;
+            for (int it = tid; it < W * F::WAB; it += NT) accr[it] = 0.0;
             if (tid == 0) AccL[i % F::RING] = 0.0;
             __syncthreads();
         }
@@ -656,7 +663,10 @@ static bool build_tmaps(Handle* h, int NX) {
         if (C.qs[a] != 1 || C.qs[b] != (int64_t)Na || C.qs[s] != (int64_t)(Na * Nb)) return false;
         const cuuint64_t dims[4] = {Na, Nb, Ns, (cuuint64_t)NG};
         const cuuint64_t strides[3] = {Na * 8, Na * Nb * 8, (cuuint64_t)C.nqp * 8};
-        const cuuint32_t box[4] = {(cuuint32_t)NX, (cuuint32_t)NX, 1, (cuuint32_t)NG};
+        // box rows padded to an even count (16-byte inner extent); every
+        // global stride must be a multiple of 16 bytes as well
+        const cuuint32_t box[4] = {(cuuint32_t)((NX + 1) & ~1), (cuuint32_t)NX, 1, (cuuint32_t)NG};
+        if (strides[0] % 16 || strides[1] % 16 || strides[2] % 16 || (C.qp_off * 8) % 16) return false;
         const cuuint32_t estr[4] = {1, 1, 1, 1};
         if (encode(&maps[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)(h->d_G + C.qp_off), dims, strides, box,
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -681,19 +691,22 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     if (h->mu != 1 || h->q != h->p + 1 || h->pencils.empty()) return false;
     const int key = h->d * 10 + (h->p + 1);
     const char* nt = getenv("SGIGA_NO_TMA");
-    const bool tma = h->d == 3 && (h->q % 2 == 0) && !(nt && nt[0] == '1') &&
+    const bool tma = h->d == 3 && !(nt && nt[0] == '1') &&
                      build_tmaps(h, (h->p + 1) * h->q);
     size_t smem = 0;
     const void* fn = nullptr;
+    int nthreads = 352;
     switch (key) {
 #define CASE(DD, PP)                                                                 \
     case DD * 10 + PP:                                                               \
         if (tma && FastCfg<DD, PP, PP, true>::TMA) {                                 \
             smem = fast_smem_bytes<DD, PP, PP, true>();                              \
             fn = (const void*)k_assemble_fast<DD, PP, PP, true>;                     \
+            nthreads = FastCfg<DD, PP, PP, true>::NT;                                \
         } else {                                                                     \
             smem = fast_smem_bytes<DD, PP, PP, false>();                             \
             fn = (const void*)k_assemble_fast<DD, PP, PP, false>;                    \
+            nthreads = FastCfg<DD, PP, PP, false>::NT;                               \
         }                                                                            \
         break;
         CASE(1, 2) CASE(1, 3) CASE(1, 4) CASE(1, 5)
@@ -713,7 +726,7 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     void* args[] = {(void*)&h->d_comps, (void*)&h->d_tabs, (void*)&h->d_pencils, (void*)&h->d_tabvals,
                     (void*)&h->d_G, (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv,
                     (void*)&prof, (void*)&h->d_tmaps};
-    *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(FAST_THREADS), args, smem, h->stream);
+    *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(nthreads), args, smem, h->stream);
     if (prof) {
         long long t[8];
         cudaMemcpy(t, prof, sizeof t, cudaMemcpyDeviceToHost);

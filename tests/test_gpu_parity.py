@@ -120,10 +120,12 @@ def test_fast_assembly_matches_generic(name, terms, monkeypatch):
         assert normwise(bf, bg) <= 1e-13
 
 
-def test_tma_plane_copies_match_cp_async(monkeypatch):
-    """The TMA tensor-copy plane loads (zero-filled out-of-patch windows)
-    assemble bitwise the same stencil as the cp.async path."""
-    cfg = configs.get_config("cfg2")
+@pytest.mark.parametrize("name,pick", [("cfg2", (0, 5, 17, 30)), ("cfg5", (0, 7, 40, 100, 135))])
+def test_tma_plane_copies_match_cp_async(name, pick, monkeypatch):
+    """The TMA tensor-copy plane loads (zero-filled out-of-patch windows; for
+    odd Q an even-aligned box read shifted by one point) assemble bitwise the
+    same stencil as the cp.async path."""
+    cfg = configs.get_config(name)
     spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
     mats = {}
     for mode in ("tma", "cpasync"):
@@ -132,7 +134,7 @@ def test_tma_plane_copies_match_cp_async(monkeypatch):
         b = Batch(spec)
         try:
             b.assemble()
-            mats[mode] = [b.export_csr(c) for c in (0, 5, 17, 30)]
+            mats[mode] = [b.export_csr(c) for c in pick]
         finally:
             b.close()
     for (A1, b1), (A2, b2) in zip(mats["tma"], mats["cpasync"]):
