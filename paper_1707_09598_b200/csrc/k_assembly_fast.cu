@@ -80,7 +80,10 @@ struct FastCfg {
     // warps, one pair each) gets a 9-warp stage-3 group on top (608 threads,
     // one CTA per SM)
     static constexpr int NT = (D == 3 && S1T > 192) ? S1T + 288 : 352;
-    static constexpr int MINB = NT > 352 ? 1 : 2;      // resident CTAs per SM (launch bounds)
+    // resident CTAs per SM (launch bounds): 3-D degree <= 3 fits three 352-thread
+    // CTAs (<= 62 registers, ~58 KB shared memory each) -- 33 warps hide the
+    // per-plane barrier and DFMA latency better than two
+    static constexpr int MINB = NT > 352 ? 1 : (D == 3 && P <= 4 ? 3 : 2);
     static constexpr bool PIPE = D == 3;
     // plane windows by one TMA tensor copy per plane (TM: the component's
     // 4-D tensor map exists -- every global stride a multiple of 16 bytes);
