@@ -102,6 +102,15 @@ def fp64_peak_tflops():
     return float(tf.value)
 
 
+def _ncu_traffic() -> dict:
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -285,8 +294,14 @@ def run_sgiga(args, cfg):
                     "frac": G["frac"], "traffic": None, "kernel": "k_pcg_small/k_cg_* (batched Jacobi-PCG)",
                     "algorithmic_bytes_per_launch": cg_bytes, "peak_source": G["peak_source"]}
     else:
+        # DRAM bytes of one launch of the dominant kernel from the committed
+        # `ncu --set full` capture (profiles/capture.sh -> profiles/summarize.py)
+        tr = _ncu_traffic().get(args.config, {})
         roofline = {"bound": "tensor", "achieved": G["achieved"], "peak": G["peak"], "unit": "TFLOP/s",
-                    "frac": G.get("frac"), "traffic": None, "kernel": dom,
+                    "frac": G.get("frac"),
+                    "traffic": tr.get("dram_bytes_per_launch") if dom == "assembly" and R == 1 else None,
+                    "traffic_source": tr.get("source") if dom == "assembly" and R == 1 else None,
+                    "kernel": dom,
                     "note": "FP64 CUDA-core bound; 'tensor' slot holds the measured DFMA peak",
                     "peak_source": G["peak_source"]}
 
