@@ -54,6 +54,11 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
                  : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ long long clk64() {   // ordered w.r.t. memory ops and barriers
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;\n" : "=l"(t)::"memory");
+    return t;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
@@ -62,6 +67,7 @@ template <int D, int P, int Q, bool TM = false>
 struct FastCfg {
     static constexpr int p = P - 1;
     static constexpr int W = 2 * P - 1;               // relative slots per axis
+    static constexpr int RP = (P + 1) & ~1;            // pair-table row stride (16-byte rows: double2 loads)
     static constexpr int NX = P * Q;                   // window points per tile axis
     static constexpr int NA = D >= 2 ? NX : 1;
     static constexpr int NB = D >= 3 ? NX : 1;
@@ -71,43 +77,45 @@ struct FastCfg {
     static constexpr int NG = D * (D + 1) / 2 + 1;     // metric entries + load
     static constexpr int NPAIR = D * D;
     static constexpr int PPW = NX <= 16 ? 2 : 1;       // pairs per warp in stage 1
-    // software-pipelined 3-D variant: stage 1 of plane j and stage 3 of plane
-    // j-1 share one barrier interval (disjoint thread groups); needs the
-    // stage-1 units in <= 192 threads, a ring of P+1 rows (a flushed row's
-    // slot is zeroed one interval later) and two stream-basis buffers
     static constexpr int S1T = 32 * ((NPAIR + 1 + PPW - 1) / PPW);
-    // threads: 352 (11 warps); a 3-D stage 1 wider than 6 warps (P = 5: ten
-    // warps, one pair each) gets a 9-warp stage-3 group on top (608 threads,
-    // one CTA per SM)
-    static constexpr int NT = (D == 3 && S1T > 192) ? S1T + 288 : 352;
-    // resident CTAs per SM (launch bounds): 3-D degree <= 3 fits three 352-thread
-    // CTAs (<= 62 registers, ~58 KB shared memory each) -- 33 warps hide the
-    // per-plane barrier and DFMA latency better than two
-    static constexpr int MINB = NT > 352 ? 1 : (D == 3 && P <= 4 ? 3 : 2);
+    // 3-D: three-stage software pipeline on disjoint thread groups -- in one
+    // barrier interval G1 runs stage 1 of plane j, G2 stage 2 of plane j-1
+    // and G3 stage 3 of plane j-2 (+ the row flushes); S1/SL1/S2 are double
+    // buffered, G2/G3 take two items per thread.  2-D: one 352-thread group,
+    // stages separated by barriers.
     static constexpr bool PIPE = D == 3;
+    // stage-2 output slots: the 4 stream types, type 0 (4 pairs in 3-D) split
+    // in two halves, + the load term
+    static constexpr bool SPLIT = D == 3;
+    static constexpr int NT2 = SPLIT ? 5 : 4;
+    static constexpr int NI2 = NT2 * WAB + 1;          // stage-2 items (+ load)
+    static constexpr int NI3 = P * WAB;                // stage-3 items
+    static constexpr int S2T = PIPE ? 32 * ((NT2 * WB + 1 + 31) / 32) : 0;   // one (slot, s_b) column each
+    static constexpr int S3T = PIPE ? 32 * ((NI3 + 63) / 64) : 0;
+    static constexpr int NT = PIPE ? S1T + S2T + S3T : 352;
+    // resident CTAs per SM (launch bounds)
+    static constexpr int MINB = PIPE ? (NT > 512 ? 1 : (NT > 352 ? 2 : 3)) : 2;
+    static constexpr int NBUF = PIPE ? 2 : 1;          // S1 / SL1 / S2 buffers
     // plane windows by one TMA tensor copy per plane (TM: the component's
     // 4-D tensor map exists -- every global stride a multiple of 16 bytes);
     // the smem rows are then NX padded to an even count (box inner extent)
     static constexpr bool TMA = TM && PIPE;
     static constexpr int NAP = D >= 2 ? (TMA ? ((NX + 1) & ~1) : (NX | 1)) : 1;   // smem row stride of a plane
-    static constexpr int RING = PIPE ? P + 1 : P;      // alive rows (+1 draining)
+    static constexpr int RING = P;                     // alive rows of the accumulator ring
     static constexpr int nGw = NG * NB * NAP;          // one plane buffer
     static constexpr int sGw = (nGw + 15) & ~15;       // buffer stride (128-byte aligned TMA destination)
+    static constexpr int nS1 = NPAIR * NA * WB;
     // shared-memory layout (doubles)
     static constexpr int oGw = 0;                      // [2][NG][NB][NAP]
-    static constexpr int oTa = oGw + 2 * sGw;          // [4][NA][P]
-    static constexpr int oTb = oTa + 4 * NA * P;       // [4][NB][P]
-    static constexpr int oPhiA = oTb + 4 * NB * P;     // [NA]
+    static constexpr int oTa = oGw + 2 * sGw;          // [4][NA][RP]
+    static constexpr int oTb = oTa + 4 * NA * RP;      // [4][NB][RP]
+    static constexpr int oPhiA = oTb + 4 * NB * RP;    // [NA]
     static constexpr int oPhiB = oPhiA + NA;           // [NB]
-    static constexpr int oS1 = oPhiB + NB;             // [NPAIR][NA][WB]
-    static constexpr int oSL1 = oS1 + NPAIR * NA * WB; // [NA]
-    // stage-2 output slots: the 4 stream types, type 0 (4 pairs in 3-D) split
-    // in two halves when the threads allow, + the load term
-    static constexpr bool SPLIT = D == 3 && 5 * WAB + 1 <= NT;
-    static constexpr int NT2 = SPLIT ? 5 : 4;
-    static constexpr int oS2 = oSL1 + NA;              // [NT2][WAB] + load
-    static constexpr int oBs = oS2 + NT2 * WAB + 1;    // [2][Q][P]
-    static constexpr int oAcc = oBs + (PIPE ? 4 : 2) * Q * P;   // Bs: [PIPE ? 2 : 1][2][Q][P]; Acc: [RING][W][WAB]
+    static constexpr int oS1 = oPhiB + NB;             // [NBUF][NPAIR][NA][WB]
+    static constexpr int oSL1 = oS1 + NBUF * nS1;      // [NBUF][NA]
+    static constexpr int oS2 = oSL1 + NBUF * NA;       // [NBUF][NI2]
+    static constexpr int oBs = oS2 + NBUF * NI2;       // [2][2][Q][P]
+    static constexpr int oAcc = oBs + 4 * Q * P;       // [RING][W][WAB]
     static constexpr int oAccL = oAcc + RING * W * WAB;
     static constexpr int total = oAccL + RING;
 };
@@ -152,11 +160,11 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     auto build_T = [&](int k, int i, double* T, double* phi, int NXk) {
         const TabInfo& TT = tabs[C.tab[k]];
         const int64_t nq = (int64_t)TT.nel * Q;
-        for (int idx = tid; idx < 4 * NXk * P; idx += NT) {
-            int kk = idx % P, x = (idx / P) % NXk, type = idx / (P * NXk);
+        for (int idx = tid; idx < 4 * NXk * F::RP; idx += NT) {
+            int kk = idx % F::RP, x = (idx / F::RP) % NXk, type = idx / (F::RP * NXk);
             int t = x / Q, g = x % Q, e = i - p + t;
             double v = 0.0;
-            if (e >= 0 && e < TT.nel) {
+            if (kk < P && e >= 0 && e < TT.nel) {
                 const double* base = vals + TT.val_off + ((int64_t)e * Q + g) * P;
                 double a = (type >> 1) ? base[nq * P + (p - t)] : base[p - t];
                 double b = (type & 1) ? base[nq * P + kk] : base[kk];
@@ -313,65 +321,88 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const int i2_tl = max(ta_lo, i2_sa - p), i2_th = min(ta_hi - 1, i2_sa);
 
     int buf = 0;
-    // flush of one completed row: every storage slot is written (zeros where
-    // the relative offset is out of the band or the column is on the boundary)
-    auto flush_row = [&](int i) {
-        const int64_t row = row_base + (int64_t)(i - 1) * rs_s;
-        const double* accr = Acc + ((i % F::RING) * W) * F::WAB;
-        double* dst = stencil + C.mat_off + row;
-        for (int it = tid; it < Ss * SAB; it += NT) {
-            const int cab = it % SAB, cs = it / SAB;
-            const int j = absm_s ? cs + 1 : i + cs - p, o = j - i;   // stream-axis column
-            const int oab = flt_rel[cab];
-            const bool ok = oab >= 0 && j >= 1 && j <= n_s - 2 && o >= -p && o <= p;
-            const double v = ok ? accr[(o + p) * F::WAB + oab] : 0.0;
-            dst[((int64_t)cs * ss_s + flt_slot[cab]) * rows_c] = v;
-        }
-        if (tid == 0) {
-            const int dsab = D >= 2 ? (p * F::WB + (D >= 3 ? p : 0)) : 0;
-            rhs[C.vec_off + row] = AccL[i % F::RING];
-            dinv[C.vec_off + row] = 1.0 / accr[p * F::WAB + dsab];
-        }
-    };
     if constexpr (F::PIPE) {
-        // interval j: [issue plane j+1, wait plane j] B1 [threads < S1T: stage 1
-        // of plane j (+ zero the ring slot flushed last interval) | the rest:
-        // stage 3 of plane j-1] B2 [stage 2 of plane j; flush the row element
-        // e(j-1) completed]; j = nplanes drains the last stage 3 and flushes
-        constexpr int S1T = F::S1T, S3T = NT - F::S1T;
+        // interval j (j = 0 .. nplanes+1), ONE barrier at its end:
+        //   start: issue plane j+1 into buffer (j+1)&1 (TMA: one thread);
+        //   G1: wait plane j, stage 1 of plane j -> S1/SL1[j&1];
+        //   G2: stage 2 of plane j-1: S1/SL1[(j-1)&1] -> S2[(j-1)&1];
+        //   G3: stage 3 of plane j-2 from S2[(j-2)&1]; when plane j-2 closes
+        //       element ep, row ep is complete: G3 flushes it and zeroes its
+        //       ring slot (two G3-only named barriers) before the next row
+        //       that maps to the slot receives its first update at j+1.
+        constexpr int S1T = F::S1T, S2T = F::S2T, S3T = F::S3T;
+        const bool inG1 = tid < S1T, inG2 = !inG1 && tid < S1T + S2T, inG3 = tid >= S1T + S2T;
+        const int g2t = tid - S1T, g3t = tid - S1T - S2T;
         const int nplanes = (e_last - e_first + 1) * Q;
-        auto load_bs = [&](int e) {
+        // this G2 thread's stage-2 column: (slot, s_b) -> all s_a, summed over
+        // the (at most two) pairs of the slot; decoded once per pencil
+        const bool s2_on = inG2 && g2t < F::NT2 * F::WB + 1, s2_load = g2t == F::NT2 * F::WB;
+        const int s2_slot = g2t / F::WB, s2_sb = g2t % F::WB;
+        int s2_sp[2] = {-1, -1}, s2_ta[2] = {0, 0};   // S1 / Ta offsets of the slot's pairs
+        {
+            const int ts = s2_slot == 4 ? 0 : s2_slot;
+            int c0 = 0, n = 0;
+#pragma unroll
+            for (int pr = 0; pr < NPAIR; ++pr) {
+                if (tsp[pr] != ts) continue;
+                const bool take = ts != 0 || ((s2_slot == 4) == (c0 >= 2));
+                if (ts == 0) ++c0;
+                if (take && n < 2) {
+                    s2_sp[n] = pr * F::NA * W + s2_sb;
+                    s2_ta[n] = tap[pr] * F::NA * F::RP;
+                    ++n;
+                }
+            }
+        }
+        auto load_bs = [&](int e) {   // G3: stream basis values/derivatives of element e
             double* Bd = Bs + (e & 1) * 2 * Q * P;
-            for (int idx = tid; idx < 2 * Q * P; idx += NT) {
+            for (int idx = g3t; idx < 2 * Q * P; idx += S3T) {
                 const int der = idx / (Q * P), rem = idx % (Q * P);
                 Bd[idx] = vals[Ts.val_off + (der ? nq_s * P : 0) + (int64_t)e * Q * P + rem];
             }
         };
-        if (nplanes > 0) {
-            load_bs(e_first);
-            if constexpr (F::TMA) load_plane_tma((int64_t)e_first * Q, 0);
-            else load_plane((int64_t)e_first * Q, 0);
-        }
-        int zrow = -1;
-        for (int j = 0; j <= nplanes; ++j) {
-            const bool has = j < nplanes;
-            const int e = e_first + j / Q, g = j % Q;
-            if (has) {
-                if constexpr (F::TMA) {
-                    if (j + 1 < nplanes) load_plane_tma((int64_t)e_first * Q + j + 1, buf ^ 1);
-                    wait_plane_tma(buf);
-                } else if (j + 1 < nplanes) {
-                    load_plane((int64_t)e_first * Q + j + 1, buf ^ 1);
-                    cp_async_wait_prev();
-                } else {
-                    cp_async_wait_all();
-                }
-                if (g == 0 && j > 0) load_bs(e);
+        auto flush3 = [&](int i) {   // G3: row i -> stencil / rhs / dinv
+            const int64_t row = row_base + (int64_t)(i - 1) * rs_s;
+            const double* accr = Acc + ((i % F::RING) * W) * F::WAB;
+            double* dst = stencil + C.mat_off + row;
+            for (int it = g3t; it < Ss * SAB; it += S3T) {
+                const int cab = it % SAB, cs = it / SAB;
+                const int j = absm_s ? cs + 1 : i + cs - p, o = j - i;   // stream-axis column
+                const int oab = flt_rel[cab];
+                const bool ok = oab >= 0 && j >= 1 && j <= n_s - 2 && o >= -p && o <= p;
+                const double v = ok ? accr[(o + p) * F::WAB + oab] : 0.0;
+                dst[((int64_t)cs * ss_s + flt_slot[cab]) * rows_c] = v;
             }
-            __syncthreads();   // B1
-            const double* Gw = sm + F::oGw + buf * F::sGw + tsh;
-            if (tid < S1T) {
-                if (has) {   // ---- stage 1 (plane j): contract tile axis b ----
+            if (g3t == 0) {
+                rhs[C.vec_off + row] = AccL[i % F::RING];
+                dinv[C.vec_off + row] = 1.0 / accr[p * F::WAB + p * F::WB + p];
+            }
+        };
+        auto bar3 = [&]() { asm volatile("bar.sync 1, %0;\n" ::"r"(S3T) : "memory"); };
+        if (nplanes > 0) {
+            if (inG3) load_bs(e_first);
+            if constexpr (F::TMA) {
+                load_plane_tma((int64_t)e_first * Q, 0);
+            } else {
+                load_plane((int64_t)e_first * Q, 0);
+                cp_async_wait_all();
+            }
+            __syncthreads();
+        }
+        // phase profile (SGIGA_ASM_PROFILE=1): block 0's group leaders record
+        // their own work and the whole interval (work + barrier wait)
+        const bool prf = prof != nullptr && blockIdx.x == 0 && (tid == 0 || tid == S1T || tid == S1T + S2T);
+        long long pw = 0, pt = 0, p0 = prf ? clk64() : 0;
+        for (int j = 0; nplanes > 0 && j < nplanes + 2; ++j) {
+            if (j + 1 < nplanes) {
+                if constexpr (F::TMA) load_plane_tma((int64_t)e_first * Q + j + 1, (j + 1) & 1);
+                else load_plane((int64_t)e_first * Q + j + 1, (j + 1) & 1);
+            }
+            if (inG1) {
+                if (j < nplanes) {   // ---- stage 1 (plane j): contract tile axis b ----
+                    if constexpr (F::TMA) wait_plane_tma(j & 1);
+                    const double* Gw = sm + F::oGw + (j & 1) * F::sGw + tsh;
+                    double* S1w = S1 + (j & 1) * F::nS1;
                     const int half = F::PPW == 2 ? (lane >> 4) : 0;
                     const int xa = F::PPW == 2 ? (lane & 15) : lane;
                     const int prr = warp * F::PPW + half;
@@ -382,7 +413,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 #pragma unroll
                         for (int q2 = 0; q2 < W; ++q2) acc[q2] = 0.0;
                         const double* gcol = Gw + gidx * F::NB * F::NAP + xa;
-                        const double* tr = Tb + tb * F::NB * P;
+                        const double* tr = Tb + tb * F::NB * F::RP;
 #pragma unroll
                         for (int t = 0; t < P; ++t) {
                             if (t < tb_lo || t >= tb_hi) continue;
@@ -390,11 +421,18 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                             for (int g2 = 0; g2 < Q; ++g2) {
                                 const int x = t * Q + g2;
                                 const double gv = gcol[x * F::NAP];
+                                double tv[F::RP];   // warp-uniform row: RP/2 broadcast 16-byte loads
 #pragma unroll
-                                for (int k = 0; k < P; ++k) acc[t + k] += gv * tr[x * P + k];
+                                for (int k2 = 0; k2 < F::RP / 2; ++k2) {
+                                    const double2 v2 = *reinterpret_cast<const double2*>(tr + x * F::RP + 2 * k2);
+                                    tv[2 * k2] = v2.x;
+                                    tv[2 * k2 + 1] = v2.y;
+                                }
+#pragma unroll
+                                for (int k = 0; k < P; ++k) acc[t + k] += gv * tv[k];
                             }
                         }
-                        double* out = S1 + (prr * F::NA + xa) * W;
+                        double* out = S1w + (prr * F::NA + xa) * W;
 #pragma unroll
                         for (int q2 = 0; q2 < W; ++q2) out[q2] = acc[q2];
                     } else if (prr == NPAIR && xa < F::NA) {   // load: SL1 = sum_xb L phiB
@@ -402,76 +440,110 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                         double acc = 0.0;
 #pragma unroll
                         for (int x = 0; x < F::NB; ++x) acc += gcol[x * F::NAP] * phiB[x];
-                        SL1[xa] = acc;
+                        SL1[(j & 1) * F::NA + xa] = acc;
                     }
                 }
-                if (zrow >= 0) {   // the row flushed last interval: its slot is not in use now
-                    double* accz = Acc + ((zrow % F::RING) * W) * F::WAB;
-                    for (int it = tid; it < W * F::WAB; it += S1T) accz[it] = 0.0;
-                    if (tid == 0) AccL[zrow % F::RING] = 0.0;
-                }
-            } else if (j > 0) {   // ---- stage 3 (plane j-1): rank-1 updates ----
-                const int jp = j - 1, ep = e_first + jp / Q, gp = jp % Q;
-                const double* Bp = Bs + (ep & 1) * 2 * Q * P;
-                const int t3 = tid - S1T;
-                for (int it = t3; it < P * F::WAB; it += S3T) {
-                    const int sab = it % F::WAB, al = it / F::WAB;
-                    const int i = ep + al;
-                    if (i < r0 || i >= r1) continue;
-                    const double va = Bp[gp * P + al], da = Bp[Q * P + gp * P + al];
-                    const double s0 = F::SPLIT ? S2[sab] + S2[4 * F::WAB + sab] : S2[sab];
-                    const double s1 = S2[F::WAB + sab], s2v = S2[2 * F::WAB + sab], s3 = S2[3 * F::WAB + sab];
-                    const double c0 = va * s0 + da * s2v, c1 = va * s1 + da * s3;
-                    double* acc = Acc + ((i % F::RING) * W) * F::WAB + sab;
+            } else if (inG2) {
+                if (j >= 1 && j <= nplanes) {   // ---- stage 2 (plane j-1): contract tile axis a ----
+                    const int b2 = (j - 1) & 1;
+                    const double* S1r = S1 + b2 * F::nS1;
+                    double* S2w = S2 + b2 * F::NI2;
+                    if (s2_load) {   // load: SL2 = sum_xa SL1 phiA
+                        const double* sl = SL1 + b2 * F::NA;
+                        double acc = 0.0;
 #pragma unroll
-                    for (int bl = 0; bl < P; ++bl) {
-                        const double vb = Bp[gp * P + bl], db = Bp[Q * P + gp * P + bl];
-                        acc[(bl - al + p) * F::WAB] += vb * c0 + db * c1;
-                    }
-                }
-                if (t3 < P) {
-                    const int i = ep + t3;
-                    if (i >= r0 && i < r1) AccL[i % F::RING] += Bp[gp * P + t3] * S2[LOAD2];
-                }
-            }
-            __syncthreads();   // B2
-            zrow = -1;
-            if (has && i2_on) {   // ---- stage 2 (plane j): contract tile axis a ----
-                if (i2_load) {
-                    double acc = 0.0;
+                        for (int x = 0; x < F::NA; ++x) acc += sl[x] * phiA[x];
+                        S2w[F::NI2 - 1] = acc;
+                    } else if (s2_on) {
+                        // S2[slot][s_a][s_b] = sum_pairs sum_xa S1[pair][xa][s_b] Ta[xa][s_a - t(xa)]
+                        double acc[W];
 #pragma unroll
-                    for (int x = 0; x < F::NA; ++x) acc += SL1[x] * phiA[x];
-                    S2[LOAD2] = acc;
-                } else {
-                    double acc0 = 0.0, acc1 = 0.0;
+                        for (int q2 = 0; q2 < W; ++q2) acc[q2] = 0.0;
 #pragma unroll
-                    for (int prr = 0; prr < NPAIR; ++prr) {
-                        if (!((i2_mask >> prr) & 1)) continue;
-                        const double* sp = S1 + prr * F::NA * W + i2_sb;
-                        const double* tp0 = Ta + tap[prr] * F::NA * P + i2_sa;
+                        for (int u = 0; u < 2; ++u) {
+                            if (s2_sp[u] < 0) continue;
+                            const double* sp = S1r + s2_sp[u];
+                            const double* ta = Ta + s2_ta[u];
 #pragma unroll
-                        for (int t = 0; t < P; ++t) {
-                            if (t < i2_tl || t > i2_th) continue;
+                            for (int t = 0; t < P; ++t) {
+                                if (t < ta_lo || t >= ta_hi) continue;
 #pragma unroll
-                            for (int g2 = 0; g2 < Q; ++g2) {
-                                const int xa = t * Q + g2;
-                                const double v = sp[xa * W] * tp0[xa * P - t];
-                                if (g2 & 1) acc1 += v; else acc0 += v;
+                                for (int g2 = 0; g2 < Q; ++g2) {
+                                    const int xa = t * Q + g2;
+                                    const double v = sp[xa * W];
+                                    double tv[F::RP];
+#pragma unroll
+                                    for (int k2 = 0; k2 < F::RP / 2; ++k2) {
+                                        const double2 v2 =
+                                            *reinterpret_cast<const double2*>(ta + xa * F::RP + 2 * k2);
+                                        tv[2 * k2] = v2.x;
+                                        tv[2 * k2 + 1] = v2.y;
+                                    }
+#pragma unroll
+                                    for (int k = 0; k < P; ++k) acc[t + k] += v * tv[k];
+                                }
                             }
                         }
+                        double* o2 = S2w + s2_slot * F::WAB + s2_sb;
+#pragma unroll
+                        for (int sa = 0; sa < W; ++sa) o2[sa * F::WB] = acc[sa];
                     }
-                    S2[i2_it] = acc0 + acc1;
+                }
+            } else {
+                if (j < nplanes && j > 0 && j % Q == 0) load_bs(e_first + j / Q);
+                if (j >= 2) {   // ---- stage 3 (plane j-2): rank-1 updates ----
+                    const int jp = j - 2, ep = e_first + jp / Q, gp = jp % Q;
+                    const double* Bp = Bs + (ep & 1) * 2 * Q * P;
+                    const double* S2r = S2 + (jp & 1) * F::NI2;
+                    for (int it = g3t; it < F::NI3; it += S3T) {
+                        const int sab = it % F::WAB, al = it / F::WAB;
+                        const int i = ep + al;
+                        if (i < r0 || i >= r1) continue;
+                        const double va = Bp[gp * P + al], da = Bp[Q * P + gp * P + al];
+                        const double s0 = S2r[sab] + S2r[4 * F::WAB + sab];
+                        const double s1 = S2r[F::WAB + sab], s2v = S2r[2 * F::WAB + sab], s3 = S2r[3 * F::WAB + sab];
+                        const double c0 = va * s0 + da * s2v, c1 = va * s1 + da * s3;
+                        double* acc = Acc + ((i % F::RING) * W) * F::WAB + sab;
+#pragma unroll
+                        for (int bl = 0; bl < P; ++bl) {
+                            const double vb = Bp[gp * P + bl], db = Bp[Q * P + gp * P + bl];
+                            acc[(bl - al + p) * F::WAB] += vb * c0 + db * c1;
+                        }
+                    }
+                    if (g3t < P) {
+                        const int i = ep + g3t;
+                        if (i >= r0 && i < r1) AccL[i % F::RING] += Bp[gp * P + g3t] * S2r[F::NI2 - 1];
+                    }
+                    if (gp == Q - 1) {   // element ep complete
+                        bar3();
+                        if (ep < e_last) {
+                            if (ep >= r0 && ep < r1) {
+                                flush3(ep);
+                                bar3();
+                                double* accz = Acc + ((ep % F::RING) * W) * F::WAB;
+                                for (int it = g3t; it < W * F::WAB; it += S3T) accz[it] = 0.0;
+                                if (g3t == 0) AccL[ep % F::RING] = 0.0;
+                            }
+                        } else {
+                            for (int i = (ep > r0 ? ep : r0); i < r1; ++i) flush3(i);
+                        }
+                    }
                 }
             }
-            if (j > 0 && (j - 1) % Q == Q - 1) {   // element e(j-1) complete
-                const int ep = e_first + (j - 1) / Q;
-                if (ep < e_last) {
-                    if (ep >= r0 && ep < r1) { flush_row(ep); zrow = ep; }
-                } else {
-                    for (int i = (ep > r0 ? ep : r0); i < r1; ++i) flush_row(i);
-                }
+            if (prf) pw += clk64() - p0;
+            if constexpr (!F::TMA) cp_async_wait_all();
+            __syncthreads();
+            if (prf) {
+                const long long t1 = clk64();
+                pt += t1 - p0;
+                p0 = t1;
             }
-            buf ^= 1;
+        }
+        if (prf) {
+            const int g = inG1 ? 0 : (inG2 ? 1 : 2);
+            prof[2 * g] = pw;
+            prof[2 * g + 1] = pt;
+            if (g == 0) prof[6] = nplanes + 2;
         }
     } else {
     const bool pr = prof != nullptr && blockIdx.x == 0 && tid == 0;   // phase profile
@@ -507,7 +579,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 #pragma unroll
                     for (int j = 0; j < W; ++j) acc[j] = 0.0;
                     const double* gcol = Gw + gidx * F::NB * F::NAP + xa;
-                    const double* tr = Tb + tb * F::NB * P;
+                    const double* tr = Tb + tb * F::NB * F::RP;
 #pragma unroll
                     for (int t = 0; t < P; ++t) {
                         if (t < tb_lo || t >= tb_hi) continue;
@@ -516,7 +588,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                             const int x = t * Q + g2;
                             const double gv = gcol[x * F::NAP];
 #pragma unroll
-                            for (int k = 0; k < P; ++k) acc[t + k] += gv * tr[x * P + k];
+                            for (int k = 0; k < P; ++k) acc[t + k] += gv * tr[x * F::RP + k];
                         }
                     }
                     double* out = S1 + (pr * F::NA + xa) * W;
@@ -554,14 +626,14 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                             const double* sp = D == 3 ? S1 + prr * F::NA * W + i2_sb
                                                       : Gw + sym_index(D, prr / D, prr % D) * F::NAP;
                             const int sstr = D == 3 ? W : 1;
-                            const double* tp0 = Ta + tap[prr] * F::NA * P + i2_sa;
+                            const double* tp0 = Ta + tap[prr] * F::NA * F::RP + i2_sa;
 #pragma unroll
                             for (int t = 0; t < P; ++t) {
                                 if (t < i2_tl || t > i2_th) continue;
 #pragma unroll
                                 for (int g2 = 0; g2 < Q; ++g2) {
                                     const int xa = t * Q + g2;
-                                    const double v = sp[xa * sstr] * tp0[xa * P - t];
+                                    const double v = sp[xa * sstr] * tp0[xa * F::RP - t];
                                     if (g2 & 1) acc1 += v; else acc0 += v;
                                 }
                             }
@@ -732,8 +804,14 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(nthreads), args, smem, h->stream);
     if (prof) {
         long long t[8];
+        cudaStreamSynchronize(h->stream);
         cudaMemcpy(t, prof, sizeof t, cudaMemcpyDeviceToHost);
         const double n = t[6] > 0 ? (double)t[6] : 1.0;
+        if (h->d == 3)
+            fprintf(stderr, "asm-profile block0 intervals=%lld cycles/interval: G1 work=%.0f total=%.0f | G2 work=%.0f"
+                    " total=%.0f | G3 work=%.0f total=%.0f\n", t[6], t[0] / n, t[1] / n, t[2] / n, t[3] / n, t[4] / n,
+                    t[5] / n);
+        else
         fprintf(stderr, "asm-profile block0 planes=%lld elements=%lld cycles/plane: load-wait=%.0f stage1=%.0f "
                 "stage2a=%.0f stage2b=%.0f stage3=%.0f ; flush/element=%.0f\n", t[6], t[7], t[0] / n, t[1] / n,
                 t[2] / n, t[3] / n, t[4] / n, t[5] / (t[7] > 0 ? (double)t[7] : 1.0));
