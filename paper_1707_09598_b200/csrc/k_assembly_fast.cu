@@ -89,12 +89,11 @@ struct FastCfg {
     static constexpr bool SPLIT = D == 3;
     static constexpr int NT2 = SPLIT ? 5 : 4;
     static constexpr int NI2 = NT2 * WAB + 1;          // stage-2 items (+ load)
-    static constexpr int NI3 = P * WAB;                // stage-3 items
     static constexpr int S2T = PIPE ? 32 * ((NT2 * WB + 1 + 31) / 32) : 0;   // one (slot, s_b) column each
-    static constexpr int S3T = PIPE ? 32 * ((NI3 + 63) / 64) : 0;
+    static constexpr int S3T = PIPE ? 32 * ((WAB + P + 31) / 32) : 0;         // one (s_a, s_b) column / load row each
     static constexpr int NT = PIPE ? S1T + S2T + S3T : 352;
     // resident CTAs per SM (launch bounds)
-    static constexpr int MINB = PIPE ? (NT > 512 ? 1 : (NT > 352 ? 2 : 3)) : 2;
+    static constexpr int MINB = PIPE && P >= 5 ? 1 : 2;
     static constexpr int NBUF = PIPE ? 2 : 1;          // S1 / SL1 / S2 buffers
     // plane windows by one TMA tensor copy per plane (TM: the component's
     // 4-D tensor map exists -- every global stride a multiple of 16 bytes);
@@ -378,6 +377,11 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 dinv[C.vec_off + row] = 1.0 / accr[p * F::WAB + p * F::WB + p];
             }
         };
+        double R3[P][P], RL3 = 0.0;   // G3: the current element's sums (registers)
+#pragma unroll
+        for (int al = 0; al < P; ++al)
+#pragma unroll
+            for (int bl = 0; bl < P; ++bl) R3[al][bl] = 0.0;
         auto bar3 = [&]() { asm volatile("bar.sync 1, %0;\n" ::"r"(S3T) : "memory"); };
         if (nplanes > 0) {
             if (inG3) load_bs(e_first);
@@ -492,29 +496,49 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             } else {
                 if (j < nplanes && j > 0 && j % Q == 0) load_bs(e_first + j / Q);
                 if (j >= 2) {   // ---- stage 3 (plane j-2): rank-1 updates ----
+                    // thread (s_a, s_b) keeps the P x P (row al, column bl) sums
+                    // of the current stream element in registers and folds them
+                    // into the shared ring once per element
                     const int jp = j - 2, ep = e_first + jp / Q, gp = jp % Q;
-                    const double* Bp = Bs + (ep & 1) * 2 * Q * P;
+                    const double* Bp = Bs + (ep & 1) * 2 * Q * P + gp * P;   // values; derivatives at +Q*P
                     const double* S2r = S2 + (jp & 1) * F::NI2;
-                    for (int it = g3t; it < F::NI3; it += S3T) {
-                        const int sab = it % F::WAB, al = it / F::WAB;
-                        const int i = ep + al;
-                        if (i < r0 || i >= r1) continue;
-                        const double va = Bp[gp * P + al], da = Bp[Q * P + gp * P + al];
+                    if (g3t < F::WAB) {
+                        const int sab = g3t;
                         const double s0 = S2r[sab] + S2r[4 * F::WAB + sab];
                         const double s1 = S2r[F::WAB + sab], s2v = S2r[2 * F::WAB + sab], s3 = S2r[3 * F::WAB + sab];
-                        const double c0 = va * s0 + da * s2v, c1 = va * s1 + da * s3;
-                        double* acc = Acc + ((i % F::RING) * W) * F::WAB + sab;
+                        double vb[P], db[P];
 #pragma unroll
                         for (int bl = 0; bl < P; ++bl) {
-                            const double vb = Bp[gp * P + bl], db = Bp[Q * P + gp * P + bl];
-                            acc[(bl - al + p) * F::WAB] += vb * c0 + db * c1;
+                            vb[bl] = Bp[bl];
+                            db[bl] = Bp[Q * P + bl];
                         }
-                    }
-                    if (g3t < P) {
-                        const int i = ep + g3t;
-                        if (i >= r0 && i < r1) AccL[i % F::RING] += Bp[gp * P + g3t] * S2r[F::NI2 - 1];
+#pragma unroll
+                        for (int al = 0; al < P; ++al) {
+                            const double c0 = vb[al] * s0 + db[al] * s2v, c1 = vb[al] * s1 + db[al] * s3;
+#pragma unroll
+                            for (int bl = 0; bl < P; ++bl) R3[al][bl] += vb[bl] * c0 + db[bl] * c1;
+                        }
+                    } else if (g3t < F::WAB + P) {
+                        RL3 += Bp[g3t - F::WAB] * S2r[F::NI2 - 1];
                     }
                     if (gp == Q - 1) {   // element ep complete
+                        if (g3t < F::WAB) {
+#pragma unroll
+                            for (int al = 0; al < P; ++al) {
+                                const int i = ep + al;
+                                if (i >= r0 && i < r1) {
+                                    double* acc = Acc + ((i % F::RING) * W) * F::WAB + g3t;
+#pragma unroll
+                                    for (int bl = 0; bl < P; ++bl) acc[(bl - al + p) * F::WAB] += R3[al][bl];
+                                }
+#pragma unroll
+                                for (int bl = 0; bl < P; ++bl) R3[al][bl] = 0.0;
+                            }
+                        } else if (g3t < F::WAB + P) {
+                            const int i = ep + g3t - F::WAB;
+                            if (i >= r0 && i < r1) AccL[i % F::RING] += RL3;
+                            RL3 = 0.0;
+                        }
                         bar3();
                         if (ep < e_last) {
                             if (ep >= r0 && ep < r1) {
