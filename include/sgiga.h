@@ -165,6 +165,15 @@ int sgiga_run(sgiga_handle* h, double rtol, int32_t maxit, const double* pts,
               int64_t npts, double* out, int32_t device, int32_t* iters_out,
               double* relres_out);
 
+/* Asynchronous form of sgiga_run with device-resident points / output:
+ * sgiga_run_async enqueues the whole pass on the handle's stream and
+ * returns without synchronising (back-to-back passes pipeline on the
+ * device); sgiga_run_wait synchronises and reports the LAST enqueued pass
+ * exactly as sgiga_run does (status, iterations, relative residuals).     */
+int sgiga_run_async(sgiga_handle* h, double rtol, int32_t maxit, const double* pts_dev,
+                    int64_t npts, double* out_dev);
+int sgiga_run_wait(sgiga_handle* h, int32_t* iters_out, double* relres_out);
+
 /* Tensor grid variant: per-axis parameter arrays concatenated; vals has
  * prod(npts) entries (C order), grads (optional, may be NULL) prod*d.
  * comp = -1 combines the plan; comp >= 0 evaluates that component alone

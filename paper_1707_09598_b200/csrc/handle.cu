@@ -54,6 +54,9 @@ static void free_all(Handle* h) {
     if (h->fd_fork) cudaEventDestroy(h->fd_fork);
     if (h->fd_join) cudaEventDestroy(h->fd_join);
     if (h->stream2) cudaStreamDestroy(h->stream2);
+    if (h->cs_fork) cudaEventDestroy(h->cs_fork);
+    if (h->cs_join) cudaEventDestroy(h->cs_join);
+    if (h->stream3) cudaStreamDestroy(h->stream3);
     if (h->run_exec) cudaGraphExecDestroy(h->run_exec);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
 }
@@ -529,6 +532,9 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     if (ea == cudaSuccess) ea = cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_fork, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_join, cudaEventDisableTiming);
+    if (ea == cudaSuccess) ea = cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking);
+    if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->cs_fork, cudaEventDisableTiming);
+    if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->cs_join, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned_flag), sizeof(int) * 4);
     // mapped pinned mirrors: the status kernel writes them directly (no copy nodes)
     if (ea == cudaSuccess) ea = cudaHostAlloc(reinterpret_cast<void**>(&h->h_err), sizeof(int), cudaHostAllocMapped);
@@ -775,6 +781,10 @@ static int stage_points(Handle* h, const double* pts, int64_t npts, size_t nout,
 static int combine_enqueue(Handle* h, const double* dp, int64_t npts, double* dout, int per_comp) {
     h->launches[2] = 0;
     h->pmark(4);
+    if (h->cs_pending) {   // the point sort ran on the side stream
+        SG_CUDA(cudaStreamWaitEvent(h->stream, h->cs_join, 0));
+        h->cs_pending = false;
+    }
     h->kstart(6);
     SG_CUDA(launch_combine_points(h, dp, npts, dout, per_comp));
     h->kstop(6);
@@ -817,20 +827,32 @@ static bool run_graphs_enabled() {
     return true;
 }
 
-int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, int64_t npts,
-              double* out, int32_t device, int32_t* iters_out, double* relres_out) {
-    Handle* h = reinterpret_cast<Handle*>(hh);
-    if (!h || npts < 0 || (npts > 0 && (!pts || !out))) { set_error("null argument"); return SGIGA_ERR_VALUE; }
-    if (device < 0) { set_error("sgiga_run: per-component output is not supported"); return SGIGA_ERR_VALUE; }
-    const double* dp = pts;
-    double* dout = out;
+// enqueue of one whole pass (device pointers): direct launches, capture, or
+// replay of the pass graph; no synchronisation
+static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, int64_t npts, double* dout) {
     int st;
-    if (npts > 0 && device == 0 && (st = stage_points(h, pts, npts, (size_t)npts, &dp, &dout))) return st;
     auto enqueue_all = [&]() -> int {
+        // the combine's point sort depends on the points only: side stream,
+        // overlapping assembly and solve
+        h->cs_ready = h->cs_pending = false;
+        if (npts > 0) {
+            bool sorted = false;
+            SG_CUDA(cudaEventRecord(h->cs_fork, h->stream));
+            SG_CUDA(cudaStreamWaitEvent(h->stream3, h->cs_fork, 0));
+            SG_CUDA(launch_combine_sort(h, dp, npts, h->stream3, &sorted));
+            SG_CUDA(cudaEventRecord(h->cs_join, h->stream3));
+            h->cs_pending = true;
+            h->cs_ready = sorted;
+        }
         int s2 = assemble_enqueue(h);
         if (!s2) s2 = solve_enqueue(h, rtol, maxit);
         if (!s2 && npts > 0) s2 = combine_enqueue(h, dp, npts, dout, 0);
         if (!s2 && launch_status(h) != cudaSuccess) s2 = SGIGA_ERR_CUDA;
+        h->cs_ready = false;
+        if (h->cs_pending) {   // not consumed (an earlier step failed): still join the side stream
+            cudaStreamWaitEvent(h->stream, h->cs_join, 0);
+            h->cs_pending = false;
+        }
         return s2;
     };
     // whole-run graph: only when the solve has no host-driven loop (every
@@ -876,16 +898,48 @@ int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, i
             h->rkey.npts = npts; h->rkey.warm = 1;
         }
     }
-    if (npts > 0 && device == 0)
-        SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * npts, cudaMemcpyDeviceToHost, h->stream));
-    SG_CUDA(cudaStreamSynchronize(h->stream));   // the one synchronisation of the call
-    st = decode_err(h);
+    h->run_npts = npts;
+    return SGIGA_OK;
+}
+
+// the one synchronisation of a pass and its verdict
+static int run_finish(Handle* h, int32_t* iters_out, double* relres_out) {
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    int st = decode_err(h);
     if (st) return st;
     SG_CUDA(h->elapsed(&h->ms[0], Handle::PHASE_EV + 0, Handle::PHASE_EV + 1));
     h->assembled = true;
     st = solve_finish(h, iters_out, relres_out);
-    if (npts > 0) SG_CUDA(h->elapsed(&h->ms[2], Handle::PHASE_EV + 4, Handle::PHASE_EV + 5));
+    if (h->run_npts > 0) SG_CUDA(h->elapsed(&h->ms[2], Handle::PHASE_EV + 4, Handle::PHASE_EV + 5));
     return st;
+}
+
+int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, int64_t npts,
+              double* out, int32_t device, int32_t* iters_out, double* relres_out) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || npts < 0 || (npts > 0 && (!pts || !out))) { set_error("null argument"); return SGIGA_ERR_VALUE; }
+    if (device < 0) { set_error("sgiga_run: per-component output is not supported"); return SGIGA_ERR_VALUE; }
+    const double* dp = pts;
+    double* dout = out;
+    int st;
+    if (npts > 0 && device == 0 && (st = stage_points(h, pts, npts, (size_t)npts, &dp, &dout))) return st;
+    if ((st = run_enqueue(h, rtol, maxit, dp, npts, dout))) return st;
+    if (npts > 0 && device == 0)
+        SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * npts, cudaMemcpyDeviceToHost, h->stream));
+    return run_finish(h, iters_out, relres_out);
+}
+
+int sgiga_run_async(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts_dev, int64_t npts,
+                    double* out_dev) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || npts < 0 || (npts > 0 && (!pts_dev || !out_dev))) { set_error("null argument"); return SGIGA_ERR_VALUE; }
+    return run_enqueue(h, rtol, maxit, pts_dev, npts, out_dev);
+}
+
+int sgiga_run_wait(sgiga_handle* hh, int32_t* iters_out, double* relres_out) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h) return SGIGA_ERR_VALUE;
+    return run_finish(h, iters_out, relres_out);
 }
 
 int sgiga_iterations(sgiga_handle* hh, int32_t* iters) {

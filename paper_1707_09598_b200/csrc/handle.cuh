@@ -115,6 +115,12 @@ struct Handle {
     cudaStream_t stream2 = nullptr;          // side stream: the eigen kernel overlaps assembly
     cudaEvent_t fd_fork = nullptr, fd_join = nullptr;
     bool fd_pending = false;                 // fd_join not yet waited on by the main stream
+    // combine point sort on its own side stream (sgiga_run: forked before the
+    // assembly, joined before the combine kernel)
+    cudaStream_t stream3 = nullptr;
+    cudaEvent_t cs_fork = nullptr, cs_join = nullptr;
+    bool cs_pending = false, cs_ready = false;
+    int64_t run_npts = 0;          // points of the last enqueued sgiga_run pass
     int* d_cperm = nullptr;        // combine: cell-order permutation of the points
     size_t cperm_cap = 0;
     int* d_chist = nullptr;        // combine: cell histogram / cursors

@@ -88,8 +88,10 @@ struct FastCfg {
     // in two halves, + the load term
     static constexpr bool SPLIT = D == 3;
     static constexpr int NT2 = SPLIT ? 5 : 4;
-    static constexpr int NI2 = NT2 * WAB + 1;          // stage-2 items (+ load)
-    static constexpr int S2T = PIPE ? 32 * ((NT2 * WB + 1 + 31) / 32) : 0;   // one (slot, s_b) column each
+    // stage-2 outputs: 3-D -- one (s_a, s_b) block per pair (summed by stream
+    // type in stage 3) + the load term; 2-D -- NT2 slots + load
+    static constexpr int NI2 = (PIPE ? NPAIR : NT2) * WAB + 1;
+    static constexpr int S2T = PIPE ? 32 * ((NPAIR * WB + 1 + 31) / 32) : 0;   // one (pair, s_b) column each
     static constexpr int S3T = PIPE ? 32 * ((WAB + P + 31) / 32) : 0;         // one (s_a, s_b) column / load row each
     static constexpr int NT = PIPE ? S1T + S2T + S3T : 352;
     // resident CTAs per SM (launch bounds)
@@ -105,8 +107,12 @@ struct FastCfg {
     static constexpr int sGw = (nGw + 15) & ~15;       // buffer stride (128-byte aligned TMA destination)
     static constexpr int nS1 = NPAIR * NA * WB;
     // shared-memory layout (doubles)
-    static constexpr int oGw = 0;                      // [2][NG][NB][NAP]
-    static constexpr int oTa = oGw + 2 * sGw;          // [4][NA][RP]
+    static constexpr int oGw = 0;                      // [NGB][NG][NB][NAP]
+    // plane buffers: TMA -- prefetch distance GPD = 2 planes (three buffers,
+    // the next two planes in flight while one is contracted); cp.async -- 1
+    static constexpr int GPD = TMA ? 2 : 1;
+    static constexpr int NGB = GPD + 1;
+    static constexpr int oTa = oGw + NGB * sGw;        // [4][NA][RP]
     static constexpr int oTb = oTa + 4 * NA * RP;      // [4][NB][RP]
     static constexpr int oPhiA = oTb + 4 * NB * RP;    // [NA]
     static constexpr int oPhiB = oPhiA + NA;           // [NB]
@@ -128,7 +134,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 const Pencil* __restrict__ pencils, const double* __restrict__ vals,
                 const double* __restrict__ Gbuf, double* __restrict__ stencil,
                 double* __restrict__ rhs, double* __restrict__ dinv, long long* __restrict__ prof,
-                const CUtensorMap* __restrict__ tmaps) {
+                const CUtensorMap* __restrict__ tmaps, int dbg) {
     using F = FastCfg<D, P, Q, TM>;
     constexpr int NT = F::NT;
     constexpr int p = F::p, W = F::W;
@@ -182,11 +188,12 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     else if (tid == 0) { Tb[0] = 1.0; Tb[1] = Tb[2] = Tb[3] = 0.0; phiB[0] = 1.0; }
     for (int idx = tid; idx < F::RING * W * F::WAB + F::RING; idx += NT) Acc[idx] = 0.0;
     // invalid window points stay zero in both plane buffers
-    for (int idx = tid; idx < 2 * F::sGw; idx += NT) sm[F::oGw + idx] = 0.0;
-    __shared__ __align__(8) uint64_t fast_mbar[2];   // TMA variant: one barrier per plane buffer
+    for (int idx = tid; idx < F::NGB * F::sGw; idx += NT) sm[F::oGw + idx] = 0.0;
+    __shared__ __align__(8) uint64_t fast_mbar[3];   // TMA variant: one barrier per plane buffer
     if (F::TMA && tid == 0) {
         mbar_init(&fast_mbar[0], 1);
         mbar_init(&fast_mbar[1], 1);
+        mbar_init(&fast_mbar[2], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
@@ -333,26 +340,21 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         const bool inG1 = tid < S1T, inG2 = !inG1 && tid < S1T + S2T, inG3 = tid >= S1T + S2T;
         const int g2t = tid - S1T, g3t = tid - S1T - S2T;
         const int nplanes = (e_last - e_first + 1) * Q;
-        // this G2 thread's stage-2 column: (slot, s_b) -> all s_a, summed over
-        // the (at most two) pairs of the slot; decoded once per pencil
-        const bool s2_on = inG2 && g2t < F::NT2 * F::WB + 1, s2_load = g2t == F::NT2 * F::WB;
-        const int s2_slot = g2t / F::WB, s2_sb = g2t % F::WB;
-        int s2_sp[2] = {-1, -1}, s2_ta[2] = {0, 0};   // S1 / Ta offsets of the slot's pairs
-        {
-            const int ts = s2_slot == 4 ? 0 : s2_slot;
-            int c0 = 0, n = 0;
+        // this G2 thread's stage-2 column: (pair, s_b) -> all s_a
+        const bool s2_on = inG2 && g2t < NPAIR * F::WB + 1, s2_load = g2t == NPAIR * F::WB;
+        const int s2_pr = g2t / F::WB, s2_sb = g2t % F::WB;
+        int s2_sp = 0, s2_ta = 0;   // S1 / Ta offsets of the pair
 #pragma unroll
-            for (int pr = 0; pr < NPAIR; ++pr) {
-                if (tsp[pr] != ts) continue;
-                const bool take = ts != 0 || ((s2_slot == 4) == (c0 >= 2));
-                if (ts == 0) ++c0;
-                if (take && n < 2) {
-                    s2_sp[n] = pr * F::NA * W + s2_sb;
-                    s2_ta[n] = tap[pr] * F::NA * F::RP;
-                    ++n;
-                }
+        for (int pr = 0; pr < NPAIR; ++pr)
+            if (pr == s2_pr) {
+                s2_sp = pr * F::NA * W + s2_sb;
+                s2_ta = tap[pr] * F::NA * F::RP;
             }
-        }
+        // stage 3 sums the pair blocks of each stream type (fixed pair order):
+        // type 0 = pairs without s, 1 = (m, s), 2 = (s, n), 3 = (s, s)
+        const int ty_off[9] = {(ka * D + ka) * F::WAB, (ka * D + kb) * F::WAB, (kb * D + ka) * F::WAB,
+                               (kb * D + kb) * F::WAB, (ka * D + s) * F::WAB,  (kb * D + s) * F::WAB,
+                               (s * D + ka) * F::WAB,  (s * D + kb) * F::WAB,  (s * D + s) * F::WAB};
         auto load_bs = [&](int e) {   // G3: stream basis values/derivatives of element e
             double* Bd = Bs + (e & 1) * 2 * Q * P;
             for (int idx = g3t; idx < 2 * Q * P; idx += S3T) {
@@ -387,6 +389,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             if (inG3) load_bs(e_first);
             if constexpr (F::TMA) {
                 load_plane_tma((int64_t)e_first * Q, 0);
+                if (nplanes > 1) load_plane_tma((int64_t)e_first * Q + 1, 1);
             } else {
                 load_plane((int64_t)e_first * Q, 0);
                 cp_async_wait_all();
@@ -398,17 +401,17 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         const bool prf = prof != nullptr && blockIdx.x == 0 && (tid == 0 || tid == S1T || tid == S1T + S2T);
         long long pw = 0, pt = 0, p0 = prf ? clk64() : 0;
         for (int j = 0; nplanes > 0 && j < nplanes + 2; ++j) {
-            if (j + 1 < nplanes) {
-                if constexpr (F::TMA) load_plane_tma((int64_t)e_first * Q + j + 1, (j + 1) & 1);
-                else load_plane((int64_t)e_first * Q + j + 1, (j + 1) & 1);
+            if (j + F::GPD < nplanes) {
+                if constexpr (F::TMA) load_plane_tma((int64_t)e_first * Q + j + F::GPD, (j + F::GPD) % F::NGB);
+                else load_plane((int64_t)e_first * Q + j + 1, (j + 1) % F::NGB);
             }
             if (inG1) {
                 if (j < nplanes) {   // ---- stage 1 (plane j): contract tile axis b ----
-                    if constexpr (F::TMA) wait_plane_tma(j & 1);
-                    const double* Gw = sm + F::oGw + (j & 1) * F::sGw + tsh;
+                    if constexpr (F::TMA) wait_plane_tma(j % F::NGB);
+                    const double* Gw = sm + F::oGw + (j % F::NGB) * F::sGw + tsh;
                     double* S1w = S1 + (j & 1) * F::nS1;
                     const int half = F::PPW == 2 ? (lane >> 4) : 0;
-                    const int xa = F::PPW == 2 ? (lane & 15) : lane;
+                    const int xa = (dbg & 1) ? 32 : (F::PPW == 2 ? (lane & 15) : lane);
                     const int prr = warp * F::PPW + half;
                     if (prr < NPAIR && xa < F::NA) {
                         const int gidx = sym_index(D, prr / D, prr % D);
@@ -448,7 +451,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     }
                 }
             } else if (inG2) {
-                if (j >= 1 && j <= nplanes) {   // ---- stage 2 (plane j-1): contract tile axis a ----
+                if (j >= 1 && j <= nplanes && !(dbg & 2)) {   // ---- stage 2 (plane j-1): contract tile axis a ----
                     const int b2 = (j - 1) & 1;
                     const double* S1r = S1 + b2 * F::nS1;
                     double* S2w = S2 + b2 * F::NI2;
@@ -459,43 +462,42 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                         for (int x = 0; x < F::NA; ++x) acc += sl[x] * phiA[x];
                         S2w[F::NI2 - 1] = acc;
                     } else if (s2_on) {
-                        // S2[slot][s_a][s_b] = sum_pairs sum_xa S1[pair][xa][s_b] Ta[xa][s_a - t(xa)]
-                        double acc[W];
+                        // S2[pair][s_a][s_b] = sum_xa S1[pair][xa][s_b] Ta[xa][s_a - t(xa)];
+                        // even / odd points in two accumulator sets (shorter chains)
+                        double acc[W], acd[W];
 #pragma unroll
-                        for (int q2 = 0; q2 < W; ++q2) acc[q2] = 0.0;
+                        for (int q2 = 0; q2 < W; ++q2) acc[q2] = acd[q2] = 0.0;
+                        const double* sp = S1r + s2_sp;
+                        const double* ta = Ta + s2_ta;
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            if (s2_sp[u] < 0) continue;
-                            const double* sp = S1r + s2_sp[u];
-                            const double* ta = Ta + s2_ta[u];
+                        for (int t = 0; t < P; ++t) {
+                            if (t < ta_lo || t >= ta_hi) continue;
 #pragma unroll
-                            for (int t = 0; t < P; ++t) {
-                                if (t < ta_lo || t >= ta_hi) continue;
+                            for (int g2 = 0; g2 < Q; ++g2) {
+                                const int xa = t * Q + g2;
+                                const double v = sp[xa * W];
+                                double tv[F::RP];
 #pragma unroll
-                                for (int g2 = 0; g2 < Q; ++g2) {
-                                    const int xa = t * Q + g2;
-                                    const double v = sp[xa * W];
-                                    double tv[F::RP];
+                                for (int k2 = 0; k2 < F::RP / 2; ++k2) {
+                                    const double2 v2 = *reinterpret_cast<const double2*>(ta + xa * F::RP + 2 * k2);
+                                    tv[2 * k2] = v2.x;
+                                    tv[2 * k2 + 1] = v2.y;
+                                }
 #pragma unroll
-                                    for (int k2 = 0; k2 < F::RP / 2; ++k2) {
-                                        const double2 v2 =
-                                            *reinterpret_cast<const double2*>(ta + xa * F::RP + 2 * k2);
-                                        tv[2 * k2] = v2.x;
-                                        tv[2 * k2 + 1] = v2.y;
-                                    }
-#pragma unroll
-                                    for (int k = 0; k < P; ++k) acc[t + k] += v * tv[k];
+                                for (int k = 0; k < P; ++k) {
+                                    if (xa & 1) acd[t + k] += v * tv[k];
+                                    else acc[t + k] += v * tv[k];
                                 }
                             }
                         }
-                        double* o2 = S2w + s2_slot * F::WAB + s2_sb;
+                        double* o2 = S2w + s2_pr * F::WAB + s2_sb;
 #pragma unroll
-                        for (int sa = 0; sa < W; ++sa) o2[sa * F::WB] = acc[sa];
+                        for (int sa = 0; sa < W; ++sa) o2[sa * F::WB] = acc[sa] + acd[sa];
                     }
                 }
             } else {
-                if (j < nplanes && j > 0 && j % Q == 0) load_bs(e_first + j / Q);
-                if (j >= 2) {   // ---- stage 3 (plane j-2): rank-1 updates ----
+                if (j < nplanes && j > 0 && j % Q == 0 && !(dbg & 16)) load_bs(e_first + j / Q);
+                if (j >= 2 && !(dbg & 4)) {   // ---- stage 3 (plane j-2): rank-1 updates ----
                     // thread (s_a, s_b) keeps the P x P (row al, column bl) sums
                     // of the current stream element in registers and folds them
                     // into the shared ring once per element
@@ -504,8 +506,11 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     const double* S2r = S2 + (jp & 1) * F::NI2;
                     if (g3t < F::WAB) {
                         const int sab = g3t;
-                        const double s0 = S2r[sab] + S2r[4 * F::WAB + sab];
-                        const double s1 = S2r[F::WAB + sab], s2v = S2r[2 * F::WAB + sab], s3 = S2r[3 * F::WAB + sab];
+                        // stream types: 0 = pairs without s, 1 = (m, s), 2 = (s, n), 3 = (s, s)
+                        const double* q = S2r + sab;
+                        const double s0 = ((q[ty_off[0]] + q[ty_off[1]]) + q[ty_off[2]]) + q[ty_off[3]];
+                        const double s1 = q[ty_off[4]] + q[ty_off[5]], s2v = q[ty_off[6]] + q[ty_off[7]];
+                        const double s3 = q[ty_off[8]];
                         double vb[P], db[P];
 #pragma unroll
                         for (int bl = 0; bl < P; ++bl) {
@@ -542,7 +547,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                         bar3();
                         if (ep < e_last) {
                             if (ep >= r0 && ep < r1) {
-                                flush3(ep);
+                                if (!(dbg & 8)) flush3(ep);
                                 bar3();
                                 double* accz = Acc + ((ep % F::RING) * W) * F::WAB;
                                 for (int it = g3t; it < W * F::WAB; it += S3T) accz[it] = 0.0;
@@ -817,6 +822,10 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     *err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (*err != cudaSuccess) return true;
     long long* prof = nullptr;
+    // SGIGA_ASM_DBG (timing experiments only, wrong results): bit 0/1/2 skip
+    // stage 1/2/3 of the 3-D pipeline
+    const char* de = getenv("SGIGA_ASM_DBG");
+    int dbg = de ? atoi(de) : 0;
     const char* pe = getenv("SGIGA_ASM_PROFILE");
     if (pe && pe[0] == '1') {
         cudaMalloc(&prof, 8 * sizeof(long long));
@@ -824,7 +833,7 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     }
     void* args[] = {(void*)&h->d_comps, (void*)&h->d_tabs, (void*)&h->d_pencils, (void*)&h->d_tabvals,
                     (void*)&h->d_G, (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv,
-                    (void*)&prof, (void*)&h->d_tmaps};
+                    (void*)&prof, (void*)&h->d_tmaps, (void*)&dbg};
     *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(nthreads), args, smem, h->stream);
     if (prof) {
         long long t[8];

@@ -544,6 +544,32 @@ __global__ void k_sum_partials(const double* __restrict__ partials, int64_t nblo
     default: return cudaErrorInvalidValue;                               \
     }
 
+cudaError_t launch_combine_sort(Handle* h, const double* d_pts, int64_t npts, cudaStream_t s, bool* sorted) {
+    *sorted = false;
+    const char* ns = getenv("SGIGA_COMBINE_NOSORT");
+    if (npts < 2048 || npts >= (int64_t)1 << 31 || (ns && ns[0] == '1')) return cudaSuccess;
+    cudaError_t e;
+    if ((size_t)npts > h->cperm_cap) {
+        if (h->d_cperm) cudaFree(h->d_cperm);
+        h->d_cperm = nullptr;
+        h->cperm_cap = 0;
+        if ((e = cudaMalloc(&h->d_cperm, sizeof(int) * npts)) != cudaSuccess) return e;
+        h->cperm_cap = (size_t)npts;
+    }
+    // d_chist is zero here: zeroed at create, re-zeroed by the combine kernel
+    // after every sorted launch
+    const unsigned sb = (unsigned)((npts + 255) / 256);
+    if (h->d == 1) k_cell_hist<1><<<sb, 256, 0, s>>>(d_pts, npts, h->d_chist);
+    else if (h->d == 2) k_cell_hist<2><<<sb, 256, 0, s>>>(d_pts, npts, h->d_chist);
+    else k_cell_hist<3><<<sb, 256, 0, s>>>(d_pts, npts, h->d_chist);
+    k_cell_scan<<<1, 1024, 0, s>>>(h->d_chist);
+    if (h->d == 1) k_cell_scatter<1><<<sb, 256, 0, s>>>(d_pts, npts, h->d_chist, h->d_cperm);
+    else if (h->d == 2) k_cell_scatter<2><<<sb, 256, 0, s>>>(d_pts, npts, h->d_chist, h->d_cperm);
+    else k_cell_scatter<3><<<sb, 256, 0, s>>>(d_pts, npts, h->d_chist, h->d_cperm);
+    *sorted = true;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, double* d_out,
                                   int per_component) {
     if (npts == 0) return cudaSuccess;
@@ -569,30 +595,21 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
     }
     const size_t smem = smem_of(npt) + sizeof(int) * npt;
     const unsigned blocks = (unsigned)((npts + npt - 1) / npt);
-    // cell sort (enough points per cell to matter, int32 indices)
-    const char* ns = getenv("SGIGA_COMBINE_NOSORT");
+    // cell sort (enough points per cell to matter, int32 indices): done here,
+    // or already enqueued on the side stream by sgiga_run (h->cs_ready)
     const int* perm = nullptr;
-    if (npts >= 2048 && npts < (int64_t)1 << 31 && !(ns && ns[0] == '1')) {
-        cudaError_t e;
-        if ((size_t)npts > h->cperm_cap) {
-            if (h->d_cperm) cudaFree(h->d_cperm);
-            h->d_cperm = nullptr;
-            h->cperm_cap = 0;
-            if ((e = cudaMalloc(&h->d_cperm, sizeof(int) * npts)) != cudaSuccess) return e;
-            h->cperm_cap = (size_t)npts;
-        }
-        // d_chist is zero here: zeroed at create, re-zeroed by the combine
-        // kernel after every sorted launch
-        const unsigned sb = (unsigned)((npts + 255) / 256);
-        if (h->d == 1) k_cell_hist<1><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist);
-        else if (h->d == 2) k_cell_hist<2><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist);
-        else k_cell_hist<3><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist);
-        k_cell_scan<<<1, 1024, 0, h->stream>>>(h->d_chist);
-        if (h->d == 1) k_cell_scatter<1><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist, h->d_cperm);
-        else if (h->d == 2) k_cell_scatter<2><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist, h->d_cperm);
-        else k_cell_scatter<3><<<sb, 256, 0, h->stream>>>(d_pts, npts, h->d_chist, h->d_cperm);
-        h->launches[2] += 3;
+    if (h->cs_ready) {
         perm = h->d_cperm;
+        h->cs_ready = false;
+        h->launches[2] += 3;
+    } else {
+        bool sorted = false;
+        cudaError_t e = launch_combine_sort(h, d_pts, npts, h->stream, &sorted);
+        if (e != cudaSuccess) return e;
+        if (sorted) {
+            perm = h->d_cperm;
+            h->launches[2] += 3;
+        }
     }
 #define LAUNCH_CPT(DD, PP)                                                                          \
     {                                                                                               \

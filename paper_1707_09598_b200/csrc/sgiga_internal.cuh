@@ -225,6 +225,9 @@ cudaError_t launch_status(Handle* h);
 cudaError_t launch_expand(Handle* h);
 cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, double* d_out,
                                   int per_component);
+// cell sort of the combine points on stream s; *sorted = false when the
+// point set is not sorted (too small / too large / SGIGA_COMBINE_NOSORT)
+cudaError_t launch_combine_sort(Handle* h, const double* d_pts, int64_t npts, cudaStream_t s, bool* sorted);
 cudaError_t launch_combine_grid(Handle* h, const double* d_pts, const int64_t* npd, int comp,
                                 double* d_vals, double* d_grads);
 cudaError_t launch_error_norms(Handle* h, const double* d_pts, const double* d_wts,

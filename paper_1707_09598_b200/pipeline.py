@@ -200,6 +200,20 @@ class Batch:
         self.iters, self.relres = it, rr
         _lib.check(code)
 
+    def run_device_async(self, pts_ptr: int, npts: int, out_ptr: int, rtol: float = 1e-13, maxit: int = 0):
+        """Enqueue one run_device pass without synchronising (passes pipeline
+        back to back on the device); run_wait() reports the last one."""
+        self._host_forcing_density()
+        _lib.check(self.lib.sgiga_run_async(self.h, float(rtol), int(maxit), pts_ptr, int(npts), out_ptr))
+
+    def run_wait(self):
+        n = self.n_comp
+        it = np.zeros(n, dtype=np.int32)
+        rr = np.zeros(n, dtype=np.float64)
+        code = self.lib.sgiga_run_wait(self.h, _lib.ptr(it, ct.c_int32), _lib.ptr(rr, ct.c_double))
+        self.iters, self.relres = it, rr
+        _lib.check(code)
+
     def coefficients(self) -> np.ndarray:
         out = np.empty(self.total_dofs)
         _lib.check(self.lib.sgiga_coefficients(self.h, _lib.ptr(out, ct.c_double)))

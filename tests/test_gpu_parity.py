@@ -375,6 +375,29 @@ def test_run_graph_replay_matches_direct_launches(monkeypatch):
         b.close()
 
 
+def test_async_passes_match_synchronous_run():
+    """sgiga_run_async x N + sgiga_run_wait == sgiga_run, bitwise (values,
+    iterations); the side-stream point sort is joined before every combine."""
+    import torch
+    cfg = configs.get_config("cfg2")
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    pts = torch.from_numpy(cfg.points(20000)).cuda()
+    out = torch.empty(pts.shape[0], dtype=torch.float64, device="cuda")
+    b = Batch(spec)
+    try:
+        b.run_device(pts.data_ptr(), pts.shape[0], out.data_ptr())
+        ref, it_ref = out.cpu().numpy().copy(), b.iters.copy()
+        for _ in range(5):   # direct, capture, replays
+            b.run_device_async(pts.data_ptr(), pts.shape[0], out.data_ptr())
+        b.run_wait()
+        assert np.array_equal(out.cpu().numpy(), ref)
+        assert np.array_equal(b.iters, it_ref)
+        host = b.run(cfg.points(20000))
+        assert np.array_equal(host, ref)
+    finally:
+        b.close()
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
 def test_tiled_combine_matches_per_thread_kernel(name, monkeypatch):
     """k_combine_points_tiled == the one-thread-per-point kernel, bitwise,
