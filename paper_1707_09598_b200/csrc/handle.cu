@@ -431,6 +431,11 @@ static int decode_err(Handle* h) {
         SG_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
         return SGIGA_ERR_CUDA;
     }
+    if (e & ERRF_POINTS) {
+        set_error("evaluation points must lie in [0, 1]^d");
+        SG_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
+        return SGIGA_ERR_VALUE;
+    }
     if (e & ERRF_SPAN) {
         set_error("quadrature node escaped its element");
         SG_CUDA(cudaMemsetAsync(h->d_err, 0, sizeof(int), h->stream));
@@ -829,7 +834,8 @@ static bool run_graphs_enabled() {
 
 // enqueue of one whole pass (device pointers): direct launches, capture, or
 // replay of the pass graph; no synchronisation
-static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, int64_t npts, double* dout) {
+static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, int64_t npts, double* dout,
+                       const double* hsrc = nullptr) {
     int st;
     auto enqueue_all = [&]() -> int {
         // the combine's point sort depends on the points only: side stream,
@@ -839,6 +845,9 @@ static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, 
             bool sorted = false;
             SG_CUDA(cudaEventRecord(h->cs_fork, h->stream));
             SG_CUDA(cudaStreamWaitEvent(h->stream3, h->cs_fork, 0));
+            if (hsrc)   // pinned host points: their upload overlaps assembly and solve too
+                SG_CUDA(cudaMemcpyAsync(const_cast<double*>(dp), hsrc, sizeof(double) * npts * h->d,
+                                        cudaMemcpyHostToDevice, h->stream3));
             SG_CUDA(launch_combine_sort(h, dp, npts, h->stream3, &sorted));
             SG_CUDA(cudaEventRecord(h->cs_join, h->stream3));
             h->cs_pending = true;
@@ -859,7 +868,7 @@ static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, 
     // component on the single-launch small path) and no profiling knob is on
     const bool can_graph = run_graphs_enabled() && h->large_comps.empty() && !h->graph_broken;
     const bool same = can_graph && h->rkey.npts == npts && h->rkey.rtol == rtol && h->rkey.maxit == maxit &&
-                      h->rkey.dp == dp && h->rkey.dout == dout;
+                      h->rkey.dp == dp && h->rkey.dout == dout && h->rkey.hp == hsrc;
     if (same && h->run_exec) {
         SG_CUDA(cudaGraphLaunch(h->run_exec, h->stream));
         h->tables_ready = true;
@@ -894,7 +903,7 @@ static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, 
         if ((st = enqueue_all())) return st;
         if (can_graph) {
             h->drop_run_graph();
-            h->rkey.rtol = rtol; h->rkey.maxit = maxit; h->rkey.dp = dp; h->rkey.dout = dout;
+            h->rkey.rtol = rtol; h->rkey.maxit = maxit; h->rkey.dp = dp; h->rkey.dout = dout; h->rkey.hp = hsrc;
             h->rkey.npts = npts; h->rkey.warm = 1;
         }
     }
@@ -921,9 +930,23 @@ int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, i
     if (device < 0) { set_error("sgiga_run: per-component output is not supported"); return SGIGA_ERR_VALUE; }
     const double* dp = pts;
     double* dout = out;
+    const double* hsrc = nullptr;
     int st;
-    if (npts > 0 && device == 0 && (st = stage_points(h, pts, npts, (size_t)npts, &dp, &dout))) return st;
-    if ((st = run_enqueue(h, rtol, maxit, dp, npts, dout))) return st;
+    if (npts > 0 && device == 0) {
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, pts) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (pinned) {   // uploaded on the point-sort side stream inside the pass
+            if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
+            if ((st = ensure_scratch(&s_out, &s_out_cap, (size_t)npts))) return st;
+            dp = s_pts;
+            dout = s_out;
+            hsrc = pts;
+        } else if ((st = stage_points(h, pts, npts, (size_t)npts, &dp, &dout))) {
+            return st;
+        }
+    }
+    if ((st = run_enqueue(h, rtol, maxit, dp, npts, dout, hsrc))) return st;
     if (npts > 0 && device == 0)
         SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * npts, cudaMemcpyDeviceToHost, h->stream));
     return run_finish(h, iters_out, relres_out);
@@ -986,7 +1009,7 @@ int sgiga_combine_points(sgiga_handle* hh, const double* pts, int64_t npts, doub
     h->begin_call();
     if ((st = combine_enqueue(h, dp, npts, dout, per_comp))) return st;
     if (!dev_ptrs) SG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream));
-    SG_CUDA(cudaStreamSynchronize(h->stream));
+    if ((st = check_err(h))) return st;   // synchronises; points outside [0,1]^d are reported here
     SG_CUDA(h->elapsed(&h->ms[2], Handle::PHASE_EV + 4, Handle::PHASE_EV + 5));
     return SGIGA_OK;
 }

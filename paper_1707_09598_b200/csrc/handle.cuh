@@ -163,6 +163,7 @@ struct Handle {
         double rtol = 0.0;
         int maxit = 0, warm = 0;
         const double* dp = nullptr;
+        const double* hp = nullptr;   // pinned host source of the points (uploaded inside the pass)
         double* dout = nullptr;
         int64_t npts = -1;
     } rkey;

@@ -189,12 +189,15 @@ __global__ void __launch_bounds__(128)
 k_combine_points(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
                  const double* __restrict__ knots, int mu, const double* __restrict__ coef,
                  const double* __restrict__ pts, int64_t npts, double* __restrict__ out,
-                 int per_component) {
+                 int per_component, int* __restrict__ err) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= npts) return;
     double xi[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) xi[k] = pts[t * D + k];
+    for (int k = 0; k < D; ++k) {
+        xi[k] = pts[t * D + k];
+        if (!(xi[k] >= 0.0 && xi[k] <= 1.0)) atomicOr(err, ERRF_POINTS);   // evaluation points in [0,1]^d
+    }
     double acc, g[D];
     combine_at<D, P, false>(comps, 0, ncomp, true, tabs, knots, mu, coef, xi, acc, g,
                             per_component ? out + t : nullptr, npts);
@@ -219,7 +222,8 @@ __global__ void __launch_bounds__(CP_THREADS)
 k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
                        int ntab, const double* __restrict__ knots, int mu, const double* __restrict__ coef,
                        const double* __restrict__ pts, int64_t npts, const int* __restrict__ perm,
-                       double* __restrict__ out, int per_component, int npt, int* __restrict__ hist) {
+                       double* __restrict__ out, int per_component, int npt, int* __restrict__ hist,
+                       int* __restrict__ err) {
     extern __shared__ double csm[];
     double* Bt = csm;                                   // [ntab][P][npt]
     double* V = Bt + (size_t)ntab * P * npt;            // [ncomp][npt]
@@ -237,6 +241,7 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
         if (pt >= nloc) continue;
         const TabInfo T = tabs[t];
         const double xi = pts[(int64_t)gidx[pt] * D + T.axis];
+        if (!(xi >= 0.0 && xi <= 1.0)) atomicOr(err, ERRF_POINTS);   // evaluation points in [0,1]^d
         double bv[P];
         first[t * npt + pt] = axis_basis<P, false>(T, knots, mu, xi, bv, nullptr);
 #pragma unroll
@@ -587,7 +592,7 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
 #define LAUNCH_CP(DD, PP)                                                                     \
     k_combine_points<DD, PP><<<blocks, 128, 0, h->stream>>>(h->d_comps, h->ncomp, h->d_tabs,   \
                                                             h->d_knots, h->mu, h->d_coef,     \
-                                                            d_pts, npts, d_out, per_component)
+                                                            d_pts, npts, d_out, per_component, h->d_err)
         SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CP)
 #undef LAUNCH_CP
         h->launches[2]++;
@@ -618,7 +623,7 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
         if (e_ != cudaSuccess) return e_;                                                           \
         k_combine_points_tiled<DD, PP><<<blocks, CP_THREADS, smem, h->stream>>>(                    \
             h->d_comps, h->ncomp, h->d_tabs, ntab, h->d_knots, h->mu, h->d_coef, d_pts, npts, perm,  \
-            d_out, per_component, npt, perm ? h->d_chist : nullptr);                                \
+            d_out, per_component, npt, perm ? h->d_chist : nullptr, h->d_err);                      \
     }
     SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CPT)
 #undef LAUNCH_CPT

@@ -31,7 +31,7 @@ constexpr int COMBINE_SORT_BITS = 12;                      // cell sort of the c
 constexpr int COMBINE_SORT_BINS = 1 << COMBINE_SORT_BITS;
 
 // device error flags (bit mask in Handle::d_err)
-enum : int { ERRF_GEOMETRY = 1, ERRF_NONFINITE = 2, ERRF_SPAN = 4 };
+enum : int { ERRF_GEOMETRY = 1, ERRF_NONFINITE = 2, ERRF_SPAN = 4, ERRF_POINTS = 16 };   // 8: cluster shape
 
 struct TabInfo {        // one analysis knot vector = (axis, level)
     int axis, level;

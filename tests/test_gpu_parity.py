@@ -394,6 +394,22 @@ def test_async_passes_match_synchronous_run():
         assert np.array_equal(b.iters, it_ref)
         host = b.run(cfg.points(20000))
         assert np.array_equal(host, ref)
+        # pinned host points: uploaded on the point-sort side stream inside
+        # the pass (direct, captured, replayed)
+        pin = torch.empty((20000, spec.d), dtype=torch.float64, pin_memory=True)
+        pin.copy_(torch.from_numpy(cfg.points(20000)))
+        for _ in range(4):
+            assert np.array_equal(b.run(pin.numpy()), ref)
+        # points outside [0, 1]^d: ValueError (device-side check), for the
+        # fused pass and the standalone combine; the handle stays usable
+        bad = cfg.points(20000)
+        bad[777, 1] = 1.5
+        with pytest.raises(ValueError):
+            b.run(bad)
+        bad[777, 1] = -0.25
+        with pytest.raises(ValueError):
+            b.combine_points(bad)
+        assert np.array_equal(b.run(pin.numpy()), ref)
     finally:
         b.close()
 
