@@ -388,8 +388,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         if (nplanes > 0) {
             if (inG3) load_bs(e_first);
             if constexpr (F::TMA) {
-                load_plane_tma((int64_t)e_first * Q, 0);
-                if (nplanes > 1) load_plane_tma((int64_t)e_first * Q + 1, 1);
+                for (int jj = 0; jj < F::GPD && jj < nplanes; ++jj) load_plane_tma((int64_t)e_first * Q + jj, jj);
             } else {
                 load_plane((int64_t)e_first * Q, 0);
                 cp_async_wait_all();
