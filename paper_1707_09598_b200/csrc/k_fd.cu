@@ -31,6 +31,8 @@ constexpr int FD_THREADS = 256;
 constexpr int EIG_THREADS = 512;
 constexpr int EIG_ITEMS = ((FD_MMAX / 2) * (FD_MMAX / 2) + (FD_MMAX / 2) * FD_MMAX + EIG_THREADS - 1) / EIG_THREADS;
 constexpr int FD_LD = FD_MMAX + 1;   // padded row stride of the eigen work arrays
+// staged quadrature tables of one knot vector: 2 nel q (p+1) + nel q <= 74 * 10 * 11
+constexpr int FD_TAB_MAX = 8192;
 
 template <int NT = FD_THREADS>
 __device__ __forceinline__ double fd_block_sum(double v, double* red) {
@@ -80,7 +82,7 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
     long long t0 = clock64();
     auto stamp = [&](int k) { if (prof && threadIdx.x == 0) prof[blockIdx.x * 8 + k] = clock64() - t0; };
     constexpr int NPMAX = FD_MMAX / 2 + 1;
-    __shared__ double rc[NPMAX + 1], rs[NPMAX + 1], red[EIG_THREADS / 32];
+    __shared__ double rc[NPMAX + 1], rs[NPMAX + 1], red[EIG_THREADS / 32], rdg[FD_MMAX];
     __shared__ int rp[NPMAX + 1], rq[NPMAX + 1];
     const int t = uniq[blockIdx.x];
     const TabInfo T = tabs[t];
@@ -88,10 +90,19 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
     double* L = fsm;                       // M, then its Cholesky factor (lower)
     double* Cm = L + FD_MMAX * FD_LD;      // K, then L^-1 K L^-T, then Lambda
     double* V = Cm + FD_MMAX * FD_LD;      // Jacobi rotations, then U
-    const int64_t nq = (int64_t)T.nel * q;
-    const double* bv = vals + T.val_off;
+    double* tb = V + FD_MMAX * FD_LD;      // staged basis values | derivatives | weights
+    const int nq = T.nel * q;
+    {   // one coalesced copy of this knot vector's quadrature tables
+        const double* bvg = vals + T.val_off;
+        const double* wg = qw + T.qp_off;
+        const int nv = 2 * nq * P;
+        for (int i = tid; i < nv; i += EIG_THREADS) tb[i] = bvg[i];
+        for (int i = tid; i < nq; i += EIG_THREADS) tb[nv + i] = wg[i];
+    }
+    const double* bv = tb;
     const double* bd = bv + nq * P;
-    const double* w = qw + T.qp_off;
+    const double* w = bd + nq * P;
+    __syncthreads();
 
     // interior mass / stiffness (global functions 1..n-2), band |i-j| <= p
     double dmx = 0.0, amx = 0.0;
@@ -105,10 +116,10 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
             for (int e = elo; e <= ehi; ++e) {
                 const int a = gi - e * mu, b = gj - e * mu;
                 for (int g = 0; g < q; ++g) {
-                    const int64_t base = ((int64_t)e * q + g) * P;
-                    const double wg = w[(int64_t)e * q + g];
-                    mv += wg * bv[base + a] * bv[base + b];
-                    kv += wg * bd[base + a] * bd[base + b];
+                    const int base = (e * q + g) * P;
+                    const double wq = w[e * q + g];
+                    mv += wq * bv[base + a] * bv[base + b];
+                    kv += wq * bd[base + a] * bd[base + b];
                 }
             }
         }
@@ -156,40 +167,72 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
             __syncthreads();
         }
     }
-    for (int idx = tid; idx < m * m; idx += EIG_THREADS) V[(idx / m) * FD_LD + idx % m] = (idx / m == idx % m) ? 1.0 : 0.0;
-    __syncthreads();
     stamp(0);
-    // banded Cholesky M = L L^T (lower triangle of L)
-    for (int k = 0; k < m; ++k) {
-        if (tid == 0) L[k * FD_LD + k] = sqrt(L[k * FD_LD + k]);
-        __syncthreads();
-        const double dk = L[k * FD_LD + k];
-        const int hi = min(m - 1, k + p);
-        if (tid < hi - k) L[(k + 1 + tid) * FD_LD + k] /= dk;
-        __syncthreads();
-        for (int idx = tid; idx < p * p; idx += EIG_THREADS) {
-            const int i = k + 1 + idx / p, j = k + 1 + idx % p;
-            if (i <= hi && j <= i) L[i * FD_LD + j] -= L[i * FD_LD + k] * L[j * FD_LD + k];
+    // banded Cholesky M = L L^T of each diagonal block (one warp per block,
+    // the two persymmetric halves side by side); rdg = 1 / diag(L)
+    {
+        const int warp = tid >> 5, lane = tid & 31;
+        const int nblk = sym && ma > 0 ? 2 : 1;
+        if (warp < nblk) {
+            const int b0 = warp ? ms : 0, b1 = warp ? m : ms;
+            // lane -> (i, j) of the p x p trailing update, 1 <= j <= i <= p
+            int ui = 0, uj = 0;
+            {
+                int c = lane;
+                for (int i = 1; i <= p && ui == 0; ++i) { if (c < i) { ui = i; uj = c + 1; } else c -= i; }
+            }
+            for (int k = b0; k < b1; ++k) {
+                const double d = sqrt(L[k * FD_LD + k]);
+                const double rd = 1.0 / d;
+                const bool wc = lane >= 1 && lane <= p && k + lane < b1, wu = ui > 0 && k + ui < b1;
+                const double cv = wc ? L[(k + lane) * FD_LD + k] : 0.0;
+                double li = 0.0, lj = 0.0, tv = 0.0;
+                if (wu) { li = L[(k + ui) * FD_LD + k] * rd; lj = L[(k + uj) * FD_LD + k] * rd; tv = L[(k + ui) * FD_LD + k + uj]; }
+                __syncwarp();
+                if (lane == 0) { L[k * FD_LD + k] = d; rdg[k] = rd; }
+                if (wc) L[(k + lane) * FD_LD + k] = cv * rd;
+                if (wu) L[(k + ui) * FD_LD + k + uj] = tv - li * lj;
+                __syncwarp();
+            }
         }
-        __syncthreads();
+        for (int idx = tid; idx < m * m; idx += EIG_THREADS)   // V = I (Jacobi accumulator)
+            V[(idx / m) * FD_LD + idx % m] = (idx / m == idx % m) ? 1.0 : 0.0;
     }
+    __syncthreads();
     stamp(1);
-    // X = L^-1 K (column j per thread), then C = X L^-T (row r per thread)
+    // X = L^-1 K (column j per thread), then C = X L^-T (row r per thread):
+    // forward substitutions with the last p results in registers
     if (tid < m) {
         const int j = tid;
-        for (int i = 0; i < m; ++i) {
+        const int b0 = (sym && j >= ms) ? ms : 0, b1 = (sym && j < ms) ? ms : m;
+        double xw[PMAX - 1] = {};
+        for (int i = b0; i < b1; ++i) {
             double s = Cm[i * FD_LD + j];
-            for (int l = max(0, i - p); l < i; ++l) s -= L[i * FD_LD + l] * Cm[l * FD_LD + j];
-            Cm[i * FD_LD + j] = s / L[i * FD_LD + i];
+#pragma unroll
+            for (int l = PMAX - 2; l >= 0; --l)   // xw[l] = X[i-1-l][j]
+                if (l < p && i - 1 - l >= b0) s -= L[i * FD_LD + i - 1 - l] * xw[l];
+            s *= rdg[i];
+#pragma unroll
+            for (int l = PMAX - 2; l > 0; --l) xw[l] = xw[l - 1];
+            xw[0] = s;
+            Cm[i * FD_LD + j] = s;
         }
     }
     __syncthreads();
     if (tid < m) {
         const int r = tid;
-        for (int i = 0; i < m; ++i) {
+        const int b0 = (sym && r >= ms) ? ms : 0, b1 = (sym && r < ms) ? ms : m;
+        double xw[PMAX - 1] = {};
+        for (int i = b0; i < b1; ++i) {
             double s = Cm[r * FD_LD + i];
-            for (int l = max(0, i - p); l < i; ++l) s -= L[i * FD_LD + l] * Cm[r * FD_LD + l];
-            Cm[r * FD_LD + i] = s / L[i * FD_LD + i];
+#pragma unroll
+            for (int l = PMAX - 2; l >= 0; --l)
+                if (l < p && i - 1 - l >= b0) s -= L[i * FD_LD + i - 1 - l] * xw[l];
+            s *= rdg[i];
+#pragma unroll
+            for (int l = PMAX - 2; l > 0; --l) xw[l] = xw[l - 1];
+            xw[0] = s;
+            Cm[r * FD_LD + i] = s;
         }
     }
     __syncthreads();
@@ -258,10 +301,14 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
                     const double apq = Cm[pi * FD_LD + qi];
                     const double app = Cm[pi * FD_LD + pi], aqq = Cm[qi * FD_LD + qi];
                     if (apq != 0.0 && apq * apq > 1e-36 * fabs(app * aqq)) {
-                        const double th = (aqq - app) / (2.0 * apq);
-                        const double tt = copysign(1.0, th) / (fabs(th) + sqrt(fma(th, th, 1.0)));
-                        c = rsqrt(fma(tt, tt, 1.0));
-                        sn = tt * c;
+                        // t = tan of the rotation = sgn(phi) psi / (|phi| + hypot(phi, psi)),
+                        // phi = aqq - app, psi = 2 apq; c = 1/sqrt(1+t^2), s = t c, written
+                        // without divisions: with D = |phi| + hypot, c = D / hypot(D, psi)
+                        const double phi = aqq - app, psi = 2.0 * apq;
+                        const double dd = fabs(phi) + sqrt(fma(phi, phi, psi * psi));
+                        const double ir = rsqrt(fma(dd, dd, psi * psi));
+                        c = dd * ir;
+                        sn = copysign(1.0, phi) * psi * ir;
                     }
                 }
                 rp[tid] = pi; rq[tid] = qi; rc[tid] = c; rs[tid] = sn;
@@ -308,13 +355,21 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
     }
     stamp(3);
     if (prof && tid == 0) { prof[blockIdx.x * 8 + 5] = nsweep; prof[blockIdx.x * 8 + 6] = m + (sym ? 1000 : 0); }
-    // U' = L^-T Q (column j per thread, back substitution with the band of L)
+    // U' = L^-T Q (column j per thread, back substitution in its diagonal block)
     if (tid < m) {
         const int j = tid;
-        for (int i = m - 1; i >= 0; --i) {
+        const int b0 = (sym && j >= ms) ? ms : 0, b1 = (sym && j < ms) ? ms : m;
+        double xw[PMAX - 1] = {};
+        for (int i = b1 - 1; i >= b0; --i) {
             double s = V[i * FD_LD + j];
-            for (int l = i + 1; l <= min(m - 1, i + p); ++l) s -= L[l * FD_LD + i] * V[l * FD_LD + j];
-            V[i * FD_LD + j] = s / L[i * FD_LD + i];
+#pragma unroll
+            for (int l = PMAX - 2; l >= 0; --l)   // xw[l] = U'[i+1+l][j]
+                if (l < p && i + 1 + l < b1) s -= L[(i + 1 + l) * FD_LD + i] * xw[l];
+            s *= rdg[i];
+#pragma unroll
+            for (int l = PMAX - 2; l > 0; --l) xw[l] = xw[l - 1];
+            xw[0] = s;
+            V[i * FD_LD + j] = s;
         }
     }
     __syncthreads();
@@ -764,7 +819,7 @@ cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
     return cudaGetLastError();
 }
 
-size_t fd_eigen_smem() { return sizeof(double) * 3 * FD_MMAX * FD_LD; }
+size_t fd_eigen_smem() { return sizeof(double) * (3 * FD_MMAX * FD_LD + FD_TAB_MAX); }
 
 size_t fd_comp_smem(const CompInfo& C, int d) {
     int64_t u = 0, l = 0;

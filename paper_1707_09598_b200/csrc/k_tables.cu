@@ -13,16 +13,19 @@ namespace sgiga {
 // ---- open knot vectors from breakpoints ---------------------------------
 __global__ void k_build_knots(const TabInfo* __restrict__ tabs, int ntab, int p, int mu,
                               const double* __restrict__ bp, double* __restrict__ knots) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntab) return;
-    TabInfo T = tabs[t];
+    // one CTA per table, one thread per knot: [0]*(p+1), interior breakpoints
+    // with multiplicity mu, [1]*(p+1)  (splines.py:26-80 make_open_knot_vector)
+    const TabInfo T = tabs[blockIdx.x];
     double* k = knots + T.knot_off;
     const double* b = bp + T.bp_off;
-    int pos = 0;
-    for (int i = 0; i <= p; ++i) k[pos++] = 0.0;
-    for (int e = 1; e < T.nel; ++e)
-        for (int j = 0; j < mu; ++j) k[pos++] = b[e];
-    for (int i = 0; i <= p; ++i) k[pos++] = 1.0;
+    const int nk = 2 * (p + 1) + (T.nel - 1) * mu;
+    for (int pos = threadIdx.x; pos < nk; pos += blockDim.x) {
+        double v;
+        if (pos <= p) v = 0.0;
+        else if (pos >= nk - (p + 1)) v = 1.0;
+        else v = b[1 + (pos - (p + 1)) / mu];
+        k[pos] = v;
+    }
 }
 
 // ---- basis + geometry-basis tables at every (table, element, node) -------
@@ -220,7 +223,8 @@ __global__ void k_metric(const CompInfo* __restrict__ comps, int ncomp,
 
 cudaError_t launch_build_knots(Handle* h) {
     int nt = (int)h->tabs.size();
-    k_build_knots<<<(nt + 127) / 128, 128, 0, h->stream>>>(h->d_tabs, nt, h->p, h->mu, h->d_bp,
+    if (nt == 0) return cudaSuccess;
+    k_build_knots<<<nt, 128, 0, h->stream>>>(h->d_tabs, nt, h->p, h->mu, h->d_bp,
                                                            h->d_knots);
     h->launches[0]++;
     return cudaGetLastError();
