@@ -43,7 +43,7 @@ static void free_all(Handle* h) {
                     h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
                     h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps,
-                    h->d_fdl_list, h->d_fdl_off, h->d_fdl};
+                    h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};
@@ -53,6 +53,7 @@ static void free_all(Handle* h) {
         if (e) cudaEventDestroy(e);
     if (h->fd_fork) cudaEventDestroy(h->fd_fork);
     if (h->fd_join) cudaEventDestroy(h->fd_join);
+    if (h->fd_metric) cudaEventDestroy(h->fd_metric);
     if (h->stream2) cudaStreamDestroy(h->stream2);
     if (h->cs_fork) cudaEventDestroy(h->cs_fork);
     if (h->cs_join) cudaEventDestroy(h->cs_join);
@@ -533,10 +534,12 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_fdl_list, h->fdl_comps.size());
     A_(d_fdl_off, h->comps.size());
     A_(d_fdl, h->fdl_total);
+    A_(d_ck, (int64_t)MAXD * h->ncomp);
 #undef A_
     if (ea == cudaSuccess) ea = cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_fork, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_join, cudaEventDisableTiming);
+    if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_metric, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->cs_fork, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->cs_join, cudaEventDisableTiming);
@@ -690,16 +693,21 @@ static int assemble_enqueue(Handle* h) {
     h->tables_ready = false;   // kernel 1 is part of every assembly pass
     int st = ensure_tables(h);
     if (st) return st;
-    if (!h->fd_uniq.empty()) {   // FD eigen-factors on the side stream, overlapping the assembly
+    if (!h->fd_uniq.empty() || !h->fd_comps.empty() || !h->fdl_comps.empty()) {   // FD eigen-factors on the side stream, overlapping the assembly
         SG_CUDA(cudaEventRecord(h->fd_fork, h->stream));
         SG_CUDA(cudaStreamWaitEvent(h->stream2, h->fd_fork, 0));
         SG_CUDA(launch_fd_eigen(h, h->stream2));
-        SG_CUDA(cudaEventRecord(h->fd_join, h->stream2));
         h->fd_pending = true;
     }
     h->kstart(1);
     SG_CUDA(launch_metric(h));
     h->kstop(1);
+    if (h->fd_pending) {   // c_k and the line factors need the metric: side stream again
+        SG_CUDA(cudaEventRecord(h->fd_metric, h->stream));
+        SG_CUDA(cudaStreamWaitEvent(h->stream2, h->fd_metric, 0));
+        SG_CUDA(launch_fd_setup(h, h->stream2));
+        SG_CUDA(cudaEventRecord(h->fd_join, h->stream2));
+    }
     h->kstart(2);
     SG_CUDA(launch_assembly(h));
     h->kstop(2);

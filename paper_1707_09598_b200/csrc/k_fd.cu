@@ -401,8 +401,9 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
          const int* __restrict__ slotoff, const double* __restrict__ stencil,
          const double* __restrict__ rhs, const double* __restrict__ Gbuf,
          const int64_t* __restrict__ uoff, const int64_t* __restrict__ loff,
-         const double* __restrict__ dU, const double* __restrict__ dL, double* __restrict__ xout,
-         CgState* __restrict__ st, double* __restrict__ relres, double rtol2, int maxit) {
+         const double* __restrict__ dU, const double* __restrict__ dL, const double* __restrict__ ckg,
+         double* __restrict__ xout, CgState* __restrict__ st, double* __restrict__ relres, double rtol2,
+         int maxit) {
     extern __shared__ double fsm[];
     __shared__ double red[FD_THREADS / 32];
     const int c = list[blockIdx.x];
@@ -427,7 +428,8 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
     double* ph = pe + H;
     double* Us = pe + R + 2 * H;      // U_k, k = 0..D-1
     double* Ls = Us + ntot_u;         // lambda_k
-    int* offs = reinterpret_cast<int*>(Ls + ntot_l);
+    double* qp = Ls + ntot_l;         // SpMV partial sums [FD_THREADS]
+    int* offs = reinterpret_cast<int*>(qp + FD_THREADS);
     const double* b = rhs + C.vec_off;
     const double* val = stencil + C.mat_off;
 
@@ -440,18 +442,10 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
     }
     for (int i = tid; i < H; i += FD_THREADS) { pe[i] = 0.0; pe[H + R + i] = 0.0; }
     // c_k = sum over the quadrature points of G_kk (the patch integral of the
-    // metric's diagonal; 1 for the identity map)
+    // metric's diagonal; 1 for the identity map), from k_fd_metric_scale
     double ck[D];
-    {
-        const double* Gc = Gbuf + C.qp_off;
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const double* g = Gc + (int64_t)sym_index(D, k, k) * C.nqp;
-            double s = 0.0;
-            for (int64_t i = tid; i < C.nqp; i += FD_THREADS) s += g[i];
-            ck[k] = fd_block_sum(s, red);
-        }
-    }
+    for (int k = 0; k < D; ++k) ck[k] = ckg[c * MAXD + k];
     // z = P^-1 v  (v -> ts -> zs -> ... ; 2D mode products, result in zs)
     auto mode = [&](const double* src, double* dst, int k, bool trans) {
         const int m = mk[k], s = rsk[k];
@@ -487,18 +481,37 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
 #pragma unroll
         for (int k = D - 1; k >= 0; --k) { mode(src, bufs[w], k, false); src = bufs[w]; w ^= 1; }
     };
-    // q = A v for v held in ph (halo-padded)
+    // q = A v for v held in ph (halo-padded).  np threads per row (slot
+    // classes t = part mod np), consecutive threads on consecutive rows so the
+    // stencil loads coalesce; the np partial sums are added in fixed order
+    const int np = max(1, min(8, FD_THREADS / max(R, 1)));
     auto spmv = [&]() {
-        for (int row = tid; row < R; row += FD_THREADS) {
+        for (int w = tid; w < R * np; w += FD_THREADS) {
+            const int part = w / R, row = w - part * R;
             const int rb = fd_row_base(C, D, row);
+            // batches of 8 independent stencil loads in flight (L2 latency)
             double y0 = 0.0, y1 = 0.0;
-            int t = 0;
-            for (; t + 1 < NS; t += 2) {
-                y0 += __ldg(val + (size_t)t * R + row) * ph[rb + offs[t]];
-                y1 += __ldg(val + (size_t)(t + 1) * R + row) * ph[rb + offs[t + 1]];
+            int t = part;
+            for (; t + 7 * np < NS; t += 8 * np) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(val + (size_t)(t + u * np) * R + row);
+#pragma unroll
+                for (int u = 0; u < 8; u += 2) {
+                    y0 += v[u] * ph[rb + offs[t + u * np]];
+                    y1 += v[u + 1] * ph[rb + offs[t + (u + 1) * np]];
+                }
             }
-            if (t < NS) y0 += __ldg(val + (size_t)t * R + row) * ph[rb + offs[t]];
-            qs[row] = y0 + y1;
+            for (; t < NS; t += np) y0 += __ldg(val + (size_t)t * R + row) * ph[rb + offs[t]];
+            if (np == 1) qs[row] = y0 + y1;
+            else qp[w] = y0 + y1;
+        }
+        __syncthreads();
+        if (np == 1) return;
+        for (int row = tid; row < R; row += FD_THREADS) {
+            double y = qp[row];
+            for (int k = 1; k < np; ++k) y += qp[k * R + row];
+            qs[row] = y;
         }
         __syncthreads();
     };
@@ -575,17 +588,157 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
 // its pencil is only factorised per line by banded Cholesky.  One CTA per
 // component, vectors in the batch's global PCG arrays (L2-resident).
 constexpr int FDL_THREADS = 256;
+constexpr int PM = PMAX - 1;   // largest degree: register windows of the banded line factors
+
+// ---- FD set-up, off the critical path (side stream, overlapping the
+// assembly; k_fd_setup_enqueue) ----------------------------------------------
+// c_k = patch integral of G_kk (sum over the quadrature points) of every FD /
+// line-FD component: one CTA per (component, axis), fixed-order block sum
+template <int D>
+__global__ void __launch_bounds__(256)
+k_fd_metric_scale(const CompInfo* __restrict__ comps, const int* __restrict__ list_a, int na,
+                  const int* __restrict__ list_b, const double* __restrict__ Gbuf, double* __restrict__ ckg) {
+    __shared__ double red[8];
+    const int c = blockIdx.x < na ? list_a[blockIdx.x] : list_b[blockIdx.x - na];
+    const int k = blockIdx.y, tid = threadIdx.x;
+    const CompInfo& C = comps[c];
+    const double* g = Gbuf + C.qp_off + (int64_t)sym_index(D, k, k) * C.nqp;
+    const int64_t n = C.nqp;
+    double s0 = 0.0, s1 = 0.0;
+    int64_t i = tid;
+    for (; i + 7 * 256 < n; i += 8 * 256) {   // 8 loads in flight
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(g + i + u * 256);
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) { s0 += v[u]; s1 += v[u + 1]; }
+    }
+    for (; i < n; i += 256) s0 += g[i];
+    const double tot = fd_block_sum<256>(s0 + s1, red);
+    if (tid == 0) ckg[c * MAXD + k] = tot;
+}
+
+// banded interior K_s, M_s of a line-FD component's stream axis (lower band,
+// [i][k] = entry (i, i - k)), one CTA per component
+template <int D>
+__global__ void __launch_bounds__(256)
+k_fdl_bands(const CompInfo* __restrict__ comps, const int* __restrict__ list, const TabInfo* __restrict__ tabs,
+            const double* __restrict__ vals, const double* __restrict__ qw, int p, int mu, int q,
+            const int64_t* __restrict__ fdl_off, double* __restrict__ fdl) {
+    const int c = list[blockIdx.x];
+    const CompInfo& C = comps[c];
+    const int P1 = p + 1, s = C.ax[D - 1], ms = C.m[s];
+    double* Kb = fdl + fdl_off[c];
+    double* Mb = Kb + (int64_t)ms * P1;
+    const TabInfo T = tabs[C.tab[s]];
+    const int64_t nq = (int64_t)T.nel * q;
+    const double* bv = vals + T.val_off;
+    const double* bd = bv + nq * P1;
+    const double* w = qw + T.qp_off;
+    for (int idx = threadIdx.x; idx < ms * P1; idx += 256) {
+        const int i = idx / P1, kk = idx % P1, j = i - kk, gi = i + 1, gj = j + 1;
+        double mv = 0.0, kv = 0.0;
+        if (j >= 0) {
+            const int num = gi - p;   // gi >= gj
+            const int elo = num <= 0 ? 0 : (num + mu - 1) / mu;
+            const int ehi = min(gj / mu, T.nel - 1);
+            for (int e = elo; e <= ehi; ++e) {
+                const int a = gi - e * mu, bb = gj - e * mu;
+                for (int g = 0; g < q; ++g) {
+                    const int64_t base = ((int64_t)e * q + g) * P1;
+                    const double wg = w[(int64_t)e * q + g];
+                    mv += wg * bv[base + a] * bv[base + bb];
+                    kv += wg * bd[base + a] * bd[base + bb];
+                }
+            }
+        }
+        Kb[idx] = kv;
+        Mb[idx] = mv;
+    }
+}
+
+// one banded Cholesky per line, c_s K_s + mu_L M_s = F F^T with
+// mu_L = sum over the other axes of c_k lambda_k(line): one thread per line,
+// the last p factor rows in registers.  Stored per row i: [0] = 1 / F(i,i),
+// [k] = F(i, i-k), k = 1..p.  Grid (line blocks, component).
+template <int D>
+__global__ void __launch_bounds__(64)
+k_fdl_factor(const CompInfo* __restrict__ comps, const int* __restrict__ list, int p,
+             const int64_t* __restrict__ loff, const double* __restrict__ dL, const double* __restrict__ ckg,
+             const int64_t* __restrict__ fdl_off, double* __restrict__ fdl) {
+    const int c = list[blockIdx.y];
+    const CompInfo& C = comps[c];
+    const int P1 = p + 1, s = C.ax[D - 1], ms = C.m[s];
+    int nlines = 1;
+#pragma unroll
+    for (int o = 0; o < D - 1; ++o) nlines *= C.m[C.ax[o]];
+    const int L = blockIdx.x * 64 + threadIdx.x;
+    if (L >= nlines) return;
+    double muL = 0.0;
+    {
+        int rem = L;
+#pragma unroll
+        for (int o = D - 2; o >= 0; --o) {
+            const int ax = C.ax[o], io = rem % C.m[ax];
+            rem /= C.m[ax];
+            muL += ckg[c * MAXD + ax] * dL[loff[C.tab[ax]] + io];
+        }
+    }
+    const double cs = ckg[c * MAXD + s];
+    const double* Kb = fdl + fdl_off[c];
+    const double* Mb = Kb + (int64_t)ms * P1;
+    double* F = fdl + fdl_off[c] + 2 * (int64_t)ms * P1 + (int64_t)L * ms * P1;
+    double Fw[PM][PM + 1], Rw[PM];   // Fw[d][k] = F(i-1-d, i-1-d-k)
+#pragma unroll
+    for (int d = 0; d < PM; ++d) {
+        Rw[d] = 0.0;
+#pragma unroll
+        for (int k = 0; k <= PM; ++k) Fw[d][k] = 0.0;
+    }
+    for (int i = 0; i < ms; ++i) {
+        double Fi[PM + 1];
+#pragma unroll
+        for (int k = 0; k <= PM; ++k) Fi[k] = 0.0;
+#pragma unroll
+        for (int kk = PM; kk >= 1; --kk) {   // F(i, j), j = i - kk, increasing j
+            if (kk <= p && kk <= i) {
+                double sv = cs * Kb[i * P1 + kk] + muL * Mb[i * P1 + kk];
+#pragma unroll
+                for (int ll = PM; ll > kk; --ll)   // l = i - ll < j
+                    if (ll <= p && ll <= i) sv -= Fi[ll] * Fw[kk - 1][ll - kk];
+                Fi[kk] = sv * Rw[kk - 1];
+            }
+        }
+        double dv = cs * Kb[i * P1] + muL * Mb[i * P1];
+#pragma unroll
+        for (int ll = PM; ll >= 1; --ll)
+            if (ll <= p && ll <= i) dv -= Fi[ll] * Fi[ll];
+        const double r = 1.0 / sqrt(dv);
+        F[i * P1] = r;
+#pragma unroll
+        for (int kk = 1; kk <= PM; ++kk)
+            if (kk <= p) F[i * P1 + kk] = Fi[kk];
+#pragma unroll
+        for (int d = PM - 1; d >= 1; --d) {
+            Rw[d] = Rw[d - 1];
+#pragma unroll
+            for (int k = 0; k <= PM; ++k) Fw[d][k] = Fw[d - 1][k];
+        }
+        Rw[0] = r;
+#pragma unroll
+        for (int k = 0; k <= PM; ++k) Fw[0][k] = Fi[k];
+    }
+}
 
 template <int D>
 __global__ void __launch_bounds__(FDL_THREADS, 1)
 k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, const int* __restrict__ slotoff,
-          const double* __restrict__ stencil, const double* __restrict__ rhs, const double* __restrict__ Gbuf,
-          const TabInfo* __restrict__ tabs, const double* __restrict__ vals, const double* __restrict__ qw,
-          int p, int mu, int q, const int64_t* __restrict__ uoff, const int64_t* __restrict__ loff,
-          const double* __restrict__ dU, const double* __restrict__ dL, const int64_t* __restrict__ fdl_off,
-          double* __restrict__ fdl, double* __restrict__ xg, double* __restrict__ rg, double* __restrict__ zg,
-          double* __restrict__ pg, double* __restrict__ qg, double* __restrict__ tg,
-          CgState* __restrict__ st, double* __restrict__ relres, double rtol2, int maxit) {
+          const double* __restrict__ stencil, const double* __restrict__ rhs, int p,
+          const int64_t* __restrict__ uoff, const double* __restrict__ dU, const double* __restrict__ ckg,
+          const int64_t* __restrict__ fdl_off, const double* __restrict__ fdl, double* __restrict__ xg,
+          double* __restrict__ rg, double* __restrict__ zg, double* __restrict__ pg, double* __restrict__ qg,
+          double* __restrict__ tg, CgState* __restrict__ st, double* __restrict__ relres, double rtol2,
+          int maxit) {
     __shared__ double red[FDL_THREADS / 32];
     const int c = list[blockIdx.x];
     const CompInfo& C = comps[c];
@@ -610,74 +763,7 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
     const double* b = rhs + C.vec_off;
     const double* val = stencil + C.mat_off;
     const int* offs = slotoff + C.so_off;
-    double* Kb = fdl + fdl_off[c];
-    double* Mb = Kb + (int64_t)ms * P1;
-    double* Fac = Mb + (int64_t)ms * P1;
-
-    // metric scale per axis (patch integral of G_kk)
-    double ck[D];
-    {
-        const double* Gc = Gbuf + C.qp_off;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const double* g = Gc + (int64_t)sym_index(D, k, k) * C.nqp;
-            double sacc = 0.0;
-            for (int64_t i = tid; i < C.nqp; i += FDL_THREADS) sacc += g[i];
-            ck[k] = fd_block_sum(sacc, red);
-        }
-    }
-    // banded interior K_s, M_s of the stream axis (lower band, k = i - j)
-    {
-        const TabInfo T = tabs[C.tab[s]];
-        const int64_t nq = (int64_t)T.nel * q;
-        const double* bv = vals + T.val_off;
-        const double* bd = bv + nq * P1;
-        const double* w = qw + T.qp_off;
-        for (int idx = tid; idx < ms * P1; idx += FDL_THREADS) {
-            const int i = idx / P1, kk = idx % P1, j = i - kk, gi = i + 1, gj = j + 1;
-            double mv = 0.0, kv = 0.0;
-            if (j >= 0) {
-                const int num = gi - p;   // gi >= gj
-                const int elo = num <= 0 ? 0 : (num + mu - 1) / mu;
-                const int ehi = min(gj / mu, T.nel - 1);
-                for (int e = elo; e <= ehi; ++e) {
-                    const int a = gi - e * mu, bb = gj - e * mu;
-                    for (int g = 0; g < q; ++g) {
-                        const int64_t base = ((int64_t)e * q + g) * P1;
-                        const double wg = w[(int64_t)e * q + g];
-                        mv += wg * bv[base + a] * bv[base + bb];
-                        kv += wg * bd[base + a] * bd[base + bb];
-                    }
-                }
-            }
-            Kb[idx] = kv;
-            Mb[idx] = mv;
-        }
-    }
-    __syncthreads();
-    // one banded Cholesky per line: c_s K_s + mu M_s = F F^T
-    for (int L = tid; L < nlines; L += FDL_THREADS) {
-        double muL = 0.0;
-        int rem = L;
-        for (int o = NO - 1; o >= 0; --o) {
-            const int io = rem % om[o];
-            rem /= om[o];
-            muL += ck[oax[o]] * dL[loff[C.tab[oax[o]]] + io];
-        }
-        double* F = Fac + (int64_t)L * ms * P1;
-        for (int i = 0; i < ms; ++i) {
-            for (int kk = min(p, i); kk >= 1; --kk) {   // F(i, j), j = i - kk, increasing j
-                const int j = i - kk;
-                double sv = ck[s] * Kb[i * P1 + kk] + muL * Mb[i * P1 + kk];
-                for (int l = max(0, i - p); l < j; ++l) sv -= F[i * P1 + (i - l)] * F[j * P1 + (j - l)];
-                F[i * P1 + kk] = sv / F[j * P1];
-            }
-            double dv = ck[s] * Kb[i * P1] + muL * Mb[i * P1];
-            for (int l = max(0, i - p); l < i; ++l) dv -= F[i * P1 + (i - l)] * F[i * P1 + (i - l)];
-            F[i * P1] = sqrt(dv);
-        }
-    }
-    __syncthreads();
+    const double* Fac = fdl + fdl_off[c] + 2 * (int64_t)ms * P1;   // k_fdl_factor
 
     // mode product over other axis o (global buffers)
     auto mode = [&](const double* src, double* dst, int o, bool trans) {
@@ -695,19 +781,48 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
         }
         __syncthreads();
     };
-    auto line_solve = [&](double* y) {   // in place, every line L = rows [L*ms, (L+1)*ms)
+    // in place, every line L = rows [L*ms, (L+1)*ms): forward then backward
+    // banded substitution; the last p results stay in registers and the next
+    // row's inputs are loaded one row ahead (the chain is FMA latency only)
+    auto line_solve = [&](double* y) {
         for (int L = tid; L < nlines; L += FDL_THREADS) {
             const double* F = Fac + (int64_t)L * ms * P1;
             double* yl = y + (int64_t)L * ms;
+            double yw[PM] = {};   // yw[d] = y(i-1-d)
+            double nf[PM + 1], ny = yl[0];
+#pragma unroll
+            for (int k = 0; k <= PM; ++k) nf[k] = k <= p ? F[k] : 0.0;
             for (int i = 0; i < ms; ++i) {
-                double sv = yl[i];
-                for (int j = max(0, i - p); j < i; ++j) sv -= F[i * P1 + (i - j)] * yl[j];
-                yl[i] = sv / F[i * P1];
+                double f[PM + 1], sv = ny;
+#pragma unroll
+                for (int k = 0; k <= PM; ++k) f[k] = nf[k];
+                if (i + 1 < ms) {
+                    ny = yl[i + 1];
+#pragma unroll
+                    for (int k = 0; k <= PM; ++k) nf[k] = k <= p ? F[(i + 1) * P1 + k] : 0.0;
+                }
+#pragma unroll
+                for (int k = PM; k >= 1; --k)
+                    if (k <= p && k <= i) sv -= f[k] * yw[k - 1];
+                sv *= f[0];
+                yl[i] = sv;
+#pragma unroll
+                for (int d = PM - 1; d >= 1; --d) yw[d] = yw[d - 1];
+                yw[0] = sv;
             }
+            // backward: y(i) = (y(i) - sum_k F(i+k, i) y(i+k)) / F(i,i); yw[d] = y(i+1+d)
+#pragma unroll
+            for (int d = 0; d < PM; ++d) yw[d] = 0.0;
             for (int i = ms - 1; i >= 0; --i) {
                 double sv = yl[i];
-                for (int j = i + 1; j <= min(ms - 1, i + p); ++j) sv -= F[j * P1 + (j - i)] * yl[j];
-                yl[i] = sv / F[i * P1];
+#pragma unroll
+                for (int k = PM; k >= 1; --k)
+                    if (k <= p && i + k < ms) sv -= F[(i + k) * P1 + k] * yw[k - 1];
+                sv *= F[i * P1];
+                yl[i] = sv;
+#pragma unroll
+                for (int d = PM - 1; d >= 1; --d) yw[d] = yw[d - 1];
+                yw[0] = sv;
             }
         }
         __syncthreads();
@@ -734,11 +849,17 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
             const int rb = fd_row_base(C, D, row);
             double y0 = 0.0, y1 = 0.0;
             int tt = 0;
-            for (; tt + 1 < NS; tt += 2) {
-                y0 += __ldg(val + (size_t)tt * R + row) * v[rb + offs[tt]];
-                y1 += __ldg(val + (size_t)(tt + 1) * R + row) * v[rb + offs[tt + 1]];
+            for (; tt + 7 < NS; tt += 8) {   // 8 independent stencil loads in flight
+                double vv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) vv[u] = __ldg(val + (size_t)(tt + u) * R + row);
+#pragma unroll
+                for (int u = 0; u < 8; u += 2) {
+                    y0 += vv[u] * v[rb + offs[tt + u]];
+                    y1 += vv[u + 1] * v[rb + offs[tt + u + 1]];
+                }
             }
-            if (tt < NS) y0 += __ldg(val + (size_t)tt * R + row) * v[rb + offs[tt]];
+            for (; tt < NS; ++tt) y0 += __ldg(val + (size_t)tt * R + row) * v[rb + offs[tt]];
             out[row] = y0 + y1;
         }
         __syncthreads();
@@ -806,11 +927,11 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
 cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
     const int n = (int)h->fdl_comps.size();
     if (n == 0) return cudaSuccess;
-#define LAUNCH_FDL(DD)                                                                                     \
-    k_pcg_fdl<DD><<<(unsigned)n, FDL_THREADS, 0, h->stream>>>(                                             \
-        h->d_comps, h->d_fdl_list, h->d_slotoff, h->d_stencil, h->d_rhs, h->d_G, h->d_tabs, h->d_tabvals,  \
-        h->d_qw, h->p, h->mu, h->q, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_fdl_off, h->d_fdl, \
-        h->d_x, h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_cg, h->d_relres, rtol * rtol, maxit)
+#define LAUNCH_FDL(DD)                                                                                   \
+    k_pcg_fdl<DD><<<(unsigned)n, FDL_THREADS, 0, h->stream>>>(                                           \
+        h->d_comps, h->d_fdl_list, h->d_slotoff, h->d_stencil, h->d_rhs, h->p, h->d_fd_uoff, h->d_fdU,  \
+        h->d_ck, h->d_fdl_off, h->d_fdl, h->d_x, h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_cg,       \
+        h->d_relres, rtol * rtol, maxit)
     if (h->d == 1) { LAUNCH_FDL(1); }
     else if (h->d == 2) { LAUNCH_FDL(2); }
     else { LAUNCH_FDL(3); }
@@ -819,12 +940,48 @@ cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
     return cudaGetLastError();
 }
 
+// FD set-up after the metric (stream s, forked from the main stream after
+// k_metric, joined before the solve): c_k of every FD / line-FD component,
+// then the line-FD stream-axis bands and per-line factors
+cudaError_t launch_fd_setup(Handle* h, cudaStream_t s) {
+    const int nf = (int)h->fd_comps.size(), nl = (int)h->fdl_comps.size();
+    if (nf + nl == 0) return cudaSuccess;
+    const dim3 g1((unsigned)(nf + nl), (unsigned)h->d);
+#define LAUNCH_SCALE(DD)                                                                              \
+    k_fd_metric_scale<DD><<<g1, 256, 0, s>>>(h->d_comps, h->d_fdlist, nf, h->d_fdl_list, h->d_G, h->d_ck)
+    if (h->d == 1) { LAUNCH_SCALE(1); }
+    else if (h->d == 2) { LAUNCH_SCALE(2); }
+    else { LAUNCH_SCALE(3); }
+#undef LAUNCH_SCALE
+    h->launches[0]++;
+    if (nl == 0) return cudaGetLastError();
+    int maxlines = 1;
+    for (int c : h->fdl_comps) {
+        const CompInfo& C = h->comps[c];
+        int lines = 1;
+        for (int o = 0; o < h->d - 1; ++o) lines *= C.m[C.ax[o]];
+        maxlines = std::max(maxlines, lines);
+    }
+    const dim3 g3((unsigned)((maxlines + 63) / 64), (unsigned)nl);
+#define LAUNCH_FACT(DD)                                                                                     \
+    k_fdl_bands<DD><<<(unsigned)nl, 256, 0, s>>>(h->d_comps, h->d_fdl_list, h->d_tabs, h->d_tabvals,       \
+                                                 h->d_qw, h->p, h->mu, h->q, h->d_fdl_off, h->d_fdl);     \
+    k_fdl_factor<DD><<<g3, 64, 0, s>>>(h->d_comps, h->d_fdl_list, h->p, h->d_fd_loff, h->d_fdL, h->d_ck, \
+                                       h->d_fdl_off, h->d_fdl)
+    if (h->d == 1) { LAUNCH_FACT(1); }
+    else if (h->d == 2) { LAUNCH_FACT(2); }
+    else { LAUNCH_FACT(3); }
+#undef LAUNCH_FACT
+    h->launches[0] += 2;
+    return cudaGetLastError();
+}
+
 size_t fd_eigen_smem() { return sizeof(double) * (3 * FD_MMAX * FD_LD + FD_TAB_MAX); }
 
 size_t fd_comp_smem(const CompInfo& C, int d) {
     int64_t u = 0, l = 0;
     for (int k = 0; k < d; ++k) { u += (int64_t)C.m[k] * C.m[k]; l += C.m[k]; }
-    return sizeof(double) * (size_t)(6 * C.rows + 2 * C.halo + u + l) + sizeof(int) * (size_t)(C.nslots + 1);
+    return sizeof(double) * (size_t)(6 * C.rows + 2 * C.halo + u + l + FD_THREADS) + sizeof(int) * (size_t)(C.nslots + 1);
 }
 
 cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s) {
@@ -866,7 +1023,7 @@ cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit) {
     if (e != cudaSuccess) return e;                                                                   \
     k_pcg_fd<DD><<<(unsigned)n, FD_THREADS, smem, h->stream>>>(                                       \
         h->d_comps, h->d_fdlist, h->d_slotoff, h->d_stencil, h->d_rhs, h->d_G, h->d_fd_uoff,          \
-        h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_x, h->d_cg, h->d_relres, rtol * rtol, maxit)
+        h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_ck, h->d_x, h->d_cg, h->d_relres, rtol * rtol, maxit)
     if (h->d == 1) { LAUNCH_FD(1); }
     else if (h->d == 2) { LAUNCH_FD(2); }
     else { LAUNCH_FD(3); }

@@ -81,7 +81,8 @@ __global__ void k_basis_tables(const TabInfo* __restrict__ tabs, int ntab,
 // ---- fused geometry -> metric + load --------------------------------------
 // One thread per (component, quadrature point), storage order (s, a, b).
 template <int D>
-__global__ void k_metric(const CompInfo* __restrict__ comps, int ncomp,
+__global__ void __launch_bounds__(256, 3)
+k_metric(const CompInfo* __restrict__ comps, int ncomp,
                          const int64_t* __restrict__ qp_cum, const TabInfo* __restrict__ tabs,
                          const double* __restrict__ qx, const double* __restrict__ qw,
                          const double* __restrict__ geob, const int* __restrict__ geofirst,
@@ -97,21 +98,31 @@ __global__ void k_metric(const CompInfo* __restrict__ comps, int ncomp,
         if (qp_cum[mid] <= gid) lo = mid; else hi = mid;
     }
     const CompInfo& C = comps[lo];
-    int64_t lin = gid - qp_cum[lo];
-    const GeoInfo Gi = *geo;
-    double xi[D], w = 1.0;
+    // per-component quadrature index < 2^31 (a component with more points
+    // would need > 16 GB of metric): 32-bit index arithmetic
+    const unsigned lin = (unsigned)(gid - qp_cum[lo]);
+    double w = 1.0;
     const double* bv[D];
     int first[D];
+    unsigned Qa[D];
+    int64_t toff[D], goff[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        int64_t Nq = (int64_t)C.nel[k] * q;
-        int64_t Qk = (lin / C.qs[k]) % Nq;
+        const unsigned Nq = (unsigned)C.nel[k] * (unsigned)q;
+        Qa[k] = (lin / (unsigned)C.qs[k]) % Nq;
         const TabInfo& T = tabs[C.tab[k]];
-        xi[k] = qx[T.qp_off + Qk];
-        double wk = qw[T.qp_off + Qk];
+        toff[k] = T.qp_off;
+        goff[k] = T.geo_off;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        first[k] = geofirst[goff[k] + Qa[k]];
+        bv[k] = geob + (goff[k] + Qa[k]) * (2 * GEO_PMAX);
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const double wk = qw[toff[k] + Qa[k]];
         w = (k == 0) ? wk : __dmul_rn(w, wk);   // _outer_product, assembly.py:186-190
-        bv[k] = geob + (T.geo_off + Qk) * (2 * GEO_PMAX);
-        first[k] = geofirst[T.geo_off + Qk];
     }
     // homogeneous contraction (geometry.py:114, 124) over active functions
     double hom[D + 1], dh[D][D + 1];
@@ -121,16 +132,19 @@ __global__ void k_metric(const CompInfo* __restrict__ comps, int ncomp,
 #pragma unroll
         for (int m = 0; m < D; ++m) dh[m][c] = 0.0;
     }
-    int c0 = Gi.deg[0] + 1, c1 = D > 1 ? Gi.deg[1] + 1 : 1, c2 = D > 2 ? Gi.deg[2] + 1 : 1;
+    int gn[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) gn[k] = geo->n[k];
+    int c0 = geo->deg[0] + 1, c1 = D > 1 ? geo->deg[1] + 1 : 1, c2 = D > 2 ? geo->deg[2] + 1 : 1;
     for (int i = 0; i < c0; ++i)
         for (int j = 0; j < c1; ++j)
             for (int l = 0; l < c2; ++l) {
                 int idx[3] = {i, j, l};
-                int64_t L = 0;
+                int L = 0;
                 double v[D], dv[D];
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                    L = L * Gi.n[k] + (first[k] + idx[k]);
+                    L = L * gn[k] + (first[k] + idx[k]);
                     v[k] = bv[k][idx[k]];
                     dv[k] = bv[k][GEO_PMAX + idx[k]];
                 }

@@ -220,6 +220,7 @@ cudaError_t launch_solve_prologue(Handle* h);
 cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s);
 cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit);
 cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit);
+cudaError_t launch_fd_setup(Handle* h, cudaStream_t s);
 size_t fd_comp_smem(const CompInfo& C, int d);
 cudaError_t launch_status(Handle* h);
 cudaError_t launch_expand(Handle* h);
