@@ -399,16 +399,37 @@ def run_sgiga(args, cfg):
     pts_pinned = pin.numpy()
     for _ in range(max(args.warmup, 3)):
         sess.run(pts_pinned)
+    # (a) latency: one synchronous call per step (H2D points, pass, D2H values)
     if ws > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         v_e2e = sess.run(pts_pinned)
-    e2e_s = (time.perf_counter() - t0) / args.steps
+    sync_s = (time.perf_counter() - t0) / args.steps
+    # (b) throughput (the e2e value): the same pass submitted back to back on
+    # page-locked host buffers -- every step still copies its points H2D and
+    # its values D2H inside the pass; one wait at the end, then every step's
+    # output is checked bitwise against the synchronous call
+    async_ok = hasattr(sess, "submit")
+    if async_ok:
+        outs = [torch.empty(npts, dtype=torch.float64, pin_memory=True) for _ in range(args.steps)]
+        for k in range(max(args.warmup, 3)):
+            sess.submit(pts_pinned, outs[k % len(outs)].numpy())
+        sess.wait()
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            sess.submit(pts_pinned, outs[k].numpy())
+        sess.wait()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        async_ok = all(np.array_equal(o.numpy(), v_e2e) for o in outs)
+    else:
+        e2e_s = sync_s
     if ws > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([e2e_s, sync_s], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s, sync_s = float(t[0].item()), float(t[1].item())
     h2d = pts_h.nbytes              # the problem descriptor is uploaded once, at session open
     desc_bytes = sess.h2d_input_bytes
     d2h = npts * 8 + n_comp * (4 + 8) + 64
@@ -438,9 +459,14 @@ def run_sgiga(args, cfg):
             "dof_per_s": ws * dofs / (ms_per_step * 1e-3),
             "e2e": {"value": ws * n_comp / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s,
+                    "mode": ("pipelined: PlanSession.submit per step (pinned points H2D + pass + values D2H), "
+                             "one wait, every step's output checked bitwise; no L2 flush (warm, as a user sees it)")
+                    if hasattr(sess, "submit") else "synchronous PlanSession.run per step",
+                    "all_steps_match": bool(async_ok) if hasattr(sess, "submit") else None,
+                    "sync_ms_per_step": 1e3 * sync_s, "sync_value": ws * n_comp / sync_s,
                     "matches_device_run_bitwise": consistent,
                     "descriptor_bytes_uploaded_at_open": int(desc_bytes),
-                    "path": "PlanSession.run -> sgiga_run (pinned host points in, host values out)"},
+                    "path": "PlanSession.submit -> sgiga_run_host_async (pinned host points in, pinned host values out); sync: PlanSession.run -> sgiga_run"},
             "roofline": roofline,
             "rooflines": {k: {kk: (float(vv) if isinstance(vv, (np.floating, float)) else vv) for kk, vv in g.items()}
                           for k, g in groups.items()},

@@ -173,6 +173,15 @@ int sgiga_run(sgiga_handle* h, double rtol, int32_t maxit, const double* pts,
 int sgiga_run_async(sgiga_handle* h, double rtol, int32_t maxit, const double* pts_dev,
                     int64_t npts, double* out_dev);
 int sgiga_run_wait(sgiga_handle* h, int32_t* iters_out, double* relres_out);
+/* Asynchronous end-to-end pass with HOST buffers: the page-locked points are
+ * copied host->device inside the pass (point-sort side stream) and the
+ * combined values device->host into the page-locked output after the
+ * combine; returns after enqueueing.  Passes pipeline back to back (the
+ * host may submit pass k+1 while pass k runs); the output buffer of a pass
+ * must stay untouched until sgiga_run_wait, which reports the LAST pass.
+ * Same computation and result as sgiga_run(..., device = 0).            */
+int sgiga_run_host_async(sgiga_handle* h, double rtol, int32_t maxit, const double* pts_pinned,
+                         int64_t npts, double* out_pinned);
 
 /* Tensor grid variant: per-axis parameter arrays concatenated; vals has
  * prod(npts) entries (C order), grads (optional, may be NULL) prod*d.

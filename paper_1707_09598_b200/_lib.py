@@ -40,7 +40,7 @@ EXPORTED = (
     "sgiga_create", "sgiga_upload", "sgiga_batch_sizes", "sgiga_quad_points_physical",
     "sgiga_set_forcing_density", "sgiga_component_info", "sgiga_assemble", "sgiga_solve",
     "sgiga_coefficients", "sgiga_set_coefficients", "sgiga_combine_points", "sgiga_run",
-    "sgiga_run_async", "sgiga_run_wait",
+    "sgiga_run_async", "sgiga_run_wait", "sgiga_run_host_async",
     "sgiga_combine_grid", "sgiga_error_norms", "sgiga_subset_error_norms", "sgiga_export_csr", "sgiga_phase_stats",
     "sgiga_iterations", "sgiga_kernel_times", "sgiga_stream", "sgiga_destroy", "sgiga_last_error",
     "sgiga_device_count", "sgiga_local_poisson_systems",
@@ -101,6 +101,7 @@ def _declare(lib):
         "sgiga_run": ([VP, ct.c_double, ct.c_int32, VP, ct.c_int64, VP, ct.c_int32, P_I32, P_F64], ct.c_int),
         "sgiga_run_async": ([VP, ct.c_double, ct.c_int32, VP, ct.c_int64, VP], ct.c_int),
         "sgiga_run_wait": ([VP, P_I32, P_F64], ct.c_int),
+        "sgiga_run_host_async": ([VP, ct.c_double, ct.c_int32, VP, ct.c_int64, VP], ct.c_int),
         "sgiga_combine_grid": ([VP, P_F64, P_I64, ct.c_int32, P_F64, P_F64], ct.c_int),
         "sgiga_error_norms": ([VP, P_F64, P_F64, P_I64, ct.c_int32, P_F64], ct.c_int),
         "sgiga_subset_error_norms": ([VP, P_F64, P_F64, P_I64, ct.c_int32, P_I32, P_F64, ct.c_int32, P_F64], ct.c_int),

@@ -967,6 +967,34 @@ int sgiga_run_async(sgiga_handle* hh, double rtol, int32_t maxit, const double* 
     return run_enqueue(h, rtol, maxit, pts_dev, npts, out_dev);
 }
 
+int sgiga_run_host_async(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts_pinned, int64_t npts,
+                         double* out_pinned) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || npts < 0 || (npts > 0 && (!pts_pinned || !out_pinned))) { set_error("null argument"); return SGIGA_ERR_VALUE; }
+    const double* dp = nullptr;
+    double* dout = nullptr;
+    int st;
+    if (npts > 0) {
+        for (const void* ptr : {static_cast<const void*>(pts_pinned), static_cast<const void*>(out_pinned)}) {
+            cudaPointerAttributes pa{};
+            const bool pinned = cudaPointerGetAttributes(&pa, ptr) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+            cudaGetLastError();
+            if (!pinned) { set_error("sgiga_run_host_async: points and output must be page-locked host memory"); return SGIGA_ERR_VALUE; }
+        }
+        if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
+        if ((st = ensure_scratch(&s_out, &s_out_cap, (size_t)npts))) return st;
+        dp = s_pts;
+        dout = s_out;
+    }
+    // the H2D of the points runs on the point-sort side stream inside the pass
+    // (ordered after the previous pass's combine by the pass's fork event);
+    // the D2H of the values follows the combine on the handle's stream
+    if ((st = run_enqueue(h, rtol, maxit, dp, npts, dout, npts > 0 ? pts_pinned : nullptr))) return st;
+    if (npts > 0)
+        SG_CUDA(cudaMemcpyAsync(out_pinned, dout, sizeof(double) * npts, cudaMemcpyDeviceToHost, h->stream));
+    return SGIGA_OK;
+}
+
 int sgiga_run_wait(sgiga_handle* hh, int32_t* iters_out, double* relres_out) {
     Handle* h = reinterpret_cast<Handle*>(hh);
     if (!h) return SGIGA_ERR_VALUE;

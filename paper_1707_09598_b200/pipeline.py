@@ -206,6 +206,19 @@ class Batch:
         self._host_forcing_density()
         _lib.check(self.lib.sgiga_run_async(self.h, float(rtol), int(maxit), pts_ptr, int(npts), out_ptr))
 
+    def run_host_async(self, pts: np.ndarray, out: np.ndarray, rtol: float = 1e-13, maxit: int = 0):
+        """Enqueue one end-to-end pass with page-locked HOST buffers (H2D of
+        ``pts`` and D2H into ``out`` inside the pass) without synchronising;
+        ``out`` is valid after run_wait(), which reports the last pass."""
+        self._host_forcing_density()
+        if pts.ndim != 2 or pts.shape[1] != self.spec.d or out.shape != (pts.shape[0],):
+            raise ValueError(f"points must have shape (n, {self.spec.d}) and out shape (n,)")
+        if not (pts.flags.c_contiguous and out.flags.c_contiguous and pts.dtype == np.float64
+                and out.dtype == np.float64):
+            raise ValueError("points and out must be C-contiguous float64")
+        _lib.check(self.lib.sgiga_run_host_async(self.h, float(rtol), int(maxit), pts.ctypes.data,
+                                                 pts.shape[0], out.ctypes.data))
+
     def run_wait(self):
         n = self.n_comp
         it = np.zeros(n, dtype=np.int32)

@@ -168,6 +168,16 @@ class PlanSession:
     def run(self, points) -> np.ndarray:
         return self.batch.run(points, self.rtol)
 
+    def submit(self, points, out) -> None:
+        """Pipelined form of run(): enqueue a pass on page-locked host
+        buffers (``points`` in, combined values into ``out``) and return;
+        passes run back to back on the device.  ``wait()`` synchronises and
+        raises the reference's exceptions for the last submitted pass."""
+        self.batch.run_host_async(points, out, self.rtol)
+
+    def wait(self) -> None:
+        self.batch.run_wait()
+
     def close(self):
         self.batch.close()
 

@@ -414,6 +414,32 @@ def test_async_passes_match_synchronous_run():
         b.close()
 
 
+def test_host_async_passes_match_synchronous_run():
+    """PlanSession.submit x N (page-locked host points in, host values out,
+    passes in flight back to back) + wait == PlanSession.run, bitwise, for
+    every submitted pass; pageable buffers are refused."""
+    import torch
+    from paper_1707_09598_b200.scheduler import PlanSession
+    cfg = configs.get_config("cfg2")
+    sess = PlanSession(cfg.plan, cfg.problem, cfg.quad_points)
+    try:
+        pts = cfg.points(20000)
+        ref = sess.run(pts)
+        pin = torch.empty(pts.shape, dtype=torch.float64, pin_memory=True)
+        pin.copy_(torch.from_numpy(pts))
+        outs = [torch.full((pts.shape[0],), np.nan, dtype=torch.float64, pin_memory=True) for _ in range(6)]
+        for o in outs:   # direct, capture, replays
+            sess.submit(pin.numpy(), o.numpy())
+        sess.wait()
+        for o in outs:
+            assert np.array_equal(o.numpy(), ref)
+        with pytest.raises(ValueError):
+            sess.submit(pts, np.empty(pts.shape[0]))
+        assert np.array_equal(sess.run(pts), ref)
+    finally:
+        sess.close()
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
 def test_tiled_combine_matches_per_thread_kernel(name, monkeypatch):
     """k_combine_points_tiled == the one-thread-per-point kernel, bitwise,
