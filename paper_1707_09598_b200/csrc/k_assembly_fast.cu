@@ -77,7 +77,13 @@ struct FastCfg {
     static constexpr int NG = D * (D + 1) / 2 + 1;     // metric entries + load
     static constexpr int NPAIR = D * D;
     static constexpr int PPW = NX <= 16 ? 2 : 1;       // pairs per warp in stage 1
-    static constexpr int S1T = 32 * ((NPAIR + 1 + PPW - 1) / PPW);
+    // 3-D stage 1 works on 5 metric groups (+ the load unit): pairs that share
+    // a pair-table row of axis b are contracted by one lane from one row load,
+    // and (a,s) / (s,a) share one S1 slot (same metric entry, same row)
+    static constexpr bool GRP = D == 3 && P >= 5;       // grouped stage 1 (P = 4: one pair per unit measured faster)
+    static constexpr int NGRP = GRP ? 5 : NPAIR;
+    static constexpr int NU1 = NGRP + 1;
+    static constexpr int S1T = 32 * ((NU1 + PPW - 1) / PPW);
     // 3-D: three-stage software pipeline on disjoint thread groups -- in one
     // barrier interval G1 runs stage 1 of plane j, G2 stage 2 of plane j-1
     // and G3 stage 3 of plane j-2 (+ the row flushes); S1/SL1/S2 are double
@@ -91,7 +97,9 @@ struct FastCfg {
     // stage-2 outputs: 3-D -- one (s_a, s_b) block per pair (summed by stream
     // type in stage 3) + the load term; 2-D -- NT2 slots + load
     static constexpr int NI2 = (PIPE ? NPAIR : NT2) * WAB + 1;
-    static constexpr int S2T = PIPE ? 32 * ((NPAIR * WB + 1 + 31) / 32) : 0;   // one (pair, s_b) column each
+    static constexpr int S2C = PIPE && P >= 5 ? 2 : 1;  // stage-2 s_b columns per thread (register budget)
+    static constexpr int NSB2 = (WB + S2C - 1) / S2C;  // stage-2 column groups (s_b .. s_b + S2C - 1)
+    static constexpr int S2T = PIPE ? 32 * ((NPAIR * NSB2 + 1 + 31) / 32) : 0;   // one (pair, s_b pair) each
     static constexpr int S3T = PIPE ? 32 * ((WAB + P + 31) / 32) : 0;         // one (s_a, s_b) column / load row each
     static constexpr int NT = PIPE ? S1T + S2T + S3T : 352;
     // resident CTAs per SM (launch bounds)
@@ -105,7 +113,10 @@ struct FastCfg {
     static constexpr int RING = P;                     // alive rows of the accumulator ring
     static constexpr int nGw = NG * NB * NAP;          // one plane buffer
     static constexpr int sGw = (nGw + 15) & ~15;       // buffer stride (128-byte aligned TMA destination)
-    static constexpr int nS1 = NPAIR * NA * WB;
+    // S1 rows [pair][xa][S1W]: 3-D pads W to even so stage 2 reads two
+    // adjacent s_b columns with one 16-byte load
+    static constexpr int S1W = S2C == 2 ? ((W + 1) & ~1) : W;
+    static constexpr int nS1 = NPAIR * NA * (PIPE ? S1W : WB);
     // shared-memory layout (doubles)
     static constexpr int oGw = 0;                      // [NGB][NG][NB][NAP]
     // plane buffers: TMA -- prefetch distance GPD = 2 planes (three buffers,
@@ -307,7 +318,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     }
     // this thread's stage-2 item (one per thread: 4 W^2 + 1 <= NT)
     constexpr int NT2 = F::NT2, LOAD2 = NT2 * F::WAB;
-    static_assert(LOAD2 + 1 <= NT, "one stage-2 item per thread");
+    static_assert(F::PIPE || LOAD2 + 1 <= NT, "one stage-2 item per thread (2-D)");
     const int i2_it = tid;
     const bool i2_on = D >= 2 && i2_it < LOAD2 + 1, i2_load = i2_it == LOAD2;
     const int i2_slot = i2_it / F::WAB, i2_sab = i2_it % F::WAB;
@@ -341,13 +352,16 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         const int g2t = tid - S1T, g3t = tid - S1T - S2T;
         const int nplanes = (e_last - e_first + 1) * Q;
         // this G2 thread's stage-2 column: (pair, s_b) -> all s_a
-        const bool s2_on = inG2 && g2t < NPAIR * F::WB + 1, s2_load = g2t == NPAIR * F::WB;
-        const int s2_pr = g2t / F::WB, s2_sb = g2t % F::WB;
+        const bool s2_on = inG2 && g2t < NPAIR * F::NSB2 + 1, s2_load = g2t == NPAIR * F::NSB2;
+        const int s2_pr = g2t / F::NSB2, s2_sb = F::S2C * (g2t % F::NSB2);   // columns s2_sb .. + S2C - 1
         int s2_sp = 0, s2_ta = 0;   // S1 / Ta offsets of the pair
 #pragma unroll
         for (int pr = 0; pr < NPAIR; ++pr)
             if (pr == s2_pr) {
-                s2_sp = pr * F::NA * W + s2_sb;
+                // (s, a) and (a, s) contract the same metric entry with the same
+                // b-row: stage 1 writes the (a, s) slot only
+                const int prs = F::GRP && pr == s * D + ka ? ka * D + s : pr;
+                s2_sp = prs * F::NA * F::S1W + s2_sb;
                 s2_ta = tap[pr] * F::NA * F::RP;
             }
         // stage 3 sums the pair blocks of each stream type (fixed pair order):
@@ -411,22 +425,35 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     double* S1w = S1 + (j & 1) * F::nS1;
                     const int half = F::PPW == 2 ? (lane >> 4) : 0;
                     const int xa = (dbg & 1) ? 32 : (F::PPW == 2 ? (lane & 15) : lane);
-                    const int prr = warp * F::PPW + half;
-                    if (prr < NPAIR && xa < F::NA) {
-                        const int gidx = sym_index(D, prr / D, prr % D);
-                        const int tb = 2 * ((prr / D) == kb) + ((prr % D) == kb);
-                        double acc[W];
-#pragma unroll
-                        for (int q2 = 0; q2 < W; ++q2) acc[q2] = 0.0;
-                        const double* gcol = Gw + gidx * F::NB * F::NAP + xa;
+                    const int unit = warp * F::PPW + half;
+                    const int prr = unit < F::NGRP ? 0 : (unit == F::NGRP ? NPAIR : NPAIR + 1);   // load unit -> NPAIR
+                    if (unit < F::NGRP && xa < F::NA) {
+                        // groups in axis roles (a = ka, b = kb, s): {aa, ss}, {as}, {ab, sb},
+                        // {ba, bs}, {bb}; both pairs of a group have the same b-type
+                        int m0 = unit / D, n0 = unit % D, m1 = -1, n1 = -1;
+                        if constexpr (F::GRP) switch (unit) {
+                            case 0: m0 = ka; n0 = ka; m1 = s; n1 = s; break;
+                            case 1: m0 = ka; n0 = s; break;
+                            case 2: m0 = ka; n0 = kb; m1 = s; n1 = kb; break;
+                            case 3: m0 = kb; n0 = ka; m1 = kb; n1 = s; break;
+                            default: m0 = kb; n0 = kb; break;
+                        }
+                        const bool two = m1 >= 0;
+                        const int tb = 2 * (m0 == kb) + (n0 == kb);
+                        const double* gcol0 = Gw + sym_index(D, m0, n0) * F::NB * F::NAP + xa;
+                        const double* gcol1 = Gw + (two ? sym_index(D, m1, n1) : 0) * F::NB * F::NAP + xa;
                         const double* tr = Tb + tb * F::NB * F::RP;
+                        double acc[W], acd[W];
+#pragma unroll
+                        for (int q2 = 0; q2 < W; ++q2) acc[q2] = acd[q2] = 0.0;
 #pragma unroll
                         for (int t = 0; t < P; ++t) {
                             if (t < tb_lo || t >= tb_hi) continue;
 #pragma unroll
                             for (int g2 = 0; g2 < Q; ++g2) {
                                 const int x = t * Q + g2;
-                                const double gv = gcol[x * F::NAP];
+                                const double gv = gcol0[x * F::NAP];
+                                const double gw = two ? gcol1[x * F::NAP] : 0.0;
                                 double tv[F::RP];   // warp-uniform row: RP/2 broadcast 16-byte loads
 #pragma unroll
                                 for (int k2 = 0; k2 < F::RP / 2; ++k2) {
@@ -435,12 +462,20 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                     tv[2 * k2 + 1] = v2.y;
                                 }
 #pragma unroll
-                                for (int k = 0; k < P; ++k) acc[t + k] += gv * tv[k];
+                                for (int k = 0; k < P; ++k) {
+                                    acc[t + k] += gv * tv[k];
+                                    if (two) acd[t + k] += gw * tv[k];
+                                }
                             }
                         }
-                        double* out = S1w + (prr * F::NA + xa) * W;
+                        double* out = S1w + ((m0 * D + n0) * F::NA + xa) * F::S1W;
 #pragma unroll
                         for (int q2 = 0; q2 < W; ++q2) out[q2] = acc[q2];
+                        if (two) {
+                            double* o1 = S1w + ((m1 * D + n1) * F::NA + xa) * F::S1W;
+#pragma unroll
+                            for (int q2 = 0; q2 < W; ++q2) o1[q2] = acd[q2];
+                        }
                     } else if (prr == NPAIR && xa < F::NA) {   // load: SL1 = sum_xb L phiB
                         const double* gcol = Gw + (F::NG - 1) * F::NB * F::NAP + xa;
                         double acc = 0.0;
@@ -461,8 +496,9 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                         for (int x = 0; x < F::NA; ++x) acc += sl[x] * phiA[x];
                         S2w[F::NI2 - 1] = acc;
                     } else if (s2_on) {
-                        // S2[pair][s_a][s_b] = sum_xa S1[pair][xa][s_b] Ta[xa][s_a - t(xa)];
-                        // even / odd points in two accumulator sets (shorter chains)
+                        // S2[pair][s_a][s_b] = sum_xa S1[pair][xa][s_b] Ta[xa][s_a - t(xa)],
+                        // two adjacent s_b columns per thread: one 16-byte S1 load and
+                        // one pair-table row feed 2P FMAs
                         double acc[W], acd[W];
 #pragma unroll
                         for (int q2 = 0; q2 < W; ++q2) acc[q2] = acd[q2] = 0.0;
@@ -474,7 +510,9 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 #pragma unroll
                             for (int g2 = 0; g2 < Q; ++g2) {
                                 const int xa = t * Q + g2;
-                                const double v = sp[xa * W];
+                                double2 v;
+                                if constexpr (F::S2C == 2) v = *reinterpret_cast<const double2*>(sp + xa * F::S1W);
+                                else v.x = sp[xa * F::S1W];
                                 double tv[F::RP];
 #pragma unroll
                                 for (int k2 = 0; k2 < F::RP / 2; ++k2) {
@@ -484,14 +522,29 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                 }
 #pragma unroll
                                 for (int k = 0; k < P; ++k) {
-                                    if (xa & 1) acd[t + k] += v * tv[k];
-                                    else acc[t + k] += v * tv[k];
+                                    if constexpr (F::S2C == 2) {
+                                        acc[t + k] += v.x * tv[k];
+                                        acd[t + k] += v.y * tv[k];
+                                    } else if (xa & 1) {   // one column: even / odd points in two chains
+                                        acd[t + k] += v.x * tv[k];
+                                    } else {
+                                        acc[t + k] += v.x * tv[k];
+                                    }
                                 }
                             }
                         }
                         double* o2 = S2w + s2_pr * F::WAB + s2_sb;
+                        if constexpr (F::S2C == 1) {
 #pragma unroll
-                        for (int sa = 0; sa < W; ++sa) o2[sa * F::WB] = acc[sa] + acd[sa];
+                            for (int sa = 0; sa < W; ++sa) o2[sa * F::WB] = acc[sa] + acd[sa];
+                        } else {
+#pragma unroll
+                            for (int sa = 0; sa < W; ++sa) o2[sa * F::WB] = acc[sa];
+                        }
+                        if (F::S2C == 2 && s2_sb + 1 < F::WB) {
+#pragma unroll
+                            for (int sa = 0; sa < W; ++sa) o2[sa * F::WB + 1] = acd[sa];
+                        }
                     }
                 }
             } else {
