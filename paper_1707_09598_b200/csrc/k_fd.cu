@@ -23,6 +23,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "handle.cuh"
 
 namespace sgiga {
@@ -731,7 +733,7 @@ k_fdl_factor(const CompInfo* __restrict__ comps, const int* __restrict__ list, i
 }
 
 template <int D>
-__global__ void __launch_bounds__(FDL_THREADS, 1)
+__global__ void __launch_bounds__(FDL_THREADS, 2)
 k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, const int* __restrict__ slotoff,
           const double* __restrict__ stencil, const double* __restrict__ rhs, int p,
           const int64_t* __restrict__ uoff, const double* __restrict__ dU, const double* __restrict__ ckg,
@@ -739,10 +741,38 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
           double* __restrict__ rg, double* __restrict__ zg, double* __restrict__ pg, double* __restrict__ qg,
           double* __restrict__ tg, CgState* __restrict__ st, double* __restrict__ relres, double rtol2,
           int maxit) {
-    __shared__ double red[FDL_THREADS / 32];
-    const int c = list[blockIdx.x];
+    // one thread-block cluster of K CTAs per component: rows, lines and
+    // vector work split over the K*FDL_THREADS threads, phases separated by
+    // cluster barriers (release / acquire: the global-memory vectors written
+    // by one CTA are visible to the others after it), dot products reduced
+    // through distributed shared memory in fixed rank order
+    namespace cgs = cooperative_groups;
+    cgs::cluster_group cluster = cgs::this_cluster();
+    __shared__ double red[FDL_THREADS / 32], cpart[2];
+    __shared__ double lsF[FDL_THREADS / 32][32 * (PM + 1)], lsy[FDL_THREADS / 32][32];
+    const int K = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+    const int c = list[blockIdx.x / K];
     const CompInfo& C = comps[c];
     const int R = (int)C.rows, NS = (int)C.nslots, tid = threadIdx.x, P1 = p + 1;
+    const int gt = rank * FDL_THREADS + tid, GT = K * FDL_THREADS;
+    int slot = 0;
+    auto csum = [&](double v) -> double {   // cluster-wide fixed-order sum
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((tid & 31) == 0) red[tid >> 5] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int w = 0; w < FDL_THREADS / 32; ++w) sacc += red[w];
+            cpart[slot] = sacc;
+        }
+        cluster.sync();
+        double tot = 0.0;
+        for (int r = 0; r < K; ++r) tot += *cluster.map_shared_rank(&cpart[slot], r);
+        slot ^= 1;
+        return tot;
+    };
     const int s = C.ax[D - 1], ms = C.m[s];
     constexpr int NO = D - 1;                      // other axes: C.ax[0 .. D-2]
     int oax[NO > 0 ? NO : 1], om[NO > 0 ? NO : 1], ors[NO > 0 ? NO : 1];
@@ -769,7 +799,7 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
     auto mode = [&](const double* src, double* dst, int o, bool trans) {
         const int m = om[o], sr = ors[o];
         const double* U = dU + uoff[C.tab[oax[o]]];
-        for (int row = tid; row < R; row += FDL_THREADS) {
+        for (int row = gt; row < R; row += GT) {
             const int a = (row / sr) % m, base = row - a * sr;
             double acc = 0.0;
             if (trans) {
@@ -779,53 +809,91 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
             }
             dst[row] = acc;
         }
-        __syncthreads();
+        cluster.sync();
     };
     // in place, every line L = rows [L*ms, (L+1)*ms): forward then backward
-    // banded substitution; the last p results stay in registers and the next
-    // row's inputs are loaded one row ahead (the chain is FMA latency only)
+    // banded substitution, ONE WARP per line: the lanes stage 32 factor rows
+    // (and y) into shared memory -- the next 32 already in flight in
+    // registers -- while lane 0 runs the serial recurrence from shared memory
+    // with the last p results (forward) / the p pending column sums
+    // (backward, column-oriented) in registers
     auto line_solve = [&](double* y) {
-        for (int L = tid; L < nlines; L += FDL_THREADS) {
+        const int warp = tid >> 5, lane = tid & 31;
+        const int gw = rank * (FDL_THREADS / 32) + warp, GW = K * (FDL_THREADS / 32);
+        double* sF = lsF[warp];
+        double* sy = lsy[warp];
+        const int nch = (ms + 31) / 32;
+        for (int L = gw; L < nlines; L += GW) {
             const double* F = Fac + (int64_t)L * ms * P1;
             double* yl = y + (int64_t)L * ms;
-            double yw[PM] = {};   // yw[d] = y(i-1-d)
-            double nf[PM + 1], ny = yl[0];
+            double rf[PM + 1], ry = 0.0;
+            auto ld = [&](int i0) {
+                const int i = i0 + lane;
 #pragma unroll
-            for (int k = 0; k <= PM; ++k) nf[k] = k <= p ? F[k] : 0.0;
-            for (int i = 0; i < ms; ++i) {
-                double f[PM + 1], sv = ny;
+                for (int k = 0; k <= PM; ++k) rf[k] = (i < ms && k <= p) ? F[(int64_t)i * P1 + k] : 0.0;
+                ry = i < ms ? yl[i] : 0.0;
+            };
+            // forward: y(i) = (y(i) - sum_k F(i, i-k) y(i-k)) / F(i, i)
+            double yw[PM];
 #pragma unroll
-                for (int k = 0; k <= PM; ++k) f[k] = nf[k];
-                if (i + 1 < ms) {
-                    ny = yl[i + 1];
+            for (int k = 0; k < PM; ++k) yw[k] = 0.0;
+            ld(0);
+            for (int ch = 0; ch < nch; ++ch) {
+                const int i0 = ch * 32, n = min(32, ms - i0);
 #pragma unroll
-                    for (int k = 0; k <= PM; ++k) nf[k] = k <= p ? F[(i + 1) * P1 + k] : 0.0;
+                for (int k = 0; k <= PM; ++k) sF[lane * (PM + 1) + k] = rf[k];
+                sy[lane] = ry;
+                __syncwarp();
+                if (ch + 1 < nch) ld(i0 + 32);
+                if (lane == 0) {
+                    for (int ii = 0; ii < n; ++ii) {
+                        const int i = i0 + ii;
+                        double sv = sy[ii];
+#pragma unroll
+                        for (int k = PM; k >= 1; --k)
+                            if (k <= p && k <= i) sv -= sF[ii * (PM + 1) + k] * yw[k - 1];
+                        sv *= sF[ii * (PM + 1)];
+                        sy[ii] = sv;
+#pragma unroll
+                        for (int d = PM - 1; d >= 1; --d) yw[d] = yw[d - 1];
+                        yw[0] = sv;
+                    }
                 }
-#pragma unroll
-                for (int k = PM; k >= 1; --k)
-                    if (k <= p && k <= i) sv -= f[k] * yw[k - 1];
-                sv *= f[0];
-                yl[i] = sv;
-#pragma unroll
-                for (int d = PM - 1; d >= 1; --d) yw[d] = yw[d - 1];
-                yw[0] = sv;
+                __syncwarp();
+                if (lane < n) yl[i0 + lane] = sy[lane];
+                __syncwarp();
             }
-            // backward: y(i) = (y(i) - sum_k F(i+k, i) y(i+k)) / F(i,i); yw[d] = y(i+1+d)
+            // backward, column-oriented: acw[d] = pending sum_k F(i+k, i) y(i+k)
+            // of row i - d
+            double acw[PM];
 #pragma unroll
-            for (int d = 0; d < PM; ++d) yw[d] = 0.0;
-            for (int i = ms - 1; i >= 0; --i) {
-                double sv = yl[i];
+            for (int k = 0; k < PM; ++k) acw[k] = 0.0;
+            ld((nch - 1) * 32);
+            for (int ch = nch - 1; ch >= 0; --ch) {
+                const int i0 = ch * 32, n = min(32, ms - i0);
 #pragma unroll
-                for (int k = PM; k >= 1; --k)
-                    if (k <= p && i + k < ms) sv -= F[(i + k) * P1 + k] * yw[k - 1];
-                sv *= F[i * P1];
-                yl[i] = sv;
+                for (int k = 0; k <= PM; ++k) sF[lane * (PM + 1) + k] = rf[k];
+                sy[lane] = ry;
+                __syncwarp();
+                if (ch > 0) ld(i0 - 32);
+                if (lane == 0) {
+                    for (int ii = n - 1; ii >= 0; --ii) {
+                        const double sv = (sy[ii] - acw[0]) * sF[ii * (PM + 1)];
+                        sy[ii] = sv;
 #pragma unroll
-                for (int d = PM - 1; d >= 1; --d) yw[d] = yw[d - 1];
-                yw[0] = sv;
+                        for (int d = 0; d < PM - 1; ++d) acw[d] = acw[d + 1];
+                        acw[PM - 1] = 0.0;
+#pragma unroll
+                        for (int k = 1; k <= PM; ++k)
+                            if (k <= p) acw[k - 1] += sF[ii * (PM + 1) + k] * sv;
+                    }
+                }
+                __syncwarp();
+                if (lane < n) yl[i0 + lane] = sy[lane];
+                __syncwarp();
             }
         }
-        __syncthreads();
+        cluster.sync();
     };
     auto precond = [&]() {   // z = P^-1 r
         if constexpr (D == 3) {
@@ -839,13 +907,13 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
             line_solve(t);
             mode(t, z, 0, false);
         } else {
-            for (int i = tid; i < R; i += FDL_THREADS) z[i] = r[i];
-            __syncthreads();
+            for (int i = gt; i < R; i += GT) z[i] = r[i];
+            cluster.sync();
             line_solve(z);
         }
     };
     auto spmv = [&](const double* v, double* out) {   // out = A v (v halo-padded)
-        for (int row = tid; row < R; row += FDL_THREADS) {
+        for (int row = gt; row < R; row += GT) {
             const int rb = fd_row_base(C, D, row);
             double y0 = 0.0, y1 = 0.0;
             int tt = 0;
@@ -862,81 +930,103 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
             for (; tt < NS; ++tt) y0 += __ldg(val + (size_t)tt * R + row) * v[rb + offs[tt]];
             out[row] = y0 + y1;
         }
-        __syncthreads();
+        cluster.sync();
     };
 
     double bbl = 0.0;
-    for (int i = tid; i < R; i += FDL_THREADS) {
+    for (int i = gt; i < R; i += GT) {
         const double bi = b[i];
         x[i] = 0.0;
         r[i] = bi;
         bbl += bi * bi;
     }
-    const double bb = fd_block_sum(bbl, red);
+    const double bb = csum(bbl);
     int it = 0, conv = (bb == 0.0);
     if (!conv) {
         precond();
         double rzl = 0.0;
-        for (int i = tid; i < R; i += FDL_THREADS) { pp[i] = z[i]; rzl += r[i] * z[i]; }
-        double rz = fd_block_sum(rzl, red);
+        for (int i = gt; i < R; i += GT) { pp[i] = z[i]; rzl += r[i] * z[i]; }
+        double rz = csum(rzl);
         while (it < maxit) {
             spmv(pp, qq);
             double pql = 0.0;
-            for (int i = tid; i < R; i += FDL_THREADS) pql += pp[i] * qq[i];
-            const double alpha = rz / fd_block_sum(pql, red);
+            for (int i = gt; i < R; i += GT) pql += pp[i] * qq[i];
+            const double alpha = rz / csum(pql);
             double rrl = 0.0;
-            for (int i = tid; i < R; i += FDL_THREADS) {
+            for (int i = gt; i < R; i += GT) {
                 x[i] += alpha * pp[i];
                 const double ri = r[i] - alpha * qq[i];
                 r[i] = ri;
                 rrl += ri * ri;
             }
-            const double rr = fd_block_sum(rrl, red);
+            const double rr = csum(rrl);
             ++it;
             if (rr <= rtol2 * bb) { conv = 1; break; }
             precond();
             double rzl2 = 0.0;
-            for (int i = tid; i < R; i += FDL_THREADS) rzl2 += r[i] * z[i];
-            const double rzn = fd_block_sum(rzl2, red);
+            for (int i = gt; i < R; i += GT) rzl2 += r[i] * z[i];
+            const double rzn = csum(rzl2);
             const double beta = rzn / rz;
             rz = rzn;
-            for (int i = tid; i < R; i += FDL_THREADS) pp[i] = z[i] + beta * pp[i];
-            __syncthreads();
+            for (int i = gt; i < R; i += GT) pp[i] = z[i] + beta * pp[i];
+            cluster.sync();
         }
     }
     // true residual ||A x - b|| / ||b|| (linsolve.py:49-53); x is copied into
     // the halo-padded p buffer for the gather
-    for (int i = tid; i < R; i += FDL_THREADS) pp[i] = x[i];
-    __syncthreads();
+    for (int i = gt; i < R; i += GT) pp[i] = x[i];
+    cluster.sync();
     spmv(pp, qq);
     double eel = 0.0;
-    for (int i = tid; i < R; i += FDL_THREADS) {
+    for (int i = gt; i < R; i += GT) {
         const double e = qq[i] - b[i];
         eel += isfinite(x[i]) ? e * e : __longlong_as_double(0x7ff8000000000000ULL);
     }
-    const double ee = fd_block_sum(eel, red);
-    if (tid == 0) {
+    const double ee = csum(eel);
+    if (gt == 0) {
         st[c].it = it;
         st[c].conv = conv;
         st[c].active = 0;
         st[c].bb = bb;
         relres[c] = bb > 0.0 ? sqrt(ee / bb) : (ee == 0.0 ? 0.0 : ee);
     }
+    cluster.sync();   // no CTA exits while others may still read its cpart
 }
 
 cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
     const int n = (int)h->fdl_comps.size();
     if (n == 0) return cudaSuccess;
-#define LAUNCH_FDL(DD)                                                                                   \
-    k_pcg_fdl<DD><<<(unsigned)n, FDL_THREADS, 0, h->stream>>>(                                           \
-        h->d_comps, h->d_fdl_list, h->d_slotoff, h->d_stencil, h->d_rhs, h->p, h->d_fd_uoff, h->d_fdU,  \
-        h->d_ck, h->d_fdl_off, h->d_fdl, h->d_x, h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_cg,       \
-        h->d_relres, rtol * rtol, maxit)
+    int64_t rmax = 0;
+    for (int c : h->fdl_comps) rmax = std::max<int64_t>(rmax, h->comps[c].rows);
+    int K = 8;   // cluster CTAs per component: >= 512 rows per CTA
+    while (K > 1 && rmax / K < 512) K >>= 1;
+    if (const char* fk = getenv("SGIGA_FDL_K")) K = std::max(1, std::min(8, atoi(fk)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(n * K));
+    cfg.blockDim = dim3(FDL_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = K;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const double rt2 = rtol * rtol;
+    cudaError_t e;
+#define LAUNCH_FDL(DD)                                                                                       \
+    e = cudaLaunchKernelEx(&cfg, k_pcg_fdl<DD>, (const CompInfo*)h->d_comps, (const int*)h->d_fdl_list,     \
+                           (const int*)h->d_slotoff, (const double*)h->d_stencil, (const double*)h->d_rhs,  \
+                           h->p, (const int64_t*)h->d_fd_uoff, (const double*)h->d_fdU,                    \
+                           (const double*)h->d_ck, (const int64_t*)h->d_fdl_off, (const double*)h->d_fdl,  \
+                           h->d_x, h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_cg, h->d_relres, rt2, maxit)
     if (h->d == 1) { LAUNCH_FDL(1); }
     else if (h->d == 2) { LAUNCH_FDL(2); }
     else { LAUNCH_FDL(3); }
 #undef LAUNCH_FDL
     h->launches[1]++;
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
