@@ -397,6 +397,46 @@ __device__ __forceinline__ int fd_row_base(const CompInfo& C, int d, int row) {
     return rb;
 }
 
+// SpMV of the FD kernel: q = A v, v halo-padded in shared memory.  np
+// threads per row (slot classes t = part mod np), consecutive threads on
+// consecutive rows so the stencil loads coalesce, 16 independent loads in
+// flight per thread; the np partial sums are added in fixed order.  Out of
+// line: both call sites (the PCG loop and the true residual) get the same
+// load batching.
+template <int D>
+__device__ __noinline__ void fd_spmv(const CompInfo& C, const double* __restrict__ val, const int* __restrict__ offs,
+                                     const double* __restrict__ ph, double* __restrict__ qs,
+                                     double* __restrict__ qp, int R, int NS, int np) {
+    const int tid = threadIdx.x;
+    for (int w = tid; w < R * np; w += FD_THREADS) {
+        const int part = w / R, row = w - part * R;
+        const int rb = fd_row_base(C, D, row);
+        double y0 = 0.0, y1 = 0.0;
+        int t = part;
+        for (; t + 15 * np < NS; t += 16 * np) {
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = __ldg(val + (size_t)(t + u * np) * R + row);
+#pragma unroll
+            for (int u = 0; u < 16; u += 2) {
+                y0 += v[u] * ph[rb + offs[t + u * np]];
+                y1 += v[u + 1] * ph[rb + offs[t + (u + 1) * np]];
+            }
+        }
+        for (; t < NS; t += np) y0 += __ldg(val + (size_t)t * R + row) * ph[rb + offs[t]];
+        if (np == 1) qs[row] = y0 + y1;
+        else qp[w] = y0 + y1;
+    }
+    __syncthreads();
+    if (np == 1) return;
+    for (int row = tid; row < R; row += FD_THREADS) {
+        double y = qp[row];
+        for (int k = 1; k < np; ++k) y += qp[k * R + row];
+        qs[row] = y;
+    }
+    __syncthreads();
+}
+
 template <int D>
 __global__ void __launch_bounds__(FD_THREADS, 1)
 k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
@@ -405,8 +445,10 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
          const int64_t* __restrict__ uoff, const int64_t* __restrict__ loff,
          const double* __restrict__ dU, const double* __restrict__ dL, const double* __restrict__ ckg,
          double* __restrict__ xout, CgState* __restrict__ st, double* __restrict__ relres, double rtol2,
-         int maxit) {
+         int maxit, long long* __restrict__ prof) {
     extern __shared__ double fsm[];
+    const long long t0 = clock64();
+    auto stamp = [&](int k) { if (prof && threadIdx.x == 0) prof[blockIdx.x * 8 + k] = clock64() - t0; };
     __shared__ double red[FD_THREADS / 32];
     const int c = list[blockIdx.x];
     const CompInfo& C = comps[c];
@@ -483,40 +525,9 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
 #pragma unroll
         for (int k = D - 1; k >= 0; --k) { mode(src, bufs[w], k, false); src = bufs[w]; w ^= 1; }
     };
-    // q = A v for v held in ph (halo-padded).  np threads per row (slot
-    // classes t = part mod np), consecutive threads on consecutive rows so the
-    // stencil loads coalesce; the np partial sums are added in fixed order
+    // q = A v for v held in ph (halo-padded), see fd_spmv
     const int np = max(1, min(8, FD_THREADS / max(R, 1)));
-    auto spmv = [&]() {
-        for (int w = tid; w < R * np; w += FD_THREADS) {
-            const int part = w / R, row = w - part * R;
-            const int rb = fd_row_base(C, D, row);
-            // batches of 8 independent stencil loads in flight (L2 latency)
-            double y0 = 0.0, y1 = 0.0;
-            int t = part;
-            for (; t + 7 * np < NS; t += 8 * np) {
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldg(val + (size_t)(t + u * np) * R + row);
-#pragma unroll
-                for (int u = 0; u < 8; u += 2) {
-                    y0 += v[u] * ph[rb + offs[t + u * np]];
-                    y1 += v[u + 1] * ph[rb + offs[t + (u + 1) * np]];
-                }
-            }
-            for (; t < NS; t += np) y0 += __ldg(val + (size_t)t * R + row) * ph[rb + offs[t]];
-            if (np == 1) qs[row] = y0 + y1;
-            else qp[w] = y0 + y1;
-        }
-        __syncthreads();
-        if (np == 1) return;
-        for (int row = tid; row < R; row += FD_THREADS) {
-            double y = qp[row];
-            for (int k = 1; k < np; ++k) y += qp[k * R + row];
-            qs[row] = y;
-        }
-        __syncthreads();
-    };
+    auto spmv = [&]() { fd_spmv<D>(C, val, offs, ph, qs, qp, R, NS, np); };
 
     double bbl = 0.0;
     for (int i = tid; i < R; i += FD_THREADS) {
@@ -527,13 +538,16 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
     }
     const double bb = fd_block_sum(bbl, red);
     int it = 0, conv = (bb == 0.0);
+    stamp(1);
     if (!conv) {
         precond(rs_);
+        stamp(2);
         double rzl = 0.0;
         for (int i = tid; i < R; i += FD_THREADS) { ph[i] = zs[i]; rzl += rs_[i] * zs[i]; }
         double rz = fd_block_sum(rzl, red);
         while (it < maxit) {
             spmv();
+            if (it == 0) stamp(3);
             double pql = 0.0;
             for (int i = tid; i < R; i += FD_THREADS) pql += ph[i] * qs[i];
             const double alpha = rz / fd_block_sum(pql, red);
@@ -557,6 +571,7 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
             __syncthreads();
         }
     }
+    stamp(4);
     // true residual ||A x - b|| / ||b|| (linsolve.py:49-53)
     for (int i = tid; i < R; i += FD_THREADS) {
         ph[i] = xs[i];
@@ -564,6 +579,7 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
     }
     __syncthreads();
     spmv();
+    stamp(5);
     double eel = 0.0;
     for (int i = tid; i < R; i += FD_THREADS) {
         const double e = qs[i] - b[i];
@@ -577,6 +593,8 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
         st[c].bb = bb;
         relres[c] = bb > 0.0 ? sqrt(ee / bb) : (ee == 0.0 ? 0.0 : ee);
     }
+    stamp(6);
+    if (prof && tid == 0) prof[blockIdx.x * 8 + 7] = R * 1000 + NS;
 }
 
 // ---- 3e: line-FD preconditioned CG for components with ONE long axis -------
@@ -1108,17 +1126,33 @@ cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit) {
     size_t smem = 0;
     for (int c : h->fd_comps) smem = std::max(smem, fd_comp_smem(h->comps[c], h->d));
     cudaError_t e;
+    long long* prof = nullptr;
+    const char* pe = getenv("SGIGA_FD_PROFILE");   // per-CTA phase cycles (probe only)
+    if (pe && pe[0] == '1') {
+        if ((e = cudaMalloc(&prof, sizeof(long long) * 8 * n)) != cudaSuccess) return e;
+        cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * n, h->stream);
+    }
 #define LAUNCH_FD(DD)                                                                                 \
     e = cudaFuncSetAttribute(k_pcg_fd<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
     if (e != cudaSuccess) return e;                                                                   \
     k_pcg_fd<DD><<<(unsigned)n, FD_THREADS, smem, h->stream>>>(                                       \
         h->d_comps, h->d_fdlist, h->d_slotoff, h->d_stencil, h->d_rhs, h->d_G, h->d_fd_uoff,          \
-        h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_ck, h->d_x, h->d_cg, h->d_relres, rtol * rtol, maxit)
+        h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_ck, h->d_x, h->d_cg, h->d_relres, rtol * rtol, maxit, prof)
     if (h->d == 1) { LAUNCH_FD(1); }
     else if (h->d == 2) { LAUNCH_FD(2); }
     else { LAUNCH_FD(3); }
 #undef LAUNCH_FD
     h->launches[1]++;
+    if (prof) {
+        std::vector<long long> t(8 * n);
+        cudaMemcpyAsync(t.data(), prof, sizeof(long long) * t.size(), cudaMemcpyDeviceToHost, h->stream);
+        cudaStreamSynchronize(h->stream);
+        for (int b = 0; b < n; ++b)
+            fprintf(stderr, "pcg-fd cta %d R=%lld NS=%lld cycles: prologue=%lld b=%lld precond=%lld spmv1=%lld "
+                    "loop=%lld spmv2=%lld end=%lld\n", b, t[8 * b + 7] / 1000, t[8 * b + 7] % 1000, t[8 * b],
+                    t[8 * b + 1], t[8 * b + 2], t[8 * b + 3], t[8 * b + 4], t[8 * b + 5], t[8 * b + 6]);
+        cudaFree(prof);
+    }
     return cudaGetLastError();
 }
 
