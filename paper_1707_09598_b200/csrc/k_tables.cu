@@ -81,7 +81,7 @@ __global__ void k_basis_tables(const TabInfo* __restrict__ tabs, int ntab,
 // ---- fused geometry -> metric + load --------------------------------------
 // One thread per (component, quadrature point), storage order (s, a, b).
 template <int D>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 2)
 k_metric(const CompInfo* __restrict__ comps, int ncomp,
                          const int64_t* __restrict__ qp_cum, const TabInfo* __restrict__ tabs,
                          const double* __restrict__ qx, const double* __restrict__ qw,
@@ -90,30 +90,71 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
                          int q, int forcing_id, const double* __restrict__ hostf,
                          double* __restrict__ xphys, double* __restrict__ Gout,
                          int* __restrict__ err) {
-    int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= qp_cum[ncomp]) return;
-    int lo = 0, hi = ncomp;
-    while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
-        if (qp_cum[mid] <= gid) lo = mid; else hi = mid;
+    // the component of the CTA's first point, found once per CTA (a CTA that
+    // straddles a component boundary: the other threads search themselves);
+    // its index strides and table offsets staged in shared memory
+    __shared__ int s_comp;
+    __shared__ int64_t s_lo, s_hi, s_tot;
+    __shared__ unsigned s_qs[D], s_nq[D];
+    __shared__ int64_t s_toff[D], s_goff[D];
+    const int64_t gid0 = (int64_t)blockIdx.x * blockDim.x;
+    if (threadIdx.x == 0) {
+        const int64_t tot = qp_cum[ncomp];
+        int lo = 0, hi = ncomp;
+        while (hi - lo > 1) {
+            int mid = (lo + hi) >> 1;
+            if (qp_cum[mid] <= gid0) lo = mid; else hi = mid;
+        }
+        s_comp = lo;
+        s_lo = qp_cum[lo];
+        s_hi = qp_cum[lo + 1];
+        s_tot = tot;
+        const CompInfo& C0 = comps[lo];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            s_qs[k] = (unsigned)C0.qs[k];
+            s_nq[k] = (unsigned)C0.nel[k] * (unsigned)q;
+            const TabInfo& T = tabs[C0.tab[k]];
+            s_toff[k] = T.qp_off;
+            s_goff[k] = T.geo_off;
+        }
+    }
+    __syncthreads();
+    const int64_t gid = gid0 + threadIdx.x;
+    if (gid >= s_tot) return;
+    int lo = s_comp;
+    unsigned qsk[D], nqk[D];
+    int64_t toff[D], goff[D];
+    if (gid < s_hi) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) { qsk[k] = s_qs[k]; nqk[k] = s_nq[k]; toff[k] = s_toff[k]; goff[k] = s_goff[k]; }
+    } else {
+        int l2 = lo, h2 = ncomp;
+        while (h2 - l2 > 1) {
+            int mid = (l2 + h2) >> 1;
+            if (qp_cum[mid] <= gid) l2 = mid; else h2 = mid;
+        }
+        lo = l2;
+        const CompInfo& C1 = comps[lo];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            qsk[k] = (unsigned)C1.qs[k];
+            nqk[k] = (unsigned)C1.nel[k] * (unsigned)q;
+            const TabInfo& T = tabs[C1.tab[k]];
+            toff[k] = T.qp_off;
+            goff[k] = T.geo_off;
+        }
     }
     const CompInfo& C = comps[lo];
     // per-component quadrature index < 2^31 (a component with more points
     // would need > 16 GB of metric): 32-bit index arithmetic
-    const unsigned lin = (unsigned)(gid - qp_cum[lo]);
+    const unsigned lin = (unsigned)(gid - (lo == s_comp ? s_lo : qp_cum[lo]));
     double w = 1.0;
     const double* bv[D];
     int first[D];
     unsigned Qa[D];
-    int64_t toff[D], goff[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-        const unsigned Nq = (unsigned)C.nel[k] * (unsigned)q;
-        Qa[k] = (lin / (unsigned)C.qs[k]) % Nq;
-        const TabInfo& T = tabs[C.tab[k]];
-        toff[k] = T.qp_off;
-        goff[k] = T.geo_off;
-    }
+    for (int k = 0; k < D; ++k) Qa[k] = (lin / qsk[k]) % nqk[k];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         first[k] = geofirst[goff[k] + Qa[k]];
@@ -136,6 +177,46 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
 #pragma unroll
     for (int k = 0; k < D; ++k) gn[k] = geo->n[k];
     int c0 = geo->deg[0] + 1, c1 = D > 1 ? geo->deg[1] + 1 : 1, c2 = D > 2 ? geo->deg[2] + 1 : 1;
+    if constexpr (D == 3) {
+        // sum-factorised: contract axis 0 (values and derivatives), then axis
+        // 1, then axis 2 -- 2(D+1)(c0 c1 c2 + 1.5 c1 c2 + 2 c2) FMAs instead of
+        // a product per control point (rounding-level reordering of einsum)
+        const int L0 = first[0] * gn[1], L1 = first[1];
+        for (int l = 0; l < c2; ++l) {
+            double Bvv[D + 1], Bdv[D + 1], Bvd[D + 1];
+#pragma unroll
+            for (int c = 0; c <= D; ++c) Bvv[c] = Bdv[c] = Bvd[c] = 0.0;
+            for (int j = 0; j < c1; ++j) {
+                double Av[D + 1], Ad[D + 1];
+#pragma unroll
+                for (int c = 0; c <= D; ++c) Av[c] = Ad[c] = 0.0;
+                for (int i = 0; i < c0; ++i) {
+                    const double b0 = bv[0][i], d0 = bv[0][GEO_PMAX + i];
+                    const double* h = hw + (int64_t)(((L0 + i * gn[1]) + (L1 + j)) * gn[2] + first[2] + l) * (D + 1);
+#pragma unroll
+                    for (int c = 0; c <= D; ++c) {
+                        Av[c] = fma(b0, h[c], Av[c]);
+                        Ad[c] = fma(d0, h[c], Ad[c]);
+                    }
+                }
+                const double b1 = bv[1][j], d1 = bv[1][GEO_PMAX + j];
+#pragma unroll
+                for (int c = 0; c <= D; ++c) {
+                    Bvv[c] = fma(b1, Av[c], Bvv[c]);
+                    Bdv[c] = fma(b1, Ad[c], Bdv[c]);
+                    Bvd[c] = fma(d1, Av[c], Bvd[c]);
+                }
+            }
+            const double b2 = bv[2][l], d2 = bv[2][GEO_PMAX + l];
+#pragma unroll
+            for (int c = 0; c <= D; ++c) {
+                hom[c] = fma(b2, Bvv[c], hom[c]);
+                dh[0][c] = fma(b2, Bdv[c], dh[0][c]);
+                dh[1][c] = fma(b2, Bvd[c], dh[1][c]);
+                dh[2][c] = fma(d2, Bvv[c], dh[2][c]);
+            }
+        }
+    } else
     for (int i = 0; i < c0; ++i)
         for (int j = 0; j < c1; ++j)
             for (int l = 0; l < c2; ++l) {
