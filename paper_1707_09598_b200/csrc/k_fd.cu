@@ -397,6 +397,30 @@ __device__ __forceinline__ int fd_row_base(const CompInfo& C, int d, int row) {
     return rb;
 }
 
+// full C-order coefficient vector of component C from its internal-order
+// interior solution x (thread t of nt): interior dofs get x, boundary dofs 0
+template <int D>
+__device__ __forceinline__ void fd_expand(const CompInfo& C, const double* __restrict__ x,
+                                          double* __restrict__ coef, int t, int nt) {
+    int n[D], rs[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) { n[k] = C.n[k]; rs[k] = (int)C.rs[k]; }
+    double* cf = coef + C.dof_off;
+    const int nd = (int)C.ndofs;
+    for (int f = t; f < nd; f += nt) {
+        int rem = f, row = 0;
+        bool inter = true;
+#pragma unroll
+        for (int k = D - 1; k >= 0; --k) {
+            const int ik = rem % n[k];
+            rem /= n[k];
+            if (ik < 1 || ik > n[k] - 2) inter = false;
+            else row += (ik - 1) * rs[k];
+        }
+        cf[f] = inter ? x[row] : 0.0;
+    }
+}
+
 // SpMV of the FD kernel: q = A v, v halo-padded in shared memory.  np
 // threads per row (slot classes t = part mod np), consecutive threads on
 // consecutive rows so the stencil loads coalesce, 16 independent loads in
@@ -444,8 +468,8 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
          const double* __restrict__ rhs, const double* __restrict__ Gbuf,
          const int64_t* __restrict__ uoff, const int64_t* __restrict__ loff,
          const double* __restrict__ dU, const double* __restrict__ dL, const double* __restrict__ ckg,
-         double* __restrict__ xout, CgState* __restrict__ st, double* __restrict__ relres, double rtol2,
-         int maxit, long long* __restrict__ prof) {
+         double* __restrict__ xout, double* __restrict__ coef, CgState* __restrict__ st,
+         double* __restrict__ relres, double rtol2, int maxit, long long* __restrict__ prof) {
     extern __shared__ double fsm[];
     const long long t0 = clock64();
     auto stamp = [&](int k) { if (prof && threadIdx.x == 0) prof[blockIdx.x * 8 + k] = clock64() - t0; };
@@ -593,6 +617,9 @@ k_pcg_fd(const CompInfo* __restrict__ comps, const int* __restrict__ list,
         st[c].bb = bb;
         relres[c] = bb > 0.0 ? sqrt(ee / bb) : (ee == 0.0 ? 0.0 : ee);
     }
+    // the component's full coefficient vector in the reference's C order,
+    // zero on the boundary (AssembledSystem.expand, assembly.py:202-206)
+    fd_expand<D>(C, xs, coef, tid, FD_THREADS);
     stamp(6);
     if (prof && tid == 0) prof[blockIdx.x * 8 + 7] = R * 1000 + NS;
 }
@@ -758,7 +785,7 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
           const int64_t* __restrict__ fdl_off, const double* __restrict__ fdl, double* __restrict__ xg,
           double* __restrict__ rg, double* __restrict__ zg, double* __restrict__ pg, double* __restrict__ qg,
           double* __restrict__ tg, CgState* __restrict__ st, double* __restrict__ relres, double rtol2,
-          int maxit) {
+          int maxit, double* __restrict__ coef) {
     // one thread-block cluster of K CTAs per component: rows, lines and
     // vector work split over the K*FDL_THREADS threads, phases separated by
     // cluster barriers (release / acquire: the global-memory vectors written
@@ -1008,6 +1035,8 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
         st[c].bb = bb;
         relres[c] = bb > 0.0 ? sqrt(ee / bb) : (ee == 0.0 ? 0.0 : ee);
     }
+    // full C-order coefficients (x complete: the last cluster barrier is in csum)
+    fd_expand<D>(C, x, coef, gt, GT);
     cluster.sync();   // no CTA exits while others may still read its cpart
 }
 
@@ -1038,7 +1067,8 @@ cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
                            (const int*)h->d_slotoff, (const double*)h->d_stencil, (const double*)h->d_rhs,  \
                            h->p, (const int64_t*)h->d_fd_uoff, (const double*)h->d_fdU,                    \
                            (const double*)h->d_ck, (const int64_t*)h->d_fdl_off, (const double*)h->d_fdl,  \
-                           h->d_x, h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_cg, h->d_relres, rt2, maxit)
+                           h->d_x, h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_cg, h->d_relres, rt2, maxit, \
+                           h->d_coef)
     if (h->d == 1) { LAUNCH_FDL(1); }
     else if (h->d == 2) { LAUNCH_FDL(2); }
     else { LAUNCH_FDL(3); }
@@ -1137,7 +1167,7 @@ cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit) {
     if (e != cudaSuccess) return e;                                                                   \
     k_pcg_fd<DD><<<(unsigned)n, FD_THREADS, smem, h->stream>>>(                                       \
         h->d_comps, h->d_fdlist, h->d_slotoff, h->d_stencil, h->d_rhs, h->d_G, h->d_fd_uoff,          \
-        h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_ck, h->d_x, h->d_cg, h->d_relres, rtol * rtol, maxit, prof)
+        h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_ck, h->d_x, h->d_coef, h->d_cg, h->d_relres, rtol * rtol, maxit, prof)
     if (h->d == 1) { LAUNCH_FD(1); }
     else if (h->d == 2) { LAUNCH_FD(2); }
     else { LAUNCH_FD(3); }

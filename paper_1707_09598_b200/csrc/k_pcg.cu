@@ -415,6 +415,7 @@ __global__ void k_expand(const CompInfo* __restrict__ comps, int ncomp,
         if (dof_cum[mid] <= gid) lo = mid; else hi = mid;
     }
     const CompInfo& C = comps[lo];
+    if (C.fd) return;   // the FD / line-FD kernels write their components' coefficients
     int64_t f = gid - dof_cum[lo], rem = f, row = 0;
     bool inter = true;
 #pragma unroll
@@ -619,6 +620,9 @@ cudaError_t launch_residual_check(Handle* h) {
 cudaError_t launch_expand(Handle* h) {
     int64_t n = h->total_dofs;
     if (n == 0) return cudaSuccess;
+    bool any = false;   // components not expanded by the FD kernels (incl. empty interiors)
+    for (const CompInfo& C : h->comps) any = any || !C.fd;
+    if (!any) return cudaSuccess;
     unsigned blocks = (unsigned)((n + 255) / 256);
     if (h->d == 1) k_expand<1><<<blocks, 256, 0, h->stream>>>(h->d_comps, h->ncomp, comp_dof_cum_ptr(h), h->d_x, h->d_coef);
     else if (h->d == 2) k_expand<2><<<blocks, 256, 0, h->stream>>>(h->d_comps, h->ncomp, comp_dof_cum_ptr(h), h->d_x, h->d_coef);
