@@ -169,6 +169,22 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
         }
         for (int k = d - 1; k >= 0; --k)
             if (C.m[k] > mmax) { mmax = C.m[k]; s = k; }
+        // assembly stream axis: the longest by default (line-FD components
+        // need their long axis there); small components solved by the FD
+        // kernel (every axis <= FD_MMAX functions, <= 2048 rows) stream along
+        // their SHORTEST axis instead -- many short pencils rather than a few
+        // long ones (the cfg2 makespan was one long pencil), fewer halo planes
+        {
+            int64_t rows_c = 1;
+            bool fd_axes = true;
+            for (int k = 0; k < d; ++k) { rows_c *= std::max(0, C.m[k]); fd_axes = fd_axes && C.m[k] <= FD_MMAX; }
+            const char* ss_env = getenv("SGIGA_STREAM_LONG");
+            if (d >= 2 && fd_axes && rows_c <= 2048 && !(ss_env && ss_env[0] == '1')) {
+                int mmin = 1 << 30;
+                for (int k = d - 1; k >= 0; --k)
+                    if (C.m[k] < mmin) { mmin = C.m[k]; s = k; }
+            }
+        }
         int j = 0;
         for (int k = 0; k < d; ++k) if (k != s) C.ax[j++] = k;
         C.ax[d - 1] = s;
