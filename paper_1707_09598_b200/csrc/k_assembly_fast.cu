@@ -198,14 +198,32 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     if (D >= 3) build_T(kb, pc.ib, Tb, phiB, F::NB);
     else if (tid == 0) { Tb[0] = 1.0; Tb[1] = Tb[2] = Tb[3] = 0.0; phiB[0] = 1.0; }
     for (int idx = tid; idx < F::RING * W * F::WAB + F::RING; idx += NT) Acc[idx] = 0.0;
-    // invalid window points stay zero in both plane buffers
-    for (int idx = tid; idx < F::NGB * F::sGw; idx += NT) sm[F::oGw + idx] = 0.0;
+    // cp.async variant: invalid window points stay zero in the plane buffers
+    // (the TMA unit zero-fills them itself)
+    if constexpr (!F::TMA)
+        for (int idx = tid; idx < F::NGB * F::sGw; idx += NT) sm[F::oGw + idx] = 0.0;
     __shared__ __align__(8) uint64_t fast_mbar[3];   // TMA variant: one barrier per plane buffer
     if (F::TMA && tid == 0) {
         mbar_init(&fast_mbar[0], 1);
         mbar_init(&fast_mbar[1], 1);
         mbar_init(&fast_mbar[2], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        // the first GPD planes are issued here, in flight while the pencil's
+        // tables and flush maps are built (short pencils: the pipeline fill)
+        const int ef = pc.r0 - p < 0 ? 0 : pc.r0 - p;
+        const int el = pc.r1 - 1 > Ts.nel - 1 ? Ts.nel - 1 : pc.r1 - 1;
+        const int np0 = (el - ef + 1) * Q;
+        const int x0u = (pc.ia - p) * Q, x1 = (pc.ib - p) * Q, x0 = x0u - (x0u & 1);
+        for (int jj = 0; jj < F::GPD && jj < np0; ++jj) {
+            double* Gw = sm + F::oGw + jj * F::sGw;
+            mbar_expect_tx(&fast_mbar[jj], (uint32_t)(F::nGw * 8));
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+                ::"r"(smem_u32(Gw)), "l"(tmaps + pc.comp), "r"(x0), "r"(x1), "r"(ef * Q + jj), "r"(0),
+                  "r"(smem_u32(&fast_mbar[jj]))
+                : "memory");
+        }
     }
     __syncthreads();
 
@@ -402,7 +420,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         if (nplanes > 0) {
             if (inG3) load_bs(e_first);
             if constexpr (F::TMA) {
-                for (int jj = 0; jj < F::GPD && jj < nplanes; ++jj) load_plane_tma((int64_t)e_first * Q + jj, jj);
+                // (the first GPD planes were issued at kernel entry)
             } else {
                 load_plane((int64_t)e_first * Q, 0);
                 cp_async_wait_all();
