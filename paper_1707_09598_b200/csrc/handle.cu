@@ -43,7 +43,7 @@ static void free_all(Handle* h) {
                     h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
                     h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps,
-                    h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck};
+                    h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck, h->d_ticket};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};
@@ -551,12 +551,21 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_fdl_off, h->comps.size());
     A_(d_fdl, h->fdl_total);
     A_(d_ck, (int64_t)MAXD * h->ncomp);
+    if (ea == cudaSuccess && !h->d_ticket) {
+        ea = cudaMalloc(&h->d_ticket, sizeof(unsigned));
+        if (ea == cudaSuccess) ea = cudaMemset(h->d_ticket, 0, sizeof(unsigned));
+    }
 #undef A_
-    if (ea == cudaSuccess) ea = cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking);
+    // side streams at the highest priority: their few CTAs (FD set-up, point
+    // sort) are scheduled as soon as an SM frees up instead of queueing behind
+    // the thousands of assembly CTAs launched before them
+    int prio_lo = 0, prio_hi = 0;
+    if (ea == cudaSuccess) ea = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (ea == cudaSuccess) ea = cudaStreamCreateWithPriority(&h->stream2, cudaStreamNonBlocking, prio_hi);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_fork, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_join, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_metric, cudaEventDisableTiming);
-    if (ea == cudaSuccess) ea = cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking);
+    if (ea == cudaSuccess) ea = cudaStreamCreateWithPriority(&h->stream3, cudaStreamNonBlocking, prio_hi);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->cs_fork, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->cs_join, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaMallocHost(reinterpret_cast<void**>(&h->h_pinned_flag), sizeof(int) * 4);
@@ -712,6 +721,7 @@ static int assemble_enqueue(Handle* h) {
     if (!h->fd_uniq.empty() || !h->fd_comps.empty() || !h->fdl_comps.empty()) {   // FD eigen-factors on the side stream, overlapping the assembly
         SG_CUDA(cudaEventRecord(h->fd_fork, h->stream));
         SG_CUDA(cudaStreamWaitEvent(h->stream2, h->fd_fork, 0));
+        SG_CUDA(launch_solve_prologue(h, h->stream2));   // solver state zeroed off the main stream
         SG_CUDA(launch_fd_eigen(h, h->stream2));
         h->fd_pending = true;
     }
@@ -736,7 +746,9 @@ static int solve_enqueue(Handle* h, double rtol, int32_t maxit) {
     if (maxit < 1) maxit = 1000000;
     h->launches[1] = 0;
     h->pmark(2);
-    SG_CUDA(launch_solve_prologue(h));   // zero the solver state and the active counts
+    // zero the solver state and the active counts (already done on the FD
+    // side stream when the assembly forked it: joined before the solve)
+    if (!h->fd_pending) SG_CUDA(launch_solve_prologue(h, h->stream));
     int st = run_pcg(h, rtol, maxit);
     if (st) return st;
     h->kstart(5);
@@ -807,7 +819,8 @@ static int stage_points(Handle* h, const double* pts, int64_t npts, size_t nout,
 }
 
 // device points -> device values
-static int combine_enqueue(Handle* h, const double* dp, int64_t npts, double* dout, int per_comp) {
+static int combine_enqueue(Handle* h, const double* dp, int64_t npts, double* dout, int per_comp,
+                           bool* status_fused = nullptr) {
     h->launches[2] = 0;
     h->pmark(4);
     if (h->cs_pending) {   // the point sort ran on the side stream
@@ -815,7 +828,7 @@ static int combine_enqueue(Handle* h, const double* dp, int64_t npts, double* do
         h->cs_pending = false;
     }
     h->kstart(6);
-    SG_CUDA(launch_combine_points(h, dp, npts, dout, per_comp));
+    SG_CUDA(launch_combine_points(h, dp, npts, dout, per_comp, status_fused));
     h->kstop(6);
     h->pmark(5);
     return SGIGA_OK;
@@ -848,7 +861,13 @@ int sgiga_solve(sgiga_handle* hh, double rtol, int32_t maxit, int32_t* iters_out
     return solve_finish(h, iters_out, relres_out);
 }
 
+// Whole-pass CUDA graphs are opt-in (SGIGA_RUN_GRAPH=1): measured on the B200,
+// passes enqueued back to back hide the host launch cost anyway (cfg2 0.248
+// ms/pass direct vs 0.251 replayed), and in a replayed graph the side-stream
+// FD set-up did not overlap the assembly (cfg5 +1 ms)
 static bool run_graphs_enabled() {
+    const char* on = getenv("SGIGA_RUN_GRAPH");
+    if (!(on && on[0] == '1')) return false;
     for (const char* k : {"SGIGA_NO_GRAPH", "SGIGA_PCG_PROFILE", "SGIGA_ASM_PROFILE", "SGIGA_PCG_TRACE"}) {
         const char* e = getenv(k);
         if (e && e[0] && !(e[0] == '0' && e[1] == 0)) return false;
@@ -879,8 +898,9 @@ static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, 
         }
         int s2 = assemble_enqueue(h);
         if (!s2) s2 = solve_enqueue(h, rtol, maxit);
-        if (!s2 && npts > 0) s2 = combine_enqueue(h, dp, npts, dout, 0);
-        if (!s2 && launch_status(h) != cudaSuccess) s2 = SGIGA_ERR_CUDA;
+        bool fused = false;   // the combine's last CTA writes the status (no k_status launch)
+        if (!s2 && npts > 0) s2 = combine_enqueue(h, dp, npts, dout, 0, &fused);
+        if (!s2 && !fused && launch_status(h) != cudaSuccess) s2 = SGIGA_ERR_CUDA;
         h->cs_ready = false;
         if (h->cs_pending) {   // not consumed (an earlier step failed): still join the side stream
             cudaStreamWaitEvent(h->stream, h->cs_join, 0);

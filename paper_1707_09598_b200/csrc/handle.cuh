@@ -112,7 +112,8 @@ struct Handle {
     int* d_fdl_list = nullptr;
     int64_t* d_fdl_off = nullptr;
     double* d_fdl = nullptr;
-    double* d_ck = nullptr;                  // [ncomp][MAXD] FD metric scales c_k (k_fd_metric_scale)
+    double* d_ck = nullptr;
+    unsigned* d_ticket = nullptr;            // last-CTA ticket of the status-fused combine (kept zero)                  // [ncomp][MAXD] FD metric scales c_k (k_fd_metric_scale)
     cudaStream_t stream2 = nullptr;          // side stream: the eigen kernel overlaps assembly
     cudaEvent_t fd_fork = nullptr, fd_join = nullptr, fd_metric = nullptr;
     bool fd_pending = false;                 // fd_join not yet waited on by the main stream

@@ -223,7 +223,7 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
                        int ntab, const double* __restrict__ knots, int mu, const double* __restrict__ coef,
                        const double* __restrict__ pts, int64_t npts, const int* __restrict__ perm,
                        double* __restrict__ out, int per_component, int npt, int* __restrict__ hist,
-                       int* __restrict__ err) {
+                       int* __restrict__ err, StatusFuse sf) {
     extern __shared__ double csm[];
     double* Bt = csm;                                   // [ntab][P][npt]
     double* V = Bt + (size_t)ntab * P * npt;            // [ncomp][npt]
@@ -275,6 +275,25 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
             acc = (c == 0) ? cv : __dadd_rn(acc, cv);
         }
         out[gidx[pt]] = acc;
+    }
+    if (sf.ticket) {   // the pass's status (k_status) by the CTA that finishes last
+        __shared__ bool last;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) last = atomicAdd(sf.ticket, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            for (int c = tid; c < sf.ncomp; c += CP_THREADS) {
+                sf.hst[c] = sf.st[c];
+                sf.hrel[c] = sf.relres[c];
+            }
+            if (tid == 0) {
+                *sf.herr = *reinterpret_cast<volatile int*>(err);
+                *sf.ticket = 0u;
+            }
+            __threadfence_system();
+        }
     }
 }
 
@@ -576,8 +595,14 @@ cudaError_t launch_combine_sort(Handle* h, const double* d_pts, int64_t npts, cu
 }
 
 cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, double* d_out,
-                                  int per_component) {
+                                  int per_component, bool* status_fused) {
+    if (status_fused) *status_fused = false;
     if (npts == 0) return cudaSuccess;
+    StatusFuse sf{};
+    if (status_fused && !per_component && h->d_ticket) {
+        sf = StatusFuse{h->d_cg, h->d_relres, h->ncomp, h->dh_cg, h->dh_rel, h->dh_err, h->d_ticket};
+        *status_fused = true;
+    }
     const int ntab = (int)h->tabs.size(), P = h->p + 1;
     // points per CTA: as many as fit ~100 KB of shared memory (2 CTAs/SM), <= 64
     auto smem_of = [&](int n) {
@@ -596,6 +621,7 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
         SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CP)
 #undef LAUNCH_CP
         h->launches[2]++;
+        if (status_fused) *status_fused = false;
         return cudaGetLastError();
     }
     const size_t smem = smem_of(npt) + sizeof(int) * npt;
@@ -623,7 +649,7 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
         if (e_ != cudaSuccess) return e_;                                                           \
         k_combine_points_tiled<DD, PP><<<blocks, CP_THREADS, smem, h->stream>>>(                    \
             h->d_comps, h->ncomp, h->d_tabs, ntab, h->d_knots, h->mu, h->d_coef, d_pts, npts, perm,  \
-            d_out, per_component, npt, perm ? h->d_chist : nullptr, h->d_err);                      \
+            d_out, per_component, npt, perm ? h->d_chist : nullptr, h->d_err, sf);                  \
     }
     SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CPT)
 #undef LAUNCH_CPT

@@ -1078,6 +1078,27 @@ cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
     return cudaGetLastError();
 }
 
+// side-stream kernels are launched with the device's highest scheduling
+// priority as a launch attribute (kept in captured graph nodes, unlike the
+// stream's priority): their few CTAs get SMs as soon as assembly CTAs retire
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_hi(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args... args) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = hi;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // FD set-up after the metric (stream s, forked from the main stream after
 // k_metric, joined before the solve): c_k of every FD / line-FD component,
 // then the line-FD stream-axis bands and per-line factors
@@ -1086,7 +1107,7 @@ cudaError_t launch_fd_setup(Handle* h, cudaStream_t s) {
     if (nf + nl == 0) return cudaSuccess;
     const dim3 g1((unsigned)(nf + nl), (unsigned)h->d);
 #define LAUNCH_SCALE(DD)                                                                              \
-    k_fd_metric_scale<DD><<<g1, 256, 0, s>>>(h->d_comps, h->d_fdlist, nf, h->d_fdl_list, h->d_G, h->d_ck)
+    launch_hi(k_fd_metric_scale<DD>, g1, dim3(256), 0, s, h->d_comps, h->d_fdlist, nf, h->d_fdl_list, h->d_G, h->d_ck)
     if (h->d == 1) { LAUNCH_SCALE(1); }
     else if (h->d == 2) { LAUNCH_SCALE(2); }
     else { LAUNCH_SCALE(3); }
@@ -1102,10 +1123,10 @@ cudaError_t launch_fd_setup(Handle* h, cudaStream_t s) {
     }
     const dim3 g3((unsigned)((maxlines + 63) / 64), (unsigned)nl);
 #define LAUNCH_FACT(DD)                                                                                     \
-    k_fdl_bands<DD><<<(unsigned)nl, 256, 0, s>>>(h->d_comps, h->d_fdl_list, h->d_tabs, h->d_tabvals,       \
-                                                 h->d_qw, h->p, h->mu, h->q, h->d_fdl_off, h->d_fdl);     \
-    k_fdl_factor<DD><<<g3, 64, 0, s>>>(h->d_comps, h->d_fdl_list, h->p, h->d_fd_loff, h->d_fdL, h->d_ck, \
-                                       h->d_fdl_off, h->d_fdl)
+    launch_hi(k_fdl_bands<DD>, dim3((unsigned)nl), dim3(256), 0, s, h->d_comps, h->d_fdl_list, h->d_tabs,   \
+              h->d_tabvals, h->d_qw, h->p, h->mu, h->q, h->d_fdl_off, h->d_fdl);                          \
+    launch_hi(k_fdl_factor<DD>, g3, dim3(64), 0, s, h->d_comps, h->d_fdl_list, h->p, h->d_fd_loff, h->d_fdL, \
+              h->d_ck, h->d_fdl_off, h->d_fdl)
     if (h->d == 1) { LAUNCH_FACT(1); }
     else if (h->d == 2) { LAUNCH_FACT(2); }
     else { LAUNCH_FACT(3); }
@@ -1134,9 +1155,10 @@ cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s) {
         if ((e = cudaMalloc(&prof, sizeof(long long) * 8 * nu)) != cudaSuccess) return e;
         cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * nu, s);
     }
-    k_fd_eigen<<<(unsigned)nu, EIG_THREADS, smem, s>>>(
-        h->d_tabs, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_tabvals, h->d_qw, h->p, h->mu, h->q,
-        h->d_fdU, h->d_fdL, prof);
+    if ((e = launch_hi(k_fd_eigen, dim3((unsigned)nu), dim3(EIG_THREADS), smem, s, h->d_tabs, h->d_fd_uniq,
+                       h->d_fd_uoff, h->d_fd_loff, h->d_tabvals, h->d_qw, h->p, h->mu, h->q, h->d_fdU, h->d_fdL,
+                       prof)) != cudaSuccess)
+        return e;
     h->launches[0]++;
     if (prof) {
         std::vector<long long> t(8 * nu);

@@ -593,8 +593,8 @@ __global__ void k_status(const CgState* __restrict__ st, const double* __restric
     __threadfence_system();
 }
 
-cudaError_t launch_solve_prologue(Handle* h) {
-    k_solve_prologue<<<1, 256, 0, h->stream>>>(h->d_cg, h->ncomp, h->d_active_count);
+cudaError_t launch_solve_prologue(Handle* h, cudaStream_t stream) {
+    k_solve_prologue<<<1, 256, 0, stream>>>(h->d_cg, h->ncomp, h->d_active_count);
     h->launches[1]++;
     return cudaGetLastError();
 }

@@ -79,6 +79,18 @@ struct GeoInfo {
     int64_t knot_off[MAXD];
 };
 
+struct CgState;
+// k_status fused into the last CTA of the tiled combine (sgiga_run passes)
+struct StatusFuse {
+    const CgState* st;
+    const double* relres;
+    int ncomp;
+    CgState* hst;
+    double* hrel;
+    int* herr;
+    unsigned* ticket;   // nullptr: not fused
+};
+
 struct Pencil {         // one CTA of the assembly kernel
     int comp;
     int ia, ib;         // full function index along tile axes ax[d-2], ax[d-3]
@@ -216,7 +228,7 @@ cudaError_t launch_assembly(Handle* h);
 int run_pcg(Handle* h, double rtol, int maxit);
 int launch_pcg_cluster(Handle* h, double rtol, int maxit);
 cudaError_t launch_residual_check(Handle* h);
-cudaError_t launch_solve_prologue(Handle* h);
+cudaError_t launch_solve_prologue(Handle* h, cudaStream_t stream);
 cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s);
 cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit);
 cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit);
@@ -225,7 +237,7 @@ size_t fd_comp_smem(const CompInfo& C, int d);
 cudaError_t launch_status(Handle* h);
 cudaError_t launch_expand(Handle* h);
 cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, double* d_out,
-                                  int per_component);
+                                  int per_component, bool* status_fused = nullptr);
 // cell sort of the combine points on stream s; *sorted = false when the
 // point set is not sorted (too small / too large / SGIGA_COMBINE_NOSORT)
 cudaError_t launch_combine_sort(Handle* h, const double* d_pts, int64_t npts, cudaStream_t s, bool* sorted);

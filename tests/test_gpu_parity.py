@@ -319,9 +319,12 @@ def test_invalid_geometry_raises():
         run_plan(CombinationPlan(2, (((1, 1), 1),)), prob)
 
 
+@pytest.mark.parametrize("graph", ["0", "1"])
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
-def test_single_call_run_matches_phase_calls(name):
-    """sgiga_run (one sync) == assemble + solve + combine_points, bitwise."""
+def test_single_call_run_matches_phase_calls(name, graph, monkeypatch):
+    """sgiga_run (one sync) == assemble + solve + combine_points, bitwise --
+    direct launches and (SGIGA_RUN_GRAPH=1) captured / replayed pass graphs."""
+    monkeypatch.setenv("SGIGA_RUN_GRAPH", graph)
     cfg = configs.get_config(name)
     pts = cfg.points(2000)
     spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
@@ -332,6 +335,7 @@ def test_single_call_run_matches_phase_calls(name):
         v0 = b.combine_points(pts)
         c0 = b.coefficients()
         # call 1: direct launches; 2: captured into a graph; 3+: replays
+        # (graphs opt-in: SGIGA_RUN_GRAPH=1, set by the test)
         for _ in range(4):
             v1 = b.run(pts, rtol=1e-13)
             assert np.array_equal(v0, v1)
@@ -349,8 +353,10 @@ def test_single_call_run_matches_phase_calls(name):
 
 
 def test_run_graph_replay_matches_direct_launches(monkeypatch):
-    """The captured whole-run graph == direct launches (SGIGA_NO_GRAPH=1)."""
+    """The captured whole-run graph (opt-in, SGIGA_RUN_GRAPH=1) == direct
+    launches (SGIGA_NO_GRAPH=1)."""
     import torch
+    monkeypatch.setenv("SGIGA_RUN_GRAPH", "1")
     cfg = configs.get_config("cfg2")
     spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
     pts = torch.from_numpy(cfg.points(5000)).cuda()
