@@ -215,10 +215,11 @@ k_combine_points(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* _
 //   C. one thread per point: the plan-order sum acc = c0 v0, acc += c v
 //      (combination.py:227-233) -- the same operations, in the same order,
 //      as combine_at, so the result is bitwise the per-thread kernel's.
-constexpr int CP_THREADS = 256;
+constexpr int CP_THREADS = 256;   // tiled combine, large plans (64 points per CTA)
+constexpr int CP_THREADS_S = 128; // small plans (32 points per CTA): more CTAs per SM
 
-template <int D, int P>
-__global__ void __launch_bounds__(CP_THREADS)
+template <int D, int P, int NTH>
+__global__ void __launch_bounds__(NTH)
 k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabInfo* __restrict__ tabs,
                        int ntab, const double* __restrict__ knots, int mu, const double* __restrict__ coef,
                        const double* __restrict__ pts, int64_t npts, const int* __restrict__ perm,
@@ -232,11 +233,11 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
     const int tid = threadIdx.x;
     const int64_t p0 = (int64_t)blockIdx.x * npt;
     const int nloc = npts - p0 < npt ? (int)(npts - p0) : npt;
-    for (int pt = tid; pt < nloc; pt += CP_THREADS) gidx[pt] = perm ? perm[p0 + pt] : (int)(p0 + pt);
+    for (int pt = tid; pt < nloc; pt += NTH) gidx[pt] = perm ? perm[p0 + pt] : (int)(p0 + pt);
     if (hist && blockIdx.x == 0)   // the sort is done: leave its cursors zero for the next call
-        for (int i = tid; i < COMBINE_SORT_BINS; i += CP_THREADS) hist[i] = 0;
+        for (int i = tid; i < COMBINE_SORT_BINS; i += NTH) hist[i] = 0;
     __syncthreads();
-    for (int it = tid; it < ntab * npt; it += CP_THREADS) {
+    for (int it = tid; it < ntab * npt; it += NTH) {
         const int pt = it % npt, t = it / npt;
         if (pt >= nloc) continue;
         const TabInfo T = tabs[t];
@@ -248,7 +249,7 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
         for (int j = 0; j < P; ++j) Bt[(t * P + j) * npt + pt] = bv[j];
     }
     __syncthreads();
-    for (int it = tid; it < ncomp * npt; it += CP_THREADS) {
+    for (int it = tid; it < ncomp * npt; it += NTH) {
         const int pt = it % npt, c = it / npt;
         if (pt >= nloc) continue;
         const CompInfo& C = comps[c];
@@ -268,7 +269,7 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
     }
     if (per_component) return;
     __syncthreads();
-    for (int pt = tid; pt < nloc; pt += CP_THREADS) {
+    for (int pt = tid; pt < nloc; pt += NTH) {
         double acc = 0.0;
         for (int c = 0; c < ncomp; ++c) {
             const double cv = (double)comps[c].coef * V[c * npt + pt];
@@ -284,7 +285,7 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
         __syncthreads();
         if (last) {
             __threadfence();
-            for (int c = tid; c < sf.ncomp; c += CP_THREADS) {
+            for (int c = tid; c < sf.ncomp; c += NTH) {
                 sf.hst[c] = sf.st[c];
                 sf.hrel[c] = sf.relres[c];
             }
@@ -609,7 +610,10 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
         return (size_t)n * (ntab * P * sizeof(double) + ntab * sizeof(int) +
                             (per_component ? 0 : (size_t)h->ncomp * sizeof(double)));
     };
-    int npt = 64;
+    // small plans (<= 64 components, degree <= 3): 32 points / 128 threads per
+    // CTA (more resident CTAs); larger: 64 points / 256 threads (measured)
+    const bool small_cta = h->ncomp <= 64 && h->p <= 3;
+    int npt = small_cta ? 32 : 64;
     while (npt > 1 && smem_of(npt) > 100 * 1024) npt >>= 1;
     const char* ev = getenv("SGIGA_COMBINE_PERTHREAD");
     if (smem_of(npt) > 200 * 1024 || (ev && ev[0] == '1')) {   // huge plans: one thread per point
@@ -644,12 +648,21 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
     }
 #define LAUNCH_CPT(DD, PP)                                                                          \
     {                                                                                               \
-        cudaError_t e_ = cudaFuncSetAttribute(k_combine_points_tiled<DD, PP>,                       \
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        if (e_ != cudaSuccess) return e_;                                                           \
-        k_combine_points_tiled<DD, PP><<<blocks, CP_THREADS, smem, h->stream>>>(                    \
-            h->d_comps, h->ncomp, h->d_tabs, ntab, h->d_knots, h->mu, h->d_coef, d_pts, npts, perm,  \
-            d_out, per_component, npt, perm ? h->d_chist : nullptr, h->d_err, sf);                  \
+        if (small_cta) {                                                                            \
+            cudaError_t e_ = cudaFuncSetAttribute(k_combine_points_tiled<DD, PP, CP_THREADS_S>,     \
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            if (e_ != cudaSuccess) return e_;                                                       \
+            k_combine_points_tiled<DD, PP, CP_THREADS_S><<<blocks, CP_THREADS_S, smem, h->stream>>>( \
+                h->d_comps, h->ncomp, h->d_tabs, ntab, h->d_knots, h->mu, h->d_coef, d_pts, npts, perm, \
+                d_out, per_component, npt, perm ? h->d_chist : nullptr, h->d_err, sf);             \
+        } else {                                                                                    \
+            cudaError_t e_ = cudaFuncSetAttribute(k_combine_points_tiled<DD, PP, CP_THREADS>,       \
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            if (e_ != cudaSuccess) return e_;                                                       \
+            k_combine_points_tiled<DD, PP, CP_THREADS><<<blocks, CP_THREADS, smem, h->stream>>>(   \
+                h->d_comps, h->ncomp, h->d_tabs, ntab, h->d_knots, h->mu, h->d_coef, d_pts, npts, perm, \
+                d_out, per_component, npt, perm ? h->d_chist : nullptr, h->d_err, sf);             \
+        }                                                                                           \
     }
     SGIGA_DISPATCH_DP(h->d, h->p + 1, LAUNCH_CPT)
 #undef LAUNCH_CPT

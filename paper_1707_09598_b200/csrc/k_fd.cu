@@ -29,7 +29,7 @@
 
 namespace sgiga {
 
-constexpr int FD_THREADS = 256;
+constexpr int FD_THREADS = 512;
 constexpr int EIG_THREADS = 512;
 constexpr int EIG_ITEMS = ((FD_MMAX / 2) * (FD_MMAX / 2) + (FD_MMAX / 2) * FD_MMAX + EIG_THREADS - 1) / EIG_THREADS;
 constexpr int FD_LD = FD_MMAX + 1;   // padded row stride of the eigen work arrays
