@@ -43,7 +43,7 @@ static void free_all(Handle* h) {
                     h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
                     h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps,
-                    h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck, h->d_ticket};
+                    h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck, h->d_ticket, h->d_mcomp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};
@@ -366,6 +366,16 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
     });
     h->asm_seg = SEG;
     h->total_vec = vec; h->total_slots = mat; h->total_qp = nqp_tot; h->total_rows = rows_tot;
+    {   // k_metric: component of each 256-point CTA's first point
+        h->mcomp.assign((size_t)((nqp_tot + 255) / 256), 0);
+        int c = 0;
+        int64_t end = h->comps.empty() ? 0 : h->comps[0].nqp;
+        for (size_t b = 0; b < h->mcomp.size(); ++b) {
+            const int64_t g0 = (int64_t)b * 256;
+            while (c + 1 < (int)h->comps.size() && g0 >= end) end += h->comps[++c].nqp;
+            h->mcomp[b] = c;
+        }
+    }
     h->total_dofs = dof;
     if (assembly_smem_bytes(h) > 227 * 1024) {
         set_error("quadrature/degree combination exceeds the assembly kernel's shared memory");
@@ -377,6 +387,8 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
 static int upload_all(Handle* h) {
     cudaStream_t s = h->stream;
     h->tmaps_state = 0;   // tensor maps follow the component table
+    if (!h->mcomp.empty())
+        SG_CUDA(cudaMemcpyAsync(h->d_mcomp, h->mcomp.data(), sizeof(int) * h->mcomp.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_comps, h->comps.data(), sizeof(CompInfo) * h->comps.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_tabs, h->tabs.data(), sizeof(TabInfo) * h->tabs.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_geo, &h->geo, sizeof(GeoInfo), cudaMemcpyHostToDevice, s));
@@ -551,6 +563,7 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_fdl_off, h->comps.size());
     A_(d_fdl, h->fdl_total);
     A_(d_ck, (int64_t)MAXD * h->ncomp);
+    A_(d_mcomp, h->mcomp.size());
     if (ea == cudaSuccess && !h->d_ticket) {
         ea = cudaMalloc(&h->d_ticket, sizeof(unsigned));
         if (ea == cudaSuccess) ea = cudaMemset(h->d_ticket, 0, sizeof(unsigned));
@@ -644,7 +657,7 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
     h->geo = tmp.geo; h->geo_knots.swap(tmp.geo_knots); h->geo_hw.swap(tmp.geo_hw);
     h->bp_host.swap(tmp.bp_host); h->comps.swap(tmp.comps); h->tabs.swap(tmp.tabs);
     h->slotoff.swap(tmp.slotoff);
-    h->pencils.swap(tmp.pencils); h->chunks.swap(tmp.chunks);
+    h->pencils.swap(tmp.pencils); h->chunks.swap(tmp.chunks); h->mcomp.swap(tmp.mcomp);
     h->small_comps.swap(tmp.small_comps); h->large_comps.swap(tmp.large_comps);
     h->fd_comps.swap(tmp.fd_comps); h->fd_uniq.swap(tmp.fd_uniq);
     h->fd_uoff.swap(tmp.fd_uoff); h->fd_loff.swap(tmp.fd_loff);

@@ -113,7 +113,9 @@ struct Handle {
     int64_t* d_fdl_off = nullptr;
     double* d_fdl = nullptr;
     double* d_ck = nullptr;
-    unsigned* d_ticket = nullptr;            // last-CTA ticket of the status-fused combine (kept zero)                  // [ncomp][MAXD] FD metric scales c_k (k_fd_metric_scale)
+    unsigned* d_ticket = nullptr;
+    std::vector<int> mcomp;                  // component of k_metric's CTA b (first point b * 256)
+    int* d_mcomp = nullptr;            // last-CTA ticket of the status-fused combine (kept zero)                  // [ncomp][MAXD] FD metric scales c_k (k_fd_metric_scale)
     cudaStream_t stream2 = nullptr;          // side stream: the eigen kernel overlaps assembly
     cudaEvent_t fd_fork = nullptr, fd_join = nullptr, fd_metric = nullptr;
     bool fd_pending = false;                 // fd_join not yet waited on by the main stream

@@ -89,52 +89,25 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
                          const GeoInfo* __restrict__ geo, const double* __restrict__ hw,
                          int q, int forcing_id, const double* __restrict__ hostf,
                          double* __restrict__ xphys, double* __restrict__ Gout,
-                         int* __restrict__ err) {
-    // the component of the CTA's first point, found once per CTA (a CTA that
-    // straddles a component boundary: the other threads search themselves);
-    // its index strides and table offsets staged in shared memory
-    __shared__ int s_comp;
-    __shared__ int64_t s_lo, s_hi, s_tot;
-    __shared__ unsigned s_qs[D], s_nq[D];
-    __shared__ int64_t s_toff[D], s_goff[D];
-    const int64_t gid0 = (int64_t)blockIdx.x * blockDim.x;
-    if (threadIdx.x == 0) {
-        const int64_t tot = qp_cum[ncomp];
-        int lo = 0, hi = ncomp;
-        while (hi - lo > 1) {
-            int mid = (lo + hi) >> 1;
-            if (qp_cum[mid] <= gid0) lo = mid; else hi = mid;
-        }
-        s_comp = lo;
-        s_lo = qp_cum[lo];
-        s_hi = qp_cum[lo + 1];
-        s_tot = tot;
-        const CompInfo& C0 = comps[lo];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            s_qs[k] = (unsigned)C0.qs[k];
-            s_nq[k] = (unsigned)C0.nel[k] * (unsigned)q;
-            const TabInfo& T = tabs[C0.tab[k]];
-            s_toff[k] = T.qp_off;
-            s_goff[k] = T.geo_off;
-        }
-    }
-    __syncthreads();
-    const int64_t gid = gid0 + threadIdx.x;
-    if (gid >= s_tot) return;
-    int lo = s_comp;
-    unsigned qsk[D], nqk[D];
-    int64_t toff[D], goff[D];
-    if (gid < s_hi) {
-#pragma unroll
-        for (int k = 0; k < D; ++k) { qsk[k] = s_qs[k]; nqk[k] = s_nq[k]; toff[k] = s_toff[k]; goff[k] = s_goff[k]; }
-    } else {
+                         int* __restrict__ err, const int* __restrict__ cta_comp) {
+    // the component of the CTA's first point from the per-CTA table (no
+    // search, no barrier); a thread past that component's end searches itself
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= qp_cum[ncomp]) return;
+    int lo = cta_comp[blockIdx.x];
+    int64_t base = qp_cum[lo];
+    if (gid >= qp_cum[lo + 1]) {
         int l2 = lo, h2 = ncomp;
         while (h2 - l2 > 1) {
             int mid = (l2 + h2) >> 1;
             if (qp_cum[mid] <= gid) l2 = mid; else h2 = mid;
         }
         lo = l2;
+        base = qp_cum[lo];
+    }
+    unsigned qsk[D], nqk[D];
+    int64_t toff[D], goff[D];
+    {
         const CompInfo& C1 = comps[lo];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
@@ -148,7 +121,7 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
     const CompInfo& C = comps[lo];
     // per-component quadrature index < 2^31 (a component with more points
     // would need > 16 GB of metric): 32-bit index arithmetic
-    const unsigned lin = (unsigned)(gid - (lo == s_comp ? s_lo : qp_cum[lo]));
+    const unsigned lin = (unsigned)(gid - base);
     double w = 1.0;
     const double* bv[D];
     int first[D];
@@ -350,7 +323,7 @@ cudaError_t launch_metric(Handle* h) {
     k_metric<DD><<<(unsigned)blocks, 256, 0, h->stream>>>(                                   \
         h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->d_geob,    \
         h->d_geofirst, h->d_geo, h->d_geo_hw, h->q, h->forcing_id, hostf, h->d_xphys, h->d_G, \
-        h->d_err)
+        h->d_err, h->d_mcomp)
     if (h->d == 1) LAUNCH_METRIC(1);
     else if (h->d == 2) LAUNCH_METRIC(2);
     else LAUNCH_METRIC(3);
