@@ -837,7 +837,12 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
     double* t = tg + C.vec_off;
     const double* b = rhs + C.vec_off;
     const double* val = stencil + C.mat_off;
-    const int* offs = slotoff + C.so_off;
+    // slot column offsets staged in shared memory (the SpMV's gathers then
+    // depend on one global load, not two)
+    __shared__ int soffs[WMAX * WMAX * WMAX];
+    for (int i = tid; i < NS; i += FDL_THREADS) soffs[i] = slotoff[C.so_off + i];
+    __syncthreads();
+    const int* offs = soffs;
     const double* Fac = fdl + fdl_off[c] + 2 * (int64_t)ms * P1;   // k_fdl_factor
 
     // mode product over other axis o (global buffers)
