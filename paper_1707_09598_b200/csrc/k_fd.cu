@@ -778,7 +778,7 @@ k_fdl_factor(const CompInfo* __restrict__ comps, const int* __restrict__ list, i
 }
 
 template <int D>
-__global__ void __launch_bounds__(FDL_THREADS, 2)
+__global__ void __launch_bounds__(FDL_THREADS, 3)
 k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, const int* __restrict__ slotoff,
           const double* __restrict__ stencil, const double* __restrict__ rhs, int p,
           const int64_t* __restrict__ uoff, const double* __restrict__ dU, const double* __restrict__ ckg,
