@@ -412,6 +412,21 @@ static int upload_all(Handle* h) {
     if (!h->fd_comps.empty())
         SG_CUDA(cudaMemcpyAsync(h->d_fdlist, h->fd_comps.data(), sizeof(int) * h->fd_comps.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_bp, h->bp_host.data(), sizeof(double) * h->bp_host.size(), cudaMemcpyHostToDevice, s));
+    {   // open knot vectors: exact metadata of the breakpoints (make_open_knot_vector,
+        // splines.py:83-110 -- [0]*(p+1), interior breakpoints with multiplicity mu,
+        // [1]*(p+1)), uploaded with the descriptor
+        h->knots_host.assign((size_t)h->total_knots, 0.0);
+        for (const TabInfo& T : h->tabs) {
+            const double* b = h->bp_host.data() + T.bp_off;
+            const int nk = 2 * (h->p + 1) + (T.nel - 1) * h->mu;
+            for (int pos = 0; pos < nk; ++pos)
+                h->knots_host[T.knot_off + pos] =
+                    pos <= h->p ? 0.0 : (pos >= nk - (h->p + 1) ? 1.0 : b[1 + (pos - (h->p + 1)) / h->mu]);
+        }
+        if (!h->knots_host.empty())
+            SG_CUDA(cudaMemcpyAsync(h->d_knots, h->knots_host.data(), sizeof(double) * h->knots_host.size(),
+                                    cudaMemcpyHostToDevice, s));
+    }
     SG_CUDA(cudaMemcpyAsync(h->d_geo_knots, h->geo_knots.data(), sizeof(double) * h->geo_knots.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_geo_hw, h->geo_hw.data(), sizeof(double) * h->geo_hw.size(), cudaMemcpyHostToDevice, s));
     // gauss + cumulative index tables
@@ -476,8 +491,7 @@ static int decode_err(Handle* h) {
 static int ensure_tables(Handle* h) {
     if (h->tables_ready) return SGIGA_OK;
     h->kstart(0);
-    SG_CUDA(launch_build_knots(h));
-    SG_CUDA(launch_basis_tables(h));
+    SG_CUDA(launch_basis_tables(h));   // (the knot vectors are uploaded with the descriptor)
     h->kstop(0);
     h->tables_ready = true;
     return SGIGA_OK;

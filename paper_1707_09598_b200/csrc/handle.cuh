@@ -114,6 +114,7 @@ struct Handle {
     double* d_fdl = nullptr;
     double* d_ck = nullptr;
     unsigned* d_ticket = nullptr;
+    std::vector<double> knots_host;          // open knot vectors (host-built, uploaded once)
     std::vector<int> mcomp;                  // component of k_metric's CTA b (first point b * 256)
     int* d_mcomp = nullptr;            // last-CTA ticket of the status-fused combine (kept zero)                  // [ncomp][MAXD] FD metric scales c_k (k_fd_metric_scale)
     cudaStream_t stream2 = nullptr;          // side stream: the eigen kernel overlaps assembly

@@ -11,23 +11,6 @@
 namespace sgiga {
 
 // ---- open knot vectors from breakpoints ---------------------------------
-__global__ void k_build_knots(const TabInfo* __restrict__ tabs, int ntab, int p, int mu,
-                              const double* __restrict__ bp, double* __restrict__ knots) {
-    // one CTA per table, one thread per knot: [0]*(p+1), interior breakpoints
-    // with multiplicity mu, [1]*(p+1)  (splines.py:26-80 make_open_knot_vector)
-    const TabInfo T = tabs[blockIdx.x];
-    double* k = knots + T.knot_off;
-    const double* b = bp + T.bp_off;
-    const int nk = 2 * (p + 1) + (T.nel - 1) * mu;
-    for (int pos = threadIdx.x; pos < nk; pos += blockDim.x) {
-        double v;
-        if (pos <= p) v = 0.0;
-        else if (pos >= nk - (p + 1)) v = 1.0;
-        else v = b[1 + (pos - (p + 1)) / mu];
-        k[pos] = v;
-    }
-}
-
 // ---- basis + geometry-basis tables at every (table, element, node) -------
 __global__ void k_basis_tables(const TabInfo* __restrict__ tabs, int ntab,
                                const int64_t* __restrict__ tab_qp_cum, int p, int mu, int q,
@@ -287,15 +270,6 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
     }
     // load = f * det * w (assembly.py:292)
     Gc[(int64_t)(D * (D + 1) / 2) * nqp + lin] = __dmul_rn(__dmul_rn(f, det), w);
-}
-
-cudaError_t launch_build_knots(Handle* h) {
-    int nt = (int)h->tabs.size();
-    if (nt == 0) return cudaSuccess;
-    k_build_knots<<<nt, 128, 0, h->stream>>>(h->d_tabs, nt, h->p, h->mu, h->d_bp,
-                                                           h->d_knots);
-    h->launches[0]++;
-    return cudaGetLastError();
 }
 
 // tab_qp_cum / qp_cum live right after d_gauss (see handle.cu)

@@ -221,7 +221,6 @@ __device__ __forceinline__ int find_span(const double* __restrict__ k, int nk, i
 // ---- launchers (defined in the .cu files) -------------------------------
 struct Handle;
 
-cudaError_t launch_build_knots(Handle* h);
 cudaError_t launch_basis_tables(Handle* h);
 cudaError_t launch_metric(Handle* h);
 cudaError_t launch_assembly(Handle* h);

@@ -33,8 +33,8 @@ def _launch_table(path: str, cfg: str) -> str:
     iN, iV = hdr.index("Kernel Name"), hdr.index("Metric Value")
     names = [r[iN].split("(")[0] for r in rows]
     # the last step = everything after the last occurrence of the first kernel
-    # of a step (k_build_knots opens every sgiga_run)
-    starts = [i for i, n in enumerate(names) if n.endswith("k_build_knots")]
+    # of a step (k_basis_tables opens every sgiga_run)
+    starts = [i for i, n in enumerate(names) if n.endswith("k_basis_tables")]
     lo = starts[-1] if starts else 0
     sel = [(names[i], float(rows[i][iV].replace(",", ""))) for i in range(lo, len(rows))]
     tot = sum(v for _, v in sel)
