@@ -210,6 +210,15 @@ int sgiga_error_norms(sgiga_handle* h, const double* pts_per_dir,
                       const double* wts_per_dir, const int64_t* npts_per_dir,
                       int32_t solution_id, double* out);
 
+/* Parity export of kernel 1's output for one (axis, level) knot vector, as
+ * assembly._direction_tables (assembly.py:209-234) returns it: basis values
+ * and first derivatives [nel][q][p+1], Gauss points xi [nel*q] and weights
+ * h*w_g [nel*q].  nel_out receives the element count; pass NULL arrays to
+ * query it.  The tables are the ones the last assembly pass computed on the
+ * device (SGIGA_ERR_STATE before any assembly).                           */
+int sgiga_basis_table(sgiga_handle* h, int32_t axis, int32_t level, int32_t* nel_out, double* vals,
+                      double* ders, double* pts, double* wts);
+
 /* Parity export of one component: interior CSR (C-order rows, sorted
  * columns, exact zeros dropped as scipy's csr addition does) and rhs.
  * Call with indices/data NULL to get nnz first.                          */

@@ -19,6 +19,27 @@ namespace sgiga {
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+static bool env_on(const char* name) {
+    const char* e = getenv(name);
+    return e && e[0] == '1';
+}
+Options Options::from_env() {
+    Options o;
+    o.no_fd = env_on("SGIGA_NO_FD");
+    o.generic_assembly = env_on("SGIGA_GENERIC_ASSEMBLY");
+    o.no_tma = env_on("SGIGA_NO_TMA");
+    o.no_ktimes = env_on("SGIGA_NO_KTIMES");
+    o.run_graph = env_on("SGIGA_RUN_GRAPH") && !env_on("SGIGA_NO_GRAPH");
+    o.no_cluster = env_on("SGIGA_NO_CLUSTER");
+    o.combine_nosort = env_on("SGIGA_COMBINE_NOSORT");
+    o.combine_perthread = env_on("SGIGA_COMBINE_PERTHREAD");
+    o.asm_profile = env_on("SGIGA_ASM_PROFILE");
+    o.fd_profile = env_on("SGIGA_FD_PROFILE");
+    o.pcg_profile = env_on("SGIGA_PCG_PROFILE");
+    o.pcg_trace = env_on("SGIGA_PCG_TRACE");
+    return o;
+}
+
 size_t assembly_smem_bytes(const Handle* h);
 
 // cumulative tables stored behind d_gauss: [2q] gauss, then
@@ -43,10 +64,11 @@ static void free_all(Handle* h) {
                     h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_coef, h->d_cg, h->d_part, h->d_err,
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
                     h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps,
-                    h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck, h->d_ticket, h->d_mcomp};
+                    h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck, h->d_ticket, h->d_mcomp,
+                    h->d_spts, h->d_sout};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel};
+    void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel, h->h_sticky};
     for (void* p : hptrs)
         if (p) cudaFreeHost(p);
     for (auto& e : h->evp)
@@ -178,8 +200,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
             int64_t rows_c = 1;
             bool fd_axes = true;
             for (int k = 0; k < d; ++k) { rows_c *= std::max(0, C.m[k]); fd_axes = fd_axes && C.m[k] <= FD_MMAX; }
-            const char* ss_env = getenv("SGIGA_STREAM_LONG");
-            if (d >= 2 && fd_axes && rows_c <= 2048 && !(ss_env && ss_env[0] == '1')) {
+            if (d >= 2 && fd_axes && rows_c <= 2048) {
                 int mmin = 1 << 30;
                 for (int k = d - 1; k >= 0; --k)
                     if (C.m[k] < mmin) { mmin = C.m[k]; s = k; }
@@ -247,8 +268,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
     // one-CTA eigen kernel (<= FD_MMAX interior functions) and whose vectors
     // fit shared memory; the others keep the Jacobi-PCG paths
     {
-        const char* nofd = getenv("SGIGA_NO_FD");
-        const bool fd_on = !(nofd && nofd[0] == '1');
+        const bool fd_on = !h->opt.no_fd;
         const int ntab = (int)h->tabs.size();
         h->fd_comps.clear(); h->fd_uniq.clear();
         h->fd_uoff.assign(ntab, 0); h->fd_loff.assign(ntab, 0);
@@ -323,8 +343,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const double slots = 2.0 * nsm, setup = 2.0;   // 2 resident CTAs/SM; setup in elements
     int SEG = 1 << 20;
-    if (const char* e = getenv("SGIGA_ASM_SEG")) SEG = std::max(1, atoi(e));
-    else {
+    {
         double best = 1e300;
         for (int cand : {1 << 20, 128, 64, 48, 32, 24, 16, 12, 8, 6, 4}) {
             double tot = 0, mx = 0;
@@ -602,6 +621,8 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
         ea = cudaHostAlloc(reinterpret_cast<void**>(&h->h_cg), sizeof(CgState) * std::max(1, h->ncomp), cudaHostAllocMapped);
     if (ea == cudaSuccess)
         ea = cudaHostAlloc(reinterpret_cast<void**>(&h->h_rel), sizeof(double) * std::max(1, h->ncomp), cudaHostAllocMapped);
+    if (ea == cudaSuccess) ea = cudaHostAlloc(reinterpret_cast<void**>(&h->h_sticky), sizeof(int), cudaHostAllocMapped);
+    if (ea == cudaSuccess) { *h->h_sticky = 0; ea = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_sticky), h->h_sticky, 0); }
     if (ea == cudaSuccess) ea = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_err), h->h_err, 0);
     if (ea == cudaSuccess) ea = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_cg), h->h_cg, 0);
     if (ea == cudaSuccess) ea = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_rel), h->h_rel, 0);
@@ -624,10 +645,8 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     st = upload_all(h);
     if (st) { free_all(h); delete h; return st; }
     h->iters.assign(h->ncomp, 0);
-    const char* gen = getenv("SGIGA_GENERIC_ASSEMBLY");
-    h->force_generic_assembly = gen && gen[0] == '1';
-    const char* nk = getenv("SGIGA_NO_KTIMES");
-    h->ktimes = !(nk && nk[0] == '1');
+    h->force_generic_assembly = h->opt.generic_assembly;
+    h->ktimes = !h->opt.no_ktimes;
     *out = reinterpret_cast<sgiga_handle*>(h);
     return SGIGA_OK;
 }
@@ -818,9 +837,16 @@ static int solve_finish(Handle* h, int32_t* iters_out, double* relres_out) {
     return status;
 }
 
-static int ensure_scratch(double** buf, size_t* cap, size_t n) {
+// per-handle staging buffers (allocated on the handle's device).  A buffer
+// that grows while passes of this handle are still in flight is freed only
+// after the handle's streams drain.
+static int ensure_scratch(Handle* h, double** buf, size_t* cap, size_t n) {
     if (*cap >= n && *buf) return SGIGA_OK;
-    if (*buf) cudaFree(*buf);
+    if (*buf) {
+        SG_CUDA(cudaStreamSynchronize(h->stream));
+        SG_CUDA(cudaStreamSynchronize(h->stream3));
+        cudaFree(*buf);
+    }
     *buf = nullptr;
     *cap = 0;
     SG_CUDA(cudaMalloc(reinterpret_cast<void**>(buf), std::max<size_t>(n, 1) * sizeof(double)));
@@ -828,20 +854,15 @@ static int ensure_scratch(double** buf, size_t* cap, size_t n) {
     return SGIGA_OK;
 }
 
-static thread_local double* s_pts = nullptr;
-static thread_local size_t s_pts_cap = 0;
-static thread_local double* s_out = nullptr;
-static thread_local size_t s_out_cap = 0;
-
 // host points -> device scratch (device = 0 / -1 of sgiga_combine_points)
 static int stage_points(Handle* h, const double* pts, int64_t npts, size_t nout, const double** dp,
                         double** dout) {
     int st;
-    if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
-    if ((st = ensure_scratch(&s_out, &s_out_cap, nout))) return st;
-    SG_CUDA(cudaMemcpyAsync(s_pts, pts, sizeof(double) * npts * h->d, cudaMemcpyHostToDevice, h->stream));
-    *dp = s_pts;
-    *dout = s_out;
+    if ((st = ensure_scratch(h, &h->d_spts, &h->spts_cap, (size_t)npts * h->d))) return st;
+    if ((st = ensure_scratch(h, &h->d_sout, &h->sout_cap, nout))) return st;
+    SG_CUDA(cudaMemcpyAsync(h->d_spts, pts, sizeof(double) * npts * h->d, cudaMemcpyHostToDevice, h->stream));
+    *dp = h->d_spts;
+    *dout = h->d_sout;
     return SGIGA_OK;
 }
 
@@ -884,6 +905,7 @@ int sgiga_solve(sgiga_handle* hh, double rtol, int32_t maxit, int32_t* iters_out
     if (st) return st;
     SG_CUDA(launch_status(h));
     SG_CUDA(cudaStreamSynchronize(h->stream));   // h_cg / h_rel / h_err are valid after it
+    *h->h_sticky = 0;                            // this call's verdict is solve_finish's
     if ((st = decode_err(h))) return st;
     return solve_finish(h, iters_out, relres_out);
 }
@@ -892,14 +914,8 @@ int sgiga_solve(sgiga_handle* hh, double rtol, int32_t maxit, int32_t* iters_out
 // passes enqueued back to back hide the host launch cost anyway (cfg2 0.248
 // ms/pass direct vs 0.251 replayed), and in a replayed graph the side-stream
 // FD set-up did not overlap the assembly (cfg5 +1 ms)
-static bool run_graphs_enabled() {
-    const char* on = getenv("SGIGA_RUN_GRAPH");
-    if (!(on && on[0] == '1')) return false;
-    for (const char* k : {"SGIGA_NO_GRAPH", "SGIGA_PCG_PROFILE", "SGIGA_ASM_PROFILE", "SGIGA_PCG_TRACE"}) {
-        const char* e = getenv(k);
-        if (e && e[0] && !(e[0] == '0' && e[1] == 0)) return false;
-    }
-    return true;
+static bool run_graphs_enabled(const Handle* h) {
+    return h->opt.run_graph && !h->opt.pcg_profile && !h->opt.asm_profile && !h->opt.pcg_trace;
 }
 
 // enqueue of one whole pass (device pointers): direct launches, capture, or
@@ -907,6 +923,7 @@ static bool run_graphs_enabled() {
 static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, int64_t npts, double* dout,
                        const double* hsrc = nullptr) {
     int st;
+    if (!(rtol > 0.0)) { set_error("rtol must be positive"); return SGIGA_ERR_VALUE; }   // before any launch
     auto enqueue_all = [&]() -> int {
         // the combine's point sort depends on the points only: side stream,
         // overlapping assembly and solve
@@ -937,7 +954,7 @@ static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, 
     };
     // whole-run graph: only when the solve has no host-driven loop (every
     // component on the single-launch small path) and no profiling knob is on
-    const bool can_graph = run_graphs_enabled() && h->large_comps.empty() && !h->graph_broken;
+    const bool can_graph = run_graphs_enabled(h) && h->large_comps.empty() && !h->graph_broken;
     const bool same = can_graph && h->rkey.npts == npts && h->rkey.rtol == rtol && h->rkey.maxit == maxit &&
                       h->rkey.dp == dp && h->rkey.dout == dout && h->rkey.hp == hsrc;
     if (same && h->run_exec) {
@@ -985,12 +1002,22 @@ static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, 
 // the one synchronisation of a pass and its verdict
 static int run_finish(Handle* h, int32_t* iters_out, double* relres_out) {
     SG_CUDA(cudaStreamSynchronize(h->stream));
+    // every pass since the last verdict OR-ed its failure into the sticky
+    // word: a pipelined pass that failed before the last one is reported too
+    const int sticky = *reinterpret_cast<volatile int*>(h->h_sticky);
+    *h->h_sticky = 0;
     int st = decode_err(h);
     if (st) return st;
     SG_CUDA(h->elapsed(&h->ms[0], Handle::PHASE_EV + 0, Handle::PHASE_EV + 1));
     h->assembled = true;
     st = solve_finish(h, iters_out, relres_out);
     if (h->run_npts > 0) SG_CUDA(h->elapsed(&h->ms[2], Handle::PHASE_EV + 4, Handle::PHASE_EV + 5));
+    if (!st && sticky) {
+        set_error((sticky & 2) ? "an earlier pipelined pass raised a device error flag"
+                               : "an earlier pipelined pass failed the solver acceptance (non-finite, not "
+                                 "converged, or relative residual > 1e-10)");
+        st = (sticky & 2) ? SGIGA_ERR_VALUE : SGIGA_ERR_SOLVE;
+    }
     return st;
 }
 
@@ -1008,10 +1035,10 @@ int sgiga_run(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts, i
         const bool pinned = cudaPointerGetAttributes(&pa, pts) == cudaSuccess && pa.type == cudaMemoryTypeHost;
         cudaGetLastError();
         if (pinned) {   // uploaded on the point-sort side stream inside the pass
-            if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
-            if ((st = ensure_scratch(&s_out, &s_out_cap, (size_t)npts))) return st;
-            dp = s_pts;
-            dout = s_out;
+            if ((st = ensure_scratch(h, &h->d_spts, &h->spts_cap, (size_t)npts * h->d))) return st;
+            if ((st = ensure_scratch(h, &h->d_sout, &h->sout_cap, (size_t)npts))) return st;
+            dp = h->d_spts;
+            dout = h->d_sout;
             hsrc = pts;
         } else if ((st = stage_points(h, pts, npts, (size_t)npts, &dp, &dout))) {
             return st;
@@ -1044,10 +1071,10 @@ int sgiga_run_host_async(sgiga_handle* hh, double rtol, int32_t maxit, const dou
             cudaGetLastError();
             if (!pinned) { set_error("sgiga_run_host_async: points and output must be page-locked host memory"); return SGIGA_ERR_VALUE; }
         }
-        if ((st = ensure_scratch(&s_pts, &s_pts_cap, (size_t)npts * h->d))) return st;
-        if ((st = ensure_scratch(&s_out, &s_out_cap, (size_t)npts))) return st;
-        dp = s_pts;
-        dout = s_out;
+        if ((st = ensure_scratch(h, &h->d_spts, &h->spts_cap, (size_t)npts * h->d))) return st;
+        if ((st = ensure_scratch(h, &h->d_sout, &h->sout_cap, (size_t)npts))) return st;
+        dp = h->d_spts;
+        dout = h->d_sout;
     }
     // the H2D of the points runs on the point-sort side stream inside the pass
     // (ordered after the previous pass's combine by the pass's fork event);
@@ -1232,6 +1259,29 @@ int sgiga_export_csr(sgiga_handle* hh, int32_t comp, int64_t* nnz_out, int64_t* 
         if (indptr) indptr[ref + 1] = nnz;
     }
     *nnz_out = nnz;
+    return SGIGA_OK;
+}
+
+int sgiga_basis_table(sgiga_handle* hh, int32_t axis, int32_t level, int32_t* nel_out, double* vals,
+                      double* ders, double* pts, double* wts) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !nel_out) { set_error("null argument"); return SGIGA_ERR_VALUE; }
+    if (axis < 0 || axis >= h->d || level < 0 || level > h->max_level) {
+        set_error("axis / level out of range");
+        return SGIGA_ERR_VALUE;
+    }
+    const int t = h->tab_of[(size_t)axis * (h->max_level + 1) + level];
+    if (t < 0) { set_error("no component of the plan uses this (axis, level)"); return SGIGA_ERR_KEY; }
+    const TabInfo& T = h->tabs[t];
+    *nel_out = T.nel;
+    if (!vals && !ders && !pts && !wts) return SGIGA_OK;
+    if (!h->assembled && !h->tables_ready) { set_error("basis tables before assembly"); return SGIGA_ERR_STATE; }
+    SG_CUDA(cudaStreamSynchronize(h->stream));
+    const size_t nv = (size_t)T.nel * h->q * (h->p + 1), nq = (size_t)T.nel * h->q;
+    if (vals) SG_CUDA(cudaMemcpy(vals, h->d_tabvals + T.val_off, sizeof(double) * nv, cudaMemcpyDeviceToHost));
+    if (ders) SG_CUDA(cudaMemcpy(ders, h->d_tabvals + T.val_off + nv, sizeof(double) * nv, cudaMemcpyDeviceToHost));
+    if (pts) SG_CUDA(cudaMemcpy(pts, h->d_qx + T.qp_off, sizeof(double) * nq, cudaMemcpyDeviceToHost));
+    if (wts) SG_CUDA(cudaMemcpy(wts, h->d_qw + T.qp_off, sizeof(double) * nq, cudaMemcpyDeviceToHost));
     return SGIGA_OK;
 }
 

@@ -30,8 +30,27 @@ struct LaunchCount {
     operator long long() const { return n; }
 };
 
+// Developer / test switches, read ONCE from the environment when a handle
+// is created (never on a launch path).  Defaults are the product path.
+struct Options {
+    bool no_fd = false;             // SGIGA_NO_FD=1: Jacobi-PCG instead of FD-PCG (parity tests)
+    bool generic_assembly = false;  // SGIGA_GENERIC_ASSEMBLY=1: runtime-size assembly kernel (parity tests)
+    bool no_tma = false;            // SGIGA_NO_TMA=1: cp.async plane copies instead of TMA (parity tests)
+    bool no_ktimes = false;         // SGIGA_NO_KTIMES=1: no kernel-group timing events
+    bool run_graph = false;         // SGIGA_RUN_GRAPH=1 (and no SGIGA_NO_GRAPH): whole-pass CUDA graphs
+    bool no_cluster = false;        // SGIGA_NO_CLUSTER=1: chunked Jacobi-PCG for the small comps (tests)
+    bool combine_nosort = false;    // SGIGA_COMBINE_NOSORT=1: no cell sort of the points (tests)
+    bool combine_perthread = false; // SGIGA_COMBINE_PERTHREAD=1: per-thread combine kernel (tests)
+    bool asm_profile = false;       // SGIGA_ASM_PROFILE=1: block-0 stage cycles to stderr (probe)
+    bool fd_profile = false;        // SGIGA_FD_PROFILE=1: FD phase cycles to stderr (probe)
+    bool pcg_profile = false;       // SGIGA_PCG_PROFILE=1 (probe)
+    bool pcg_trace = false;         // SGIGA_PCG_TRACE=1 (probe)
+    static Options from_env();
+};
+
 struct Handle {
     int dev = 0;
+    Options opt = Options::from_env();
     cudaStream_t stream = nullptr;
     bool own_stream = false;
 
@@ -112,11 +131,11 @@ struct Handle {
     int* d_fdl_list = nullptr;
     int64_t* d_fdl_off = nullptr;
     double* d_fdl = nullptr;
-    double* d_ck = nullptr;
-    unsigned* d_ticket = nullptr;
+    double* d_ck = nullptr;                  // [ncomp][MAXD] FD metric scales c_k (k_fd_metric_scale)
+    unsigned* d_ticket = nullptr;            // last-CTA ticket of the status-fused combine (kept zero)
     std::vector<double> knots_host;          // open knot vectors (host-built, uploaded once)
     std::vector<int> mcomp;                  // component of k_metric's CTA b (first point b * 256)
-    int* d_mcomp = nullptr;            // last-CTA ticket of the status-fused combine (kept zero)                  // [ncomp][MAXD] FD metric scales c_k (k_fd_metric_scale)
+    int* d_mcomp = nullptr;                  // k_metric: component of each 256-point CTA
     cudaStream_t stream2 = nullptr;          // side stream: the eigen kernel overlaps assembly
     cudaEvent_t fd_fork = nullptr, fd_join = nullptr, fd_metric = nullptr;
     bool fd_pending = false;                 // fd_join not yet waited on by the main stream
@@ -128,11 +147,18 @@ struct Handle {
     int64_t run_npts = 0;          // points of the last enqueued sgiga_run pass
     int* d_cperm = nullptr;        // combine: cell-order permutation of the points
     size_t cperm_cap = 0;
-    int* d_chist = nullptr;        // combine: cell histogram / cursors
+    int* d_chist = nullptr;        // combine: cell histogram / cursors (zeroed by every sort)
+    double* d_spts = nullptr;      // staging of host points (sgiga_run / _combine_points), per handle
+    size_t spts_cap = 0;
+    double* d_sout = nullptr;      // staging of the values read back to the host, per handle
+    size_t sout_cap = 0;
     int* h_pinned_flag = nullptr;  // pinned host mirror of the active count
     int* h_err = nullptr;          // mapped pinned mirrors read after the one sync of a call
     CgState* h_cg = nullptr;
     double* h_rel = nullptr;
+    int* h_sticky = nullptr;       // failure word OR-ed by every pass's status writer (mapped)
+    int* dh_sticky = nullptr;
+    int passes_pending = 0;        // passes enqueued since the last verdict
     int* dh_err = nullptr;         // ... and their device-side addresses
     CgState* dh_cg = nullptr;
     double* dh_rel = nullptr;

@@ -145,7 +145,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 const Pencil* __restrict__ pencils, const double* __restrict__ vals,
                 const double* __restrict__ Gbuf, double* __restrict__ stencil,
                 double* __restrict__ rhs, double* __restrict__ dinv, long long* __restrict__ prof,
-                const CUtensorMap* __restrict__ tmaps, int dbg) {
+                const CUtensorMap* __restrict__ tmaps) {
     using F = FastCfg<D, P, Q, TM>;
     constexpr int NT = F::NT;
     constexpr int p = F::p, W = F::W;
@@ -442,7 +442,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     const double* Gw = sm + F::oGw + (j % F::NGB) * F::sGw + tsh;
                     double* S1w = S1 + (j & 1) * F::nS1;
                     const int half = F::PPW == 2 ? (lane >> 4) : 0;
-                    const int xa = (dbg & 1) ? 32 : (F::PPW == 2 ? (lane & 15) : lane);
+                    const int xa = F::PPW == 2 ? (lane & 15) : lane;
                     const int unit = warp * F::PPW + half;
                     const int prr = unit < F::NGRP ? 0 : (unit == F::NGRP ? NPAIR : NPAIR + 1);   // load unit -> NPAIR
                     if (unit < F::NGRP && xa < F::NA) {
@@ -503,7 +503,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     }
                 }
             } else if (inG2) {
-                if (j >= 1 && j <= nplanes && !(dbg & 2)) {   // ---- stage 2 (plane j-1): contract tile axis a ----
+                if (j >= 1 && j <= nplanes) {   // ---- stage 2 (plane j-1): contract tile axis a ----
                     const int b2 = (j - 1) & 1;
                     const double* S1r = S1 + b2 * F::nS1;
                     double* S2w = S2 + b2 * F::NI2;
@@ -566,8 +566,8 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     }
                 }
             } else {
-                if (j < nplanes && j > 0 && j % Q == 0 && !(dbg & 16)) load_bs(e_first + j / Q);
-                if (j >= 2 && !(dbg & 4)) {   // ---- stage 3 (plane j-2): rank-1 updates ----
+                if (j < nplanes && j > 0 && j % Q == 0) load_bs(e_first + j / Q);
+                if (j >= 2) {   // ---- stage 3 (plane j-2): rank-1 updates ----
                     // thread (s_a, s_b) keeps the P x P (row al, column bl) sums
                     // of the current stream element in registers and folds them
                     // into the shared ring once per element
@@ -617,7 +617,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                         bar3();
                         if (ep < e_last) {
                             if (ep >= r0 && ep < r1) {
-                                if (!(dbg & 8)) flush3(ep);
+                                flush3(ep);
                                 bar3();
                                 double* accz = Acc + ((ep % F::RING) * W) * F::WAB;
                                 for (int it = g3t; it < W * F::WAB; it += S3T) accz[it] = 0.0;
@@ -864,8 +864,8 @@ static bool build_tmaps(Handle* h, int NX) {
 bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     if (h->mu != 1 || h->q != h->p + 1 || h->pencils.empty()) return false;
     const int key = h->d * 10 + (h->p + 1);
-    const char* nt = getenv("SGIGA_NO_TMA");
-    const bool tma = h->d == 3 && !(nt && nt[0] == '1') &&
+    const bool no_tma = h->opt.no_tma;
+    const bool tma = h->d == 3 && !no_tma &&
                      build_tmaps(h, (h->p + 1) * h->q);
     size_t smem = 0;
     const void* fn = nullptr;
@@ -892,18 +892,13 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     *err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (*err != cudaSuccess) return true;
     long long* prof = nullptr;
-    // SGIGA_ASM_DBG (timing experiments only, wrong results): bit 0/1/2 skip
-    // stage 1/2/3 of the 3-D pipeline
-    const char* de = getenv("SGIGA_ASM_DBG");
-    int dbg = de ? atoi(de) : 0;
-    const char* pe = getenv("SGIGA_ASM_PROFILE");
-    if (pe && pe[0] == '1') {
+    if (h->opt.asm_profile) {
         cudaMalloc(&prof, 8 * sizeof(long long));
         cudaMemsetAsync(prof, 0, 8 * sizeof(long long), h->stream);
     }
     void* args[] = {(void*)&h->d_comps, (void*)&h->d_tabs, (void*)&h->d_pencils, (void*)&h->d_tabvals,
                     (void*)&h->d_G, (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv,
-                    (void*)&prof, (void*)&h->d_tmaps, (void*)&dbg};
+                    (void*)&prof, (void*)&h->d_tmaps};
     *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(nthreads), args, smem, h->stream);
     if (prof) {
         long long t[8];

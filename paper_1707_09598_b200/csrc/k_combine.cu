@@ -285,12 +285,19 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
         __syncthreads();
         if (last) {
             __threadfence();
+            int fail = 0;
             for (int c = tid; c < sf.ncomp; c += NTH) {
-                sf.hst[c] = sf.st[c];
-                sf.hrel[c] = sf.relres[c];
+                const CgState s = sf.st[c];
+                const double rel = sf.relres[c];
+                sf.hst[c] = s;
+                sf.hrel[c] = rel;
+                fail |= cg_failed(s, rel);
             }
+            fail = __syncthreads_or(fail);
             if (tid == 0) {
-                *sf.herr = *reinterpret_cast<volatile int*>(err);
+                const int e = *reinterpret_cast<volatile int*>(err);
+                *sf.herr = e;
+                *sf.hsticky |= (fail ? 1 : 0) | (e ? 2 : 0);
                 *sf.ticket = 0u;
             }
             __threadfence_system();
@@ -571,8 +578,7 @@ __global__ void k_sum_partials(const double* __restrict__ partials, int64_t nblo
 
 cudaError_t launch_combine_sort(Handle* h, const double* d_pts, int64_t npts, cudaStream_t s, bool* sorted) {
     *sorted = false;
-    const char* ns = getenv("SGIGA_COMBINE_NOSORT");
-    if (npts < 2048 || npts >= (int64_t)1 << 31 || (ns && ns[0] == '1')) return cudaSuccess;
+    if (npts < 2048 || npts >= (int64_t)1 << 31 || h->opt.combine_nosort) return cudaSuccess;
     cudaError_t e;
     if ((size_t)npts > h->cperm_cap) {
         if (h->d_cperm) cudaFree(h->d_cperm);
@@ -581,8 +587,10 @@ cudaError_t launch_combine_sort(Handle* h, const double* d_pts, int64_t npts, cu
         if ((e = cudaMalloc(&h->d_cperm, sizeof(int) * npts)) != cudaSuccess) return e;
         h->cperm_cap = (size_t)npts;
     }
-    // d_chist is zero here: zeroed at create, re-zeroed by the combine kernel
-    // after every sorted launch
+    // the histogram is zeroed on the sort's own stream by every sort: a pass
+    // that never reached its combine (an error after the sort was enqueued,
+    // the per-thread combine) must not leave stale cursors behind
+    if ((e = cudaMemsetAsync(h->d_chist, 0, sizeof(int) * COMBINE_SORT_BINS, s)) != cudaSuccess) return e;
     const unsigned sb = (unsigned)((npts + 255) / 256);
     if (h->d == 1) k_cell_hist<1><<<sb, 256, 0, s>>>(d_pts, npts, h->d_chist);
     else if (h->d == 2) k_cell_hist<2><<<sb, 256, 0, s>>>(d_pts, npts, h->d_chist);
@@ -601,7 +609,7 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
     if (npts == 0) return cudaSuccess;
     StatusFuse sf{};
     if (status_fused && !per_component && h->d_ticket) {
-        sf = StatusFuse{h->d_cg, h->d_relres, h->ncomp, h->dh_cg, h->dh_rel, h->dh_err, h->d_ticket};
+        sf = StatusFuse{h->d_cg, h->d_relres, h->ncomp, h->dh_cg, h->dh_rel, h->dh_err, h->dh_sticky, h->d_ticket};
         *status_fused = true;
     }
     const int ntab = (int)h->tabs.size(), P = h->p + 1;
@@ -615,8 +623,7 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
     const bool small_cta = h->ncomp <= 64 && h->p <= 3;
     int npt = small_cta ? 32 : 64;
     while (npt > 1 && smem_of(npt) > 100 * 1024) npt >>= 1;
-    const char* ev = getenv("SGIGA_COMBINE_PERTHREAD");
-    if (smem_of(npt) > 200 * 1024 || (ev && ev[0] == '1')) {   // huge plans: one thread per point
+    if (smem_of(npt) > 200 * 1024 || h->opt.combine_perthread) {   // huge plans: one thread per point
         unsigned blocks = (unsigned)((npts + 127) / 128);
 #define LAUNCH_CP(DD, PP)                                                                     \
     k_combine_points<DD, PP><<<blocks, 128, 0, h->stream>>>(h->d_comps, h->ncomp, h->d_tabs,   \

@@ -1048,11 +1048,10 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
 cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
     const int n = (int)h->fdl_comps.size();
     if (n == 0) return cudaSuccess;
-    int64_t rmax = 0;
-    for (int c : h->fdl_comps) rmax = std::max<int64_t>(rmax, h->comps[c].rows);
-    int K = 8;   // cluster CTAs per component: >= 512 rows per CTA
-    while (K > 1 && rmax / K < 512) K >>= 1;
-    if (const char* fk = getenv("SGIGA_FDL_K")) K = std::max(1, std::min(8, atoi(fk)));
+    // cluster CTAs per component: a constant, so a component's reduction
+    // order (and its bits) never depends on which other components share
+    // the batch (a rank's subset of a plan computes what the full plan does)
+    const int K = 8;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(n * K));
     cfg.blockDim = dim3(FDL_THREADS);
@@ -1155,8 +1154,7 @@ cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     const int nu = (int)h->fd_uniq.size();
     long long* prof = nullptr;
-    const char* pe = getenv("SGIGA_FD_PROFILE");   // per-CTA phase cycles (probe only)
-    if (pe && pe[0] == '1') {
+    if (h->opt.fd_profile) {   // per-CTA phase cycles (probe only)
         if ((e = cudaMalloc(&prof, sizeof(long long) * 8 * nu)) != cudaSuccess) return e;
         cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * nu, s);
     }
@@ -1184,8 +1182,7 @@ cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit) {
     for (int c : h->fd_comps) smem = std::max(smem, fd_comp_smem(h->comps[c], h->d));
     cudaError_t e;
     long long* prof = nullptr;
-    const char* pe = getenv("SGIGA_FD_PROFILE");   // per-CTA phase cycles (probe only)
-    if (pe && pe[0] == '1') {
+    if (h->opt.fd_profile) {   // per-CTA phase cycles (probe only)
         if ((e = cudaMalloc(&prof, sizeof(long long) * 8 * n)) != cudaSuccess) return e;
         cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * n, h->stream);
     }

@@ -457,7 +457,7 @@ size_t small_smem_bytes(const Handle* h, int64_t* smem_doubles) {
 int run_pcg(Handle* h, double rtol, int maxit) {
     ChunkCtx X = make_ctx(h, rtol, maxit);
     int nch = (int)h->chunks.size();
-    const char* nc = getenv("SGIGA_NO_CLUSTER");
+    const bool no_cluster = h->opt.no_cluster;
     h->small_checked = false;
     const bool any_fd = !h->fd_comps.empty() || !h->fdl_comps.empty();
     if (any_fd) {   // FD-preconditioned CG (k_fd.cu), which also checks its true residuals
@@ -470,7 +470,7 @@ int run_pcg(Handle* h, double rtol, int maxit) {
         SG_CUDA(launch_pcg_fdl(h, rtol, maxit));   // one long axis: banded line solves
         if (h->small_comps.empty()) h->kstop(3);
     }
-    if (!h->small_comps.empty() && !(nc && nc[0] == '1')) {
+    if (!h->small_comps.empty() && !no_cluster) {
         h->small_checked = true;   // the cluster kernel also computes the true residual
         if (!any_fd) h->kstart(3);
         int st = launch_pcg_cluster(h, rtol, maxit);   // k_pcg_cluster.cu
@@ -540,8 +540,7 @@ int run_pcg(Handle* h, double rtol, int maxit) {
         int st = capture(grid);
         if (st) return st;
         int max_rounds = maxit / GRAPH_ITERS + 2;
-        const char* tr = getenv("SGIGA_PCG_TRACE");
-        const bool trace = tr && tr[0] == '1';
+        const bool trace = h->opt.pcg_trace;
         cudaEvent_t tev0 = nullptr, tev1 = nullptr;
         if (trace) { cudaEventCreate(&tev0); cudaEventCreate(&tev1); cudaEventRecord(tev0, h->stream); }
         for (int round = 0; round < max_rounds; ++round) {
@@ -584,12 +583,20 @@ __global__ void k_solve_prologue(CgState* __restrict__ st, int ncomp, int* __res
 
 // solver state, true residuals and the error flags -> mapped host memory
 __global__ void k_status(const CgState* __restrict__ st, const double* __restrict__ relres,
-                         const int* __restrict__ err, int ncomp, CgState* hst, double* hrel, int* herr) {
+                         const int* __restrict__ err, int ncomp, CgState* hst, double* hrel, int* herr,
+                         int* hsticky) {
+    int fail = 0;
     for (int c = threadIdx.x; c < ncomp; c += blockDim.x) {
-        hst[c] = st[c];
+        const CgState s = st[c];
+        hst[c] = s;
         hrel[c] = relres[c];
+        fail |= cg_failed(s, relres[c]);
     }
-    if (threadIdx.x == 0) *herr = *err;
+    fail = __syncthreads_or(fail);
+    if (threadIdx.x == 0) {
+        *herr = *err;
+        *hsticky |= (fail ? 1 : 0) | (*err ? 2 : 0);
+    }
     __threadfence_system();
 }
 
@@ -600,7 +607,8 @@ cudaError_t launch_solve_prologue(Handle* h, cudaStream_t stream) {
 }
 
 cudaError_t launch_status(Handle* h) {
-    k_status<<<1, 256, 0, h->stream>>>(h->d_cg, h->d_relres, h->d_err, h->ncomp, h->dh_cg, h->dh_rel, h->dh_err);
+    k_status<<<1, 256, 0, h->stream>>>(h->d_cg, h->d_relres, h->d_err, h->ncomp, h->dh_cg, h->dh_rel, h->dh_err,
+                                       h->dh_sticky);
     h->launches[1]++;
     return cudaGetLastError();
 }

@@ -276,11 +276,10 @@ k_pcg_cg1(const CompInfo* __restrict__ comps, const int* __restrict__ list,
 int launch_pcg_cluster(Handle* h, double rtol, int maxit) {
     const int ns = (int)h->small_comps.size();
     if (ns == 0) return SGIGA_OK;
-    int64_t rmax = 0;
-    for (int c : h->small_comps) rmax = std::max<int64_t>(rmax, h->comps[c].rows);
-    int K = 8;   // as many SMs as the batch leaves, >= 32 rows per CTA
-    while (K > 1 && (K * ns > 148 || rmax / K < 32)) K >>= 1;
-    if (const char* fk = getenv("SGIGA_CLUSTER_K")) K = std::max(1, std::min(8, atoi(fk)));
+    // cluster CTAs per component: a constant, so a component's reduction
+    // order (and its bits) never depends on which other components share
+    // the batch (a rank's subset of a plan computes what the full plan does)
+    const int K = 8;
     const int64_t limit = (224 * 1024) / 8;
     int64_t total = 0;
     for (int c : h->small_comps) {
@@ -304,8 +303,7 @@ int launch_pcg_cluster(Handle* h, double rtol, int maxit) {
     cfg.numAttrs = 1;
     const double rt2 = rtol * rtol;
     const int sd = (int)total;
-    const char* pe = getenv("SGIGA_PCG_PROFILE");
-    const int pslot = pe ? atoi(pe) : -1;
+    const int pslot = h->opt.pcg_profile ? 0 : -1;
     long long* dprof = nullptr;
     if (pslot >= 0) {
         SG_CUDA(cudaMalloc(&dprof, 8 * sizeof(long long)));

@@ -88,8 +88,10 @@ struct StatusFuse {
     CgState* hst;
     double* hrel;
     int* herr;
+    int* hsticky;       // failure word OR-ed over pipelined passes (mapped host memory)
     unsigned* ticket;   // nullptr: not fused
 };
+
 
 struct Pencil {         // one CTA of the assembly kernel
     int comp;
@@ -109,6 +111,13 @@ struct CgState {
     int it, active, conv, pad;
     unsigned int cnt1, cnt2;
 };
+
+// a component's pass failed (linsolve.py:47-53 verdict, evaluated on the
+// device so pipelined passes can OR it into a sticky word)
+__device__ __forceinline__ bool cg_failed(const CgState& s, double rel) {
+    if (s.bb == 0.0) return false;   // empty interior / zero right-hand side
+    return !isfinite(rel) || !s.conv || rel > 1e-10;
+}
 
 // ---- Cox-de Boor (NURBS book A2.3) with the reference's rounding -------
 // splines.py:172-224.  __dadd_rn/__dmul_rn keep nvcc from contracting

@@ -320,6 +320,19 @@ class Batch:
         mat = sps.csr_matrix((data[:n], indices[:n], indptr), shape=(rows, rows))
         return mat, rhs[:rows]
 
+    def basis_table(self, axis: int, level: int):
+        """Kernel 1's device output for one (axis, level): (vals, ders, pts,
+        wts) shaped like assembly._direction_tables (assembly.py:209-234)."""
+        nel = ct.c_int32(0)
+        _lib.check(self.lib.sgiga_basis_table(self.h, axis, level, ct.byref(nel), None, None, None, None))
+        n, q, P = nel.value, self.spec.quad_points, self.spec.degree + 1
+        vals, ders = np.empty((n, q, P)), np.empty((n, q, P))
+        pts, wts = np.empty(n * q), np.empty(n * q)
+        _lib.check(self.lib.sgiga_basis_table(self.h, axis, level, ct.byref(nel), _lib.ptr(vals, ct.c_double),
+                                              _lib.ptr(ders, ct.c_double), _lib.ptr(pts, ct.c_double),
+                                              _lib.ptr(wts, ct.c_double)))
+        return vals, ders, pts, wts
+
     def phase_stats(self):
         ms = np.zeros(3, dtype=np.float32)
         ln = np.zeros(3, dtype=np.int64)

@@ -33,6 +33,12 @@ def golden():
     return load_golden
 
 
+def probe_vector(i, n):
+    """Seeded probe vector of stored component i (tests/golden/make_golden.py
+    test_vector): the goldens store A @ v, not v."""
+    return np.random.default_rng(1234 + int(i)).standard_normal(n)
+
+
 def rel_l2(a, b) -> float:
     a, b = np.ravel(a), np.ravel(b)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
