@@ -65,7 +65,7 @@ static void free_all(Handle* h) {
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
                     h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps,
                     h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck, h->d_ticket, h->d_mcomp,
-                    h->d_spts, h->d_sout};
+                    h->d_spts, h->d_sout, h->d_blocks2};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel, h->h_sticky};
@@ -87,6 +87,10 @@ static void free_all(Handle* h) {
 // ---------------------------------------------------------------------------
 // descriptor -> component table (host)
 // ---------------------------------------------------------------------------
+// k_assembly2d walks the shorter axis of a 2-D component (few, full-width
+// barrier intervals) and tiles the longer one
+static inline int walk2d_axis(const CompInfo& C) { return C.m[0] <= C.m[1] ? 0 : 1; }
+
 static int build_tables(Handle* h, const sgiga_problem_desc* D) {
     const int d = D->d, p = D->degree;
     if (d < 1 || d > 3) { set_error("dimension must be 1, 2 or 3"); return SGIGA_ERR_VALUE; }
@@ -174,7 +178,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
 
     // components
     h->comps.assign(D->n_comp, CompInfo{});
-    h->pencils.clear(); h->chunks.clear(); h->small_comps.clear(); h->large_comps.clear(); h->slotoff.clear();
+    h->pencils.clear(); h->blocks2.clear(); h->chunks.clear(); h->small_comps.clear(); h->large_comps.clear(); h->slotoff.clear();
     int64_t vec = 0, mat = 0, qpo = 0, dof = 0, rows_tot = 0, nqp_tot = 0;
     const int W = 2 * p + 1, nG = d * (d + 1) / 2 + 1;
     h->max_slots_comp = 0;
@@ -221,11 +225,17 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
             C.ss[k] = ps; ps *= C.S[k];
         }
         // qp storage order: stream axis s = ax[d-1] outermost, tile axis
-        // a = ax[d-2] innermost (a pencil's plane window is contiguous in a)
+        // a = ax[d-2] innermost (a pencil's plane window is contiguous in a);
+        // 2-D components assembled by k_assembly2d: the tile axis (the
+        // longer one, walk2d_axis) innermost, so a walk line is contiguous
         int64_t pq = 1;
         const int qorder[3] = {d >= 2 ? C.ax[d - 2] : C.ax[0], d >= 3 ? C.ax[0] : C.ax[d - 1], C.ax[d - 1]};
+        const bool asm2d = d == 2 && h->mu == 1 && h->q == p + 1 && !h->opt.generic_assembly;
         for (int jj = 0; jj < d; ++jj) {
-            int k = (d == 1) ? C.ax[0] : (d == 2 ? (jj == 0 ? C.ax[0] : C.ax[1]) : qorder[jj]);
+            int k = (d == 1) ? C.ax[0]
+                             : (d == 2 ? (asm2d ? (jj == 0 ? 1 - walk2d_axis(C) : walk2d_axis(C))
+                                                : (jj == 0 ? C.ax[0] : C.ax[1]))
+                                       : qorder[jj]);
             C.qs[k] = pq;
             pq *= (int64_t)C.nel[k] * h->q;
         }
@@ -384,6 +394,68 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
         return seg_elems(h->comps[x.comp], x.r0, x.r1) > seg_elems(h->comps[y.comp], y.r0, y.r1);
     });
     h->asm_seg = SEG;
+    // 2-D components (maximal regularity, q = p + 1): blocks of up to ASM2_BA
+    // tile rows x a segment of the walk axis for k_assembly2d.  A block walks
+    // the SHORTER axis (few barrier intervals of full width -- a thin tile
+    // walked along a long axis is a chain of near-empty intervals) and tiles
+    // the longer one; the stencil's row order is unaffected.  Cost of a block
+    // ~ setup + its walk elements x (tile rows + window halo); the segment
+    // length minimises max(longest block, total / resident CTAs)
+    if (d == 2 && h->mu == 1 && h->q == p + 1 && !h->opt.generic_assembly) {
+        const int BA = ASM2_BA;
+        auto walk_of = [&](const CompInfo& C) { return walk2d_axis(C); };
+        auto seg_w = [&](const CompInfo& C, int r0, int r1) {
+            const int nel_w = C.nel[walk_of(C)];
+            const int ef = std::max(0, r0 - p), el = std::min(r1 - 1, nel_w - 1);
+            return std::max(0, el - ef + 1);
+        };
+        auto split_a = [&](const CompInfo& C, std::vector<std::pair<int, int>>& out) {
+            const int ma = C.m[1 - walk_of(C)];
+            const int nb = (ma + BA - 1) / BA;
+            for (int b = 0, start = 0; b < nb; ++b) {
+                const int cnt = (ma - start + (nb - b) - 1) / (nb - b);
+                out.push_back({1 + start, cnt});
+                start += cnt;
+            }
+        };
+        const double slots2 = 2.0 * nsm;
+        int SEG2 = 1 << 20;
+        double best = 1e300;
+        for (int cand : {1 << 20, 64, 32, 16, 8, 4}) {
+            double tot = 0, mx = 0;
+            for (const CompInfo& C : h->comps) {
+                if (!C.rows) continue;
+                std::vector<std::pair<int, int>> ab;
+                split_a(C, ab);
+                const int ms = C.m[walk_of(C)];
+                for (auto& [ia0, na] : ab)
+                    for (int r0 = 1; r0 < 1 + ms; r0 += cand) {
+                        const double cost = (seg_w(C, r0, std::min(1 + ms, r0 + cand)) + 3.0) * (na + p + 2.0);
+                        tot += cost;
+                        mx = std::max(mx, cost);
+                    }
+            }
+            const double span = std::max(mx, tot / slots2);
+            if (span < best * 0.97) { best = span; SEG2 = cand; }
+        }
+        for (int c = 0; c < D->n_comp; ++c) {
+            const CompInfo& C = h->comps[c];
+            if (!C.rows) continue;
+            std::vector<std::pair<int, int>> ab;
+            split_a(C, ab);
+            const int ms = C.m[walk_of(C)];
+            for (auto& [ia0, na] : ab)
+                for (int r0 = 1; r0 < 1 + ms; r0 += SEG2) {
+                    Block2 bk;
+                    bk.comp = c; bk.walk = walk_of(C); bk.ia0 = ia0; bk.na = na;
+                    bk.r0 = r0; bk.r1 = std::min(1 + ms, r0 + SEG2);
+                    h->blocks2.push_back(bk);
+                }
+        }
+        std::stable_sort(h->blocks2.begin(), h->blocks2.end(), [&](const Block2& x, const Block2& y) {
+            return seg_w(h->comps[x.comp], x.r0, x.r1) * (x.na + p) > seg_w(h->comps[y.comp], y.r0, y.r1) * (y.na + p);
+        });
+    }
     h->total_vec = vec; h->total_slots = mat; h->total_qp = nqp_tot; h->total_rows = rows_tot;
     {   // k_metric: component of each 256-point CTA's first point
         h->mcomp.assign((size_t)((nqp_tot + 255) / 256), 0);
@@ -413,6 +485,8 @@ static int upload_all(Handle* h) {
     SG_CUDA(cudaMemcpyAsync(h->d_geo, &h->geo, sizeof(GeoInfo), cudaMemcpyHostToDevice, s));
     if (!h->pencils.empty())
         SG_CUDA(cudaMemcpyAsync(h->d_pencils, h->pencils.data(), sizeof(Pencil) * h->pencils.size(), cudaMemcpyHostToDevice, s));
+    if (!h->blocks2.empty())
+        SG_CUDA(cudaMemcpyAsync(h->d_blocks2, h->blocks2.data(), sizeof(Block2) * h->blocks2.size(), cudaMemcpyHostToDevice, s));
     if (!h->chunks.empty())
         SG_CUDA(cudaMemcpyAsync(h->d_chunks, h->chunks.data(), sizeof(Chunk) * h->chunks.size(), cudaMemcpyHostToDevice, s));
     if (!h->small_comps.empty())
@@ -554,6 +628,7 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_tabs, h->tabs.size());
     A_(d_geo, 1);
     A_(d_pencils, h->pencils.size());
+    A_(d_blocks2, h->blocks2.size());
     A_(d_chunks, h->chunks.size());
     A_(d_small, h->small_comps.size());
     A_(d_large, h->large_comps.size());
@@ -661,6 +736,7 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
     if (tmp.total_slots != h->total_slots || tmp.total_qp != h->total_qp ||
         tmp.ncomp != h->ncomp || tmp.tabs.size() != h->tabs.size() || tmp.d != h->d ||
         tmp.p != h->p || tmp.q != h->q || tmp.pencils.size() != h->pencils.size() ||
+        tmp.blocks2.size() != h->blocks2.size() ||
         tmp.chunks.size() != h->chunks.size() || tmp.small_comps.size() != h->small_comps.size() ||
         tmp.large_comps.size() != h->large_comps.size() || tmp.slotoff.size() != h->slotoff.size() ||
         tmp.fd_comps.size() != h->fd_comps.size() || tmp.fd_uniq.size() != h->fd_uniq.size() ||
@@ -679,6 +755,7 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
                            same_bytes(tmp.geo_hw, h->geo_hw) && same_bytes(tmp.bp_host, h->bp_host) &&
                            same_bytes(tmp.comps, h->comps) && same_bytes(tmp.tabs, h->tabs) &&
                            same_bytes(tmp.slotoff, h->slotoff) && same_bytes(tmp.pencils, h->pencils) &&
+                           same_bytes(tmp.blocks2, h->blocks2) &&
                            same_bytes(tmp.chunks, h->chunks) && same_bytes(tmp.small_comps, h->small_comps) &&
                            same_bytes(tmp.large_comps, h->large_comps) && same_bytes(tmp.fd_comps, h->fd_comps) &&
                            same_bytes(tmp.fd_uniq, h->fd_uniq) && same_bytes(tmp.fd_uoff, h->fd_uoff) &&
@@ -690,7 +767,7 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
     h->geo = tmp.geo; h->geo_knots.swap(tmp.geo_knots); h->geo_hw.swap(tmp.geo_hw);
     h->bp_host.swap(tmp.bp_host); h->comps.swap(tmp.comps); h->tabs.swap(tmp.tabs);
     h->slotoff.swap(tmp.slotoff);
-    h->pencils.swap(tmp.pencils); h->chunks.swap(tmp.chunks); h->mcomp.swap(tmp.mcomp);
+    h->pencils.swap(tmp.pencils); h->blocks2.swap(tmp.blocks2); h->chunks.swap(tmp.chunks); h->mcomp.swap(tmp.mcomp);
     h->small_comps.swap(tmp.small_comps); h->large_comps.swap(tmp.large_comps);
     h->fd_comps.swap(tmp.fd_comps); h->fd_uniq.swap(tmp.fd_uniq);
     h->fd_uoff.swap(tmp.fd_uoff); h->fd_loff.swap(tmp.fd_loff);

@@ -67,6 +67,8 @@ struct Handle {
     std::vector<int> tab_of;           // [d*(max_level+1)] -> tab index
     std::vector<double> bp_host;       // concatenated breakpoints
     std::vector<Pencil> pencils;
+    std::vector<Block2> blocks2;       // 2-D assembly blocks (k_assembly2d.cu)
+    Block2* d_blocks2 = nullptr;
     std::vector<Chunk> chunks;
     std::vector<int> small_comps, large_comps;
     std::vector<int> slotoff;          // per-component slot column offsets

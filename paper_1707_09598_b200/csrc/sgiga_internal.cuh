@@ -99,6 +99,14 @@ struct Pencil {         // one CTA of the assembly kernel
     int r0, r1;         // full function row range [r0, r1) along the stream axis
 };
 
+constexpr int ASM2_BA = 8;   // 2-D assembly: tile rows per block (k_assembly2d.cu)
+struct Block2 {         // one CTA of the 2-D assembly kernel
+    int comp;
+    int walk;           // original axis the block walks along; the other is tiled
+    int ia0, na;        // tile rows [ia0, ia0 + na) (full indices)
+    int r0, r1;         // walk rows [r0, r1) (full indices)
+};
+
 struct Chunk {          // PCG row block of a large component
     int comp;
     int row0;

@@ -336,3 +336,47 @@ def test_cfg2_permutation_classes_match_reference(golden):
             assert normwise(rhs, g[f"k{i}_rhs"]) <= 1e-12
     finally:
         b.close()
+
+
+# ---------------------------------------------------------------------------
+# cfg5's comparison point: the full tensor-grid solve at 2^6 per direction
+# ---------------------------------------------------------------------------
+@pytest.mark.slow
+def test_cfg5_tensor_matches_reference(golden):
+    """CombinationPlan(3, (((6,6,6),1),)) (reference analysis.py:317-320):
+    287 496 interior rows, 189 M nnz.  Element matrices and load from the
+    reference's own kernel; the golden solution is the LABELLED scipy
+    Jacobi-PCG restatement at rtol 1e-13 (reference spsolve is infeasible,
+    SURVEY 8(c)); see tests/golden/make_golden_tensor.py."""
+    g = golden("cfg5_tensor")
+    cfg = configs.get_config("cfg5_tensor")
+    b = Batch(make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points))
+    try:
+        b.assemble()
+        A_, rhs = b.export_csr(0)
+        assert A_.shape[0] == int(g["rows"]) and A_.nnz == int(g["nnz"])
+        mx = float(g["maxabs"])
+        for k, r in enumerate(g["full_rows"]):
+            s, e = A_.indptr[r], A_.indptr[r + 1]
+            assert np.array_equal(A_.indices[s:e], g[f"row{k}_cols"]), f"row {r} pattern"
+            assert np.max(np.abs(A_.data[s:e] - g[f"row{k}_vals"])) <= 1e-12 * mx
+        Av = A_ @ np.random.default_rng(1234).standard_normal(A_.shape[0])
+        dots = [np.random.default_rng(5000 + k).standard_normal(A_.shape[0]) for k in range(3)]
+        assert normwise(Av[g["sample_rows"]], g["Av_sample"]) <= 1e-12
+        assert abs(np.linalg.norm(Av) - g["Av_norm"]) <= 1e-12 * g["Av_norm"]
+        np.testing.assert_allclose([w @ Av for w in dots], g["Av_dots"], rtol=0, atol=1e-11 * g["Av_norm"] * 600)
+        assert normwise(rhs[g["sample_rows"]], g["b_sample"]) <= 1e-12
+        np.testing.assert_allclose([w @ rhs for w in dots], g["b_dots"], rtol=0, atol=1e-11 * g["b_norm"] * 600)
+        del A_
+        it, rr = b.solve(rtol=1e-13)
+        assert rr[0] <= 1e-12 and 1 <= it[0] <= int(g["cg_iterations"])
+        coef = b.coefficients()
+        assert abs(np.linalg.norm(coef) - g["coef_norm"]) <= 1e-9 * g["coef_norm"]
+        assert normwise(coef[g["coef_sample_idx"]], g["coef_sample"]) <= 1e-9
+        vals = b.combine_points(g["points"])
+        assert rel_l2(vals, g["combined"]) <= 1e-9
+        sid = A.solution_id_of(cfg.problem.solution)
+        l2, h1 = b.error_norms(cfg.grid().points_per_dir, cfg.grid().weights_per_dir, sid)
+        np.testing.assert_allclose([l2, h1], g["errors"], rtol=5e-4)   # 3 significant digits
+    finally:
+        b.close()
