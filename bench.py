@@ -21,8 +21,10 @@ CUDA events on the library's stream, L2 flushed before each step).
 `e2e`   = the same metric through the public API with host buffers
 (PlanSession.run: H2D of the problem inputs + points, pipeline, D2H of
 the combined values), wall clock.
-N > 1 (torchrun): one independent plan per rank (weak scaling; the
-combination technique has no exchange unless components are split).
+N > 1 (torchrun): --mode split (default) shards ONE plan's components over
+the ranks (LPT on a modelled cost), with one NCCL all-gather of per-
+component point values and the plan-order sum on the device (strong
+scaling); --mode replicas runs one independent plan per rank (weak).
 """
 from __future__ import annotations
 
@@ -295,6 +297,101 @@ def run_reference(args, cfg):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def run_split(args, cfg):
+    """N > 1, --mode split: ONE plan's components LPT-sharded over the ranks
+    (distributed.DistributedPlan): per step every rank assembles + solves its
+    share and evaluates it at the points into a device buffer, one NCCL
+    all-gather, the plan-order sum on the device.  Strong scaling: the value
+    is the whole plan's components / the max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_09598_b200.distributed import DistributedPlan, component_cost_model
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if "MASTER_ADDR" not in os.environ:   # --split-world1 outside torchrun
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", device_id=dev)
+    dp = DistributedPlan(cfg.plan, cfg.problem, cfg.quad_points, rtol=args.rtol)
+    pts_h = cfg.points()
+    npts = pts_h.shape[0]
+    pts_d = torch.from_numpy(pts_h).to(dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > L2
+    for _ in range(max(args.warmup, 3)):
+        dp.step(pts_d)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler = clock_sampler(local)
+    time.sleep(0.01)
+    sampler.begin()
+    for k in range(args.steps):
+        flush.zero_()
+        starts[k].record()
+        vals = dp.step(pts_d)
+        ends[k].record()
+    torch.cuda.synchronize()
+    sampler.end()
+    clocks = sampler.stop()
+    total_ms = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    # e2e: host points in (pinned, H2D inside the step), host values out
+    pin = torch.empty(pts_h.shape, dtype=torch.float64, pin_memory=True)
+    pin.copy_(torch.from_numpy(pts_h))
+    out_h = torch.empty(npts, dtype=torch.float64, pin_memory=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        pts_step = pin.to(dev, non_blocking=True)
+        out_h.copy_(dp.step(pts_step), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    same = bool(torch.equal(vals.cpu(), out_h))
+    n_comp = len(cfg.plan)
+    cost = component_cost_model(cfg.plan.terms, cfg.problem.degree, cfg.plan.d)
+    loads = [float(cost[p].sum()) for p in dp.parts]
+    launches = 0
+    if dp.batch is not None:
+        _, ln = dp.batch.phase_stats()
+        launches = int(ln.sum()) + 2    # + the all-gather's NCCL kernel and the plan-order sum
+    lt = torch.tensor([launches], dtype=torch.float64, device=dev)
+    dist.all_reduce(lt)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": n_comp / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE config recipe; seeded points)",
+            "config": config_dict(cfg, ws, 1, "split", args.rtol),
+            "timing": "CUDA events around each step on every rank, max over ranks; 256 MB L2 flush before "
+                      "every timed step (outside the events)",
+            "e2e": {"value": n_comp / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(pts_h.nbytes),
+                    "d2h_bytes_per_step": int(npts * 8), "ms_per_step": 1e3 * e2e_s,
+                    "matches_device_run_bitwise": same,
+                    "path": "pinned points H2D -> DistributedPlan.step (assemble + solve + per-component "
+                            "combine, NCCL all-gather, plan-order sum) -> pinned values D2H, per step"},
+            "partition": {"components_per_rank": [len(p) for p in dp.parts],
+                          "modelled_load_s": loads, "model": "distributed.component_cost_model (LPT)"},
+            "gpu_launches": int(lt.item()) * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dp.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def run_sgiga(args, cfg):
     import torch
     import torch.distributed as dist
@@ -538,9 +635,11 @@ def main():
     ap.add_argument("--rtol", type=float, default=1e-13)
     ap.add_argument("--ref-budget", type=float, default=600.0,
                     help="reference arm: stop timing further full-plan steps after this many seconds")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "split"],
-                    help="N > 1: independent plan replicas per GPU (weak) or one plan split over the GPUs (strong)")
+    ap.add_argument("--mode", default="split", choices=["replicas", "split"],
+                    help="N > 1: one plan split over the GPUs (strong, default) or independent plan replicas per "
+                         "GPU (weak)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split-world1", action="store_true", help=argparse.SUPPRESS)   # test the split path at N = 1
     ap.add_argument("--replicas", type=int, default=1,
                     help="replicated batch: R copies of the plan in one launch (SURVEY 8(d) roofline scaling)")
     args = ap.parse_args()
@@ -549,6 +648,8 @@ def main():
     cfg = get_config(args.config)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.mode == "split" and (dist_env()[0] > 1 or args.split_world1):
+        return run_split(args, cfg)
     return run_sgiga(args, cfg)
 
 

@@ -210,6 +210,22 @@ int sgiga_error_norms(sgiga_handle* h, const double* pts_per_dir,
                       const double* wts_per_dir, const int64_t* npts_per_dir,
                       int32_t solution_id, double* out);
 
+/* sgiga_run_async with per-component output: out_dev[c * npts + i] = value
+ * of component c (plan order, coefficient NOT applied) at point i -- the
+ * local half of a plan split over ranks (distributed.py).  No sync; the
+ * verdict comes from sgiga_run_wait.                                      */
+int sgiga_run_components_async(sgiga_handle* h, double rtol, int32_t maxit, const double* pts_dev,
+                               int64_t npts, double* out_dev);
+
+/* Multi-GPU combine: out[pt] = sum_c coef[c] * src[row[c]][pt]
+ * over the plan's terms in plan order, with the exact operations of the
+ * single-GPU combine (vals = c*v; vals += c*v, combination.py:227-233), so
+ * a plan split over ranks reproduces the one-GPU values bitwise after the
+ * per-component values (rows of npts doubles) are all-gathered.  Device
+ * pointers; enqueued on `stream`, no synchronisation.                    */
+int sgiga_plan_order_sum(void* stream, int32_t nterm, int64_t npts, const int32_t* d_coef,
+                         const int64_t* d_row, const double* d_src, double* d_out);
+
 /* Parity export of kernel 1's output for one (axis, level) knot vector, as
  * assembly._direction_tables (assembly.py:209-234) returns it: basis values
  * and first derivatives [nel][q][p+1], Gauss points xi [nel*q] and weights

@@ -76,6 +76,8 @@ static void free_all(Handle* h) {
     if (h->fd_fork) cudaEventDestroy(h->fd_fork);
     if (h->fd_join) cudaEventDestroy(h->fd_join);
     if (h->fd_metric) cudaEventDestroy(h->fd_metric);
+    if (h->pcg_fork) cudaEventDestroy(h->pcg_fork);
+    if (h->pcg_join) cudaEventDestroy(h->pcg_join);
     if (h->stream2) cudaStreamDestroy(h->stream2);
     if (h->cs_fork) cudaEventDestroy(h->cs_fork);
     if (h->cs_join) cudaEventDestroy(h->cs_join);
@@ -686,6 +688,8 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_fork, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_join, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->fd_metric, cudaEventDisableTiming);
+    if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->pcg_fork, cudaEventDisableTiming);
+    if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->pcg_join, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaStreamCreateWithPriority(&h->stream3, cudaStreamNonBlocking, prio_hi);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->cs_fork, cudaEventDisableTiming);
     if (ea == cudaSuccess) ea = cudaEventCreateWithFlags(&h->cs_join, cudaEventDisableTiming);
@@ -998,7 +1002,7 @@ static bool run_graphs_enabled(const Handle* h) {
 // enqueue of one whole pass (device pointers): direct launches, capture, or
 // replay of the pass graph; no synchronisation
 static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, int64_t npts, double* dout,
-                       const double* hsrc = nullptr) {
+                       const double* hsrc = nullptr, int per_comp = 0) {
     int st;
     if (!(rtol > 0.0)) { set_error("rtol must be positive"); return SGIGA_ERR_VALUE; }   // before any launch
     auto enqueue_all = [&]() -> int {
@@ -1020,7 +1024,7 @@ static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, 
         int s2 = assemble_enqueue(h);
         if (!s2) s2 = solve_enqueue(h, rtol, maxit);
         bool fused = false;   // the combine's last CTA writes the status (no k_status launch)
-        if (!s2 && npts > 0) s2 = combine_enqueue(h, dp, npts, dout, 0, &fused);
+        if (!s2 && npts > 0) s2 = combine_enqueue(h, dp, npts, dout, per_comp, &fused);
         if (!s2 && !fused && launch_status(h) != cudaSuccess) s2 = SGIGA_ERR_CUDA;
         h->cs_ready = false;
         if (h->cs_pending) {   // not consumed (an earlier step failed): still join the side stream
@@ -1031,7 +1035,7 @@ static int run_enqueue(Handle* h, double rtol, int32_t maxit, const double* dp, 
     };
     // whole-run graph: only when the solve has no host-driven loop (every
     // component on the single-launch small path) and no profiling knob is on
-    const bool can_graph = run_graphs_enabled(h) && h->large_comps.empty() && !h->graph_broken;
+    const bool can_graph = run_graphs_enabled(h) && h->large_comps.empty() && !h->graph_broken && !per_comp;
     const bool same = can_graph && h->rkey.npts == npts && h->rkey.rtol == rtol && h->rkey.maxit == maxit &&
                       h->rkey.dp == dp && h->rkey.dout == dout && h->rkey.hp == hsrc;
     if (same && h->run_exec) {
@@ -1132,6 +1136,13 @@ int sgiga_run_async(sgiga_handle* hh, double rtol, int32_t maxit, const double* 
     Handle* h = reinterpret_cast<Handle*>(hh);
     if (!h || npts < 0 || (npts > 0 && (!pts_dev || !out_dev))) { set_error("null argument"); return SGIGA_ERR_VALUE; }
     return run_enqueue(h, rtol, maxit, pts_dev, npts, out_dev);
+}
+
+int sgiga_run_components_async(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts_dev, int64_t npts,
+                               double* out_dev) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || npts < 0 || (npts > 0 && (!pts_dev || !out_dev))) { set_error("null argument"); return SGIGA_ERR_VALUE; }
+    return run_enqueue(h, rtol, maxit, pts_dev, npts, out_dev, nullptr, 1);
 }
 
 int sgiga_run_host_async(sgiga_handle* hh, double rtol, int32_t maxit, const double* pts_pinned, int64_t npts,

@@ -140,6 +140,7 @@ struct Handle {
     int* d_mcomp = nullptr;                  // k_metric: component of each 256-point CTA
     cudaStream_t stream2 = nullptr;          // side stream: the eigen kernel overlaps assembly
     cudaEvent_t fd_fork = nullptr, fd_join = nullptr, fd_metric = nullptr;
+    cudaEvent_t pcg_fork = nullptr, pcg_join = nullptr;   // FD-PCG beside the line-FD PCG
     bool fd_pending = false;                 // fd_join not yet waited on by the main stream
     // combine point sort on its own side stream (sgiga_run: forked before the
     // assembly, joined before the combine kernel)

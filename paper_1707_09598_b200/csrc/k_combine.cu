@@ -715,3 +715,37 @@ cudaError_t launch_error_norms(Handle* h, const double* d_pts, const double* d_w
 }
 
 }  // namespace sgiga
+
+// ---- multi-GPU combine: plan-order sum of gathered per-component values ----
+// out[pt] = sum_c coef_c * src[row_c][pt] with the single-GPU combine's
+// exact operations and order (vals = c*v; vals += c*v, combination.py:
+// 227-233): a plan split over ranks reproduces the one-GPU values bit for
+// bit once every rank's per-component values are all-gathered.
+namespace sgiga {
+__global__ void k_plan_order_sum(int nterm, int64_t npts, const int* __restrict__ coef,
+                                 const int64_t* __restrict__ row, const double* __restrict__ src,
+                                 double* __restrict__ out) {
+    const int64_t pt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pt >= npts) return;
+    double acc = 0.0;
+    for (int c = 0; c < nterm; ++c) {
+        const double cv = (double)coef[c] * src[row[c] * npts + pt];
+        acc = (c == 0) ? cv : __dadd_rn(acc, cv);
+    }
+    out[pt] = acc;
+}
+}  // namespace sgiga
+
+extern "C" int sgiga_plan_order_sum(void* stream, int32_t nterm, int64_t npts, const int32_t* d_coef,
+                                    const int64_t* d_row, const double* d_src, double* d_out) {
+    using namespace sgiga;
+    if (nterm < 1 || npts < 0 || !d_coef || !d_row || !d_src || !d_out) {
+        set_error("sgiga_plan_order_sum: bad argument");
+        return SGIGA_ERR_VALUE;
+    }
+    if (npts == 0) return SGIGA_OK;
+    k_plan_order_sum<<<(unsigned)((npts + 255) / 256), 256, 0, (cudaStream_t)stream>>>(nterm, npts, d_coef, d_row,
+                                                                                         d_src, d_out);
+    SG_CUDA(cudaGetLastError());
+    return SGIGA_OK;
+}

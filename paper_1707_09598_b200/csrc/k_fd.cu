@@ -1175,7 +1175,8 @@ cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit) {
+cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit, cudaStream_t stream) {
+    if (!stream) stream = h->stream;
     const int n = (int)h->fd_comps.size();
     if (n == 0) return cudaSuccess;
     size_t smem = 0;
@@ -1184,12 +1185,12 @@ cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit) {
     long long* prof = nullptr;
     if (h->opt.fd_profile) {   // per-CTA phase cycles (probe only)
         if ((e = cudaMalloc(&prof, sizeof(long long) * 8 * n)) != cudaSuccess) return e;
-        cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * n, h->stream);
+        cudaMemsetAsync(prof, 0, sizeof(long long) * 8 * n, stream);
     }
 #define LAUNCH_FD(DD)                                                                                 \
     e = cudaFuncSetAttribute(k_pcg_fd<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
     if (e != cudaSuccess) return e;                                                                   \
-    k_pcg_fd<DD><<<(unsigned)n, FD_THREADS, smem, h->stream>>>(                                       \
+    k_pcg_fd<DD><<<(unsigned)n, FD_THREADS, smem, stream>>>(                                       \
         h->d_comps, h->d_fdlist, h->d_slotoff, h->d_stencil, h->d_rhs, h->d_G, h->d_fd_uoff,          \
         h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_ck, h->d_x, h->d_coef, h->d_cg, h->d_relres, rtol * rtol, maxit, prof)
     if (h->d == 1) { LAUNCH_FD(1); }
@@ -1199,8 +1200,8 @@ cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit) {
     h->launches[1]++;
     if (prof) {
         std::vector<long long> t(8 * n);
-        cudaMemcpyAsync(t.data(), prof, sizeof(long long) * t.size(), cudaMemcpyDeviceToHost, h->stream);
-        cudaStreamSynchronize(h->stream);
+        cudaMemcpyAsync(t.data(), prof, sizeof(long long) * t.size(), cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
         for (int b = 0; b < n; ++b)
             fprintf(stderr, "pcg-fd cta %d R=%lld NS=%lld cycles: prologue=%lld b=%lld precond=%lld spmv1=%lld "
                     "loop=%lld spmv2=%lld end=%lld\n", b, t[8 * b + 7] / 1000, t[8 * b + 7] % 1000, t[8 * b],

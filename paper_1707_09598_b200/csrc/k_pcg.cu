@@ -466,8 +466,19 @@ int run_pcg(Handle* h, double rtol, int maxit) {
             h->fd_pending = false;
         }
         h->kstart(3);
-        SG_CUDA(launch_pcg_fd(h, rtol, maxit));    // small: everything in shared memory
-        SG_CUDA(launch_pcg_fdl(h, rtol, maxit));   // one long axis: banded line solves
+        if (!h->fd_comps.empty() && !h->fdl_comps.empty()) {
+            // the one-CTA FD solves (few, long CTAs) run on the high-priority
+            // side stream beside the line-FD clusters instead of before them
+            SG_CUDA(cudaEventRecord(h->pcg_fork, h->stream));
+            SG_CUDA(cudaStreamWaitEvent(h->stream2, h->pcg_fork, 0));
+            SG_CUDA(launch_pcg_fd(h, rtol, maxit, h->stream2));   // small: everything in shared memory
+            SG_CUDA(cudaEventRecord(h->pcg_join, h->stream2));
+            SG_CUDA(launch_pcg_fdl(h, rtol, maxit));              // one long axis: banded line solves
+            SG_CUDA(cudaStreamWaitEvent(h->stream, h->pcg_join, 0));
+        } else {
+            SG_CUDA(launch_pcg_fd(h, rtol, maxit));    // small: everything in shared memory
+            SG_CUDA(launch_pcg_fdl(h, rtol, maxit));   // one long axis: banded line solves
+        }
         if (h->small_comps.empty()) h->kstop(3);
     }
     if (!h->small_comps.empty() && !no_cluster) {

@@ -246,7 +246,7 @@ int launch_pcg_cluster(Handle* h, double rtol, int maxit);
 cudaError_t launch_residual_check(Handle* h);
 cudaError_t launch_solve_prologue(Handle* h, cudaStream_t stream);
 cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s);
-cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit);
+cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit, cudaStream_t stream = nullptr);
 cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit);
 cudaError_t launch_fd_setup(Handle* h, cudaStream_t s);
 size_t fd_comp_smem(const CompInfo& C, int d);

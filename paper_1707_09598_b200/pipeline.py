@@ -206,6 +206,13 @@ class Batch:
         self._host_forcing_density()
         _lib.check(self.lib.sgiga_run_async(self.h, float(rtol), int(maxit), pts_ptr, int(npts), out_ptr))
 
+    def run_components_async(self, pts_ptr: int, npts: int, out_ptr: int, rtol: float = 1e-13, maxit: int = 0):
+        """Enqueue assemble + solve + PER-COMPONENT combine (out = n_comp x
+        npts device doubles, coefficients not applied) without synchronising:
+        the local half of a plan split over ranks."""
+        self._host_forcing_density()
+        _lib.check(self.lib.sgiga_run_components_async(self.h, float(rtol), int(maxit), pts_ptr, int(npts), out_ptr))
+
     def run_host_async(self, pts: np.ndarray, out: np.ndarray, rtol: float = 1e-13, maxit: int = 0):
         """Enqueue one end-to-end pass with page-locked HOST buffers (H2D of
         ``pts`` and D2H into ``out`` inside the pass) without synchronising;
