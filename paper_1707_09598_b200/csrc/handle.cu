@@ -65,7 +65,7 @@ static void free_all(Handle* h) {
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
                     h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps,
                     h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck, h->d_ticket, h->d_mcomp,
-                    h->d_spts, h->d_sout, h->d_blocks2};
+                    h->d_spts, h->d_sout, h->d_blocks2, h->d_fdg_list, h->d_fdg_part};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel, h->h_sticky};
@@ -288,6 +288,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
         std::vector<char> used(ntab, 0);
         std::vector<int> keep_small, keep_large;
         h->fdl_comps.clear();
+        h->fdg_comps.clear();
         h->fdl_off.assign(h->comps.size(), -1);
         h->fdl_total = 0;
         for (int c = 0; c < D->n_comp; ++c) {
@@ -301,7 +302,12 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
                 all_ok = all_ok && ok_k;
                 if (k != C.ax[d - 1]) others_ok = others_ok && ok_k;
             }
-            if (all_ok && was_small && fd_comp_smem(C, d) <= 200 * 1024) {   // one CTA, everything in smem
+            if (all_ok && C.rows >= FDG_MIN_ROWS) {   // whole-GPU FD-PCG (cooperative grid)
+                C.fd = 3;
+                C.small = 1;   // keeps the chunked Jacobi kernels away from it
+                h->fdg_comps.push_back(c);
+                for (int k = 0; k < d; ++k) used[C.tab[k]] = 1;
+            } else if (all_ok && was_small && fd_comp_smem(C, d) <= 200 * 1024) {   // one CTA, everything in smem
                 C.fd = 1;
                 h->fd_comps.push_back(c);
                 for (int k = 0; k < d; ++k) used[C.tab[k]] = 1;
@@ -495,6 +501,8 @@ static int upload_all(Handle* h) {
         SG_CUDA(cudaMemcpyAsync(h->d_small, h->small_comps.data(), sizeof(int) * h->small_comps.size(), cudaMemcpyHostToDevice, s));
     if (!h->slotoff.empty())
         SG_CUDA(cudaMemcpyAsync(h->d_slotoff, h->slotoff.data(), sizeof(int) * h->slotoff.size(), cudaMemcpyHostToDevice, s));
+    if (!h->fdg_comps.empty())
+        SG_CUDA(cudaMemcpyAsync(h->d_fdg_list, h->fdg_comps.data(), sizeof(int) * h->fdg_comps.size(), cudaMemcpyHostToDevice, s));
     if (!h->fdl_comps.empty()) {
         SG_CUDA(cudaMemcpyAsync(h->d_fdl_list, h->fdl_comps.data(), sizeof(int) * h->fdl_comps.size(), cudaMemcpyHostToDevice, s));
         SG_CUDA(cudaMemcpyAsync(h->d_fdl_off, h->fdl_off.data(), sizeof(int64_t) * h->fdl_off.size(), cudaMemcpyHostToDevice, s));
@@ -670,6 +678,8 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_fdU, h->fd_u_total);
     A_(d_fdL, h->fd_l_total);
     A_(d_fdl_list, h->fdl_comps.size());
+    A_(d_fdg_list, h->fdg_comps.size());
+    A_(d_fdg_part, 2 * FDG_MAX_CTAS);
     A_(d_fdl_off, h->comps.size());
     A_(d_fdl, h->fdl_total);
     A_(d_ck, (int64_t)MAXD * h->ncomp);
@@ -745,7 +755,8 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
         tmp.large_comps.size() != h->large_comps.size() || tmp.slotoff.size() != h->slotoff.size() ||
         tmp.fd_comps.size() != h->fd_comps.size() || tmp.fd_uniq.size() != h->fd_uniq.size() ||
         tmp.fd_u_total != h->fd_u_total || tmp.fd_l_total != h->fd_l_total ||
-        tmp.fdl_comps.size() != h->fdl_comps.size() || tmp.fdl_total != h->fdl_total) {
+        tmp.fdl_comps.size() != h->fdl_comps.size() || tmp.fdl_total != h->fdl_total ||
+        tmp.fdg_comps.size() != h->fdg_comps.size()) {
         set_error("sgiga_upload: descriptor shape differs from the handle's");
         return SGIGA_ERR_VALUE;
     }
@@ -764,6 +775,7 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
                            same_bytes(tmp.large_comps, h->large_comps) && same_bytes(tmp.fd_comps, h->fd_comps) &&
                            same_bytes(tmp.fd_uniq, h->fd_uniq) && same_bytes(tmp.fd_uoff, h->fd_uoff) &&
                            same_bytes(tmp.fdl_comps, h->fdl_comps) && same_bytes(tmp.fdl_off, h->fdl_off) &&
+                           same_bytes(tmp.fdg_comps, h->fdg_comps) &&
                            tmp.forcing_id == h->forcing_id;
     if (!identical) h->drop_run_graph();
     h->levels.swap(tmp.levels); h->coefs.swap(tmp.coefs);
@@ -775,7 +787,7 @@ int sgiga_upload(sgiga_handle* hh, const sgiga_problem_desc* desc) {
     h->small_comps.swap(tmp.small_comps); h->large_comps.swap(tmp.large_comps);
     h->fd_comps.swap(tmp.fd_comps); h->fd_uniq.swap(tmp.fd_uniq);
     h->fd_uoff.swap(tmp.fd_uoff); h->fd_loff.swap(tmp.fd_loff);
-    h->fdl_comps.swap(tmp.fdl_comps); h->fdl_off.swap(tmp.fdl_off);
+    h->fdl_comps.swap(tmp.fdl_comps); h->fdl_off.swap(tmp.fdl_off); h->fdg_comps.swap(tmp.fdg_comps);
     h->forcing_id = tmp.forcing_id;
     if (identical) return SGIGA_OK;   // device copies are already these bytes
     return upload_all(h);
@@ -845,7 +857,7 @@ static int assemble_enqueue(Handle* h) {
     h->tables_ready = false;   // kernel 1 is part of every assembly pass
     int st = ensure_tables(h);
     if (st) return st;
-    if (!h->fd_uniq.empty() || !h->fd_comps.empty() || !h->fdl_comps.empty()) {   // FD eigen-factors on the side stream, overlapping the assembly
+    if (!h->fd_uniq.empty() || !h->fd_comps.empty() || !h->fdl_comps.empty() || !h->fdg_comps.empty()) {   // FD eigen-factors on the side stream, overlapping the assembly
         SG_CUDA(cudaEventRecord(h->fd_fork, h->stream));
         SG_CUDA(cudaStreamWaitEvent(h->stream2, h->fd_fork, 0));
         SG_CUDA(launch_solve_prologue(h, h->stream2));   // solver state zeroed off the main stream

@@ -125,6 +125,10 @@ struct Handle {
     int64_t* d_fd_loff = nullptr;
     double* d_fdU = nullptr;
     double* d_fdL = nullptr;
+    // whole-GPU FD-PCG comps (k_pcg_grid.cu): large components, every axis FD
+    std::vector<int> fdg_comps;
+    int* d_fdg_list = nullptr;
+    double* d_fdg_part = nullptr;            // [2][FDG_MAX_CTAS] per-CTA partial sums
     // line-FD comps (one long axis; k_pcg_fdl): per-comp offset into d_fdl
     // (stream-axis K / M bands + one banded Cholesky factor per line)
     std::vector<int> fdl_comps;

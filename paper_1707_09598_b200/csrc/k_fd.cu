@@ -1107,8 +1107,18 @@ static cudaError_t launch_hi(void (*kern)(KArgs...), dim3 grid, dim3 block, size
 // k_metric, joined before the solve): c_k of every FD / line-FD component,
 // then the line-FD stream-axis bands and per-line factors
 cudaError_t launch_fd_setup(Handle* h, cudaStream_t s) {
-    const int nf = (int)h->fd_comps.size(), nl = (int)h->fdl_comps.size();
-    if (nf + nl == 0) return cudaSuccess;
+    const int nf = (int)h->fd_comps.size(), nl = (int)h->fdl_comps.size(), ng = (int)h->fdg_comps.size();
+    if (ng > 0) {   // c_k of the whole-GPU FD components
+        const dim3 gg((unsigned)ng, (unsigned)h->d);
+#define LAUNCH_SCALE_G(DD)                                                                            \
+    launch_hi(k_fd_metric_scale<DD>, gg, dim3(256), 0, s, h->d_comps, h->d_fdg_list, ng, h->d_fdg_list, h->d_G, h->d_ck)
+        if (h->d == 1) { LAUNCH_SCALE_G(1); }
+        else if (h->d == 2) { LAUNCH_SCALE_G(2); }
+        else { LAUNCH_SCALE_G(3); }
+#undef LAUNCH_SCALE_G
+        h->launches[0]++;
+    }
+    if (nf + nl == 0) return cudaGetLastError();
     const dim3 g1((unsigned)(nf + nl), (unsigned)h->d);
 #define LAUNCH_SCALE(DD)                                                                              \
     launch_hi(k_fd_metric_scale<DD>, g1, dim3(256), 0, s, h->d_comps, h->d_fdlist, nf, h->d_fdl_list, h->d_G, h->d_ck)

@@ -459,7 +459,7 @@ int run_pcg(Handle* h, double rtol, int maxit) {
     int nch = (int)h->chunks.size();
     const bool no_cluster = h->opt.no_cluster;
     h->small_checked = false;
-    const bool any_fd = !h->fd_comps.empty() || !h->fdl_comps.empty();
+    const bool any_fd = !h->fd_comps.empty() || !h->fdl_comps.empty() || !h->fdg_comps.empty();
     if (any_fd) {   // FD-preconditioned CG (k_fd.cu), which also checks its true residuals
         if (h->fd_pending) {
             SG_CUDA(cudaStreamWaitEvent(h->stream, h->fd_join, 0));
@@ -479,6 +479,7 @@ int run_pcg(Handle* h, double rtol, int maxit) {
             SG_CUDA(launch_pcg_fd(h, rtol, maxit));    // small: everything in shared memory
             SG_CUDA(launch_pcg_fdl(h, rtol, maxit));   // one long axis: banded line solves
         }
+        SG_CUDA(launch_pcg_fdg(h, rtol, maxit));       // large, every axis FD: whole-GPU cooperative PCG
         if (h->small_comps.empty()) h->kstop(3);
     }
     if (!h->small_comps.empty() && !no_cluster) {

@@ -1,0 +1,267 @@
+// k_pcg_grid.cu -- kernel 3f: FD-preconditioned CG of ONE large component on
+// the whole GPU (a cooperative grid, grid-wide barriers between phases).
+//
+// For components too large for a CTA or a thread-block cluster (cfg5's full
+// tensor comparison solve at 2^6 elements per direction: 287 496 rows, 189 M
+// nnz, 1.67 GB of stencil) whose axes all fit the FD eigen kernel.  Same
+// preconditioner as the one-CTA FD kernel (k_fd.cu): with K_k U_k = M_k U_k
+// Lambda_k, U_k^T M_k U_k = I,
+//   P^-1 = (U_0 x U_1 x U_2) diag(1 / sum_k c_k lambda_k) (U_0 x U_1 x U_2)^T
+// applied as 2d mode products (P = A up to rounding for the identity map:
+// one or two iterations).  The SpMV streams the stencil from HBM with every
+// SM busy -- the HBM-bound phase of the solve.  Reference: linsolve.solve_spd
+// (linsolve.py:16-54): the reference solves directly (SuperLU), infeasible
+// at this size; its acceptance ||A x - b|| <= 1e-10 ||b|| is
+// checked on the true residual (linsolve.py:49-53).
+//
+// Deterministic: every reduction is per-CTA partials in fixed order, then
+// the partials summed in CTA order by every CTA (identical values).
+#include <cooperative_groups.h>
+
+#include "handle.cuh"
+
+namespace sgiga {
+
+constexpr int FDG_THREADS = 512;
+
+__device__ __forceinline__ int fdg_row_base(const CompInfo& C, int d, int row) {
+    int rb = row;
+    for (int k = 0; k < d; ++k)
+        if (C.absm[k]) rb -= ((row / (int)C.rs[k]) % C.m[k]) * (int)C.rs[k];
+    return rb;
+}
+
+template <int D>
+__global__ void __launch_bounds__(FDG_THREADS, 2)
+k_pcg_fdg(const CompInfo* __restrict__ comps, int c, const int* __restrict__ slotoff,
+          const double* __restrict__ stencil, const double* __restrict__ rhs,
+          const int64_t* __restrict__ uoff, const int64_t* __restrict__ loff, const double* __restrict__ dU,
+          const double* __restrict__ dL, const double* __restrict__ ckg, double* __restrict__ xg,
+          double* __restrict__ rg, double* __restrict__ zg, double* __restrict__ pg, double* __restrict__ qg,
+          double* __restrict__ tg, double* __restrict__ part, CgState* __restrict__ st,
+          double* __restrict__ relres, double* __restrict__ coef, double rtol2, int maxit) {
+    namespace cgs = cooperative_groups;
+    cgs::grid_group grid = cgs::this_grid();
+    __shared__ double red[FDG_THREADS / 32];
+    __shared__ double tot_s;
+    __shared__ int soffs[WMAX * WMAX * WMAX];
+    const CompInfo& C = comps[c];
+    const int R = (int)C.rows, NS = (int)C.nslots, tid = threadIdx.x;
+    const int gt = blockIdx.x * FDG_THREADS + tid, GT = gridDim.x * FDG_THREADS;
+    for (int i = tid; i < NS; i += FDG_THREADS) soffs[i] = slotoff[C.so_off + i];
+    __syncthreads();
+    int slot = 0;
+    // grid-wide fixed-order sum: warp, CTA, then the CTA partials in order
+    auto gsum = [&](double v) -> double {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((tid & 31) == 0) red[tid >> 5] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < FDG_THREADS / 32; ++w) s += red[w];
+            part[slot * gridDim.x + blockIdx.x] = s;
+        }
+        grid.sync();
+        if (tid < 32) {
+            double s = 0.0;
+            for (int b = tid; b < (int)gridDim.x; b += 32) s += part[slot * gridDim.x + b];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (tid == 0) tot_s = s;
+        }
+        __syncthreads();
+        slot ^= 1;
+        return tot_s;
+    };
+    double* x = xg + C.vec_off;
+    double* r = rg + C.vec_off;
+    double* z = zg + C.vec_off;
+    double* pp = pg + C.vec_off;   // zero halos on both sides (SpMV gathers)
+    double* qq = qg + C.vec_off;
+    double* t = tg + C.vec_off;
+    const double* b = rhs + C.vec_off;
+    const double* val = stencil + C.mat_off;
+    double ck[D];
+    int mk[D], rsk[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        ck[k] = ckg[c * MAXD + k];
+        mk[k] = C.m[k];
+        rsk[k] = (int)C.rs[k];
+    }
+    // mode product along ORIGINAL axis k (trans: U^T), optional diagonal scale
+    auto mode = [&](const double* src, double* dst, int k, bool trans, bool scale) {
+        const int m = mk[k], s = rsk[k];
+        const double* U = dU + uoff[C.tab[k]];
+        for (int row = gt; row < R; row += GT) {
+            const int a = (row / s) % m, base = row - a * s;
+            double a0 = 0.0, a1 = 0.0;
+            int j = 0;
+            if (trans) {
+                const double* Ur = U + a * m;
+                for (; j + 1 < m; j += 2) {
+                    a0 += __ldg(Ur + j) * src[base + j * s];
+                    a1 += __ldg(Ur + j + 1) * src[base + (j + 1) * s];
+                }
+                if (j < m) a0 += __ldg(Ur + j) * src[base + j * s];
+            } else {
+                for (; j + 1 < m; j += 2) {
+                    a0 += __ldg(U + j * m + a) * src[base + j * s];
+                    a1 += __ldg(U + (j + 1) * m + a) * src[base + (j + 1) * s];
+                }
+                if (j < m) a0 += __ldg(U + j * m + a) * src[base + j * s];
+            }
+            double acc = a0 + a1;
+            if (scale) {
+                double den = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < D; ++kk) den += ck[kk] * __ldg(dL + loff[C.tab[kk]] + (row / rsk[kk]) % mk[kk]);
+                acc /= den;
+            }
+            dst[row] = acc;
+        }
+        grid.sync();
+    };
+    auto precond = [&]() {   // z = P^-1 r  (r -> t -> z -> ... -> z)
+        double* bufs[2] = {t, z};
+        const double* src = r;
+        int w = 0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) { mode(src, bufs[w], k, true, k == D - 1); src = bufs[w]; w ^= 1; }
+#pragma unroll
+        for (int k = D - 1; k >= 0; --k) { mode(src, bufs[w], k, false, false); src = bufs[w]; w ^= 1; }
+        if (src != z) {   // (D odd: the last product landed in t)
+            for (int i = gt; i < R; i += GT) z[i] = t[i];
+            grid.sync();
+        }
+    };
+    // out = A v (v halo-padded): one row per thread, 16 stencil loads in
+    // flight (two CTAs of 512 threads per SM: ~128 KB of loads in flight per
+    // SM, enough to cover the HBM latency-bandwidth product)
+    auto spmv = [&](const double* v, double* out) {
+        for (int row = gt; row < R; row += GT) {
+            const int rb = fdg_row_base(C, D, row);
+            double y0 = 0.0, y1 = 0.0;
+            int tt = 0;
+            for (; tt + 15 < NS; tt += 16) {
+                double vv[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) vv[u] = __ldcs(val + (size_t)(tt + u) * R + row);
+#pragma unroll
+                for (int u = 0; u < 16; u += 2) {
+                    y0 += vv[u] * v[rb + soffs[tt + u]];
+                    y1 += vv[u + 1] * v[rb + soffs[tt + u + 1]];
+                }
+            }
+            for (; tt < NS; ++tt) y0 += __ldcs(val + (size_t)tt * R + row) * v[rb + soffs[tt]];
+            out[row] = y0 + y1;
+        }
+        grid.sync();
+    };
+
+    double bbl = 0.0;
+    for (int i = gt; i < R; i += GT) {
+        const double bi = b[i];
+        x[i] = 0.0;
+        r[i] = bi;
+        bbl += bi * bi;
+    }
+    const double bb = gsum(bbl);
+    int it = 0, conv = (bb == 0.0);
+    if (!conv) {
+        precond();
+        double rzl = 0.0;
+        for (int i = gt; i < R; i += GT) { pp[i] = z[i]; rzl += r[i] * z[i]; }
+        double rz = gsum(rzl);
+        while (it < maxit) {
+            spmv(pp, qq);
+            double pql = 0.0;
+            for (int i = gt; i < R; i += GT) pql += pp[i] * qq[i];
+            const double alpha = rz / gsum(pql);
+            double rrl = 0.0;
+            for (int i = gt; i < R; i += GT) {
+                x[i] += alpha * pp[i];
+                const double ri = r[i] - alpha * qq[i];
+                r[i] = ri;
+                rrl += ri * ri;
+            }
+            const double rr = gsum(rrl);
+            ++it;
+            if (rr <= rtol2 * bb) { conv = 1; break; }
+            precond();
+            double rzl2 = 0.0;
+            for (int i = gt; i < R; i += GT) rzl2 += r[i] * z[i];
+            const double rzn = gsum(rzl2);
+            const double beta = rzn / rz;
+            rz = rzn;
+            for (int i = gt; i < R; i += GT) pp[i] = z[i] + beta * pp[i];
+            grid.sync();
+        }
+    }
+    // true residual ||A x - b|| / ||b|| (linsolve.py:49-53); x is copied into
+    // the halo-padded p buffer for the gather
+    for (int i = gt; i < R; i += GT) pp[i] = x[i];
+    grid.sync();
+    spmv(pp, qq);
+    double eel = 0.0;
+    for (int i = gt; i < R; i += GT) {
+        const double e = qq[i] - b[i];
+        eel += isfinite(x[i]) ? e * e : __longlong_as_double(0x7ff8000000000000ULL);
+    }
+    const double ee = gsum(eel);
+    if (gt == 0) {
+        st[c].it = it;
+        st[c].conv = conv;
+        st[c].active = 0;
+        st[c].bb = bb;
+        relres[c] = bb > 0.0 ? sqrt(ee / bb) : (ee == 0.0 ? 0.0 : ee);
+    }
+    // full C-order coefficients: interior dofs get x, boundary dofs 0
+    {
+        int n[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) n[k] = C.n[k];
+        double* cf = coef + C.dof_off;
+        const int nd = (int)C.ndofs;
+        for (int f = gt; f < nd; f += GT) {
+            int rem = f, row = 0;
+            bool inter = true;
+#pragma unroll
+            for (int k = D - 1; k >= 0; --k) {
+                const int ik = rem % n[k];
+                rem /= n[k];
+                if (ik < 1 || ik > n[k] - 2) inter = false;
+                else row += (ik - 1) * rsk[k];
+            }
+            cf[f] = inter ? x[row] : 0.0;
+        }
+    }
+}
+
+cudaError_t launch_pcg_fdg(Handle* h, double rtol, int maxit) {
+    if (h->fdg_comps.empty()) return cudaSuccess;
+    cudaError_t e;
+    const void* fn = h->d == 3 ? (const void*)k_pcg_fdg<3> : (h->d == 2 ? (const void*)k_pcg_fdg<2> : (const void*)k_pcg_fdg<1>);
+    int per_sm = 0, nsm = 148;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, FDG_THREADS, 0)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev)) != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    int grid = nsm * per_sm;
+    if (grid > FDG_MAX_CTAS) grid = FDG_MAX_CTAS;
+    const double rt2 = rtol * rtol;
+    for (int c : h->fdg_comps) {
+        void* args[] = {(void*)&h->d_comps, (void*)&c, (void*)&h->d_slotoff, (void*)&h->d_stencil, (void*)&h->d_rhs,
+                        (void*)&h->d_fd_uoff, (void*)&h->d_fd_loff, (void*)&h->d_fdU, (void*)&h->d_fdL,
+                        (void*)&h->d_ck, (void*)&h->d_x, (void*)&h->d_r, (void*)&h->d_z, (void*)&h->d_p,
+                        (void*)&h->d_q, (void*)&h->d_q2, (void*)&h->d_fdg_part, (void*)&h->d_cg,
+                        (void*)&h->d_relres, (void*)&h->d_coef, (void*)&rt2, (void*)&maxit};
+        if ((e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(FDG_THREADS), args, 0, h->stream)) != cudaSuccess)
+            return e;
+        h->launches[1]++;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace sgiga

@@ -27,6 +27,8 @@ constexpr int QMAX = 10;  // gauss_rule accepts q <= 10 (assembly.py:43)
 constexpr int WMAX = 2 * PMAX - 1;  // stencil slots per axis (2p+1)
 constexpr int GEO_PMAX = 8;         // geometry degree <= 7
 constexpr int FD_MMAX = 72;         // FD preconditioner: interior functions per diagonalised axis (smem eigen)
+constexpr int64_t FDG_MIN_ROWS = 65536;   // FD components at least this large: whole-GPU PCG (k_pcg_grid.cu)
+constexpr int FDG_MAX_CTAS = 1024;        // cooperative grid cap (partial-sum buffer size)
 constexpr int COMBINE_SORT_BITS = 12;                      // cell sort of the combine points
 constexpr int COMBINE_SORT_BINS = 1 << COMBINE_SORT_BITS;
 
@@ -249,6 +251,7 @@ cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s);
 cudaError_t launch_pcg_fd(Handle* h, double rtol, int maxit, cudaStream_t stream = nullptr);
 cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit);
 cudaError_t launch_fd_setup(Handle* h, cudaStream_t s);
+cudaError_t launch_pcg_fdg(Handle* h, double rtol, int maxit);
 size_t fd_comp_smem(const CompInfo& C, int d);
 cudaError_t launch_status(Handle* h);
 cudaError_t launch_expand(Handle* h);
