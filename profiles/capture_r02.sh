@@ -1,15 +1,28 @@
 #!/bin/bash
 # ncu evidence behind profiles/r02/ (run on the GPU box, one GPU, after the
-# same bench command exited 0 without ncu).  Usage: capture_r02.sh <outdir> [cfg]
-set -e
-OUT=${1:-gpurun_out/r02}; CFG=${2:-cfg5}
+# same bench commands exited 0 without ncu).  Usage: capture_r02.sh <outdir>
+# Then, here: python profiles/summarize.py <outdir> profiles/r02
+OUT=${1:-gpurun_out/r02}
 mkdir -p "$OUT"
-B="python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline"
-# launch list: per-launch durations of every kernel of the bench run
-ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
-    --log-file "$OUT/launches_${CFG}.csv" $B > "$OUT/ncu_launch_${CFG}.log" 2>&1
-# full section sets of the hot kernels (first launch of each)
-for k in k_assemble_fast k_metric k_combine_points_tiled k_pcg_fdl k_pcg_fd; do
-  ncu --set full --clock-control none --import-source on -k regex:"^${k}" -c 1 \
-      -o "$OUT/${k}_${CFG}" -f $B > "$OUT/ncu_${k}_${CFG}.log" 2>&1 || true
+# launch lists: per-launch durations of every kernel of one bench step
+for wl in cfg5 cfg5_tensor cfg2 cfg3 cfg1; do
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+      --log-file "$OUT/launches_${wl}.csv" python bench.py --config $wl --steps 1 --warmup 3 --no-cpu-baseline \
+      > "$OUT/ncu_launch_${wl}.log" 2>&1
 done
+full() {   # <kernel regex> <name> <bench args...>
+  local k=$1 n=$2; shift 2
+  ncu --set full --clock-control none --import-source on -k regex:"$k" -c 1 -o "$OUT/$n" -f \
+      python bench.py "$@" --steps 1 --warmup 3 --no-cpu-baseline > "$OUT/ncu_$n.log" 2>&1
+}
+full '^k_assemble_fast' k_assemble_fast_cfg5 --config cfg5
+full '^k_metric' k_metric_cfg5 --config cfg5
+full '^k_combine_points_tiled' k_combine_points_tiled_cfg5 --config cfg5
+full '^k_pcg_fdl' k_pcg_fdl_cfg5 --config cfg5
+full '^k_pcg_fd<' k_pcg_fd_cfg5 --config cfg5
+full '^k_pcg_fdg' k_pcg_fdg_cfg5_tensor --config cfg5_tensor
+full '^k_assemble_fast' k_assemble_fast_cfg5_tensor --config cfg5_tensor
+full '^k_assemble_fast' k_assemble_fast_cfg2 --config cfg2
+full '^k_assemble2d' k_assemble2d_cfg3_x1024 --config cfg3 --replicas 1024
+full '^k_assemble2d' k_assemble2d_cfg1_x1024 --config cfg1 --replicas 1024
+ls "$OUT"

@@ -5,8 +5,11 @@ wavefronts (bank conflicts) per CUDA source line.  Runs here.
     python profiles/hot_lines.py <report.ncu-rep> [top]
 """
 import csv
+import signal
 import subprocess
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25

@@ -31,17 +31,19 @@ def _launch_table(path: str, cfg: str) -> str:
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr, rows = rows[0], rows[1:]
     iN, iV = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    iS = hdr.index("Stream") if "Stream" in hdr else None
     names = [r[iN].split("(")[0] for r in rows]
     # the last step = everything after the last occurrence of the first kernel
     # of a step (k_basis_tables opens every sgiga_run)
     starts = [i for i, n in enumerate(names) if n.endswith("k_basis_tables")]
     lo = starts[-1] if starts else 0
-    sel = [(names[i], float(rows[i][iV].replace(",", ""))) for i in range(lo, len(rows))]
-    tot = sum(v for _, v in sel)
-    out = [f"# ncu launch list, {cfg} bench step (python bench.py --config {cfg} --steps 1 --warmup 3), last step",
+    sel = [(names[i], float(rows[i][iV].replace(",", "")), rows[i][iS] if iS is not None else "")
+           for i in range(lo, len(rows))]
+    tot = sum(v for _, v, _ in sel)
+    out = [f"# ncu launch list, {cfg} bench step (python bench.py --config <workload> --steps 1 --warmup 3), last step",
            "# ncu --metrics gpu__time_duration.sum --clock-control none (serialised, cold-ish caches)",
-           "# kernel, ns, share of the step's kernel time"]
-    out += [f"{n:48s} {v:10.0f} {100 * v / tot:6.1f}%" for n, v in sel]
+           "# kernel, ns, share of the step's summed kernel time, stream (side streams overlap the main one)"]
+    out += [f"{n:48s} {v:10.0f} {100 * v / tot:6.1f}%  stream {st}" for n, v, st in sel]
     out.append(f"{'total':48s} {tot:10.0f}")
     return "\n".join(out) + "\n"
 
@@ -73,24 +75,37 @@ def _full_summary(rep: str):
     return "\n".join(lines) + "\n", got
 
 
+def _hot_lines(rep: str, top: int = 15) -> str:
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = subprocess.run([sys.executable, os.path.join(here, "hot_lines.py"), rep, str(top)],
+                         capture_output=True, text=True).stdout
+    return "# per-source-line warp-stall samples and shared-memory excess wavefronts (profiles/hot_lines.py)\n" + out
+
+
 def main(src: str, dst: str) -> None:
+    """Every launches_<workload>.csv -> launches_<workload>.txt; every
+    <kernel>_<workload>.ncu-rep -> ncu_full_<kernel>_<workload>.txt (section
+    metrics, warp-state samples, hot source lines); the assembly captures
+    feed profiles/traffic.json (bench.py's roofline.traffic)."""
     os.makedirs(dst, exist_ok=True)
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    for cfg in ("cfg2", "cfg5"):
-        lp = os.path.join(src, f"launches_{cfg}.csv")
-        if os.path.exists(lp):
-            open(os.path.join(dst, f"launches_{cfg}.txt"), "w").write(_launch_table(lp, cfg))
-        rp = os.path.join(src, f"asm_{cfg}.ncu-rep")
-        if os.path.exists(rp):
-            txt, got = _full_summary(rp)
-            open(os.path.join(dst, f"ncu_full_assembly_{cfg}.txt"), "w").write(
-                f"# ncu --set full --clock-control none -k regex:k_assemble_fast -c 1, {cfg} bench\n" + txt)
-            if "dram__bytes_read.sum" in got:
-                traffic[cfg] = {
+    for f in sorted(os.listdir(src)):
+        path = os.path.join(src, f)
+        if f.startswith("launches_") and f.endswith(".csv"):
+            wl = f[len("launches_"):-4]
+            open(os.path.join(dst, f"launches_{wl}.txt"), "w").write(_launch_table(path, wl))
+        elif f.endswith(".ncu-rep"):
+            stem = f[:-8]
+            txt, got = _full_summary(path)
+            head = f"# ncu --set full --clock-control none --import-source on, first launch ({stem})\n"
+            open(os.path.join(dst, f"ncu_full_{stem}.txt"), "w").write(head + txt + _hot_lines(path))
+            if stem.startswith("k_assemble_fast_") and "dram__bytes_read.sum" in got:
+                wl = stem[len("k_assemble_fast_"):]
+                traffic[wl] = {
                     "kernel": "k_assemble_fast",
                     "dram_bytes_per_launch": got["dram__bytes_read.sum"] + got.get("dram__bytes_write.sum", 0.0),
-                    "source": os.path.join(os.path.basename(os.path.normpath(dst)), f"ncu_full_assembly_{cfg}.txt"),
+                    "source": os.path.join(os.path.basename(os.path.normpath(dst)), f"ncu_full_{stem}.txt"),
                 }
     json.dump(traffic, open(tpath, "w"), indent=1)
 
