@@ -65,7 +65,7 @@ static void free_all(Handle* h) {
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
                     h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps,
                     h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck, h->d_ticket, h->d_mcomp,
-                    h->d_spts, h->d_sout, h->d_blocks2, h->d_fdg_list, h->d_fdg_part};
+                    h->d_spts, h->d_sout, h->d_blocks2, h->d_fdg_list, h->d_fdg_part, h->d_fdg_ckpart};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel, h->h_sticky};
@@ -680,6 +680,7 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_fdl_list, h->fdl_comps.size());
     A_(d_fdg_list, h->fdg_comps.size());
     A_(d_fdg_part, 2 * FDG_MAX_CTAS);
+    A_(d_fdg_ckpart, h->fdg_comps.size() * MAXD * 256);   // k_fd_metric_scale_part chunk partials
     A_(d_fdl_off, h->comps.size());
     A_(d_fdl, h->fdl_total);
     A_(d_ck, (int64_t)MAXD * h->ncomp);

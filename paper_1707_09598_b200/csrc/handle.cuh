@@ -129,6 +129,7 @@ struct Handle {
     std::vector<int> fdg_comps;
     int* d_fdg_list = nullptr;
     double* d_fdg_part = nullptr;            // [2][FDG_MAX_CTAS] per-CTA partial sums
+    double* d_fdg_ckpart = nullptr;          // [n_fdg][MAXD][256] chunk partials of their c_k
     // line-FD comps (one long axis; k_pcg_fdl): per-comp offset into d_fdl
     // (stream-axis K / M bands + one banded Cholesky factor per line)
     std::vector<int> fdl_comps;

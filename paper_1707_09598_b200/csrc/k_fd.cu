@@ -665,6 +665,38 @@ k_fd_metric_scale(const CompInfo* __restrict__ comps, const int* __restrict__ li
     if (tid == 0) ckg[c * MAXD + k] = tot;
 }
 
+// the same c_k for the whole-GPU FD components (millions of points each):
+// FDG_SCALE_CHUNKS CTAs per (component, axis) write fixed-order partials,
+// one CTA per (component, axis) sums them in chunk order (deterministic)
+constexpr int FDG_SCALE_CHUNKS = 256;
+template <int D>
+__global__ void __launch_bounds__(256)
+k_fd_metric_scale_part(const CompInfo* __restrict__ comps, const int* __restrict__ list,
+                       const double* __restrict__ Gbuf, double* __restrict__ part) {
+    __shared__ double red[8];
+    const int ci = blockIdx.y, k = blockIdx.z, chunk = blockIdx.x, tid = threadIdx.x;
+    const CompInfo& C = comps[list[ci]];
+    const double* g = Gbuf + C.qp_off + (int64_t)sym_index(D, k, k) * C.nqp;
+    const int64_t n = C.nqp, per = (n + FDG_SCALE_CHUNKS - 1) / FDG_SCALE_CHUNKS;
+    const int64_t lo = chunk * per, hi = lo + per < n ? lo + per : n;
+    double s0 = 0.0, s1 = 0.0;
+    int64_t i = lo + tid;
+    for (; i + 256 < hi; i += 512) { s0 += __ldg(g + i); s1 += __ldg(g + i + 256); }
+    for (; i < hi; i += 256) s0 += g[i];
+    const double tot = fd_block_sum<256>(s0 + s1, red);
+    if (tid == 0) part[((int64_t)ci * MAXD + k) * FDG_SCALE_CHUNKS + chunk] = tot;
+}
+
+__global__ void __launch_bounds__(256)
+k_fd_metric_scale_fin(const int* __restrict__ list, const double* __restrict__ part, double* __restrict__ ckg) {
+    __shared__ double red[8];
+    const int ci = blockIdx.x, k = blockIdx.y, tid = threadIdx.x;
+    const double v = part[((int64_t)ci * MAXD + k) * FDG_SCALE_CHUNKS + tid];
+    const double tot = fd_block_sum<256>(v, red);
+    if (tid == 0) ckg[list[ci] * MAXD + k] = tot;
+}
+static_assert(FDG_SCALE_CHUNKS == 256, "one partial per thread of the finishing CTA");
+
 // banded interior K_s, M_s of a line-FD component's stream axis (lower band,
 // [i][k] = entry (i, i - k)), one CTA per component
 template <int D>
@@ -1108,15 +1140,18 @@ static cudaError_t launch_hi(void (*kern)(KArgs...), dim3 grid, dim3 block, size
 // then the line-FD stream-axis bands and per-line factors
 cudaError_t launch_fd_setup(Handle* h, cudaStream_t s) {
     const int nf = (int)h->fd_comps.size(), nl = (int)h->fdl_comps.size(), ng = (int)h->fdg_comps.size();
-    if (ng > 0) {   // c_k of the whole-GPU FD components
-        const dim3 gg((unsigned)ng, (unsigned)h->d);
-#define LAUNCH_SCALE_G(DD)                                                                            \
-    launch_hi(k_fd_metric_scale<DD>, gg, dim3(256), 0, s, h->d_comps, h->d_fdg_list, ng, h->d_fdg_list, h->d_G, h->d_ck)
+    if (ng > 0) {   // c_k of the whole-GPU FD components: chunked two-level sum
+        const dim3 gp(FDG_SCALE_CHUNKS, (unsigned)ng, (unsigned)h->d);
+#define LAUNCH_SCALE_G(DD)                                                                                       \
+    launch_hi(k_fd_metric_scale_part<DD>, gp, dim3(256), 0, s, (const CompInfo*)h->d_comps, (const int*)h->d_fdg_list, \
+              (const double*)h->d_G, h->d_fdg_ckpart)
         if (h->d == 1) { LAUNCH_SCALE_G(1); }
         else if (h->d == 2) { LAUNCH_SCALE_G(2); }
         else { LAUNCH_SCALE_G(3); }
 #undef LAUNCH_SCALE_G
-        h->launches[0]++;
+        launch_hi(k_fd_metric_scale_fin, dim3((unsigned)ng, (unsigned)h->d), dim3(256), 0, s,
+                  (const int*)h->d_fdg_list, (const double*)h->d_fdg_ckpart, h->d_ck);
+        h->launches[0] += 2;
     }
     if (nf + nl == 0) return cudaGetLastError();
     const dim3 g1((unsigned)(nf + nl), (unsigned)h->d);

@@ -380,3 +380,36 @@ def test_cfg5_tensor_matches_reference(golden):
         np.testing.assert_allclose([l2, h1], g["errors"], rtol=5e-4)   # 3 significant digits
     finally:
         b.close()
+
+
+def test_distributed_plan_step_world1_bitwise():
+    """DistributedPlan (the per-step form bench.py --gpus N uses: per-component
+    values on the device, NCCL all-gather, device plan-order sum) at world 1
+    equals the single-GPU combine bitwise, step after step."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_09598_b200.combination import evaluate_combined_points
+    from paper_1707_09598_b200.distributed import DistributedPlan
+    from paper_1707_09598_b200.scheduler import run_plan
+
+    cfg = configs.get_config("cfg2")
+    pts = cfg.points(4096)
+    sols, _ = run_plan(cfg.plan, cfg.problem)
+    ref = evaluate_combined_points(cfg.plan, sols, pts)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        dp = DistributedPlan(cfg.plan, cfg.problem, cfg.quad_points)
+        pd = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+        for _ in range(3):
+            assert np.array_equal(dp.step(pd).cpu().numpy(), ref)
+        dp.close()
+    finally:
+        dist.destroy_process_group()
