@@ -328,6 +328,14 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
         }
         h->small_comps.swap(keep_small);
         h->large_comps.swap(keep_large);
+        // line-FD / FD solves are issued longest first (LPT over the waves of
+        // clusters / CTAs): the cost of a component ~ its stored stencil
+        auto by_cost = [&](int a, int b) {
+            const int64_t ca = h->comps[a].rows * h->comps[a].nslots, cb = h->comps[b].rows * h->comps[b].nslots;
+            return ca != cb ? ca > cb : a < b;
+        };
+        std::stable_sort(h->fdl_comps.begin(), h->fdl_comps.end(), by_cost);
+        std::stable_sort(h->fd_comps.begin(), h->fd_comps.end(), by_cost);
         // tables with identical knot vectors share one factorisation
         for (int t = 0; t < ntab; ++t) {
             if (!used[t]) continue;

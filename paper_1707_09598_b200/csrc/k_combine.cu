@@ -622,7 +622,9 @@ cudaError_t launch_combine_points(Handle* h, const double* d_pts, int64_t npts, 
     // CTA (more resident CTAs); larger: 64 points / 256 threads (measured)
     const bool small_cta = h->ncomp <= 64 && h->p <= 3;
     int npt = small_cta ? 32 : 64;
-    while (npt > 1 && smem_of(npt) > 100 * 1024) npt >>= 1;
+    // <= 40 KB per CTA: the (component, point) contractions are gather-latency
+    // bound, so more resident CTAs (5 per SM) beat more points per CTA
+    while (npt > 1 && smem_of(npt) > 40 * 1024) npt >>= 1;
     if (smem_of(npt) > 200 * 1024 || h->opt.combine_perthread) {   // huge plans: one thread per point
         unsigned blocks = (unsigned)((npts + 127) / 128);
 #define LAUNCH_CP(DD, PP)                                                                     \
