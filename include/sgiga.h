@@ -103,8 +103,14 @@ typedef struct sgiga_problem_desc {
     const double* geo_knots;    /* concatenated [sum geo_nknots]              */
     const double* geo_hw;       /* [n_1*...*n_d*(d+1)] C order: (w*P, w)      */
     int32_t forcing_id;         /* enum sgiga_forcing                         */
-    int32_t reserved;
+    int32_t flags;              /* SGIGA_FLAG_*                               */
 } sgiga_problem_desc;
+
+/* descriptor flags */
+enum sgiga_flags {
+    SGIGA_FLAG_ASSEMBLY_ONLY = 1   /* the handle only assembles (the multipatch driver glues and solves
+                                      on its own): no FD preconditioner set-up is enqueued            */
+};
 
 typedef struct sgiga_handle sgiga_handle;
 
@@ -216,6 +222,14 @@ int sgiga_error_norms(sgiga_handle* h, const double* pts_per_dir,
  * verdict comes from sgiga_run_wait.                                      */
 int sgiga_run_components_async(sgiga_handle* h, double rtol, int32_t maxit, const double* pts_dev,
                                int64_t npts, double* out_dev);
+
+/* Batched sgiga_edge_projection_system: one launch for nedge edges of this
+ * patch handle.  d_edges [nedge][3] = (component, running axis, side),
+ * d_offsets [nedge] = offset of the edge's band [n][2p+1] in d_base (its
+ * rhs [n] follows the band); max_edge_qp >= nel*q of every edge.  Device
+ * arrays; enqueued on the handle's stream.                                */
+int sgiga_edge_projection_batch(sgiga_handle* h, int32_t nedge, const int32_t* d_edges, const int64_t* d_offsets,
+                                int32_t max_edge_qp, int32_t solution_id, double* d_base);
 
 /* Multi-GPU combine: out[pt] = sum_c coef[c] * src[row[c]][pt]
  * over the plan's terms in plan order, with the exact operations of the

@@ -24,6 +24,8 @@ SGIGA_ERR_CUDA = -5
 SGIGA_ERR_STATE = -6
 SGIGA_ERR_KEY = -7
 
+FLAG_ASSEMBLY_ONLY = 1   # sgiga_flags
+
 FORCING_HOST = -1
 FORCING_ZERO = 0
 FORCING_SIN_PRODUCT = 1
@@ -42,7 +44,7 @@ EXPORTED = (
     "sgiga_coefficients", "sgiga_set_coefficients", "sgiga_combine_points", "sgiga_run",
     "sgiga_run_async", "sgiga_run_wait", "sgiga_run_host_async",
     "sgiga_combine_grid", "sgiga_error_norms", "sgiga_subset_error_norms", "sgiga_export_csr", "sgiga_phase_stats",
-    "sgiga_basis_table", "sgiga_plan_order_sum", "sgiga_run_components_async",
+    "sgiga_basis_table", "sgiga_plan_order_sum", "sgiga_run_components_async", "sgiga_edge_projection_batch",
     "sgiga_iterations", "sgiga_kernel_times", "sgiga_stream", "sgiga_destroy", "sgiga_last_error",
     "sgiga_device_count", "sgiga_local_poisson_systems",
     "sgiga_full_patch_system", "sgiga_edge_projection_system", "sgiga_gather_sum", "sgiga_gather",
@@ -72,7 +74,7 @@ class ProblemDesc(ct.Structure):
         ("geo_knots", ct.POINTER(ct.c_double)),
         ("geo_hw", ct.POINTER(ct.c_double)),
         ("forcing_id", ct.c_int32),
-        ("reserved", ct.c_int32),
+        ("flags", ct.c_int32),
     ]
 
 
@@ -117,6 +119,7 @@ def _declare(lib):
         "sgiga_export_csr": ([VP, ct.c_int32, P_I64, P_I64, P_I32, P_F64, P_F64], ct.c_int),
         "sgiga_phase_stats": ([VP, P_F32, P_I64], ct.c_int),
         "sgiga_run_components_async": ([VP, ct.c_double, ct.c_int32, VP, ct.c_int64, VP], ct.c_int),
+        "sgiga_edge_projection_batch": ([VP, ct.c_int32, VP, VP, ct.c_int32, ct.c_int32, VP], ct.c_int),
         "sgiga_plan_order_sum": ([VP, ct.c_int32, ct.c_int64, VP, VP, VP, VP], ct.c_int),
         "sgiga_basis_table": ([VP, ct.c_int32, ct.c_int32, P_I32, P_F64, P_F64, P_F64, P_F64], ct.c_int),
         "sgiga_iterations": ([VP, P_I32], ct.c_int),

@@ -280,7 +280,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
     // one-CTA eigen kernel (<= FD_MMAX interior functions) and whose vectors
     // fit shared memory; the others keep the Jacobi-PCG paths
     {
-        const bool fd_on = !h->opt.no_fd;
+        const bool fd_on = !h->opt.no_fd && !(D->flags & SGIGA_FLAG_ASSEMBLY_ONLY);
         const int ntab = (int)h->tabs.size();
         h->fd_comps.clear(); h->fd_uniq.clear();
         h->fd_uoff.assign(ntab, 0); h->fd_loff.assign(ntab, 0);

@@ -40,6 +40,7 @@ class PlanSpec:
     knot_tables: dict       # (axis, key) -> breakpoints; key = level (or table id)
     patch: object           # NurbsPatch-like
     forcing_id: int
+    flags: int = 0          # sgiga_flags (include/sgiga.h), e.g. 1 = assembly only
 
 
 def knot_tables_for(terms, d, degree, regularity, grading=1.0, knot_rule: Callable | None = None):
@@ -91,7 +92,7 @@ def make_desc(spec: PlanSpec):
         max_level, _lib.ptr(K["bp_off"], ct.c_int64), _lib.ptr(K["bp_cnt"], ct.c_int32),
         _lib.ptr(K["bps"], ct.c_double), _lib.ptr(K["gdeg"], ct.c_int32),
         _lib.ptr(K["gnk"], ct.c_int32), _lib.ptr(K["gk"], ct.c_double),
-        _lib.ptr(K["hw"], ct.c_double), spec.forcing_id, 0,
+        _lib.ptr(K["hw"], ct.c_double), spec.forcing_id, int(spec.flags),
     )
     return desc, keep
 

@@ -413,3 +413,52 @@ def test_distributed_plan_step_world1_bitwise():
         dp.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("graded", [False, True])
+def test_batched_edge_projection_matches_per_edge(graded):
+    """sgiga_edge_projection_batch (one launch per patch, per-point map /
+    tangent / Dirichlet data shared) == sgiga_edge_projection_system per
+    edge, bitwise (same operations, same order)."""
+    import dataclasses
+
+    import torch
+
+    from paper_1707_09598_b200.analysis import solution_id_of
+    from paper_1707_09598_b200.multipatch import _PatchProblem, lshape_problem
+    prob = lshape_problem(graded=graded)
+    cfg = configs.get_multipatch_config("cfg4_graded" if graded else "cfg4")
+    lib = _lib.load()
+    sid = solution_id_of(prob.dirichlet)
+    p, W = prob.degree, 2 * prob.degree + 1
+    for pi, patch in enumerate(prob.patches):
+        spec = make_spec(tuple(cfg.plan.terms), _PatchProblem(patch, prob.forcing, p, prob.regularity), None,
+                         knot_rule=prob.knot_rules[pi])
+        b = Batch(dataclasses.replace(spec, flags=_lib.FLAG_ASSEMBLY_ONLY))
+        try:
+            b.assemble()
+            edges, offs, tot, maxq = [], [], 0, 0
+            for c in range(len(cfg.plan)):
+                for axis in (0, 1):
+                    for side in (0, 1):
+                        n = int(b.dims[c][1 - axis])
+                        edges.append((c, 1 - axis, side))
+                        offs.append(tot)
+                        tot += n * W + n
+                        maxq = max(maxq, 3 * 2 ** int(cfg.plan.betas[c][1 - axis]))
+            ref = torch.zeros(tot, dtype=torch.float64, device="cuda")
+            for (c, ax, side), o in zip(edges, offs):
+                n = int(b.dims[c][ax])
+                _lib.check(lib.sgiga_edge_projection_system(b.h, c, ax, side, sid,
+                                                            ct.c_void_p(ref.data_ptr() + 8 * o),
+                                                            ct.c_void_p(ref.data_ptr() + 8 * (o + n * W))))
+            got = torch.zeros(tot, dtype=torch.float64, device="cuda")
+            e = torch.as_tensor(np.array(edges, dtype=np.int32), device="cuda")
+            od = torch.as_tensor(np.array(offs, dtype=np.int64), device="cuda")
+            _lib.check(lib.sgiga_edge_projection_batch(b.h, len(edges), ct.c_void_p(e.data_ptr()),
+                                                       ct.c_void_p(od.data_ptr()), maxq, sid,
+                                                       ct.c_void_p(got.data_ptr())))
+            torch.cuda.synchronize()
+            assert torch.equal(got, ref)
+        finally:
+            b.close()

@@ -141,3 +141,88 @@ def test_cfg4_full_runs_and_grading_helps():
 def test_interface_dataclass():
     f = Interface(0, 0, 1, 1, 0, 0)
     assert (f.a, f.b) == (0, 1)
+
+
+def _loop_structures(dims, glue, p):
+    """Straightforward restatement of the cfg4 bookkeeping (the round-1 loop
+    builder): per-entry source lists in insertion order, keys sorted."""
+    W = 2 * p + 1
+    ncomp, npatch = len(dims), len(dims[0])
+    src_off, total = {}, 0
+    for c in range(ncomp):
+        for pi in range(npatch):
+            nx, ny = dims[c][pi]
+            src_off[(c, pi)] = total
+            total += nx * ny * W * W + nx * ny
+    eoff, etot = {}, 0
+    for c in range(ncomp):
+        for (pi, axis, side) in glue[c].dir_sides:
+            eoff[(c, pi, axis, side)] = etot
+            etot += dims[c][pi][1 - axis] * (W + 1)
+    mats = {"AI": ({}, {}), "AB": ({}, {}), "BB": ({}, {})}
+    offI, offB = [0], [0]
+    for c in range(ncomp):
+        g = glue[c]
+        baseI, baseB = offI[-1], offB[-1]
+        for pi in range(npatch):
+            nx, ny = dims[c][pi]
+            o, rows = src_off[(c, pi)], nx * ny
+            gp = g.gpos[g.base[pi]:g.base[pi] + rows]
+            for r in range(rows):
+                gr = gp[r]
+                if gr >= g.nI:
+                    continue
+                ix, iy = divmod(r, ny)
+                mats["AI"][1].setdefault(baseI + gr, []).append(o + rows * W * W + r)
+                for sx in range(W):
+                    for sy in range(W):
+                        jx, jy = ix + sx - p, iy + sy - p
+                        if not (0 <= jx < nx and 0 <= jy < ny):
+                            continue
+                        gc = gp[jx * ny + jy]
+                        s_idx = o + (sx * W + sy) * rows + r
+                        if gc < g.nI:
+                            mats["AI"][0].setdefault((baseI + gr, baseI + gc), []).append(s_idx)
+                        else:
+                            mats["AB"][0].setdefault((baseI + gr, baseB + gc - g.nI), []).append(s_idx)
+        for (pi, axis, side) in g.dir_sides:
+            o, n = eoff[(c, pi, axis, side)], dims[c][pi][1 - axis]
+            gl = [g.gpos[d] - g.nI for d in g.side_dofs(pi, axis, side)]
+            for i in range(n):
+                mats["BB"][1].setdefault(baseB + gl[i], []).append(o + n * W + i)
+                for jj in range(max(0, i - p), min(n, i + p + 1)):
+                    mats["BB"][0].setdefault((baseB + gl[i], baseB + gl[jj]), []).append(o + i * W + (jj - i + p))
+        offI.append(baseI + g.nI)
+        offB.append(baseB + g.nB)
+    return mats, offI, offB, total, etot
+
+
+@pytest.mark.parametrize("graded", [False, True])
+def test_vectorised_multipatch_structures_match_loop_builder(graded):
+    """The vectorised bookkeeping of the cfg4 session equals the per-entry
+    loop builder: same CSR keys, same source lists in the same order (so the
+    device's fixed-order sums are unchanged)."""
+    from paper_1707_09598_b200.multipatch import _Glue, multipatch_structures
+
+    cfg = configs.get_multipatch_config("cfg4_graded" if graded else "cfg4")
+    prob, p = cfg.problem, cfg.problem.degree
+    dims = [[tuple(prob.knot_rules[pi](k, beta[k]).n for k in range(2)) for pi in range(3)]
+            for beta in cfg.plan.betas]
+    glue = [_Glue(d, prob) for d in dims]
+    st = multipatch_structures(dims, glue, p)
+    mats, offI, offB, total, etot = _loop_structures(dims, glue, p)
+    assert st["offI"] == offI and st["offB"] == offB
+    assert st["src_total"] == total and st["esrc_total"] == etot
+    for name in ("AI", "AB", "BB"):
+        csr = st[name]
+        ent, rhs = mats[name]
+        keys = sorted(ent)
+        assert csr["nnz"] == len(keys)
+        rows = np.repeat(np.arange(csr["nrows"]), np.diff(csr["rowptr"]))
+        assert [(int(r), int(c)) for r, c in zip(rows, csr["col"])] == keys
+        for k, key in enumerate(keys):
+            s, e = csr["src_start"][k], csr["src_start"][k + 1]
+            assert csr["src_idx"][s:e].tolist() == ent[key]
+        for r in range(csr["nrows"]):
+            s, e = csr["rhs_start"][r], csr["rhs_start"][r + 1]
+            assert csr["rhs_idx"][s:e].tolist() == rhs.get(r, [])
