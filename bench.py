@@ -300,6 +300,83 @@ def run_reference(args, cfg):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def run_multipatch(args, name):
+    """BASELINE configs[3] (cfg4 / cfg4_graded): the L-shape from 3 patches,
+    p = 2, w = 9, 15 components glued C0 with Dirichlet lifting
+    (multipatch.MultipatchSession).  A step = assemble every patch, glue,
+    project the Dirichlet data, solve (batched cluster CSR PCG), expand, then
+    evaluate the 4 096 points on every patch."""
+    import torch
+
+    from paper_1707_09598_b200.configs import get_multipatch_config
+    from paper_1707_09598_b200.multipatch import MultipatchSession
+
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    cfg = get_multipatch_config(name)
+    pts = cfg.points()
+    n_comp = len(cfg.plan)
+    if args.impl == "reference":   # the multipatch oracle (numpy restatement), one step
+        from oracle import multipatch_oracle as MO
+        from paper_1707_09598_b200.multipatch import _PatchProblem
+        from paper_1707_09598_b200.scheduler import make_spec
+        prob = cfg.problem
+        specs = [make_spec(tuple(cfg.plan.terms), _PatchProblem(pt, prob.forcing, prob.degree, prob.regularity),
+                           cfg.quad_points, knot_rule=prob.knot_rules[pi]) for pi, pt in enumerate(prob.patches)]
+        t0 = time.perf_counter()
+        MO.run_plan(specs, prob, cfg.quad_points)
+        dt = time.perf_counter() - t0
+        line = {"impl": "reference", "metric": METRIC, "value": n_comp / dt, "unit": UNIT, "n_gpus": ws,
+                "steps": 1, "warmup": 0, "ms_per_step": 1e3 * dt, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config recipe)",
+                "config": {"workload": name, "d": 2, "degree": 2, "level_w": 9, "components": n_comp, "patches": 3,
+                           "points": cfg.n_points, "rtol": args.rtol},
+                "cpu_baseline": {"value": n_comp / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                                 "cpu_model": cpu_model(),
+                                 "sample": "oracle/multipatch_oracle.py (dense numpy restatement), full plan, one step"},
+                "e2e": {"value": n_comp / dt, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+    sess = MultipatchSession(cfg.plan, cfg.problem, cfg.quad_points, rtol=args.rtol)
+    for _ in range(max(args.warmup, 3)):
+        sess.solve()
+    torch.cuda.synchronize()
+    sampler = clock_sampler(local)
+    time.sleep(0.01)
+    sampler.begin()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0 = time.perf_counter()
+    for s, e in ev:
+        s.record()
+        sess.solve()
+        vals = [sess.batches[pi].combine_points(pts) for pi in range(3)]
+        e.record()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / args.steps
+    sampler.end()
+    clocks = sampler.stop()
+    ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
+    line = {"metric": METRIC, "value": n_comp / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config recipe)",
+            "config": {"workload": name, "d": 2, "degree": 2, "level_w": 9, "components": n_comp, "patches": 3,
+                       "points": cfg.n_points, "rtol": args.rtol},
+            "timing": "CUDA events around each step (the session's host synchronisations included)",
+            "e2e": {"value": n_comp / wall, "unit": UNIT, "h2d_bytes_per_step": int(3 * pts.nbytes),
+                    "d2h_bytes_per_step": int(3 * pts.shape[0] * 8), "ms_per_step": 1e3 * wall,
+                    "path": "MultipatchSession.solve + Batch.combine_points (host points in, host values out)"},
+            "pcg_iterations": {"interior_max": int(sess.iters.max()), "interior_sum": int(sess.iters.sum()),
+                               "boundary_max": int(sess.bnd_iters.max())},
+            "clocks": clocks, "cpu_baseline": None}
+    sol = sess.solution()
+    line["errors_l2_h1"] = list(sol.error_norms((8, 8), cfg.quad_points))
+    print(json.dumps(line), flush=True)
+    sol.close()
+    return 0
+
+
 def run_split(args, cfg):
     """N > 1, --mode split: ONE plan's components LPT-sharded over the ranks
     (distributed.DistributedPlan): per step every rank assembles + solves its
@@ -655,6 +732,8 @@ def main():
     args = ap.parse_args()
     from paper_1707_09598_b200.configs import get_config
 
+    if args.config in ("cfg4", "cfg4_graded"):
+        return run_multipatch(args, args.config)
     cfg = get_config(args.config)
     if args.impl == "reference":
         return run_reference(args, cfg)
