@@ -96,8 +96,14 @@ struct FastCfg {
     static constexpr int NT2 = SPLIT ? 5 : 4;
     // stage-2 outputs: 3-D -- one (s_a, s_b) block per pair (summed by stream
     // type in stage 3) + the load term; 2-D -- NT2 slots + load
-    static constexpr int NI2 = (PIPE ? NPAIR : NT2) * WAB + 1;
     static constexpr int S2C = PIPE && P >= 5 ? 2 : 1;  // stage-2 s_b columns per thread (register budget)
+    // 3-D: S2[pair][s_a][S2R] rows padded to an even length, so a stage-2
+    // thread's two adjacent s_b columns leave as ONE 16-byte store (lanes on
+    // distinct bank quads); even buffer stride
+    static constexpr int S2R = PIPE && S2C == 2 ? ((WB + 1) & ~1) : WB;
+    static constexpr int S2B = WA * S2R;               // one pair block
+    static constexpr int NI2 = PIPE ? ((NPAIR * S2B + 2) & ~1) : NT2 * WAB + 1;
+    static constexpr int LOAD2P = PIPE ? NPAIR * S2B : NT2 * WAB;   // the load term's slot
     static constexpr int NSB2 = (WB + S2C - 1) / S2C;  // stage-2 column groups (s_b .. s_b + S2C - 1)
     static constexpr int S2T = PIPE ? 32 * ((NPAIR * NSB2 + 1 + 31) / 32) : 0;   // one (pair, s_b pair) each
     static constexpr int S3T = PIPE ? 32 * ((WAB + P + 31) / 32) : 0;         // one (s_a, s_b) column / load row each
@@ -384,16 +390,16 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             }
         // stage 3 sums the pair blocks of each stream type (fixed pair order):
         // type 0 = pairs without s, 1 = (m, s), 2 = (s, n), 3 = (s, s)
-        const int ty_off[9] = {(ka * D + ka) * F::WAB, (ka * D + kb) * F::WAB, (kb * D + ka) * F::WAB,
-                               (kb * D + kb) * F::WAB, (ka * D + s) * F::WAB,  (kb * D + s) * F::WAB,
-                               (s * D + ka) * F::WAB,  (s * D + kb) * F::WAB,  (s * D + s) * F::WAB};
+        const int ty_off[9] = {(ka * D + ka) * F::S2B, (ka * D + kb) * F::S2B, (kb * D + ka) * F::S2B,
+                               (kb * D + kb) * F::S2B, (ka * D + s) * F::S2B,  (kb * D + s) * F::S2B,
+                               (s * D + ka) * F::S2B,  (s * D + kb) * F::S2B,  (s * D + s) * F::S2B};
         auto load_bs = [&](int e) {   // G3: stream basis values/derivatives of element e
             double* Bd = Bs + (e & 1) * 2 * Q * P;
             for (int idx = g3t; idx < 2 * Q * P; idx += S3T) {
                 const int der = idx / (Q * P), rem = idx % (Q * P);
-                Bd[idx] = vals[Ts.val_off + (der ? nq_s * P : 0) + (int64_t)e * Q * P + rem];
+                cp_async8(&Bd[idx], vals + Ts.val_off + (der ? nq_s * P : 0) + (int64_t)e * Q * P + rem);
             }
-        };
+        };   // (cp.async: completed by the G3 wait at the end of the NEXT interval)
         auto flush3 = [&](int i) {   // G3: row i -> stencil / rhs / dinv
             const int64_t row = row_base + (int64_t)(i - 1) * rs_s;
             const double* accr = Acc + ((i % F::RING) * W) * F::WAB;
@@ -418,7 +424,11 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             for (int bl = 0; bl < P; ++bl) R3[al][bl] = 0.0;
         auto bar3 = [&]() { asm volatile("bar.sync 1, %0;\n" ::"r"(S3T) : "memory"); };
         if (nplanes > 0) {
-            if (inG3) load_bs(e_first);
+            if (inG3) {
+                load_bs(e_first);
+                cp_async_commit();
+                cp_async_wait_all();
+            }
             if constexpr (F::TMA) {
                 // (the first GPD planes were issued at kernel entry)
             } else {
@@ -429,7 +439,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         }
         // phase profile (SGIGA_ASM_PROFILE=1): block 0's group leaders record
         // their own work and the whole interval (work + barrier wait)
-        const bool prf = prof != nullptr && blockIdx.x == 0 && (tid == 0 || tid == S1T || tid == S1T + S2T);
+        const bool prf = prof != nullptr && blockIdx.x == 0 && (tid & 31) == 0;   // every warp's lane 0
         long long pw = 0, pt = 0, p0 = prf ? clk64() : 0;
         for (int j = 0; nplanes > 0 && j < nplanes + 2; ++j) {
             if (j + F::GPD < nplanes) {
@@ -443,7 +453,10 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     double* S1w = S1 + (j & 1) * F::nS1;
                     const int half = F::PPW == 2 ? (lane >> 4) : 0;
                     const int xa = F::PPW == 2 ? (lane & 15) : lane;
-                    const int unit = warp * F::PPW + half;
+                    // GRP: warps -> units so the heavy (two-pair) units sit on SM
+                    // sub-partitions (warp % 4) apart from stage 2's two warps
+                    // (6, 7): {T, T, S, T, S, load}
+                    const int unit = F::GRP ? (warp == 1 ? 2 : warp == 2 ? 1 : warp) : warp * F::PPW + half;
                     const int prr = unit < F::NGRP ? 0 : (unit == F::NGRP ? NPAIR : NPAIR + 1);   // load unit -> NPAIR
                     if (unit < F::NGRP && xa < F::NA) {
                         // groups in axis roles (a = ka, b = kb, s): {aa, ss}, {as}, {ab, sb},
@@ -486,14 +499,19 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                 }
                             }
                         }
-                        double* out = S1w + ((m0 * D + n0) * F::NA + xa) * F::S1W;
+                        // 16-byte stores when the rows are even (lanes on distinct bank quads)
+                        auto store_row = [&](double* o, const double* a) {
+                            if constexpr (F::S1W % 2 == 0) {
 #pragma unroll
-                        for (int q2 = 0; q2 < W; ++q2) out[q2] = acc[q2];
-                        if (two) {
-                            double* o1 = S1w + ((m1 * D + n1) * F::NA + xa) * F::S1W;
+                                for (int q2 = 0; q2 < W; q2 += 2)
+                                    *reinterpret_cast<double2*>(o + q2) = make_double2(a[q2], q2 + 1 < W ? a[q2 + 1] : 0.0);
+                            } else {
 #pragma unroll
-                            for (int q2 = 0; q2 < W; ++q2) o1[q2] = acd[q2];
-                        }
+                                for (int q2 = 0; q2 < W; ++q2) o[q2] = a[q2];
+                            }
+                        };
+                        store_row(S1w + ((m0 * D + n0) * F::NA + xa) * F::S1W, acc);
+                        if (two) store_row(S1w + ((m1 * D + n1) * F::NA + xa) * F::S1W, acd);
                     } else if (prr == NPAIR && xa < F::NA) {   // load: SL1 = sum_xb L phiB
                         const double* gcol = Gw + (F::NG - 1) * F::NB * F::NAP + xa;
                         double acc = 0.0;
@@ -512,7 +530,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                         double acc = 0.0;
 #pragma unroll
                         for (int x = 0; x < F::NA; ++x) acc += sl[x] * phiA[x];
-                        S2w[F::NI2 - 1] = acc;
+                        S2w[F::LOAD2P] = acc;
                     } else if (s2_on) {
                         // S2[pair][s_a][s_b] = sum_xa S1[pair][xa][s_b] Ta[xa][s_a - t(xa)],
                         // two adjacent s_b columns per thread: one 16-byte S1 load and
@@ -551,17 +569,14 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                 }
                             }
                         }
-                        double* o2 = S2w + s2_pr * F::WAB + s2_sb;
+                        double* o2 = S2w + s2_pr * F::S2B + s2_sb;
                         if constexpr (F::S2C == 1) {
 #pragma unroll
-                            for (int sa = 0; sa < W; ++sa) o2[sa * F::WB] = acc[sa] + acd[sa];
-                        } else {
+                            for (int sa = 0; sa < W; ++sa) o2[sa * F::S2R] = acc[sa] + acd[sa];
+                        } else {   // columns s_b, s_b + 1 (the pad column for the last s_b)
 #pragma unroll
-                            for (int sa = 0; sa < W; ++sa) o2[sa * F::WB] = acc[sa];
-                        }
-                        if (F::S2C == 2 && s2_sb + 1 < F::WB) {
-#pragma unroll
-                            for (int sa = 0; sa < W; ++sa) o2[sa * F::WB + 1] = acd[sa];
+                            for (int sa = 0; sa < W; ++sa)
+                                *reinterpret_cast<double2*>(o2 + sa * F::S2R) = make_double2(acc[sa], acd[sa]);
                         }
                     }
                 }
@@ -575,9 +590,8 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     const double* Bp = Bs + (ep & 1) * 2 * Q * P + gp * P;   // values; derivatives at +Q*P
                     const double* S2r = S2 + (jp & 1) * F::NI2;
                     if (g3t < F::WAB) {
-                        const int sab = g3t;
                         // stream types: 0 = pairs without s, 1 = (m, s), 2 = (s, n), 3 = (s, s)
-                        const double* q = S2r + sab;
+                        const double* q = S2r + (g3t / F::WB) * F::S2R + g3t % F::WB;
                         const double s0 = ((q[ty_off[0]] + q[ty_off[1]]) + q[ty_off[2]]) + q[ty_off[3]];
                         const double s1 = q[ty_off[4]] + q[ty_off[5]], s2v = q[ty_off[6]] + q[ty_off[7]];
                         const double s3 = q[ty_off[8]];
@@ -594,7 +608,7 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                             for (int bl = 0; bl < P; ++bl) R3[al][bl] += vb[bl] * c0 + db[bl] * c1;
                         }
                     } else if (g3t < F::WAB + P) {
-                        RL3 += Bp[g3t - F::WAB] * S2r[F::NI2 - 1];
+                        RL3 += Bp[g3t - F::WAB] * S2r[F::LOAD2P];
                     }
                     if (gp == Q - 1) {   // element ep complete
                         if (g3t < F::WAB) {
@@ -631,6 +645,10 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             }
             if (prf) pw += clk64() - p0;
             if constexpr (!F::TMA) cp_async_wait_all();
+            else if (inG3) {   // one (possibly empty) group per interval: wait for all but this one
+                cp_async_commit();
+                cp_async_wait_prev();
+            }
             __syncthreads();
             if (prf) {
                 const long long t1 = clk64();
@@ -640,9 +658,12 @@ k_assemble_fast(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         }
         if (prf) {
             const int g = inG1 ? 0 : (inG2 ? 1 : 2);
-            prof[2 * g] = pw;
-            prof[2 * g + 1] = pt;
-            if (g == 0) prof[6] = nplanes + 2;
+            if (tid == 0 || tid == S1T || tid == S1T + S2T) {
+                prof[2 * g] = pw;
+                prof[2 * g + 1] = pt;
+            }
+            if (g == 0 && tid == 0) prof[6] = nplanes + 2;
+            prof[8 + (tid >> 5)] = pw;   // per-warp work
         }
     } else {
     const bool pr = prof != nullptr && blockIdx.x == 0 && tid == 0;   // phase profile
@@ -893,18 +914,23 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     if (*err != cudaSuccess) return true;
     long long* prof = nullptr;
     if (h->opt.asm_profile) {
-        cudaMalloc(&prof, 8 * sizeof(long long));
-        cudaMemsetAsync(prof, 0, 8 * sizeof(long long), h->stream);
+        cudaMalloc(&prof, 40 * sizeof(long long));
+        cudaMemsetAsync(prof, 0, 40 * sizeof(long long), h->stream);
     }
     void* args[] = {(void*)&h->d_comps, (void*)&h->d_tabs, (void*)&h->d_pencils, (void*)&h->d_tabvals,
                     (void*)&h->d_G, (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv,
                     (void*)&prof, (void*)&h->d_tmaps};
     *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(nthreads), args, smem, h->stream);
     if (prof) {
-        long long t[8];
+        long long t[40];
         cudaStreamSynchronize(h->stream);
         cudaMemcpy(t, prof, sizeof t, cudaMemcpyDeviceToHost);
         const double n = t[6] > 0 ? (double)t[6] : 1.0;
+        if (h->d == 3) {
+            fprintf(stderr, "asm-profile per-warp work cycles/interval:");
+            for (int w = 0; w < nthreads / 32; ++w) fprintf(stderr, " %.0f", t[8 + w] / n);
+            fprintf(stderr, "\n");
+        }
         if (h->d == 3)
             fprintf(stderr, "asm-profile block0 intervals=%lld cycles/interval: G1 work=%.0f total=%.0f | G2 work=%.0f"
                     " total=%.0f | G3 work=%.0f total=%.0f\n", t[6], t[0] / n, t[1] / n, t[2] / n, t[3] / n, t[4] / n,
