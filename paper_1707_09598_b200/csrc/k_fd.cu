@@ -256,6 +256,7 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
     const int nc0 = np0 * np0, nc1 = np1 * np1, ncs = nc0 + nc1;
     const int nitems = ncs + np0 * s0 + np1 * s1;
     int nsweep = 0;
+    long long acc_rot = 0, acc_upd = 0;   // probe (SGIGA_FD_PROFILE)
     // this thread's update items, decoded once: (pair k, pair l) blocks of C
     // (same half), then (pair k, row i of its half) rotations of V
     int dk_[EIG_ITEMS], dl_[EIG_ITEMS];
@@ -283,6 +284,7 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
         if (off <= 1e-26 * dia) break;
         ++nsweep;
         for (int st = 0; st < nsteps; ++st) {
+            long long tr0 = (prof && tid == 0) ? clock64() : 0;
             if (tid < npt) {   // rotation of pair tid (its half's round-robin pairing, step st)
                 const int b = tid < np0 ? 0 : 1, k = b ? tid - np0 : tid;
                 const int nb = b ? n1 : n0, sb = b ? s1 : s0, ob = b ? o1 : 0;
@@ -316,6 +318,7 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
                 rp[tid] = pi; rq[tid] = qi; rc[tid] = c; rs[tid] = sn;
             }
             __syncthreads();
+            long long tr1 = (prof && tid == 0) ? clock64() : 0;
 #pragma unroll
             for (int u = 0; u < EIG_ITEMS; ++u) {
                 const int idx = tid + u * EIG_THREADS;
@@ -353,10 +356,16 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
                 }
             }
             __syncthreads();
+            if (prof && tid == 0) { acc_rot += tr1 - tr0; acc_upd += clock64() - tr1; }
         }
     }
     stamp(3);
-    if (prof && tid == 0) { prof[blockIdx.x * 8 + 5] = nsweep; prof[blockIdx.x * 8 + 6] = m + (sym ? 1000 : 0); }
+    if (prof && tid == 0) {
+        prof[blockIdx.x * 8 + 5] = nsweep;
+        prof[blockIdx.x * 8 + 6] = m + (sym ? 1000 : 0);
+        prof[blockIdx.x * 8 + 7] = acc_rot;
+        prof[blockIdx.x * 8 + 4] = acc_upd;
+    }
     // U' = L^-T Q (column j per thread, back substitution in its diagonal block)
     if (tid < m) {
         const int j = tid;
@@ -386,7 +395,6 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
         U[idx] = v;
     }
     for (int a = tid; a < m; a += EIG_THREADS) dL[loff[t] + a] = Cm[a * FD_LD + a];
-    stamp(4);
 }
 
 // ---- 3b: FD-preconditioned CG, one CTA per component -----------------------
@@ -1213,8 +1221,8 @@ cudaError_t launch_fd_eigen(Handle* h, cudaStream_t s) {
         cudaMemcpyAsync(t.data(), prof, sizeof(long long) * t.size(), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
         for (int b = 0; b < nu; ++b)
-            fprintf(stderr, "fd-eigen cta %d m=%lld sweeps=%lld cycles: build=%lld chol=%lld C=%lld jacobi=%lld end=%lld\n",
-                    b, t[8 * b + 6], t[8 * b + 5], t[8 * b], t[8 * b + 1], t[8 * b + 2], t[8 * b + 3], t[8 * b + 4]);
+            fprintf(stderr, "fd-eigen cta %d m=%lld sweeps=%lld cycles: build=%lld chol=%lld C=%lld jacobi=%lld upd=%lld rot=%lld\n",
+                    b, t[8 * b + 6], t[8 * b + 5], t[8 * b], t[8 * b + 1], t[8 * b + 2], t[8 * b + 3], t[8 * b + 4], t[8 * b + 7]);
         cudaFree(prof);
     }
     return cudaGetLastError();
