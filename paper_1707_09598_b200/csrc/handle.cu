@@ -206,7 +206,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
             int64_t rows_c = 1;
             bool fd_axes = true;
             for (int k = 0; k < d; ++k) { rows_c *= std::max(0, C.m[k]); fd_axes = fd_axes && C.m[k] <= FD_MMAX; }
-            if (d >= 2 && fd_axes && rows_c <= 2048) {
+            if (d >= 2 && fd_axes && rows_c <= 2048 && !(d == 2 && mmax > FD_FULL_MMAX2)) {
                 int mmin = 1 << 30;
                 for (int k = d - 1; k >= 0; --k)
                     if (C.m[k] < mmin) { mmin = C.m[k]; s = k; }
@@ -307,7 +307,8 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
                 C.small = 1;   // keeps the chunked Jacobi kernels away from it
                 h->fdg_comps.push_back(c);
                 for (int k = 0; k < d; ++k) used[C.tab[k]] = 1;
-            } else if (all_ok && was_small && fd_comp_smem(C, d) <= 200 * 1024) {   // one CTA, everything in smem
+            } else if (all_ok && was_small && fd_comp_smem(C, d) <= 200 * 1024 &&
+                       !(d == 2 && C.m[C.ax[d - 1]] > FD_FULL_MMAX2)) {   // one CTA, everything in smem
                 C.fd = 1;
                 h->fd_comps.push_back(c);
                 for (int k = 0; k < d; ++k) used[C.tab[k]] = 1;

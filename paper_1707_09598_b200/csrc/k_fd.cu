@@ -253,8 +253,15 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
     const int o1 = ms, s0 = ms, s1 = ma;
     const int n0 = s0 + (s0 & 1), n1 = s1 + (s1 & 1), np0 = n0 / 2, np1 = n1 / 2, npt = np0 + np1;
     const int nsteps = max(n0, n1) - 1;
-    const int nc0 = np0 * np0, nc1 = np1 * np1, ncs = nc0 + nc1;
+    // C stays exactly symmetric: only the blocks k <= l are computed, the
+    // (l, k) block is written as the transpose of (k, l)
+    const int nc0 = np0 * (np0 + 1) / 2, nc1 = np1 * (np1 + 1) / 2, ncs = nc0 + nc1;
     const int nitems = ncs + np0 * s0 + np1 * s1;
+    auto tri = [](int r, int n, int& k, int& l) {   // r-th (k, l), k <= l < n, row-major
+        k = 0;
+        while (r >= n - k) { r -= n - k; ++k; }
+        l = k + r;
+    };
     int nsweep = 0;
     long long acc_rot = 0, acc_upd = 0;   // probe (SGIGA_FD_PROFILE)
     // this thread's update items, decoded once: (pair k, pair l) blocks of C
@@ -264,8 +271,8 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
     for (int u = 0; u < EIG_ITEMS; ++u) {
         const int idx = tid + u * EIG_THREADS;
         dk_[u] = 0; dl_[u] = 0;
-        if (idx < nc0) { dk_[u] = idx / np0; dl_[u] = idx % np0; }
-        else if (idx < ncs) { const int r = idx - nc0; dk_[u] = np0 + r / np1; dl_[u] = np0 + r % np1; }
+        if (idx < nc0) tri(idx, np0, dk_[u], dl_[u]);
+        else if (idx < ncs) { tri(idx - nc0, np1, dk_[u], dl_[u]); dk_[u] += np0; dl_[u] += np0; }
         else if (idx < ncs + np0 * s0) { const int r = idx - ncs; dk_[u] = r / s0; dl_[u] = r % s0; }
         else if (idx < nitems) { const int r = idx - ncs - np0 * s0; dk_[u] = np0 + r / s1; dl_[u] = o1 + r % s1; }
     }
@@ -344,6 +351,12 @@ k_fd_eigen(const TabInfo* __restrict__ tabs, const int* __restrict__ uniq,
                     if (hl) Cm[pk * FD_LD + ql] = b;
                     if (hq) Cm[qk * FD_LD + pl] = c;
                     if (hq && hl) Cm[qk * FD_LD + ql] = d;
+                    if (k != l) {   // the transposed block (l, k)
+                        Cm[pl * FD_LD + pk] = a;
+                        if (hl) Cm[ql * FD_LD + pk] = b;
+                        if (hq) Cm[pl * FD_LD + qk] = c;
+                        if (hq && hl) Cm[ql * FD_LD + qk] = d;
+                    }
                 } else {               // V J_k, row i
                     const int k = dk_[u], i = dl_[u];
                     const double sk = rs[k];
@@ -747,12 +760,15 @@ k_fdl_bands(const CompInfo* __restrict__ comps, const int* __restrict__ list, co
 // one banded Cholesky per line, c_s K_s + mu_L M_s = F F^T with
 // mu_L = sum over the other axes of c_k lambda_k(line): one thread per line,
 // the last p factor rows in registers.  Stored per row i: [0] = 1 / F(i,i),
-// [k] = F(i, i-k), k = 1..p.  Grid (line blocks, component).
+// [k] = F(i, i-k), k = 1..p.  Grid (line blocks, component).  The
+// component's K_s / M_s bands are staged in shared memory first: the row
+// recurrence then waits on shared-memory, not L2, latency (cfg3: 106 us ->
+// the serial chain of its longest line).
 template <int D>
 __global__ void __launch_bounds__(64)
 k_fdl_factor(const CompInfo* __restrict__ comps, const int* __restrict__ list, int p,
              const int64_t* __restrict__ loff, const double* __restrict__ dL, const double* __restrict__ ckg,
-             const int64_t* __restrict__ fdl_off, double* __restrict__ fdl) {
+             const int64_t* __restrict__ fdl_off, double* __restrict__ fdl, int staged) {
     const int c = list[blockIdx.y];
     const CompInfo& C = comps[c];
     const int P1 = p + 1, s = C.ax[D - 1], ms = C.m[s];
@@ -760,6 +776,14 @@ k_fdl_factor(const CompInfo* __restrict__ comps, const int* __restrict__ list, i
 #pragma unroll
     for (int o = 0; o < D - 1; ++o) nlines *= C.m[C.ax[o]];
     const int L = blockIdx.x * 64 + threadIdx.x;
+    if (blockIdx.x * 64 >= nlines) return;
+    extern __shared__ double fband[];   // [K_s band | M_s band], ms * P1 each (when staged)
+    const double* Kb = fdl + fdl_off[c];
+    if (staged) {
+        for (int i = threadIdx.x; i < 2 * ms * P1; i += blockDim.x) fband[i] = Kb[i];
+        __syncthreads();
+        Kb = fband;
+    }
     if (L >= nlines) return;
     double muL = 0.0;
     {
@@ -772,8 +796,7 @@ k_fdl_factor(const CompInfo* __restrict__ comps, const int* __restrict__ list, i
         }
     }
     const double cs = ckg[c * MAXD + s];
-    const double* Kb = fdl + fdl_off[c];
-    const double* Mb = Kb + (int64_t)ms * P1;
+    const double* Mb = Kb + ms * P1;
     double* F = fdl + fdl_off[c] + 2 * (int64_t)ms * P1 + (int64_t)L * ms * P1;
     double Fw[PM][PM + 1], Rw[PM];   // Fw[d][k] = F(i-1-d, i-1-d-k)
 #pragma unroll
@@ -1179,11 +1202,20 @@ cudaError_t launch_fd_setup(Handle* h, cudaStream_t s) {
         maxlines = std::max(maxlines, lines);
     }
     const dim3 g3((unsigned)((maxlines + 63) / 64), (unsigned)nl);
+    int maxms = 1;
+    for (int c : h->fdl_comps) maxms = std::max(maxms, h->comps[c].m[h->comps[c].ax[h->d - 1]]);
+    // staged only while small: a large staging buffer would keep the 3-D
+    // assembly's CTAs (this kernel runs beside it on the side stream) off
+    // the SM for the factor's duration
+    const size_t fsm0 = sizeof(double) * 2 * (size_t)maxms * (h->p + 1);
+    const int staged = fsm0 <= 24 * 1024;
+    const size_t fsm = staged ? fsm0 : 0;
 #define LAUNCH_FACT(DD)                                                                                     \
     launch_hi(k_fdl_bands<DD>, dim3((unsigned)nl), dim3(256), 0, s, h->d_comps, h->d_fdl_list, h->d_tabs,   \
               h->d_tabvals, h->d_qw, h->p, h->mu, h->q, h->d_fdl_off, h->d_fdl);                          \
-    launch_hi(k_fdl_factor<DD>, g3, dim3(64), 0, s, h->d_comps, h->d_fdl_list, h->p, h->d_fd_loff, h->d_fdL, \
-              h->d_ck, h->d_fdl_off, h->d_fdl)
+    cudaFuncSetAttribute(k_fdl_factor<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);         \
+    launch_hi(k_fdl_factor<DD>, g3, dim3(64), fsm, s, h->d_comps, h->d_fdl_list, h->p, h->d_fd_loff, h->d_fdL, \
+              h->d_ck, h->d_fdl_off, h->d_fdl, staged)
     if (h->d == 1) { LAUNCH_FACT(1); }
     else if (h->d == 2) { LAUNCH_FACT(2); }
     else { LAUNCH_FACT(3); }

@@ -26,6 +26,10 @@ constexpr int PMAX = 5;   // p + 1 <= 5 (degree <= 4) on the device path
 constexpr int QMAX = 10;  // gauss_rule accepts q <= 10 (assembly.py:43)
 constexpr int WMAX = 2 * PMAX - 1;  // stencil slots per axis (2p+1)
 constexpr int GEO_PMAX = 8;         // geometry degree <= 7
+// 2-D components whose longest axis exceeds this run the line-FD PCG along
+// it (only the short axis is diagonalised), not the full FD: the largest
+// eigen-problems (m ~ 33..72, Jacobi, one SM) were the critical path of cfg1 / cfg3
+constexpr int FD_FULL_MMAX2 = 24;
 constexpr int FD_MMAX = 72;         // FD preconditioner: interior functions per diagonalised axis (smem eigen)
 constexpr int64_t FDG_MIN_ROWS = 65536;   // FD components at least this large: whole-GPU PCG (k_pcg_grid.cu)
 constexpr int FDG_MAX_CTAS = 1024;        // cooperative grid cap (partial-sum buffer size)
