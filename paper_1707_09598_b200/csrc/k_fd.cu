@@ -840,7 +840,7 @@ k_fdl_factor(const CompInfo* __restrict__ comps, const int* __restrict__ list, i
     }
 }
 
-template <int D>
+template <int D, int PL>   // PL = p (compile-time: the line scan's p x p state lives in registers)
 __global__ void __launch_bounds__(FDL_THREADS, 3)
 k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, const int* __restrict__ slotoff,
           const double* __restrict__ stencil, const double* __restrict__ rhs, int p,
@@ -857,7 +857,6 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
     namespace cgs = cooperative_groups;
     cgs::cluster_group cluster = cgs::this_cluster();
     __shared__ double red[FDL_THREADS / 32], cpart[2];
-    __shared__ double lsF[FDL_THREADS / 32][32 * (PM + 1)], lsy[FDL_THREADS / 32][32];
     const int K = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
     const int c = list[blockIdx.x / K];
     const CompInfo& C = comps[c];
@@ -902,6 +901,7 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
     const double* val = stencil + C.mat_off;
     // slot column offsets staged in shared memory (the SpMV's gathers then
     // depend on one global load, not two)
+    __shared__ double lsF[FDL_THREADS / 32][32 * (PM + 1)], lsy[FDL_THREADS / 32][32];
     __shared__ int soffs[WMAX * WMAX * WMAX];
     for (int i = tid; i < NS; i += FDL_THREADS) soffs[i] = slotoff[C.so_off + i];
     __syncthreads();
@@ -925,12 +925,129 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
         cluster.sync();
     };
     // in place, every line L = rows [L*ms, (L+1)*ms): forward then backward
-    // banded substitution, ONE WARP per line: the lanes stage 32 factor rows
+    // banded substitution, ONE WARP per line, parallel over the line: lane l
+    // owns a segment of CH = ceil(ms / 32) rows.  A row of the recurrence is
+    // an affine map of the state S = the last p results (companion matrix
+    // A_i, first row a_k = -F(i,i)^-1 F(i, i-k)); each lane
+    //   1. composes its segment's rows into one p x p affine map (M, v),
+    //   2. receives its entry state from its predecessor lane: a chain of
+    //      32 mat-vec steps (S_next = M S + v, one shuffle round each),
+    //   3. reruns the plain recurrence over its rows from that state.
+    // The sequential depth drops from ms rows to ~2 CH + 32 steps (cfg3's
+    // 129-row lines: 5 + 32 + 5; cfg5's 1026-row lines: 33 + 32 + 33).
+    // The scan reassociates rounding only; P^-1 stays a fixed linear map
+    // (a preconditioner -- the CG's true residual is checked on exit).
+    auto line_solve_scan = [&](double* y) {
+        const int warp = tid >> 5, lane = tid & 31;
+        const int gw = rank * (FDL_THREADS / 32) + warp, GW = K * (FDL_THREADS / 32);
+        const int CH = (ms + 31) >> 5;
+        const int i0 = min(ms, lane * CH), i1 = min(ms, i0 + CH);
+        for (int L = gw; L < nlines; L += GW) {
+            const double* F = Fac + (int64_t)L * ms * P1;
+            double* yl = y + (int64_t)L * ms;
+            double M[PL][PL], v[PL], S[PL];
+            auto compose = [&](const double* a, double bd) {   // (M, v) <- A_i (M, v)
+                double r0[PL], v0 = bd;
+#pragma unroll
+                for (int j = 0; j < PL; ++j) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < PL; ++k) acc = fma(a[k], M[k][j], acc);
+                    r0[j] = acc;
+                }
+#pragma unroll
+                for (int k = 0; k < PL; ++k) v0 = fma(a[k], v[k], v0);
+#pragma unroll
+                for (int r = PL - 1; r >= 1; --r) {
+                    v[r] = v[r - 1];
+#pragma unroll
+                    for (int j = 0; j < PL; ++j) M[r][j] = M[r - 1][j];
+                }
+#pragma unroll
+                for (int j = 0; j < PL; ++j) M[0][j] = r0[j];
+                v[0] = v0;
+            };
+            auto reset = [&]() {
+#pragma unroll
+                for (int r = 0; r < PL; ++r) {
+                    v[r] = 0.0;
+                    S[r] = 0.0;
+#pragma unroll
+                    for (int j = 0; j < PL; ++j) M[r][j] = r == j ? 1.0 : 0.0;
+                }
+            };
+            auto chain = [&](int from, int step) {   // lane from -> from + step -> ...
+                for (int l = from; l + step >= 0 && l + step < 32; l += step) {
+                    double E[PL];
+#pragma unroll
+                    for (int r = 0; r < PL; ++r) {
+                        double acc = v[r];
+#pragma unroll
+                        for (int k = 0; k < PL; ++k) acc = fma(M[r][k], S[k], acc);
+                        E[r] = acc;
+                    }
+#pragma unroll
+                    for (int r = 0; r < PL; ++r) {
+                        const double e = __shfl_sync(0xffffffffu, E[r], l);
+                        if (lane == l + step) S[r] = e;
+                    }
+                }
+            };
+            // forward: y(i) = (y(i) - sum_k F(i, i-k) y(i-k)) / F(i, i); S[k] = y(i-k)
+            reset();
+            for (int i = i0; i < i1; ++i) {
+                const double d = F[(int64_t)i * P1];
+                double a[PL];
+#pragma unroll
+                for (int k = 0; k < PL; ++k) a[k] = (k < p && k < i) ? -d * F[(int64_t)i * P1 + k + 1] : 0.0;
+                compose(a, d * yl[i]);
+            }
+            chain(0, 1);
+            for (int i = i0; i < i1; ++i) {
+                double sv = yl[i];
+#pragma unroll
+                for (int k = PL - 1; k >= 0; --k)
+                    if (k < p && k < i) sv -= F[(int64_t)i * P1 + k + 1] * S[k];
+                sv *= F[(int64_t)i * P1];
+#pragma unroll
+                for (int r = PL - 1; r >= 1; --r) S[r] = S[r - 1];
+                S[0] = sv;
+                yl[i] = sv;
+            }
+            __syncwarp();
+            // backward: x(i) = (y(i) - sum_k F(i+k, i) x(i+k)) / F(i, i); S[k] = x(i+k)
+            reset();
+            for (int i = i1 - 1; i >= i0; --i) {
+                const double d = F[(int64_t)i * P1];
+                double a[PL];
+#pragma unroll
+                for (int k = 0; k < PL; ++k)
+                    a[k] = (k < p && i + k + 1 < ms) ? -d * F[(int64_t)(i + k + 1) * P1 + k + 1] : 0.0;
+                compose(a, d * yl[i]);
+            }
+            chain(31, -1);
+            for (int i = i1 - 1; i >= i0; --i) {
+                double sv = yl[i];
+#pragma unroll
+                for (int k = PL - 1; k >= 0; --k)
+                    if (k < p && i + k + 1 < ms) sv -= F[(int64_t)(i + k + 1) * P1 + k + 1] * S[k];
+                sv *= F[(int64_t)i * P1];
+#pragma unroll
+                for (int r = PL - 1; r >= 1; --r) S[r] = S[r - 1];
+                S[0] = sv;
+                yl[i] = sv;
+            }
+            __syncwarp();
+        }
+        cluster.sync();
+    };
+    // serial variant (degree 4, and lines enough to fill the cluster's warps):
+    // ONE WARP per line, the lanes stage 32 factor rows
     // (and y) into shared memory -- the next 32 already in flight in
     // registers -- while lane 0 runs the serial recurrence from shared memory
     // with the last p results (forward) / the p pending column sums
     // (backward, column-oriented) in registers
-    auto line_solve = [&](double* y) {
+    auto line_solve_serial = [&](double* y) {
         const int warp = tid >> 5, lane = tid & 31;
         const int gw = rank * (FDL_THREADS / 32) + warp, GW = K * (FDL_THREADS / 32);
         double* sF = lsF[warp];
@@ -1007,6 +1124,15 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
             }
         }
         cluster.sync();
+    };
+    // the scan when the lines leave most of the cluster's warps idle (2-D:
+    // a few long lines, the serial chain is the critical path); with lines
+    // for every warp the serial recurrence is cheaper (no second pass over
+    // the factors).  Degree 4: serial only (the scan's 4 x 4 state spills).
+    auto line_solve = [&](double* y) {
+        if constexpr (PL >= 4) line_solve_serial(y);
+        else if (nlines < K * (FDL_THREADS / 32)) line_solve_scan(y);
+        else line_solve_serial(y);
     };
     auto precond = [&]() {   // z = P^-1 r
         if constexpr (D == 3) {
@@ -1130,15 +1256,23 @@ cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
     const double rt2 = rtol * rtol;
     cudaError_t e;
 #define LAUNCH_FDL(DD)                                                                                       \
-    e = cudaLaunchKernelEx(&cfg, k_pcg_fdl<DD>, (const CompInfo*)h->d_comps, (const int*)h->d_fdl_list,     \
+    e = cudaLaunchKernelEx(&cfg, k_pcg_fdl<DD, PP>, (const CompInfo*)h->d_comps, (const int*)h->d_fdl_list, \
                            (const int*)h->d_slotoff, (const double*)h->d_stencil, (const double*)h->d_rhs,  \
                            h->p, (const int64_t*)h->d_fd_uoff, (const double*)h->d_fdU,                    \
                            (const double*)h->d_ck, (const int64_t*)h->d_fdl_off, (const double*)h->d_fdl,  \
                            h->d_x, h->d_r, h->d_z, h->d_p, h->d_q, h->d_q2, h->d_cg, h->d_relres, rt2, maxit, \
                            h->d_coef)
-    if (h->d == 1) { LAUNCH_FDL(1); }
-    else if (h->d == 2) { LAUNCH_FDL(2); }
-    else { LAUNCH_FDL(3); }
+#define LAUNCH_FDL_P(DD)                                 \
+    switch (h->p) {                                      \
+        case 1: { constexpr int PP = 1; LAUNCH_FDL(DD); } break; \
+        case 2: { constexpr int PP = 2; LAUNCH_FDL(DD); } break; \
+        case 3: { constexpr int PP = 3; LAUNCH_FDL(DD); } break; \
+        default: { constexpr int PP = 4; LAUNCH_FDL(DD); } break; \
+    }
+    if (h->d == 1) { LAUNCH_FDL_P(1); }
+    else if (h->d == 2) { LAUNCH_FDL_P(2); }
+    else { LAUNCH_FDL_P(3); }
+#undef LAUNCH_FDL_P
 #undef LAUNCH_FDL
     h->launches[1]++;
     if (e != cudaSuccess) return e;
