@@ -34,6 +34,7 @@ Options Options::from_env() {
     o.combine_nosort = env_on("SGIGA_COMBINE_NOSORT");
     o.combine_perthread = env_on("SGIGA_COMBINE_PERTHREAD");
     o.asm_profile = env_on("SGIGA_ASM_PROFILE");
+    o.asm_pencil = env_on("SGIGA_ASM_PENCIL");
     o.fd_profile = env_on("SGIGA_FD_PROFILE");
     o.pcg_profile = env_on("SGIGA_PCG_PROFILE");
     o.pcg_trace = env_on("SGIGA_PCG_TRACE");
@@ -65,7 +66,8 @@ static void free_all(Handle* h) {
                     h->d_active_count, h->d_relres, h->d_slotoff, h->d_alist, h->d_cperm, h->d_chist,
                     h->d_fdlist, h->d_fd_uniq, h->d_fd_uoff, h->d_fd_loff, h->d_fdU, h->d_fdL, h->d_tmaps,
                     h->d_fdl_list, h->d_fdl_off, h->d_fdl, h->d_ck, h->d_ticket, h->d_mcomp,
-                    h->d_spts, h->d_sout, h->d_blocks2, h->d_fdg_list, h->d_fdg_part, h->d_fdg_ckpart};
+                    h->d_spts, h->d_sout, h->d_blocks2, h->d_fdg_list, h->d_fdg_part, h->d_fdg_ckpart,
+                    h->d_tiles3, h->d_tmaps3};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel, h->h_sticky};
@@ -202,7 +204,9 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
         // kernel (every axis <= FD_MMAX functions, <= 2048 rows) stream along
         // their SHORTEST axis instead -- many short pencils rather than a few
         // long ones (the cfg2 makespan was one long pencil), fewer halo planes
-        {
+        // (the tiled 3-D assembly keeps the longest axis: its tiles cover the
+        // thin cross-section, so a long stream axis is what it wants)
+        if (!tile3_eligible(h)) {
             int64_t rows_c = 1;
             bool fd_axes = true;
             for (int k = 0; k < d; ++k) { rows_c *= std::max(0, C.m[k]); fd_axes = fd_axes && C.m[k] <= FD_MMAX; }
@@ -215,6 +219,9 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
         int j = 0;
         for (int k = 0; k < d; ++k) if (k != s) C.ax[j++] = k;
         C.ax[d - 1] = s;
+        // 3-D: the thinner cross-section axis is a = ax[1] (innermost in the
+        // metric storage; the tiled assembly covers it with one union window)
+        if (d == 3 && C.m[C.ax[1]] > C.m[C.ax[0]]) std::swap(C.ax[0], C.ax[1]);
         C.rows = 1; C.nslots = 1; C.ndofs = 1; C.nqp = 1;
         for (int k = 0; k < d; ++k) {
             C.rows *= C.m[k]; C.nslots *= C.S[k]; C.ndofs *= C.n[k];
@@ -495,6 +502,7 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
 static int upload_all(Handle* h) {
     cudaStream_t s = h->stream;
     h->tmaps_state = 0;   // tensor maps follow the component table
+    h->tiles3_state = 0;
     if (!h->mcomp.empty())
         SG_CUDA(cudaMemcpyAsync(h->d_mcomp, h->mcomp.data(), sizeof(int) * h->mcomp.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_comps, h->comps.data(), sizeof(CompInfo) * h->comps.size(), cudaMemcpyHostToDevice, s));

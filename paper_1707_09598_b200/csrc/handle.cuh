@@ -42,6 +42,7 @@ struct Options {
     bool combine_nosort = false;    // SGIGA_COMBINE_NOSORT=1: no cell sort of the points (tests)
     bool combine_perthread = false; // SGIGA_COMBINE_PERTHREAD=1: per-thread combine kernel (tests)
     bool asm_profile = false;       // SGIGA_ASM_PROFILE=1: block-0 stage cycles to stderr (probe)
+    bool asm_pencil = false;        // SGIGA_ASM_PENCIL=1: one-pencil-per-CTA 3-D assembly (parity tests)
     bool fd_profile = false;        // SGIGA_FD_PROFILE=1: FD phase cycles to stderr (probe)
     bool pcg_profile = false;       // SGIGA_PCG_PROFILE=1 (probe)
     bool pcg_trace = false;         // SGIGA_PCG_TRACE=1 (probe)
@@ -192,6 +193,13 @@ struct Handle {
     int asm_seg = 0;                       // stream-axis segment length of the pencils
     void* d_tmaps = nullptr;               // per-component CUtensorMap of d_G (TMA plane copies)
     int tmaps_state = 0;                   // 0 = not built, 1 = ready, -1 = unavailable
+    // tiled 3-D assembly (k_assembly_tile.cu): tiles, per-component tensor
+    // maps with the tile's window box, dynamic shared memory of the launch
+    std::vector<Tile3> tiles3;
+    Tile3* d_tiles3 = nullptr;
+    void* d_tmaps3 = nullptr;
+    int tiles3_state = 0;                  // 0 = not built, 1 = ready, -1 = not applicable
+    size_t tiles3_smem = 0;
     bool small_checked = false;            // small comps' true residual came from the cluster PCG
 
     // whole-run CUDA graph (sgiga_run): captured on the second call with the
@@ -238,6 +246,10 @@ struct Handle {
     int ncg() const { return d * (d + 1) / 2; }   // symmetric metric entries
     int nG() const { return ncg() + 1; }           // + load
 };
+
+// the tiled 3-D assembly (k_assembly_tile.cu) serves this plan (static
+// properties only: d = 3, maximal regularity, q = p + 1, degree 3 or 4)
+bool tile3_eligible(const Handle* h);
 
 // symmetric index of (m, n) in the packed metric (row-major upper triangle)
 __host__ __device__ inline int sym_index(int d, int m, int n) {

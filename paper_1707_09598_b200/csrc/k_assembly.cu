@@ -300,12 +300,15 @@ size_t assembly_smem_bytes(const Handle* h) {
 
 bool launch_assembly_fast(Handle* h, cudaError_t* err);
 bool launch_assembly_2d(Handle* h, cudaError_t* err);
+bool launch_assembly_tile(Handle* h, cudaError_t* err);
 
 cudaError_t launch_assembly(Handle* h) {
     int np = (int)h->pencils.size();
     if (np == 0) return cudaSuccess;
     cudaError_t fe = cudaSuccess;
     if (!h->force_generic_assembly && launch_assembly_2d(h, &fe))     // 2-D blocks, q = p+1
+        return fe == cudaSuccess ? cudaGetLastError() : fe;
+    if (!h->force_generic_assembly && launch_assembly_tile(h, &fe))   // 3-D tiles, q = p+1, p = 3, 4
         return fe == cudaSuccess ? cudaGetLastError() : fe;
     if (!h->force_generic_assembly && launch_assembly_fast(h, &fe))   // maximal regularity, q = p+1
         return fe == cudaSuccess ? cudaGetLastError() : fe;

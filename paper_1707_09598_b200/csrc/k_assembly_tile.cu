@@ -1,0 +1,801 @@
+// k_assembly_tile.cu -- kernel 2 for 3-D components (maximal regularity,
+// q = p + 1, degree 3 or 4): tiled cross-sections, warp-specialised.
+//
+// Reference: the element loop of _assemble_full / local_poisson_systems
+// (S/assembly.py:264-354, S/_kernels/_compiled.pyx:48-90) restated as a
+// global sum factorisation into the implicit-column stencil (derivation in
+// k_assembly.cu).  Where k_assembly_fast.cu gives every cross-section row
+// (i_a, i_b) its own CTA, a CTA here owns a TILE of rows -- na rows along
+// a = ax[1] times nb rows along b = ax[0] -- and a segment of the stream
+// axis s = ax[2]:
+//   * one TMA tensor copy per quadrature plane brings the UNION window of
+//     the tile's rows, so a thin axis (2 or 4 elements: most of a sparse
+//     grid's components) is read once per plane instead of once per row, and
+//     stage 1 -- which does not depend on i_a -- is computed once for all
+//     na rows;
+//   * warps 0..11 (G12), plane j:  stage 1 (contract b) -> S1[ib][pair slot][xa][w_b],
+//     named barrier, stage 2 (contract a) -> S2[row][unit][c_a][c_b] (pairs summed
+//     per unit of the stream-direction type stage 3 needs, storage columns);
+//   * warps 12..15 (G3), plane j-1 in the same barrier interval: stage 3 --
+//     one work item per (row, storage column (c_a, c_b)); the P alive stream
+//     rows of an item (a ring of 35 doubles for p = 4) live in TENSOR MEMORY
+//     (tcgen05.ld / .st, each G3 warp in its own TMEM lane quadrant, up to
+//     7 rings per thread), so the ring costs no registers between planes and
+//     the tile size is not capped by the register file; completed stream rows
+//     go straight to the stencil.
+// One CTA barrier per plane.  Deterministic, no atomics, each stencil entry
+// written once; a row's value does not depend on the tiling.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "handle.cuh"
+
+namespace sgiga {
+
+namespace {
+
+__device__ __forceinline__ uint32_t t3_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// 8 TMEM columns <-> 8 registers of this thread's lane (32x32b shape)
+__device__ __forceinline__ void tm_ld8(uint32_t a, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(a));
+}
+__device__ __forceinline__ void tm_st8(uint32_t a, const uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n"
+                 ::"r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+// one double (two TMEM columns) of this thread's lane
+__device__ __forceinline__ double tm_ld2_issue(uint32_t a, uint32_t& lo, uint32_t& hi) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(a));
+    return 0.0;
+}
+__device__ __forceinline__ void tm_st2(uint32_t a, double v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n"
+                 ::"r"(a), "r"((uint32_t)__double2loint(v)), "r"((uint32_t)__double2hiint(v)) : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+template <int P>
+struct TCfg {
+    static constexpr int p = P - 1, Q = P, W = 2 * P - 1;
+    static constexpr int RP = (P + 1) & ~1;     // pair-table row (16-byte pair loads)
+    static constexpr int PQ = P * Q;            // window points of one row
+    static constexpr int S1W = (W + 1) & ~1;    // S1 row (w_b pairs by 16-byte loads)
+    static constexpr int NC2 = (W + 1) / 2;     // stage-2 column pairs
+    static constexpr int NG = 7;                // 6 metric entries + load
+    static constexpr int NU = 5;                // stage-2 units
+    static constexpr int SC = tile3_slot_cols(P);     // TMEM columns per ring
+    static constexpr int RC = 2 * W;                  // TMEM columns per physical stream row
+    static constexpr int NSLOT = tile3_nslot(P);
+};
+
+// per-CTA shared-memory layout (doubles)
+struct TLay {
+    int sGw, oTa, oTb, oPhiA, oPhiB, oS1, s1slot, oSL1, oS2, s2sz, oRL, total;
+};
+
+__host__ __device__ inline TLay tile3_layout(int P, int na, int nb, int xa, int xap, int xb, int n3) {
+    const int Q = P, W = 2 * P - 1, RP = (P + 1) & ~1, PQ = P * Q, S1W = (W + 1) & ~1;
+    const int rows = na * nb;
+    TLay L;
+    L.sGw = (7 * xb * xap + 15) & ~15;
+    L.oTa = 2 * L.sGw;
+    L.oTb = L.oTa + na * 4 * PQ * RP;
+    L.oPhiA = L.oTb + nb * 4 * PQ * RP;
+    L.oPhiB = L.oPhiA + na * PQ;
+    L.oS1 = (L.oPhiB + nb * PQ + 1) & ~1;
+    L.s1slot = xa * S1W + 2;
+    L.oSL1 = L.oS1 + nb * 8 * L.s1slot;
+    L.oS2 = L.oSL1 + nb * xa;
+    L.s2sz = 5 * n3 + rows;                      // [row][unit][c_a][c_b] + load [row]
+    L.oRL = L.oS2 + 2 * L.s2sz;
+    L.total = L.oRL + rows * P;
+    return L;
+}
+
+// stage-1 pair slots: aa, as(=sa), ss, ab, sb, ba, bs, bb -- b-type of each
+// (2 (m == b) + (n == b): derivative of the row / column function along b)
+__device__ __constant__ int c_t3_btype[8] = {0, 0, 0, 1, 1, 2, 2, 3};
+// stage-2 units (pairs summed per stream type; type 0 split in two):
+//   u0 {aa, ab}, u1 {ba, bb}, u2 {as, bs} (type 1), u3 {sa, sb} (type 2), u4 {ss}
+// (S1 slot, a-type) of the two pairs of each unit (u4: one pair)
+__device__ __constant__ int c_t3_uslot[5][2] = {{0, 3}, {5, 7}, {1, 6}, {1, 4}, {2, 2}};
+__device__ __constant__ int c_t3_uat[5][2] = {{3, 2}, {1, 0}, {2, 0}, {1, 0}, {0, 0}};
+
+template <int P>
+__global__ void __launch_bounds__(TILE3_THREADS, 1)
+k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tabs,
+                const Tile3* __restrict__ tiles, const double* __restrict__ vals,
+                double* __restrict__ stencil, double* __restrict__ rhs, double* __restrict__ dinv,
+                const CUtensorMap* __restrict__ tmaps, long long* __restrict__ prof) {
+    using F = TCfg<P>;
+    constexpr int p = F::p, Q = F::Q, W = F::W, RP = F::RP, PQ = F::PQ, S1W = F::S1W;
+    constexpr int NC2 = F::NC2, G12 = TILE3_G12, NT = TILE3_THREADS;
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int s_ent[8];
+    __shared__ uint32_t s_tmem;
+    // the tile, its component and tables staged in shared memory: values the
+    // compiler rematerialises under register pressure reload from there
+    __shared__ Tile3 sT;
+    __shared__ CompInfo sC;
+    __shared__ TabInfo sTab[3];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0) sT = tiles[blockIdx.x];
+    __syncthreads();
+    if (tid == 0) sC = comps[sT.comp];
+    __syncthreads();
+    if (tid < 3) sTab[tid] = tabs[sC.tab[sC.ax[tid == 0 ? 1 : (tid == 1 ? 0 : 2)]]];
+    __syncthreads();
+    const Tile3& T = sT;
+    const CompInfo& C = sC;
+    const int ka = C.ax[1], kb = C.ax[0], ks = C.ax[2];
+    const TabInfo& TA = sTab[0];
+    const TabInfo& TB = sTab[1];
+    const TabInfo& TS = sTab[2];
+    const int nel_a = TA.nel, nel_b = TB.nel, nel_s = TS.nel;
+    const int na = T.na, nb = T.nb, rows = na * nb;
+    const int EA0 = max(0, T.a0 - p), EB0 = max(0, T.b0 - p);
+    const int EA1 = min(nel_a - 1, T.a0 + na - 1);
+    const int XAv = (EA1 - EA0 + 1) * Q;                   // valid union extent along a
+    const int r0 = T.r0, r1 = T.r1;
+    const int e_first = max(0, r0 - p), e_last = min(r1 - 1, nel_s - 1);
+    const int nE = e_last - e_first + 1;
+    const int nplanes = nE > 0 ? nE * Q : 0;
+    if (nplanes == 0) return;   // uniform over the CTA
+    const int Sa = C.S[ka], Sb = C.S[kb], SAB = Sa * Sb;
+    const int n3 = rows * SAB;
+    const TLay L = tile3_layout(P, na, nb, T.xa, T.xap, T.xb, n3);
+    const int xap = T.xap, xb = T.xb;
+    double* Ta = sm + L.oTa;
+    double* Tb = sm + L.oTb;
+    double* phiA = sm + L.oPhiA;
+    double* phiB = sm + L.oPhiB;
+    double* S1 = sm + L.oS1;
+    double* SL1 = sm + L.oSL1;
+    double* S2 = sm + L.oS2;
+    double* RLs = sm + L.oRL;
+    // odd Q: the box's inner start must be 16-byte aligned -- an odd window
+    // start is rounded down one point and the plane is read shifted by tsh
+    const int tsh = (Q & 1) ? ((EA0 * Q) & 1) : 0;
+    const int tx0 = EA0 * Q - tsh, tx1 = EB0 * Q;
+    const CUtensorMap* tmap = tmaps + T.comp;
+    const uint32_t pbytes = (uint32_t)(F::NG * xb * xap * 8);
+
+    auto issue_plane = [&](int j) {   // one thread: plane j -> buffer j & 1
+        const int b = j & 1;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(t3_smem_u32(&bar[b])),
+                     "r"(pbytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+            ::"r"(t3_smem_u32(sm + b * L.sGw)), "l"(tmap), "r"(tx0), "r"(tx1), "r"(e_first * Q + j), "r"(0),
+              "r"(t3_smem_u32(&bar[b]))
+            : "memory");
+    };
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        issue_plane(0);
+        if (nplanes > 1) issue_plane(1);
+    }
+    if (tid < 8) {   // metric entry of each stage-1 pair slot: aa as ss ab sb ba bs bb
+        const int mm = tid == 2 || tid == 4 ? ks : (tid >= 5 ? kb : ka);
+        const int nn = tid == 0 || tid == 5 ? ka : (tid == 3 || tid == 4 || tid == 7 ? kb : ks);
+        s_ent[tid] = sym_index(3, mm, nn);
+    }
+    if (warp == G12 / 32) {   // first G3 warp: the whole tensor memory (one CTA per SM)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
+                     ::"r"(t3_smem_u32(&s_tmem)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+
+    // ---- 1-D pair tables of the tile rows (relative window coordinates):
+    // T[row][type][x = t Q + g][k] = (row fn p-t)^(type>>1)' (e, g) * (fn k)^(type&1)' (e, g),
+    // e = i - p + t; phi[row][x] = row function value (load) -------------
+    auto build_T = [&](const TabInfo& TT, int i0, int nr, double* Tt, double* phi) {
+        const int64_t nq = (int64_t)TT.nel * Q;
+        for (int idx = tid; idx < nr * 4 * PQ * RP; idx += NT) {
+            const int kk = idx % RP, x = (idx / RP) % PQ, type = (idx / (RP * PQ)) % 4, r = idx / (RP * PQ * 4);
+            const int t = x / Q, g = x % Q, e = i0 + r - p + t;
+            double v = 0.0;
+            if (kk < P && e >= 0 && e < TT.nel) {
+                const double* base = vals + TT.val_off + ((int64_t)e * Q + g) * P;
+                const double a = (type >> 1) ? base[nq * P + (p - t)] : base[p - t];
+                const double b = (type & 1) ? base[nq * P + kk] : base[kk];
+                v = a * b;
+            }
+            Tt[idx] = v;
+        }
+        for (int idx = tid; idx < nr * PQ; idx += NT) {
+            const int x = idx % PQ, r = idx / PQ, t = x / Q, g = x % Q, e = i0 + r - p + t;
+            phi[idx] = (e >= 0 && e < TT.nel) ? vals[TT.val_off + ((int64_t)e * Q + g) * P + (p - t)] : 0.0;
+        }
+    };
+    build_T(TA, T.a0, na, Ta, phiA);
+    build_T(TB, T.b0, nb, Tb, phiB);
+    for (int idx = tid; idx < rows * P; idx += NT) RLs[idx] = 0.0;
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+
+    // ---- stage 3 (G3): rings in tensor memory --------------------------------
+    const bool inG3 = tid >= G12;
+    const int g3t = tid - G12;   // 0..127: TMEM lane 32 (warp % 4) + lane
+    const uint32_t tbase = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    const int n3r = n3 + rows;   // + one load-ring item per row (shared memory)
+    const int nslot = (n3r + TILE3_G3 - 1) / TILE3_G3;   // <= NSLOT (host-checked)
+    const int64_t rs_s = C.rs[ks], ss_s = C.ss[ks], rows_c = C.rows;
+    const int absm_s = C.absm[ks], m_s = C.m[ks], S_s = C.S[ks];
+    const int64_t nq_s = (int64_t)nel_s * Q;
+    if (inG3) {   // rings start at zero
+        for (int k = 0; k < nslot; ++k)
+#pragma unroll
+            for (int c = 0; c < F::SC; c += 2) tm_st2(tbase + k * F::SC + c, 0.0);
+        tm_wait_st();
+    }
+
+    const bool prf = prof != nullptr && blockIdx.x == 0;
+    long long gt0 = 0;
+    if (prof != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+    long long pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0;
+    const int n1 = nb * 9 * XAv;
+    // stage-2 work items (row, unit, column group): an absolute b axis (thin:
+    // m_b <= 2p+1) enumerates its storage columns c_b only (w_b = c_b + 1 - i_b + p),
+    // a relative one its 2p+1 offsets, one or two per item
+    const int cw = T.cw;
+    const int absm_b = C.absm[kb];
+    const int ncol2 = absm_b ? Sb : (cw == 2 ? NC2 : W);
+    const int n2 = rows * F::NU * ncol2;
+    for (int j = 0; j <= nplanes; ++j) {
+        const long long c0 = prf ? clock64() : 0;
+        if (!inG3) {
+            if (j < nplanes) {
+                // ---- wait for plane j ----------------------------------------
+                {
+                    const uint32_t par = (uint32_t)((j >> 1) & 1);
+                    const uint32_t ba = t3_smem_u32(&bar[j & 1]);
+                    uint32_t ok = 0;
+                    while (!ok)
+                        asm volatile("{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+                                     " selp.u32 %0, 1, 0, q;\n}\n" : "=r"(ok) : "r"(ba), "r"(par) : "memory");
+                }
+                const double* Gw = sm + (j & 1) * L.sGw + tsh;
+                // ---- stage 1: contract b -> S1[ib][slot][xa][w_b], SL1[ib][xa] --
+                for (int it = tid; it < n1; it += G12) {
+                    const int xa = it % XAv, q = it / XAv, sig = q % 9, rb = q / 9;
+                    const int ib = T.b0 + rb;
+                    const int tlo = max(0, p - ib), thi = min(P, nel_b + p - ib);
+                    const int xoff = (ib - p - EB0) * Q;   // union row of the row's window point x = 0
+                    if (sig < 8) {
+                        const double* gp = Gw + (s_ent[sig] * xb + xoff) * xap + xa;
+                        const double* tr = Tb + (rb * 4 + c_t3_btype[sig]) * PQ * RP;
+                        double acc[W];
+#pragma unroll
+                        for (int w = 0; w < W; ++w) acc[w] = 0.0;
+#pragma unroll
+                        for (int t = 0; t < P; ++t) {
+                            if (t < tlo || t >= thi) continue;
+#pragma unroll
+                            for (int g = 0; g < Q; ++g) {
+                                const int x = t * Q + g;
+                                const double gv = gp[x * xap];
+                                double tv[RP];
+#pragma unroll
+                                for (int k2 = 0; k2 < RP / 2; ++k2) {
+                                    const double2 v2 = *reinterpret_cast<const double2*>(tr + x * RP + 2 * k2);
+                                    tv[2 * k2] = v2.x;
+                                    tv[2 * k2 + 1] = v2.y;
+                                }
+#pragma unroll
+                                for (int k = 0; k < P; ++k) acc[t + k] = fma(gv, tv[k], acc[t + k]);
+                            }
+                        }
+                        double* o = S1 + (rb * 8 + sig) * L.s1slot + xa * S1W;
+#pragma unroll
+                        for (int w = 0; w < W; w += 2)
+                            *reinterpret_cast<double2*>(o + w) = make_double2(acc[w], w + 1 < W ? acc[w + 1] : 0.0);
+                    } else {
+                        const double* gp = Gw + (6 * xb + xoff) * xap + xa;
+                        const double* ph = phiB + rb * PQ;
+                        double acc = 0.0;
+#pragma unroll
+                        for (int t = 0; t < P; ++t) {
+                            if (t < tlo || t >= thi) continue;
+#pragma unroll
+                            for (int g = 0; g < Q; ++g) acc = fma(gp[(t * Q + g) * xap], ph[t * Q + g], acc);
+                        }
+                        SL1[rb * T.xa + xa] = acc;
+                    }
+                }
+                asm volatile("bar.sync 1, %0;\n" ::"r"(G12) : "memory");
+                if (tid == 0 && j + 2 < nplanes) issue_plane(j + 2);   // buffer j & 1 is free now
+                // ---- stage 2: contract a -> S2[row][unit][c_a][c_b], S2L[row] -----
+                double* S2w = S2 + (j & 1) * L.s2sz;
+                auto stage2 = [&](auto CWc) {
+                    constexpr int CW = decltype(CWc)::value;
+                    for (int it = tid; it < n2 + rows; it += G12) {
+                        if (it < n2) {
+                            const int cg = it % ncol2, u = (it / ncol2) % F::NU, r = it / (ncol2 * F::NU);
+                            const int ra = r % na, rb = r / na, ia = T.a0 + ra, ib = T.b0 + rb;
+                            const int wb0 = absm_b ? cg + 1 - ib + p : CW * cg;   // first w_b of the item
+                            if (wb0 < 0 || wb0 >= W) continue;   // column outside the band: dead stage-3 items
+                            const int tlo = max(0, p - ia), thi = min(P, nel_a + p - ia);
+                            const int xoff = (ia - p - EA0) * Q;
+                            double acc0[W], acc1[W];
+#pragma unroll
+                            for (int w = 0; w < W; ++w) acc0[w] = acc1[w] = 0.0;
+#pragma unroll
+                            for (int pr = 0; pr < 2; ++pr) {
+                                if (pr == 1 && u == 4) break;
+                                const double* sp = S1 + (rb * 8 + c_t3_uslot[u][pr]) * L.s1slot + xoff * S1W + wb0;
+                                const double* ta = Ta + (ra * 4 + c_t3_uat[u][pr]) * PQ * RP;
+#pragma unroll
+                                for (int t = 0; t < P; ++t) {
+                                    if (t < tlo || t >= thi) continue;
+#pragma unroll
+                                    for (int g = 0; g < Q; ++g) {
+                                        const int x = t * Q + g;
+                                        double2 v;
+                                        if constexpr (CW == 2) v = *reinterpret_cast<const double2*>(sp + x * S1W);
+                                        else v.x = sp[x * S1W];
+                                        double tv[RP];
+#pragma unroll
+                                        for (int k2 = 0; k2 < RP / 2; ++k2) {
+                                            const double2 v2 = *reinterpret_cast<const double2*>(ta + x * RP + 2 * k2);
+                                            tv[2 * k2] = v2.x;
+                                            tv[2 * k2 + 1] = v2.y;
+                                        }
+#pragma unroll
+                                        for (int k = 0; k < P; ++k) {
+                                            acc0[t + k] = fma(v.x, tv[k], acc0[t + k]);
+                                            if constexpr (CW == 2) acc1[t + k] = fma(v.y, tv[k], acc1[t + k]);
+                                        }
+                                    }
+                                }
+                            }
+                            // relative (w_a, w_b) -> storage columns (c_a, c_b)
+                            double* o = S2w + (r * F::NU + u) * SAB;
+#pragma unroll
+                            for (int cc = 0; cc < CW; ++cc) {
+                                const int wb = wb0 + cc;
+                                const int cb = absm_b ? wb - p + ib - 1 : wb;
+                                if (wb >= W || cb < 0 || cb >= Sb) continue;
+#pragma unroll
+                                for (int wa = 0; wa < W; ++wa) {
+                                    const int ca = C.absm[ka] ? wa - p + ia - 1 : wa;
+                                    if (ca >= 0 && ca < Sa) o[ca * Sb + cb] = cc == 0 ? acc0[wa] : acc1[wa];
+                                }
+                            }
+                        } else {
+                            const int r = it - n2, ra = r % na, rb = r / na, ia = T.a0 + ra;
+                            const int tlo = max(0, p - ia), thi = min(P, nel_a + p - ia);
+                            const double* sl = SL1 + rb * T.xa + (ia - p - EA0) * Q;
+                            const double* ph = phiA + ra * PQ;
+                            double acc = 0.0;
+#pragma unroll
+                            for (int t = 0; t < P; ++t) {
+                                if (t < tlo || t >= thi) continue;
+#pragma unroll
+                                for (int g = 0; g < Q; ++g) acc = fma(sl[t * Q + g], ph[t * Q + g], acc);
+                            }
+                            S2w[5 * n3 + r] = acc;
+                        }
+                    }
+                };
+                if (cw == 2) stage2(std::integral_constant<int, 2>{});
+                else stage2(std::integral_constant<int, 1>{});
+            }
+        } else if (j >= 1) {
+            // ---- stage 3 (plane jj = j - 1): stream axis, rank-1 updates ---------
+            const int jj = j - 1, el = jj / Q, g = jj - el * Q, e = e_first + el;
+            const double* S2r = S2 + (jj & 1) * L.s2sz;
+            double vb[P], db[P];
+            {
+                const double* bp = vals + TS.val_off + ((int64_t)e * Q + g) * P;
+#pragma unroll
+                for (int k = 0; k < P; ++k) {
+                    vb[k] = __ldg(bp + k);
+                    db[k] = __ldg(bp + nq_s * P + k);
+                }
+            }
+            const bool last_pt = g == Q - 1;
+            const int nfl = e < e_last ? 1 : P;   // the last element completes rows e .. e + p
+            const int emod = e % P;
+            for (int k = 0; k < nslot; ++k) {
+                const int i = g3t + TILE3_G3 * k;
+                const uint32_t ta = tbase + k * F::SC;
+                const uint32_t t3 = ta + tile3_ring_cols(P);   // element partial R3[al][bl]
+                // R3 accumulates this element's Q planes; at the element's last
+                // plane it is added to the ring window it touches -- stream row
+                // e + al (physical row (e + al) mod P), offsets w = p - al .. 2p - al
+                // (two-level sum: element partials, then elements, as the
+                // reference's element-by-element assembly)
+                uint32_t lo[P][P], hi[P][P], wlo[P][P], whi[P][P];
+#pragma unroll
+                for (int al = 0; al < P; ++al)
+#pragma unroll
+                    for (int bl = 0; bl < P; ++bl) tm_ld2_issue(t3 + 2 * (al * P + bl), lo[al][bl], hi[al][bl]);
+                if (last_pt) {
+#pragma unroll
+                    for (int al = 0; al < P; ++al) {
+                        const int h = emod + al < P ? emod + al : emod + al - P;
+#pragma unroll
+                        for (int bl = 0; bl < P; ++bl)
+                            tm_ld2_issue(ta + h * F::RC + 2 * (bl - al + p), wlo[al][bl], whi[al][bl]);
+                    }
+                }
+                tm_wait_ld();
+                double r3[P][P];
+#pragma unroll
+                for (int al = 0; al < P; ++al)
+#pragma unroll
+                    for (int bl = 0; bl < P; ++bl) r3[al][bl] = __hiloint2double((int)hi[al][bl], (int)lo[al][bl]);
+                int ia = 0, ib = 0, ca = 0, cb = 0, r = 0;
+                bool live = false, item = i < n3;
+                if (item) {
+                    cb = i % Sb; ca = (i / Sb) % Sa; r = i / SAB;
+                    ia = T.a0 + r % na; ib = T.b0 + r / na;
+                    const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
+                    live = ja >= 1 && ja <= C.m[ka] && abs(ja - ia) <= p && jb >= 1 && jb <= C.m[kb] && abs(jb - ib) <= p;
+                    if (live) {
+                        const double* s2p = S2r + (r * F::NU) * SAB + ca * Sb + cb;
+                        const double s0 = s2p[0] + s2p[SAB], s1 = s2p[2 * SAB], s2v = s2p[3 * SAB], s3 = s2p[4 * SAB];
+#pragma unroll
+                        for (int al = 0; al < P; ++al) {
+                            const double c0 = fma(vb[al], s0, db[al] * s2v), c1 = fma(vb[al], s1, db[al] * s3);
+#pragma unroll
+                            for (int bl = 0; bl < P; ++bl) r3[al][bl] = fma(vb[bl], c0, fma(db[bl], c1, r3[al][bl]));
+                        }
+                    }
+                }
+                if (!last_pt) {
+#pragma unroll
+                    for (int al = 0; al < P; ++al)
+#pragma unroll
+                        for (int bl = 0; bl < P; ++bl) tm_st2(t3 + 2 * (al * P + bl), r3[al][bl]);
+                } else {
+#pragma unroll
+                    for (int al = 0; al < P; ++al) {
+                        const int h = emod + al < P ? emod + al : emod + al - P;
+#pragma unroll
+                        for (int bl = 0; bl < P; ++bl) {
+                            tm_st2(ta + h * F::RC + 2 * (bl - al + p),
+                                   __hiloint2double((int)whi[al][bl], (int)wlo[al][bl]) + r3[al][bl]);
+                            tm_st2(t3 + 2 * (al * P + bl), 0.0);
+                        }
+                    }
+                }
+                // (tcgen05 ops are warp-collective: the flush's TMEM traffic runs on
+                // every lane, the global stores only for real items)
+                if (last_pt) {   // element e complete: flush row e (+ the trailing rows), zero them
+                    tm_wait_st();
+                    const int64_t rowbase = (int64_t)(ia - 1) * C.rs[ka] + (int64_t)(ib - 1) * C.rs[kb];
+                    const int64_t slotab = (int64_t)ca * C.ss[ka] + (int64_t)cb * C.ss[kb];
+                    const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
+                    const bool diag = live && ja == ia && jb == ib;
+                    for (int f = 0; f < nfl; ++f) {
+                        const int h = emod + f < P ? emod + f : emod + f - P;
+                        uint32_t rl[W], rh[W];
+#pragma unroll
+                        for (int w = 0; w < W; ++w) tm_ld2_issue(ta + h * F::RC + 2 * w, rl[w], rh[w]);
+                        tm_wait_ld();
+                        const int irow = e + f;
+                        if (item && irow >= r0 && irow < r1) {
+                            const int64_t row = rowbase + (int64_t)(irow - 1) * rs_s;
+                            double* dst = stencil + C.mat_off + row;
+#pragma unroll
+                            for (int w = 0; w < W; ++w) {
+                                const int jc = irow + w - p;
+                                const bool inr = jc >= 1 && jc <= m_s;
+                                if (absm_s && !inr) continue;
+                                const int cs = absm_s ? jc - 1 : w;
+                                dst[((int64_t)cs * ss_s + slotab) * rows_c] =
+                                    inr ? __hiloint2double((int)rh[w], (int)rl[w]) : 0.0;
+                            }
+                            if (absm_s)
+                                for (int cs = 0; cs < S_s; ++cs)
+                                    if (abs(cs + 1 - irow) > p) dst[((int64_t)cs * ss_s + slotab) * rows_c] = 0.0;
+                            if (diag) dinv[C.vec_off + row] = 1.0 / __hiloint2double((int)rh[p], (int)rl[p]);
+                        }
+#pragma unroll
+                        for (int w = 0; w < W; ++w) tm_st2(ta + h * F::RC + 2 * w, 0.0);   // becomes stream row e + f + P
+                    }
+                }
+                if (!item && i < n3r) {   // load ring of row r (shared memory)
+                    const int rr = i - n3;
+                    double* RL = RLs + rr * P;
+                    const double sl = S2r[5 * n3 + rr];
+#pragma unroll
+                    for (int al = 0; al < P; ++al) RL[al] = fma(vb[al], sl, RL[al]);
+                    if (last_pt) {
+                        const int ia2 = T.a0 + rr % na, ib2 = T.b0 + rr / na;
+                        const int64_t rowbase = (int64_t)(ia2 - 1) * C.rs[ka] + (int64_t)(ib2 - 1) * C.rs[kb];
+                        for (int f = 0; f < nfl; ++f) {
+                            const int irow = e + f;
+                            if (irow >= r0 && irow < r1) rhs[C.vec_off + rowbase + (int64_t)(irow - 1) * rs_s] = RL[0];
+#pragma unroll
+                            for (int al = 0; al < p; ++al) RL[al] = RL[al + 1];
+                            RL[p] = 0.0;
+                        }
+                    }
+                }
+            }
+            tm_wait_st();   // this interval's rings are in TMEM before the next interval loads them
+        }
+        const long long c1 = prf ? clock64() : 0;
+        __syncthreads();
+        if (prf) {
+            const long long c2 = clock64();
+            if (tid == 0) { pc0 += c1 - c0; pc1 += c2 - c1; }
+            if (tid == G12) { pc2 += c1 - c0; pc3 += 1; }
+        }
+    }
+    if (prf) {
+        if (tid == 0) { prof[0] = pc0; prof[1] = pc1; }
+        if (tid == G12) { prof[2] = pc2; prof[3] = pc3; }
+    }
+    if (prof != nullptr && tid == 0) {   // per-CTA timeline: start, end (ns), SM
+        long long gt1;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        prof[8 + 3 * blockIdx.x] = gt0;
+        prof[9 + 3 * blockIdx.x] = gt1;
+        prof[10 + 3 * blockIdx.x] = smid;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp == G12 / 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(s_tmem) : "memory");
+}
+
+}  // namespace
+
+bool tile3_eligible(const Handle* h) {
+    return h->d == 3 && h->mu == 1 && h->q == h->p + 1 && (h->p == 3 || h->p == 4) && !h->opt.no_tma &&
+           !h->opt.asm_pencil && !h->opt.generic_assembly && !h->force_generic_assembly;
+}
+
+// Tile shapes, stream segments and tensor maps (host, once per component
+// table).  Per component the tile (na x nb rows) minimises a per-row model of
+// one barrier interval -- max(G12: stage 1 + stage 2, G3: stage 3), each
+// stage max(work-item rounds x item length, FMAs / throughput) -- subject to
+// the tensor-memory ring capacity and the shared-memory budget; the stream
+// segment length minimises the estimated makespan max(longest tile, total /
+// SMs); tiles are issued longest first.
+static bool build_tiles3(Handle* h) {
+    if (h->tiles3_state != 0) return h->tiles3_state > 0;
+    h->tiles3_state = -1;
+    if (!tile3_eligible(h)) return false;
+    const int p = h->p, P = p + 1, Q = h->q, W = 2 * p + 1, NC2 = (W + 1) / 2;
+    const int NSLOT = tile3_nslot(P);
+    const size_t SMEM_CAP = 225 * 1024;
+    void* fnp = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &qres) != cudaSuccess ||
+        qres != cudaDriverEntryPointSuccess || !fnp) {
+        cudaGetLastError();
+        return false;
+    }
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    EncodeFn encode = reinterpret_cast<EncodeFn>(fnp);
+    const int segs[] = {96, 64, 48, 32, 24, 16, 12, 8};
+    constexpr int NSEG = 8;
+
+    struct Shape { int na, nb, ta, tb, xa, xap, xb, cw; double plane; };
+    std::vector<Shape> shp(h->ncomp);
+    std::vector<CUtensorMap> maps(h->ncomp);
+    for (int c = 0; c < h->ncomp; ++c) {
+        const CompInfo& C = h->comps[c];
+        if (!C.rows) continue;
+        const int ka = C.ax[1], kb = C.ax[0], ks = C.ax[2];
+        const int ma = C.m[ka], mb = C.m[kb], Sa = C.S[ka], Sb = C.S[kb];
+        const int nel_a = C.nel[ka], nel_b = C.nel[kb];
+        const int Ir = Sa * Sb;
+        double best = 1e300;
+        Shape bs{};
+        for (int ta = 1; ta <= ma; ++ta) {
+            const int na = (ma + ta - 1) / ta;
+            if (ta > 1 && (ma + ta - 2) / (ta - 1) == na) continue;
+            for (int tb = 1; tb <= mb; ++tb) {
+                const int nb = (mb + tb - 1) / tb;
+                if (tb > 1 && (mb + tb - 2) / (tb - 1) == nb) continue;
+                const int rows = na * nb, n3 = rows * Ir;
+                if (n3 + rows > TILE3_G3 * NSLOT) continue;
+                const int xa = std::min(na + p, nel_a) * Q, xb = std::min(nb + p, nel_b) * Q;
+                const int xap = (Q & 1) ? ((xa + 2) & ~1) : ((xa + 1) & ~1);
+                if (xap > 256 || xb > 256) continue;
+                const TLay L = tile3_layout(P, na, nb, xa, xap, xb, n3);
+                if ((size_t)L.total * 8 > SMEM_CAP) continue;
+                const double xbw = std::min(P, nel_b) * Q, xaw = std::min(P, nel_a) * Q;
+                // one barrier interval, in cycles: a work item's chain at ~2
+                // cycles per FMA, the SM's sustained FP64 rate ~32 FMA / cycle
+                auto stage = [&](double items, double nthr, double per_item) {
+                    return std::max(std::ceil(items / nthr) * per_item * 2.0, items * per_item / 32.0);
+                };
+                const int cw = C.absm[kb] || rows * 5 * W <= TILE3_G12 ? 1 : 2;
+                const double n2 = (double)rows * 5 * (C.absm[kb] ? Sb : (cw == 2 ? NC2 : W));
+                const double t12 = stage((double)nb * 9 * xa, TILE3_G12, xbw * P) +
+                                   stage(n2, TILE3_G12, 2.0 * xaw * P * cw) + 300.0;
+                const double t3 = std::ceil((n3 + rows) / (double)TILE3_G3) * 260.0;
+                const double cost = std::max(t12, t3) + 150.0;
+                const double per_row = cost / rows;
+                if (per_row < best * 0.999) {
+                    best = per_row;
+                    bs = Shape{na, nb, ta, tb, xa, xap, xb, cw, cost};
+                }
+            }
+        }
+        if (best >= 1e299) return false;
+        shp[c] = bs;
+        const cuuint64_t Na = (cuuint64_t)C.nel[ka] * Q, Nb = (cuuint64_t)C.nel[kb] * Q, Ns = (cuuint64_t)C.nel[ks] * Q;
+        if (C.qs[ka] != 1 || C.qs[kb] != (int64_t)Na || C.qs[ks] != (int64_t)(Na * Nb)) return false;
+        const cuuint64_t dims[4] = {Na, Nb, Ns, (cuuint64_t)h->nG()};
+        const cuuint64_t strides[3] = {Na * 8, Na * Nb * 8, (cuuint64_t)C.nqp * 8};
+        const cuuint32_t box[4] = {(cuuint32_t)bs.xap, (cuuint32_t)bs.xb, 1, (cuuint32_t)h->nG()};
+        if (strides[0] % 16 || strides[1] % 16 || strides[2] % 16 || (C.qp_off * 8) % 16) return false;
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (encode(&maps[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)(h->d_G + C.qp_off), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    // stream segment length: makespan model over the SMs (one CTA each)
+    int nsm = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const double setup_planes = 6.0;
+    int SEG = segs[0];
+    {
+        double bestspan = 1e300;
+        for (int si = 0; si < NSEG; ++si) {
+            const int cand = segs[si];
+            double tot = 0, mx = 0;
+            for (int c = 0; c < h->ncomp; ++c) {
+                const CompInfo& C = h->comps[c];
+                if (!C.rows) continue;
+                const int ks = C.ax[2], ms = C.m[ks], nel_s = C.nel[ks];
+                const double ntile = (double)shp[c].ta * shp[c].tb;
+                for (int r0 = 1; r0 < 1 + ms; r0 += cand) {
+                    const int r1 = std::min(1 + ms, r0 + cand);
+                    const int ne = std::min(r1 - 1, nel_s - 1) - std::max(0, r0 - p) + 1;
+                    const double cost = (ne * Q + setup_planes) * shp[c].plane;
+                    tot += cost * ntile;
+                    mx = std::max(mx, cost);
+                }
+            }
+            const double span = std::max(mx, tot / nsm);
+            if (span < bestspan * 0.97) { bestspan = span; SEG = cand; }
+        }
+    }
+    std::vector<Tile3> tl;
+    std::vector<double> tcost;
+    size_t smem = 0;
+    for (int c = 0; c < h->ncomp; ++c) {
+        const CompInfo& C = h->comps[c];
+        if (!C.rows) continue;
+        const Shape& S = shp[c];
+        const int ka = C.ax[1], kb = C.ax[0], ks = C.ax[2];
+        const int ma = C.m[ka], mb = C.m[kb], ms = C.m[ks], nel_s = C.nel[ks];
+        for (int tb = 0; tb < S.tb; ++tb) {
+            const int b0 = 1 + (int)((int64_t)tb * mb / S.tb), b1 = 1 + (int)((int64_t)(tb + 1) * mb / S.tb);
+            for (int ta = 0; ta < S.ta; ++ta) {
+                const int a0 = 1 + (int)((int64_t)ta * ma / S.ta), a1 = 1 + (int)((int64_t)(ta + 1) * ma / S.ta);
+                for (int r0 = 1; r0 < 1 + ms; r0 += SEG) {
+                    Tile3 t;
+                    t.comp = c;
+                    t.a0 = a0; t.na = a1 - a0; t.b0 = b0; t.nb = b1 - b0;
+                    t.r0 = r0; t.r1 = std::min(1 + ms, r0 + SEG);
+                    t.xa = S.xa; t.xap = S.xap; t.xb = S.xb; t.cw = S.cw;
+                    const int ne = std::min(t.r1 - 1, nel_s - 1) - std::max(0, t.r0 - p) + 1;
+                    const TLay L = tile3_layout(P, t.na, t.nb, t.xa, t.xap, t.xb,
+                                                t.na * t.nb * C.S[C.ax[1]] * C.S[C.ax[0]]);
+                    smem = std::max(smem, (size_t)L.total * 8);
+                    tl.push_back(t);
+                    tcost.push_back((ne * Q + setup_planes) * S.plane);
+                }
+            }
+        }
+    }
+    if (tl.empty() || smem > SMEM_CAP) return false;
+    std::vector<int> order(tl.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return tcost[x] > tcost[y]; });
+    h->tiles3.resize(tl.size());
+    for (size_t i = 0; i < order.size(); ++i) h->tiles3[i] = tl[order[i]];
+    if (h->d_tiles3) { cudaFree(h->d_tiles3); h->d_tiles3 = nullptr; }
+    if (h->d_tmaps3) { cudaFree(h->d_tmaps3); h->d_tmaps3 = nullptr; }
+    if (cudaMalloc(&h->d_tiles3, sizeof(Tile3) * h->tiles3.size()) != cudaSuccess ||
+        cudaMalloc(&h->d_tmaps3, sizeof(CUtensorMap) * h->ncomp) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (cudaMemcpyAsync(h->d_tiles3, h->tiles3.data(), sizeof(Tile3) * h->tiles3.size(), cudaMemcpyHostToDevice,
+                        h->stream) != cudaSuccess ||
+        cudaMemcpyAsync(h->d_tmaps3, maps.data(), sizeof(CUtensorMap) * h->ncomp, cudaMemcpyHostToDevice,
+                        h->stream) != cudaSuccess ||
+        cudaStreamSynchronize(h->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    h->tiles3_smem = smem;
+    h->asm_seg = SEG;
+    h->tiles3_state = 1;
+    return true;
+}
+
+// returns false when the plan has no tiled instantiation (the caller then
+// runs k_assemble_fast)
+bool launch_assembly_tile(Handle* h, cudaError_t* err) {
+    if (!build_tiles3(h)) return false;
+    const void* fn = nullptr;
+    switch (h->p + 1) {
+        case 4: fn = (const void*)k_assemble_tile<4>; break;
+        case 5: fn = (const void*)k_assemble_tile<5>; break;
+        default: return false;
+    }
+    *err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tiles3_smem);
+    if (*err != cudaSuccess) return true;
+    long long* prof = nullptr;
+    const size_t nprof = 8 + 3 * h->tiles3.size();
+    if (h->opt.asm_profile) {
+        cudaMalloc(&prof, nprof * sizeof(long long));
+        cudaMemsetAsync(prof, 0, nprof * sizeof(long long), h->stream);
+    }
+    void* args[] = {(void*)&h->d_comps, (void*)&h->d_tabs, (void*)&h->d_tiles3, (void*)&h->d_tabvals,
+                    (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv, (void*)&h->d_tmaps3, (void*)&prof};
+    *err = cudaLaunchKernel(fn, dim3((unsigned)h->tiles3.size()), dim3(TILE3_THREADS), args, h->tiles3_smem,
+                            h->stream);
+    if (prof) {
+        std::vector<long long> tv(nprof);
+        long long* t = tv.data();
+        cudaStreamSynchronize(h->stream);
+        cudaMemcpy(t, prof, nprof * sizeof(long long), cudaMemcpyDeviceToHost);
+        {   // timeline: makespan, SM busy fraction, busy time per tile class
+            long long t0 = t[8], t1 = t[9];
+            double busy = 0;
+            std::vector<double> cls(64, 0.0);
+            std::vector<int> ncls(64, 0);
+            for (size_t b = 0; b < h->tiles3.size(); ++b) {
+                t0 = std::min(t0, t[8 + 3 * b]);
+                t1 = std::max(t1, t[9 + 3 * b]);
+                const double d = (double)(t[9 + 3 * b] - t[8 + 3 * b]);
+                busy += d;
+                const Tile3& tt = h->tiles3[b];
+                const CompInfo& C = h->comps[tt.comp];
+                const int la = std::min(7, 31 - __builtin_clz(std::max(1, C.nel[C.ax[1]])));
+                const int lb = std::min(7, 31 - __builtin_clz(std::max(1, C.nel[C.ax[0]])));
+                cls[la * 8 + lb] += d;
+                ncls[la * 8 + lb] += 1;
+            }
+            int nsm = 148;
+            fprintf(stderr, "asm-tile timeline: makespan %.3f ms, SM busy %.1f%%; busy ms by (log2 nel_a, log2 nel_b):",
+                    (t1 - t0) * 1e-6, 100.0 * busy / ((double)nsm * (t1 - t0)));
+            for (int c = 0; c < 64; ++c)
+                if (ncls[c]) fprintf(stderr, " (%d,%d):%.2f/%d", c / 8, c % 8, cls[c] * 1e-6 / nsm, ncls[c]);
+            fprintf(stderr, "\n");
+        }
+        const double n = t[3] > 0 ? (double)t[3] : 1.0;
+        const Tile3& t0 = h->tiles3[0];
+        fprintf(stderr, "asm-tile block0 comp=%d rows=%dx%d cw=%d intervals=%lld cycles/interval: G12 work=%.0f "
+                "barrier=%.0f | G3 work=%.0f ; tiles=%zu seg=%d smem=%zu\n", t0.comp, t0.na, t0.nb, t0.cw, t[3],
+                t[0] / n, t[1] / n, t[2] / n, h->tiles3.size(), h->asm_seg, h->tiles3_smem);
+        cudaFree(prof);
+    }
+    h->launches[0] += 1;
+    return true;
+}
+
+}  // namespace sgiga

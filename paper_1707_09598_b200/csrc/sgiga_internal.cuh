@@ -105,6 +105,30 @@ struct Pencil {         // one CTA of the assembly kernel
     int r0, r1;         // full function row range [r0, r1) along the stream axis
 };
 
+// one CTA of the tiled 3-D assembly (k_assembly_tile.cu): a block of the
+// cross-section (rows a0 .. a0+na-1 along a = ax[1], b0 .. b0+nb-1 along
+// b = ax[0], full function indices) times a segment [r0, r1) of the stream
+// axis ax[2]; xa / xb = the component's union plane-window extents (points),
+// xap = the TMA box's inner extent (the plane buffer's row stride); cw =
+// stage-2 columns per work item (1 or 2)
+struct Tile3 {
+    int comp;
+    int a0, na, b0, nb;
+    int r0, r1;
+    int xa, xap, xb;
+    int cw;
+};
+constexpr int TILE3_G12 = 256;                 // stage-1/2 threads (warps 0..7)
+constexpr int TILE3_G3 = 128;                  // stage-3 threads (warps 12..15, one per TMEM lane quadrant)
+constexpr int TILE3_THREADS = TILE3_G12 + TILE3_G3;
+// TMEM columns of one stage-3 work item: the ring -- P physical stream rows
+// (row R at R mod P) of 2p+1 doubles -- and the current element's P x P
+// partial block, two 32-bit columns per double (p = 4: 90 + 50 columns,
+// 3 items per thread; p = 3: 56 + 32, 5 items)
+__host__ __device__ constexpr int tile3_ring_cols(int P) { return 2 * P * (2 * P - 1); }
+__host__ __device__ constexpr int tile3_slot_cols(int P) { return tile3_ring_cols(P) + 2 * P * P; }
+__host__ __device__ constexpr int tile3_nslot(int P) { return 512 / tile3_slot_cols(P); }   // rings per stage-3 thread
+
 constexpr int ASM2_BA = 8;   // 2-D assembly: tile rows per block (k_assembly2d.cu)
 struct Block2 {         // one CTA of the 2-D assembly kernel
     int comp;

@@ -124,10 +124,11 @@ def test_fast_assembly_matches_generic(name, terms, monkeypatch):
 def test_tma_plane_copies_match_cp_async(name, pick, monkeypatch):
     """The TMA tensor-copy plane loads (zero-filled out-of-patch windows; for
     odd Q an even-aligned box read shifted by one point) assemble bitwise the
-    same stencil as the cp.async path."""
+    same stencil as the cp.async path (one-pencil-per-CTA kernel)."""
     cfg = configs.get_config(name)
     spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
     mats = {}
+    monkeypatch.setenv("SGIGA_ASM_PENCIL", "1")
     for mode in ("tma", "cpasync"):
         if mode == "cpasync":
             monkeypatch.setenv("SGIGA_NO_TMA", "1")
@@ -139,6 +140,29 @@ def test_tma_plane_copies_match_cp_async(name, pick, monkeypatch):
             b.close()
     for (A1, b1), (A2, b2) in zip(mats["tma"], mats["cpasync"]):
         assert np.array_equal(A1.data, A2.data) and np.array_equal(b1, b2)
+
+
+@pytest.mark.parametrize("name,pick", [("cfg2", (0, 5, 17, 30)), ("cfg5", (0, 4, 7, 40, 68, 100, 135))])
+def test_tiled_assembly_matches_pencil(name, pick, monkeypatch):
+    """The tiled 3-D assembly (k_assembly_tile.cu: union plane windows, stage-3
+    rings in tensor memory) and the one-pencil-per-CTA kernel assemble the
+    same stencil (same patterns; values to rounding -- the stream-axis sums
+    run in a different order)."""
+    cfg = configs.get_config(name)
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    mats = {}
+    for mode in ("tile", "pencil"):
+        monkeypatch.setenv("SGIGA_ASM_PENCIL", "1" if mode == "pencil" else "0")
+        b = Batch(spec)
+        try:
+            b.assemble()
+            mats[mode] = [b.export_csr(c) for c in pick]
+        finally:
+            b.close()
+    for (A1, b1), (A2, b2) in zip(mats["tile"], mats["pencil"]):
+        assert np.array_equal(A1.indptr, A2.indptr) and np.array_equal(A1.indices, A2.indices)
+        assert normwise(A1.data, A2.data) <= 1e-13
+        assert normwise(b1, b2) <= 1e-13
 
 
 def test_pcg_residual_contract():
