@@ -39,17 +39,6 @@ namespace {
 
 __device__ __forceinline__ uint32_t t3_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// 8 TMEM columns <-> 8 registers of this thread's lane (32x32b shape)
-__device__ __forceinline__ void tm_ld8(uint32_t a, uint32_t* r) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(a));
-}
-__device__ __forceinline__ void tm_st8(uint32_t a, const uint32_t* r) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n"
-                 ::"r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                 : "memory");
-}
 // one double (two TMEM columns) of this thread's lane
 __device__ __forceinline__ double tm_ld2_issue(uint32_t a, uint32_t& lo, uint32_t& hi) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(lo), "=r"(hi) : "r"(a));
@@ -58,6 +47,36 @@ __device__ __forceinline__ double tm_ld2_issue(uint32_t a, uint32_t& lo, uint32_
 __device__ __forceinline__ void tm_st2(uint32_t a, double v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n"
                  ::"r"(a), "r"((uint32_t)__double2loint(v)), "r"((uint32_t)__double2hiint(v)) : "memory");
+}
+// n consecutive TMEM columns (n even, 16-column chunks + pairs) of this thread's lane
+template <int N>
+__device__ __forceinline__ void tm_ldn(uint32_t a, uint32_t* r) {
+#pragma unroll
+    for (int c = 0; c + 16 <= N; c += 16)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                     "%13, %14, %15}, [%16];\n"
+                     : "=r"(r[c]), "=r"(r[c + 1]), "=r"(r[c + 2]), "=r"(r[c + 3]), "=r"(r[c + 4]), "=r"(r[c + 5]),
+                       "=r"(r[c + 6]), "=r"(r[c + 7]), "=r"(r[c + 8]), "=r"(r[c + 9]), "=r"(r[c + 10]), "=r"(r[c + 11]),
+                       "=r"(r[c + 12]), "=r"(r[c + 13]), "=r"(r[c + 14]), "=r"(r[c + 15])
+                     : "r"(a + c));
+#pragma unroll
+    for (int c = N & ~15; c < N; c += 2)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(r[c]), "=r"(r[c + 1]) : "r"(a + c));
+}
+template <int N>
+__device__ __forceinline__ void tm_stn(uint32_t a, const uint32_t* r) {
+#pragma unroll
+    for (int c = 0; c + 16 <= N; c += 16)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                     "%13, %14, %15, %16};\n"
+                     ::"r"(a + c), "r"(r[c]), "r"(r[c + 1]), "r"(r[c + 2]), "r"(r[c + 3]), "r"(r[c + 4]), "r"(r[c + 5]),
+                       "r"(r[c + 6]), "r"(r[c + 7]), "r"(r[c + 8]), "r"(r[c + 9]), "r"(r[c + 10]), "r"(r[c + 11]),
+                       "r"(r[c + 12]), "r"(r[c + 13]), "r"(r[c + 14]), "r"(r[c + 15])
+                     : "memory");
+#pragma unroll
+    for (int c = N & ~15; c < N; c += 2)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(a + c), "r"(r[c]), "r"(r[c + 1])
+                     : "memory");
 }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
@@ -71,9 +90,10 @@ struct TCfg {
     static constexpr int NC2 = (W + 1) / 2;     // stage-2 column pairs
     static constexpr int NG = 7;                // 6 metric entries + load
     static constexpr int NU = 5;                // stage-2 units
-    static constexpr int SC = tile3_slot_cols(P);     // TMEM columns per ring
-    static constexpr int RC = 2 * W;                  // TMEM columns per physical stream row
+    static constexpr int SC = tile3_slot_cols(P);     // TMEM columns per stage-3 item
+    static constexpr int R3C = tile3_r3_cols(P);      // its element partial (slot start)
     static constexpr int NSLOT = tile3_nslot(P);
+    static constexpr int RC = 2 * W;                  // TMEM columns per physical stream row
 };
 
 // per-CTA shared-memory layout (doubles)
@@ -244,6 +264,21 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         tm_wait_st();
     }
 
+    // each stage-3 item's S2 offset (-1: dead column -- outside the band or on
+    // the boundary -- whose stencil entries are written as zeros)
+    int s2off[F::NSLOT];
+#pragma unroll
+    for (int k = 0; k < F::NSLOT; ++k) {
+        const int i = g3t + TILE3_G3 * k;
+        s2off[k] = -1;
+        if (inG3 && i < n3) {
+            const int cb = i % Sb, ca = (i / Sb) % Sa, r = i / SAB;
+            const int ia = T.a0 + r % na, ib = T.b0 + r / na;
+            const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
+            if (ja >= 1 && ja <= C.m[ka] && abs(ja - ia) <= p && jb >= 1 && jb <= C.m[kb] && abs(jb - ib) <= p)
+                s2off[k] = (r * F::NU) * SAB + ca * Sb + cb;
+        }
+    }
     const bool prf = prof != nullptr && blockIdx.x == 0;
     long long gt0 = 0;
     if (prof != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
@@ -411,66 +446,59 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             const bool last_pt = g == Q - 1;
             const int nfl = e < e_last ? 1 : P;   // the last element completes rows e .. e + p
             const int emod = e % P;
+#pragma unroll 1
             for (int k = 0; k < nslot; ++k) {
                 const int i = g3t + TILE3_G3 * k;
-                const uint32_t ta = tbase + k * F::SC;
-                const uint32_t t3 = ta + tile3_ring_cols(P);   // element partial R3[al][bl]
+                const uint32_t t3 = tbase + k * F::SC;    // element partial R3[al][bl]
+                const uint32_t ta = t3 + F::R3C;          // ring: physical row h at ta + h * RC
                 // R3 accumulates this element's Q planes; at the element's last
                 // plane it is added to the ring window it touches -- stream row
                 // e + al (physical row (e + al) mod P), offsets w = p - al .. 2p - al
                 // (two-level sum: element partials, then elements, as the
                 // reference's element-by-element assembly)
-                uint32_t lo[P][P], hi[P][P], wlo[P][P], whi[P][P];
-#pragma unroll
-                for (int al = 0; al < P; ++al)
-#pragma unroll
-                    for (int bl = 0; bl < P; ++bl) tm_ld2_issue(t3 + 2 * (al * P + bl), lo[al][bl], hi[al][bl]);
-                if (last_pt) {
-#pragma unroll
-                    for (int al = 0; al < P; ++al) {
-                        const int h = emod + al < P ? emod + al : emod + al - P;
-#pragma unroll
-                        for (int bl = 0; bl < P; ++bl)
-                            tm_ld2_issue(ta + h * F::RC + 2 * (bl - al + p), wlo[al][bl], whi[al][bl]);
-                    }
-                }
+                uint32_t rr[F::R3C];
+                tm_ldn<F::R3C>(t3, rr);
                 tm_wait_ld();
                 double r3[P][P];
 #pragma unroll
                 for (int al = 0; al < P; ++al)
 #pragma unroll
-                    for (int bl = 0; bl < P; ++bl) r3[al][bl] = __hiloint2double((int)hi[al][bl], (int)lo[al][bl]);
-                int ia = 0, ib = 0, ca = 0, cb = 0, r = 0;
-                bool live = false, item = i < n3;
-                if (item) {
-                    cb = i % Sb; ca = (i / Sb) % Sa; r = i / SAB;
-                    ia = T.a0 + r % na; ib = T.b0 + r / na;
-                    const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
-                    live = ja >= 1 && ja <= C.m[ka] && abs(ja - ia) <= p && jb >= 1 && jb <= C.m[kb] && abs(jb - ib) <= p;
-                    if (live) {
-                        const double* s2p = S2r + (r * F::NU) * SAB + ca * Sb + cb;
-                        const double s0 = s2p[0] + s2p[SAB], s1 = s2p[2 * SAB], s2v = s2p[3 * SAB], s3 = s2p[4 * SAB];
+                    for (int bl = 0; bl < P; ++bl)
+                        r3[al][bl] = __hiloint2double((int)rr[2 * (al * P + bl) + 1], (int)rr[2 * (al * P + bl)]);
+                const bool item = i < n3;
+                int s2o = s2off[0];   // (register select, no local-memory indexing)
 #pragma unroll
-                        for (int al = 0; al < P; ++al) {
-                            const double c0 = fma(vb[al], s0, db[al] * s2v), c1 = fma(vb[al], s1, db[al] * s3);
+                for (int kk = 1; kk < F::NSLOT; ++kk) s2o = k == kk ? s2off[kk] : s2o;
+                if (s2o >= 0) {   // live item
+                    const double* s2p = S2r + s2o;
+                    const double s0 = s2p[0] + s2p[SAB], s1 = s2p[2 * SAB], s2v = s2p[3 * SAB], s3 = s2p[4 * SAB];
 #pragma unroll
-                            for (int bl = 0; bl < P; ++bl) r3[al][bl] = fma(vb[bl], c0, fma(db[bl], c1, r3[al][bl]));
-                        }
+                    for (int al = 0; al < P; ++al) {
+                        const double c0 = fma(vb[al], s0, db[al] * s2v), c1 = fma(vb[al], s1, db[al] * s3);
+#pragma unroll
+                        for (int bl = 0; bl < P; ++bl) r3[al][bl] = fma(vb[bl], c0, fma(db[bl], c1, r3[al][bl]));
                     }
                 }
                 if (!last_pt) {
 #pragma unroll
                     for (int al = 0; al < P; ++al)
 #pragma unroll
-                        for (int bl = 0; bl < P; ++bl) tm_st2(t3 + 2 * (al * P + bl), r3[al][bl]);
-                } else {
+                        for (int bl = 0; bl < P; ++bl) {
+                            rr[2 * (al * P + bl)] = (uint32_t)__double2loint(r3[al][bl]);
+                            rr[2 * (al * P + bl) + 1] = (uint32_t)__double2hiint(r3[al][bl]);
+                        }
+                    tm_stn<F::R3C>(t3, rr);
+                } else {   // window row by row (registers): ring += R3, R3 = 0
 #pragma unroll
                     for (int al = 0; al < P; ++al) {
                         const int h = emod + al < P ? emod + al : emod + al - P;
+                        uint32_t wlo[P], whi[P];
+#pragma unroll
+                        for (int bl = 0; bl < P; ++bl) tm_ld2_issue(ta + h * F::RC + 2 * (bl - al + p), wlo[bl], whi[bl]);
+                        tm_wait_ld();
 #pragma unroll
                         for (int bl = 0; bl < P; ++bl) {
-                            tm_st2(ta + h * F::RC + 2 * (bl - al + p),
-                                   __hiloint2double((int)whi[al][bl], (int)wlo[al][bl]) + r3[al][bl]);
+                            tm_st2(ta + h * F::RC + 2 * (bl - al + p), __hiloint2double((int)whi[bl], (int)wlo[bl]) + r3[al][bl]);
                             tm_st2(t3 + 2 * (al * P + bl), 0.0);
                         }
                     }
@@ -479,10 +507,12 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 // every lane, the global stores only for real items)
                 if (last_pt) {   // element e complete: flush row e (+ the trailing rows), zero them
                     tm_wait_st();
+                    const int cb = i % Sb, ca = (i / Sb) % Sa, r = i / SAB;
+                    const int ia = T.a0 + r % na, ib = T.b0 + r / na;
                     const int64_t rowbase = (int64_t)(ia - 1) * C.rs[ka] + (int64_t)(ib - 1) * C.rs[kb];
                     const int64_t slotab = (int64_t)ca * C.ss[ka] + (int64_t)cb * C.ss[kb];
                     const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
-                    const bool diag = live && ja == ia && jb == ib;
+                    const bool diag = s2o >= 0 && ja == ia && jb == ib;
                     for (int f = 0; f < nfl; ++f) {
                         const int h = emod + f < P ? emod + f : emod + f - P;
                         uint32_t rl[W], rh[W];

@@ -118,15 +118,19 @@ struct Tile3 {
     int xa, xap, xb;
     int cw;
 };
-constexpr int TILE3_G12 = 256;                 // stage-1/2 threads (warps 0..7)
-constexpr int TILE3_G3 = 128;                  // stage-3 threads (warps 12..15, one per TMEM lane quadrant)
+#ifndef SGIGA_TILE3_G12
+#define SGIGA_TILE3_G12 256
+#endif
+constexpr int TILE3_G12 = SGIGA_TILE3_G12;     // stage-1/2 threads (warps 0 .. G12/32 - 1)
+constexpr int TILE3_G3 = 128;                  // stage-3 threads (the last 4 warps, one per TMEM lane quadrant)
 constexpr int TILE3_THREADS = TILE3_G12 + TILE3_G3;
 // TMEM columns of one stage-3 work item: the ring -- P physical stream rows
 // (row R at R mod P) of 2p+1 doubles -- and the current element's P x P
 // partial block, two 32-bit columns per double (p = 4: 90 + 50 columns,
 // 3 items per thread; p = 3: 56 + 32, 5 items)
 __host__ __device__ constexpr int tile3_ring_cols(int P) { return 2 * P * (2 * P - 1); }
-__host__ __device__ constexpr int tile3_slot_cols(int P) { return tile3_ring_cols(P) + 2 * P * P; }
+__host__ __device__ constexpr int tile3_r3_cols(int P) { return 2 * P * P; }   // at the slot start (16-aligned)
+__host__ __device__ constexpr int tile3_slot_cols(int P) { return (tile3_r3_cols(P) + tile3_ring_cols(P) + 15) & ~15; }
 __host__ __device__ constexpr int tile3_nslot(int P) { return 512 / tile3_slot_cols(P); }   // rings per stage-3 thread
 
 constexpr int ASM2_BA = 8;   // 2-D assembly: tile rows per block (k_assembly2d.cu)
