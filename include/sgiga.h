@@ -266,6 +266,12 @@ int sgiga_phase_stats(sgiga_handle* h, float* ms3, int64_t* launches3);
  * iterations), [5] residual check + expand, [6] combine / grid evaluation. */
 int sgiga_kernel_times(sgiga_handle* h, float* ms7);
 
+/* FP64 operations the last stencil assembly executed (FMA = 2), counted
+ * on the host from the launch's work decomposition (the tiled 3-D kernel;
+ * 0 when the plan ran another assembly kernel).  The bench reports it
+ * beside the canonical sum-factorised count of SURVEY 8(d).              */
+int sgiga_assembly_flops(sgiga_handle* h, double* executed);
+
 /* Per-component PCG iteration counts of the last solve.                 */
 int sgiga_iterations(sgiga_handle* h, int32_t* iters);
 

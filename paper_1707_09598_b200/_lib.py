@@ -48,7 +48,7 @@ EXPORTED = (
     "sgiga_iterations", "sgiga_kernel_times", "sgiga_stream", "sgiga_destroy", "sgiga_last_error",
     "sgiga_device_count", "sgiga_local_poisson_systems",
     "sgiga_full_patch_system", "sgiga_edge_projection_system", "sgiga_gather_sum", "sgiga_gather",
-    "sgiga_csr_spmv_sub", "sgiga_csr_pcg", "sgiga_set_coefficients_device",
+    "sgiga_csr_spmv_sub", "sgiga_csr_pcg", "sgiga_set_coefficients_device", "sgiga_assembly_flops",
 )
 
 
@@ -124,6 +124,7 @@ def _declare(lib):
         "sgiga_basis_table": ([VP, ct.c_int32, ct.c_int32, P_I32, P_F64, P_F64, P_F64, P_F64], ct.c_int),
         "sgiga_iterations": ([VP, P_I32], ct.c_int),
         "sgiga_kernel_times": ([VP, P_F32], ct.c_int),
+        "sgiga_assembly_flops": ([VP, P_F64], ct.c_int),
         "sgiga_stream": ([VP], VP),
         "sgiga_destroy": ([VP], ct.c_int),
         "sgiga_last_error": ([], ct.c_char_p),

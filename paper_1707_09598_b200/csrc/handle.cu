@@ -1426,6 +1426,13 @@ int sgiga_kernel_times(sgiga_handle* hh, float* ms7) {
     return SGIGA_OK;
 }
 
+int sgiga_assembly_flops(sgiga_handle* hh, double* executed) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !executed) return SGIGA_ERR_VALUE;
+    *executed = h->asm_tiled ? h->tiles3_flops : 0.0;
+    return SGIGA_OK;
+}
+
 void* sgiga_stream(sgiga_handle* hh) {
     Handle* h = reinterpret_cast<Handle*>(hh);
     return h ? (void*)h->stream : nullptr;

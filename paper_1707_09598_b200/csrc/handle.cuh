@@ -200,6 +200,8 @@ struct Handle {
     void* d_tmaps3 = nullptr;
     int tiles3_state = 0;                  // 0 = not built, 1 = ready, -1 = not applicable
     size_t tiles3_smem = 0;
+    double tiles3_flops = 0.0;             // FP64 operations one tiled-assembly launch executes
+    bool asm_tiled = false;                // the last assembly ran k_assemble_tile
     bool small_checked = false;            // small comps' true residual came from the cluster PCG
 
     // whole-run CUDA graph (sgiga_run): captured on the second call with the

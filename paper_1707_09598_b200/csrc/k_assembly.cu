@@ -308,8 +308,11 @@ cudaError_t launch_assembly(Handle* h) {
     cudaError_t fe = cudaSuccess;
     if (!h->force_generic_assembly && launch_assembly_2d(h, &fe))     // 2-D blocks, q = p+1
         return fe == cudaSuccess ? cudaGetLastError() : fe;
-    if (!h->force_generic_assembly && launch_assembly_tile(h, &fe))   // 3-D tiles, q = p+1, p = 3, 4
+    h->asm_tiled = false;
+    if (!h->force_generic_assembly && launch_assembly_tile(h, &fe)) {   // 3-D tiles, q = p+1, p = 3, 4
+        h->asm_tiled = true;
         return fe == cudaSuccess ? cudaGetLastError() : fe;
+    }
     if (!h->force_generic_assembly && launch_assembly_fast(h, &fe))   // maximal regularity, q = p+1
         return fe == cudaSuccess ? cudaGetLastError() : fe;
     size_t smem = assembly_smem_bytes(h);

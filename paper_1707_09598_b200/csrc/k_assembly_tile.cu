@@ -656,7 +656,11 @@ static bool build_tiles3(Handle* h) {
                 auto stage = [&](double items, double nthr, double per_item) {
                     return std::max(std::ceil(items / nthr) * per_item * 2.0, items * per_item / 32.0);
                 };
+#ifndef SGIGA_TILE3_CW
                 const int cw = C.absm[kb] || rows * 5 * W <= TILE3_G12 ? 1 : 2;
+#else
+                const int cw = C.absm[kb] ? 1 : SGIGA_TILE3_CW;
+#endif
                 const double n2 = (double)rows * 5 * (C.absm[kb] ? Sb : (cw == 2 ? NC2 : W));
                 const double t12 = stage((double)nb * 9 * xa, TILE3_G12, xbw * P) +
                                    stage(n2, TILE3_G12, 2.0 * xaw * P * cw) + 300.0;
@@ -740,6 +744,46 @@ static bool build_tiles3(Handle* h) {
         }
     }
     if (tl.empty() || smem > SMEM_CAP) return false;
+    // FP64 operations the launch executes (FMA = 2): per plane, stage 1 --
+    // 8 pair slots x valid a-window x valid b-window x P (+ load), stage 2 --
+    // 9 pairs x executed w_b columns x valid a-window x P (+ load), stage 3 --
+    // per live column 2 P^2 + 2 P FMAs + 2 P products + 1 sum (+ load ring),
+    // and per element the ring fold (P^2 adds)
+    double flops = 0.0;
+    for (const Tile3& t : tl) {
+        const CompInfo& C = h->comps[t.comp];
+        const int ka = C.ax[1], kb = C.ax[0], ks = C.ax[2];
+        const int nel_a = C.nel[ka], nel_b = C.nel[kb], nel_s = C.nel[ks];
+        const int ne = std::min(t.r1 - 1, nel_s - 1) - std::max(0, t.r0 - p) + 1;
+        if (ne <= 0) continue;
+        auto win = [&](int i, int nel) { return (std::min(nel - 1, i) - std::max(0, i - p) + 1) * Q; };
+        const int EA0 = std::max(0, t.a0 - p), EA1 = std::min(nel_a - 1, t.a0 + t.na - 1);
+        const double XAv = (double)(EA1 - EA0 + 1) * Q;
+        double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        for (int rb = 0; rb < t.nb; ++rb) s1 += XAv * win(t.b0 + rb, nel_b) * (8.0 * P + 1.0) * 2.0;
+        const int Sa = C.S[ka], Sb = C.S[kb];
+        for (int rb = 0; rb < t.nb; ++rb)
+            for (int ra = 0; ra < t.na; ++ra) {
+                const int ia = t.a0 + ra, ib = t.b0 + rb;
+                int ncol = 0;
+                if (C.absm[kb]) {
+                    for (int cb = 0; cb < Sb; ++cb) ncol += std::abs(cb + 1 - ib) <= p;
+                } else {
+                    ncol = t.cw == 2 ? 2 * ((W + 1) / 2) : W;
+                }
+                s2 += (9.0 * ncol * P + 1.0) * win(ia, nel_a) * 2.0;
+                for (int ca = 0; ca < Sa; ++ca)
+                    for (int cb = 0; cb < Sb; ++cb) {
+                        const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
+                        if (ja >= 1 && ja <= C.m[ka] && std::abs(ja - ia) <= p && jb >= 1 && jb <= C.m[kb] &&
+                            std::abs(jb - ib) <= p)
+                            s3 += (2.0 * (2.0 * P * P + 2.0 * P) + 2.0 * P + 1.0) + (double)P * P / Q;
+                    }
+                s3 += 2.0 * P;   // load ring
+            }
+        flops += (s1 + s2 + s3) * ne * Q;
+    }
+    h->tiles3_flops = flops;
     std::vector<int> order(tl.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return tcost[x] > tcost[y]; });

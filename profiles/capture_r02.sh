@@ -15,14 +15,14 @@ full() {   # <kernel regex> <name> <bench args...>
   ncu --set full --clock-control none --import-source on -k regex:"$k" -c 1 -o "$OUT/$n" -f \
       python bench.py "$@" --steps 1 --warmup 3 --no-cpu-baseline > "$OUT/ncu_$n.log" 2>&1
 }
-full '^k_assemble_fast' k_assemble_fast_cfg5 --config cfg5
+full '^k_assemble_tile' k_assemble_tile_cfg5 --config cfg5
 full '^k_metric' k_metric_cfg5 --config cfg5
 full '^k_combine_points_tiled' k_combine_points_tiled_cfg5 --config cfg5
 full '^k_pcg_fdl' k_pcg_fdl_cfg5 --config cfg5
 full '^k_pcg_fd<' k_pcg_fd_cfg5 --config cfg5
 full '^k_pcg_fdg' k_pcg_fdg_cfg5_tensor --config cfg5_tensor
-full '^k_assemble_fast' k_assemble_fast_cfg5_tensor --config cfg5_tensor
-full '^k_assemble_fast' k_assemble_fast_cfg2 --config cfg2
+full '^k_assemble_tile' k_assemble_tile_cfg5_tensor --config cfg5_tensor
+full '^k_assemble_tile' k_assemble_tile_cfg2 --config cfg2
 full '^k_assemble2d' k_assemble2d_cfg3_x1024 --config cfg3 --replicas 1024
 full '^k_assemble2d' k_assemble2d_cfg1_x1024 --config cfg1 --replicas 1024
 ls "$OUT"

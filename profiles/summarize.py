@@ -100,13 +100,16 @@ def main(src: str, dst: str) -> None:
             txt, got = _full_summary(path)
             head = f"# ncu --set full --clock-control none --import-source on, first launch ({stem})\n"
             open(os.path.join(dst, f"ncu_full_{stem}.txt"), "w").write(head + txt + _hot_lines(path))
-            if stem.startswith("k_assemble_fast_") and "dram__bytes_read.sum" in got:
-                wl = stem[len("k_assemble_fast_"):]
-                traffic[wl] = {
-                    "kernel": "k_assemble_fast",
-                    "dram_bytes_per_launch": got["dram__bytes_read.sum"] + got.get("dram__bytes_write.sum", 0.0),
-                    "source": os.path.join(os.path.basename(os.path.normpath(dst)), f"ncu_full_{stem}.txt"),
-                }
+            for kern in ("k_assemble_tile", "k_assemble_fast"):
+                if stem.startswith(kern + "_") and "dram__bytes_read.sum" in got:
+                    wl = stem[len(kern) + 1:]
+                    if wl in traffic and traffic[wl].get("kernel") == "k_assemble_tile" and kern != "k_assemble_tile":
+                        continue   # the product kernel's capture wins
+                    traffic[wl] = {
+                        "kernel": kern,
+                        "dram_bytes_per_launch": got["dram__bytes_read.sum"] + got.get("dram__bytes_write.sum", 0.0),
+                        "source": os.path.join(os.path.basename(os.path.normpath(dst)), f"ncu_full_{stem}.txt"),
+                    }
     json.dump(traffic, open(tpath, "w"), indent=1)
 
 
