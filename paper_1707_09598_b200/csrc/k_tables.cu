@@ -63,16 +63,27 @@ __global__ void k_basis_tables(const TabInfo* __restrict__ tabs, int ntab,
 
 // ---- fused geometry -> metric + load --------------------------------------
 // One thread per (component, quadrature point), storage order (s, a, b).
-template <int D>
+// GP > 0: every geometry axis has degree GP - 1 (compile-time contraction
+// loops); the homogeneous control net is staged in shared memory when it
+// fits (nsh > 0 doubles).  Same operations in the same order for every GP:
+// the metric does not depend on the instantiation.
+template <int D, int GP>
 __global__ void __launch_bounds__(256, 2)
 k_metric(const CompInfo* __restrict__ comps, int ncomp,
                          const int64_t* __restrict__ qp_cum, const TabInfo* __restrict__ tabs,
                          const double* __restrict__ qx, const double* __restrict__ qw,
                          const double* __restrict__ geob, const int* __restrict__ geofirst,
-                         const GeoInfo* __restrict__ geo, const double* __restrict__ hw,
+                         const GeoInfo* __restrict__ geo, const double* __restrict__ hw_g,
                          int q, int forcing_id, const double* __restrict__ hostf,
                          double* __restrict__ xphys, double* __restrict__ Gout,
-                         int* __restrict__ err, const int* __restrict__ cta_comp) {
+                         int* __restrict__ err, const int* __restrict__ cta_comp, int nsh) {
+    extern __shared__ double s_hw[];
+    const double* hw = hw_g;
+    if (nsh > 0) {
+        for (int i = threadIdx.x; i < nsh; i += blockDim.x) s_hw[i] = hw_g[i];
+        __syncthreads();
+        hw = s_hw;
+    }
     // the component of the CTA's first point from the per-CTA table (no
     // search, no barrier); a thread past that component's end searches itself
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -132,20 +143,25 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
     int gn[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) gn[k] = geo->n[k];
-    int c0 = geo->deg[0] + 1, c1 = D > 1 ? geo->deg[1] + 1 : 1, c2 = D > 2 ? geo->deg[2] + 1 : 1;
+    const int c0 = GP > 0 ? GP : geo->deg[0] + 1;
+    const int c1 = D > 1 ? (GP > 0 ? GP : geo->deg[1] + 1) : 1;
+    const int c2 = D > 2 ? (GP > 0 ? GP : geo->deg[2] + 1) : 1;
     if constexpr (D == 3) {
         // sum-factorised: contract axis 0 (values and derivatives), then axis
         // 1, then axis 2 -- 2(D+1)(c0 c1 c2 + 1.5 c1 c2 + 2 c2) FMAs instead of
         // a product per control point (rounding-level reordering of einsum)
         const int L0 = first[0] * gn[1], L1 = first[1];
+#pragma unroll
         for (int l = 0; l < c2; ++l) {
             double Bvv[D + 1], Bdv[D + 1], Bvd[D + 1];
 #pragma unroll
             for (int c = 0; c <= D; ++c) Bvv[c] = Bdv[c] = Bvd[c] = 0.0;
+#pragma unroll
             for (int j = 0; j < c1; ++j) {
                 double Av[D + 1], Ad[D + 1];
 #pragma unroll
                 for (int c = 0; c <= D; ++c) Av[c] = Ad[c] = 0.0;
+#pragma unroll
                 for (int i = 0; i < c0; ++i) {
                     const double b0 = bv[0][i], d0 = bv[0][GEO_PMAX + i];
                     const double* h = hw + (int64_t)(((L0 + i * gn[1]) + (L1 + j)) * gn[2] + first[2] + l) * (D + 1);
@@ -173,8 +189,11 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
             }
         }
     } else
+#pragma unroll
     for (int i = 0; i < c0; ++i)
+#pragma unroll
         for (int j = 0; j < c1; ++j)
+#pragma unroll
             for (int l = 0; l < c2; ++l) {
                 int idx[3] = {i, j, l};
                 int L = 0;
@@ -293,14 +312,30 @@ cudaError_t launch_metric(Handle* h) {
     if (n == 0) return cudaSuccess;
     int64_t blocks = (n + 255) / 256;
     const double* hostf = (h->forcing_id == SGIGA_FORCING_HOST) ? h->d_hostf : nullptr;
-#define LAUNCH_METRIC(DD)                                                                    \
-    k_metric<DD><<<(unsigned)blocks, 256, 0, h->stream>>>(                                   \
+    // geometry degree of every axis (compile-time loops for degree 1..3) and
+    // the control net in shared memory when it is at most 24 KB
+    int gp = h->geo.deg[0] + 1;
+    for (int k = 1; k < h->d; ++k)
+        if (h->geo.deg[k] + 1 != gp) gp = 0;
+    if (gp > (h->d == 3 ? 3 : 4)) gp = 0;   // (3-D, degree 3: register spills -- runtime loops)
+    const int nsh = h->geo_hw.size() <= 3072 ? (int)h->geo_hw.size() : 0;
+    const size_t shb = sizeof(double) * (size_t)nsh;
+#define LAUNCH_METRIC(DD, GG)                                                                 \
+    k_metric<DD, GG><<<(unsigned)blocks, 256, shb, h->stream>>>(                              \
         h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->d_geob,    \
         h->d_geofirst, h->d_geo, h->d_geo_hw, h->q, h->forcing_id, hostf, h->d_xphys, h->d_G, \
-        h->d_err, h->d_mcomp)
-    if (h->d == 1) LAUNCH_METRIC(1);
-    else if (h->d == 2) LAUNCH_METRIC(2);
-    else LAUNCH_METRIC(3);
+        h->d_err, h->d_mcomp, nsh)
+#define LAUNCH_METRIC_D(DD)                                                                   \
+    switch (gp) {                                                                             \
+        case 2: LAUNCH_METRIC(DD, 2); break;                                                  \
+        case 3: LAUNCH_METRIC(DD, 3); break;                                                  \
+        case 4: if (DD < 3) { LAUNCH_METRIC(DD, 4); break; } [[fallthrough]];                \
+        default: LAUNCH_METRIC(DD, 0); break;                                                 \
+    }
+    if (h->d == 1) { LAUNCH_METRIC_D(1) }
+    else if (h->d == 2) { LAUNCH_METRIC_D(2) }
+    else { LAUNCH_METRIC_D(3) }
+#undef LAUNCH_METRIC_D
 #undef LAUNCH_METRIC
     h->launches[0]++;
     return cudaGetLastError();
