@@ -146,6 +146,28 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
     const int c0 = GP > 0 ? GP : geo->deg[0] + 1;
     const int c1 = D > 1 ? (GP > 0 ? GP : geo->deg[1] + 1) : 1;
     const int c2 = D > 2 ? (GP > 0 ? GP : geo->deg[2] + 1) : 1;
+    // compile-time degree: the point's geometry basis values / derivatives
+    // in registers, read as 16-byte pairs (same values, same operations)
+    constexpr int GR = GP > 0 ? GP : 1;
+    double gvb[D][GR], gdb[D][GR];
+    if constexpr (GP > 0) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+#pragma unroll
+            for (int i = 0; i + 1 < GP; i += 2) {
+                const double2 v2 = __ldg(reinterpret_cast<const double2*>(bv[k] + i));
+                const double2 d2 = __ldg(reinterpret_cast<const double2*>(bv[k] + GEO_PMAX + i));
+                gvb[k][i] = v2.x; gvb[k][i + 1] = v2.y;
+                gdb[k][i] = d2.x; gdb[k][i + 1] = d2.y;
+            }
+            if constexpr (GP & 1) {
+                gvb[k][GP - 1] = __ldg(bv[k] + GP - 1);
+                gdb[k][GP - 1] = __ldg(bv[k] + GEO_PMAX + GP - 1);
+            }
+        }
+    }
+    auto BV = [&](int k, int i) { if constexpr (GP > 0) return gvb[k][i]; else return bv[k][i]; };
+    auto BD = [&](int k, int i) { if constexpr (GP > 0) return gdb[k][i]; else return bv[k][GEO_PMAX + i]; };
     if constexpr (D == 3) {
         // sum-factorised: contract axis 0 (values and derivatives), then axis
         // 1, then axis 2 -- 2(D+1)(c0 c1 c2 + 1.5 c1 c2 + 2 c2) FMAs instead of
@@ -163,7 +185,7 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
                 for (int c = 0; c <= D; ++c) Av[c] = Ad[c] = 0.0;
 #pragma unroll
                 for (int i = 0; i < c0; ++i) {
-                    const double b0 = bv[0][i], d0 = bv[0][GEO_PMAX + i];
+                    const double b0 = BV(0, i), d0 = BD(0, i);
                     const double* h = hw + (int64_t)(((L0 + i * gn[1]) + (L1 + j)) * gn[2] + first[2] + l) * (D + 1);
 #pragma unroll
                     for (int c = 0; c <= D; ++c) {
@@ -171,7 +193,7 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
                         Ad[c] = fma(d0, h[c], Ad[c]);
                     }
                 }
-                const double b1 = bv[1][j], d1 = bv[1][GEO_PMAX + j];
+                const double b1 = BV(1, j), d1 = BD(1, j);
 #pragma unroll
                 for (int c = 0; c <= D; ++c) {
                     Bvv[c] = fma(b1, Av[c], Bvv[c]);
@@ -179,7 +201,7 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
                     Bvd[c] = fma(d1, Av[c], Bvd[c]);
                 }
             }
-            const double b2 = bv[2][l], d2 = bv[2][GEO_PMAX + l];
+            const double b2 = BV(2, l), d2 = BD(2, l);
 #pragma unroll
             for (int c = 0; c <= D; ++c) {
                 hom[c] = fma(b2, Bvv[c], hom[c]);
@@ -201,8 +223,8 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
                     L = L * gn[k] + (first[k] + idx[k]);
-                    v[k] = bv[k][idx[k]];
-                    dv[k] = bv[k][GEO_PMAX + idx[k]];
+                    v[k] = BV(k, idx[k]);
+                    dv[k] = BD(k, idx[k]);
                 }
                 double prod = v[0];
 #pragma unroll

@@ -37,9 +37,10 @@ __all__ = ["component_cost_model", "plan_partition", "plan_rows", "ordered_combi
            "allgather_padded", "DistributedPlan", "run_plan_distributed"]
 
 # modelling constants (measured on the B200, bench.py / profiles/r02):
-ASM_RATE = 17.0e12      # canonical sum-factorised FP64 FLOP/s of the 3-D assembly (cfg5)
+ASM_RATE = 40.0e12      # canonical sum-factorised FP64 FLOP/s of the tiled 3-D assembly, thin cross-section
+ASM_RATE_LONG = 30.0e12 # ... cross-sections with no axis of <= 4 elements (cfg5 per-class timeline)
 ASM_RATE_2D = 4.0e12    # ... of the 2-D assembly (cfg3 x1024)
-HBM_RATE = 3.5e12       # bytes/s the FD / line-FD PCG streams its stencils at
+HBM_RATE = 4.0e12       # bytes/s the FD / line-FD PCG streams its stencils at
 JACOBI_ITER = 2.0       # Jacobi-PCG iterations grow ~ 2**max(level) (conditioning of K)
 FD_MMAX = 72            # axes the FD preconditioner diagonalises (csrc/sgiga_internal.cuh)
 
@@ -48,9 +49,10 @@ def component_cost_model(terms, degree: int, d: int) -> np.ndarray:
     """Modelled device seconds per component.
 
     * assembly: canonical sum-factorised FLOPs F_el = 2 d^2 sum_k P^(d+k+1)
-      + 2 d P^(d+1) per element at the measured rate -- on
-      cfg5 the assembly is ~87 % of a pass and scales with the element
-      count 2^|beta|, not with the solver;
+      + 2 d P^(d+1) per element at the measured rate of the
+      tiled kernel for the component's cross-section class -- on cfg5 the
+      assembly is ~75 % of a pass and scales with the element count
+      2^|beta|, not with the solver;
     * solve: FD-preconditioned components (every axis but the longest
       within the FD range) converge in 1-2 iterations: ~3 stencil sweeps
       (iterations + true residual) plus the line factors; the others run
@@ -59,10 +61,13 @@ def component_cost_model(terms, degree: int, d: int) -> np.ndarray:
     P = degree + 1
     W = 2 * degree + 1
     F_el = 2 * d * d * sum(P ** (d + k + 1) for k in range(1, d + 1)) + 2 * d * P ** (d + 1)
-    rate = ASM_RATE if d == 3 else ASM_RATE_2D
     out = []
     for beta, _ in terms:
         nel = float(np.prod([2.0 ** b for b in beta]))
+        # the tiled kernel covers a thin cross-section axis whole (the stream
+        # axis is the longest one); long x long cross-sections run slower
+        thin = d == 3 and min(sorted(beta)[:-1]) <= 2
+        rate = (ASM_RATE if thin else ASM_RATE_LONG) if d == 3 else ASM_RATE_2D
         m = np.array([2 ** b + degree - 2 for b in beta], dtype=np.float64)
         rows = float(np.prod(np.maximum(m, 0)))
         slots = float(np.prod(np.minimum(np.maximum(m, 1), W)))

@@ -91,8 +91,8 @@ def test_cost_model_is_assembly_dominated_on_cfg5():
         sel = cost[nel == 2.0 ** s]
         assert sel.max() / sel.min() < 1.6, s
     assert cost[nel == 2 ** 12].min() > cost[nel == 2 ** 11].max() * 1.2
-    # the modelled plan total is the measured single-GPU pass within 2x
-    assert 0.02 < cost.sum() < 0.08
+    # the modelled plan total is the measured single-GPU pass (~19.5 ms) within 2x
+    assert 0.01 < cost.sum() < 0.04
     # 8-way LPT is balanced to within one component
     parts = plan_partition(cfg.plan, 8, cfg.problem.degree)
     loads = np.array([cost[p].sum() for p in parts])
