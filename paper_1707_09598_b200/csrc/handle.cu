@@ -206,7 +206,12 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
         // long ones (the cfg2 makespan was one long pencil), fewer halo planes
         // (the tiled 3-D assembly keeps the longest axis: its tiles cover the
         // thin cross-section, so a long stream axis is what it wants)
-        if (!tile3_eligible(h)) {
+        {
+            int ls = 0;
+            for (int k = 0; k < d; ++k) ls += C.lv[k];
+            C.tile3 = tile3_eligible(h) && std::ldexp(1.0, ls) >= TILE3_MIN_ELEMENTS ? 1 : 0;
+        }
+        if (!C.tile3) {
             int64_t rows_c = 1;
             bool fd_axes = true;
             for (int k = 0; k < d; ++k) { rows_c *= std::max(0, C.m[k]); fd_axes = fd_axes && C.m[k] <= FD_MMAX; }
@@ -414,9 +419,15 @@ static int build_tables(Handle* h, const sgiga_problem_desc* D) {
                     h->pencils.push_back(pc);
                 }
     }
+    // the pencils of components the tiled kernel does not take come first
+    // (launched alone when the tiled kernel runs), each group longest first
     std::stable_sort(h->pencils.begin(), h->pencils.end(), [&](const Pencil& x, const Pencil& y) {
+        const int tx = h->comps[x.comp].tile3, ty = h->comps[y.comp].tile3;
+        if (tx != ty) return tx < ty;
         return seg_elems(h->comps[x.comp], x.r0, x.r1) > seg_elems(h->comps[y.comp], y.r0, y.r1);
     });
+    h->n_pencils_other = 0;
+    for (const Pencil& pc : h->pencils) h->n_pencils_other += h->comps[pc.comp].tile3 ? 0 : 1;
     h->asm_seg = SEG;
     // 2-D components (maximal regularity, q = p + 1): blocks of up to ASM2_BA
     // tile rows x a segment of the walk axis for k_assembly2d.  A block walks

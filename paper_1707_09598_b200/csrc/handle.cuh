@@ -191,6 +191,7 @@ struct Handle {
     std::vector<int> iters;
     bool force_generic_assembly = false;   // SGIGA_GENERIC_ASSEMBLY=1 (parity cross-check)
     int asm_seg = 0;                       // stream-axis segment length of the pencils
+    int n_pencils_other = 0;               // pencils of the components the tiled kernel does not take (first)
     void* d_tmaps = nullptr;               // per-component CUtensorMap of d_G (TMA plane copies)
     int tmaps_state = 0;                   // 0 = not built, 1 = ready, -1 = unavailable
     // tiled 3-D assembly (k_assembly_tile.cu): tiles, per-component tensor
@@ -249,9 +250,11 @@ struct Handle {
     int nG() const { return ncg() + 1; }           // + load
 };
 
-// the tiled 3-D assembly (k_assembly_tile.cu) serves this plan (static
-// properties only: d = 3, maximal regularity, q = p + 1, degree 3 or 4)
+// the tiled 3-D assembly (k_assembly_tile.cu) can serve this plan (d = 3,
+// maximal regularity, q = p + 1, degree 3 or 4); the per-component choice
+// is CompInfo::tile3 (components with at least TILE3_MIN_ELEMENTS elements)
 bool tile3_eligible(const Handle* h);
+constexpr double TILE3_MIN_ELEMENTS = 512.0;
 
 // symmetric index of (m, n) in the packed metric (row-major upper triangle)
 __host__ __device__ inline int sym_index(int d, int m, int n) {

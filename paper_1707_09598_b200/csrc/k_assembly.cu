@@ -298,7 +298,7 @@ size_t assembly_smem_bytes(const Handle* h) {
     return n * sizeof(double);
 }
 
-bool launch_assembly_fast(Handle* h, cudaError_t* err);
+bool launch_assembly_fast(Handle* h, cudaError_t* err, int npencils);
 bool launch_assembly_2d(Handle* h, cudaError_t* err);
 bool launch_assembly_tile(Handle* h, cudaError_t* err);
 
@@ -311,9 +311,13 @@ cudaError_t launch_assembly(Handle* h) {
     h->asm_tiled = false;
     if (!h->force_generic_assembly && launch_assembly_tile(h, &fe)) {   // 3-D tiles, q = p+1, p = 3, 4
         h->asm_tiled = true;
-        return fe == cudaSuccess ? cudaGetLastError() : fe;
+        if (fe != cudaSuccess) return fe;
+        // the components below the tile threshold: one row per CTA
+        if (h->n_pencils_other > 0 && launch_assembly_fast(h, &fe, h->n_pencils_other))
+            return fe == cudaSuccess ? cudaGetLastError() : fe;
+        return cudaGetLastError();
     }
-    if (!h->force_generic_assembly && launch_assembly_fast(h, &fe))   // maximal regularity, q = p+1
+    if (!h->force_generic_assembly && launch_assembly_fast(h, &fe, np))   // maximal regularity, q = p+1
         return fe == cudaSuccess ? cudaGetLastError() : fe;
     size_t smem = assembly_smem_bytes(h);
     cudaError_t e;

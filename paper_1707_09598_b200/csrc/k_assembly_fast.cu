@@ -882,8 +882,9 @@ static bool build_tmaps(Handle* h, int NX) {
     return true;
 }
 
-bool launch_assembly_fast(Handle* h, cudaError_t* err) {
+bool launch_assembly_fast(Handle* h, cudaError_t* err, int npencils) {
     if (h->mu != 1 || h->q != h->p + 1 || h->pencils.empty()) return false;
+    if (npencils <= 0) return true;
     const int key = h->d * 10 + (h->p + 1);
     const bool no_tma = h->opt.no_tma;
     const bool tma = h->d == 3 && !no_tma &&
@@ -920,7 +921,7 @@ bool launch_assembly_fast(Handle* h, cudaError_t* err) {
     void* args[] = {(void*)&h->d_comps, (void*)&h->d_tabs, (void*)&h->d_pencils, (void*)&h->d_tabvals,
                     (void*)&h->d_G, (void*)&h->d_stencil, (void*)&h->d_rhs, (void*)&h->d_dinv,
                     (void*)&prof, (void*)&h->d_tmaps};
-    *err = cudaLaunchKernel(fn, dim3((unsigned)h->pencils.size()), dim3(nthreads), args, smem, h->stream);
+    *err = cudaLaunchKernel(fn, dim3((unsigned)npencils), dim3(nthreads), args, smem, h->stream);
     if (prof) {
         long long t[40];
         cudaStreamSynchronize(h->stream);

@@ -28,6 +28,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
@@ -630,7 +631,7 @@ static bool build_tiles3(Handle* h) {
     std::vector<CUtensorMap> maps(h->ncomp);
     for (int c = 0; c < h->ncomp; ++c) {
         const CompInfo& C = h->comps[c];
-        if (!C.rows) continue;
+        if (!C.rows || !C.tile3) continue;
         const int ka = C.ax[1], kb = C.ax[0], ks = C.ax[2];
         const int ma = C.m[ka], mb = C.m[kb], Sa = C.S[ka], Sb = C.S[kb];
         const int nel_a = C.nel[ka], nel_b = C.nel[kb];
@@ -699,7 +700,7 @@ static bool build_tiles3(Handle* h) {
             double tot = 0, mx = 0;
             for (int c = 0; c < h->ncomp; ++c) {
                 const CompInfo& C = h->comps[c];
-                if (!C.rows) continue;
+                if (!C.rows || !C.tile3) continue;
                 const int ks = C.ax[2], ms = C.m[ks], nel_s = C.nel[ks];
                 const double ntile = (double)shp[c].ta * shp[c].tb;
                 for (int r0 = 1; r0 < 1 + ms; r0 += cand) {
@@ -714,12 +715,13 @@ static bool build_tiles3(Handle* h) {
             if (span < bestspan * 0.97) { bestspan = span; SEG = cand; }
         }
     }
+
     std::vector<Tile3> tl;
     std::vector<double> tcost;
     size_t smem = 0;
     for (int c = 0; c < h->ncomp; ++c) {
         const CompInfo& C = h->comps[c];
-        if (!C.rows) continue;
+        if (!C.rows || !C.tile3) continue;
         const Shape& S = shp[c];
         const int ka = C.ax[1], kb = C.ax[0], ks = C.ax[2];
         const int ma = C.m[ka], mb = C.m[kb], ms = C.m[ks], nel_s = C.nel[ks];

@@ -77,6 +77,8 @@ struct CompInfo {
     int64_t chunk_off;  // first PCG chunk (large path)
     int nchunks;
     int fd;             // 1 = solved by the FD-preconditioned one-CTA CG (k_fd.cu)
+    int tile3;          // 1 = assembled by the tiled 3-D kernel (k_assembly_tile.cu; per component:
+                        //     the choice never depends on the batch the component is in)
 };
 
 struct GeoInfo {
