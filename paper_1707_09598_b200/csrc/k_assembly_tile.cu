@@ -99,7 +99,7 @@ struct TCfg {
 
 // per-CTA shared-memory layout (doubles)
 struct TLay {
-    int sGw, oTa, oTb, oPhiA, oPhiB, oS1, s1slot, oSL1, oS2, s2sz, oRL, total;
+    int sGw, oTa, oTb, oPhiA, oPhiB, oS1, s1slot, oSL1, oS2, s2sz, oRL, oList, total;
 };
 
 __host__ __device__ inline TLay tile3_layout(int P, int na, int nb, int xa, int xap, int xb, int n3) {
@@ -117,8 +117,28 @@ __host__ __device__ inline TLay tile3_layout(int P, int na, int nb, int xa, int 
     L.oS2 = L.oSL1 + nb * xa;
     L.s2sz = 5 * n3 + rows;                      // [row][unit][c_a][c_b] + load [row]
     L.oRL = L.oS2 + 2 * L.s2sz;
-    L.total = L.oRL + rows * P;
+    L.oList = L.oRL + rows * P;                  // stage-3 item list (ints): computed items first
+    L.total = L.oList + (n3 + 1) / 2;
     return L;
+}
+
+// Symmetry: A(i, j) = A(j, i), so a stage-3 work item -- a cross-section row
+// and one storage column (c_a, c_b) -- is computed only for non-negative
+// cross-section offsets (o_b > 0, or o_b = 0 and o_a >= 0) and writes the
+// mirrored entries of the twin row too; for (o_a, o_b) = (0, 0) only the
+// stream offsets o_s >= 0 are written (and mirrored).  Categories of a
+// storage column: computed (POS, POS0 = the (0, 0) column), NEG (its
+// in-band entries come from twins; only its structural zeros are written
+// here), DEAD (outside the band or on the boundary: zeros).
+enum : int { T3_DEAD = 0, T3_NEG = 1, T3_POS = 2, T3_POS0 = 3 };
+__host__ __device__ inline int tile3_category(int ia, int ib, int ca, int cb, int absa, int absb, int ma, int mb,
+                                              int p) {
+    const int ja = absa ? ca + 1 : ia + ca - p, jb = absb ? cb + 1 : ib + cb - p;
+    const int oa = ja - ia, ob = jb - ib;
+    if (!(ja >= 1 && ja <= ma && oa >= -p && oa <= p && jb >= 1 && jb <= mb && ob >= -p && ob <= p)) return T3_DEAD;
+    if (ob > 0 || (ob == 0 && oa > 0)) return T3_POS;
+    if (ob == 0 && oa == 0) return T3_POS0;
+    return T3_NEG;
 }
 
 // stage-1 pair slots: aa, as(=sa), ss, ab, sb, ba, bs, bb -- b-type of each
@@ -253,7 +273,22 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const bool inG3 = tid >= G12;
     const int g3t = tid - G12;   // 0..127: TMEM lane 32 (warp % 4) + lane
     const uint32_t tbase = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-    const int n3r = n3 + rows;   // + one load-ring item per row (shared memory)
+    // item list: computed columns first (packed r*SAB + c_a*Sb + c_b, bit 30 =
+    // POS0), then the others (bit 30 = DEAD); built once per tile
+    __shared__ int s_cnt[2];
+    int* s_list = reinterpret_cast<int*>(sm + L.oList);
+    if (tid < 2) s_cnt[tid] = 0;
+    __syncthreads();
+    for (int it = tid; it < n3; it += NT) {
+        const int cb = it % Sb, ca = (it / Sb) % Sa, r = it / SAB;
+        const int cat = tile3_category(T.a0 + r % na, T.b0 + r / na, ca, cb, C.absm[ka], C.absm[kb], C.m[ka],
+                                       C.m[kb], p);
+        if (cat >= T3_POS) s_list[atomicAdd(&s_cnt[0], 1)] = it | (cat == T3_POS0 ? 1 << 30 : 0);
+        else s_list[n3 - 1 - atomicAdd(&s_cnt[1], 1)] = it | (cat == T3_DEAD ? 1 << 30 : 0);
+    }
+    __syncthreads();
+    const int npos = s_cnt[0];
+    const int n3r = npos + rows;   // + one load-ring item per row (shared memory)
     const int nslot = (n3r + TILE3_G3 - 1) / TILE3_G3;   // <= NSLOT (host-checked)
     const int64_t rs_s = C.rs[ks], ss_s = C.ss[ks], rows_c = C.rows;
     const int absm_s = C.absm[ks], m_s = C.m[ks], S_s = C.S[ks];
@@ -272,12 +307,10 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     for (int k = 0; k < F::NSLOT; ++k) {
         const int i = g3t + TILE3_G3 * k;
         s2off[k] = -1;
-        if (inG3 && i < n3) {
-            const int cb = i % Sb, ca = (i / Sb) % Sa, r = i / SAB;
-            const int ia = T.a0 + r % na, ib = T.b0 + r / na;
-            const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
-            if (ja >= 1 && ja <= C.m[ka] && abs(ja - ia) <= p && jb >= 1 && jb <= C.m[kb] && abs(jb - ib) <= p)
-                s2off[k] = (r * F::NU) * SAB + ca * Sb + cb;
+        if (inG3 && i < npos) {
+            const int it = s_list[i] & ((1 << 30) - 1);
+            const int cb = it % Sb, ca = (it / Sb) % Sa, r = it / SAB;
+            s2off[k] = (r * F::NU) * SAB + ca * Sb + cb;
         }
     }
     const bool prf = prof != nullptr && blockIdx.x == 0;
@@ -290,7 +323,10 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     // a relative one its 2p+1 offsets, one or two per item
     const int cw = T.cw;
     const int absm_b = C.absm[kb];
-    const int ncol2 = absm_b ? Sb : (cw == 2 ? NC2 : W);
+    // (symmetry: only columns with o_b >= 0, i.e. w_b >= p; a relative axis
+    // starts its column groups at the even w_b = p & ~1 for aligned pair loads)
+    const int wbs = cw == 2 ? (p & ~1) : p;
+    const int ncol2 = absm_b ? Sb : (W - wbs + cw - 1) / cw;
     const int n2 = rows * F::NU * ncol2;
     for (int j = 0; j <= nplanes; ++j) {
         const long long c0 = prf ? clock64() : 0;
@@ -363,8 +399,9 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                         if (it < n2) {
                             const int cg = it % ncol2, u = (it / ncol2) % F::NU, r = it / (ncol2 * F::NU);
                             const int ra = r % na, rb = r / na, ia = T.a0 + ra, ib = T.b0 + rb;
-                            const int wb0 = absm_b ? cg + 1 - ib + p : CW * cg;   // first w_b of the item
+                            const int wb0 = absm_b ? cg + 1 - ib + p : wbs + CW * cg;   // first w_b of the item
                             if (wb0 < 0 || wb0 >= W) continue;   // column outside the band: dead stage-3 items
+                            if (absm_b && wb0 < p) continue;     // o_b < 0: computed by the twin row
                             const int tlo = max(0, p - ia), thi = min(P, nel_a + p - ia);
                             const int xoff = (ia - p - EA0) * Q;
                             double acc0[W], acc1[W];
@@ -466,7 +503,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 #pragma unroll
                     for (int bl = 0; bl < P; ++bl)
                         r3[al][bl] = __hiloint2double((int)rr[2 * (al * P + bl) + 1], (int)rr[2 * (al * P + bl)]);
-                const bool item = i < n3;
+                const bool item = i < npos;
                 int s2o = s2off[0];   // (register select, no local-memory indexing)
 #pragma unroll
                 for (int kk = 1; kk < F::NSLOT; ++kk) s2o = k == kk ? s2off[kk] : s2o;
@@ -508,12 +545,18 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 // every lane, the global stores only for real items)
                 if (last_pt) {   // element e complete: flush row e (+ the trailing rows), zero them
                     tm_wait_st();
-                    const int cb = i % Sb, ca = (i / Sb) % Sa, r = i / SAB;
+                    const int le = item ? s_list[i] : 0;
+                    const bool pos0 = (le >> 30) & 1;
+                    const int it = le & ((1 << 30) - 1);
+                    const int cb = it % Sb, ca = (it / Sb) % Sa, r = it / SAB;
                     const int ia = T.a0 + r % na, ib = T.b0 + r / na;
+                    const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
                     const int64_t rowbase = (int64_t)(ia - 1) * C.rs[ka] + (int64_t)(ib - 1) * C.rs[kb];
                     const int64_t slotab = (int64_t)ca * C.ss[ka] + (int64_t)cb * C.ss[kb];
-                    const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
-                    const bool diag = s2o >= 0 && ja == ia && jb == ib;
+                    // the twin row (ja, jb) and this row's column slots in it
+                    const int64_t rowbaseM = (int64_t)(ja - 1) * C.rs[ka] + (int64_t)(jb - 1) * C.rs[kb];
+                    const int caM = C.absm[ka] ? ia - 1 : 2 * p - ca, cbM = C.absm[kb] ? ib - 1 : 2 * p - cb;
+                    const int64_t slotabM = (int64_t)caM * C.ss[ka] + (int64_t)cbM * C.ss[kb];
                     for (int f = 0; f < nfl; ++f) {
                         const int h = emod + f < P ? emod + f : emod + f - P;
                         uint32_t rl[W], rh[W];
@@ -528,22 +571,30 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                             for (int w = 0; w < W; ++w) {
                                 const int jc = irow + w - p;
                                 const bool inr = jc >= 1 && jc <= m_s;
-                                if (absm_s && !inr) continue;
-                                const int cs = absm_s ? jc - 1 : w;
-                                dst[((int64_t)cs * ss_s + slotab) * rows_c] =
-                                    inr ? __hiloint2double((int)rh[w], (int)rl[w]) : 0.0;
+                                const double v = __hiloint2double((int)rh[w], (int)rl[w]);
+                                // own entry (the (0,0) column's o_s < 0 entries are its twins' mirrors)
+                                if (!(absm_s && !inr) && !(pos0 && w < p && inr)) {
+                                    const int cs = absm_s ? jc - 1 : w;
+                                    dst[((int64_t)cs * ss_s + slotab) * rows_c] = inr ? v : 0.0;
+                                }
+                                // mirrored entry A(twin, this row)
+                                if (inr && !(pos0 && w <= p)) {
+                                    const int csM = absm_s ? irow - 1 : 2 * p - w;
+                                    stencil[C.mat_off + rowbaseM + (int64_t)(jc - 1) * rs_s +
+                                            ((int64_t)csM * ss_s + slotabM) * rows_c] = v;
+                                }
                             }
                             if (absm_s)
                                 for (int cs = 0; cs < S_s; ++cs)
                                     if (abs(cs + 1 - irow) > p) dst[((int64_t)cs * ss_s + slotab) * rows_c] = 0.0;
-                            if (diag) dinv[C.vec_off + row] = 1.0 / __hiloint2double((int)rh[p], (int)rl[p]);
+                            if (pos0) dinv[C.vec_off + row] = 1.0 / __hiloint2double((int)rh[p], (int)rl[p]);
                         }
 #pragma unroll
                         for (int w = 0; w < W; ++w) tm_st2(ta + h * F::RC + 2 * w, 0.0);   // becomes stream row e + f + P
                     }
                 }
                 if (!item && i < n3r) {   // load ring of row r (shared memory)
-                    const int rr = i - n3;
+                    const int rr = i - npos;
                     double* RL = RLs + rr * P;
                     const double sl = S2r[5 * n3 + rr];
 #pragma unroll
@@ -557,6 +608,28 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 #pragma unroll
                             for (int al = 0; al < p; ++al) RL[al] = RL[al + 1];
                             RL[p] = 0.0;
+                        }
+                    }
+                }
+            }
+            if (last_pt) {   // NEG / DEAD columns of the flushed rows: their structural zeros
+                for (int f = 0; f < nfl; ++f) {
+                    const int irow = e + f;
+                    if (irow < r0 || irow >= r1) continue;
+                    for (int q = npos + g3t; q < n3; q += TILE3_G3) {
+                        const int le = s_list[q];
+                        const bool dead = (le >> 30) & 1;
+                        const int it = le & ((1 << 30) - 1);
+                        const int cb = it % Sb, ca = (it / Sb) % Sa, r = it / SAB;
+                        const int ia = T.a0 + r % na, ib = T.b0 + r / na;
+                        const int64_t row = (int64_t)(ia - 1) * C.rs[ka] + (int64_t)(ib - 1) * C.rs[kb] +
+                                            (int64_t)(irow - 1) * rs_s;
+                        double* dst = stencil + C.mat_off + row;
+                        const int64_t slotab = (int64_t)ca * C.ss[ka] + (int64_t)cb * C.ss[kb];
+                        for (int cs = 0; cs < S_s; ++cs) {
+                            const int jc = absm_s ? cs + 1 : irow + cs - p;
+                            const bool band = jc >= 1 && jc <= m_s && abs(jc - irow) <= p;
+                            if (dead || !band) dst[((int64_t)cs * ss_s + slotab) * rows_c] = 0.0;
                         }
                     }
                 }
@@ -645,7 +718,21 @@ static bool build_tiles3(Handle* h) {
                 const int nb = (mb + tb - 1) / tb;
                 if (tb > 1 && (mb + tb - 2) / (tb - 1) == nb) continue;
                 const int rows = na * nb, n3 = rows * Ir;
-                if (n3 + rows > TILE3_G3 * NSLOT) continue;
+                // computed (POS) stage-3 items of the fullest tile of this shape
+                int npos = 0;
+                for (int tbi = 0; tbi < tb; ++tbi)
+                    for (int tai = 0; tai < ta; ++tai) {
+                        const int a0 = 1 + (int)((int64_t)tai * ma / ta), a1 = 1 + (int)((int64_t)(tai + 1) * ma / ta);
+                        const int b0 = 1 + (int)((int64_t)tbi * mb / tb), b1 = 1 + (int)((int64_t)(tbi + 1) * mb / tb);
+                        int cnt = 0;
+                        for (int ib = b0; ib < b1; ++ib)
+                            for (int ia = a0; ia < a1; ++ia)
+                                for (int ca = 0; ca < Sa; ++ca)
+                                    for (int cb = 0; cb < Sb; ++cb)
+                                        cnt += tile3_category(ia, ib, ca, cb, C.absm[ka], C.absm[kb], ma, mb, p) >= T3_POS;
+                        npos = std::max(npos, cnt);
+                    }
+                if (npos + rows > TILE3_G3 * NSLOT) continue;
                 const int xa = std::min(na + p, nel_a) * Q, xb = std::min(nb + p, nel_b) * Q;
                 const int xap = (Q & 1) ? ((xa + 2) & ~1) : ((xa + 1) & ~1);
                 if (xap > 256 || xb > 256) continue;
@@ -662,10 +749,11 @@ static bool build_tiles3(Handle* h) {
 #else
                 const int cw = C.absm[kb] ? 1 : SGIGA_TILE3_CW;
 #endif
-                const double n2 = (double)rows * 5 * (C.absm[kb] ? Sb : (cw == 2 ? NC2 : W));
+                const int wbs = cw == 2 ? (p & ~1) : p;
+                const double n2 = (double)rows * 5 * (C.absm[kb] ? (Sb + 1) / 2 : (W - wbs + cw - 1) / cw);
                 const double t12 = stage((double)nb * 9 * xa, TILE3_G12, xbw * P) +
                                    stage(n2, TILE3_G12, 2.0 * xaw * P * cw) + 300.0;
-                const double t3 = std::ceil((n3 + rows) / (double)TILE3_G3) * 260.0;
+                const double t3 = std::ceil((npos + rows) / (double)TILE3_G3) * 260.0 + (double)n3 / TILE3_G3 * 20.0;
                 const double cost = std::max(t12, t3) + 150.0;
                 const double per_row = cost / rows;
                 if (per_row < best * 0.999) {
@@ -767,20 +855,18 @@ static bool build_tiles3(Handle* h) {
         for (int rb = 0; rb < t.nb; ++rb)
             for (int ra = 0; ra < t.na; ++ra) {
                 const int ia = t.a0 + ra, ib = t.b0 + rb;
-                int ncol = 0;
+                int ncol = 0;   // stage-2 columns executed (o_b >= 0; pair groups padded)
                 if (C.absm[kb]) {
-                    for (int cb = 0; cb < Sb; ++cb) ncol += std::abs(cb + 1 - ib) <= p;
+                    for (int cb = 0; cb < Sb; ++cb) ncol += cb + 1 - ib >= 0 && cb + 1 - ib <= p;
                 } else {
-                    ncol = t.cw == 2 ? 2 * ((W + 1) / 2) : W;
+                    const int wbs = t.cw == 2 ? (p & ~1) : p;
+                    ncol = t.cw * ((W - wbs + t.cw - 1) / t.cw);
                 }
                 s2 += (9.0 * ncol * P + 1.0) * win(ia, nel_a) * 2.0;
                 for (int ca = 0; ca < Sa; ++ca)
-                    for (int cb = 0; cb < Sb; ++cb) {
-                        const int ja = C.absm[ka] ? ca + 1 : ia + ca - p, jb = C.absm[kb] ? cb + 1 : ib + cb - p;
-                        if (ja >= 1 && ja <= C.m[ka] && std::abs(ja - ia) <= p && jb >= 1 && jb <= C.m[kb] &&
-                            std::abs(jb - ib) <= p)
+                    for (int cb = 0; cb < Sb; ++cb)
+                        if (tile3_category(ia, ib, ca, cb, C.absm[ka], C.absm[kb], C.m[ka], C.m[kb], p) >= T3_POS)
                             s3 += (2.0 * (2.0 * P * P + 2.0 * P) + 2.0 * P + 1.0) + (double)P * P / Q;
-                    }
                 s3 += 2.0 * P;   // load ring
             }
         flops += (s1 + s2 + s3) * ne * Q;
