@@ -87,7 +87,10 @@ struct TCfg {
     static constexpr int p = P - 1, Q = P, W = 2 * P - 1;
     static constexpr int RP = (P + 1) & ~1;     // pair-table row (16-byte pair loads)
     static constexpr int PQ = P * Q;            // window points of one row
-    static constexpr int S1W = (W + 1) & ~1;    // S1 row (w_b pairs by 16-byte loads)
+    // symmetry: stage 2 reads only w_b >= p & ~1 (o_b >= 0, even start for
+    // aligned pair loads), so stage 1 keeps the columns WBS1 .. W-1 only
+    static constexpr int WBS1 = p & ~1;
+    static constexpr int S1W = (W - WBS1 + 1) & ~1;   // S1 row (w_b pairs by 16-byte loads)
     static constexpr int NC2 = (W + 1) / 2;     // stage-2 column pairs
     static constexpr int NG = 7;                // 6 metric entries + load
     static constexpr int NU = 5;                // stage-2 units
@@ -103,7 +106,7 @@ struct TLay {
 };
 
 __host__ __device__ inline TLay tile3_layout(int P, int na, int nb, int xa, int xap, int xb, int n3) {
-    const int Q = P, W = 2 * P - 1, RP = (P + 1) & ~1, PQ = P * Q, S1W = (W + 1) & ~1;
+    const int Q = P, W = 2 * P - 1, RP = (P + 1) & ~1, PQ = P * Q, S1W = (W - ((P - 1) & ~1) + 1) & ~1;
     const int rows = na * nb;
     TLay L;
     L.sGw = (7 * xb * xap + 15) & ~15;
@@ -157,7 +160,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 double* __restrict__ stencil, double* __restrict__ rhs, double* __restrict__ dinv,
                 const CUtensorMap* __restrict__ tmaps, long long* __restrict__ prof) {
     using F = TCfg<P>;
-    constexpr int p = F::p, Q = F::Q, W = F::W, RP = F::RP, PQ = F::PQ, S1W = F::S1W;
+    constexpr int p = F::p, Q = F::Q, W = F::W, RP = F::RP, PQ = F::PQ, S1W = F::S1W, WBS1 = F::WBS1;
     constexpr int NC2 = F::NC2, G12 = TILE3_G12, NT = TILE3_THREADS;
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bar[2];
@@ -369,12 +372,13 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                     tv[2 * k2 + 1] = v2.y;
                                 }
 #pragma unroll
-                                for (int k = 0; k < P; ++k) acc[t + k] = fma(gv, tv[k], acc[t + k]);
+                                for (int k = 0; k < P; ++k)
+                                    if (t + k >= WBS1) acc[t + k] = fma(gv, tv[k], acc[t + k]);
                             }
                         }
-                        double* o = S1 + (rb * 8 + sig) * L.s1slot + xa * S1W;
+                        double* o = S1 + (rb * 8 + sig) * L.s1slot + xa * S1W - WBS1;
 #pragma unroll
-                        for (int w = 0; w < W; w += 2)
+                        for (int w = WBS1; w < W; w += 2)
                             *reinterpret_cast<double2*>(o + w) = make_double2(acc[w], w + 1 < W ? acc[w + 1] : 0.0);
                     } else {
                         const double* gp = Gw + (6 * xb + xoff) * xap + xa;
@@ -410,7 +414,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 #pragma unroll
                             for (int pr = 0; pr < 2; ++pr) {
                                 if (pr == 1 && u == 4) break;
-                                const double* sp = S1 + (rb * 8 + c_t3_uslot[u][pr]) * L.s1slot + xoff * S1W + wb0;
+                                const double* sp = S1 + (rb * 8 + c_t3_uslot[u][pr]) * L.s1slot + xoff * S1W + (wb0 - WBS1);
                                 const double* ta = Ta + (ra * 4 + c_t3_uat[u][pr]) * PQ * RP;
 #pragma unroll
                                 for (int t = 0; t < P; ++t) {
@@ -850,7 +854,13 @@ static bool build_tiles3(Handle* h) {
         const int EA0 = std::max(0, t.a0 - p), EA1 = std::min(nel_a - 1, t.a0 + t.na - 1);
         const double XAv = (double)(EA1 - EA0 + 1) * Q;
         double s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        for (int rb = 0; rb < t.nb; ++rb) s1 += XAv * win(t.b0 + rb, nel_b) * (8.0 * P + 1.0) * 2.0;
+        for (int rb = 0; rb < t.nb; ++rb) {   // stage 1: only the kept columns t + k >= p & ~1
+            const int ib = t.b0 + rb;
+            double fk = 0.0;
+            for (int tt = std::max(0, p - ib); tt < std::min(P, nel_b + p - ib); ++tt)
+                fk += Q * (P - std::max(0, (p & ~1) - tt));
+            s1 += XAv * (8.0 * fk + win(ib, nel_b)) * 2.0;
+        }
         const int Sa = C.S[ka], Sb = C.S[kb];
         for (int rb = 0; rb < t.nb; ++rb)
             for (int ra = 0; ra < t.na; ++ra) {
