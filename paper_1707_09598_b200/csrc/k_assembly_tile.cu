@@ -675,6 +675,15 @@ bool tile3_eligible(const Handle* h) {
            !h->opt.asm_pencil && !h->opt.generic_assembly && !h->force_generic_assembly;
 }
 
+#ifndef SGIGA_TILE3_C3
+#define SGIGA_TILE3_C3 260.0    // cost model: cycles of one stage-3 item slot per plane
+#endif
+#ifndef SGIGA_TILE3_O12
+#define SGIGA_TILE3_O12 300.0   // ... fixed cycles of the G12 part of an interval
+#endif
+#ifndef SGIGA_TILE3_OVH
+#define SGIGA_TILE3_OVH 150.0   // ... fixed cycles of an interval
+#endif
 // Tile shapes, stream segments and tensor maps (host, once per component
 // table).  Per component the tile (na x nb rows) minimises a per-row model of
 // one barrier interval -- max(G12: stage 1 + stage 2, G3: stage 3), each
@@ -756,9 +765,10 @@ static bool build_tiles3(Handle* h) {
                 const int wbs = cw == 2 ? (p & ~1) : p;
                 const double n2 = (double)rows * 5 * (C.absm[kb] ? (Sb + 1) / 2 : (W - wbs + cw - 1) / cw);
                 const double t12 = stage((double)nb * 9 * xa, TILE3_G12, xbw * P) +
-                                   stage(n2, TILE3_G12, 2.0 * xaw * P * cw) + 300.0;
-                const double t3 = std::ceil((npos + rows) / (double)TILE3_G3) * 260.0 + (double)n3 / TILE3_G3 * 20.0;
-                const double cost = std::max(t12, t3) + 150.0;
+                                   stage(n2, TILE3_G12, 2.0 * xaw * P * cw) + SGIGA_TILE3_O12;
+                const double t3 = std::ceil((npos + rows) / (double)TILE3_G3) * SGIGA_TILE3_C3 +
+                                  (double)n3 / TILE3_G3 * 20.0;
+                const double cost = std::max(t12, t3) + SGIGA_TILE3_OVH;
                 const double per_row = cost / rows;
                 if (per_row < best * 0.999) {
                     best = per_row;
