@@ -35,6 +35,7 @@ Options Options::from_env() {
     o.combine_perthread = env_on("SGIGA_COMBINE_PERTHREAD");
     o.asm_profile = env_on("SGIGA_ASM_PROFILE");
     o.asm_pencil = env_on("SGIGA_ASM_PENCIL");
+    o.no_diag_metric = env_on("SGIGA_NO_DIAG");
     o.fd_profile = env_on("SGIGA_FD_PROFILE");
     o.pcg_profile = env_on("SGIGA_PCG_PROFILE");
     o.pcg_trace = env_on("SGIGA_PCG_TRACE");

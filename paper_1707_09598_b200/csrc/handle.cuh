@@ -43,6 +43,7 @@ struct Options {
     bool combine_perthread = false; // SGIGA_COMBINE_PERTHREAD=1: per-thread combine kernel (tests)
     bool asm_profile = false;       // SGIGA_ASM_PROFILE=1: block-0 stage cycles to stderr (probe)
     bool asm_pencil = false;        // SGIGA_ASM_PENCIL=1: one-pencil-per-CTA 3-D assembly (parity tests)
+    bool no_diag_metric = false;    // SGIGA_NO_DIAG=1: general-metric tiled assembly on box geometries (tests)
     bool fd_profile = false;        // SGIGA_FD_PROFILE=1: FD phase cycles to stderr (probe)
     bool pcg_profile = false;       // SGIGA_PCG_PROFILE=1 (probe)
     bool pcg_trace = false;         // SGIGA_PCG_TRACE=1 (probe)
@@ -202,6 +203,7 @@ struct Handle {
     int tiles3_state = 0;                  // 0 = not built, 1 = ready, -1 = not applicable
     size_t tiles3_smem = 0;
     double tiles3_flops = 0.0;             // FP64 operations one tiled-assembly launch executes
+    bool tiles3_dg = false;                // diagonal-metric instantiation (axis-aligned box geometry)
     bool asm_tiled = false;                // the last assembly ran k_assemble_tile
     bool small_checked = false;            // small comps' true residual came from the cluster PCG
 

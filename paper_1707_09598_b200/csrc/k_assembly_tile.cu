@@ -102,23 +102,28 @@ struct TCfg {
 
 // per-CTA shared-memory layout (doubles)
 struct TLay {
-    int sGw, oTa, oTb, oPhiA, oPhiB, oS1, s1slot, oSL1, oS2, s2sz, oRL, oList, total;
+    int est, sGw, oTa, oTb, oPhiA, oPhiB, oS1, s1slot, oSL1, oS2, s2sz, oRL, oList, total;
 };
 
-__host__ __device__ inline TLay tile3_layout(int P, int na, int nb, int xa, int xap, int xb, int n3) {
+// dg: diagonal metric (axis-aligned box geometry): 4 plane entries (G_aa,
+// G_bb, G_ss, load), 3 stage-1 slots, 3 stage-2 units
+__host__ __device__ inline TLay tile3_layout(int P, int na, int nb, int xa, int xap, int xb, int n3, bool dg) {
     const int Q = P, W = 2 * P - 1, RP = (P + 1) & ~1, PQ = P * Q, S1W = (W - ((P - 1) & ~1) + 1) & ~1;
     const int rows = na * nb;
     TLay L;
-    L.sGw = (7 * xb * xap + 15) & ~15;
+    // plane buffer: 7 dense entries (one TMA box) or 4 entries at a 128-byte
+    // aligned stride (four TMA boxes, each destination 128-byte aligned)
+    L.est = dg ? ((xb * xap + 15) & ~15) : xb * xap;
+    L.sGw = ((dg ? 4 : 7) * L.est + 15) & ~15;
     L.oTa = 2 * L.sGw;
     L.oTb = L.oTa + na * 4 * PQ * RP;
     L.oPhiA = L.oTb + nb * 4 * PQ * RP;
     L.oPhiB = L.oPhiA + na * PQ;
     L.oS1 = (L.oPhiB + nb * PQ + 1) & ~1;
     L.s1slot = xa * S1W + 2;
-    L.oSL1 = L.oS1 + nb * 8 * L.s1slot;
+    L.oSL1 = L.oS1 + nb * (dg ? 3 : 8) * L.s1slot;
     L.oS2 = L.oSL1 + nb * xa;
-    L.s2sz = 5 * n3 + rows;                      // [row][unit][c_a][c_b] + load [row]
+    L.s2sz = (dg ? 3 : 5) * n3 + rows;           // [row][unit][c_a][c_b] + load [row]
     L.oRL = L.oS2 + 2 * L.s2sz;
     L.oList = L.oRL + rows * P;                  // stage-3 item list (ints): computed items first
     L.total = L.oList + (n3 + 1) / 2;
@@ -153,13 +158,22 @@ __device__ __constant__ int c_t3_btype[8] = {0, 0, 0, 1, 1, 2, 2, 3};
 __device__ __constant__ int c_t3_uslot[5][2] = {{0, 3}, {5, 7}, {1, 6}, {1, 4}, {2, 2}};
 __device__ __constant__ int c_t3_uat[5][2] = {{3, 2}, {1, 0}, {2, 0}, {1, 0}, {0, 0}};
 
-template <int P>
+// diagonal-metric mode: stage-1 slot -> (plane entry, b-type): aa (0, 0), ss (2, 0), bb (1, 3), load (3);
+// stage-2 units: aa (S1 slot 0, a-type 3), bb (slot 2, a-type 0), ss (slot 1, a-type 0)
+__device__ __constant__ int c_t3d_btype[3] = {0, 0, 3};
+__device__ __constant__ int c_t3d_uslot[3] = {0, 2, 1};
+__device__ __constant__ int c_t3d_uat[3] = {3, 0, 0};
+
+template <int P, bool DG>
 __global__ void __launch_bounds__(TILE3_THREADS, 1)
 k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tabs,
                 const Tile3* __restrict__ tiles, const double* __restrict__ vals,
                 double* __restrict__ stencil, double* __restrict__ rhs, double* __restrict__ dinv,
                 const CUtensorMap* __restrict__ tmaps, long long* __restrict__ prof) {
     using F = TCfg<P>;
+    // general metric: 7 plane entries, 8 stage-1 pair slots + load, 5 stage-2
+    // units; diagonal metric (G_ab = G_as = G_bs = 0 exactly): 4 / 3 + 1 / 3
+    constexpr int NGE = DG ? 4 : 7, NS1 = DG ? 3 : 8, NI1 = NS1 + 1, NU = DG ? 3 : 5;
     constexpr int p = F::p, Q = F::Q, W = F::W, RP = F::RP, PQ = F::PQ, S1W = F::S1W, WBS1 = F::WBS1;
     constexpr int NC2 = F::NC2, G12 = TILE3_G12, NT = TILE3_THREADS;
     extern __shared__ __align__(128) double sm[];
@@ -196,7 +210,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     if (nplanes == 0) return;   // uniform over the CTA
     const int Sa = C.S[ka], Sb = C.S[kb], SAB = Sa * Sb;
     const int n3 = rows * SAB;
-    const TLay L = tile3_layout(P, na, nb, T.xa, T.xap, T.xb, n3);
+    const TLay L = tile3_layout(P, na, nb, T.xa, T.xap, T.xb, n3, DG);
     const int xap = T.xap, xb = T.xb;
     double* Ta = sm + L.oTa;
     double* Tb = sm + L.oTb;
@@ -211,19 +225,32 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const int tsh = (Q & 1) ? ((EA0 * Q) & 1) : 0;
     const int tx0 = EA0 * Q - tsh, tx1 = EB0 * Q;
     const CUtensorMap* tmap = tmaps + T.comp;
-    const uint32_t pbytes = (uint32_t)(F::NG * xb * xap * 8);
+    const uint32_t pbytes = (uint32_t)(NGE * xb * xap * 8);
 
     auto issue_plane = [&](int j) {   // one thread: plane j -> buffer j & 1
         const int b = j & 1;
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(t3_smem_u32(&bar[b])),
                      "r"(pbytes) : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
-            ::"r"(t3_smem_u32(sm + b * L.sGw)), "l"(tmap), "r"(tx0), "r"(tx1), "r"(e_first * Q + j), "r"(0),
-              "r"(t3_smem_u32(&bar[b]))
-            : "memory");
+        if constexpr (!DG) {   // one copy: box (x_a, x_b, 1 plane, 7 entries)
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+                ::"r"(t3_smem_u32(sm + b * L.sGw)), "l"(tmap), "r"(tx0), "r"(tx1), "r"(e_first * Q + j), "r"(0),
+                  "r"(t3_smem_u32(&bar[b]))
+                : "memory");
+        } else {               // four copies of box (x_a, x_b, 1, 1): G_aa, G_bb, G_ss, load
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int ent = k == 0 ? sym_index(3, ka, ka) : (k == 1 ? sym_index(3, kb, kb) : (k == 2 ? sym_index(3, ks, ks) : 6));
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+                    ::"r"(t3_smem_u32(sm + b * L.sGw + k * L.est)), "l"(tmap), "r"(tx0), "r"(tx1),
+                      "r"(e_first * Q + j), "r"(ent), "r"(t3_smem_u32(&bar[b]))
+                    : "memory");
+            }
+        }
     };
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[0])) : "memory");
@@ -232,10 +259,10 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         issue_plane(0);
         if (nplanes > 1) issue_plane(1);
     }
-    if (tid < 8) {   // metric entry of each stage-1 pair slot: aa as ss ab sb ba bs bb
+    if (tid < 8) {   // plane entry of each stage-1 pair slot: aa as ss ab sb ba bs bb
         const int mm = tid == 2 || tid == 4 ? ks : (tid >= 5 ? kb : ka);
         const int nn = tid == 0 || tid == 5 ? ka : (tid == 3 || tid == 4 || tid == 7 ? kb : ks);
-        s_ent[tid] = sym_index(3, mm, nn);
+        s_ent[tid] = DG ? (tid == 0 ? 0 : (tid == 1 ? 2 : 1)) : sym_index(3, mm, nn);   // DG: aa ss bb -> 0 2 1
     }
     if (warp == G12 / 32) {   // first G3 warp: the whole tensor memory (one CTA per SM)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
@@ -313,14 +340,14 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         if (inG3 && i < npos) {
             const int it = s_list[i] & ((1 << 30) - 1);
             const int cb = it % Sb, ca = (it / Sb) % Sa, r = it / SAB;
-            s2off[k] = (r * F::NU) * SAB + ca * Sb + cb;
+            s2off[k] = (r * NU) * SAB + ca * Sb + cb;
         }
     }
     const bool prf = prof != nullptr && blockIdx.x == 0;
     long long gt0 = 0;
     if (prof != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
     long long pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0;
-    const int n1 = nb * 9 * XAv;
+    const int n1 = nb * NI1 * XAv;
     // stage-2 work items (row, unit, column group): an absolute b axis (thin:
     // m_b <= 2p+1) enumerates its storage columns c_b only (w_b = c_b + 1 - i_b + p),
     // a relative one its 2p+1 offsets, one or two per item
@@ -330,7 +357,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     // starts its column groups at the even w_b = p & ~1 for aligned pair loads)
     const int wbs = cw == 2 ? (p & ~1) : p;
     const int ncol2 = absm_b ? Sb : (W - wbs + cw - 1) / cw;
-    const int n2 = rows * F::NU * ncol2;
+    const int n2 = rows * NU * ncol2;
     for (int j = 0; j <= nplanes; ++j) {
         const long long c0 = prf ? clock64() : 0;
         if (!inG3) {
@@ -347,13 +374,13 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 const double* Gw = sm + (j & 1) * L.sGw + tsh;
                 // ---- stage 1: contract b -> S1[ib][slot][xa][w_b], SL1[ib][xa] --
                 for (int it = tid; it < n1; it += G12) {
-                    const int xa = it % XAv, q = it / XAv, sig = q % 9, rb = q / 9;
+                    const int xa = it % XAv, q = it / XAv, sig = q % NI1, rb = q / NI1;
                     const int ib = T.b0 + rb;
                     const int tlo = max(0, p - ib), thi = min(P, nel_b + p - ib);
                     const int xoff = (ib - p - EB0) * Q;   // union row of the row's window point x = 0
-                    if (sig < 8) {
-                        const double* gp = Gw + (s_ent[sig] * xb + xoff) * xap + xa;
-                        const double* tr = Tb + (rb * 4 + c_t3_btype[sig]) * PQ * RP;
+                    if (sig < NS1) {
+                        const double* gp = Gw + s_ent[sig] * L.est + xoff * xap + xa;
+                        const double* tr = Tb + (rb * 4 + (DG ? c_t3d_btype[sig] : c_t3_btype[sig])) * PQ * RP;
                         double acc[W];
 #pragma unroll
                         for (int w = 0; w < W; ++w) acc[w] = 0.0;
@@ -376,12 +403,12 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                     if (t + k >= WBS1) acc[t + k] = fma(gv, tv[k], acc[t + k]);
                             }
                         }
-                        double* o = S1 + (rb * 8 + sig) * L.s1slot + xa * S1W - WBS1;
+                        double* o = S1 + (rb * NS1 + sig) * L.s1slot + xa * S1W - WBS1;
 #pragma unroll
                         for (int w = WBS1; w < W; w += 2)
                             *reinterpret_cast<double2*>(o + w) = make_double2(acc[w], w + 1 < W ? acc[w + 1] : 0.0);
                     } else {
-                        const double* gp = Gw + (6 * xb + xoff) * xap + xa;
+                        const double* gp = Gw + (NGE - 1) * L.est + xoff * xap + xa;
                         const double* ph = phiB + rb * PQ;
                         double acc = 0.0;
 #pragma unroll
@@ -401,7 +428,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     constexpr int CW = decltype(CWc)::value;
                     for (int it = tid; it < n2 + rows; it += G12) {
                         if (it < n2) {
-                            const int cg = it % ncol2, u = (it / ncol2) % F::NU, r = it / (ncol2 * F::NU);
+                            const int cg = it % ncol2, u = (it / ncol2) % NU, r = it / (ncol2 * NU);
                             const int ra = r % na, rb = r / na, ia = T.a0 + ra, ib = T.b0 + rb;
                             const int wb0 = absm_b ? cg + 1 - ib + p : wbs + CW * cg;   // first w_b of the item
                             if (wb0 < 0 || wb0 >= W) continue;   // column outside the band: dead stage-3 items
@@ -413,9 +440,11 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                             for (int w = 0; w < W; ++w) acc0[w] = acc1[w] = 0.0;
 #pragma unroll
                             for (int pr = 0; pr < 2; ++pr) {
-                                if (pr == 1 && u == 4) break;
-                                const double* sp = S1 + (rb * 8 + c_t3_uslot[u][pr]) * L.s1slot + xoff * S1W + (wb0 - WBS1);
-                                const double* ta = Ta + (ra * 4 + c_t3_uat[u][pr]) * PQ * RP;
+                                if (pr == 1 && (DG || u == 4)) break;
+                                const int sl1 = DG ? c_t3d_uslot[u] : c_t3_uslot[u][pr];
+                                const int at = DG ? c_t3d_uat[u] : c_t3_uat[u][pr];
+                                const double* sp = S1 + (rb * NS1 + sl1) * L.s1slot + xoff * S1W + (wb0 - WBS1);
+                                const double* ta = Ta + (ra * 4 + at) * PQ * RP;
 #pragma unroll
                                 for (int t = 0; t < P; ++t) {
                                     if (t < tlo || t >= thi) continue;
@@ -441,7 +470,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                 }
                             }
                             // relative (w_a, w_b) -> storage columns (c_a, c_b)
-                            double* o = S2w + (r * F::NU + u) * SAB;
+                            double* o = S2w + (r * NU + u) * SAB;
 #pragma unroll
                             for (int cc = 0; cc < CW; ++cc) {
                                 const int wb = wb0 + cc;
@@ -465,7 +494,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 #pragma unroll
                                 for (int g = 0; g < Q; ++g) acc = fma(sl[t * Q + g], ph[t * Q + g], acc);
                             }
-                            S2w[5 * n3 + r] = acc;
+                            S2w[NU * n3 + r] = acc;
                         }
                     }
                 };
@@ -513,7 +542,11 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 for (int kk = 1; kk < F::NSLOT; ++kk) s2o = k == kk ? s2off[kk] : s2o;
                 if (s2o >= 0) {   // live item
                     const double* s2p = S2r + s2o;
-                    const double s0 = s2p[0] + s2p[SAB], s1 = s2p[2 * SAB], s2v = s2p[3 * SAB], s3 = s2p[4 * SAB];
+                    // stream types 0 (no s), 1 (m, s), 2 (s, n), 3 (s, s); a diagonal
+                    // metric has no type-1/2 pairs (their sums are exactly zero)
+                    const double s0 = s2p[0] + s2p[SAB];
+                    const double s1 = DG ? 0.0 : s2p[2 * SAB], s2v = DG ? 0.0 : s2p[3 * SAB];
+                    const double s3 = DG ? s2p[2 * SAB] : s2p[4 * SAB];
 #pragma unroll
                     for (int al = 0; al < P; ++al) {
                         const double c0 = fma(vb[al], s0, db[al] * s2v), c1 = fma(vb[al], s1, db[al] * s3);
@@ -600,7 +633,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 if (!item && i < n3r) {   // load ring of row r (shared memory)
                     const int rr = i - npos;
                     double* RL = RLs + rr * P;
-                    const double sl = S2r[5 * n3 + rr];
+                    const double sl = S2r[NU * n3 + rr];
 #pragma unroll
                     for (int al = 0; al < P; ++al) RL[al] = fma(vb[al], sl, RL[al]);
                     if (last_pt) {
@@ -675,6 +708,31 @@ bool tile3_eligible(const Handle* h) {
            !h->opt.asm_pencil && !h->opt.generic_assembly && !h->force_generic_assembly;
 }
 
+// The metric G = det w J^-1 J^-T is diagonal -- G_ab = G_as = G_bs = 0.0
+// exactly as k_metric computes them -- when the geometry is an axis-aligned
+// box: degree 1 on [0, 1] per axis (basis derivatives exactly -1, +1, so the
+// off-diagonal Jacobian sums cancel exactly), unit weights, control point
+// coordinate i a function of index i only.  The tiled kernel then skips the
+// off-diagonal pairs (their contributions are exact zeros: same bits).
+static bool tile3_metric_diagonal(const Handle* h) {
+    if (h->d != 3 || h->opt.no_diag_metric) return false;
+    for (int k = 0; k < 3; ++k) {
+        if (h->geo.deg[k] != 1 || h->geo.n[k] != 2 || h->geo.nk[k] != 4) return false;
+        const double* kv = h->geo_knots.data() + h->geo.knot_off[k];
+        if (!(kv[0] == 0.0 && kv[1] == 0.0 && kv[2] == 1.0 && kv[3] == 1.0)) return false;
+    }
+    auto hw = [&](int a, int b, int c, int comp) { return h->geo_hw[(size_t)((a * 2 + b) * 2 + c) * 4 + comp]; };
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int c = 0; c < 2; ++c) {
+                if (hw(a, b, c, 3) != 1.0) return false;
+                if (hw(a, b, c, 0) != hw(a, 0, 0, 0) || hw(a, b, c, 1) != hw(0, b, 0, 1) ||
+                    hw(a, b, c, 2) != hw(0, 0, c, 2))
+                    return false;
+            }
+    return true;
+}
+
 #ifndef SGIGA_TILE3_C3
 #define SGIGA_TILE3_C3 260.0    // cost model: cycles of one stage-3 item slot per plane
 #endif
@@ -698,6 +756,7 @@ static bool build_tiles3(Handle* h) {
     const int p = h->p, P = p + 1, Q = h->q, W = 2 * p + 1, NC2 = (W + 1) / 2;
     const int NSLOT = tile3_nslot(P);
     const size_t SMEM_CAP = 225 * 1024;
+    const bool dg = tile3_metric_diagonal(h);
     void* fnp = nullptr;
     cudaDriverEntryPointQueryResult qres;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &qres) != cudaSuccess ||
@@ -749,7 +808,7 @@ static bool build_tiles3(Handle* h) {
                 const int xa = std::min(na + p, nel_a) * Q, xb = std::min(nb + p, nel_b) * Q;
                 const int xap = (Q & 1) ? ((xa + 2) & ~1) : ((xa + 1) & ~1);
                 if (xap > 256 || xb > 256) continue;
-                const TLay L = tile3_layout(P, na, nb, xa, xap, xb, n3);
+                const TLay L = tile3_layout(P, na, nb, xa, xap, xb, n3, dg);
                 if ((size_t)L.total * 8 > SMEM_CAP) continue;
                 const double xbw = std::min(P, nel_b) * Q, xaw = std::min(P, nel_a) * Q;
                 // one barrier interval, in cycles: a work item's chain at ~2
@@ -764,8 +823,9 @@ static bool build_tiles3(Handle* h) {
 #endif
                 const int wbs = cw == 2 ? (p & ~1) : p;
                 const double n2 = (double)rows * 5 * (C.absm[kb] ? (Sb + 1) / 2 : (W - wbs + cw - 1) / cw);
-                const double t12 = stage((double)nb * 9 * xa, TILE3_G12, xbw * P) +
-                                   stage(n2, TILE3_G12, 2.0 * xaw * P * cw) + SGIGA_TILE3_O12;
+                const double t12 = stage((double)nb * (dg ? 4 : 9) * xa, TILE3_G12, xbw * P) +
+                                   stage(n2 * (dg ? 0.6 : 1.0), TILE3_G12, (dg ? 1.0 : 2.0) * xaw * P * cw) +
+                                   SGIGA_TILE3_O12;
                 const double t3 = std::ceil((npos + rows) / (double)TILE3_G3) * SGIGA_TILE3_C3 +
                                   (double)n3 / TILE3_G3 * 20.0;
                 const double cost = std::max(t12, t3) + SGIGA_TILE3_OVH;
@@ -782,7 +842,7 @@ static bool build_tiles3(Handle* h) {
         if (C.qs[ka] != 1 || C.qs[kb] != (int64_t)Na || C.qs[ks] != (int64_t)(Na * Nb)) return false;
         const cuuint64_t dims[4] = {Na, Nb, Ns, (cuuint64_t)h->nG()};
         const cuuint64_t strides[3] = {Na * 8, Na * Nb * 8, (cuuint64_t)C.nqp * 8};
-        const cuuint32_t box[4] = {(cuuint32_t)bs.xap, (cuuint32_t)bs.xb, 1, (cuuint32_t)h->nG()};
+        const cuuint32_t box[4] = {(cuuint32_t)bs.xap, (cuuint32_t)bs.xb, 1, dg ? 1u : (cuuint32_t)h->nG()};
         if (strides[0] % 16 || strides[1] % 16 || strides[2] % 16 || (C.qp_off * 8) % 16) return false;
         const cuuint32_t estr[4] = {1, 1, 1, 1};
         if (encode(&maps[c], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)(h->d_G + C.qp_off), dims, strides, box,
@@ -839,7 +899,7 @@ static bool build_tiles3(Handle* h) {
                     t.xa = S.xa; t.xap = S.xap; t.xb = S.xb; t.cw = S.cw;
                     const int ne = std::min(t.r1 - 1, nel_s - 1) - std::max(0, t.r0 - p) + 1;
                     const TLay L = tile3_layout(P, t.na, t.nb, t.xa, t.xap, t.xb,
-                                                t.na * t.nb * C.S[C.ax[1]] * C.S[C.ax[0]]);
+                                                t.na * t.nb * C.S[C.ax[1]] * C.S[C.ax[0]], dg);
                     smem = std::max(smem, (size_t)L.total * 8);
                     tl.push_back(t);
                     tcost.push_back((ne * Q + setup_planes) * S.plane);
@@ -869,7 +929,7 @@ static bool build_tiles3(Handle* h) {
             double fk = 0.0;
             for (int tt = std::max(0, p - ib); tt < std::min(P, nel_b + p - ib); ++tt)
                 fk += Q * (P - std::max(0, (p & ~1) - tt));
-            s1 += XAv * (8.0 * fk + win(ib, nel_b)) * 2.0;
+            s1 += XAv * ((dg ? 3.0 : 8.0) * fk + win(ib, nel_b)) * 2.0;
         }
         const int Sa = C.S[ka], Sb = C.S[kb];
         for (int rb = 0; rb < t.nb; ++rb)
@@ -882,7 +942,7 @@ static bool build_tiles3(Handle* h) {
                     const int wbs = t.cw == 2 ? (p & ~1) : p;
                     ncol = t.cw * ((W - wbs + t.cw - 1) / t.cw);
                 }
-                s2 += (9.0 * ncol * P + 1.0) * win(ia, nel_a) * 2.0;
+                s2 += ((dg ? 3.0 : 9.0) * ncol * P + 1.0) * win(ia, nel_a) * 2.0;
                 for (int ca = 0; ca < Sa; ++ca)
                     for (int cb = 0; cb < Sb; ++cb)
                         if (tile3_category(ia, ib, ca, cb, C.absm[ka], C.absm[kb], C.m[ka], C.m[kb], p) >= T3_POS)
@@ -913,6 +973,7 @@ static bool build_tiles3(Handle* h) {
         return false;
     }
     h->tiles3_smem = smem;
+    h->tiles3_dg = dg;
     h->asm_seg = SEG;
     h->tiles3_state = 1;
     return true;
@@ -923,9 +984,11 @@ static bool build_tiles3(Handle* h) {
 bool launch_assembly_tile(Handle* h, cudaError_t* err) {
     if (!build_tiles3(h)) return false;
     const void* fn = nullptr;
-    switch (h->p + 1) {
-        case 4: fn = (const void*)k_assemble_tile<4>; break;
-        case 5: fn = (const void*)k_assemble_tile<5>; break;
+    switch ((h->p + 1) * 2 + (h->tiles3_dg ? 1 : 0)) {
+        case 8: fn = (const void*)k_assemble_tile<4, false>; break;
+        case 9: fn = (const void*)k_assemble_tile<4, true>; break;
+        case 10: fn = (const void*)k_assemble_tile<5, false>; break;
+        case 11: fn = (const void*)k_assemble_tile<5, true>; break;
         default: return false;
     }
     *err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tiles3_smem);

@@ -165,6 +165,27 @@ def test_tiled_assembly_matches_pencil(name, pick, monkeypatch):
         assert normwise(b1, b2) <= 1e-13
 
 
+@pytest.mark.parametrize("name,pick", [("cfg5", (0, 4, 7, 40, 68, 100, 135))])
+def test_diagonal_metric_tiles_bitwise(name, pick, monkeypatch):
+    """On an axis-aligned box geometry the metric's off-diagonal entries are
+    exact zeros, and the tiled assembly's diagonal-metric instantiation (which
+    skips those pairs) assembles bitwise the stencil of the general one."""
+    cfg = configs.get_config(name)
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    mats = {}
+    for mode in ("diag", "general"):
+        monkeypatch.setenv("SGIGA_NO_DIAG", "1" if mode == "general" else "0")
+        b = Batch(spec)
+        try:
+            b.assemble()
+            mats[mode] = [b.export_csr(c) for c in pick]
+        finally:
+            b.close()
+    for (A1, b1), (A2, b2) in zip(mats["diag"], mats["general"]):
+        assert np.array_equal(A1.indptr, A2.indptr) and np.array_equal(A1.indices, A2.indices)
+        assert np.array_equal(A1.data, A2.data) and np.array_equal(b1, b2)
+
+
 def test_pcg_residual_contract():
     cfg = configs.get_config("cfg2")
     spec, b = _batch(cfg)
