@@ -204,6 +204,7 @@ struct Handle {
     size_t tiles3_smem = 0;
     double tiles3_flops = 0.0;             // FP64 operations one tiled-assembly launch executes
     bool tiles3_dg = false;                // diagonal-metric instantiation (axis-aligned box geometry)
+    bool stencil_zeroed = false;           // the stencil's structural zeros are in place (set once per layout)
     bool asm_tiled = false;                // the last assembly ran k_assemble_tile
     bool small_checked = false;            // small comps' true residual came from the cluster PCG
 

@@ -79,6 +79,49 @@ __device__ __forceinline__ void tm_stn(uint32_t a, const uint32_t* r) {
         asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(a + c), "r"(r[c]), "r"(r[c + 1])
                      : "memory");
 }
+// 8 doubles = 16 TMEM columns of this thread's lane, the 32-bit halves
+// paired inside the asm (no register copies between the TMEM and FP64 views)
+__device__ __forceinline__ void tm_ld_d8(uint32_t a, double* d) {
+    asm volatile("{\n .reg .b32 r<16>;\n"
+                 " tcgen05.ld.sync.aligned.32x32b.x16.b32 {r0, r1, r2, r3, r4, r5, r6, r7, r8, r9, r10, r11, r12, r13, "
+                 "r14, r15}, [%8];\n"
+                 " mov.b64 %0, {r0, r1};\n mov.b64 %1, {r2, r3};\n mov.b64 %2, {r4, r5};\n mov.b64 %3, {r6, r7};\n"
+                 " mov.b64 %4, {r8, r9};\n mov.b64 %5, {r10, r11};\n mov.b64 %6, {r12, r13};\n"
+                 " mov.b64 %7, {r14, r15};\n}\n"
+                 : "=d"(d[0]), "=d"(d[1]), "=d"(d[2]), "=d"(d[3]), "=d"(d[4]), "=d"(d[5]), "=d"(d[6]), "=d"(d[7])
+                 : "r"(a));
+}
+__device__ __forceinline__ void tm_ld_d1(uint32_t a, double& d) {
+    asm volatile("{\n .reg .b32 r<2>;\n tcgen05.ld.sync.aligned.32x32b.x2.b32 {r0, r1}, [%1];\n"
+                 " mov.b64 %0, {r0, r1};\n}\n" : "=d"(d) : "r"(a));
+}
+__device__ __forceinline__ void tm_st_d8(uint32_t a, const double* d) {
+    asm volatile("{\n .reg .b32 r<16>;\n"
+                 " mov.b64 {r0, r1}, %1;\n mov.b64 {r2, r3}, %2;\n mov.b64 {r4, r5}, %3;\n mov.b64 {r6, r7}, %4;\n"
+                 " mov.b64 {r8, r9}, %5;\n mov.b64 {r10, r11}, %6;\n mov.b64 {r12, r13}, %7;\n"
+                 " mov.b64 {r14, r15}, %8;\n"
+                 " tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {r0, r1, r2, r3, r4, r5, r6, r7, r8, r9, r10, r11, r12, "
+                 "r13, r14, r15};\n}\n"
+                 ::"r"(a), "d"(d[0]), "d"(d[1]), "d"(d[2]), "d"(d[3]), "d"(d[4]), "d"(d[5]), "d"(d[6]), "d"(d[7])
+                 : "memory");
+}
+// the element partial R3 (P*P doubles at the slot start)
+template <int P>
+__device__ __forceinline__ void tm_ld_r3(uint32_t a, double (*r3)[P]) {
+    double* d = &r3[0][0];
+#pragma unroll
+    for (int c = 0; c + 8 <= P * P; c += 8) tm_ld_d8(a + 2 * c, d + c);
+#pragma unroll
+    for (int c = (P * P) & ~7; c < P * P; ++c) tm_ld_d1(a + 2 * c, d[c]);
+}
+template <int P>
+__device__ __forceinline__ void tm_st_r3(uint32_t a, double (*r3)[P]) {
+    double* d = &r3[0][0];
+#pragma unroll
+    for (int c = 0; c + 8 <= P * P; c += 8) tm_st_d8(a + 2 * c, d + c);
+#pragma unroll
+    for (int c = (P * P) & ~7; c < P * P; ++c) tm_st2(a + 2 * c, d[c]);
+}
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
@@ -527,15 +570,9 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 // e + al (physical row (e + al) mod P), offsets w = p - al .. 2p - al
                 // (two-level sum: element partials, then elements, as the
                 // reference's element-by-element assembly)
-                uint32_t rr[F::R3C];
-                tm_ldn<F::R3C>(t3, rr);
-                tm_wait_ld();
                 double r3[P][P];
-#pragma unroll
-                for (int al = 0; al < P; ++al)
-#pragma unroll
-                    for (int bl = 0; bl < P; ++bl)
-                        r3[al][bl] = __hiloint2double((int)rr[2 * (al * P + bl) + 1], (int)rr[2 * (al * P + bl)]);
+                tm_ld_r3<P>(t3, r3);
+                tm_wait_ld();
                 const bool item = i < npos;
                 int s2o = s2off[0];   // (register select, no local-memory indexing)
 #pragma unroll
@@ -549,20 +586,14 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     const double s3 = DG ? s2p[2 * SAB] : s2p[4 * SAB];
 #pragma unroll
                     for (int al = 0; al < P; ++al) {
-                        const double c0 = fma(vb[al], s0, db[al] * s2v), c1 = fma(vb[al], s1, db[al] * s3);
+                        const double c0 = DG ? vb[al] * s0 : fma(vb[al], s0, db[al] * s2v);
+                        const double c1 = DG ? db[al] * s3 : fma(vb[al], s1, db[al] * s3);
 #pragma unroll
                         for (int bl = 0; bl < P; ++bl) r3[al][bl] = fma(vb[bl], c0, fma(db[bl], c1, r3[al][bl]));
                     }
                 }
                 if (!last_pt) {
-#pragma unroll
-                    for (int al = 0; al < P; ++al)
-#pragma unroll
-                        for (int bl = 0; bl < P; ++bl) {
-                            rr[2 * (al * P + bl)] = (uint32_t)__double2loint(r3[al][bl]);
-                            rr[2 * (al * P + bl) + 1] = (uint32_t)__double2hiint(r3[al][bl]);
-                        }
-                    tm_stn<F::R3C>(t3, rr);
+                    tm_st_r3<P>(t3, r3);
                 } else {   // window row by row (registers): ring += R3, R3 = 0
 #pragma unroll
                     for (int al = 0; al < P; ++al) {
@@ -609,10 +640,11 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                 const int jc = irow + w - p;
                                 const bool inr = jc >= 1 && jc <= m_s;
                                 const double v = __hiloint2double((int)rh[w], (int)rl[w]);
-                                // own entry (the (0,0) column's o_s < 0 entries are its twins' mirrors)
-                                if (!(absm_s && !inr) && !(pos0 && w < p && inr)) {
+                                // own entry (the (0,0) column's o_s < 0 entries are its twins'
+                                // mirrors; structural zeros are in place: stencil_zeroed)
+                                if (inr && !(pos0 && w < p)) {
                                     const int cs = absm_s ? jc - 1 : w;
-                                    dst[((int64_t)cs * ss_s + slotab) * rows_c] = inr ? v : 0.0;
+                                    dst[((int64_t)cs * ss_s + slotab) * rows_c] = v;
                                 }
                                 // mirrored entry A(twin, this row)
                                 if (inr && !(pos0 && w <= p)) {
@@ -621,9 +653,6 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                             ((int64_t)csM * ss_s + slotabM) * rows_c] = v;
                                 }
                             }
-                            if (absm_s)
-                                for (int cs = 0; cs < S_s; ++cs)
-                                    if (abs(cs + 1 - irow) > p) dst[((int64_t)cs * ss_s + slotab) * rows_c] = 0.0;
                             if (pos0) dinv[C.vec_off + row] = 1.0 / __hiloint2double((int)rh[p], (int)rl[p]);
                         }
 #pragma unroll
@@ -645,28 +674,6 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
 #pragma unroll
                             for (int al = 0; al < p; ++al) RL[al] = RL[al + 1];
                             RL[p] = 0.0;
-                        }
-                    }
-                }
-            }
-            if (last_pt) {   // NEG / DEAD columns of the flushed rows: their structural zeros
-                for (int f = 0; f < nfl; ++f) {
-                    const int irow = e + f;
-                    if (irow < r0 || irow >= r1) continue;
-                    for (int q = npos + g3t; q < n3; q += TILE3_G3) {
-                        const int le = s_list[q];
-                        const bool dead = (le >> 30) & 1;
-                        const int it = le & ((1 << 30) - 1);
-                        const int cb = it % Sb, ca = (it / Sb) % Sa, r = it / SAB;
-                        const int ia = T.a0 + r % na, ib = T.b0 + r / na;
-                        const int64_t row = (int64_t)(ia - 1) * C.rs[ka] + (int64_t)(ib - 1) * C.rs[kb] +
-                                            (int64_t)(irow - 1) * rs_s;
-                        double* dst = stencil + C.mat_off + row;
-                        const int64_t slotab = (int64_t)ca * C.ss[ka] + (int64_t)cb * C.ss[kb];
-                        for (int cs = 0; cs < S_s; ++cs) {
-                            const int jc = absm_s ? cs + 1 : irow + cs - p;
-                            const bool band = jc >= 1 && jc <= m_s && abs(jc - irow) <= p;
-                            if (dead || !band) dst[((int64_t)cs * ss_s + slotab) * rows_c] = 0.0;
                         }
                     }
                 }
@@ -993,6 +1000,14 @@ bool launch_assembly_tile(Handle* h, cudaError_t* err) {
     }
     *err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tiles3_smem);
     if (*err != cudaSuccess) return true;
+    // the kernel writes only the band's live entries: the structural zeros of
+    // the stencil (columns outside the band or on the boundary) are set once
+    // per layout (the buffer is rewritten by every pass, the zeros never change)
+    if (!h->stencil_zeroed) {
+        *err = cudaMemsetAsync(h->d_stencil, 0, sizeof(double) * (size_t)h->total_slots, h->stream);
+        if (*err != cudaSuccess) return true;
+        h->stencil_zeroed = true;
+    }
     long long* prof = nullptr;
     const size_t nprof = 8 + 3 * h->tiles3.size();
     if (h->opt.asm_profile) {
