@@ -516,6 +516,7 @@ static int upload_all(Handle* h) {
     h->tmaps_state = 0;   // tensor maps follow the component table
     h->tiles3_state = 0;
     h->stencil_zeroed = false;
+    h->metric_offdiag_zeroed = false;
     if (!h->mcomp.empty())
         SG_CUDA(cudaMemcpyAsync(h->d_mcomp, h->mcomp.data(), sizeof(int) * h->mcomp.size(), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(h->d_comps, h->comps.data(), sizeof(CompInfo) * h->comps.size(), cudaMemcpyHostToDevice, s));

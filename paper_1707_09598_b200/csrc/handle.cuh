@@ -205,6 +205,7 @@ struct Handle {
     double tiles3_flops = 0.0;             // FP64 operations one tiled-assembly launch executes
     bool tiles3_dg = false;                // diagonal-metric instantiation (axis-aligned box geometry)
     bool stencil_zeroed = false;           // the stencil's structural zeros are in place (set once per layout)
+    bool metric_offdiag_zeroed = false;    // the metric's exactly-zero off-diagonal entries are in place (box geometry)
     bool asm_tiled = false;                // the last assembly ran k_assemble_tile
     bool small_checked = false;            // small comps' true residual came from the cluster PCG
 
@@ -257,6 +258,8 @@ struct Handle {
 // maximal regularity, q = p + 1, degree 3 or 4); the per-component choice
 // is CompInfo::tile3 (components with at least TILE3_MIN_ELEMENTS elements)
 bool tile3_eligible(const Handle* h);
+// axis-aligned box geometry: the metric's off-diagonal entries are exact zeros
+bool metric_diagonal(const Handle* h);
 constexpr double TILE3_MIN_ELEMENTS = 512.0;
 
 // symmetric index of (m, n) in the packed metric (row-major upper triangle)

@@ -721,7 +721,7 @@ bool tile3_eligible(const Handle* h) {
 // off-diagonal Jacobian sums cancel exactly), unit weights, control point
 // coordinate i a function of index i only.  The tiled kernel then skips the
 // off-diagonal pairs (their contributions are exact zeros: same bits).
-static bool tile3_metric_diagonal(const Handle* h) {
+bool metric_diagonal(const Handle* h) {
     if (h->d != 3 || h->opt.no_diag_metric) return false;
     for (int k = 0; k < 3; ++k) {
         if (h->geo.deg[k] != 1 || h->geo.n[k] != 2 || h->geo.nk[k] != 4) return false;
@@ -763,7 +763,7 @@ static bool build_tiles3(Handle* h) {
     const int p = h->p, P = p + 1, Q = h->q, W = 2 * p + 1, NC2 = (W + 1) / 2;
     const int NSLOT = tile3_nslot(P);
     const size_t SMEM_CAP = 225 * 1024;
-    const bool dg = tile3_metric_diagonal(h);
+    const bool dg = metric_diagonal(h);
     void* fnp = nullptr;
     cudaDriverEntryPointQueryResult qres;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &qres) != cudaSuccess ||

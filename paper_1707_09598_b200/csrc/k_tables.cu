@@ -67,7 +67,7 @@ __global__ void k_basis_tables(const TabInfo* __restrict__ tabs, int ntab,
 // loops); the homogeneous control net is staged in shared memory when it
 // fits (nsh > 0 doubles).  Same operations in the same order for every GP:
 // the metric does not depend on the instantiation.
-template <int D, int GP>
+template <int D, int GP, bool DG>
 __global__ void __launch_bounds__(256, 2)
 k_metric(const CompInfo* __restrict__ comps, int ncomp,
                          const int64_t* __restrict__ qp_cum, const TabInfo* __restrict__ tabs,
@@ -256,7 +256,9 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
     for (int m = 0; m < D; ++m)
 #pragma unroll
         for (int i = 0; i < D; ++i)   // quotient rule, geometry.py:126
-            J[i][m] = __dmul_rn(__dsub_rn(dh[m][i], __dmul_rn(x[i], dh[m][D])), invW);
+            // diagonal metric (axis-aligned box, DG): the off-diagonal terms are
+            // exact zeros in the general evaluation too -- same diagonal bits
+            J[i][m] = (DG && i != m) ? 0.0 : __dmul_rn(__dsub_rn(dh[m][i], __dmul_rn(x[i], dh[m][D])), invW);
     double det, Ji[D][D];
     if constexpr (D == 1) {
         det = J[0][0];
@@ -295,6 +297,7 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
     for (int m = 0; m < D; ++m)
 #pragma unroll
         for (int n = m; n < D; ++n) {    // (Jinv Jinv^T) * (det * w), assembly.py:288-289
+            if (DG && n != m) continue;   // exact zeros, set once per layout
             double s = 0.0;
 #pragma unroll
             for (int i = 0; i < D; ++i) s = __dadd_rn(s, __dmul_rn(Ji[m][i], Ji[n][i]));
@@ -342,8 +345,20 @@ cudaError_t launch_metric(Handle* h) {
     if (gp > (h->d == 3 ? 3 : 4)) gp = 0;   // (3-D, degree 3: register spills -- runtime loops)
     const int nsh = h->geo_hw.size() <= 3072 ? (int)h->geo_hw.size() : 0;
     const size_t shb = sizeof(double) * (size_t)nsh;
+    // axis-aligned box geometry (3-D): the off-diagonal metric entries are
+    // exact zeros -- written once per layout, the pass writes the diagonal
+    const bool dg = h->d == 3 && metric_diagonal(h);
+    if (dg && !h->metric_offdiag_zeroed) {
+        cudaError_t e0 = cudaMemsetAsync(h->d_G, 0, sizeof(double) * (size_t)h->nG() * h->total_qp, h->stream);
+        if (e0 != cudaSuccess) return e0;
+        h->metric_offdiag_zeroed = true;
+    }
 #define LAUNCH_METRIC(DD, GG)                                                                 \
-    k_metric<DD, GG><<<(unsigned)blocks, 256, shb, h->stream>>>(                              \
+    if (dg && DD == 3) k_metric<DD, GG, true><<<(unsigned)blocks, 256, shb, h->stream>>>(     \
+        h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->d_geob,    \
+        h->d_geofirst, h->d_geo, h->d_geo_hw, h->q, h->forcing_id, hostf, h->d_xphys, h->d_G, \
+        h->d_err, h->d_mcomp, nsh);                                                          \
+    else k_metric<DD, GG, false><<<(unsigned)blocks, 256, shb, h->stream>>>(                   \
         h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->d_geob,    \
         h->d_geofirst, h->d_geo, h->d_geo_hw, h->q, h->forcing_id, hostf, h->d_xphys, h->d_G, \
         h->d_err, h->d_mcomp, nsh)
