@@ -122,6 +122,12 @@ __device__ __forceinline__ void tm_st_r3(uint32_t a, double (*r3)[P]) {
 #pragma unroll
     for (int c = (P * P) & ~7; c < P * P; ++c) tm_st2(a + 2 * c, d[c]);
 }
+// stencil store that asks L2 to keep the line (the 8-byte entries of one
+// 32-byte sector arrive over four stream rows; an early eviction of the
+// partial sector costs a DRAM read-modify-write)
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
@@ -366,6 +372,8 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const int64_t rs_s = C.rs[ks], ss_s = C.ss[ks], rows_c = C.rows;
     const int absm_s = C.absm[ks], m_s = C.m[ks], S_s = C.S[ks];
     const int64_t nq_s = (int64_t)nel_s * Q;
+    uint64_t l2keep;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(l2keep));
     if (inG3) {   // rings start at zero
         for (int k = 0; k < nslot; ++k)
 #pragma unroll
@@ -644,13 +652,13 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                 // mirrors; structural zeros are in place: stencil_zeroed)
                                 if (inr && !(pos0 && w < p)) {
                                     const int cs = absm_s ? jc - 1 : w;
-                                    dst[((int64_t)cs * ss_s + slotab) * rows_c] = v;
+                                    st_keep(dst + ((int64_t)cs * ss_s + slotab) * rows_c, v, l2keep);
                                 }
                                 // mirrored entry A(twin, this row)
                                 if (inr && !(pos0 && w <= p)) {
                                     const int csM = absm_s ? irow - 1 : 2 * p - w;
-                                    stencil[C.mat_off + rowbaseM + (int64_t)(jc - 1) * rs_s +
-                                            ((int64_t)csM * ss_s + slotabM) * rows_c] = v;
+                                    st_keep(stencil + C.mat_off + rowbaseM + (int64_t)(jc - 1) * rs_s +
+                                                ((int64_t)csM * ss_s + slotabM) * rows_c, v, l2keep);
                                 }
                             }
                             if (pos0) dinv[C.vec_off + row] = 1.0 / __hiloint2double((int)rh[p], (int)rl[p]);
