@@ -128,6 +128,15 @@ __device__ __forceinline__ void tm_st_r3(uint32_t a, double (*r3)[P]) {
 __device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(t3_smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile("{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, q;\n}\n" : "=r"(ok) : "r"(t3_smem_u32(b)), "r"(parity) : "memory");
+}
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
@@ -227,6 +236,10 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     constexpr int NC2 = F::NC2, G12 = TILE3_G12, NT = TILE3_THREADS;
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bar[2];
+    // S2 hand-off between the groups: full[b] (G12 wrote plane buffer b),
+    // empty[b] (G3 consumed it) -- no CTA-wide barrier per plane, so a slow
+    // stage-3 plane (an element's flush) does not stall stages 1/2
+    __shared__ __align__(8) uint64_t s2full[2], s2empty[2];
     __shared__ int s_ent[8];
     __shared__ uint32_t s_tmem;
     // the tile, its component and tables staged in shared memory: values the
@@ -304,6 +317,11 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[0])) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[1])) : "memory");
+        for (int b = 0; b < 2; ++b) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(t3_smem_u32(&s2full[b])), "r"(G12) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(t3_smem_u32(&s2empty[b])), "r"(TILE3_G3)
+                         : "memory");
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         issue_plane(0);
         if (nplanes > 1) issue_plane(1);
@@ -409,10 +427,10 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const int wbs = cw == 2 ? (p & ~1) : p;
     const int ncol2 = absm_b ? Sb : (W - wbs + cw - 1) / cw;
     const int n2 = rows * NU * ncol2;
-    for (int j = 0; j <= nplanes; ++j) {
-        const long long c0 = prf ? clock64() : 0;
-        if (!inG3) {
-            if (j < nplanes) {
+    if (!inG3) {
+        for (int j = 0; j < nplanes; ++j) {
+            const long long c0 = prf ? clock64() : 0;
+            {
                 // ---- wait for plane j ----------------------------------------
                 {
                     const uint32_t par = (uint32_t)((j >> 1) & 1);
@@ -474,6 +492,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 asm volatile("bar.sync 1, %0;\n" ::"r"(G12) : "memory");
                 if (tid == 0 && j + 2 < nplanes) issue_plane(j + 2);   // buffer j & 1 is free now
                 // ---- stage 2: contract a -> S2[row][unit][c_a][c_b], S2L[row] -----
+                if (j >= 2) mb_wait(&s2empty[j & 1], (uint32_t)(((j >> 1) - 1) & 1));   // stage 3 done with plane j-2
                 double* S2w = S2 + (j & 1) * L.s2sz;
                 auto stage2 = [&](auto CWc) {
                     constexpr int CW = decltype(CWc)::value;
@@ -551,10 +570,17 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 };
                 if (cw == 2) stage2(std::integral_constant<int, 2>{});
                 else stage2(std::integral_constant<int, 1>{});
+                mb_arrive(&s2full[j & 1]);                            // plane j's S2 is written
+                asm volatile("bar.sync 1, %0;\n" ::"r"(G12) : "memory");   // S1 read: stage 1 of j+1 may write it
             }
-        } else if (j >= 1) {
-            // ---- stage 3 (plane jj = j - 1): stream axis, rank-1 updates ---------
-            const int jj = j - 1, el = jj / Q, g = jj - el * Q, e = e_first + el;
+            if (prf && tid == 0) { pc0 += clock64() - c0; pc3 += 1; }
+        }
+    } else {
+        for (int jj = 0; jj < nplanes; ++jj) {
+            const long long c0 = prf ? clock64() : 0;
+            mb_wait(&s2full[jj & 1], (uint32_t)((jj >> 1) & 1));
+            // ---- stage 3 (plane jj): stream axis, rank-1 updates ---------------------
+            const int el = jj / Q, g = jj - el * Q, e = e_first + el;
             const double* S2r = S2 + (jj & 1) * L.s2sz;
             double vb[P], db[P];
             {
@@ -686,16 +712,12 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     }
                 }
             }
-            tm_wait_st();   // this interval's rings are in TMEM before the next interval loads them
-        }
-        const long long c1 = prf ? clock64() : 0;
-        __syncthreads();
-        if (prf) {
-            const long long c2 = clock64();
-            if (tid == 0) { pc0 += c1 - c0; pc1 += c2 - c1; }
-            if (tid == G12) { pc2 += c1 - c0; pc3 += 1; }
+            tm_wait_st();   // this plane's rings are in TMEM before the next plane loads them
+            mb_arrive(&s2empty[jj & 1]);                              // plane jj's S2 is consumed
+            if (prf && tid == G12) pc2 += clock64() - c0;
         }
     }
+    __syncthreads();
     if (prf) {
         if (tid == 0) { prof[0] = pc0; prof[1] = pc1; }
         if (tid == G12) { prof[2] = pc2; prof[3] = pc3; }
