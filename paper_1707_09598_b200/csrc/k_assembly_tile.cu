@@ -36,6 +36,11 @@
 
 namespace sgiga {
 
+#ifndef SGIGA_TILE3_NS2
+#define SGIGA_TILE3_NS2 4
+#endif
+constexpr int TILE3_NS2 = SGIGA_TILE3_NS2;   // S2 buffers between the stage-2 and stage-3 warps
+
 namespace {
 
 __device__ __forceinline__ uint32_t t3_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -182,7 +187,7 @@ __host__ __device__ inline TLay tile3_layout(int P, int na, int nb, int xa, int 
     L.oSL1 = L.oS1 + nb * (dg ? 3 : 8) * L.s1slot;
     L.oS2 = L.oSL1 + nb * xa;
     L.s2sz = (dg ? 3 : 5) * n3 + rows;           // [row][unit][c_a][c_b] + load [row]
-    L.oRL = L.oS2 + 2 * L.s2sz;
+    L.oRL = L.oS2 + TILE3_NS2 * L.s2sz;
     L.oList = L.oRL + rows * P;                  // stage-3 item list (ints): computed items first
     L.total = L.oList + (n3 + 1) / 2;
     return L;
@@ -239,7 +244,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     // S2 hand-off between the groups: full[b] (G12 wrote plane buffer b),
     // empty[b] (G3 consumed it) -- no CTA-wide barrier per plane, so a slow
     // stage-3 plane (an element's flush) does not stall stages 1/2
-    __shared__ __align__(8) uint64_t s2full[2], s2empty[2];
+    __shared__ __align__(8) uint64_t s2full[TILE3_NS2], s2empty[TILE3_NS2];
     __shared__ int s_ent[8];
     __shared__ uint32_t s_tmem;
     // the tile, its component and tables staged in shared memory: values the
@@ -317,7 +322,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[0])) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[1])) : "memory");
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < TILE3_NS2; ++b) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(t3_smem_u32(&s2full[b])), "r"(G12) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(t3_smem_u32(&s2empty[b])), "r"(TILE3_G3)
                          : "memory");
@@ -492,8 +497,9 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 asm volatile("bar.sync 1, %0;\n" ::"r"(G12) : "memory");
                 if (tid == 0 && j + 2 < nplanes) issue_plane(j + 2);   // buffer j & 1 is free now
                 // ---- stage 2: contract a -> S2[row][unit][c_a][c_b], S2L[row] -----
-                if (j >= 2) mb_wait(&s2empty[j & 1], (uint32_t)(((j >> 1) - 1) & 1));   // stage 3 done with plane j-2
-                double* S2w = S2 + (j & 1) * L.s2sz;
+                const int jb = j % TILE3_NS2, ju = j / TILE3_NS2;   // S2 buffer and its use count
+                if (ju >= 1) mb_wait(&s2empty[jb], (uint32_t)((ju - 1) & 1));   // stage 3 done with plane j - NS2
+                double* S2w = S2 + jb * L.s2sz;
                 auto stage2 = [&](auto CWc) {
                     constexpr int CW = decltype(CWc)::value;
                     for (int it = tid; it < n2 + rows; it += G12) {
@@ -570,7 +576,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 };
                 if (cw == 2) stage2(std::integral_constant<int, 2>{});
                 else stage2(std::integral_constant<int, 1>{});
-                mb_arrive(&s2full[j & 1]);                            // plane j's S2 is written
+                mb_arrive(&s2full[jb]);                               // plane j's S2 is written
                 asm volatile("bar.sync 1, %0;\n" ::"r"(G12) : "memory");   // S1 read: stage 1 of j+1 may write it
             }
             if (prf && tid == 0) { pc0 += clock64() - c0; pc3 += 1; }
@@ -578,10 +584,11 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     } else {
         for (int jj = 0; jj < nplanes; ++jj) {
             const long long c0 = prf ? clock64() : 0;
-            mb_wait(&s2full[jj & 1], (uint32_t)((jj >> 1) & 1));
+            const int jb = jj % TILE3_NS2;
+            mb_wait(&s2full[jb], (uint32_t)((jj / TILE3_NS2) & 1));
             // ---- stage 3 (plane jj): stream axis, rank-1 updates ---------------------
             const int el = jj / Q, g = jj - el * Q, e = e_first + el;
-            const double* S2r = S2 + (jj & 1) * L.s2sz;
+            const double* S2r = S2 + jb * L.s2sz;
             double vb[P], db[P];
             {
                 const double* bp = vals + TS.val_off + ((int64_t)e * Q + g) * P;
@@ -713,7 +720,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 }
             }
             tm_wait_st();   // this plane's rings are in TMEM before the next plane loads them
-            mb_arrive(&s2empty[jj & 1]);                              // plane jj's S2 is consumed
+            mb_arrive(&s2empty[jb]);                                  // plane jj's S2 is consumed
             if (prf && tid == G12) pc2 += clock64() - c0;
         }
     }
