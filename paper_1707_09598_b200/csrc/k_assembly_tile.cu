@@ -39,6 +39,10 @@ namespace sgiga {
 #ifndef SGIGA_TILE3_NS2
 #define SGIGA_TILE3_NS2 4
 #endif
+#ifndef SGIGA_TILE3_NPB
+#define SGIGA_TILE3_NPB 2
+#endif
+constexpr int TILE3_NPB = SGIGA_TILE3_NPB;   // TMA plane buffers (prefetch distance NPB)
 constexpr int TILE3_NS2 = SGIGA_TILE3_NS2;   // S2 buffers between the stage-2 and stage-3 warps
 
 namespace {
@@ -178,7 +182,7 @@ __host__ __device__ inline TLay tile3_layout(int P, int na, int nb, int xa, int 
     // aligned stride (four TMA boxes, each destination 128-byte aligned)
     L.est = dg ? ((xb * xap + 15) & ~15) : xb * xap;
     L.sGw = ((dg ? 4 : 7) * L.est + 15) & ~15;
-    L.oTa = 2 * L.sGw;
+    L.oTa = TILE3_NPB * L.sGw;
     L.oTb = L.oTa + na * 4 * PQ * RP;
     L.oPhiA = L.oTb + nb * 4 * PQ * RP;
     L.oPhiB = L.oPhiA + na * PQ;
@@ -240,7 +244,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     constexpr int p = F::p, Q = F::Q, W = F::W, RP = F::RP, PQ = F::PQ, S1W = F::S1W, WBS1 = F::WBS1;
     constexpr int NC2 = F::NC2, G12 = TILE3_G12, NT = TILE3_THREADS;
     extern __shared__ __align__(128) double sm[];
-    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(8) uint64_t bar[TILE3_NPB];
     // S2 hand-off between the groups: full[b] (G12 wrote plane buffer b),
     // empty[b] (G3 consumed it) -- no CTA-wide barrier per plane, so a slow
     // stage-3 plane (an element's flush) does not stall stages 1/2
@@ -294,8 +298,8 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     const CUtensorMap* tmap = tmaps + T.comp;
     const uint32_t pbytes = (uint32_t)(NGE * xb * xap * 8);
 
-    auto issue_plane = [&](int j) {   // one thread: plane j -> buffer j & 1
-        const int b = j & 1;
+    auto issue_plane = [&](int j) {   // one thread: plane j -> buffer j % NPB
+        const int b = j % TILE3_NPB;
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(t3_smem_u32(&bar[b])),
                      "r"(pbytes) : "memory");
@@ -320,16 +324,15 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
         }
     };
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[0])) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[1])) : "memory");
+        for (int b = 0; b < TILE3_NPB; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(t3_smem_u32(&bar[b])) : "memory");
         for (int b = 0; b < TILE3_NS2; ++b) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(t3_smem_u32(&s2full[b])), "r"(G12) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(t3_smem_u32(&s2empty[b])), "r"(TILE3_G3)
                          : "memory");
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        issue_plane(0);
-        if (nplanes > 1) issue_plane(1);
+        for (int jj = 0; jj < TILE3_NPB && jj < nplanes; ++jj) issue_plane(jj);
     }
     if (tid < 8) {   // plane entry of each stage-1 pair slot: aa as ss ab sb ba bs bb
         const int mm = tid == 2 || tid == 4 ? ks : (tid >= 5 ? kb : ka);
@@ -438,14 +441,14 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
             {
                 // ---- wait for plane j ----------------------------------------
                 {
-                    const uint32_t par = (uint32_t)((j >> 1) & 1);
-                    const uint32_t ba = t3_smem_u32(&bar[j & 1]);
+                    const uint32_t par = (uint32_t)((j / TILE3_NPB) & 1);
+                    const uint32_t ba = t3_smem_u32(&bar[j % TILE3_NPB]);
                     uint32_t ok = 0;
                     while (!ok)
                         asm volatile("{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
                                      " selp.u32 %0, 1, 0, q;\n}\n" : "=r"(ok) : "r"(ba), "r"(par) : "memory");
                 }
-                const double* Gw = sm + (j & 1) * L.sGw + tsh;
+                const double* Gw = sm + (j % TILE3_NPB) * L.sGw + tsh;
                 // ---- stage 1: contract b -> S1[ib][slot][xa][w_b], SL1[ib][xa] --
                 for (int it = tid; it < n1; it += G12) {
                     const int xa = it % XAv, q = it / XAv, sig = q % NI1, rb = q / NI1;
@@ -495,7 +498,7 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                     }
                 }
                 asm volatile("bar.sync 1, %0;\n" ::"r"(G12) : "memory");
-                if (tid == 0 && j + 2 < nplanes) issue_plane(j + 2);   // buffer j & 1 is free now
+                if (tid == 0 && j + TILE3_NPB < nplanes) issue_plane(j + TILE3_NPB);   // buffer j % NPB is free now
                 // ---- stage 2: contract a -> S2[row][unit][c_a][c_b], S2L[row] -----
                 const int jb = j % TILE3_NS2, ju = j / TILE3_NS2;   // S2 buffer and its use count
                 if (ju >= 1) mb_wait(&s2empty[jb], (uint32_t)((ju - 1) & 1));   // stage 3 done with plane j - NS2
