@@ -11,8 +11,9 @@ from paper_1707_09598_b200.pipeline import Batch  # noqa: E402
 from paper_1707_09598_b200.scheduler import make_spec  # noqa: E402
 
 name = sys.argv[1]
+R = int(sys.argv[2]) if len(sys.argv) > 2 else 1   # replicated batch (R copies of the plan)
 cfg = configs.get_config(name)
-b = Batch(make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points))
+b = Batch(make_spec(tuple(cfg.plan.terms) * R, cfg.problem, cfg.quad_points))
 ts = []
 for _ in range(3):
     b.assemble()
@@ -20,4 +21,4 @@ for _ in range(3):
     b.lib.sgiga_kernel_times(b.h, kt.ctypes.data_as(ct.POINTER(ct.c_float)))
     ts.append(kt[2])
 b.close()
-print(f"{name} pencil={os.environ.get('SGIGA_ASM_PENCIL', '0')}: assembly {min(ts):.3f} ms (metric {kt[1]:.3f})")
+print(f"{name} x{R} pencil={os.environ.get('SGIGA_ASM_PENCIL', '0')}: assembly {min(ts):.3f} ms (metric {kt[1]:.3f})")

@@ -44,12 +44,22 @@ struct Asm2Cfg {
     static constexpr int F = 4;                     // stream rows per flush
     static constexpr int RING = F + P;              // alive stream rows
     static constexpr int NG = 4;                    // G_00, G_01, G_11, load
-    static constexpr int NQ = Q <= 2 ? 2 : (Q <= 4 ? 4 : 8);   // lines per stage-2 item group (power of two)
+#ifndef SGIGA_A2_NQ
+#define SGIGA_A2_NQ 0
+#endif
+#ifndef SGIGA_A2_DISJ
+#define SGIGA_A2_DISJ 0
+#endif
+    // lanes per stage-2 item (power of two; each lane sums lines g = lane mod NQ)
+    // (cfg3 x1024, Q = 4: NQ 4 / 2 / 1 = 5.64 / 5.07 / 5.59 ms; cfg1 x1024, Q = 3: 0.46 / 0.42 / 0.40 ms)
+    static constexpr int NQ = SGIGA_A2_NQ > 0 ? SGIGA_A2_NQ : (Q <= 3 ? 1 : 2);
+    static constexpr bool DISJ = SGIGA_A2_DISJ;     // stage-1 and stage-2 items on disjoint threads
     static constexpr int N1 = NEA * P * 4;          // stage-1 items (e_a, la, t)
     static constexpr int N1L = NEA * P;             // stage-1 load items (e_a, la)
     static constexpr int N2 = BA * W * NQ;          // stage-2 items (i_a, o_a, line)
     static constexpr int N2L = BA;                  // stage-2 load items (i_a)
-    static constexpr int NT = 32 * (((N1 + N1L > N2 + N2L ? N1 + N1L : N2 + N2L) + 31) / 32);
+    static constexpr int NT = DISJ ? 32 * ((N1 + N1L + N2 + N2L + 31) / 32)
+                                   : 32 * (((N1 + N1L > N2 + N2L ? N1 + N1L : N2 + N2L) + 31) / 32);
     // shared memory (doubles)
     static constexpr int sGe = Q * NXA + 2;         // one entry's Q lines (+2: bank skew between entries)
     static constexpr int sB = 2 * Q * P;            // stream basis values + derivatives of the element
@@ -59,8 +69,11 @@ struct Asm2Cfg {
     // element k-1's (its stream basis tables feed stage 2 in interval k)
     static constexpr int NGB = 4;
     static constexpr int oG = 0;                    // [NGB][NG][Q][NXA] + [2][Q][P]
-    static constexpr int nS1 = Q * 4 * BA * W * P;
-    static constexpr int oS1 = oG + NGB * sG;       // [2][Q][4][BA][W][P]
+    // one line's S1 block, padded by 16 bytes: the stage-2 reads of the NQ
+    // lines of an item group then fall on different banks
+    static constexpr int S1G = 4 * BA * W * P + 2;
+    static constexpr int nS1 = Q * S1G;
+    static constexpr int oS1 = oG + NGB * sG;       // [2][Q][S1G = [4][BA][W][P] + 2]
     static constexpr int nSL = Q * BA * P;
     static constexpr int oSL = oS1 + 2 * nS1;       // [2][Q][BA][P]
     static constexpr int oAcc = oSL + 2 * nSL;      // [RING][BA][W][W]
@@ -190,10 +203,11 @@ k_assemble2d(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tab
     const int s1_gent = s1_t == 0 ? g_ss : (s1_t == 3 ? g_aa : g_as);
 
     // ---- stage-2 item (every thread one): (tile row, offset, line) ---------
-    const int s2_ia = tid < F::N2 ? tid / (NQ * W) : tid - F::N2;   // local tile row (full row bk.ia0 + s2_ia)
-    const int s2_oi = (tid / NQ) % W, s2_g = tid % NQ;              // offset index o_a + p, line
-    const bool s2_on = tid < F::N2 && s2_ia < na && s2_g < Q;
-    const bool s2_load = tid >= F::N2 && tid < F::N2 + F::N2L && s2_ia < na;
+    const int j2 = F::DISJ ? tid - (F::N1 + F::N1L) : tid;
+    const int s2_ia = j2 < F::N2 ? j2 / (NQ * W) : j2 - F::N2;      // local tile row (full row bk.ia0 + s2_ia)
+    const int s2_oi = (j2 / NQ) % W, s2_g = j2 % NQ;                // offset index o_a + p, first line
+    const bool s2_on = j2 >= 0 && j2 < F::N2 && s2_ia < na && s2_g < Q;
+    const bool s2_load = j2 >= F::N2 && j2 < F::N2 + F::N2L && s2_ia < na;
     double R[P][P], RL[P];
 #pragma unroll
     for (int a = 0; a < P; ++a) {
@@ -232,7 +246,7 @@ k_assemble2d(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tab
 #pragma unroll
                         for (int lb = 0; lb < P; ++lb) acc[lb] = fma(gv, T[ga][lb], acc[lb]);
                     }
-                    double* o = out + g * 4 * BA * W * P;
+                    double* o = out + g * F::S1G;
 #pragma unroll
                     for (int lb = 0; lb < P; ++lb) o[lb * P] = acc[lb];   // offset o_a = lb - la
                 }
@@ -255,12 +269,15 @@ k_assemble2d(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tab
             const double* SLr = sm + F::oSL + ((k - 1) & 1) * F::nSL;
             const double* Bv = sm + F::oG + ((k - 1) % F::NGB) * F::sG + F::NG * F::sGe;   // [Q][P] values
             const double* Bd = Bv + Q * P;                                                  // derivatives
-            if (s2_on) {   // line s2_g of the element: S_t = sum_la S1, then the P x P block
-                const int g = s2_g;
+            if (s2_on) {   // lines g = s2_g (mod NQ) of the element: S_t = sum_la S1, then the P x P block
+#pragma unroll
+              for (int gi = 0; gi < (Q + NQ - 1) / NQ; ++gi) {
+                const int g = s2_g + gi * NQ;
+                if (NQ * ((Q + NQ - 1) / NQ) != Q && g >= Q) break;
                 double S[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
-                    const double* src = S1r + ((g * 4 + t) * BA + s2_ia) * W * P + s2_oi * P;
+                    const double* src = S1r + g * F::S1G + (t * BA + s2_ia) * W * P + s2_oi * P;
                     if constexpr (P % 2 == 0) {
                         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
@@ -289,8 +306,10 @@ k_assemble2d(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ tab
                     const double c0 = db[ls] * S[1] + vb[ls] * S[3];   // x V(ms)
                     const double c1 = db[ls] * S[0] + vb[ls] * S[2];   // x D(ms)
 #pragma unroll
-                    for (int ms = 0; ms < P; ++ms) R[ls][ms] = fma(c0, vb[ms], c1 * db[ms]);
+                    for (int ms = 0; ms < P; ++ms)
+                        R[ls][ms] = gi == 0 ? fma(c0, vb[ms], c1 * db[ms]) : R[ls][ms] + fma(c0, vb[ms], c1 * db[ms]);
                 }
+              }
             } else if (s2_load) {
 #pragma unroll
                 for (int g = 0; g < Q; ++g) {

@@ -67,8 +67,14 @@ __global__ void k_basis_tables(const TabInfo* __restrict__ tabs, int ntab,
 // loops); the homogeneous control net is staged in shared memory when it
 // fits (nsh > 0 doubles).  Same operations in the same order for every GP:
 // the metric does not depend on the instantiation.
+// resident CTAs per SM: as many as the registers allow without (or with a
+// negligible) spill -- the kernel is latency-bound (global loads, divisions);
+// cfg5 (D 3, degree-1 box, diagonal metric): 2 CTAs 1.74 ms, 3 1.32, 4 1.23
+constexpr int metric_minb(int D, int GP, bool DG) {
+    return D < 3 ? ((D == 2 && GP == 4 && !DG) ? 3 : 4) : (GP == 2 ? (DG ? 4 : 3) : 2);
+}
 template <int D, int GP, bool DG>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, metric_minb(D, GP, DG))
 k_metric(const CompInfo* __restrict__ comps, int ncomp,
                          const int64_t* __restrict__ qp_cum, const TabInfo* __restrict__ tabs,
                          const double* __restrict__ qx, const double* __restrict__ qw,
