@@ -693,7 +693,7 @@ int sgiga_create(const sgiga_problem_desc* desc, void* stream, sgiga_handle** ou
     A_(d_p, h->total_vec);
     A_(d_q, h->total_vec);
     A_(d_q2, h->total_vec);
-    A_(d_coef, h->total_dofs);
+    A_(d_coef, h->total_dofs + 2);   // +2: the combine's 16-byte row loads may read past the end
     A_(d_cg, h->ncomp);
     A_(d_part, 3 * h->chunks.size());
     A_(d_err, 1);

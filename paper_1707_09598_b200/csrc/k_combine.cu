@@ -38,7 +38,28 @@ __device__ __forceinline__ int axis_basis(const TabInfo& T, const double* __rest
     return span - p;
 }
 
-template <int D, int P, bool GRAD>
+// the P contiguous coefficients at row[0..P) by ceil((P+1)/2) aligned 16-byte
+// loads (the coefficient buffer is padded by 2 doubles past its end)
+template <int P>
+__device__ __forceinline__ void load_row_v(const double* row, double* c) {
+    constexpr int NV = (P + 2) / 2;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(row);
+    const bool odd = (a & 8) != 0;
+    const double2* r2 = reinterpret_cast<const double2*>(a & ~(uintptr_t)15);
+    double w[2 * NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const double2 v = __ldg(r2 + i);
+        w[2 * i] = v.x;
+        w[2 * i + 1] = v.y;
+    }
+#pragma unroll
+    for (int l = 0; l < P; ++l) c[l] = odd ? w[l + 1] : w[l];
+}
+
+// VEC: coefficient rows by 16-byte loads (coef must be the padded d_coef);
+// same values, same operations
+template <int D, int P, bool GRAD, bool VEC = false>
 __device__ __forceinline__ void eval_component(const CompInfo& C, const double* __restrict__ coef,
                                                const int* first, const double (*Bv)[P],
                                                const double (*Bd)[P], double& v, double* g) {
@@ -60,9 +81,11 @@ __device__ __forceinline__ void eval_component(const CompInfo& C, const double* 
         for (int a = 0; a < P; ++a) {
             const double* row = cf + (int64_t)(first[0] + a) * n1 + first[1];
             double tv = 0.0, td = 0.0;
+            double cr[P];
+            if constexpr (VEC) load_row_v<P>(row, cr);
 #pragma unroll
             for (int b = 0; b < P; ++b) {
-                double c = __ldg(row + b);
+                double c = VEC ? cr[b] : __ldg(row + b);
                 tv += Bv[1][b] * c;
                 if (GRAD) td += Bd[1][b] * c;
             }
@@ -81,9 +104,11 @@ __device__ __forceinline__ void eval_component(const CompInfo& C, const double* 
             for (int b = 0; b < P; ++b) {
                 const double* row = cf + ((int64_t)(first[0] + a) * n1 + (first[1] + b)) * n2 + first[2];
                 double tv = 0.0, td = 0.0;
+                double cr[P];
+                if constexpr (VEC) load_row_v<P>(row, cr);
 #pragma unroll
                 for (int l = 0; l < P; ++l) {
-                    double c = __ldg(row + l);
+                    double c = VEC ? cr[l] : __ldg(row + l);
                     tv += Bv[2][l] * c;
                     if (GRAD) td += Bd[2][l] * c;
                 }
@@ -263,7 +288,7 @@ k_combine_points_tiled(const CompInfo* __restrict__ comps, int ncomp, const TabI
             for (int j = 0; j < P; ++j) Bv[k][j] = Bt[(t * P + j) * npt + pt];
         }
         double v, g[D];
-        eval_component<D, P, false>(C, coef, fs, Bv, Bv, v, g);
+        eval_component<D, P, false, true>(C, coef, fs, Bv, Bv, v, g);
         if (per_component) out[(int64_t)c * npts + gidx[pt]] = v;
         else V[c * npt + pt] = v;
     }
