@@ -37,12 +37,16 @@
 namespace sgiga {
 
 #ifndef SGIGA_TILE3_NS2
-#define SGIGA_TILE3_NS2 4
+#define SGIGA_TILE3_NS2 3
 #endif
 #ifndef SGIGA_TILE3_NPB
 #define SGIGA_TILE3_NPB 2
 #endif
 constexpr int TILE3_NPB = SGIGA_TILE3_NPB;   // TMA plane buffers (prefetch distance NPB)
+#ifndef SGIGA_TILE3_NS1
+#define SGIGA_TILE3_NS1 2
+#endif
+constexpr int TILE3_NS1 = SGIGA_TILE3_NS1;   // stage-1 output buffers (2: one G12 barrier per plane)
 constexpr int TILE3_NS2 = SGIGA_TILE3_NS2;   // S2 buffers between the stage-2 and stage-3 warps
 
 namespace {
@@ -188,8 +192,8 @@ __host__ __device__ inline TLay tile3_layout(int P, int na, int nb, int xa, int 
     L.oPhiB = L.oPhiA + na * PQ;
     L.oS1 = (L.oPhiB + nb * PQ + 1) & ~1;
     L.s1slot = xa * S1W + 2;
-    L.oSL1 = L.oS1 + nb * (dg ? 3 : 8) * L.s1slot;
-    L.oS2 = L.oSL1 + nb * xa;
+    L.oSL1 = L.oS1 + TILE3_NS1 * nb * (dg ? 3 : 8) * L.s1slot;   // TILE3_NS1 stage-1 buffers
+    L.oS2 = (L.oSL1 + TILE3_NS1 * nb * xa + 1) & ~1;
     L.s2sz = (dg ? 3 : 5) * n3 + rows;           // [row][unit][c_a][c_b] + load [row]
     L.oRL = L.oS2 + TILE3_NS2 * L.s2sz;
     L.oList = L.oRL + rows * P;                  // stage-3 item list (ints): computed items first
@@ -287,8 +291,10 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
     double* Tb = sm + L.oTb;
     double* phiA = sm + L.oPhiA;
     double* phiB = sm + L.oPhiB;
-    double* S1 = sm + L.oS1;
-    double* SL1 = sm + L.oSL1;
+    double* const S1b = sm + L.oS1;
+    double* const SL1b = sm + L.oSL1;
+    double* S1 = S1b;
+    double* SL1 = SL1b;
     double* S2 = sm + L.oS2;
     double* RLs = sm + L.oRL;
     // odd Q: the box's inner start must be 16-byte aligned -- an odd window
@@ -449,6 +455,10 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                                      " selp.u32 %0, 1, 0, q;\n}\n" : "=r"(ok) : "r"(ba), "r"(par) : "memory");
                 }
                 const double* Gw = sm + (j % TILE3_NPB) * L.sGw + tsh;
+                if constexpr (TILE3_NS1 > 1) {   // plane j's stage-1 buffer
+                    S1 = S1b + (j % TILE3_NS1) * (nb * NS1 * L.s1slot);
+                    SL1 = SL1b + (j % TILE3_NS1) * (nb * T.xa);
+                }
                 // ---- stage 1: contract b -> S1[ib][slot][xa][w_b], SL1[ib][xa] --
                 for (int it = tid; it < n1; it += G12) {
                     const int xa = it % XAv, q = it / XAv, sig = q % NI1, rb = q / NI1;
@@ -580,7 +590,9 @@ k_assemble_tile(const CompInfo* __restrict__ comps, const TabInfo* __restrict__ 
                 if (cw == 2) stage2(std::integral_constant<int, 2>{});
                 else stage2(std::integral_constant<int, 1>{});
                 mb_arrive(&s2full[jb]);                               // plane j's S2 is written
-                asm volatile("bar.sync 1, %0;\n" ::"r"(G12) : "memory");   // S1 read: stage 1 of j+1 may write it
+                // S1 read: stage 1 of j+1 may write it (two S1 buffers: the
+                // barrier after stage 1 of j+1 orders it before plane j+2's writes)
+                if constexpr (TILE3_NS1 == 1) asm volatile("bar.sync 1, %0;\n" ::"r"(G12) : "memory");
             }
             if (prf && tid == 0) { pc0 += clock64() - c0; pc3 += 1; }
         }
