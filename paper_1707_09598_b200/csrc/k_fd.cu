@@ -29,6 +29,11 @@
 
 namespace sgiga {
 
+#ifndef SGIGA_FDL_UNR
+#define SGIGA_FDL_UNR 16
+#endif
+constexpr int FDL_UNR = SGIGA_FDL_UNR;   // line-FD SpMV: stencil loads in flight per thread (even)
+
 constexpr int FD_THREADS = 512;
 constexpr int EIG_THREADS = 512;
 constexpr int EIG_ITEMS = ((FD_MMAX / 2) * (FD_MMAX / 2) + (FD_MMAX / 2) * FD_MMAX + EIG_THREADS - 1) / EIG_THREADS;
@@ -1156,12 +1161,12 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
             const int rb = fd_row_base(C, D, row);
             double y0 = 0.0, y1 = 0.0;
             int tt = 0;
-            for (; tt + 7 < NS; tt += 8) {   // 8 independent stencil loads in flight
-                double vv[8];
+            for (; tt + FDL_UNR - 1 < NS; tt += FDL_UNR) {   // FDL_UNR independent stencil loads in flight
+                double vv[FDL_UNR];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) vv[u] = __ldg(val + (size_t)(tt + u) * R + row);
+                for (int u = 0; u < FDL_UNR; ++u) vv[u] = __ldg(val + (size_t)(tt + u) * R + row);
 #pragma unroll
-                for (int u = 0; u < 8; u += 2) {
+                for (int u = 0; u < FDL_UNR; u += 2) {
                     y0 += vv[u] * v[rb + offs[tt + u]];
                     y1 += vv[u + 1] * v[rb + offs[tt + u + 1]];
                 }
