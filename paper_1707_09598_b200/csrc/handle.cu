@@ -36,6 +36,7 @@ Options Options::from_env() {
     o.asm_profile = env_on("SGIGA_ASM_PROFILE");
     o.asm_pencil = env_on("SGIGA_ASM_PENCIL");
     o.no_diag_metric = env_on("SGIGA_NO_DIAG");
+    o.no_box_metric = env_on("SGIGA_NO_BOX_METRIC");
     o.fd_profile = env_on("SGIGA_FD_PROFILE");
     o.pcg_profile = env_on("SGIGA_PCG_PROFILE");
     o.pcg_trace = env_on("SGIGA_PCG_TRACE");

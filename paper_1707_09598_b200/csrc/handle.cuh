@@ -43,6 +43,7 @@ struct Options {
     bool combine_perthread = false; // SGIGA_COMBINE_PERTHREAD=1: per-thread combine kernel (tests)
     bool asm_profile = false;       // SGIGA_ASM_PROFILE=1: block-0 stage cycles to stderr (probe)
     bool asm_pencil = false;        // SGIGA_ASM_PENCIL=1: one-pencil-per-CTA 3-D assembly (parity tests)
+    bool no_box_metric = false;     // SGIGA_NO_BOX_METRIC=1: box geometries through the general contraction (k_metric; tests)
     bool no_diag_metric = false;    // SGIGA_NO_DIAG=1: general-metric tiled assembly on box geometries (tests)
     bool fd_profile = false;        // SGIGA_FD_PROFILE=1: FD phase cycles to stderr (probe)
     bool pcg_profile = false;       // SGIGA_PCG_PROFILE=1 (probe)

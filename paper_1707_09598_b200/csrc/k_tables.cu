@@ -322,6 +322,63 @@ k_metric(const CompInfo* __restrict__ comps, int ncomp,
     Gc[(int64_t)(D * (D + 1) / 2) * nqp + lin] = __dmul_rn(__dmul_rn(f, det), w);
 }
 
+// ---- metric + load of an axis-aligned box (metric_diagonal) ---------------
+// The map is x_k = c0_k + L_k xi_k per axis, so J = diag(L), det = L0 L1 L2
+// and G_kk = det / L_k^2 * w are closed forms (geometry.py:114-132 and
+// assembly.py:286-294 evaluated symbolically for this patch class): per point
+// only the weight product w = w0 w1 w2 (assembly.py:186-190, same order) and
+// the forcing remain.  g[k] = det / L_k^2 and det are per-patch constants
+// folded on the host; the off-diagonal entries are the exact zeros set once
+// per layout.  Rounding-level differences from the general contraction
+// (k_metric), which SGIGA_NO_BOX_METRIC keeps.  Write-bound: 4 doubles per
+// quadrature point.
+__global__ void __launch_bounds__(256) k_metric_box(
+    const CompInfo* __restrict__ comps, int ncomp, const int64_t* __restrict__ qp_cum,
+    const TabInfo* __restrict__ tabs, const double* __restrict__ qx, const double* __restrict__ qw,
+    int q, int forcing_id, const double* __restrict__ hostf, double* __restrict__ xphys,
+    double* __restrict__ Gout, int* __restrict__ err, const int* __restrict__ cta_comp, double3 c0,
+    double3 L, double3 g, double det) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid == 0 && !(det > 0.0)) atomicOr(err, ERRF_GEOMETRY);   // geometry.py:128-131
+    if (gid >= qp_cum[ncomp]) return;
+    int lo = cta_comp[blockIdx.x];
+    if (gid >= qp_cum[lo + 1]) {
+        int l2 = lo, h2 = ncomp;
+        while (h2 - l2 > 1) {
+            int mid = (l2 + h2) >> 1;
+            if (qp_cum[mid] <= gid) l2 = mid; else h2 = mid;
+        }
+        lo = l2;
+    }
+    const CompInfo& C = comps[lo];
+    const unsigned lin = (unsigned)(gid - qp_cum[lo]);
+    double w = 1.0, x[3];
+    const double c0k[3] = {c0.x, c0.y, c0.z}, Lk[3] = {L.x, L.y, L.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const unsigned Qa = (lin / (unsigned)C.qs[k]) % ((unsigned)C.nel[k] * (unsigned)q);
+        const int64_t t = tabs[C.tab[k]].qp_off + Qa;
+        const double wk = qw[t];
+        w = (k == 0) ? wk : __dmul_rn(w, wk);
+        x[k] = __fma_rn(Lk[k], qx[t], c0k[k]);
+    }
+    const int64_t nqp = C.nqp;
+    double* Gc = Gout + C.qp_off;
+    Gc[(int64_t)sym_index(3, 0, 0) * nqp + lin] = __dmul_rn(g.x, w);
+    Gc[(int64_t)sym_index(3, 1, 1) * nqp + lin] = __dmul_rn(g.y, w);
+    Gc[(int64_t)sym_index(3, 2, 2) * nqp + lin] = __dmul_rn(g.z, w);
+    double f;
+    if (forcing_id == SGIGA_FORCING_HOST) {
+        f = hostf ? hostf[gid] : 0.0;
+        if (xphys)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) xphys[gid * 3 + i] = x[i];
+    } else {
+        f = forcing_value<3>(forcing_id, x);
+    }
+    Gc[(int64_t)6 * nqp + lin] = __dmul_rn(__dmul_rn(f, det), w);
+}
+
 // tab_qp_cum / qp_cum live right after d_gauss (see handle.cu)
 extern int64_t* tab_qp_cum_ptr(Handle* h);
 extern int64_t* comp_qp_cum_ptr(Handle* h);
@@ -359,7 +416,25 @@ cudaError_t launch_metric(Handle* h) {
         if (e0 != cudaSuccess) return e0;
         h->metric_offdiag_zeroed = true;
     }
-#define LAUNCH_METRIC(DD, GG)                                                                 \
+    if (dg && !h->opt.no_box_metric) {
+        // control points: coordinate k of corner (a, b, c) depends on index k only
+        auto hw = [&](int a, int b, int c, int comp) { return h->geo_hw[(size_t)((a * 2 + b) * 2 + c) * 4 + comp]; };
+        const double c0[3] = {hw(0, 0, 0, 0), hw(0, 0, 0, 1), hw(0, 0, 0, 2)};
+        const double L[3] = {hw(1, 0, 0, 0) - c0[0], hw(0, 1, 0, 1) - c0[1], hw(0, 0, 1, 2) - c0[2]};
+        const double det = L[0] * (L[1] * L[2]);
+        double g[3];
+        for (int k = 0; k < 3; ++k) {
+            const double il = 1.0 / L[k];
+            g[k] = (il * il) * det;
+        }
+        k_metric_box<<<(unsigned)blocks, 256, 0, h->stream>>>(
+            h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->q, h->forcing_id,
+            hostf, h->d_xphys, h->d_G, h->d_err, h->d_mcomp, make_double3(c0[0], c0[1], c0[2]),
+            make_double3(L[0], L[1], L[2]), make_double3(g[0], g[1], g[2]), det);
+        h->launches[0]++;
+        return cudaGetLastError();
+    }
+#define LAUNCH_METRIC(DD, GG)                                                                \
     if (dg && DD == 3) k_metric<DD, GG, true><<<(unsigned)blocks, 256, shb, h->stream>>>(     \
         h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->d_geob,    \
         h->d_geofirst, h->d_geo, h->d_geo_hw, h->q, h->forcing_id, hostf, h->d_xphys, h->d_G, \

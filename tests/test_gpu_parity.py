@@ -173,6 +173,9 @@ def test_diagonal_metric_tiles_bitwise(name, pick, monkeypatch):
     cfg = configs.get_config(name)
     spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
     mats = {}
+    # the general contraction on both sides (the closed-form box metric is
+    # checked separately: test_box_metric_matches_general_contraction)
+    monkeypatch.setenv("SGIGA_NO_BOX_METRIC", "1")
     for mode in ("diag", "general"):
         monkeypatch.setenv("SGIGA_NO_DIAG", "1" if mode == "general" else "0")
         b = Batch(spec)
@@ -184,6 +187,29 @@ def test_diagonal_metric_tiles_bitwise(name, pick, monkeypatch):
     for (A1, b1), (A2, b2) in zip(mats["diag"], mats["general"]):
         assert np.array_equal(A1.indptr, A2.indptr) and np.array_equal(A1.indices, A2.indices)
         assert np.array_equal(A1.data, A2.data) and np.array_equal(b1, b2)
+
+
+@pytest.mark.parametrize("name,pick", [("cfg5", (0, 4, 7, 40, 68, 100, 135)), ("cfg2", (0, 5, 17, 30))])
+def test_box_metric_matches_general_contraction(name, pick, monkeypatch):
+    """Axis-aligned box: k_metric_box's closed-form metric (J = diag(L),
+    G_kk = det / L_k^2 * w) assembles the systems of the general geometry
+    contraction (geometry.py:114-132, assembly.py:286-294) to rounding level;
+    same sparsity pattern."""
+    cfg = configs.get_config(name)
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    mats = {}
+    for mode in ("box", "contraction"):
+        monkeypatch.setenv("SGIGA_NO_BOX_METRIC", "1" if mode == "contraction" else "0")
+        b = Batch(spec)
+        try:
+            b.assemble()
+            mats[mode] = [b.export_csr(c) for c in pick]
+        finally:
+            b.close()
+    for (A1, b1), (A2, b2) in zip(mats["box"], mats["contraction"]):
+        assert np.array_equal(A1.indptr, A2.indptr) and np.array_equal(A1.indices, A2.indices)
+        assert normwise(A1.data, A2.data) <= 1e-14
+        assert normwise(b1, b2) <= 1e-14
 
 
 def test_pcg_residual_contract():
