@@ -37,6 +37,7 @@ Options Options::from_env() {
     o.asm_pencil = env_on("SGIGA_ASM_PENCIL");
     o.no_diag_metric = env_on("SGIGA_NO_DIAG");
     o.no_box_metric = env_on("SGIGA_NO_BOX_METRIC");
+    o.no_box_asm = env_on("SGIGA_NO_BOX_ASM");
     o.fd_profile = env_on("SGIGA_FD_PROFILE");
     o.pcg_profile = env_on("SGIGA_PCG_PROFILE");
     o.pcg_trace = env_on("SGIGA_PCG_TRACE");
@@ -72,6 +73,7 @@ static void free_all(Handle* h) {
                     h->d_tiles3, h->d_tmaps3};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    free_box(h);
     void* hptrs[] = {h->h_pinned_flag, h->h_err, h->h_cg, h->h_rel, h->h_sticky};
     for (void* p : hptrs)
         if (p) cudaFreeHost(p);
@@ -516,6 +518,7 @@ static int upload_all(Handle* h) {
     cudaStream_t s = h->stream;
     h->tmaps_state = 0;   // tensor maps follow the component table
     h->tiles3_state = 0;
+    free_box(h);
     h->stencil_zeroed = false;
     h->metric_offdiag_zeroed = false;
     if (!h->mcomp.empty())

@@ -43,6 +43,7 @@ struct Options {
     bool combine_perthread = false; // SGIGA_COMBINE_PERTHREAD=1: per-thread combine kernel (tests)
     bool asm_profile = false;       // SGIGA_ASM_PROFILE=1: block-0 stage cycles to stderr (probe)
     bool asm_pencil = false;        // SGIGA_ASM_PENCIL=1: one-pencil-per-CTA 3-D assembly (parity tests)
+    bool no_box_asm = false;        // SGIGA_NO_BOX_ASM=1: box geometries through the tiled / pencil assembly (tests)
     bool no_box_metric = false;     // SGIGA_NO_BOX_METRIC=1: box geometries through the general contraction (k_metric; tests)
     bool no_diag_metric = false;    // SGIGA_NO_DIAG=1: general-metric tiled assembly on box geometries (tests)
     bool fd_profile = false;        // SGIGA_FD_PROFILE=1: FD phase cycles to stderr (probe)
@@ -205,6 +206,16 @@ struct Handle {
     size_t tiles3_smem = 0;
     double tiles3_flops = 0.0;             // FP64 operations one tiled-assembly launch executes
     bool tiles3_dg = false;                // diagonal-metric instantiation (axis-aligned box geometry)
+    // Kronecker assembly of box geometries (k_assembly_box.cu)
+    int box_state = 0;                     // 0 = not built, 1 = ready, -1 = not applicable
+    double* d_box1d = nullptr;             // 1-D mass / stiffness bands per knot vector
+    int64_t* d_box_tcum = nullptr;         // band offsets (entries) per knot vector
+    void* d_box_stage = nullptr;           // load sum-factorisation stages (3 per component)
+    void* d_box_work = nullptr;            // their CTA work lists
+    double* d_box_x1 = nullptr;            // stage buffers
+    double* d_box_x2 = nullptr;
+    int box_nwork[3] = {0, 0, 0};
+    int64_t box_tab_total = 0;
     bool stencil_zeroed = false;           // the stencil's structural zeros are in place (set once per layout)
     bool metric_offdiag_zeroed = false;    // the metric's exactly-zero off-diagonal entries are in place (box geometry)
     bool asm_tiled = false;                // the last assembly ran k_assemble_tile
@@ -261,6 +272,10 @@ struct Handle {
 bool tile3_eligible(const Handle* h);
 // axis-aligned box geometry: the metric's off-diagonal entries are exact zeros
 bool metric_diagonal(const Handle* h);
+// box geometry constants: corner c0, edge lengths L, g_k = det / L_k^2, det
+void box_constants(const Handle* h, double* c0, double* L, double* g, double* det);
+bool box_assembly_eligible(const Handle* h);
+void free_box(Handle* h);
 constexpr double TILE3_MIN_ELEMENTS = 512.0;
 
 // symmetric index of (m, n) in the packed metric (row-major upper triangle)

@@ -301,6 +301,7 @@ size_t assembly_smem_bytes(const Handle* h) {
 bool launch_assembly_fast(Handle* h, cudaError_t* err, int npencils);
 bool launch_assembly_2d(Handle* h, cudaError_t* err);
 bool launch_assembly_tile(Handle* h, cudaError_t* err);
+bool launch_assembly_box(Handle* h, cudaError_t* err);
 
 cudaError_t launch_assembly(Handle* h) {
     int np = (int)h->pencils.size();
@@ -309,6 +310,8 @@ cudaError_t launch_assembly(Handle* h) {
     if (!h->force_generic_assembly && launch_assembly_2d(h, &fe))     // 2-D blocks, q = p+1
         return fe == cudaSuccess ? cudaGetLastError() : fe;
     h->asm_tiled = false;
+    if (launch_assembly_box(h, &fe))   // axis-aligned box: Kronecker stiffness + factorised load
+        return fe == cudaSuccess ? cudaGetLastError() : fe;
     if (!h->force_generic_assembly && launch_assembly_tile(h, &fe)) {   // 3-D tiles, q = p+1, p = 3, 4
         h->asm_tiled = true;
         if (fe != cudaSuccess) return fe;

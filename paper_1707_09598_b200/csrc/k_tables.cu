@@ -379,6 +379,18 @@ __global__ void __launch_bounds__(256) k_metric_box(
     Gc[(int64_t)6 * nqp + lin] = __dmul_rn(__dmul_rn(f, det), w);
 }
 
+void box_constants(const Handle* h, double* c0, double* L, double* g, double* det) {
+    // control points: coordinate k of corner (a, b, c) depends on index k only
+    auto hw = [&](int a, int b, int c, int comp) { return h->geo_hw[(size_t)((a * 2 + b) * 2 + c) * 4 + comp]; };
+    c0[0] = hw(0, 0, 0, 0); c0[1] = hw(0, 0, 0, 1); c0[2] = hw(0, 0, 0, 2);
+    L[0] = hw(1, 0, 0, 0) - c0[0]; L[1] = hw(0, 1, 0, 1) - c0[1]; L[2] = hw(0, 0, 1, 2) - c0[2];
+    *det = L[0] * (L[1] * L[2]);
+    for (int k = 0; k < 3; ++k) {
+        const double il = 1.0 / L[k];
+        g[k] = (il * il) * *det;
+    }
+}
+
 // tab_qp_cum / qp_cum live right after d_gauss (see handle.cu)
 extern int64_t* tab_qp_cum_ptr(Handle* h);
 extern int64_t* comp_qp_cum_ptr(Handle* h);
@@ -417,16 +429,8 @@ cudaError_t launch_metric(Handle* h) {
         h->metric_offdiag_zeroed = true;
     }
     if (dg && !h->opt.no_box_metric) {
-        // control points: coordinate k of corner (a, b, c) depends on index k only
-        auto hw = [&](int a, int b, int c, int comp) { return h->geo_hw[(size_t)((a * 2 + b) * 2 + c) * 4 + comp]; };
-        const double c0[3] = {hw(0, 0, 0, 0), hw(0, 0, 0, 1), hw(0, 0, 0, 2)};
-        const double L[3] = {hw(1, 0, 0, 0) - c0[0], hw(0, 1, 0, 1) - c0[1], hw(0, 0, 1, 2) - c0[2]};
-        const double det = L[0] * (L[1] * L[2]);
-        double g[3];
-        for (int k = 0; k < 3; ++k) {
-            const double il = 1.0 / L[k];
-            g[k] = (il * il) * det;
-        }
+        double c0[3], L[3], g[3], det;
+        box_constants(h, c0, L, g, &det);
         k_metric_box<<<(unsigned)blocks, 256, 0, h->stream>>>(
             h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->q, h->forcing_id,
             hostf, h->d_xphys, h->d_G, h->d_err, h->d_mcomp, make_double3(c0[0], c0[1], c0[2]),

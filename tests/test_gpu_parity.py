@@ -151,6 +151,7 @@ def test_tiled_assembly_matches_pencil(name, pick, monkeypatch):
     cfg = configs.get_config(name)
     spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
     mats = {}
+    monkeypatch.setenv("SGIGA_NO_BOX_ASM", "1")   # the tiled kernel, not the box path
     for mode in ("tile", "pencil"):
         monkeypatch.setenv("SGIGA_ASM_PENCIL", "1" if mode == "pencil" else "0")
         b = Batch(spec)
@@ -176,6 +177,7 @@ def test_diagonal_metric_tiles_bitwise(name, pick, monkeypatch):
     # the general contraction on both sides (the closed-form box metric is
     # checked separately: test_box_metric_matches_general_contraction)
     monkeypatch.setenv("SGIGA_NO_BOX_METRIC", "1")
+    monkeypatch.setenv("SGIGA_NO_BOX_ASM", "1")
     for mode in ("diag", "general"):
         monkeypatch.setenv("SGIGA_NO_DIAG", "1" if mode == "general" else "0")
         b = Batch(spec)
@@ -198,6 +200,7 @@ def test_box_metric_matches_general_contraction(name, pick, monkeypatch):
     cfg = configs.get_config(name)
     spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
     mats = {}
+    monkeypatch.setenv("SGIGA_NO_BOX_ASM", "1")   # same (tiled / pencil) assembly on both sides
     for mode in ("box", "contraction"):
         monkeypatch.setenv("SGIGA_NO_BOX_METRIC", "1" if mode == "contraction" else "0")
         b = Batch(spec)
@@ -210,6 +213,34 @@ def test_box_metric_matches_general_contraction(name, pick, monkeypatch):
         assert np.array_equal(A1.indptr, A2.indptr) and np.array_equal(A1.indices, A2.indices)
         assert normwise(A1.data, A2.data) <= 1e-14
         assert normwise(b1, b2) <= 1e-14
+
+
+@pytest.mark.parametrize("name,pick", [("cfg5", (0, 4, 7, 40, 68, 100, 135)), ("cfg2", (0, 5, 17, 30))])
+def test_box_kronecker_assembly_matches_tiled(name, pick, monkeypatch):
+    """Axis-aligned box: the Kronecker stiffness + factorised load
+    (k_assembly_box.cu) assembles the systems of the quadrature-point kernels
+    (tiled / pencil, SGIGA_NO_BOX_ASM) to rounding level, with the same
+    sparsity pattern; its stiffness is exactly symmetric."""
+    cfg = configs.get_config(name)
+    spec = make_spec(tuple(cfg.plan.terms), cfg.problem, cfg.quad_points)
+    mats = {}
+    for mode in ("box", "tiled"):
+        monkeypatch.setenv("SGIGA_NO_BOX_ASM", "1" if mode == "tiled" else "0")
+        b = Batch(spec)
+        try:
+            b.assemble()
+            mats[mode] = [b.export_csr(c) for c in pick]
+        finally:
+            b.close()
+    for (A1, b1), (A2, b2) in zip(mats["box"], mats["tiled"]):
+        assert np.array_equal(A1.indptr, A2.indptr) and np.array_equal(A1.indices, A2.indices)
+        assert normwise(A1.data, A2.data) <= 1e-13
+        assert normwise(b1, b2) <= 1e-13
+        At = A1.T.tocsr()
+        At.sort_indices()
+        A1s = A1.copy()
+        A1s.sort_indices()
+        assert np.array_equal(At.indices, A1s.indices) and np.array_equal(At.data, A1s.data)
 
 
 def test_pcg_residual_contract():
