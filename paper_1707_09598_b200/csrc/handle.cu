@@ -900,10 +900,17 @@ static int assemble_enqueue(Handle* h) {
         SG_CUDA(launch_fd_eigen(h, h->stream2));
         h->fd_pending = true;
     }
+    // Kronecker box assembly: c_k is a closed form and the line factors need
+    // only kernel 1's tables -- the whole FD set-up runs beside the metric
+    const bool fd_early = h->fd_pending && box_assembly_ready(h);
+    if (fd_early) {
+        SG_CUDA(launch_fd_setup(h, h->stream2));
+        SG_CUDA(cudaEventRecord(h->fd_join, h->stream2));
+    }
     h->kstart(1);
     SG_CUDA(launch_metric(h));
     h->kstop(1);
-    if (h->fd_pending) {   // c_k and the line factors need the metric: side stream again
+    if (h->fd_pending && !fd_early) {   // c_k and the line factors need the metric: side stream again
         SG_CUDA(cudaEventRecord(h->fd_metric, h->stream));
         SG_CUDA(cudaStreamWaitEvent(h->stream2, h->fd_metric, 0));
         SG_CUDA(launch_fd_setup(h, h->stream2));

@@ -275,6 +275,7 @@ bool metric_diagonal(const Handle* h);
 // box geometry constants: corner c0, edge lengths L, g_k = det / L_k^2, det
 void box_constants(const Handle* h, double* c0, double* L, double* g, double* det);
 bool box_assembly_eligible(const Handle* h);
+bool box_assembly_ready(Handle* h);   // eligible and its tables built (the pass will run it)
 void free_box(Handle* h);
 constexpr double TILE3_MIN_ELEMENTS = 512.0;
 

@@ -89,7 +89,7 @@ __global__ void k_box_tables(const TabInfo* __restrict__ tabs, int ntab, const i
 // (stream, slot stride 1): consecutive threads = consecutive stream rows,
 // so every store instruction of a warp writes one contiguous 256-byte run.
 template <int P>
-__global__ void __launch_bounds__(BOX_THREADS, 2)
+__global__ void __launch_bounds__(BOX_THREADS, 3)
 k_stencil_box(const CompInfo* __restrict__ comps, const Chunk* __restrict__ chunks,
               const int64_t* __restrict__ tcum, const double* __restrict__ box1d, double3 gk,
               double* __restrict__ stencil, double* __restrict__ dinv) {
@@ -99,12 +99,14 @@ k_stencil_box(const CompInfo* __restrict__ comps, const Chunk* __restrict__ chun
     const CompInfo& C = comps[ch.comp];
     const int row = ch.row0 + (int)threadIdx.x;
     const int64_t R = C.rows;
-    // bands of the row along the inner axes in registers; the outer axis's
-    // factor is read per o0 (L1)
-    double Mv[3][W], Kv[3][W], g[3];
+    // the row's band along the stream axis in registers (the unrolled inner
+    // loop); the two outer factors are read per iteration (L1 hits) -- only
+    // the inner loop is unrolled: a fully unrolled W^3 body overflowed the
+    // instruction cache (85 % no_instruction stalls)
+    double Ms[W], Ks[W], g[3];
     int ik[3], mk[3], absk[3];
     int64_t ssk[3];
-    const double2* b0 = nullptr;
+    const double2* bb[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
         const int k = C.ax[j];
@@ -112,48 +114,41 @@ k_stencil_box(const CompInfo* __restrict__ comps, const Chunk* __restrict__ chun
         absk[j] = C.absm[k];
         ssk[j] = C.ss[k];
         ik[j] = (row / (int)C.rs[k]) % mk[j];
-        const double2* b = reinterpret_cast<const double2*>(box1d) + tcum[C.tab[k]] + (int64_t)ik[j] * W;
-        if (j == 0) {
-            b0 = b;
-        } else {
-#pragma unroll
-            for (int o = 0; o < W; ++o) {
-                const double2 v = __ldg(b + o);
-                Mv[j][o] = v.x;
-                Kv[j][o] = v.y;
-            }
-        }
+        bb[j] = reinterpret_cast<const double2*>(box1d) + tcum[C.tab[k]] + (int64_t)ik[j] * W;
         g[j] = k == 0 ? gk.x : (k == 1 ? gk.y : gk.z);
     }
-    double* out = stencil + C.mat_off + row;
 #pragma unroll
+    for (int o = 0; o < W; ++o) {
+        const double2 v = __ldg(bb[2] + o);
+        Ms[o] = v.x;
+        Ks[o] = v.y;
+    }
+    double* out = stencil + C.mat_off + row;
+#pragma unroll 1
     for (int o0 = 0; o0 < W; ++o0) {
         const int c0 = ik[0] + o0 - p;
         if (c0 < 0 || c0 >= mk[0]) continue;   // structural zero (set once per layout)
         const int64_t t0 = (int64_t)(absk[0] ? c0 : o0) * ssk[0];
-        {
-            const double2 v = __ldg(b0 + o0);
-            Mv[0][o0] = v.x;
-            Kv[0][o0] = v.y;
-        }
-#pragma unroll
+        const double2 f0 = __ldg(bb[0] + o0);
+#pragma unroll 1
         for (int o1 = 0; o1 < W; ++o1) {
             const int c1 = ik[1] + o1 - p;
             if (c1 < 0 || c1 >= mk[1]) continue;
             const int64_t t1 = t0 + (int64_t)(absk[1] ? c1 : o1) * ssk[1];
-            const double mm = __dmul_rn(Mv[0][o0], Mv[1][o1]);
-            const double km = __dmul_rn(Kv[0][o0], Mv[1][o1]);
-            const double mk2 = __dmul_rn(Mv[0][o0], Kv[1][o1]);
+            const double2 f1 = __ldg(bb[1] + o1);
+            // A = (g_0 K_0 M_1 + g_1 M_0 K_1) M_2 + g_2 M_0 M_1 K_2: the same
+            // expression of the (symmetric) factors for every entry
+            const double ab = __dadd_rn(__dmul_rn(g[0], __dmul_rn(f0.y, f1.x)), __dmul_rn(g[1], __dmul_rn(f0.x, f1.y)));
+            const double cc = __dmul_rn(g[2], __dmul_rn(f0.x, f1.x));
+            double* o = out + t1 * R;
+            const bool diag01 = o0 == p && o1 == p;
 #pragma unroll
             for (int o2 = 0; o2 < W; ++o2) {
                 const int c2 = ik[2] + o2 - p;
                 if (c2 < 0 || c2 >= mk[2]) continue;
-                const int64_t t = t1 + (absk[2] ? c2 : o2);
-                const double v = __dadd_rn(__dadd_rn(__dmul_rn(g[0], __dmul_rn(km, Mv[2][o2])),
-                                                     __dmul_rn(g[1], __dmul_rn(mk2, Mv[2][o2]))),
-                                           __dmul_rn(g[2], __dmul_rn(mm, Kv[2][o2])));
-                out[t * R] = v;
-                if (o0 == p && o1 == p && o2 == p) dinv[C.vec_off + row] = 1.0 / v;
+                const double v = __fma_rn(ab, Ms[o2], __dmul_rn(cc, Ks[o2]));
+                o[(int64_t)(absk[2] ? c2 : o2) * R] = v;
+                if (o2 == p && diag01) dinv[C.vec_off + row] = 1.0 / v;
             }
         }
     }
@@ -275,6 +270,28 @@ static bool build_box(Handle* h) {
     h->box_tab_total = tcum[ntab];
     h->box_state = 1;
     return true;
+}
+
+bool box_assembly_ready(Handle* h) { return build_box(h); }
+
+// FD metric scales c_k of a box: G_kk = g_k w exactly, and the quadrature
+// weights sum to the unit parameter volume, so c_k = sum_x G_kk(x) = g_k
+// (the FD preconditioner is then the exact inverse of the Kronecker
+// stiffness up to rounding); replaces k_fd_metric_scale's quadrature sums
+__global__ void k_fd_box_scale(int n, double3 g, double* __restrict__ ckg) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int k = i % MAXD;
+    ckg[i] = k == 0 ? g.x : (k == 1 ? g.y : (k == 2 ? g.z : 0.0));
+}
+
+cudaError_t launch_fd_box_scale(Handle* h, cudaStream_t s) {
+    double c0[3], L[3], g[3], det;
+    box_constants(h, c0, L, g, &det);
+    const int n = h->ncomp * MAXD;
+    if (n > 0) k_fd_box_scale<<<(n + 127) / 128, 128, 0, s>>>(n, make_double3(g[0], g[1], g[2]), h->d_ck);
+    h->launches[0]++;
+    return cudaGetLastError();
 }
 
 void free_box(Handle* h) {

@@ -1308,9 +1308,16 @@ static cudaError_t launch_hi(void (*kern)(KArgs...), dim3 grid, dim3 block, size
 // FD set-up after the metric (stream s, forked from the main stream after
 // k_metric, joined before the solve): c_k of every FD / line-FD component,
 // then the line-FD stream-axis bands and per-line factors
+cudaError_t launch_fd_box_scale(Handle* h, cudaStream_t s);
+
 cudaError_t launch_fd_setup(Handle* h, cudaStream_t s) {
     const int nf = (int)h->fd_comps.size(), nl = (int)h->fdl_comps.size(), ng = (int)h->fdg_comps.size();
-    if (ng > 0) {   // c_k of the whole-GPU FD components: chunked two-level sum
+    const bool box = h->box_state > 0;   // Kronecker assembly: c_k in closed form, no metric sums
+    if (box && nf + nl + ng > 0) {
+        cudaError_t e = launch_fd_box_scale(h, s);
+        if (e != cudaSuccess) return e;
+    }
+    if (ng > 0 && !box) {   // c_k of the whole-GPU FD components: chunked two-level sum
         const dim3 gp(FDG_SCALE_CHUNKS, (unsigned)ng, (unsigned)h->d);
 #define LAUNCH_SCALE_G(DD)                                                                                       \
     launch_hi(k_fd_metric_scale_part<DD>, gp, dim3(256), 0, s, (const CompInfo*)h->d_comps, (const int*)h->d_fdg_list, \
@@ -1325,6 +1332,7 @@ cudaError_t launch_fd_setup(Handle* h, cudaStream_t s) {
     }
     if (nf + nl == 0) return cudaGetLastError();
     const dim3 g1((unsigned)(nf + nl), (unsigned)h->d);
+    if (!box) {
 #define LAUNCH_SCALE(DD)                                                                              \
     launch_hi(k_fd_metric_scale<DD>, g1, dim3(256), 0, s, h->d_comps, h->d_fdlist, nf, h->d_fdl_list, h->d_G, h->d_ck)
     if (h->d == 1) { LAUNCH_SCALE(1); }
@@ -1332,6 +1340,7 @@ cudaError_t launch_fd_setup(Handle* h, cudaStream_t s) {
     else { LAUNCH_SCALE(3); }
 #undef LAUNCH_SCALE
     h->launches[0]++;
+    }
     if (nl == 0) return cudaGetLastError();
     int maxlines = 1;
     for (int c : h->fdl_comps) {

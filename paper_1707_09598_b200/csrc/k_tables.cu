@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(256) k_metric_box(
     const TabInfo* __restrict__ tabs, const double* __restrict__ qx, const double* __restrict__ qw,
     int q, int forcing_id, const double* __restrict__ hostf, double* __restrict__ xphys,
     double* __restrict__ Gout, int* __restrict__ err, const int* __restrict__ cta_comp, double3 c0,
-    double3 L, double3 g, double det) {
+    double3 L, double3 g, double det, int load_only) {
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid == 0 && !(det > 0.0)) atomicOr(err, ERRF_GEOMETRY);   // geometry.py:128-131
     if (gid >= qp_cum[ncomp]) return;
@@ -354,9 +354,14 @@ __global__ void __launch_bounds__(256) k_metric_box(
     const unsigned lin = (unsigned)(gid - qp_cum[lo]);
     double w = 1.0, x[3];
     const double c0k[3] = {c0.x, c0.y, c0.z}, Lk[3] = {L.x, L.y, L.z};
+    // storage order (s, b, a), a = ax[1] innermost: two divisions per point
+    const int ka = C.ax[1], kb = C.ax[0];
+    const unsigned nqa = (unsigned)C.nel[ka] * (unsigned)q, nqb = (unsigned)C.nel[kb] * (unsigned)q;
+    const unsigned t1 = lin / nqa, Qs = t1 / nqb;
+    const unsigned Qa_ = lin - t1 * nqa, Qb_ = t1 - Qs * nqb;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const unsigned Qa = (lin / (unsigned)C.qs[k]) % ((unsigned)C.nel[k] * (unsigned)q);
+        const unsigned Qa = k == ka ? Qa_ : (k == kb ? Qb_ : Qs);
         const int64_t t = tabs[C.tab[k]].qp_off + Qa;
         const double wk = qw[t];
         w = (k == 0) ? wk : __dmul_rn(w, wk);
@@ -364,9 +369,11 @@ __global__ void __launch_bounds__(256) k_metric_box(
     }
     const int64_t nqp = C.nqp;
     double* Gc = Gout + C.qp_off;
-    Gc[(int64_t)sym_index(3, 0, 0) * nqp + lin] = __dmul_rn(g.x, w);
-    Gc[(int64_t)sym_index(3, 1, 1) * nqp + lin] = __dmul_rn(g.y, w);
-    Gc[(int64_t)sym_index(3, 2, 2) * nqp + lin] = __dmul_rn(g.z, w);
+    if (!load_only) {   // the Kronecker assembly (k_assembly_box.cu) reads the load only
+        Gc[(int64_t)sym_index(3, 0, 0) * nqp + lin] = __dmul_rn(g.x, w);
+        Gc[(int64_t)sym_index(3, 1, 1) * nqp + lin] = __dmul_rn(g.y, w);
+        Gc[(int64_t)sym_index(3, 2, 2) * nqp + lin] = __dmul_rn(g.z, w);
+    }
     double f;
     if (forcing_id == SGIGA_FORCING_HOST) {
         f = hostf ? hostf[gid] : 0.0;
@@ -434,7 +441,7 @@ cudaError_t launch_metric(Handle* h) {
         k_metric_box<<<(unsigned)blocks, 256, 0, h->stream>>>(
             h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->q, h->forcing_id,
             hostf, h->d_xphys, h->d_G, h->d_err, h->d_mcomp, make_double3(c0[0], c0[1], c0[2]),
-            make_double3(L[0], L[1], L[2]), make_double3(g[0], g[1], g[2]), det);
+            make_double3(L[0], L[1], L[2]), make_double3(g[0], g[1], g[2]), det, box_assembly_ready(h) ? 1 : 0);
         h->launches[0]++;
         return cudaGetLastError();
     }
