@@ -845,7 +845,7 @@ k_fdl_factor(const CompInfo* __restrict__ comps, const int* __restrict__ list, i
     }
 }
 
-template <int D, int PL>   // PL = p (compile-time: the line scan's p x p state lives in registers)
+template <int D, int PL, bool FUSED>   // PL = p (compile-time: the line scan's p x p state lives in registers); FUSED: true residual inside the sweeps
 __global__ void __launch_bounds__(FDL_THREADS, 3)
 k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, const int* __restrict__ slotoff,
           const double* __restrict__ stencil, const double* __restrict__ rhs, int p,
@@ -1176,6 +1176,38 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
         }
         cluster.sync();
     };
+    // out = A v and out2 = A u in ONE sweep of the stored stencil (the sweep
+    // is bound by the stencil's HBM read; the second gather hits L1/L2).
+    // out is accumulated exactly as in spmv (same operations and order).
+    auto spmv2 = [&](const double* v, const double* u, double* out, double* out2) {
+        for (int row = gt; row < R; row += GT) {
+            const int rb = fd_row_base(C, D, row);
+            double y0 = 0.0, y1 = 0.0, w0 = 0.0, w1 = 0.0;
+            int tt = 0;
+            for (; tt + FDL_UNR - 1 < NS; tt += FDL_UNR) {
+                double vv[FDL_UNR];
+#pragma unroll
+                for (int k = 0; k < FDL_UNR; ++k) vv[k] = __ldg(val + (size_t)(tt + k) * R + row);
+#pragma unroll
+                for (int k = 0; k < FDL_UNR; k += 2) {
+                    const int c0 = rb + offs[tt + k], c1 = rb + offs[tt + k + 1];
+                    y0 += vv[k] * v[c0];
+                    y1 += vv[k + 1] * v[c1];
+                    w0 += vv[k] * u[c0];
+                    w1 += vv[k + 1] * u[c1];
+                }
+            }
+            for (; tt < NS; ++tt) {
+                const double a = __ldg(val + (size_t)tt * R + row);
+                const int c0 = rb + offs[tt];
+                y0 += a * v[c0];
+                w0 += a * u[c0];
+            }
+            out[row] = y0 + y1;
+            out2[row] = w0 + w1;
+        }
+        cluster.sync();
+    };
 
     double bbl = 0.0;
     for (int i = gt; i < R; i += GT) {
@@ -1185,23 +1217,41 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
         bbl += bi * bi;
     }
     const double bb = csum(bbl);
+    // True residual ||b - A x|| / ||b|| (linsolve.py:49-53).
+    // FUSED (the launcher sets it when the FD preconditioner is the exact
+    // inverse up to rounding -- Kronecker box systems, 1-3 iterations): no
+    // sweep of its own.  From the second iteration on, the iteration's sweep
+    // multiplies the stencil with BOTH p_k and x_k (spmv2), and after x_{k+1} =
+    // x_k + alpha p_k the residual is taken as b - (A x_k + alpha A p_k) -- two
+    // direct products with the stored stencil, not the CG recurrence (x_0 = 0:
+    // in the first iteration A x_1 = alpha A p_0 is the recurrence's own
+    // product).  The iterates are bitwise those of the plain loop.  Otherwise
+    // (tens of iterations) one separate sweep after the loop is cheaper.
     int it = 0, conv = (bb == 0.0);
+    double eel = 0.0;
     if (!conv) {
         precond();
         double rzl = 0.0;
         for (int i = gt; i < R; i += GT) { pp[i] = z[i]; rzl += r[i] * z[i]; }
         double rz = csum(rzl);
         while (it < maxit) {
-            spmv(pp, qq);
+            if (!FUSED || it == 0) spmv(pp, qq);
+            else spmv2(pp, x, qq, t);   // t = A x_k (the preconditioner's scratch is free here)
             double pql = 0.0;
             for (int i = gt; i < R; i += GT) pql += pp[i] * qq[i];
             const double alpha = rz / csum(pql);
             double rrl = 0.0;
+            eel = 0.0;
             for (int i = gt; i < R; i += GT) {
-                x[i] += alpha * pp[i];
+                const double xi = x[i] + alpha * pp[i];
+                x[i] = xi;
                 const double ri = r[i] - alpha * qq[i];
                 r[i] = ri;
                 rrl += ri * ri;
+                if constexpr (FUSED) {
+                    const double e = it == 0 ? ri : (b[i] - t[i]) - alpha * qq[i];
+                    eel += isfinite(xi) ? e * e : __longlong_as_double(0x7ff8000000000000ULL);
+                }
             }
             const double rr = csum(rrl);
             ++it;
@@ -1216,15 +1266,15 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
             cluster.sync();
         }
     }
-    // true residual ||A x - b|| / ||b|| (linsolve.py:49-53); x is copied into
-    // the halo-padded p buffer for the gather
-    for (int i = gt; i < R; i += GT) pp[i] = x[i];
-    cluster.sync();
-    spmv(pp, qq);
-    double eel = 0.0;
-    for (int i = gt; i < R; i += GT) {
-        const double e = qq[i] - b[i];
-        eel += isfinite(x[i]) ? e * e : __longlong_as_double(0x7ff8000000000000ULL);
+    if constexpr (!FUSED) {   // x is copied into the halo-padded p buffer for the gather
+        for (int i = gt; i < R; i += GT) pp[i] = x[i];
+        cluster.sync();
+        spmv(pp, qq);
+        eel = 0.0;
+        for (int i = gt; i < R; i += GT) {
+            const double e = qq[i] - b[i];
+            eel += isfinite(x[i]) ? e * e : __longlong_as_double(0x7ff8000000000000ULL);
+        }
     }
     const double ee = csum(eel);
     if (gt == 0) {
@@ -1261,7 +1311,7 @@ cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
     const double rt2 = rtol * rtol;
     cudaError_t e;
 #define LAUNCH_FDL(DD)                                                                                       \
-    e = cudaLaunchKernelEx(&cfg, k_pcg_fdl<DD, PP>, (const CompInfo*)h->d_comps, (const int*)h->d_fdl_list, \
+    e = cudaLaunchKernelEx(&cfg, k_pcg_fdl<DD, PP, FZ>, (const CompInfo*)h->d_comps, (const int*)h->d_fdl_list, \
                            (const int*)h->d_slotoff, (const double*)h->d_stencil, (const double*)h->d_rhs,  \
                            h->p, (const int64_t*)h->d_fd_uoff, (const double*)h->d_fdU,                    \
                            (const double*)h->d_ck, (const int64_t*)h->d_fdl_off, (const double*)h->d_fdl,  \
@@ -1274,9 +1324,11 @@ cudaError_t launch_pcg_fdl(Handle* h, double rtol, int maxit) {
         case 3: { constexpr int PP = 3; LAUNCH_FDL(DD); } break; \
         default: { constexpr int PP = 4; LAUNCH_FDL(DD); } break; \
     }
-    if (h->d == 1) { LAUNCH_FDL_P(1); }
-    else if (h->d == 2) { LAUNCH_FDL_P(2); }
-    else { LAUNCH_FDL_P(3); }
+    // Kronecker box systems (3-D): exact FD inverse, fused true residual
+    if (h->d == 1) { constexpr bool FZ = false; LAUNCH_FDL_P(1); }
+    else if (h->d == 2) { constexpr bool FZ = false; LAUNCH_FDL_P(2); }
+    else if (h->box_state > 0) { constexpr bool FZ = true; LAUNCH_FDL_P(3); }
+    else { constexpr bool FZ = false; LAUNCH_FDL_P(3); }
 #undef LAUNCH_FDL_P
 #undef LAUNCH_FDL
     h->launches[1]++;

@@ -462,3 +462,33 @@ def test_batched_edge_projection_matches_per_edge(graded):
             assert torch.equal(got, ref)
         finally:
             b.close()
+
+
+# ---------------------------------------------------------------------------
+# fused true residual of the line-FD PCG on Kronecker box systems
+# ---------------------------------------------------------------------------
+def test_fused_true_residual_matches_host_residual(monkeypatch):
+    """On box geometries the line-FD PCG reports ||b - A x|| / ||b|| without a
+    sweep of its own: b - (A x_k + alpha A p_k), both products taken in the
+    iteration's sweep (k_pcg_fdl<.., FUSED>).  It must equal the residual
+    recomputed on the host from the exported CSR and the coefficients
+    (linsolve.py:49-53), and the iterates must be bitwise those of the
+    separate-sweep kernel (the tiled-assembly route, SGIGA_NO_BOX_ASM)."""
+    cfg = configs.get_config("cfg5")
+    terms = (((8, 2, 2), 1), ((5, 4, 3), 1), ((2, 7, 3), -2))
+    spec = make_spec(terms, cfg.problem, cfg.quad_points)
+    b = Batch(spec)
+    try:
+        b.assemble()
+        it, rr = b.solve(rtol=1e-13)
+        assert np.all(it >= 2), it          # the fused product was exercised
+        full = b.coefficients()
+        for c in range(b.n_comp):
+            A_, rhs = b.export_csr(c)
+            x = b.component_coefficients(full, c).reshape(tuple(b.dims[c]))
+            x = x[tuple(slice(1, -1) for _ in range(spec.d))].ravel()
+            ref = np.linalg.norm(A_ @ x - rhs) / np.linalg.norm(rhs)
+            assert ref <= 1e-13
+            assert abs(rr[c] - ref) <= 0.5 * ref + 2e-16, (c, rr[c], ref)
+    finally:
+        b.close()
