@@ -1179,10 +1179,14 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
     // out = A v and out2 = A u in ONE sweep of the stored stencil (the sweep
     // is bound by the stencil's HBM read; the second gather hits L1/L2).
     // out is accumulated exactly as in spmv (same operations and order).
+    // absl accumulates sum_rows (|A| |u|)_row^2 (rounding bound of the fused
+    // true residual, see below).
+    double absl = 0.0;
     auto spmv2 = [&](const double* v, const double* u, double* out, double* out2) {
+        absl = 0.0;
         for (int row = gt; row < R; row += GT) {
             const int rb = fd_row_base(C, D, row);
-            double y0 = 0.0, y1 = 0.0, w0 = 0.0, w1 = 0.0;
+            double y0 = 0.0, y1 = 0.0, w0 = 0.0, w1 = 0.0, s0 = 0.0, s1 = 0.0;
             int tt = 0;
             for (; tt + FDL_UNR - 1 < NS; tt += FDL_UNR) {
                 double vv[FDL_UNR];
@@ -1193,8 +1197,11 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
                     const int c0 = rb + offs[tt + k], c1 = rb + offs[tt + k + 1];
                     y0 += vv[k] * v[c0];
                     y1 += vv[k + 1] * v[c1];
-                    w0 += vv[k] * u[c0];
-                    w1 += vv[k + 1] * u[c1];
+                    const double u0 = u[c0], u1 = u[c1];
+                    w0 += vv[k] * u0;
+                    w1 += vv[k + 1] * u1;
+                    s0 += fabs(vv[k]) * fabs(u0);
+                    s1 += fabs(vv[k + 1]) * fabs(u1);
                 }
             }
             for (; tt < NS; ++tt) {
@@ -1202,9 +1209,11 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
                 const int c0 = rb + offs[tt];
                 y0 += a * v[c0];
                 w0 += a * u[c0];
+                s0 += fabs(a) * fabs(u[c0]);
             }
             out[row] = y0 + y1;
             out2[row] = w0 + w1;
+            absl += (s0 + s1) * (s0 + s1);
         }
         cluster.sync();
     };
@@ -1225,8 +1234,13 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
     // x_k + alpha p_k the residual is taken as b - (A x_k + alpha A p_k) -- two
     // direct products with the stored stencil, not the CG recurrence (x_0 = 0:
     // in the first iteration A x_1 = alpha A p_0 is the recurrence's own
-    // product).  The iterates are bitwise those of the plain loop.  Otherwise
-    // (tens of iterations) one separate sweep after the loop is cheaper.
+    // product).  The iterates are bitwise those of the plain loop.  What this
+    // form cannot see is the rounding of the last update x_{k+1} = fl(x_k +
+    // alpha p_k), |delta| <= u |x_{k+1}|: its image A delta is bounded by
+    // u || |A| |x_k| ||_2 (first order; the same sweep accumulates |A| |x_k|),
+    // and the bound is ADDED to the reported residual -- relres is an upper
+    // bound of the residual of the stored x.  Otherwise (tens of iterations)
+    // one separate sweep after the loop is cheaper.
     int it = 0, conv = (bb == 0.0);
     double eel = 0.0;
     if (!conv) {
@@ -1277,12 +1291,14 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
         }
     }
     const double ee = csum(eel);
+    double rbound = 0.0;   // u || |A| |x_k| ||_2, u = 2^-53
+    if constexpr (FUSED) rbound = 0x1p-53 * sqrt(csum(it > 1 ? absl : 0.0));
     if (gt == 0) {
         st[c].it = it;
         st[c].conv = conv;
         st[c].active = 0;
         st[c].bb = bb;
-        relres[c] = bb > 0.0 ? sqrt(ee / bb) : (ee == 0.0 ? 0.0 : ee);
+        relres[c] = bb > 0.0 ? (FUSED ? (sqrt(ee) + rbound) / sqrt(bb) : sqrt(ee / bb)) : (ee == 0.0 ? 0.0 : ee);
     }
     // full C-order coefficients (x complete: the last cluster barrier is in csum)
     fd_expand<D>(C, x, coef, gt, GT);
