@@ -555,11 +555,25 @@ def run_sgiga(args, cfg):
     cg_bytes = sum(int(it) * (8 * w["nnz"] + 104 * w["rows"]) for it, w in zip(iters, work))
     # the sweeps the FD-PCG actually makes: one stencil read per iteration
     # plus the true-residual SpMV (linsolve.py:49-53), over the stored slots
-    cg_sweep_bytes = sum((int(it) + 1) * 8 * w["stored"] + int(it) * 104 * w["rows"] for it, w in zip(iters, work))
+    # (Kronecker box systems above the small-component kernel's 2048 rows:
+    # the true residual rides in the iteration sweeps, no sweep of its own)
+    def _sweeps(it, w):
+        return int(it) + (0 if (_box and w["rows"] > 2048 and it >= 1) else 1)
+    _akind = ct.c_int32(0)
+    batch.lib.sgiga_assembly_kind(batch.h, ct.byref(_akind))
+    _box = int(_akind.value) == 2
+    cg_sweep_bytes = sum(_sweeps(it, w) * 8 * w["stored"] + int(it) * 104 * w["rows"] for it, w in zip(iters, work))
     asm_flops = sum(w["flops"] for w in work)
     ex = ct.c_double(0.0)   # FP64 operations the assembly launch executed (host count of its work items)
     batch.lib.sgiga_assembly_flops(batch.h, ct.byref(ex))
     asm_exec = float(ex.value)
+    akind = ct.c_int32(0)   # 0 row/2-D/generic kernels, 1 tiled 3-D, 2 Kronecker box assembly
+    batch.lib.sgiga_assembly_kind(batch.h, ct.byref(akind))
+    asm_kind = {0: "row", 1: "tiled", 2: "box"}[int(akind.value)]
+    # box assembly: 1-D bands -> ONE store pass over the live stencil entries
+    # (HBM-store bound), the load by three sum-factorisation stages of f det w
+    nqp = sum(w["nel"] for w in work) * spec.quad_points ** spec.d
+    asm_box_bytes = sum(8 * w["stored"] + 16 * w["rows"] for w in work) + 8 * nqp
     d = spec.d
     comb_flops_pt = 0
     P = spec.degree + 1
@@ -578,13 +592,27 @@ def run_sgiga(args, cfg):
                     stencil_sweep_bytes=cg_sweep_bytes,
                     stencil_sweep_gbs=cg_sweep_bytes / (cg_ms * 1e-3) / 1e9 if cg_ms > 0 else 0.0,
                     note="achieved/frac: SURVEY B_it = iterations x (8 nnz + 104 n); stencil_sweep_*: the stored "
-                         "stencil read once per iteration + once for the true residual",
+                         "stencil read once per iteration + once for the true residual (box systems on the line-FD / "
+                         "whole-GPU kernels: the true residual is fused into the iteration sweeps)",
                     peak_source=f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"),
-        "assembly": dict(ms=kt[2], bound="fp64", achieved=asm_flops / (kt[2] * 1e-3) / 1e12 if kt[2] > 0 else 0.0,
-                         peak=fp64, unit="TFLOP/s", canonical_flops=asm_flops,
-                         executed_flops=asm_exec,
-                         executed_tflops=asm_exec / (kt[2] * 1e-3) / 1e12 if kt[2] > 0 and asm_exec > 0 else None,
-                         peak_source="DFMA micro-benchmark on this GPU (tools/fp64_peak.cu)"),
+        "assembly": (dict(ms=kt[2], bound="hbm", kernel="k_stencil_box + k_rhs_box_stage x3 (Kronecker box assembly)",
+                          achieved=asm_box_bytes / (kt[2] * 1e-3) / 1e9 if kt[2] > 0 else 0.0,
+                          peak=hbm_peak, unit="GB/s", algorithmic_bytes=asm_box_bytes,
+                          canonical_flops=asm_flops,
+                          canonical_tflops=asm_flops / (kt[2] * 1e-3) / 1e12 if kt[2] > 0 else 0.0,
+                          note="axis-aligned box geometry: the stiffness is a Kronecker sum of 1-D mass/stiffness "
+                               "bands, so the kernel does not execute SURVEY 8(d)'s per-element FLOPs (canonical_tflops "
+                               "is what the canonical count would imply); its floor is the store of the stencil: "
+                               "bytes = 8 x live stencil slots + 16 x rows (load, diagonal) + 8 x quadrature points "
+                               "(f det w read by the load stages)",
+                          peak_source=f"{peak_kind} MEASURED_PEAKS.json hbm_gbs")
+                     if asm_kind == "box" else
+                     dict(ms=kt[2], bound="fp64", kernel=f"stencil assembly ({asm_kind})",
+                          achieved=asm_flops / (kt[2] * 1e-3) / 1e12 if kt[2] > 0 else 0.0,
+                          peak=fp64, unit="TFLOP/s", canonical_flops=asm_flops,
+                          executed_flops=asm_exec,
+                          executed_tflops=asm_exec / (kt[2] * 1e-3) / 1e12 if kt[2] > 0 and asm_exec > 0 else None,
+                          peak_source="DFMA micro-benchmark on this GPU (tools/fp64_peak.cu)")),
         "combine": dict(ms=kt[6], bound="fp64", achieved=comb_flops / (kt[6] * 1e-3) / 1e12 if kt[6] > 0 else 0.0,
                         peak=fp64, unit="TFLOP/s", canonical_flops=comb_flops,
                         hbm_gbs=comb_bytes / (kt[6] * 1e-3) / 1e9 if kt[6] > 0 else 0.0,
@@ -600,18 +628,27 @@ def run_sgiga(args, cfg):
                 g["executed_frac"] = g["executed_tflops"] / g["peak"]
     dom = max(("pcg", "assembly", "combine"), key=lambda k: groups[k]["ms"])
     G = groups[dom]
+    tr = _ncu_traffic().get(args.config, {}).get(dom, {}) if R == 1 else {}
     if G["bound"] == "hbm":
+        # dominant group bound by HBM: the FD-PCG (stencil sweeps) or the box assembly (stencil store)
+        if dom == "pcg":
+            kname = ("FD-preconditioned CG: k_pcg_fdl (one cluster per component) / k_pcg_fdg (whole GPU) / "
+                     "k_pcg_fd (small components, side stream)")
+            abytes = cg_bytes
+        else:
+            kname, abytes = G.get("kernel", dom), G.get("algorithmic_bytes")
         roofline = {"bound": "hbm", "achieved": G["achieved"], "peak": G["peak"], "unit": "GB/s",
-                    "frac": G["frac"], "traffic": None, "kernel": "k_pcg_small/k_cg_* (batched Jacobi-PCG)",
-                    "algorithmic_bytes_per_launch": cg_bytes, "peak_source": G["peak_source"]}
+                    "frac": G["frac"], "traffic": tr.get("dram_bytes_per_launch"),
+                    "traffic_source": tr.get("source"), "traffic_kernel": tr.get("kernel"),
+                    "group": dom, "kernel": kname,
+                    "algorithmic_bytes_per_launch": abytes, "peak_source": G["peak_source"]}
     else:
         # DRAM bytes of one launch of the dominant kernel from the committed
         # `ncu --set full` capture (profiles/capture.sh -> profiles/summarize.py)
-        tr = _ncu_traffic().get(args.config, {})
         roofline = {"bound": "tensor", "achieved": G["achieved"], "peak": G["peak"], "unit": "TFLOP/s",
                     "frac": G.get("frac"),
-                    "traffic": tr.get("dram_bytes_per_launch") if dom == "assembly" and R == 1 else None,
-                    "traffic_source": tr.get("source") if dom == "assembly" and R == 1 else None,
+                    "traffic": tr.get("dram_bytes_per_launch"),
+                    "traffic_source": tr.get("source"),
                     "kernel": dom,
                     "note": "FP64 CUDA-core bound; 'tensor' slot holds the measured DFMA peak. achieved = the "
                             "canonical sum-factorised FLOPs of SURVEY 8(d) (F_el per element) / kernel time; the "

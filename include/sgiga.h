@@ -272,6 +272,13 @@ int sgiga_kernel_times(sgiga_handle* h, float* ms7);
  * beside the canonical sum-factorised count of SURVEY 8(d).              */
 int sgiga_assembly_flops(sgiga_handle* h, double* executed);
 
+/* Which stencil assembly the last pass ran (measurement only; the bench
+ * picks the roofline that bounds it): 0 = one-row-per-CTA / 2-D block /
+ * generic kernels (FP64 bound), 1 = tiled 3-D kernel (FP64 bound), 2 =
+ * Kronecker box assembly (axis-aligned box geometries: 1-D bands, one store
+ * pass over the stencil -- HBM-store bound).                              */
+int sgiga_assembly_kind(sgiga_handle* h, int32_t* kind);
+
 /* Per-component PCG iteration counts of the last solve.                 */
 int sgiga_iterations(sgiga_handle* h, int32_t* iters);
 

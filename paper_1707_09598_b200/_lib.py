@@ -49,6 +49,7 @@ EXPORTED = (
     "sgiga_device_count", "sgiga_local_poisson_systems",
     "sgiga_full_patch_system", "sgiga_edge_projection_system", "sgiga_gather_sum", "sgiga_gather",
     "sgiga_csr_spmv_sub", "sgiga_csr_pcg", "sgiga_set_coefficients_device", "sgiga_assembly_flops",
+    "sgiga_assembly_kind",
 )
 
 
@@ -125,6 +126,7 @@ def _declare(lib):
         "sgiga_iterations": ([VP, P_I32], ct.c_int),
         "sgiga_kernel_times": ([VP, P_F32], ct.c_int),
         "sgiga_assembly_flops": ([VP, P_F64], ct.c_int),
+        "sgiga_assembly_kind": ([VP, P_I32], ct.c_int),
         "sgiga_stream": ([VP], VP),
         "sgiga_destroy": ([VP], ct.c_int),
         "sgiga_last_error": ([], ct.c_char_p),

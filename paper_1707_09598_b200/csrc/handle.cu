@@ -1458,6 +1458,13 @@ int sgiga_assembly_flops(sgiga_handle* hh, double* executed) {
     return SGIGA_OK;
 }
 
+int sgiga_assembly_kind(sgiga_handle* hh, int32_t* kind) {
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    if (!h || !kind) return SGIGA_ERR_VALUE;
+    *kind = h->asm_tiled ? 1 : (h->box_state > 0 ? 2 : 0);
+    return SGIGA_OK;
+}
+
 void* sgiga_stream(sgiga_handle* hh) {
     Handle* h = reinterpret_cast<Handle*>(hh);
     return h ? (void*)h->stream : nullptr;

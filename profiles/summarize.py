@@ -89,7 +89,7 @@ def main(src: str, dst: str) -> None:
     feed profiles/traffic.json (bench.py's roofline.traffic)."""
     os.makedirs(dst, exist_ok=True)
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "traffic.json")
-    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    traffic = {}   # rebuilt from the captures in src (one entry per workload and kernel group)
     for f in sorted(os.listdir(src)):
         path = os.path.join(src, f)
         if f.startswith("launches_") and f.endswith(".csv"):
@@ -100,12 +100,13 @@ def main(src: str, dst: str) -> None:
             txt, got = _full_summary(path)
             head = f"# ncu --set full --clock-control none --import-source on, first launch ({stem})\n"
             open(os.path.join(dst, f"ncu_full_{stem}.txt"), "w").write(head + txt + _hot_lines(path))
-            for kern in ("k_assemble_tile", "k_assemble_fast"):
+            # per workload and kernel group (bench.py's rooflines keys): DRAM bytes of one launch
+            groups = {"k_assemble_tile": "assembly", "k_stencil_box": "assembly", "k_assemble2d": "assembly",
+                      "k_pcg_fdl": "pcg", "k_pcg_fdg": "pcg", "k_combine_points_tiled": "combine"}
+            for kern, grp in groups.items():
                 if stem.startswith(kern + "_") and "dram__bytes_read.sum" in got:
                     wl = stem[len(kern) + 1:]
-                    if wl in traffic and traffic[wl].get("kernel") == "k_assemble_tile" and kern != "k_assemble_tile":
-                        continue   # the product kernel's capture wins
-                    traffic[wl] = {
+                    traffic.setdefault(wl, {})[grp] = {
                         "kernel": kern,
                         "dram_bytes_per_launch": got["dram__bytes_read.sum"] + got.get("dram__bytes_write.sum", 0.0),
                         "source": os.path.join(os.path.basename(os.path.normpath(dst)), f"ncu_full_{stem}.txt"),
