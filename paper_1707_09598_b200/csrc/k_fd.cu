@@ -32,6 +32,20 @@ namespace sgiga {
 #ifndef SGIGA_FDL_UNR
 #define SGIGA_FDL_UNR 16
 #endif
+#ifndef SGIGA_FDL_UNR2
+#define SGIGA_FDL_UNR2 32
+#endif
+#ifndef SGIGA_FDL_FUSED_UNR1
+#define SGIGA_FDL_FUSED_UNR1 0
+#endif
+#ifndef SGIGA_FDL_FUSED_MINB
+#define SGIGA_FDL_FUSED_MINB 2
+#endif
+// the fused-residual instantiation: 2 CTAs per SM (128 registers) and 32
+// stencil loads in flight in the double-product sweep -- at 3 CTAs / 80
+// registers ptxas serialises the load batch (measured: cfg5 pass 3.58 -> 3.46
+// ms; 24 loads 3.49, 1 CTA x 64 loads 4.27, first sweep at 32 loads 3.47)
+constexpr int FDL_UNR2 = SGIGA_FDL_UNR2;   // the double-product sweep's loads in flight (even)
 constexpr int FDL_UNR = SGIGA_FDL_UNR;   // line-FD SpMV: stencil loads in flight per thread (even)
 
 constexpr int FD_THREADS = 512;
@@ -846,7 +860,7 @@ k_fdl_factor(const CompInfo* __restrict__ comps, const int* __restrict__ list, i
 }
 
 template <int D, int PL, bool FUSED>   // PL = p (compile-time: the line scan's p x p state lives in registers); FUSED: true residual inside the sweeps
-__global__ void __launch_bounds__(FDL_THREADS, 3)
+__global__ void __launch_bounds__(FDL_THREADS, FUSED ? SGIGA_FDL_FUSED_MINB : 3)
 k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, const int* __restrict__ slotoff,
           const double* __restrict__ stencil, const double* __restrict__ rhs, int p,
           const int64_t* __restrict__ uoff, const double* __restrict__ dU, const double* __restrict__ ckg,
@@ -1156,17 +1170,18 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
             line_solve(z);
         }
     };
+    constexpr int UNR1 = (FUSED && SGIGA_FDL_FUSED_UNR1) ? FDL_UNR2 : FDL_UNR;
     auto spmv = [&](const double* v, double* out) {   // out = A v (v halo-padded)
         for (int row = gt; row < R; row += GT) {
             const int rb = fd_row_base(C, D, row);
             double y0 = 0.0, y1 = 0.0;
             int tt = 0;
-            for (; tt + FDL_UNR - 1 < NS; tt += FDL_UNR) {   // FDL_UNR independent stencil loads in flight
-                double vv[FDL_UNR];
+            for (; tt + UNR1 - 1 < NS; tt += UNR1) {   // UNR1 independent stencil loads in flight
+                double vv[UNR1];
 #pragma unroll
-                for (int u = 0; u < FDL_UNR; ++u) vv[u] = __ldg(val + (size_t)(tt + u) * R + row);
+                for (int u = 0; u < UNR1; ++u) vv[u] = __ldg(val + (size_t)(tt + u) * R + row);
 #pragma unroll
-                for (int u = 0; u < FDL_UNR; u += 2) {
+                for (int u = 0; u < UNR1; u += 2) {
                     y0 += vv[u] * v[rb + offs[tt + u]];
                     y1 += vv[u + 1] * v[rb + offs[tt + u + 1]];
                 }
@@ -1188,12 +1203,12 @@ k_pcg_fdl(const CompInfo* __restrict__ comps, const int* __restrict__ list, cons
             const int rb = fd_row_base(C, D, row);
             double y0 = 0.0, y1 = 0.0, w0 = 0.0, w1 = 0.0, s0 = 0.0, s1 = 0.0;
             int tt = 0;
-            for (; tt + FDL_UNR - 1 < NS; tt += FDL_UNR) {
-                double vv[FDL_UNR];
+            for (; tt + FDL_UNR2 - 1 < NS; tt += FDL_UNR2) {
+                double vv[FDL_UNR2];
 #pragma unroll
-                for (int k = 0; k < FDL_UNR; ++k) vv[k] = __ldg(val + (size_t)(tt + k) * R + row);
+                for (int k = 0; k < FDL_UNR2; ++k) vv[k] = __ldg(val + (size_t)(tt + k) * R + row);
 #pragma unroll
-                for (int k = 0; k < FDL_UNR; k += 2) {
+                for (int k = 0; k < FDL_UNR2; k += 2) {
                     const int c0 = rb + offs[tt + k], c1 = rb + offs[tt + k + 1];
                     y0 += vv[k] * v[c0];
                     y1 += vv[k + 1] * v[c1];
