@@ -157,6 +157,10 @@ k_stencil_box(const CompInfo* __restrict__ comps, const Chunk* __restrict__ chun
 // One axis of the load's sum factorisation: out[u] = sum over the
 // quadrature points x of the support of interior function u[cdim]
 // of in[...x...] N_{u[cdim]+1}(x).
+// QT = quadrature points per element at compile time (0: run-time q): the
+// g loop is unrolled, QT loads in flight per thread instead of one (same
+// operations and order).
+template <int QT>
 __global__ void __launch_bounds__(BOX_THREADS)
 k_rhs_box_stage(const BoxStage* __restrict__ ents, const BoxWork* __restrict__ work,
                 const TabInfo* __restrict__ tabs, const double* __restrict__ vals, int p, int mu, int q,
@@ -165,11 +169,19 @@ k_rhs_box_stage(const BoxStage* __restrict__ ents, const BoxWork* __restrict__ w
     const BoxStage& S = ents[wk.ent];
     const int64_t u = wk.first + threadIdx.x;
     const int n1 = S.n[1], n2 = S.n[2];
-    if (u >= (int64_t)S.n[0] * n1 * n2) return;
+    const int64_t tot = (int64_t)S.n[0] * n1 * n2;
+    if (u >= tot) return;
     int uu[3];
-    uu[2] = (int)(u % n2);
-    uu[1] = (int)((u / n2) % n1);
-    uu[0] = (int)(u / ((int64_t)n1 * n2));
+    if (tot <= 0x7fffffff) {   // 32-bit index arithmetic (always, in practice)
+        const unsigned ul = (unsigned)u, t1 = ul / (unsigned)n2;
+        uu[2] = (int)(ul - t1 * (unsigned)n2);
+        uu[0] = (int)(t1 / (unsigned)n1);
+        uu[1] = (int)(t1 - (unsigned)uu[0] * (unsigned)n1);
+    } else {
+        uu[2] = (int)(u % n2);
+        uu[1] = (int)((u / n2) % n1);
+        uu[0] = (int)(u / ((int64_t)n1 * n2));
+    }
     const int cd = S.cdim;
     int64_t ib = S.in_off, ob = S.out_off;
 #pragma unroll
@@ -178,17 +190,26 @@ k_rhs_box_stage(const BoxStage* __restrict__ ents, const BoxWork* __restrict__ w
         if (d != cd) ib += uu[d] * S.in_str[d];
     }
     const TabInfo& T = tabs[S.tab];
-    const int P = p + 1, f = uu[cd] + 1;
+    const int P = p + 1, f = (cd == 0 ? uu[0] : (cd == 1 ? uu[1] : uu[2])) + 1;   // (no dynamic register index)
     const int e0 = f - p <= 0 ? 0 : (f - p + mu - 1) / mu;
     const int e1 = min(T.nel - 1, f / mu);
     const double* V = vals + T.val_off;
     const int64_t cs = S.in_str[cd];
+    const int qq = QT ? QT : q;
     double acc = 0.0;
-    for (int e = e0; e <= e1; ++e)
-        for (int g = 0; g < q; ++g) {
-            const int64_t x = (int64_t)e * q + g;
-            acc = __fma_rn(in[ib + x * cs], V[x * P + f - e * mu], acc);
+    for (int e = e0; e <= e1; ++e) {
+        const double* ip = in + ib + (int64_t)e * qq * cs;
+        const double* vp = V + (int64_t)e * qq * P + f - e * mu;
+        if constexpr (QT > 0) {
+            double a[QT], b[QT];
+#pragma unroll
+            for (int g = 0; g < QT; ++g) { a[g] = ip[g * cs]; b[g] = vp[g * P]; }
+#pragma unroll
+            for (int g = 0; g < QT; ++g) acc = __fma_rn(a[g], b[g], acc);
+        } else {
+            for (int g = 0; g < qq; ++g) acc = __fma_rn(ip[g * cs], vp[g * P], acc);
         }
+    }
     out[ob] = acc;
 }
 
@@ -333,9 +354,19 @@ bool launch_assembly_box(Handle* h, cudaError_t* err) {
     double* outs[3] = {h->d_box_x1, h->d_box_x2, h->d_rhs};
     int64_t wo = 0;
     for (int k = 0; k < 3; ++k) {
-        if (h->box_nwork[k] > 0)
-            k_rhs_box_stage<<<(unsigned)h->box_nwork[k], BOX_THREADS, 0, h->stream>>>(
-                ents, w + wo, h->d_tabs, h->d_tabvals, h->p, h->mu, h->q, ins[k], outs[k]);
+        if (h->box_nwork[k] > 0) {
+#define RHS_STAGE(QT)                                                                       \
+    k_rhs_box_stage<QT><<<(unsigned)h->box_nwork[k], BOX_THREADS, 0, h->stream>>>(          \
+        ents, w + wo, h->d_tabs, h->d_tabvals, h->p, h->mu, h->q, ins[k], outs[k])
+            switch (h->q) {
+                case 2: RHS_STAGE(2); break;
+                case 3: RHS_STAGE(3); break;
+                case 4: RHS_STAGE(4); break;
+                case 5: RHS_STAGE(5); break;
+                default: RHS_STAGE(0); break;
+            }
+#undef RHS_STAGE
+        }
         wo += h->box_nwork[k];
     }
     h->launches[0] += 5;
