@@ -386,6 +386,81 @@ __global__ void __launch_bounds__(256) k_metric_box(
     Gc[(int64_t)6 * nqp + lin] = __dmul_rn(__dmul_rn(f, det), w);
 }
 
+// NPT consecutive points (along the innermost quadrature axis) per thread:
+// one index decomposition (two divisions) per NPT points, the rest by
+// increment-with-carry; the load is stored as 16-byte vectors.  Requires every
+// component's point count to be a multiple of NPT and the load rows 16-byte
+// aligned (the launcher checks; true for every box plan with >= 2 elements
+// per axis).  Per point the operations and their order are k_metric_box's.
+template <int NPT>
+__global__ void __launch_bounds__(256) k_metric_box_v(
+    const CompInfo* __restrict__ comps, int ncomp, const int64_t* __restrict__ qp_cum,
+    const TabInfo* __restrict__ tabs, const double* __restrict__ qx, const double* __restrict__ qw,
+    int q, int forcing_id, const double* __restrict__ hostf, double* __restrict__ xphys,
+    double* __restrict__ Gout, int* __restrict__ err, const int* __restrict__ cta_comp, double3 c0,
+    double3 L, double3 g, double det, int load_only) {
+    static_assert(NPT % 2 == 0, "vector stores");
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * NPT;
+    if (gid == 0 && !(det > 0.0)) atomicOr(err, ERRF_GEOMETRY);   // geometry.py:128-131
+    if (gid >= qp_cum[ncomp]) return;
+    int lo = cta_comp[blockIdx.x * NPT];   // (table per 256 points)
+    if (gid >= qp_cum[lo + 1]) {
+        int l2 = lo, h2 = ncomp;
+        while (h2 - l2 > 1) {
+            int mid = (l2 + h2) >> 1;
+            if (qp_cum[mid] <= gid) l2 = mid; else h2 = mid;
+        }
+        lo = l2;
+    }
+    const CompInfo& C = comps[lo];
+    const unsigned lin = (unsigned)(gid - qp_cum[lo]);
+    const double c0k[3] = {c0.x, c0.y, c0.z}, Lk[3] = {L.x, L.y, L.z};
+    const int ka = C.ax[1], kb = C.ax[0];
+    const unsigned nqa = (unsigned)C.nel[ka] * (unsigned)q, nqb = (unsigned)C.nel[kb] * (unsigned)q;
+    const unsigned t1 = lin / nqa;
+    unsigned Qs = t1 / nqb, Qa_ = lin - t1 * nqa, Qb_ = t1 - Qs * nqb;
+    int64_t toff[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) toff[k] = tabs[C.tab[k]].qp_off;
+    const int64_t nqp = C.nqp;
+    double* Gc = Gout + C.qp_off;
+    double fv[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        double w = 1.0, x[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const unsigned Qa = k == ka ? Qa_ : (k == kb ? Qb_ : Qs);
+            const int64_t t = toff[k] + Qa;
+            const double wk = qw[t];
+            w = (k == 0) ? wk : __dmul_rn(w, wk);
+            x[k] = __fma_rn(Lk[k], qx[t], c0k[k]);
+        }
+        if (!load_only) {
+            Gc[(int64_t)sym_index(3, 0, 0) * nqp + lin + j] = __dmul_rn(g.x, w);
+            Gc[(int64_t)sym_index(3, 1, 1) * nqp + lin + j] = __dmul_rn(g.y, w);
+            Gc[(int64_t)sym_index(3, 2, 2) * nqp + lin + j] = __dmul_rn(g.z, w);
+        }
+        double f;
+        if (forcing_id == SGIGA_FORCING_HOST) {
+            f = hostf ? hostf[gid + j] : 0.0;
+            if (xphys)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) xphys[(gid + j) * 3 + i] = x[i];
+        } else {
+            f = forcing_value<3>(forcing_id, x);
+        }
+        fv[j] = __dmul_rn(__dmul_rn(f, det), w);
+        if (++Qa_ == nqa) {
+            Qa_ = 0;
+            if (++Qb_ == nqb) { Qb_ = 0; ++Qs; }
+        }
+    }
+    double2* o = reinterpret_cast<double2*>(Gc + (int64_t)6 * nqp + lin);
+#pragma unroll
+    for (int j = 0; j < NPT; j += 2) o[j / 2] = make_double2(fv[j], fv[j + 1]);
+}
+
 void box_constants(const Handle* h, double* c0, double* L, double* g, double* det) {
     // control points: coordinate k of corner (a, b, c) depends on index k only
     auto hw = [&](int a, int b, int c, int comp) { return h->geo_hw[(size_t)((a * 2 + b) * 2 + c) * 4 + comp]; };
@@ -438,6 +513,16 @@ cudaError_t launch_metric(Handle* h) {
     if (dg && !h->opt.no_box_metric) {
         double c0[3], L[3], g[3], det;
         box_constants(h, c0, L, g, &det);
+        constexpr int NPT = 4;
+        bool vec = true;   // NPT points per thread: no group straddles a component, 16-byte aligned load rows
+        for (const CompInfo& C : h->comps)
+            if (C.nqp % NPT != 0 || ((C.qp_off + 6 * C.nqp) & 1)) { vec = false; break; }
+        if (vec)
+            k_metric_box_v<NPT><<<(unsigned)((n + 256 * NPT - 1) / (256 * NPT)), 256, 0, h->stream>>>(
+                h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->q, h->forcing_id,
+                hostf, h->d_xphys, h->d_G, h->d_err, h->d_mcomp, make_double3(c0[0], c0[1], c0[2]),
+                make_double3(L[0], L[1], L[2]), make_double3(g[0], g[1], g[2]), det, box_assembly_ready(h) ? 1 : 0);
+        else
         k_metric_box<<<(unsigned)blocks, 256, 0, h->stream>>>(
             h->d_comps, h->ncomp, comp_qp_cum_ptr(h), h->d_tabs, h->d_qx, h->d_qw, h->q, h->forcing_id,
             hostf, h->d_xphys, h->d_G, h->d_err, h->d_mcomp, make_double3(c0[0], c0[1], c0[2]),
