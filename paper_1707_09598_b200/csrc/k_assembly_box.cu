@@ -30,6 +30,9 @@ namespace sgiga {
 namespace {
 
 constexpr int BOX_THREADS = 256;
+#ifndef SGIGA_BOX_MINB
+#define SGIGA_BOX_MINB 2   // resident CTAs per SM of k_stencil_box: 2 (109 registers, no spills) measured best -- cfg5 assembly 1.09 / 1.04 / 1.17 / 1.28 ms at 3 / 2 / 4 / 6
+#endif
 
 struct BoxStage {
     int tab;             // TabInfo of the contracted axis
@@ -89,7 +92,7 @@ __global__ void k_box_tables(const TabInfo* __restrict__ tabs, int ntab, const i
 // (stream, slot stride 1): consecutive threads = consecutive stream rows,
 // so every store instruction of a warp writes one contiguous 256-byte run.
 template <int P>
-__global__ void __launch_bounds__(BOX_THREADS, 3)
+__global__ void __launch_bounds__(BOX_THREADS, SGIGA_BOX_MINB)
 k_stencil_box(const CompInfo* __restrict__ comps, const Chunk* __restrict__ chunks,
               const int64_t* __restrict__ tcum, const double* __restrict__ box1d, double3 gk,
               double* __restrict__ stencil, double* __restrict__ dinv) {
